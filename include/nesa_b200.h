@@ -1,0 +1,183 @@
+/*
+ * nesa_b200.h -- C ABI of the B200-native NESA matrix-vector product.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (taskfmm, /root/reference/pkg/src/taskfmm) has no FFI; its operator API is
+ * Python:
+ *
+ *   mvp_serial(tree, ops, q, near=True, far=True)           fastmvp.py:142-172
+ *   mvp(tree, ops, q, runtime, vec=None, near, far)          fastmvp.py:124-139
+ *   StageVectors / make_stage_vectors / reset                fastmvp.py:24-59
+ *   Task(kind, accesses, _gemv_body(A, x, y))                fastmvp.py:62-65,
+ *                                                             runtime.py:73-86
+ *
+ * The Python host package (paper_1801_03589_b200.fastmvp.mvp) keeps those
+ * signatures and calls this library through ctypes:
+ *
+ *   nesa_plan_create   <- the one-time part of mvp(): flattening Tree +
+ *                         OperatorSet (quadtree.py:71-93, operators.py:158-253)
+ *                         and allocating StageVectors (fastmvp.py:48-59);
+ *                         the plan owns every device buffer.
+ *   nesa_matvec        <- one call of mvp_serial / mvp: gather q[perm]
+ *                         (fastmvp.py:148), near field (152-156), radiation,
+ *                         source transfer, translation, potential transfer,
+ *                         reception (157-171), scatter phi[inverse_perm]
+ *                         (172).  Zeroing of the work vectors (StageVectors.
+ *                         reset, fastmvp.py:42-45) is internal.
+ *   nesa_plan_destroy  <- end of the Runtime / StageVectors lifetime.
+ *   nesa_last_error    <- the exception text the reference raises at
+ *                         Runtime.barrier (runtime.py:163-168).
+ *
+ * Conventions: 0 = NESA_OK, any other return is a nesa_status; the detail
+ * is in nesa_last_error() (thread-local).  All pointers in
+ * nesa_plan_desc are HOST pointers and are copied during create.  Vector
+ * pointers passed to nesa_matvec are DEVICE pointers owned by the caller.
+ * A plan is immutable after create except for its workspace, so one plan
+ * serves one stream at a time (the reference's single-submitter rule,
+ * SPEC.md:461).
+ */
+#ifndef NESA_B200_H
+#define NESA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NESA_ABI_VERSION 1
+
+typedef enum {
+  NESA_OK = 0,
+  NESA_ERR_INVALID = 1,   /* bad descriptor / argument  (reference: ValueError) */
+  NESA_ERR_CUDA = 2,      /* CUDA runtime or launch failure                       */
+  NESA_ERR_OOM = 3,       /* device allocation failed                             */
+  NESA_ERR_UNSUPPORTED = 4
+} nesa_status;
+
+typedef enum { NESA_F64 = 0, NESA_F32 = 1 } nesa_dtype;
+
+/* nesa_matvec flags (reference: mvp_serial's near= / far= keywords). */
+#define NESA_NEAR 1u
+#define NESA_FAR 2u
+#define NESA_PROFILE 16u /* record per-stage CUDA events (nesa_profile_*) */
+
+typedef struct nesa_plan nesa_plan;
+
+/*
+ * Flattened Tree + operator tables.  Group ids follow the reference
+ * (quadtree.py:177-199): leaves 0..n_leaves-1, then level L-1 ... l0, each
+ * level a contiguous id range in Morton order.
+ */
+typedef struct nesa_plan_desc {
+  int32_t abi_version;   /* NESA_ABI_VERSION */
+  int32_t op_dtype;      /* nesa_dtype: storage + arithmetic precision */
+  int32_t Q;             /* equivalent sources per group (NesaParams.Q) */
+  int32_t n_check;       /* oversampling * Q                              */
+  int64_t N;             /* points                                        */
+  int64_t n_leaves;
+  int64_t n_groups;
+  int32_t l0, L;         /* coarsest / leaf level                          */
+
+  /* tree (Tree.perm, Group.start/stop/parent, quadrant, level ranges) */
+  const int64_t* perm;          /* [N] tree position -> original index     */
+  const int64_t* group_start;   /* [G] point range in tree order           */
+  const int64_t* group_stop;    /* [G]                                     */
+  const int64_t* parent;        /* [G] parent id, -1 at level l0           */
+  const int32_t* quad;          /* [G] 2*(ix&1)+(iy&1)                     */
+  const int64_t* level_first;   /* [L-l0+1] first id of level l0+i         */
+  const int64_t* level_count;   /* [L-l0+1]                                */
+  const int64_t* nbr_ptr;       /* [n_leaves+1] Group.neighbors CSR        */
+  const int64_t* nbr_idx;
+  const int64_t* int_ptr;       /* [G+1] Group.interaction CSR             */
+  const int64_t* int_idx;
+  const int64_t* int_dtab;      /* [nnz] index of the entry's D matrix     */
+
+  /* shared operator tables, float64 row-major (y = M x) */
+  const double* C;              /* [(L-l0) * 4 * Q * Q] child level l -> row l-l0-1 */
+  const double* B;              /* same layout                                      */
+  const double* D;              /* [n_dtab * Q * Q]                                 */
+  int64_t n_dtab;
+
+  /* Per-leaf / per-pair blocks computed on the host (OperatorSet), float64,
+   * or NULL to assemble them on the device from the geometry below:
+   *   near_blob: per leaf a, the n_a x W_a slab [K_a,b1 | ... | K_a,bk]
+   *              (neighbor order), column-major, leaves concatenated;
+   *   V_blob:    per leaf, Q x n column-major;  U_blob: n x Q column-major. */
+  const double* near_blob;
+  const double* V_blob;
+  const double* U_blob;
+
+  /* device-assembly inputs (operators.py:107-155 restated on the GPU) */
+  const double* points_tree;    /* [N*2] Tree.points                       */
+  const double* leaf_center;    /* [n_leaves*2] Group.center               */
+  const double* leaf_r_check;   /* [n_leaves] rho_out_check * half_side    */
+  const double* leaf_r_inaux;   /* [n_leaves] rho_in_aux * half_side       */
+  const double* out_fit_leaf;   /* [Q * n_check] outgoing fit at level L   */
+  const double* check_cos;      /* [n_check] cos(2 pi i / n_check)         */
+  const double* check_sin;
+  const double* aux_cos;        /* [Q] cos(2 pi i / Q)                     */
+  const double* aux_sin;
+
+  /* Multi-GPU sub-plan: leaves [leaf_begin, leaf_end) are this rank's
+   * targets (leaf_end <= leaf_begin means all leaves).  The plan then
+   * computes near/V/U for those leaves and C/D/B for their ancestors;
+   * source amplitudes of remote interaction partners arrive through the
+   * halo exchange between nesa_matvec_stage 1 and 2. */
+  int64_t leaf_begin, leaf_end;
+} nesa_plan_desc;
+
+int nesa_plan_create(const nesa_plan_desc* desc, int device, nesa_plan** out);
+
+/*
+ * phi = K~ q for nrhs right-hand sides.  q_dev / phi_dev hold N x nrhs
+ * values in ORIGINAL point order, point-major (numpy (N,) or (N, nrhs)
+ * C-order); complex vectors are interleaved (re, im) pairs.  The element
+ * type follows op_dtype: NESA_F64 -> float64 / complex128, NESA_F32 ->
+ * float32 / complex64.  stream = cudaStream_t or NULL (legacy default).
+ * Stream-ordered, no host synchronisation.
+ */
+int nesa_matvec(nesa_plan* plan, const void* q_dev, void* phi_dev,
+                int32_t nrhs, int32_t is_complex, uint32_t flags, void* stream);
+
+/* Multi-GPU pieces of one product (used by the Python dist layer):
+ * stage 1 = gather + near + radiation + source transfer (up to the exchange),
+ * stage 2 = translation + potential transfer + reception + scatter.
+ * s_dev() exposes the (G, Q, nrhs_real) source-amplitude workspace for the
+ * halo exchange between the two stages. */
+int nesa_matvec_stage(nesa_plan* plan, int32_t stage, const void* q_dev,
+                      void* phi_dev, int32_t nrhs, int32_t is_complex,
+                      uint32_t flags, void* stream);
+void* nesa_plan_s_dev(nesa_plan* plan, int32_t nrhs_real);
+
+int nesa_plan_destroy(nesa_plan* plan);
+
+const char* nesa_last_error(void);
+int nesa_abi_version(void);
+
+/* Plan statistics: see NESA_STAT_* */
+#define NESA_STAT_NEAR_ENTRIES 0   /* stored near entries (sum n_a * W_a)   */
+#define NESA_STAT_V_ENTRIES 1
+#define NESA_STAT_U_ENTRIES 2
+#define NESA_STAT_D_REFS 3
+#define NESA_STAT_N_DTAB 4
+#define NESA_STAT_DEVICE_BYTES 5
+#define NESA_STAT_NEAR_CTAS 6
+#define NESA_STAT_KERNELS_PER_MATVEC 7
+int64_t nesa_plan_stat(nesa_plan* plan, int32_t which);
+
+/* Profiling: with NESA_PROFILE in flags each nesa_matvec records CUDA
+ * events around its stages on the streams the kernels run on. */
+#define NESA_STAGE_TOTAL 0
+#define NESA_STAGE_NEAR 1
+#define NESA_STAGE_FAR 2     /* radiation .. potential transfer */
+#define NESA_STAGE_RECEPTION 3
+#define NESA_N_STAGES 4
+int nesa_profile_reset(nesa_plan* plan);
+/* Synchronises; fills up to max durations (ms) of `stage`, returns count. */
+int nesa_profile_read(nesa_plan* plan, int32_t stage, float* ms, int32_t max);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NESA_B200_H */

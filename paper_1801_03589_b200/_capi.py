@@ -1,0 +1,118 @@
+"""ctypes binding of libnesa_b200.so (include/nesa_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  Loading fails loudly if it is missing: there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnesa_b200.so")
+
+NESA_ABI_VERSION = 1
+NESA_OK = 0
+NESA_ERR_INVALID = 1
+NESA_ERR_CUDA = 2
+NESA_ERR_OOM = 3
+NESA_ERR_UNSUPPORTED = 4
+NESA_F64 = 0
+NESA_F32 = 1
+NESA_NEAR = 1
+NESA_FAR = 2
+NESA_PROFILE = 16
+
+STAT = {"near_entries": 0, "v_entries": 1, "u_entries": 2, "d_refs": 3, "n_dtab": 4,
+        "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7}
+STAGE = {"total": 0, "near": 1, "far": 2, "reception": 3}
+
+EXPORTED_SYMBOLS = (
+    "nesa_plan_create", "nesa_matvec", "nesa_matvec_stage", "nesa_plan_s_dev",
+    "nesa_plan_destroy", "nesa_last_error", "nesa_abi_version", "nesa_plan_stat",
+    "nesa_profile_reset", "nesa_profile_read",
+)
+
+_p = ctypes.c_void_p
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+
+class NesaPlanDesc(ctypes.Structure):
+    """Mirror of ``struct nesa_plan_desc`` (field order matters)."""
+
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("op_dtype", ctypes.c_int32),
+        ("Q", ctypes.c_int32), ("n_check", ctypes.c_int32),
+        ("N", ctypes.c_int64), ("n_leaves", ctypes.c_int64), ("n_groups", ctypes.c_int64),
+        ("l0", ctypes.c_int32), ("L", ctypes.c_int32),
+        ("perm", _i64p), ("group_start", _i64p), ("group_stop", _i64p),
+        ("parent", _i64p), ("quad", _i32p), ("level_first", _i64p),
+        ("level_count", _i64p), ("nbr_ptr", _i64p), ("nbr_idx", _i64p),
+        ("int_ptr", _i64p), ("int_idx", _i64p), ("int_dtab", _i64p),
+        ("C", _f64p), ("B", _f64p), ("D", _f64p), ("n_dtab", ctypes.c_int64),
+        ("near_blob", _f64p), ("V_blob", _f64p), ("U_blob", _f64p),
+        ("points_tree", _f64p), ("leaf_center", _f64p), ("leaf_r_check", _f64p),
+        ("leaf_r_inaux", _f64p), ("out_fit_leaf", _f64p),
+        ("check_cos", _f64p), ("check_sin", _f64p), ("aux_cos", _f64p), ("aux_sin", _f64p),
+        ("leaf_begin", ctypes.c_int64), ("leaf_end", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the NESA matvec has no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    lib.nesa_plan_create.argtypes = [ctypes.POINTER(NesaPlanDesc), ctypes.c_int,
+                                     ctypes.POINTER(_p)]
+    lib.nesa_plan_create.restype = ctypes.c_int
+    lib.nesa_matvec.argtypes = [_p, _p, _p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _p]
+    lib.nesa_matvec.restype = ctypes.c_int
+    lib.nesa_matvec_stage.argtypes = [_p, ctypes.c_int32, _p, _p, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_uint32, _p]
+    lib.nesa_matvec_stage.restype = ctypes.c_int
+    lib.nesa_plan_s_dev.argtypes = [_p, ctypes.c_int32]
+    lib.nesa_plan_s_dev.restype = _p
+    lib.nesa_plan_destroy.argtypes = [_p]
+    lib.nesa_plan_destroy.restype = ctypes.c_int
+    lib.nesa_last_error.argtypes = []
+    lib.nesa_last_error.restype = ctypes.c_char_p
+    lib.nesa_abi_version.argtypes = []
+    lib.nesa_abi_version.restype = ctypes.c_int
+    lib.nesa_plan_stat.argtypes = [_p, ctypes.c_int32]
+    lib.nesa_plan_stat.restype = ctypes.c_int64
+    lib.nesa_profile_reset.argtypes = [_p]
+    lib.nesa_profile_reset.restype = ctypes.c_int
+    lib.nesa_profile_read.argtypes = [_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_float),
+                                      ctypes.c_int32]
+    lib.nesa_profile_read.restype = ctypes.c_int
+    if lib.nesa_abi_version() != NESA_ABI_VERSION:
+        raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+class NesaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"nesa error {code}: {msg}")
+        self.code = code
+
+
+def check(code: int) -> None:
+    if code != NESA_OK:
+        msg = load().nesa_last_error().decode(errors="replace")
+        if code in (NESA_ERR_INVALID, NESA_ERR_UNSUPPORTED):
+            raise ValueError(msg)
+        raise NesaError(code, msg)

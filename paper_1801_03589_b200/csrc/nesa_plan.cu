@@ -1,0 +1,1005 @@
+// nesa_plan.cu -- plan construction, device operator assembly, CUDA-graph
+// launch and the C ABI declared in include/nesa_b200.h.
+//
+// The plan is the GPU form of the reference's Tree + OperatorSet +
+// StageVectors (quadtree.py:71-93, operators.py:158-253, fastmvp.py:24-59):
+// every per-task gemv of fastmvp.mvp becomes a row of a batched launch, the
+// handle generations of runtime.py:137-161 become the edges of a CUDA graph
+// (gather -> {near | radiation -> upward levels -> translation -> downward
+// levels} -> reception), and the near-field branch runs concurrently with the
+// far-field chain (the paper's near/far task mixing).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/nesa_b200.h"
+#include "nesa_kernels.cuh"
+
+using namespace nesa;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct NesaError : std::runtime_error {
+  int code;
+  NesaError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(expr)                                                                \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      throw NesaError(_e == cudaErrorMemoryAllocation ? NESA_ERR_OOM : NESA_ERR_CUDA, \
+                      std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw NesaError(NESA_ERR_INVALID, msg);
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count, size_t pad_bytes = 0) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    size_t bytes = count * sizeof(T) + pad_bytes;
+    if (bytes == 0) bytes = 16;
+    CUDA_OK(cudaMalloc(&p, bytes));
+    CUDA_OK(cudaMemset(p, 0, bytes));
+  }
+  void upload(const std::vector<T>& v) {
+    alloc(v.size());
+    if (!v.empty()) CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+};
+
+// Host description of one batched block-GEMV launch.
+struct HostBlockSet {
+  std::vector<BlockItem> items;
+  std::vector<BlockSeg> segs;
+  std::vector<BlockChunk> chunks;
+  std::vector<int32_t> cta_ptr;
+  int64_t blob_elems = 0;
+  int64_t entries = 0;
+};
+
+struct DevBlockSet {
+  DevBuf<unsigned char> blob;  // T elements
+  DevBuf<BlockItem> items;
+  DevBuf<BlockSeg> segs;
+  DevBuf<BlockChunk> chunks;
+  DevBuf<int32_t> cta_ptr;
+  int grid = 0;
+  int64_t n_items = 0;
+  int64_t entries = 0;
+};
+
+// Split items into bulk-copy chunks and give each CTA a contiguous,
+// byte-balanced range of whole items (a target row is never split across
+// CTAs, so it has exactly one writer).
+void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
+  hs.chunks.clear();
+  std::vector<int64_t> item_first_chunk(hs.items.size() + 1);
+  std::vector<double> item_bytes(hs.items.size());
+  for (size_t i = 0; i < hs.items.size(); ++i) {
+    const BlockItem& it = hs.items[i];
+    item_first_chunk[i] = int64_t(hs.chunks.size());
+    int per = int(std::min<int64_t>(kMaxC, kABytes / (int64_t(it.m) * int64_t(elem_bytes))));
+    per = std::max(per, 1);
+    for (int c = 0; c < it.n; c += per)
+      hs.chunks.push_back(BlockChunk{int32_t(i), c, std::min(per, it.n - c), 0});
+    item_bytes[i] = double(it.m) * it.n * elem_bytes + 256.0;  // + per-item overhead
+  }
+  item_first_chunk[hs.items.size()] = int64_t(hs.chunks.size());
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_grid, int64_t(hs.items.size()))));
+  double total = 0;
+  for (double b : item_bytes) total += b;
+  hs.cta_ptr.assign(grid + 1, 0);
+  size_t it = 0;
+  double acc = 0;
+  for (int c = 0; c < grid; ++c) {
+    hs.cta_ptr[c] = int32_t(item_first_chunk[it]);
+    const double target = total * double(c + 1) / grid;
+    // take items while the running sum stays closer to the target
+    while (it < hs.items.size()) {
+      const double nb = acc + item_bytes[it];
+      if (c < grid - 1 && nb > target && (nb - target) > (target - acc) && acc > 0 &&
+          hs.cta_ptr[c] != int32_t(item_first_chunk[it]))
+        break;
+      acc = nb;
+      ++it;
+      if (acc >= target && c < grid - 1) break;
+    }
+  }
+  hs.cta_ptr[grid] = int32_t(hs.chunks.size());
+  // any items left (rounding) go to the last CTA implicitly via cta_ptr[grid]
+}
+
+template <typename T>
+void upload_blockset(DevBlockSet& d, const HostBlockSet& h) {
+  d.blob.alloc(size_t(h.blob_elems) * sizeof(T), 256);
+  d.items.upload(h.items);
+  d.segs.upload(h.segs);
+  d.chunks.upload(h.chunks);
+  d.cta_ptr.upload(h.cta_ptr);
+  d.grid = int(h.cta_ptr.size()) - 1;
+  d.n_items = int64_t(h.items.size());
+  d.entries = h.entries;
+}
+
+// ---------------------------------------------------------------------------
+// Device assembly of near / V / U blocks (operators.py:107-155 on the GPU).
+// Entries are evaluated in float64 exactly as linalg.kernel_matrix does:
+// d2 = (t - s)_x^2 + (t - s)_y^2 without contraction, -0.5 * log(d2).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double kernel_entry(double tx, double ty, double sx, double sy) {
+  const double dx = __dsub_rn(tx, sx), dy = __dsub_rn(ty, sy);
+  const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  return -0.5 * log(d2);
+}
+
+template <typename T>
+__global__ void assemble_near_kernel(const BlockItem* items, const BlockSeg* segs,
+                                     const double* pts, T* blob) {
+  const BlockItem it = items[blockIdx.x];
+  for (int sg = it.seg_begin; sg < it.seg_begin + it.seg_count; ++sg) {
+    const BlockSeg S = segs[sg];
+    const int scol1 = (sg + 1 < it.seg_begin + it.seg_count) ? segs[sg + 1].col0 : it.n;
+    const int64_t cnt = int64_t(scol1 - S.col0) * it.m;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int c = S.col0 + int(e / it.m), r = int(e % it.m);
+      const int64_t i = it.y_row0 + r, j = S.x_row0 + (c - S.col0);
+      const double v = (i == j) ? 0.0
+                                : kernel_entry(pts[2 * i], pts[2 * i + 1], pts[2 * j], pts[2 * j + 1]);
+      blob[it.a_off + int64_t(c) * it.m + r] = T(v);
+    }
+  }
+}
+
+// V_b = fit @ K(out_check_b, pts_b): item m = Q rows, n = n_b columns.
+template <typename T>
+__global__ void assemble_V_kernel(const BlockItem* items, const int64_t* item_leaf,
+                                  const double* pts, const double* center, const double* r_check,
+                                  const double* fit, const double* ccos, const double* csin,
+                                  int Q, int n_check, T* blob) {
+  extern __shared__ double kc[];  // n_check
+  const BlockItem it = items[blockIdx.x];
+  const int64_t leaf = item_leaf[blockIdx.x];
+  const double cx = center[2 * leaf], cy = center[2 * leaf + 1], rc = r_check[leaf];
+  for (int c = 0; c < it.n; ++c) {
+    // column c is point (segment x_row0 + c); V items carry one segment.
+    const int64_t j = int64_t(it.pad) + c;  // pad holds the leaf's first point
+    const double px = pts[2 * j], py = pts[2 * j + 1];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_check; i += blockDim.x) {
+      const double chx = __dadd_rn(cx, __dmul_rn(rc, ccos[i]));
+      const double chy = __dadd_rn(cy, __dmul_rn(rc, csin[i]));
+      kc[i] = kernel_entry(chx, chy, px, py);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < Q; k += blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i < n_check; ++i) acc = fma(fit[int64_t(k) * n_check + i], kc[i], acc);
+      blob[it.a_off + int64_t(c) * Q + k] = T(acc);
+    }
+  }
+}
+
+// U_a = K(pts_a, in_aux_a): item m = rows of the panel, n = Q columns.
+template <typename T>
+__global__ void assemble_U_kernel(const BlockItem* items, const int64_t* item_leaf,
+                                  const double* pts, const double* center, const double* r_aux,
+                                  const double* acos_, const double* asin_, T* blob) {
+  const BlockItem it = items[blockIdx.x];
+  const int64_t leaf = item_leaf[blockIdx.x];
+  const double cx = center[2 * leaf], cy = center[2 * leaf + 1], ra = r_aux[leaf];
+  const int64_t cnt = int64_t(it.m) * it.n;
+  for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+    const int k = int(e / it.m), r = int(e % it.m);
+    const int64_t i = it.y_row0 + r;
+    const double ax = __dadd_rn(cx, __dmul_rn(ra, acos_[k]));
+    const double ay = __dadd_rn(cy, __dmul_rn(ra, asin_[k]));
+    blob[it.a_off + int64_t(k) * it.m + r] = T(kernel_entry(pts[2 * i], pts[2 * i + 1], ax, ay));
+  }
+}
+
+template <typename T>
+__global__ void convert_kernel(const double* src, T* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = T(src[i]);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------
+struct nesa_plan {
+  int device = 0;
+  int dtype = NESA_F64;
+  size_t esz = 8;
+  int Q = 0, n_check = 0, l0 = 0, L = 0;
+  int64_t N = 0, NL = 0, G = 0;
+  int64_t leaf_begin = 0, leaf_end = 0;  // local target leaves
+  int64_t pt_begin = 0, pt_end = 0;      // local tree-order point range
+  int n_sm = 148;
+
+  std::vector<int64_t> lvl_first, lvl_count;  // global, index level - l0
+  std::vector<int64_t> loc_first, loc_count;  // local (ancestors of local leaves)
+
+  DevBuf<int64_t> perm;        // [N]
+  DevBuf<int32_t> quad;        // [G]
+  DevBuf<int64_t> parent;      // [G]
+  DevBuf<int64_t> child_first; // [G]
+  DevBuf<int32_t> n_child;     // [G]
+  DevBuf<unsigned char> CT, BT, DT;  // T tables (transposed)
+  int64_t dstride = 0, n_dtab = 0, d_refs = 0;
+
+  DevBlockSet nearset, Vset, Uset;
+
+  DevBuf<TransTile> ttiles;
+  DevBuf<TransRun> truns;
+  DevBuf<TransPair> tpairs;
+  int n_ttiles = 0;
+
+  // workspace for R real columns
+  int ws_R = 0;
+  DevBuf<unsigned char> qt, phin, s, o;
+
+  cudaStream_t s0 = nullptr, s1 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
+  struct GraphKey {
+    const void* q;
+    void* phi;
+    int R;
+    uint32_t flags;
+    int stage;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(q, phi, R, flags, stage) < std::tie(o.q, o.phi, o.R, o.flags, o.stage);
+    }
+  };
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<std::pair<cudaGraphNode_t, int>> ev_nodes;  // node, slot (stage*2+end)
+  };
+  std::map<GraphKey, GraphEntry> graphs;
+  int kernels_per_matvec = 0;
+
+  // profiling: per matvec a set of 2*NESA_N_STAGES events
+  std::vector<std::vector<cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
+  cudaEvent_t cap_events[2 * NESA_N_STAGES] = {};
+
+  ~nesa_plan() {
+    cudaSetDevice(device);
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& v : prof_events)
+      for (auto e : v) cudaEventDestroy(e);
+    for (auto e : cap_events)
+      if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (s0) cudaStreamDestroy(s0);
+    if (s1) cudaStreamDestroy(s1);
+  }
+};
+
+namespace {
+
+template <typename T>
+void upload_table_T(DevBuf<unsigned char>& dst, const double* src, int64_t n_mats, int Q,
+                    int64_t stride, bool transpose) {
+  std::vector<T> h(size_t(std::max<int64_t>(n_mats, 1) * stride), T(0));
+  for (int64_t m = 0; m < n_mats; ++m)
+    for (int k = 0; k < Q; ++k)
+      for (int j = 0; j < Q; ++j) {
+        const double v = src[(m * Q + k) * Q + j];
+        if (transpose)
+          h[m * stride + int64_t(j) * Q + k] = T(v);
+        else
+          h[m * stride + int64_t(k) * Q + j] = T(v);
+      }
+  dst.alloc(h.size() * sizeof(T));
+  CUDA_OK(cudaMemcpy(dst.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// Host blob (reference layout, float64) -> device layout (type T, paneled).
+template <typename T>
+void upload_host_blob(DevBlockSet& d, const HostBlockSet& h, const double* src,
+                      const std::vector<int64_t>& item_src_off,
+                      const std::vector<int32_t>& item_src_rows,
+                      const std::vector<int32_t>& item_row0) {
+  std::vector<T> stage(size_t(h.blob_elems));
+  for (size_t i = 0; i < h.items.size(); ++i) {
+    const BlockItem& it = h.items[i];
+    const int64_t so = item_src_off[i];
+    const int32_t ld = item_src_rows[i], r0 = item_row0[i];
+    for (int c = 0; c < it.n; ++c)
+      for (int r = 0; r < it.m; ++r)
+        stage[it.a_off + int64_t(c) * it.m + r] = T(src[so + int64_t(c) * ld + r0 + r]);
+  }
+  if (!stage.empty())
+    CUDA_OK(cudaMemcpy(d.blob.p, stage.data(), stage.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+template <typename T>
+void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
+  const int Q = P->Q;
+  const int64_t NL = P->NL, G = P->G;
+  const size_t es = sizeof(T);
+  const int64_t lb = P->leaf_begin, le = P->leaf_end;
+
+  // ---- tree arrays
+  {
+    std::vector<int64_t> perm(d->perm, d->perm + P->N);  // full: near halo columns
+    for (auto v : perm) require(v >= 0 && v < P->N, "perm out of range");
+    P->perm.upload(perm);
+    std::vector<int32_t> quad(d->quad, d->quad + G);
+    P->quad.upload(quad);
+    std::vector<int64_t> parent(d->parent, d->parent + G);
+    P->parent.upload(parent);
+    std::vector<int64_t> cf(G, -1);
+    std::vector<int32_t> nc(G, 0);
+    for (int64_t g = G - 1; g >= 0; --g) {
+      const int64_t p = parent[g];
+      if (p >= 0) {
+        require(p < G && p > g, "parent ids must follow child ids");
+        cf[p] = g;  // smallest child id wins (iterating downward)
+        nc[p] += 1;
+      }
+    }
+    P->child_first.upload(cf);
+    P->n_child.upload(nc);
+  }
+
+  // ---- local (ancestor) level ranges
+  const int nlev = P->L - P->l0 + 1;
+  P->loc_first.assign(nlev, 0);
+  P->loc_count.assign(nlev, 0);
+  {
+    int64_t lo = lb, hi = le - 1;  // ids at level L
+    for (int lv = P->L; lv >= P->l0; --lv) {
+      const int li = lv - P->l0;
+      if (le > lb) {
+        P->loc_first[li] = lo;
+        P->loc_count[li] = hi - lo + 1;
+        if (lv > P->l0) {
+          lo = d->parent[lo];
+          hi = d->parent[hi];
+        }
+      }
+    }
+  }
+
+  // ---- tables
+  const int64_t QQ = int64_t(Q) * Q;
+  const int64_t per16 = 16 / int64_t(es);
+  P->dstride = (QQ + per16 - 1) / per16 * per16;
+  const int64_t nlt = P->L - P->l0;
+  if (nlt > 0) {
+    upload_table_T<T>(P->CT, d->C, nlt * 4, Q, QQ, true);
+    upload_table_T<T>(P->BT, d->B, nlt * 4, Q, QQ, true);
+  }
+  P->n_dtab = d->n_dtab;
+  upload_table_T<T>(P->DT, d->D, d->n_dtab, Q, P->dstride, true);
+
+  // ---- near / V / U block sets (local leaves)
+  HostBlockSet hn, hv, hu;
+  std::vector<int64_t> near_src_off, v_src_off, u_src_off;
+  std::vector<int32_t> near_src_rows, near_row0, u_src_rows, u_row0, v_src_rows, v_row0;
+  std::vector<int64_t> v_leaf, u_leaf;
+  {
+    // host-blob offsets of every leaf (reference layout, whole leaves)
+    int64_t near_off = 0, v_off = 0, u_off = 0;
+    for (int64_t a = 0; a < NL; ++a) {
+      const int64_t na = d->group_stop[a] - d->group_start[a];
+      require(na >= 1, "empty leaf");
+      int64_t W = 0;
+      for (int64_t e = d->nbr_ptr[a]; e < d->nbr_ptr[a + 1]; ++e) {
+        const int64_t b = d->nbr_idx[e];
+        require(b >= 0 && b < NL, "neighbor id out of range");
+        W += d->group_stop[b] - d->group_start[b];
+      }
+      require(W < (int64_t(1) << 31), "near slab too wide");
+      if (a >= lb && a < le) {
+        // near item(s): panels of <= kMaxRows rows
+        const int32_t seg_begin = int32_t(hn.segs.size());
+        int32_t col = 0;
+        for (int64_t e = d->nbr_ptr[a]; e < d->nbr_ptr[a + 1]; ++e) {
+          const int64_t b = d->nbr_idx[e];
+          const int64_t bs = d->group_start[b], bn = d->group_stop[b] - bs;
+          if (int32_t(hn.segs.size()) > seg_begin) {
+            BlockSeg& last = hn.segs.back();
+            if (int64_t(last.x_row0) + (col - last.col0) == bs) {
+              col += int32_t(bn);
+              continue;
+            }
+          }
+          hn.segs.push_back(BlockSeg{int32_t(bs), col});
+          col += int32_t(bn);
+        }
+        const int32_t seg_count = int32_t(hn.segs.size()) - seg_begin;
+        for (int64_t r0 = 0; r0 < na; r0 += kMaxRows) {
+          const int32_t m = int32_t(std::min<int64_t>(kMaxRows, na - r0));
+          hn.items.push_back(BlockItem{hn.blob_elems, m, int32_t(W),
+                                       int32_t(d->group_start[a] + r0), seg_begin, seg_count, 0});
+          near_src_off.push_back(near_off);
+          near_src_rows.push_back(int32_t(na));
+          near_row0.push_back(int32_t(r0));
+          hn.blob_elems += int64_t(m) * W;
+          hn.entries += int64_t(m) * W;
+        }
+        // V: Q x na, x = qt rows of the leaf, y = s rows of leaf a
+        {
+          const int32_t sb = int32_t(hv.segs.size());
+          hv.segs.push_back(BlockSeg{int32_t(d->group_start[a]), 0});
+          BlockItem it{hv.blob_elems, Q, int32_t(na), int32_t(a * Q), sb, 1,
+                       int32_t(d->group_start[a])};
+          hv.items.push_back(it);
+          v_src_off.push_back(v_off);
+          v_src_rows.push_back(Q);
+          v_row0.push_back(0);
+          v_leaf.push_back(a);
+          hv.blob_elems += int64_t(Q) * na;
+          hv.entries += int64_t(Q) * na;
+        }
+        // U: na x Q, x = o rows of leaf a, y = phi rows
+        {
+          const int32_t sb = int32_t(hu.segs.size());
+          hu.segs.push_back(BlockSeg{int32_t(a * Q), 0});
+          for (int64_t r0 = 0; r0 < na; r0 += kMaxRows) {
+            const int32_t m = int32_t(std::min<int64_t>(kMaxRows, na - r0));
+            hu.items.push_back(BlockItem{hu.blob_elems, m, Q,
+                                         int32_t(d->group_start[a] + r0), sb, 1, 0});
+            u_src_off.push_back(u_off);
+            u_src_rows.push_back(int32_t(na));
+            u_row0.push_back(int32_t(r0));
+            u_leaf.push_back(a);
+            hu.blob_elems += int64_t(m) * Q;
+            hu.entries += int64_t(m) * Q;
+          }
+        }
+      }
+      near_off += na * W;
+      v_off += int64_t(Q) * na;
+      u_off += na * Q;
+    }
+    require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
+  }
+  chunk_and_balance(hn, es, P->n_sm);
+  chunk_and_balance(hv, es, P->n_sm);
+  chunk_and_balance(hu, es, P->n_sm);
+  upload_blockset<T>(P->nearset, hn);
+  upload_blockset<T>(P->Vset, hv);
+  upload_blockset<T>(P->Uset, hu);
+
+  // ---- fill the blobs: from host operators or assembled on the device
+  DevBuf<double> pts;
+  const bool need_geom = !d->near_blob || !d->V_blob || !d->U_blob;
+  if (need_geom) {
+    require(d->points_tree && d->leaf_center && d->leaf_r_check && d->leaf_r_inaux &&
+                d->out_fit_leaf && d->check_cos && d->check_sin && d->aux_cos && d->aux_sin,
+            "device assembly needs the geometry fields of nesa_plan_desc");
+    pts.upload(std::vector<double>(d->points_tree, d->points_tree + 2 * P->N));
+  }
+  T* nblob = reinterpret_cast<T*>(P->nearset.blob.p);
+  T* vblob = reinterpret_cast<T*>(P->Vset.blob.p);
+  T* ublob = reinterpret_cast<T*>(P->Uset.blob.p);
+  if (d->near_blob) {
+    upload_host_blob<T>(P->nearset, hn, d->near_blob, near_src_off, near_src_rows, near_row0);
+  } else if (!hn.items.empty()) {
+    assemble_near_kernel<T><<<int(hn.items.size()), 256>>>(P->nearset.items.p, P->nearset.segs.p,
+                                                            pts.p, nblob);
+    CUDA_OK(cudaGetLastError());
+  }
+  DevBuf<double> center, rck, rax, fit, cc, cs, ac, as;
+  DevBuf<int64_t> vleaf, uleaf;
+  if (!d->V_blob || !d->U_blob) {
+    center.upload(std::vector<double>(d->leaf_center, d->leaf_center + 2 * NL));
+    rck.upload(std::vector<double>(d->leaf_r_check, d->leaf_r_check + NL));
+    rax.upload(std::vector<double>(d->leaf_r_inaux, d->leaf_r_inaux + NL));
+    fit.upload(std::vector<double>(d->out_fit_leaf, d->out_fit_leaf + int64_t(Q) * P->n_check));
+    cc.upload(std::vector<double>(d->check_cos, d->check_cos + P->n_check));
+    cs.upload(std::vector<double>(d->check_sin, d->check_sin + P->n_check));
+    ac.upload(std::vector<double>(d->aux_cos, d->aux_cos + Q));
+    as.upload(std::vector<double>(d->aux_sin, d->aux_sin + Q));
+    vleaf.upload(v_leaf);
+    uleaf.upload(u_leaf);
+  }
+  if (d->V_blob) {
+    upload_host_blob<T>(P->Vset, hv, d->V_blob, v_src_off, v_src_rows, v_row0);
+  } else if (!hv.items.empty()) {
+    assemble_V_kernel<T><<<int(hv.items.size()), 128, P->n_check * sizeof(double)>>>(
+        P->Vset.items.p, vleaf.p, pts.p, center.p, rck.p, fit.p, cc.p, cs.p, Q, P->n_check, vblob);
+    CUDA_OK(cudaGetLastError());
+  }
+  if (d->U_blob) {
+    upload_host_blob<T>(P->Uset, hu, d->U_blob, u_src_off, u_src_rows, u_row0);
+  } else if (!hu.items.empty()) {
+    assemble_U_kernel<T><<<int(hu.items.size()), 256>>>(P->Uset.items.p, uleaf.p, pts.p, center.p,
+                                                         rax.p, ac.p, as.p, ublob);
+    CUDA_OK(cudaGetLastError());
+  }
+  CUDA_OK(cudaDeviceSynchronize());
+
+  // ---- translation tiles over the local targets of every level
+  {
+    std::vector<TransTile> tiles;
+    std::vector<TransRun> runs;
+    std::vector<TransPair> pairs;
+    struct E {
+      int32_t dtab, tgt, src;
+    };
+    std::vector<E> buf;
+    for (int lv = P->l0; lv <= P->L; ++lv) {
+      const int li = lv - P->l0;
+      const int64_t tf = P->loc_first[li], tc = P->loc_count[li];
+      for (int64_t t0 = 0; t0 < tc; t0 += kTransTile) {
+        const int32_t nt = int32_t(std::min<int64_t>(kTransTile, tc - t0));
+        buf.clear();
+        for (int32_t t = 0; t < nt; ++t) {
+          const int64_t g = tf + t0 + t;
+          for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
+            const int64_t dt = d->int_dtab[e];
+            require(dt >= 0 && dt < d->n_dtab, "D index out of range");
+            buf.push_back(E{int32_t(dt), t, int32_t(d->int_idx[e])});
+          }
+        }
+        std::stable_sort(buf.begin(), buf.end(), [](const E& x, const E& y) {
+          return x.dtab != y.dtab ? x.dtab < y.dtab : x.tgt < y.tgt;
+        });
+        TransTile tl{int32_t(tf + t0), nt, int32_t(runs.size()), 0};
+        for (size_t i = 0; i < buf.size();) {
+          size_t j = i;
+          while (j < buf.size() && buf[j].dtab == buf[i].dtab) ++j;
+          runs.push_back(TransRun{buf[i].dtab, int32_t(pairs.size()),
+                                  int32_t(pairs.size() + (j - i)), 0});
+          for (size_t k = i; k < j; ++k) {
+            require(k == i || buf[k].tgt != buf[k - 1].tgt, "duplicate offset for one target");
+            pairs.push_back(TransPair{buf[k].tgt, buf[k].src});
+          }
+          i = j;
+        }
+        tl.run_end = int32_t(runs.size());
+        tiles.push_back(tl);
+        P->d_refs += int64_t(buf.size());
+      }
+    }
+    P->ttiles.upload(tiles);
+    P->truns.upload(runs);
+    P->tpairs.upload(pairs);
+    P->n_ttiles = int(tiles.size());
+  }
+}
+
+template <typename T>
+void ensure_workspace(nesa_plan* P, int R) {
+  if (P->ws_R >= R) return;
+  const size_t es = sizeof(T);
+  P->qt.alloc(size_t(P->N) * R * es);
+  P->phin.alloc(size_t(P->N) * R * es);
+  P->s.alloc(size_t(P->G) * P->Q * R * es);
+  P->o.alloc(size_t(P->G) * P->Q * R * es);
+  P->ws_R = R;
+}
+
+inline int grid_for(int64_t n, int threads, int cap) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap)));
+}
+
+template <typename T, int R, int MODE>
+void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
+                      int64_t perm_offset, cudaStream_t st) {
+  if (bs.n_items == 0) return;
+  BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.items.p, bs.segs.p, bs.chunks.p,
+                     bs.cta_ptr.p, x, y, base, perm, perm_offset};
+  constexpr size_t sm = blockgemv_smem_bytes<T, R>();
+  blockgemv_kernel<T, R, MODE><<<bs.grid, kBGThreads, sm, st>>>(a);
+}
+
+template <typename T, int R>
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  constexpr size_t sm = blockgemv_smem_bytes<T, R>();
+  CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeStore>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeScatter>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  CUDA_OK(cudaFuncSetAttribute(translate_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               200 * 1024));
+  done = true;
+}
+
+
+// Record a profiling event; during capture this becomes an event-record node
+// on the stream the neighbouring kernels run on.
+void prof_mark(nesa_plan* P, bool profile, int slot, cudaStream_t st) {
+  if (!profile) return;
+  CUDA_OK(cudaEventRecordWithFlags(P->cap_events[slot], st, cudaEventRecordExternal));
+}
+
+// Enqueue one product, or one of its two stages (multi-GPU), on P->s0/P->s1.
+//   stage 0: gather, fork{near | V, up, translate, down}, join, reception
+//   stage 1: gather, V, up                  (before the s halo exchange)
+//   stage 2: fork{near | translate, down}, join, reception
+template <typename T, int R>
+int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
+  const bool near = flags & NESA_NEAR, far = flags & NESA_FAR, prof = flags & NESA_PROFILE;
+  cudaStream_t s0 = P->s0, s1 = P->s1;
+  T* qt = reinterpret_cast<T*>(P->qt.p);
+  T* phin = reinterpret_cast<T*>(P->phin.p);
+  T* s = reinterpret_cast<T*>(P->s.p);
+  T* o = reinterpret_cast<T*>(P->o.p);
+  const T* CT = reinterpret_cast<const T*>(P->CT.p);
+  const T* BT = reinterpret_cast<const T*>(P->BT.p);
+  const int Q = P->Q;
+  const int64_t QQ = int64_t(Q) * Q;
+  const int cap = P->n_sm * 8;
+  const int NG = kLvlThreads / Q;
+  const int64_t nloc = P->pt_end - P->pt_begin;
+  int nk = 0;
+
+  auto up_pass = [&]() {
+    for (int lv = P->L; lv > P->l0; --lv) {
+      const int ci = lv - P->l0, pi = ci - 1;
+      const int64_t pc = P->loc_count[pi];
+      if (pc == 0) continue;
+      upward_kernel<T, R><<<grid_for(pc, NG, cap), kLvlThreads, 0, s0>>>(
+          CT + int64_t(ci - 1) * 4 * QQ, P->quad.p, P->child_first.p, P->n_child.p,
+          P->loc_first[pi], pc, P->loc_first[ci], P->loc_first[ci] + P->loc_count[ci], s, Q);
+      nk++;
+    }
+  };
+  auto down_pass = [&]() {
+    if (P->n_ttiles > 0) {
+      TransArgs<T> ta{P->ttiles.p, P->truns.p, P->tpairs.p, reinterpret_cast<const T*>(P->DT.p),
+                      P->dstride, s, o, Q};
+      translate_kernel<T, R>
+          <<<P->n_ttiles, kTransThreads, trans_smem_bytes<T, R>(Q, P->dstride), s0>>>(ta);
+      nk++;
+    }
+    for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
+      const int ci = lv - P->l0;
+      const int64_t cc = P->loc_count[ci];
+      if (cc == 0) continue;
+      downward_kernel<T, R><<<grid_for(cc, NG, cap), kLvlThreads, 0, s0>>>(
+          BT + int64_t(ci - 1) * 4 * QQ, P->quad.p, P->parent.p, P->loc_first[ci], cc, o, Q);
+      nk++;
+    }
+  };
+  auto gather = [&]() {
+    gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N);
+    nk++;
+  };
+  auto finish = [&]() {
+    prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
+    if (far) {
+      launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p, 0,
+                                           s0);
+      nk++;
+    } else if (near) {
+      scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
+          phin, P->perm.p + P->pt_begin, phi, P->pt_begin, nloc);
+      nk++;
+    } else {
+      CUDA_OK(cudaMemsetAsync(phi, 0, size_t(P->N) * R * sizeof(T), s0));
+    }
+    prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
+  };
+
+  if (stage == 0) {
+    prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
+    gather();
+    CUDA_OK(cudaEventRecord(P->ev_fork, s0));
+    CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
+    if (near) {
+      prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
+      launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
+      nk++;
+      prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
+    }
+    if (far) {
+      prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
+      launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
+      nk++;
+      up_pass();
+      down_pass();
+      prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
+    }
+    CUDA_OK(cudaEventRecord(P->ev_join, s1));
+    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
+    finish();
+    prof_mark(P, prof, 2 * NESA_STAGE_TOTAL + 1, s0);
+  } else if (stage == 1) {
+    gather();
+    if (far) {
+      launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
+      nk++;
+      up_pass();
+    }
+  } else {
+    CUDA_OK(cudaEventRecord(P->ev_fork, s0));
+    CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
+    if (near) {
+      launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
+      nk++;
+    }
+    if (far) down_pass();
+    CUDA_OK(cudaEventRecord(P->ev_join, s1));
+    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
+    finish();
+  }
+  return nk;
+}
+
+template <typename T>
+int enqueue_dispatch(nesa_plan* P, const void* q, void* phi, int R, uint32_t flags, int stage) {
+  switch (R) {
+    case 1:
+      set_smem_attrs<T, 1>();
+      return enqueue_T<T, 1>(P, static_cast<const T*>(q), static_cast<T*>(phi), flags, stage);
+    case 2:
+      set_smem_attrs<T, 2>();
+      return enqueue_T<T, 2>(P, static_cast<const T*>(q), static_cast<T*>(phi), flags, stage);
+    case 4:
+      set_smem_attrs<T, 4>();
+      return enqueue_T<T, 4>(P, static_cast<const T*>(q), static_cast<T*>(phi), flags, stage);
+    default:
+      throw NesaError(NESA_ERR_UNSUPPORTED, "nrhs * (1 + is_complex) must be 1, 2 or 4");
+  }
+}
+
+int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_complex,
+               uint32_t flags, void* stream, int stage) {
+  require(P != nullptr, "null plan");
+  require(nrhs >= 1, "nrhs must be >= 1");
+  require(q != nullptr && phi != nullptr, "null vector");
+  require(stage == 0 || !(flags & NESA_PROFILE), "profiling needs a full product");
+  const int R = nrhs * (is_complex ? 2 : 1);
+  CUDA_OK(cudaSetDevice(P->device));
+  if (P->dtype == NESA_F64)
+    ensure_workspace<double>(P, R);
+  else
+    ensure_workspace<float>(P, R);
+  nesa_plan::GraphKey key{q, phi, R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE), stage};
+  auto itg = P->graphs.find(key);
+  if (itg == P->graphs.end()) {
+    cudaGraph_t g = nullptr;
+    CUDA_OK(cudaStreamBeginCapture(P->s0, cudaStreamCaptureModeThreadLocal));
+    int nk = 0;
+    try {
+      nk = P->dtype == NESA_F64 ? enqueue_dispatch<double>(P, q, phi, R, flags, stage)
+                                : enqueue_dispatch<float>(P, q, phi, R, flags, stage);
+    } catch (...) {
+      cudaStreamEndCapture(P->s0, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CUDA_OK(cudaStreamEndCapture(P->s0, &g));
+    nesa_plan::GraphEntry ent;
+    CUDA_OK(cudaGraphInstantiate(&ent.exec, g, 0));
+    if (flags & NESA_PROFILE) {
+      size_t n = 0;
+      CUDA_OK(cudaGraphGetNodes(g, nullptr, &n));
+      std::vector<cudaGraphNode_t> nodes(n);
+      CUDA_OK(cudaGraphGetNodes(g, nodes.data(), &n));
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        CUDA_OK(cudaGraphNodeGetType(nd, &ty));
+        if (ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev;
+        CUDA_OK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+        for (int slot = 0; slot < 2 * NESA_N_STAGES; ++slot)
+          if (P->cap_events[slot] == ev) ent.ev_nodes.emplace_back(nd, slot);
+      }
+    }
+    CUDA_OK(cudaGraphDestroy(g));
+    if (stage == 0) P->kernels_per_matvec = nk;
+    itg = P->graphs.emplace(key, ent).first;
+  }
+  if (flags & NESA_PROFILE) {
+    if (P->prof_used == P->prof_events.size()) {
+      std::vector<cudaEvent_t> evs(2 * NESA_N_STAGES);
+      for (auto& e : evs) CUDA_OK(cudaEventCreate(&e));
+      P->prof_events.push_back(evs);
+    }
+    auto& evs = P->prof_events[P->prof_used++];
+    for (auto& pr : itg->second.ev_nodes)
+      CUDA_OK(cudaGraphExecEventRecordNodeSetEvent(itg->second.exec, pr.first, evs[pr.second]));
+  }
+  CUDA_OK(cudaGraphLaunch(itg->second.exec, static_cast<cudaStream_t>(stream)));
+  return NESA_OK;
+}
+
+}  // namespace
+
+#define NESA_API extern "C" __attribute__((visibility("default")))
+
+#define NESA_GUARD(body)                              \
+  try {                                               \
+    body;                                             \
+  } catch (const NesaError& e) {                      \
+    g_last_error = e.what();                          \
+    return e.code;                                    \
+  } catch (const std::exception& e) {                 \
+    g_last_error = e.what();                          \
+    return NESA_ERR_INVALID;                          \
+  }
+
+NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** out) {
+  NESA_GUARD({
+    require(d != nullptr && out != nullptr, "null argument");
+    *out = nullptr;
+    require(d->abi_version == NESA_ABI_VERSION, "ABI version mismatch");
+    require(d->op_dtype == NESA_F64 || d->op_dtype == NESA_F32, "op_dtype must be F64 or F32");
+    require(d->Q >= 3 && d->Q <= 256, "Q must be in [3, 256]");
+    require(d->N >= 1 && d->n_leaves >= 1 && d->n_groups >= d->n_leaves, "bad sizes");
+    require(d->L >= d->l0 && d->l0 >= 0, "bad levels");
+    require(d->N < (int64_t(1) << 31), "N must fit in int32");
+    require(d->perm && d->group_start && d->group_stop && d->parent && d->quad && d->level_first &&
+                d->level_count && d->nbr_ptr && d->nbr_idx && d->int_ptr && d->int_idx &&
+                d->int_dtab && d->D,
+            "missing tree / table arrays");
+    require(d->L == d->l0 || (d->C && d->B), "missing C/B tables");
+    std::unique_ptr<nesa_plan> P(new nesa_plan());
+    P->device = device;
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaDeviceGetAttribute(&P->n_sm, cudaDevAttrMultiProcessorCount, device));
+    P->dtype = d->op_dtype;
+    P->esz = d->op_dtype == NESA_F64 ? 8 : 4;
+    P->Q = d->Q;
+    P->n_check = d->n_check;
+    P->l0 = d->l0;
+    P->L = d->L;
+    P->N = d->N;
+    P->NL = d->n_leaves;
+    P->G = d->n_groups;
+    P->leaf_begin = d->leaf_begin;
+    P->leaf_end = d->leaf_end;
+    if (P->leaf_end <= P->leaf_begin) {
+      P->leaf_begin = 0;
+      P->leaf_end = P->NL;
+    }
+    require(P->leaf_begin >= 0 && P->leaf_end <= P->NL, "leaf range out of bounds");
+    P->pt_begin = d->group_start[P->leaf_begin];
+    P->pt_end = d->group_stop[P->leaf_end - 1];
+    const int nlev = P->L - P->l0 + 1;
+    P->lvl_first.assign(d->level_first, d->level_first + nlev);
+    P->lvl_count.assign(d->level_count, d->level_count + nlev);
+    require(P->lvl_first[nlev - 1] == 0 && P->lvl_count[nlev - 1] == P->NL,
+            "leaves must be ids 0..n_leaves-1");
+    if (P->dtype == NESA_F64)
+      build_plan_T<double>(P.get(), d);
+    else
+      build_plan_T<float>(P.get(), d);
+    CUDA_OK(cudaStreamCreateWithFlags(&P->s0, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&P->s1, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
+    for (auto& e : P->cap_events) CUDA_OK(cudaEventCreate(&e));
+    *out = P.release();
+    return NESA_OK;
+  })
+}
+
+NESA_API int nesa_matvec(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t nrhs,
+                         int32_t is_complex, uint32_t flags, void* stream) {
+  NESA_GUARD(return run_matvec(plan, q_dev, phi_dev, nrhs, is_complex, flags, stream, 0));
+}
+
+NESA_API int nesa_matvec_stage(nesa_plan* plan, int32_t stage, const void* q_dev, void* phi_dev,
+                               int32_t nrhs, int32_t is_complex, uint32_t flags, void* stream) {
+  NESA_GUARD({
+    require(stage == 1 || stage == 2, "stage must be 1 or 2");
+    return run_matvec(plan, q_dev, phi_dev, nrhs, is_complex, flags, stream, stage);
+  })
+}
+
+NESA_API void* nesa_plan_s_dev(nesa_plan* plan, int32_t nrhs_real) {
+  try {
+    if (!plan) return nullptr;
+    CUDA_OK(cudaSetDevice(plan->device));
+    if (plan->dtype == NESA_F64)
+      ensure_workspace<double>(plan, nrhs_real);
+    else
+      ensure_workspace<float>(plan, nrhs_real);
+    return plan->s.p;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return nullptr;
+  }
+}
+
+NESA_API int nesa_plan_destroy(nesa_plan* plan) {
+  NESA_GUARD({
+    delete plan;
+    return NESA_OK;
+  })
+}
+
+NESA_API const char* nesa_last_error(void) { return g_last_error.c_str(); }
+
+NESA_API int nesa_abi_version(void) { return NESA_ABI_VERSION; }
+
+NESA_API int64_t nesa_plan_stat(nesa_plan* P, int32_t which) {
+  if (!P) return -1;
+  switch (which) {
+    case NESA_STAT_NEAR_ENTRIES:
+      return P->nearset.entries;
+    case NESA_STAT_V_ENTRIES:
+      return P->Vset.entries;
+    case NESA_STAT_U_ENTRIES:
+      return P->Uset.entries;
+    case NESA_STAT_D_REFS:
+      return P->d_refs;
+    case NESA_STAT_N_DTAB:
+      return P->n_dtab;
+    case NESA_STAT_DEVICE_BYTES: {
+      int64_t b = int64_t(P->nearset.blob.n + P->Vset.blob.n + P->Uset.blob.n + P->CT.n +
+                          P->BT.n + P->DT.n + P->qt.n + P->phin.n + P->s.n + P->o.n);
+      return b;
+    }
+    case NESA_STAT_NEAR_CTAS:
+      return P->nearset.grid;
+    case NESA_STAT_KERNELS_PER_MATVEC:
+      return P->kernels_per_matvec;
+    default:
+      return -1;
+  }
+}
+
+NESA_API int nesa_profile_reset(nesa_plan* P) {
+  NESA_GUARD({
+    require(P != nullptr, "null plan");
+    CUDA_OK(cudaSetDevice(P->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    P->prof_used = 0;
+    return NESA_OK;
+  })
+}
+
+NESA_API int nesa_profile_read(nesa_plan* P, int32_t stage, float* ms, int32_t max) {
+  try {
+    require(P != nullptr && ms != nullptr, "null argument");
+    require(stage >= 0 && stage < NESA_N_STAGES, "bad stage");
+    CUDA_OK(cudaSetDevice(P->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    int n = 0;
+    for (size_t i = 0; i < P->prof_used && n < max; ++i) {
+      float t = 0;
+      if (cudaEventElapsedTime(&t, P->prof_events[i][2 * stage], P->prof_events[i][2 * stage + 1]) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      ms[n++] = t;
+    }
+    return n;
+  } catch (const NesaError& e) {
+    g_last_error = e.what();
+    return -e.code;
+  }
+}

@@ -1,0 +1,162 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs and the oracle.
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-12 for float64 /
+complex128 plans, <= 1e-5 for float32 / complex64 plans, near field alone
+<= 1e-13 (test_fastmvp.py:35-40 bar) in float64.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, grid_points
+from oracle.mvp_oracle import mvp_serial as oracle_mvp, rel_l2
+from paper_1801_03589_b200 import geometry as geo
+from paper_1801_03589_b200 import mvp, task_counts
+from paper_1801_03589_b200.operators import NesaParams, build_all
+from paper_1801_03589_b200.plan import NesaPlan
+from paper_1801_03589_b200.quadtree import TreeParams, build_tree
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _problem(g):
+    tree = build_tree(g["points"], TreeParams(P=int(g["P"])))
+    params = NesaParams(Q=int(g["Q"]))
+    return tree, params
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_f64_device_assembled_vs_golden(golden, name):
+    g = golden(name)
+    tree, params = _problem(g)
+    q = g["q"]
+    assert rel_l2(mvp(tree, params, q), g["phi"]) <= 1e-12
+    assert rel_l2(mvp(tree, params, q, far=False), g["phi_near"]) <= 1e-13
+    assert rel_l2(mvp(tree, params, q, near=False), g["phi_far"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["fastmvp_1500", "grid4_single_level", "c1_wave_2000",
+                                  "c1_circle_2000", "annulus_1024"])
+def test_f64_host_operators_vs_golden(golden, name):
+    # drop-in route: host OperatorSet (build_all) uploaded as is
+    g = golden(name)
+    tree, params = _problem(g)
+    ops = build_all(tree, params)
+    q = g["q"]
+    assert rel_l2(mvp(tree, ops, q), g["phi"]) <= 1e-12
+    assert rel_l2(mvp(tree, ops, q, far=False), g["phi_near"]) <= 1e-13
+    assert rel_l2(mvp(tree, ops, q, near=False), g["phi_far"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_c64_vs_golden(golden, name):
+    g = golden(name)
+    tree, params = _problem(g)
+    q = g["q"]
+    q32 = q.astype(np.complex64 if np.iscomplexobj(q) else np.float32)
+    phi = mvp(tree, params, q32)
+    assert phi.dtype == q32.dtype
+    assert rel_l2(phi, g["phi"]) <= 1e-5
+
+
+def test_zero_in_zero_out_and_wrong_length(golden):
+    g = golden("fastmvp_1500")
+    tree, params = _problem(g)
+    z = mvp(tree, params, np.zeros(tree.n_points))
+    assert (z == 0).all()
+    with pytest.raises(ValueError):
+        mvp(tree, params, np.ones(3))
+    with pytest.raises(ValueError):
+        mvp(tree, params, np.ones((tree.n_points, 2, 2)))
+
+
+def test_deterministic_and_no_stale_sums(golden):
+    g = golden("c1_wave_2000")
+    tree, params = _problem(g)
+    q = g["q"]
+    a = mvp(tree, params, q)
+    b = mvp(tree, params, 3.0 * q)
+    c = mvp(tree, params, q)
+    assert np.array_equal(a, c)                 # bitwise run-to-run
+    assert rel_l2(b, 3.0 * a) <= 1e-14          # linearity, no stale sums
+
+
+def test_multi_rhs_matches_columns(golden):
+    g = golden("c1_circle_2000")
+    tree, params = _problem(g)
+    pts = g["points"]
+    Qm = geo.plane_wave_rhs(tree.points[np.argsort(tree.perm)], 4.0, n_waves=2)
+    ref = np.stack([g["phi"]], 1)
+    phi = mvp(tree, params, Qm)
+    assert phi.shape == Qm.shape
+    ops = build_all(tree, params)
+    exp = oracle_mvp(tree, ops, Qm)
+    assert rel_l2(phi, exp) <= 1e-12
+    del ref, pts
+
+
+def test_single_level_tree():
+    pts = grid_points(4)
+    tree = build_tree(pts, TreeParams(P=16))
+    params = NesaParams(Q=14)
+    q = np.random.default_rng(1).standard_normal(16)
+    counts = task_counts(tree)
+    assert counts["source-transfer"] == 0
+    assert rel_l2(mvp(tree, params, q), oracle_mvp(tree, build_all(tree, params), q)) <= 1e-12
+
+
+def test_permutation_equivariance():
+    # test_fastmvp.py:156-168
+    pts = geo.generate_sources(geo.CurveSpec(), 1500)
+    rng = np.random.default_rng(5)
+    perm = rng.permutation(len(pts))
+    q = rng.standard_normal(len(pts))
+    ta = build_tree(pts, TreeParams(P=40))
+    tb = build_tree(pts[perm], TreeParams(P=40))
+    p = NesaParams(Q=12)
+    phi_a = mvp(ta, p, q)
+    phi_b = mvp(tb, p, q[perm])
+    np.testing.assert_allclose(phi_b, phi_a[perm], rtol=1e-10, atol=1e-12)
+
+
+def test_torch_device_tensors_roundtrip(golden):
+    g = golden("c1_wave_2000")
+    tree, params = _problem(g)
+    qd = torch.from_numpy(g["q"]).cuda()
+    phi = mvp(tree, params, qd)
+    assert phi.is_cuda and phi.dtype == torch.complex128
+    assert rel_l2(phi.cpu().numpy(), g["phi"]) <= 1e-12
+
+
+def test_large_tall_leaves_paneled():
+    # leaves with > 512 points exercise the row panels of near and U
+    pts = geo.generate_sources(geo.CurveSpec(), 6000)
+    tree = build_tree(pts, TreeParams(P=700))
+    assert max(g.n_points for g in tree.leaves()) > 512
+    params = NesaParams(Q=12)
+    q = np.random.default_rng(3).standard_normal(6000)
+    ops = build_all(tree, params)
+    assert rel_l2(mvp(tree, params, q), oracle_mvp(tree, ops, q)) <= 1e-12
+
+
+def test_plan_stats(golden):
+    g = golden("c2_wave_20000")
+    tree, params = _problem(g)
+    plan = NesaPlan(tree, params, dtype="f32")
+    a = tree.arrays
+    sizes = a.stop - a.start
+    e_near = sum(int(sizes[i]) * int(sizes[a.nbr_idx[a.nbr_ptr[i]:a.nbr_ptr[i + 1]]].sum())
+                 for i in range(a.level_count[tree.L]))
+    assert plan.stat("near_entries") == e_near
+    assert plan.stat("v_entries") == tree.n_points * params.Q
+    assert plan.stat("d_refs") == int(a.int_ptr[-1])
+    plan.close()

@@ -1,0 +1,117 @@
+"""The CPU oracle pinned to the reference's own outputs (tests/golden).
+
+oracle/mvp_oracle.mvp_serial restates fastmvp.py:142-172; in real float64 it
+must be bit-identical to the reference, for complex q equal to the
+reference's Re/Im pair of calls to <= 1e-14.  The host operator assembly
+(paper_1801_03589_b200.operators.build_all) is pinned by the reference's
+per-matrix checksums.  Also the reference's hot-path property tests
+(test_fastmvp.py:35-168) against the oracle.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, grid_points
+from oracle.mvp_oracle import (dense_matvec, mvp_serial, near_mask_dense, rel_l2,
+                               task_counts)
+from paper_1801_03589_b200 import geometry as geo
+from paper_1801_03589_b200.operators import NesaParams, build_all
+from paper_1801_03589_b200.quadtree import TreeParams, build_tree
+
+COUNT_KEYS = ("near", "radiation", "source-transfer", "translation", "potential-transfer",
+              "reception")
+
+
+def _problem(g):
+    tree = build_tree(g["points"], TreeParams(P=int(g["P"])))
+    ops = build_all(tree, NesaParams(Q=int(g["Q"])))
+    return tree, ops
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_operator_checksums(golden, name):
+    g = golden(name)
+    tree, ops = _problem(g)
+    for tab in ("V", "U", "C", "B", "D", "near"):
+        d = getattr(ops, tab)
+        keys = sorted(d)
+        s = np.array([float(np.sum(d[k])) for k in keys])
+        a = np.array([float(np.sum(np.abs(d[k]))) for k in keys])
+        np.testing.assert_allclose(s, g[f"ops_{tab}_sum"], rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(a, g[f"ops_{tab}_abs"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_oracle_matches_reference(golden, name):
+    g = golden(name)
+    tree, ops = _problem(g)
+    q = g["q"]
+    for key, kw in (("phi", {}), ("phi_near", {"far": False}), ("phi_far", {"near": False})):
+        phi = mvp_serial(tree, ops, q, **kw)
+        if np.iscomplexobj(q):
+            assert rel_l2(phi, g[key]) <= 1e-14, key
+        else:
+            assert np.array_equal(phi, g[key]), key      # bit-identical in float64
+    assert [task_counts(tree)[k] for k in COUNT_KEYS] == g["task_counts"].tolist()
+
+
+@pytest.mark.parametrize("name", ["fastmvp_1500", "c1_wave_2000", "c1_circle_2000",
+                                  "annulus_1024"])
+def test_oracle_accuracy_vs_dense(golden, name):
+    g = golden(name)
+    tree, ops = _problem(g)
+    q = g["q"]
+    assert rel_l2(dense_matvec(g["points"], q), g["phi_dense"]) <= 1e-14
+    # NESA approximation error: ~2e-4 at Q=10, <=1e-4 from Q=12 (README.md:50-54)
+    tol = 1e-3 if int(g["Q"]) <= 10 else 1e-4
+    assert rel_l2(mvp_serial(tree, ops, q), g["phi_dense"]) <= tol
+
+
+def test_near_field_exact():
+    pts = geo.generate_sources(geo.CurveSpec(), 1500)
+    tree = build_tree(pts, TreeParams(P=40))
+    ops = build_all(tree, NesaParams(Q=12))
+    q = np.random.default_rng(0).standard_normal(1500)
+    ref = near_mask_dense(tree, pts) @ q
+    assert rel_l2(mvp_serial(tree, ops, q, far=False), ref) <= 1e-13
+
+
+def test_zero_and_wrong_length():
+    pts = geo.generate_sources(geo.CurveSpec(), 800)
+    tree = build_tree(pts, TreeParams(P=20))
+    ops = build_all(tree, NesaParams(Q=10))
+    assert (mvp_serial(tree, ops, np.zeros(800)) == 0).all()
+    with pytest.raises(ValueError):
+        mvp_serial(tree, ops, np.ones(3))
+
+
+def test_single_level_tree():
+    pts = grid_points(4)
+    tree = build_tree(pts, TreeParams(P=16))
+    assert tree.L == tree.l0
+    ops = build_all(tree, NesaParams(Q=14))
+    q = np.random.default_rng(1).standard_normal(16)
+    assert rel_l2(mvp_serial(tree, ops, q), dense_matvec(pts, q)) <= 1e-5
+
+
+def test_multi_rhs_oracle_is_columnwise():
+    pts = geo.generate_sources(geo.CurveSpec(), 1000)
+    tree = build_tree(pts, TreeParams(P=30))
+    ops = build_all(tree, NesaParams(Q=10))
+    Qm = geo.plane_wave_rhs(pts, 5.0, n_waves=3)
+    phi = mvp_serial(tree, ops, Qm)
+    for m in range(3):
+        assert rel_l2(phi[:, m], mvp_serial(tree, ops, Qm[:, m])) <= 1e-15
+
+
+def test_sampled_oracle_is_prefix():
+    pts = geo.generate_sources(geo.CurveSpec(), 3000)
+    tree = build_tree(pts, TreeParams(P=30))
+    ops = build_all(tree, NesaParams(Q=10))
+    q = np.random.default_rng(2).standard_normal(3000)
+    full = mvp_serial(tree, ops, q, far=False)
+    part = mvp_serial(tree, ops, q, far=False, fraction=0.5)
+    nl = len(tree.leaves())
+    done = tree.leaves()[(nl + 1) // 2 - 1].stop
+    rows = tree.perm[:done]
+    assert np.array_equal(part[rows], full[rows])
