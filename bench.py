@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: NESA matvecs/s at N = 2M on 1..8 B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3], "C4"), Track A 2D analog:
+N = 2,000,000 points on the ellipse+plates union (seed 3), leaf target P = 64,
+Q = 64 equivalent sources, complex64 right-hand side (N(0,1) + 1j N(0,1),
+seed 3, separate generator), float32 operators.  One step = one full product
+phi = K~ q (gather, near field, radiation, upward, translation, downward,
+reception, scatter).  Inputs stay resident in HBM for ``value``; ``e2e``
+goes through the public API (paper_1801_03589_b200.mvp) with pinned host
+buffers, host<->device copies inside the timed region.
+
+``--impl reference`` times the reference's CPU algorithm -- the oracle port
+(oracle/mvp_oracle.py, the restated taskfmm mvp_serial; the reference itself
+is pure Python and not present on the GPU box) -- on a bounded sample of the
+same workload (first 1/16 of every stage loop, Re and Im as two real calls),
+scaled to matvecs/s.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+N_POINTS = 2_000_000
+SEED = 3
+LEAF_P = 64
+Q_AUX = 64
+SAMPLE_FRACTION = 1.0 / 16.0
+METRIC = "NESA matvecs/sec at N=2M (1/2/4/8 B200); achieved HBM GB/s vs roofline"
+UNIT = "matvecs/s"
+
+
+def workload_config(n=N_POINTS, world=1):
+    return {
+        "workload": f"C4 2D analog: ellipse(5,0.5)+2 plates, N={n:,}, seed {SEED}, "
+                    f"leaf P={LEAF_P}, Q={Q_AUX}, complex64 rhs, float32 operators",
+        "N": n, "P": LEAF_P, "Q": Q_AUX, "geometry": "ellipse-plates", "seed": SEED,
+        "vectors": "complex64", "operators": "float32",
+        "parallelism": f"morton-partition x{world}" if world > 1 else "single-gpu",
+        "l2": "no flush needed: each step streams ~3.3 GB of operators (> 126 MB L2)",
+    }
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_POINTS, help="points (default 2M)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args(argv)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def build_problem(n):
+    import paper_1801_03589_b200 as nesa
+    t0 = time.perf_counter()
+    pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=SEED), n)
+    t1 = time.perf_counter()
+    tree = nesa.build_tree(pts, nesa.TreeParams(P=LEAF_P))
+    t2 = time.perf_counter()
+    params = nesa.NesaParams(Q=Q_AUX)
+    tables = nesa.build_tables(tree, params)
+    t3 = time.perf_counter()
+    q = nesa.random_rhs(n, SEED).astype(np.complex64)
+    return pts, tree, params, tables, q, {"points_s": t1 - t0, "tree_s": t2 - t1,
+                                          "tables_s": t3 - t2}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except (OSError, ValueError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r)
+                          if v.lower().startswith("active")})
+        sm = [r[0] for r in rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """dram bytes/launch of the near kernel from the committed ncu capture."""
+    p = os.path.join(HERE, "profiles", "ncu_near_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port on a bounded sample)
+# ---------------------------------------------------------------------------
+def cpu_sample_setup(tree, params):
+    from oracle.sample import build_sampled_opset
+    return build_sampled_opset(tree, params, SAMPLE_FRACTION)
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_cpu_baseline(tree, params, q, repeats=2):
+    from oracle.sample import time_sample
+    ops = cpu_sample_setup(tree, params)
+    ts = [time_sample(tree, ops, q, SAMPLE_FRACTION) for _ in range(repeats)]
+    t = min(ts)
+    return {"value": SAMPLE_FRACTION / t, "unit": UNIT, "cores": cpu_threads(),
+            "kind": "port",
+            "sample": f"oracle port of taskfmm mvp_serial (fastmvp.py:142-172) on the first "
+                      f"1/{int(1 / SAMPLE_FRACTION)} of every stage loop at N={tree.n_points:,}; "
+                      f"complex q as two real calls (Re, Im); min of {repeats}; "
+                      f"{t:.3f} s per sample; value = fraction / time",
+            "seconds_per_sample": t}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if world > 1 and rank != 0:
+        return
+    pts, tree, params, tables, q, _ = build_problem(args.n)
+    from oracle.sample import time_sample
+    ops = cpu_sample_setup(tree, params)
+    for _ in range(args.warmup):
+        time_sample(tree, ops, q, SAMPLE_FRACTION)
+    times = [time_sample(tree, ops, q, SAMPLE_FRACTION) for _ in range(args.steps)]
+    tot = float(np.sum(times))
+    value = args.steps * SAMPLE_FRACTION / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.n, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                         "sample": f"each step: first 1/{int(1 / SAMPLE_FRACTION)} of every "
+                                   "stage loop of the oracle port of mvp_serial "
+                                   "(float64, complex q as Re+Im real calls); "
+                                   "matvecs/s = steps * fraction / time"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.plan import NesaPlan, algorithmic_bytes
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    pts, tree, params, tables, q, build_t = build_problem(args.n)
+    t0 = time.perf_counter()
+    if world > 1:
+        from paper_1801_03589_b200.dist import DistNesa
+        engine = DistNesa(tree, tables, dtype="f32", device=local_rank)
+        plan = engine.plan
+    else:
+        engine = None
+        plan = NesaPlan(tree, tables, dtype="f32", device=local_rank)
+    torch.cuda.synchronize()
+    build_t["plan_s"] = time.perf_counter() - t0
+
+    qd = torch.from_numpy(q).to(dev)
+    phid = torch.empty_like(qd)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=False):
+        if engine is not None:
+            engine.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream)
+        else:
+            plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream,
+                            profile=profile)
+
+    prof = engine is None
+    for _ in range(max(args.warmup, 3)):
+        step(prof)
+    # grow the profiling event pool to K before timing, soak clocks ~1 s
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    if prof:
+        plan.profile_reset()
+    t_soak = time.perf_counter()
+    n_soak = 0
+    while time.perf_counter() - t_soak < 1.0 or (prof and n_soak < args.steps):
+        step(prof)
+        n_soak += 1
+        if n_soak % 50 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    if prof:
+        plan.profile_reset()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(prof)
+    ev1.record(stream)
+    ev1.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = 1e3 / ms_step            # whole-job products per second (strong scaling)
+
+    # roofline of the dominant kernel (near field), from the in-graph events
+    alg = algorithmic_bytes(plan, 2)
+    roofline = None
+    stages = {}
+    if prof:
+        for st in ("total", "near", "far", "reception"):
+            d = plan.profile_read(st)
+            stages[st] = float(np.mean(d)) if d.size else None
+        near_ms = stages["near"]
+        peak, peak_src = load_peaks()
+        near_bytes = alg["near"]
+        ach = near_bytes / (near_ms * 1e-3) / 1e9
+        traffic = load_traffic()
+        roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak,
+                    "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                    "kernel": "blockgemv_kernel<float,2,store> (near field)",
+                    "alg_bytes_per_launch": near_bytes, "avg_launch_ms": near_ms,
+                    "peak_source": peak_src}
+    matvec_bw = alg["total"] / (ms_step * 1e-3) / 1e9
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        qh = torch.from_numpy(q).pin_memory()
+        for _ in range(3):
+            nesa.mvp(tree, tables, qh)
+        torch.cuda.synchronize()
+        k2 = max(10, min(args.steps, 100))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k2):
+            out = nesa.mvp(tree, tables, qh)
+        e1.record(stream)
+        e1.synchronize()
+        e_ms = e0.elapsed_time(e1) / k2
+        e2e = {"value": 1e3 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(qh.numel() * 8),
+               "d2h_bytes_per_step": int(out.numel() * 8), "ms_per_step": e_ms,
+               "api": "paper_1801_03589_b200.mvp(tree, tables, pinned torch.complex64 (N,))"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(tree, params, q)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c64", "data": "synthetic (seeded ellipse+plates geometry, N(0,1) rhs)",
+            "config": workload_config(args.n, world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": plan.stat("kernels_per_matvec") * args.steps,
+            "clocks": clocks,
+            "matvec_alg_bytes": alg["total"], "matvec_achieved_gbs": matvec_bw,
+            "stage_ms": stages, "build_s": build_t,
+            "plan": {"near_entries": plan.stat("near_entries"),
+                     "v_entries": plan.stat("v_entries"), "d_refs": plan.stat("d_refs"),
+                     "n_dtab": plan.stat("n_dtab"), "levels": tree.L - tree.l0 + 1,
+                     "groups": tree.arrays.n_groups, "leaves": tree.n_leaves,
+                     "device_bytes": plan.stat("device_bytes")},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

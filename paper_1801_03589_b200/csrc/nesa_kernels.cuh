@@ -45,12 +45,23 @@ struct BlockSeg {
   int32_t x_row0;  // first x row of the segment
   int32_t col0;    // first column (within the item) of the segment
 };
-struct BlockChunk {
-  int32_t item;
-  int32_t col0;
-  int32_t ncols;
+
+// One bulk-copy chunk, self-contained in 128 bytes so the producer warp
+// fetches it with ONE coalesced load (lane l <- word l) and prefetches the
+// next one while the current is in flight: no dependent metadata loads on
+// the streaming path.
+constexpr int kRecSegs = 12;
+struct __align__(128) ChunkRec {
+  int64_t src_off;   // element offset of the chunk's first element in blob
+  int32_t m;         // rows of the item
+  int32_t ncols;     // columns in this chunk
+  int32_t y_row0;    // first output row of the item
+  int32_t flags;     // bit0 first chunk of its item, bit1 last chunk
+  int32_t nseg;      // x segments of this chunk (<= kRecSegs)
   int32_t pad;
+  int32_t seg[2 * kRecSegs];  // (x_row0, first column within the chunk) pairs
 };
+static_assert(sizeof(ChunkRec) == 128, "ChunkRec must be 128 bytes");
 
 constexpr int kStages = 4;
 constexpr int kABytes = 24 * 1024;         // payload per stage
@@ -66,44 +77,44 @@ enum { kModeStore = 0, kModeScatter = 1 };
 template <typename T>
 struct BlockGemvArgs {
   const T* blob;
-  const BlockItem* items;
-  const BlockSeg* segs;
-  const BlockChunk* chunks;
+  const ChunkRec* recs;
   const int32_t* cta_chunk_ptr;  // [grid + 1]
   const T* x;                    // x rows (R values each)
   T* y;                          // store: y rows; scatter: output in original order
   const T* base;                 // scatter: added per tree row (may be null)
   const int64_t* perm;           // scatter: tree row -> original row
-  int64_t perm_offset;           // scatter: tree row of perm[0] (sub-plans)
 };
 
-template <typename T, int R>
-constexpr size_t blockgemv_smem_bytes() {
-  return size_t(kStages) * kAStride + size_t(kStages) * kMaxC * R * sizeof(T) +
-         size_t(kNCT) * R * sizeof(T) + 2 * kStages * sizeof(uint64_t) + 16;
-}
+struct StageHdr {
+  int32_t m, ncols, delta, flags, y_row0, pad[3];
+};
+
+// Per-stage shared memory: [A | X | header | (scatter) perm | base]
+template <typename T, int R, int MODE>
+struct BGLayout {
+  static constexpr size_t kX = size_t(kMaxC) * R * sizeof(T);
+  static constexpr size_t kFinPerm = MODE == kModeScatter ? size_t(kMaxRows) * 8 : 0;
+  static constexpr size_t kFinBase = MODE == kModeScatter ? size_t(kMaxRows) * R * sizeof(T) : 0;
+  static constexpr size_t kStage =
+      ((kAStride + kX + sizeof(StageHdr) + kFinPerm + kFinBase) + 127) & ~size_t(127);
+  static constexpr size_t kRed = size_t(kNCT) * R * sizeof(T);
+  static constexpr size_t kBytes = kStages * kStage + kRed + 2 * kStages * sizeof(uint64_t) + 16;
+  static constexpr size_t offX = kAStride;
+  static constexpr size_t offHdr = kAStride + kX;
+  static constexpr size_t offPerm = offHdr + sizeof(StageHdr);
+  static constexpr size_t offBase = offPerm + kFinPerm;
+};
 
 template <typename T, int R, int MODE>
-__device__ __forceinline__ void bg_write(const BlockGemvArgs<T>& a, int row, const T* v) {
-  if constexpr (MODE == kModeStore) {
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) a.y[int64_t(row) * R + rr] = v[rr];
-  } else {
-    const int64_t dst = a.perm[row - a.perm_offset];
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
-      T b = a.base ? a.base[int64_t(row) * R + rr] : T(0);
-      a.y[dst * R + rr] = b + v[rr];
-    }
-  }
+constexpr size_t blockgemv_smem_bytes() {
+  return BGLayout<T, R, MODE>::kBytes;
 }
 
 template <typename T, int R, int MODE>
 __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGemvArgs<T> a) {
+  using Lay = BGLayout<T, R, MODE>;
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* sA = smem;
-  T* sX = reinterpret_cast<T*>(smem + size_t(kStages) * kAStride);
-  T* sRed = sX + kStages * kMaxC * R;
+  T* sRed = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
   uint64_t* full = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(sRed + kNCT * R) + 15) & ~uintptr_t(15));
   uint64_t* empty = full + kStages;
@@ -123,31 +134,54 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
 
   if (warp == kNCW) {
     // ------------------------------ producer ------------------------------
+    const int32_t* recw = reinterpret_cast<const int32_t*>(a.recs);
+    int32_t w_next = c0 < c1 ? __ldg(recw + int64_t(c0) * 32 + lane) : 0;
     for (int i = c0; i < c1; ++i) {
+      const int32_t w = w_next;
+      if (i + 1 < c1) w_next = __ldg(recw + int64_t(i + 1) * 32 + lane);
       const int k = i - c0, st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
-      mbar_wait(&empty[st], (round & 1u) ^ 1u);
-      const BlockChunk ch = a.chunks[i];
-      const BlockItem it = a.items[ch.item];
-      const uintptr_t src =
-          reinterpret_cast<uintptr_t>(a.blob + it.a_off + int64_t(ch.col0) * it.m);
-      const uint32_t bytes = uint32_t(ch.ncols) * uint32_t(it.m) * uint32_t(sizeof(T));
+      unsigned char* stg = smem + size_t(st) * Lay::kStage;
+      const uint32_t lo = uint32_t(__shfl_sync(0xffffffffu, w, 0));
+      const uint32_t hi = uint32_t(__shfl_sync(0xffffffffu, w, 1));
+      const int64_t src_off = int64_t((uint64_t(hi) << 32) | lo);
+      const int m = __shfl_sync(0xffffffffu, w, 2);
+      const int ncols = __shfl_sync(0xffffffffu, w, 3);
+      const int y_row0 = __shfl_sync(0xffffffffu, w, 4);
+      const int flags = __shfl_sync(0xffffffffu, w, 5);
+      const int nseg = __shfl_sync(0xffffffffu, w, 6);
+      const uintptr_t src = reinterpret_cast<uintptr_t>(a.blob + src_off);
+      const uint32_t bytes = uint32_t(ncols) * uint32_t(m) * uint32_t(sizeof(T));
       const uintptr_t s0 = src & ~uintptr_t(15);
       const uintptr_t s1 = (src + bytes + 15) & ~uintptr_t(15);
+      mbar_wait(&empty[st], (round & 1u) ^ 1u);
       if (lane == 0) {
+        StageHdr* h = reinterpret_cast<StageHdr*>(stg + Lay::offHdr);
+        h->m = m;
+        h->ncols = ncols;
+        h->delta = int(src - s0);
+        h->flags = flags;
+        h->y_row0 = y_row0;
         mbar_arrive_expect_tx(&full[st], uint32_t(s1 - s0));
-        bulk_g2s(sA + size_t(st) * kAStride, reinterpret_cast<const void*>(s0),
-                 uint32_t(s1 - s0), &full[st]);
+        bulk_g2s(stg, reinterpret_cast<const void*>(s0), uint32_t(s1 - s0), &full[st]);
       }
-      T* xs = sX + st * kMaxC * R;
-      const int cend = ch.col0 + ch.ncols;
-      for (int sg = it.seg_begin; sg < it.seg_begin + it.seg_count; ++sg) {
-        const BlockSeg S = a.segs[sg];
-        const int scol1 = (sg + 1 < it.seg_begin + it.seg_count) ? a.segs[sg + 1].col0 : it.n;
-        const int lo = max(S.col0, ch.col0), hi = min(scol1, cend);
-        for (int c = lo + lane; c < hi; c += 32)
-          cp_async_n<R * sizeof(T)>(xs + (c - ch.col0) * R,
-                                  a.x + int64_t(S.x_row0 + (c - S.col0)) * R);
+      T* xs = reinterpret_cast<T*>(stg + Lay::offX);
+      for (int sg = 0; sg < nseg; ++sg) {
+        const int xr = __shfl_sync(0xffffffffu, w, 8 + 2 * sg);
+        const int cs = __shfl_sync(0xffffffffu, w, 9 + 2 * sg);
+        const int ce = sg + 1 < nseg ? __shfl_sync(0xffffffffu, w, 11 + 2 * sg) : ncols;
+        for (int c = cs + lane; c < ce; c += 32)
+          cp_async_n<R * sizeof(T)>(xs + c * R, a.x + int64_t(xr + (c - cs)) * R);
+      }
+      if constexpr (MODE == kModeScatter) {
+        if (flags & 2) {
+          int64_t* sp = reinterpret_cast<int64_t*>(stg + Lay::offPerm);
+          T* sb = reinterpret_cast<T*>(stg + Lay::offBase);
+          for (int r = lane; r < m; r += 32) {
+            cp_async<8>(sp + r, a.perm + y_row0 + r);
+            if (a.base) cp_async_n<R * sizeof(T)>(sb + r * R, a.base + int64_t(y_row0 + r) * R);
+          }
+        }
       }
       cp_async_mbar_arrive_noinc(&full[st]);
     }
@@ -155,21 +189,21 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
     // ------------------------------ consumers -----------------------------
     const int tid = threadIdx.x;
     T acc0[R], acc1[R], accB[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = T(0);
     for (int i = c0; i < c1; ++i) {
       const int k = i - c0, st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
-      const BlockChunk ch = a.chunks[i];
-      const BlockItem it = a.items[ch.item];
-      const int m = it.m, nc = ch.ncols;
-      const uintptr_t src =
-          reinterpret_cast<uintptr_t>(a.blob + it.a_off + int64_t(ch.col0) * m);
-      const T* A = reinterpret_cast<const T*>(sA + size_t(st) * kAStride + (src & 15));
-      const T* X = sX + st * kMaxC * R;
-      if (ch.col0 == 0) {
+      const unsigned char* stg = smem + size_t(st) * Lay::kStage;
+      mbar_wait(&full[st], round & 1u);
+      const StageHdr h = *reinterpret_cast<const StageHdr*>(stg + Lay::offHdr);
+      const int m = h.m, nc = h.ncols;
+      const T* A = reinterpret_cast<const T*>(stg + h.delta);
+      const T* X = reinterpret_cast<const T*>(stg + Lay::offX);
+      if (h.flags & 1) {
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = T(0);
       }
-      mbar_wait(&full[st], round & 1u);
       if (m <= kNCT) {
         const int CL = kNCT / m;
         const int r = tid % m, cl = tid / m;
@@ -206,10 +240,21 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
 
-      if (ch.col0 + nc == it.n) {  // last chunk of the item: reduce + write
+      if (h.flags & 2) {  // last chunk of the item: reduce + write
+        const int64_t* sperm = reinterpret_cast<const int64_t*>(stg + Lay::offPerm);
+        const T* sbase = reinterpret_cast<const T*>(stg + Lay::offBase);
+        auto write = [&](int row, const T* v) {
+          if constexpr (MODE == kModeStore) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) a.y[int64_t(h.y_row0 + row) * R + rr] = v[rr];
+          } else {
+            const int64_t dst = sperm[row];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr)
+              a.y[dst * R + rr] = (a.base ? sbase[row * R + rr] : T(0)) + v[rr];
+          }
+        };
         if (m <= kNCT / 2) {
           const int CL = kNCT / m;
           const int r = tid % m, cl = tid / m;
@@ -226,13 +271,20 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
 #pragma unroll
               for (int rr = 0; rr < R; ++rr) v[rr] += sRed[(l * m + tid) * R + rr];
             }
-            bg_write<T, R, MODE>(a, it.y_row0 + tid, v);
+            write(tid, v);
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
           named_bar_sync(1, kNCT);
         } else {
-          if (tid < m) bg_write<T, R, MODE>(a, it.y_row0 + tid, acc0);
-          if (tid + kNCT < m) bg_write<T, R, MODE>(a, it.y_row0 + tid + kNCT, acc1);
+          if (tid < m) write(tid, acc0);
+          if (tid + kNCT < m) write(tid + kNCT, acc1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
         }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
       }
     }
   }
@@ -264,179 +316,420 @@ __global__ void scatter_kernel(const T* __restrict__ phin, const int64_t* __rest
 }
 
 // ----------------------------------------------------------------------------
-// Level transfers.  CT/BT hold the four quadrant matrices of one level,
-// transposed (MT[q][j][k] = M[q][k][j]) so thread k reads consecutive words.
+// Far-field micro-kernel.  All Q x Q operators (C, B, D) are stored
+// transposed with the output index padded to Qp = ceil(Q/4)*4:
+// MT[j * Qp + k] = M[k][j] (zero for k >= Q).  Amplitude vectors are staged
+// in shared memory as X[j * NC + col], one column per (group, rhs).  Thread
+// (rg, cg) owns a 4 x 4 register tile: rows 4rg.., columns 4cg.. and per j
+// does two 16-byte shared loads for 16 FMAs.
 // ----------------------------------------------------------------------------
-constexpr int kLvlThreads = 256;
+constexpr int kFarThreads = 256;
 
-// s[p] = sum over local children c of C[quad c] s[c]   (parents pf .. pf+pc-1)
-template <typename T, int R>
-__global__ void __launch_bounds__(kLvlThreads) upward_kernel(
-    const T* __restrict__ CT, const int32_t* __restrict__ quad,
-    const int64_t* __restrict__ child_first, const int32_t* __restrict__ n_child,
-    int64_t pf, int64_t pc, int64_t cf, int64_t cl, T* s, int Q) {
-  const int NG = kLvlThreads / Q;
-  const int g = threadIdx.x / Q, k = threadIdx.x % Q;
-  if (g >= NG) return;
-  const int64_t QQ = int64_t(Q) * Q;
-  for (int64_t pi = int64_t(blockIdx.x) * NG + g; pi < pc; pi += int64_t(gridDim.x) * NG) {
-    const int64_t p = pf + pi;
-    const int64_t c_lo = max(child_first[p], cf);
-    const int64_t c_hi = min(child_first[p] + n_child[p], cl);
-    T acc[R];
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) acc[rr] = T(0);
-    for (int64_t c = c_lo; c < c_hi; ++c) {
-      const T* M = CT + quad[c] * QQ;
-      const T* sv = s + c * Q * R;
-      T part[R];
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) part[rr] = T(0);
-      for (int j = 0; j < Q; ++j) {
-        const T mv = __ldg(M + j * Q + k);
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) part[rr] = fma(mv, __ldg(sv + j * R + rr), part[rr]);
-      }
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] += part[rr];
-    }
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) s[(p * Q + k) * R + rr] = acc[rr];
-  }
+struct FarGeom {
+  int Q, Qp, RG, CG, NC;  // rows, padded rows, row groups, column groups, columns
+};
+
+__host__ __device__ inline FarGeom far_geom(int Q) {
+  FarGeom g;
+  g.Q = Q;
+  g.Qp = (Q + 3) / 4 * 4;
+  g.RG = g.Qp / 4;
+  g.CG = kFarThreads / g.RG;
+  g.NC = g.CG * 4;
+  return g;
 }
 
-// o[c] += B[quad c] o[parent c]   (children cf .. cf+cc-1)
-template <typename T, int R>
-__global__ void __launch_bounds__(kLvlThreads) downward_kernel(
-    const T* __restrict__ BT, const int32_t* __restrict__ quad,
-    const int64_t* __restrict__ parent, int64_t cf, int64_t cc, T* o, int Q) {
-  const int NG = kLvlThreads / Q;
-  const int g = threadIdx.x / Q, k = threadIdx.x % Q;
-  if (g >= NG) return;
-  const int64_t QQ = int64_t(Q) * Q;
-  for (int64_t ci = int64_t(blockIdx.x) * NG + g; ci < cc; ci += int64_t(gridDim.x) * NG) {
-    const int64_t c = cf + ci;
-    const T* M = BT + quad[c] * QQ;
-    const T* ov = o + parent[c] * Q * R;
-    T acc[R];
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) acc[rr] = T(0);
-    for (int j = 0; j < Q; ++j) {
-      const T mv = __ldg(M + j * Q + k);
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] = fma(mv, ov[j * R + rr], acc[rr]);
-    }
-#pragma unroll
-    for (int rr = 0; rr < R; ++rr) o[(c * Q + k) * R + rr] += acc[rr];
-  }
-}
-
-// ----------------------------------------------------------------------------
-// Translation: one CTA per tile of <= kTransTile consecutive same-level
-// targets.  The tile's (target, source) pairs are grouped in runs that share
-// one D matrix (same level and offset; operators.py:225-239 caches D by
-// exactly that key).  Each D is bulk-copied once per tile into a double-
-// buffered smem slot and applied to every pair of its run; a run touches
-// each target at most once, so the pairs of a run accumulate into the tile's
-// smem o buffer without races.
-// ----------------------------------------------------------------------------
-constexpr int kTransTile = 32;
-constexpr int kTransThreads = 256;
-
-struct TransTile {
-  int32_t first_target;
-  int32_t n_targets;
-  int32_t run_begin;
-  int32_t run_end;
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  using type = float4;
 };
-struct TransRun {
-  int32_t dtab;
-  int32_t pair_begin;
-  int32_t pair_end;
-  int32_t pad;
-};
-struct TransPair {
-  int32_t tgt;  // local target index in the tile
-  int32_t src;  // source group id
+template <>
+struct Vec4<double> {
+  using type = double4;
 };
 
 template <typename T>
-struct TransArgs {
-  const TransTile* tiles;
-  const TransRun* runs;
-  const TransPair* pairs;
-  const T* DT;        // transposed D table, stride dstride elements
-  int64_t dstride;
-  const T* s;
-  T* o;
-  int Q;
+__device__ __forceinline__ void ld4(const T* p, T v[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+
+// acc[r][c] += sum_{j in [jb, je)} MT[j*Qp + k0 + r] * X[j*NC + c0 + c]
+template <typename T>
+__device__ __forceinline__ void mm4x4(const T* __restrict__ MT, const T* __restrict__ X,
+                                      const FarGeom& G, int k0, int c0, T acc[4][4], int jb = 0,
+                                      int je = -1) {
+  if (je < 0) je = G.Q;
+#pragma unroll 4
+  for (int j = jb; j < je; ++j) {
+    T m[4], x[4];
+    ld4(MT + j * G.Qp + k0, m);
+    ld4(X + j * G.NC + c0, x);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = fma(m[r], x[c], acc[r][c]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void zero4x4(T acc[4][4]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
+}
+
+// bytes of one padded Q x Qp matrix, rounded to 16 B
+__host__ __device__ inline size_t mat_bytes(int Q, size_t es) {
+  return ((size_t(Q) * ((Q + 3) / 4 * 4) * es) + 15) & ~size_t(15);
+}
+
+// ----------------------------------------------------------------------------
+// Level transfers.  Per level the host precomputes flat index tables so a
+// CTA issues all its gathers at once (no dependent metadata loads):
+//   upward   slot[(p - pf) * 4 + q] = child of local parent p in quadrant q
+//            (-1 if absent);  s[p] = sum_q C_q s[slot]      (operators.py C)
+//   downward order[i] = children sorted by (quadrant, id), opar[i] = their
+//            parents;          o[c] += B_{quad c} o[parent c]
+// The needed quadrant matrices arrive by bulk copy (TMA bulk engine) and the
+// amplitudes by zero-filling cp.async, all on one mbarrier / group, then the
+// 4 x 4 micro-kernel runs without further synchronisation.  QS quadrant
+// slots are staged at a time (4 in float32 at Q <= 64; fewer if the shared
+// memory would not fit).
+// ----------------------------------------------------------------------------
+template <typename T>
+__host__ __device__ inline size_t xblk_bytes(int Q) {
+  const FarGeom G = far_geom(Q);
+  return (size_t(G.Q) * G.NC * sizeof(T) + 127) & ~size_t(127);
+}
+
+// Thread roles for one CTA whose tile has only ncol live columns: row group
+// rg, column group cgi < CGn and reduction slice js < JS of the j loop (small
+// coarse-level tiles split the Q-long dot products over idle threads).
+struct TileMap {
+  int rg, cgi, js, JS, CGn, jb, je;
+  bool live;
 };
 
+__device__ __forceinline__ TileMap tile_map(const FarGeom& G, int ncol, int tid) {
+  TileMap m;
+  m.CGn = (ncol + 3) / 4;
+  m.JS = 1;
+  while (m.JS < 16 && m.CGn * m.JS * 2 <= G.CG && G.Q / (m.JS * 2) >= 4) m.JS *= 2;
+  m.rg = tid % G.RG;
+  const int rest = tid / G.RG;
+  m.js = rest % m.JS;
+  m.cgi = rest / m.JS;
+  m.live = tid < G.RG * G.CG && m.cgi < m.CGn;
+  m.jb = m.js * G.Q / m.JS;
+  m.je = (m.js + 1) * G.Q / m.JS;
+  return m;
+}
+
+// Sum the JS partial tiles into the js == 0 thread (fixed order; deterministic).
+template <typename T>
+__device__ __forceinline__ void tile_reduce(const FarGeom& G, const TileMap& m, T acc[4][4],
+                                            T* red, int tid) {
+  if (m.JS == 1) return;
+  __syncthreads();
+  if (m.live && m.js) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) red[(r * 4 + c) * kFarThreads + tid] = acc[r][c];
+  }
+  __syncthreads();
+  if (m.live && m.js == 0) {
+    for (int js = 1; js < m.JS; ++js) {
+      const int t2 = tid + js * G.RG;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += red[(r * 4 + c) * kFarThreads + t2];
+    }
+  }
+}
+
+template <typename T>
+size_t level_smem_bytes(int Q, int qs) {
+  return size_t(qs) * (mat_bytes(Q, sizeof(T)) + xblk_bytes<T>(Q)) +
+         size_t(16) * kFarThreads * sizeof(T) + 64;
+}
+
+// ----------------------------------------------------------------------------
+// Upward pass, one level: s[p] = sum_q C_q s[slot[p][q]] for local parents
+// pf .. pf+pc-1 (slot = -1: no child in that quadrant).  Matrices by bulk
+// copy, children by zero-filling cp.async, QS quadrants per round.
+// ----------------------------------------------------------------------------
 template <typename T, int R>
-size_t trans_smem_bytes(int Q, int64_t dstride) {
-  size_t oacc = (size_t(kTransTile) * Q * R * sizeof(T) + 127) & ~size_t(127);
-  return oacc + 2 * size_t(dstride) * sizeof(T) + 2 * sizeof(uint64_t) + 16;
+__global__ void __launch_bounds__(kFarThreads) upward_kernel(
+    const T* __restrict__ CT, const int32_t* __restrict__ slot, int64_t pf, int64_t pc, T* s,
+    int Q, int QS) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const FarGeom G = far_geom(Q);
+  const int TP = G.NC / R;
+  const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
+  unsigned char* Mbase = smem;
+  unsigned char* Xbase = smem + QS * mb;
+  T* red = reinterpret_cast<T*>(Xbase + QS * xb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 16 * kFarThreads);
+  const int64_t t0 = int64_t(blockIdx.x) * TP;
+  const int np = int(pc - t0 < TP ? pc - t0 : TP);
+  const int tid = threadIdx.x;
+  const TileMap tm = tile_map(G, np * R, tid);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  T acc[4][4];
+  zero4x4(acc);
+  for (int q0 = 0; q0 < 4; q0 += QS) {
+    if (q0) __syncthreads();  // previous slots consumed
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar, uint32_t(QS * mb));
+      bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(CT) + q0 * mb, uint32_t(QS * mb), bar);
+    }
+    // X_q[j][pp*R + rr] = s[child][j][rr]  (zeros for absent children)
+    for (int i = tid; i < QS * G.Q * np; i += kFarThreads) {
+      const int pp = i % np, j = (i / np) % G.Q, qq = i / (np * G.Q);
+      const int c = slot[(t0 + pp) * 4 + q0 + qq];
+      T* dst = reinterpret_cast<T*>(Xbase + qq * xb) + j * G.NC + pp * R;
+      cp_async_zfill_n<R * sizeof(T)>(dst, s + (int64_t(c < 0 ? 0 : c) * G.Q + j) * R, c >= 0);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    mbar_wait(bar, uint32_t(q0 / QS) & 1u);
+    __syncthreads();
+    if (tm.live)
+      for (int qq = 0; qq < QS; ++qq)
+        mm4x4(reinterpret_cast<const T*>(Mbase + qq * mb),
+              reinterpret_cast<const T*>(Xbase + qq * xb), G, 4 * tm.rg, 4 * tm.cgi, acc, tm.jb,
+              tm.je);
+  }
+  tile_reduce(G, tm, acc, red, tid);
+  if (tm.live && tm.js == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int col = 4 * tm.cgi + c, pp = col / R, rr = col % R;
+      if (pp >= np) continue;
+      T* dst = s + (pf + t0 + pp) * int64_t(Q) * R + rr;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (4 * tm.rg + r < Q) dst[(4 * tm.rg + r) * R] = acc[r][c];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Downward pass fused with the translation reduce, one level:
+//   o[c] = sum_{e in interaction entries of c} Y[e]  +  B_{quad c} o[parent c]
+// (reference order: translation sums over c's interaction list, then the
+// potential transfer adds; fastmvp.py:163-169).  Children are visited in
+// `order` (sorted by quadrant, then id); `opar` are their parents.  With
+// has_parent = 0 (level l0) only the reduce runs.
+// ----------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(kFarThreads) downward_kernel(
+    const T* __restrict__ BT, const int32_t* __restrict__ quad, const int32_t* __restrict__ order,
+    const int32_t* __restrict__ opar, const int64_t* __restrict__ int_ptr,
+    const T* __restrict__ Y, int64_t cc, T* o, int Q, int QS, int has_parent) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const FarGeom G = far_geom(Q);
+  const int TC = G.NC / R, QR = Q * R;
+  const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
+  unsigned char* Xp = smem;            // parent amplitudes, column layout
+  unsigned char* Ys = smem + xb;       // translation sums, column layout
+  unsigned char* Mbase = smem + 2 * xb;
+  T* red = reinterpret_cast<T*>(Mbase + QS * mb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 16 * kFarThreads);
+  const int64_t t0 = int64_t(blockIdx.x) * TC;
+  const int nc = int(cc - t0 < TC ? cc - t0 : TC);
+  const int tid = threadIdx.x;
+  const TileMap tm = tile_map(G, nc * R, tid);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (has_parent) {
+    for (int i = tid; i < G.Q * nc; i += kFarThreads) {
+      const int cc_ = i % nc, j = i / nc;
+      cp_async_n<R * sizeof(T)>(reinterpret_cast<T*>(Xp) + j * G.NC + cc_ * R,
+                                o + (int64_t(opar[t0 + cc_]) * G.Q + j) * R);
+    }
+    cp_async_commit();
+  }
+  // Ys[j][cc*R + rr] = sum_e Y[e][j][rr] in entry order
+  for (int i = tid; i < nc * QR; i += kFarThreads) {
+    const int cc_ = i / QR, w = i % QR;
+    const int64_t c = order[t0 + cc_];
+    T v = T(0);
+    for (int64_t e = int_ptr[c]; e < int_ptr[c + 1]; ++e) v += Y[e * QR + w];
+    reinterpret_cast<T*>(Ys)[(w / R) * G.NC + cc_ * R + (w % R)] = v;
+  }
+  int colq[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int cc_ = (4 * tm.cgi + c) / R;
+    colq[c] = (tm.live && cc_ < nc) ? quad[order[t0 + cc_]] : -1;
+  }
+  T acc[4][4];
+  zero4x4(acc);
+  if (has_parent) {
+    const int q_lo = quad[order[t0]], q_hi = quad[order[t0 + nc - 1]];
+    int round = 0;
+    for (int q0 = q_lo; q0 <= q_hi; q0 += QS, ++round) {
+      const int nq = min(QS, q_hi - q0 + 1);
+      if (round) __syncthreads();
+      if (tid == 0) {
+        mbar_arrive_expect_tx(bar, uint32_t(nq * mb));
+        bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(BT) + q0 * mb, uint32_t(nq * mb),
+                 bar);
+      }
+      cp_async_wait_all();
+      mbar_wait(bar, uint32_t(round) & 1u);
+      __syncthreads();
+      if (tm.live) {
+        for (int qq = 0; qq < nq; ++qq) {
+          T part[4][4];
+          zero4x4(part);
+          mm4x4(reinterpret_cast<const T*>(Mbase + qq * mb), reinterpret_cast<const T*>(Xp), G,
+                4 * tm.rg, 4 * tm.cgi, part, tm.jb, tm.je);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (colq[c] == q0 + qq)
+#pragma unroll
+              for (int r = 0; r < 4; ++r) acc[r][c] += part[r][c];
+        }
+      }
+    }
+    tile_reduce(G, tm, acc, red, tid);
+  }
+  __syncthreads();  // Ys complete
+  if (tm.live && tm.js == 0) {
+    const T* ys = reinterpret_cast<const T*>(Ys);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (colq[c] < 0) continue;
+      const int col = 4 * tm.cgi + c;
+      T* dst = o + int64_t(order[t0 + col / R]) * QR + (col % R);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int k = 4 * tm.rg + r;
+        if (k < Q) dst[k * R] = ys[k * G.NC + col] + acc[r][c];
+      }
+    }
+  }
+}
+
+template <typename T>
+size_t down_smem_bytes(int Q, int qs) {
+  return 2 * xblk_bytes<T>(Q) + size_t(qs) * mat_bytes(Q, sizeof(T)) +
+         size_t(16) * kFarThreads * sizeof(T) + 64;
+}
+
+// ----------------------------------------------------------------------------
+// Translation as a pair-major GEMM: Y[e] = D_{dtab} s[src(e)] for every
+// interaction entry e.  Entries are grouped by unique D (operators.py:225-239
+// caches D per (level, offset)); a unit = one D and up to kTUnitPasses x
+// NC/R entries.  D arrives by bulk copy, sources by cp.async (double-
+// buffered across passes); results go straight to Y (the per-target sums
+// happen in the fused downward kernel, in reference order).
+// ----------------------------------------------------------------------------
+constexpr int kTUnitPasses = 4;
+
+struct TUnit {
+  int32_t dtab;
+  int32_t ent_begin;  // into the dtab-sorted entry list
+  int32_t ent_end;
+  int32_t pad;
+};
+struct TEnt {
+  int32_t src;  // source group
+  int32_t e;    // interaction entry (Y row)
+};
+
+template <typename T>
+size_t tgemm_smem_bytes(int Q) {
+  return mat_bytes(Q, sizeof(T)) + 2 * xblk_bytes<T>(Q) + 64;
 }
 
 template <typename T, int R>
-__global__ void __launch_bounds__(kTransThreads) translate_kernel(const TransArgs<T> a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int Q = a.Q;
-  const TransTile tile = a.tiles[blockIdx.x];
-  T* oacc = reinterpret_cast<T*>(smem);
-  const size_t oacc_bytes = (size_t(kTransTile) * Q * R * sizeof(T) + 127) & ~size_t(127);
-  T* Ds0 = reinterpret_cast<T*>(smem + oacc_bytes);
-  T* Ds1 = Ds0 + a.dstride;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Ds1 + a.dstride);
-  const uint32_t dbytes = uint32_t(a.dstride * sizeof(T));
-
-  const int n_out = tile.n_targets * Q * R;
-  for (int i = threadIdx.x; i < n_out; i += kTransThreads) oacc[i] = T(0);
-  const int nruns = tile.run_end - tile.run_begin;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-    if (nruns > 0) {
-      mbar_arrive_expect_tx(&bar[0], dbytes);
-      bulk_g2s(Ds0, a.DT + int64_t(a.runs[tile.run_begin].dtab) * a.dstride, dbytes, &bar[0]);
-    }
+__device__ __forceinline__ void tgemm_stage(const TEnt* ents, int eb, int n, const T* s,
+                                            const FarGeom& G, T* X, int tid) {
+  for (int i = tid; i < n * G.Q; i += kFarThreads) {
+    const int p = i % n, j = i / n;
+    cp_async_n<R * sizeof(T)>(X + j * G.NC + p * R, s + (int64_t(ents[eb + p].src) * G.Q + j) * R);
   }
-  __syncthreads();
-  const int NG = kTransThreads / Q;
-  const int g = threadIdx.x / Q, k = threadIdx.x % Q;
-  for (int r = 0; r < nruns; ++r) {
-    const int buf = r & 1;
-    if (threadIdx.x == 0 && r + 1 < nruns) {
-      mbar_arrive_expect_tx(&bar[buf ^ 1], dbytes);
-      bulk_g2s(buf ? Ds0 : Ds1,
-               a.DT + int64_t(a.runs[tile.run_begin + r + 1].dtab) * a.dstride, dbytes,
-               &bar[buf ^ 1]);
-    }
-    mbar_wait(&bar[buf], uint32_t(r >> 1) & 1u);
-    const TransRun run = a.runs[tile.run_begin + r];
-    const T* Dm = buf ? Ds1 : Ds0;
-    if (g < NG) {
-      for (int p = run.pair_begin + g; p < run.pair_end; p += NG) {
-        const TransPair pr = a.pairs[p];
-        const T* sv = a.s + int64_t(pr.src) * Q * R;
-        T acc[R];
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) acc[rr] = T(0);
-#pragma unroll 4
-        for (int j = 0; j < Q; ++j) {
-          const T d = Dm[j * Q + k];
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) acc[rr] = fma(d, __ldg(sv + j * R + rr), acc[rr]);
-        }
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) oacc[(pr.tgt * Q + k) * R + rr] += acc[rr];
-      }
+  cp_async_commit();
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kFarThreads) tgemm_kernel(const TUnit* __restrict__ units,
+                                                            const TEnt* __restrict__ ents,
+                                                            const T* __restrict__ DT,
+                                                            const T* __restrict__ s, T* Y, int Q) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const FarGeom G = far_geom(Q);
+  const int QR = Q * R, per = G.NC / R;
+  const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
+  T* Dm = reinterpret_cast<T*>(smem);
+  T* X0 = reinterpret_cast<T*>(smem + mb);
+  T* X1 = reinterpret_cast<T*>(smem + mb + xb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + 2 * xb);
+  const TUnit u = units[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int rg = tid % G.RG, cg = tid / G.RG;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, uint32_t(mb));
+    bulk_g2s(Dm, reinterpret_cast<const unsigned char*>(DT) + size_t(u.dtab) * mb, uint32_t(mb),
+             bar);
+  }
+  const int n_all = u.ent_end - u.ent_begin;
+  const int npass = (n_all + per - 1) / per;
+  tgemm_stage<T, R>(ents, u.ent_begin, min(per, n_all), s, G, X0, tid);
+  __syncthreads();  // barrier init visible before anyone waits
+  mbar_wait(bar, 0);
+  for (int ps = 0; ps < npass; ++ps) {
+    T* X = (ps & 1) ? X1 : X0;
+    const int eb = u.ent_begin + ps * per;
+    const int n = min(per, u.ent_end - eb);
+    if (ps + 1 < npass) {
+      const int eb2 = eb + per;
+      tgemm_stage<T, R>(ents, eb2, min(per, u.ent_end - eb2), s, G, (ps & 1) ? X0 : X1, tid);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      cp_async_wait_all();
     }
     __syncthreads();
+    if (cg < G.CG && 4 * cg < n * R) {
+      T acc[4][4];
+      zero4x4(acc);
+      mm4x4(Dm, X, G, 4 * rg, 4 * cg, acc);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int col = 4 * cg + c, p = col / R, rr = col % R;
+        if (p >= n) continue;
+        T* dst = Y + int64_t(ents[eb + p].e) * QR + rr;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (4 * rg + r < Q) dst[(4 * rg + r) * R] = acc[r][c];
+      }
+    }
+    __syncthreads();  // X buffer reuse
   }
-  T* dst = a.o + int64_t(tile.first_target) * Q * R;
-  for (int i = threadIdx.x; i < n_out; i += kTransThreads) dst[i] = oacc[i];
 }
 
 }  // namespace nesa

@@ -54,6 +54,10 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
   ~DevBuf() {
     if (p) cudaFree(p);
   }
@@ -76,7 +80,7 @@ struct DevBuf {
 struct HostBlockSet {
   std::vector<BlockItem> items;
   std::vector<BlockSeg> segs;
-  std::vector<BlockChunk> chunks;
+  std::vector<ChunkRec> recs;
   std::vector<int32_t> cta_ptr;
   int64_t blob_elems = 0;
   int64_t entries = 0;
@@ -86,7 +90,7 @@ struct DevBlockSet {
   DevBuf<unsigned char> blob;  // T elements
   DevBuf<BlockItem> items;
   DevBuf<BlockSeg> segs;
-  DevBuf<BlockChunk> chunks;
+  DevBuf<ChunkRec> recs;
   DevBuf<int32_t> cta_ptr;
   int grid = 0;
   int64_t n_items = 0;
@@ -97,19 +101,46 @@ struct DevBlockSet {
 // byte-balanced range of whole items (a target row is never split across
 // CTAs, so it has exactly one writer).
 void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
-  hs.chunks.clear();
+  hs.recs.clear();
   std::vector<int64_t> item_first_chunk(hs.items.size() + 1);
   std::vector<double> item_bytes(hs.items.size());
   for (size_t i = 0; i < hs.items.size(); ++i) {
     const BlockItem& it = hs.items[i];
-    item_first_chunk[i] = int64_t(hs.chunks.size());
+    item_first_chunk[i] = int64_t(hs.recs.size());
     int per = int(std::min<int64_t>(kMaxC, kABytes / (int64_t(it.m) * int64_t(elem_bytes))));
     per = std::max(per, 1);
-    for (int c = 0; c < it.n; c += per)
-      hs.chunks.push_back(BlockChunk{int32_t(i), c, std::min(per, it.n - c), 0});
+    const int seg_end = it.seg_begin + it.seg_count;
+    int c = 0;
+    while (c < it.n) {
+      ChunkRec r{};
+      r.src_off = it.a_off + int64_t(c) * it.m;
+      r.m = it.m;
+      r.y_row0 = it.y_row0;
+      int ce = std::min(it.n, c + per);
+      // segments overlapping [c, ce); cut the chunk if more than kRecSegs
+      int ns = 0;
+      for (int sg = it.seg_begin; sg < seg_end; ++sg) {
+        const int s0 = hs.segs[sg].col0;
+        const int s1 = sg + 1 < seg_end ? hs.segs[sg + 1].col0 : it.n;
+        const int lo = std::max(s0, c), hi = std::min(s1, ce);
+        if (lo >= hi) continue;
+        if (ns == kRecSegs) {
+          ce = lo;
+          break;
+        }
+        r.seg[2 * ns] = hs.segs[sg].x_row0 + (lo - s0);
+        r.seg[2 * ns + 1] = lo - c;
+        ++ns;
+      }
+      r.nseg = ns;
+      r.ncols = ce - c;
+      r.flags = (c == 0 ? 1 : 0) | (ce == it.n ? 2 : 0);
+      hs.recs.push_back(r);
+      c = ce;
+    }
     item_bytes[i] = double(it.m) * it.n * elem_bytes + 256.0;  // + per-item overhead
   }
-  item_first_chunk[hs.items.size()] = int64_t(hs.chunks.size());
+  item_first_chunk[hs.items.size()] = int64_t(hs.recs.size());
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_grid, int64_t(hs.items.size()))));
   double total = 0;
   for (double b : item_bytes) total += b;
@@ -119,19 +150,17 @@ void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
   for (int c = 0; c < grid; ++c) {
     hs.cta_ptr[c] = int32_t(item_first_chunk[it]);
     const double target = total * double(c + 1) / grid;
-    // take items while the running sum stays closer to the target
-    while (it < hs.items.size()) {
+    while (it < hs.items.size() && c < grid - 1) {
       const double nb = acc + item_bytes[it];
-      if (c < grid - 1 && nb > target && (nb - target) > (target - acc) && acc > 0 &&
-          hs.cta_ptr[c] != int32_t(item_first_chunk[it]))
+      // stop before an item that overshoots the target by more than it undershoots
+      if (nb > target && (nb - target) > (target - acc) && int64_t(hs.cta_ptr[c]) != item_first_chunk[it])
         break;
       acc = nb;
       ++it;
-      if (acc >= target && c < grid - 1) break;
+      if (acc >= target) break;
     }
   }
-  hs.cta_ptr[grid] = int32_t(hs.chunks.size());
-  // any items left (rounding) go to the last CTA implicitly via cta_ptr[grid]
+  hs.cta_ptr[grid] = int32_t(hs.recs.size());
 }
 
 template <typename T>
@@ -139,7 +168,7 @@ void upload_blockset(DevBlockSet& d, const HostBlockSet& h) {
   d.blob.alloc(size_t(h.blob_elems) * sizeof(T), 256);
   d.items.upload(h.items);
   d.segs.upload(h.segs);
-  d.chunks.upload(h.chunks);
+  d.recs.upload(h.recs);
   d.cta_ptr.upload(h.cta_ptr);
   d.grid = int(h.cta_ptr.size()) - 1;
   d.n_items = int64_t(h.items.size());
@@ -253,18 +282,25 @@ struct nesa_plan {
   DevBuf<int64_t> child_first; // [G]
   DevBuf<int32_t> n_child;     // [G]
   DevBuf<unsigned char> CT, BT, DT;  // T tables (transposed)
-  int64_t dstride = 0, n_dtab = 0, d_refs = 0;
+  int64_t n_dtab = 0, d_refs = 0;
 
   DevBlockSet nearset, Vset, Uset;
 
-  DevBuf<TransTile> ttiles;
-  DevBuf<TransRun> truns;
-  DevBuf<TransPair> tpairs;
-  int n_ttiles = 0;
+  // translation: entries grouped by unique D (see tgemm_kernel)
+  DevBuf<TUnit> tunits;
+  DevBuf<TEnt> tents;
+  int n_tunits = 0;
+  DevBuf<int64_t> int_ptr;  // [G+1] interaction CSR (Y rows of each target)
+  int64_t nnz = 0;
+  size_t mbytes = 0;                       // padded matrix stride (bytes)
+  std::vector<DevBuf<int32_t>> up_slot;     // per child level (lv-l0): parent x quadrant -> child
+  std::vector<DevBuf<int32_t>> down_order;  // per level (index lv-l0): children by quadrant
+  std::vector<DevBuf<int32_t>> down_par;    // parents of down_order
+  int qs = 4;                               // quadrant slots staged per round
 
   // workspace for R real columns
   int ws_R = 0;
-  DevBuf<unsigned char> qt, phin, s, o;
+  DevBuf<unsigned char> qt, phin, s, o, Y;
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -280,6 +316,7 @@ struct nesa_plan {
     }
   };
   struct GraphEntry {
+    cudaGraph_t graph = nullptr;  // kept alive: its nodes address the exec's nodes
     cudaGraphExec_t exec = nullptr;
     std::vector<std::pair<cudaGraphNode_t, int>> ev_nodes;  // node, slot (stage*2+end)
   };
@@ -293,8 +330,10 @@ struct nesa_plan {
 
   ~nesa_plan() {
     cudaSetDevice(device);
-    for (auto& kv : graphs)
+    for (auto& kv : graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
     for (auto& v : prof_events)
       for (auto e : v) cudaEventDestroy(e);
     for (auto e : cap_events)
@@ -308,19 +347,16 @@ struct nesa_plan {
 
 namespace {
 
+// Q x Q float64 row-major matrices -> padded transposed device layout
+// MT[j * Qp + k] = M[k][j], matrix stride mat_bytes(Q) (see nesa_kernels.cuh).
 template <typename T>
-void upload_table_T(DevBuf<unsigned char>& dst, const double* src, int64_t n_mats, int Q,
-                    int64_t stride, bool transpose) {
-  std::vector<T> h(size_t(std::max<int64_t>(n_mats, 1) * stride), T(0));
+void upload_table_T(DevBuf<unsigned char>& dst, const double* src, int64_t n_mats, int Q) {
+  const int Qp = (Q + 3) / 4 * 4;
+  const size_t stride = mat_bytes(Q, sizeof(T)) / sizeof(T);
+  std::vector<T> h(size_t(std::max<int64_t>(n_mats, 1)) * stride, T(0));
   for (int64_t m = 0; m < n_mats; ++m)
     for (int k = 0; k < Q; ++k)
-      for (int j = 0; j < Q; ++j) {
-        const double v = src[(m * Q + k) * Q + j];
-        if (transpose)
-          h[m * stride + int64_t(j) * Q + k] = T(v);
-        else
-          h[m * stride + int64_t(k) * Q + j] = T(v);
-      }
+      for (int j = 0; j < Q; ++j) h[m * stride + size_t(j) * Qp + k] = T(src[(m * Q + k) * Q + j]);
   dst.alloc(h.size() * sizeof(T));
   CUDA_OK(cudaMemcpy(dst.p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
 }
@@ -394,16 +430,53 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
 
   // ---- tables
-  const int64_t QQ = int64_t(Q) * Q;
-  const int64_t per16 = 16 / int64_t(es);
-  P->dstride = (QQ + per16 - 1) / per16 * per16;
   const int64_t nlt = P->L - P->l0;
+  P->mbytes = mat_bytes(Q, sizeof(T));
   if (nlt > 0) {
-    upload_table_T<T>(P->CT, d->C, nlt * 4, Q, QQ, true);
-    upload_table_T<T>(P->BT, d->B, nlt * 4, Q, QQ, true);
+    upload_table_T<T>(P->CT, d->C, nlt * 4, Q);
+    upload_table_T<T>(P->BT, d->B, nlt * 4, Q);
   }
   P->n_dtab = d->n_dtab;
-  upload_table_T<T>(P->DT, d->D, d->n_dtab, Q, P->dstride, true);
+  upload_table_T<T>(P->DT, d->D, d->n_dtab, Q);
+  // quadrant slots per round: keep the level kernels <= ~96 KB so they can
+  // co-reside with the persistent near-field CTAs (~110 KB) on one SM
+  P->qs = 2;
+  while (P->qs > 1 && (level_smem_bytes<T>(Q, P->qs) > 96 * 1024 ||
+                       down_smem_bytes<T>(Q, P->qs) > 96 * 1024))
+    P->qs /= 2;
+  require(level_smem_bytes<T>(Q, 1) <= 200 * 1024 && down_smem_bytes<T>(Q, 1) <= 200 * 1024 &&
+              tgemm_smem_bytes<T>(Q) <= 200 * 1024,
+          "Q too large for the far-field kernels");
+  // per-level gather tables (see nesa_kernels.cuh "Level transfers")
+  P->up_slot.resize(nlev);
+  P->down_order.resize(nlev);
+  P->down_par.resize(nlev);
+  for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
+    const int li = lv - P->l0;
+    const int64_t cf = P->loc_first[li], cn = P->loc_count[li];
+    const int64_t pf = P->loc_first[li - 1], pn = P->loc_count[li - 1];
+    std::vector<int32_t> slot(size_t(pn) * 4, -1);
+    for (int64_t c = cf; c < cf + cn; ++c) {
+      const int64_t pl = d->parent[c] - pf;
+      require(pl >= 0 && pl < pn, "local child with a non-local parent");
+      require(slot[pl * 4 + d->quad[c]] < 0, "two children in one quadrant");
+      slot[pl * 4 + d->quad[c]] = int32_t(c);
+    }
+    P->up_slot[li].upload(slot);
+    std::vector<int32_t> ord(static_cast<size_t>(cn)), par(static_cast<size_t>(cn));
+    for (int64_t i = 0; i < cn; ++i) ord[i] = int32_t(cf + i);
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int32_t x, int32_t y) { return d->quad[x] < d->quad[y]; });
+    for (int64_t i = 0; i < cn; ++i) par[i] = int32_t(d->parent[ord[i]]);
+    P->down_order[li].upload(ord);
+    P->down_par[li].upload(par);
+  }
+  {  // level l0: reduce-only pass over its local groups
+    std::vector<int32_t> ord(static_cast<size_t>(P->loc_count[0])), par(ord.size(), 0);
+    for (size_t i = 0; i < ord.size(); ++i) ord[i] = int32_t(P->loc_first[0] + int64_t(i));
+    P->down_order[0].upload(ord);
+    P->down_par[0].upload(par);
+  }
 
   // ---- near / V / U block sets (local leaves)
   HostBlockSet hn, hv, hu;
@@ -544,53 +617,37 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
   CUDA_OK(cudaDeviceSynchronize());
 
-  // ---- translation tiles over the local targets of every level
+  // ---- translation entries of the local targets, grouped by unique D
   {
-    std::vector<TransTile> tiles;
-    std::vector<TransRun> runs;
-    std::vector<TransPair> pairs;
-    struct E {
-      int32_t dtab, tgt, src;
-    };
-    std::vector<E> buf;
+    P->nnz = d->int_ptr[G];
+    P->int_ptr.upload(std::vector<int64_t>(d->int_ptr, d->int_ptr + G + 1));
+    std::vector<std::vector<TEnt>> by_d(size_t(std::max<int64_t>(d->n_dtab, 1)));
     for (int lv = P->l0; lv <= P->L; ++lv) {
       const int li = lv - P->l0;
-      const int64_t tf = P->loc_first[li], tc = P->loc_count[li];
-      for (int64_t t0 = 0; t0 < tc; t0 += kTransTile) {
-        const int32_t nt = int32_t(std::min<int64_t>(kTransTile, tc - t0));
-        buf.clear();
-        for (int32_t t = 0; t < nt; ++t) {
-          const int64_t g = tf + t0 + t;
-          for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
-            const int64_t dt = d->int_dtab[e];
-            require(dt >= 0 && dt < d->n_dtab, "D index out of range");
-            buf.push_back(E{int32_t(dt), t, int32_t(d->int_idx[e])});
-          }
+      for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
+        for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
+          const int64_t dt = d->int_dtab[e];
+          require(dt >= 0 && dt < d->n_dtab, "D index out of range");
+          require(d->int_idx[e] >= 0 && d->int_idx[e] < G, "interaction id out of range");
+          by_d[dt].push_back(TEnt{int32_t(d->int_idx[e]), int32_t(e)});
         }
-        std::stable_sort(buf.begin(), buf.end(), [](const E& x, const E& y) {
-          return x.dtab != y.dtab ? x.dtab < y.dtab : x.tgt < y.tgt;
-        });
-        TransTile tl{int32_t(tf + t0), nt, int32_t(runs.size()), 0};
-        for (size_t i = 0; i < buf.size();) {
-          size_t j = i;
-          while (j < buf.size() && buf[j].dtab == buf[i].dtab) ++j;
-          runs.push_back(TransRun{buf[i].dtab, int32_t(pairs.size()),
-                                  int32_t(pairs.size() + (j - i)), 0});
-          for (size_t k = i; k < j; ++k) {
-            require(k == i || buf[k].tgt != buf[k - 1].tgt, "duplicate offset for one target");
-            pairs.push_back(TransPair{buf[k].tgt, buf[k].src});
-          }
-          i = j;
-        }
-        tl.run_end = int32_t(runs.size());
-        tiles.push_back(tl);
-        P->d_refs += int64_t(buf.size());
-      }
     }
-    P->ttiles.upload(tiles);
-    P->truns.upload(runs);
-    P->tpairs.upload(pairs);
-    P->n_ttiles = int(tiles.size());
+    require(P->nnz < (int64_t(1) << 31), "too many interaction entries");
+    const int per = kTUnitPasses * (far_geom(Q).NC / 4);  // sized for R = 4; smaller R packs more
+    std::vector<TEnt> ents;
+    std::vector<TUnit> units;
+    for (int64_t dt = 0; dt < d->n_dtab; ++dt) {
+      const auto& v = by_d[dt];
+      for (size_t i = 0; i < v.size(); i += size_t(per)) {
+        const size_t j = std::min(v.size(), i + size_t(per));
+        units.push_back(TUnit{int32_t(dt), int32_t(ents.size()), int32_t(ents.size() + (j - i)), 0});
+        ents.insert(ents.end(), v.begin() + i, v.begin() + j);
+      }
+      P->d_refs += int64_t(v.size());
+    }
+    P->tunits.upload(units);
+    P->tents.upload(ents);
+    P->n_tunits = int(units.size());
   }
 }
 
@@ -602,6 +659,7 @@ void ensure_workspace(nesa_plan* P, int R) {
   P->phin.alloc(size_t(P->N) * R * es);
   P->s.alloc(size_t(P->G) * P->Q * R * es);
   P->o.alloc(size_t(P->G) * P->Q * R * es);
+  P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
   P->ws_R = R;
 }
 
@@ -613,9 +671,10 @@ template <typename T, int R, int MODE>
 void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
                       int64_t perm_offset, cudaStream_t st) {
   if (bs.n_items == 0) return;
-  BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.items.p, bs.segs.p, bs.chunks.p,
-                     bs.cta_ptr.p, x, y, base, perm, perm_offset};
-  constexpr size_t sm = blockgemv_smem_bytes<T, R>();
+  BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p, x, y, base,
+                     perm};
+  (void)perm_offset;
+  constexpr size_t sm = blockgemv_smem_bytes<T, R, MODE>();
   blockgemv_kernel<T, R, MODE><<<bs.grid, kBGThreads, sm, st>>>(a);
 }
 
@@ -623,13 +682,16 @@ template <typename T, int R>
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  constexpr size_t sm = blockgemv_smem_bytes<T, R>();
   CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeStore>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(blockgemv_smem_bytes<T, R, kModeStore>())));
   CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeScatter>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-  CUDA_OK(cudaFuncSetAttribute(translate_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               200 * 1024));
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(blockgemv_smem_bytes<T, R, kModeScatter>())));
+  const int lim = 220 * 1024;
+  CUDA_OK(cudaFuncSetAttribute(tgemm_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(upward_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(downward_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   done = true;
 }
 
@@ -656,37 +718,41 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   const T* CT = reinterpret_cast<const T*>(P->CT.p);
   const T* BT = reinterpret_cast<const T*>(P->BT.p);
   const int Q = P->Q;
-  const int64_t QQ = int64_t(Q) * Q;
   const int cap = P->n_sm * 8;
-  const int NG = kLvlThreads / Q;
   const int64_t nloc = P->pt_end - P->pt_begin;
   int nk = 0;
 
+  const size_t mstride = P->mbytes / sizeof(T);
+  const FarGeom FG = far_geom(Q);
+  const size_t lvl_sm = level_smem_bytes<T>(Q, P->qs);
   auto up_pass = [&]() {
+    const int TP = FG.NC / R;
     for (int lv = P->L; lv > P->l0; --lv) {
       const int ci = lv - P->l0, pi = ci - 1;
       const int64_t pc = P->loc_count[pi];
       if (pc == 0) continue;
-      upward_kernel<T, R><<<grid_for(pc, NG, cap), kLvlThreads, 0, s0>>>(
-          CT + int64_t(ci - 1) * 4 * QQ, P->quad.p, P->child_first.p, P->n_child.p,
-          P->loc_first[pi], pc, P->loc_first[ci], P->loc_first[ci] + P->loc_count[ci], s, Q);
+      upward_kernel<T, R><<<int((pc + TP - 1) / TP), kFarThreads, lvl_sm, s0>>>(
+          CT + size_t(ci - 1) * 4 * mstride, P->up_slot[ci].p, P->loc_first[pi], pc, s, Q, P->qs);
       nk++;
     }
   };
   auto down_pass = [&]() {
-    if (P->n_ttiles > 0) {
-      TransArgs<T> ta{P->ttiles.p, P->truns.p, P->tpairs.p, reinterpret_cast<const T*>(P->DT.p),
-                      P->dstride, s, o, Q};
-      translate_kernel<T, R>
-          <<<P->n_ttiles, kTransThreads, trans_smem_bytes<T, R>(Q, P->dstride), s0>>>(ta);
+    T* Y = reinterpret_cast<T*>(P->Y.p);
+    if (P->n_tunits > 0) {
+      tgemm_kernel<T, R><<<P->n_tunits, kFarThreads, tgemm_smem_bytes<T>(Q), s0>>>(
+          P->tunits.p, P->tents.p, reinterpret_cast<const T*>(P->DT.p), s, Y, Q);
       nk++;
     }
-    for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
+    const int TC = FG.NC / R;
+    const size_t dsm = down_smem_bytes<T>(Q, P->qs);
+    for (int lv = P->l0; lv <= P->L; ++lv) {
       const int ci = lv - P->l0;
       const int64_t cc = P->loc_count[ci];
       if (cc == 0) continue;
-      downward_kernel<T, R><<<grid_for(cc, NG, cap), kLvlThreads, 0, s0>>>(
-          BT + int64_t(ci - 1) * 4 * QQ, P->quad.p, P->parent.p, P->loc_first[ci], cc, o, Q);
+      const T* Bl = ci > 0 ? BT + size_t(ci - 1) * 4 * mstride : BT;
+      downward_kernel<T, R><<<int((cc + TC - 1) / TC), kFarThreads, dsm, s0>>>(
+          Bl, P->quad.p, P->down_order[ci].p, P->down_par[ci].p, P->int_ptr.p, Y, cc, o, Q, P->qs,
+          ci > 0 ? 1 : 0);
       nk++;
     }
   };
@@ -816,7 +882,7 @@ int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_
           if (P->cap_events[slot] == ev) ent.ev_nodes.emplace_back(nd, slot);
       }
     }
-    CUDA_OK(cudaGraphDestroy(g));
+    ent.graph = g;
     if (stage == 0) P->kernels_per_matvec = nk;
     itg = P->graphs.emplace(key, ent).first;
   }

@@ -86,6 +86,40 @@ __device__ __forceinline__ void cp_async_n(void* dst, const void* src) {
   }
 }
 
+// cp.async of BYTES (4, 8, 16) that writes zeros instead when !valid.
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(void* dst, const void* src, bool valid) {
+  const int n = valid ? BYTES : 0;
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(n)
+                 : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(dst)), "l"(src),
+                 "n"(BYTES), "r"(n)
+                 : "memory");
+  }
+}
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill_n(void* dst, const void* src, bool valid) {
+  if constexpr (BYTES <= 16) {
+    cp_async_zfill<BYTES>(dst, src, valid);
+  } else {
+#pragma unroll
+    for (int i = 0; i < BYTES / 16; ++i)
+      cp_async_zfill<16>(static_cast<char*>(dst) + 16 * i, static_cast<const char*>(src) + 16 * i,
+                         valid);
+  }
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Arrive on `bar` once all prior cp.async of this thread have landed.  The
 // barrier's expected count must include this arrival (.noinc).
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {

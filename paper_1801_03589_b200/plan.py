@@ -83,6 +83,27 @@ def _blobs_from_opset(tree: Tree, ops: OperatorSet):
     return np.concatenate(near), np.concatenate(V), np.concatenate(U)
 
 
+def _radiation_blob(tree: Tree, tables: OperatorTables, leaf_range=None) -> np.ndarray:
+    """Per-leaf V in the C ABI layout (Q x n column-major, leaves concatenated).
+
+    Leaves outside ``leaf_range`` are left zero (the sub-plan never reads them).
+    """
+    from .operators import aux_at, build_radiation
+    a = tree.arrays
+    params = tables.params
+    L = tree.L
+    nl = a.level_count[L]
+    lb, le = (0, nl) if leaf_range is None else leaf_range
+    out = np.zeros(tree.n_points * params.Q)
+    fit = tables.out_fit[L]
+    for g in range(lb, le):
+        s0, s1 = int(a.start[g]), int(a.stop[g])
+        aux = aux_at(tuple(tables.leaf_center[g]), float(tables.leaf_h[g]), params)
+        V = build_radiation(aux, tree.points[s0:s1], params, fit=fit)
+        out[s0 * params.Q:s1 * params.Q] = V.ravel(order="F")
+    return out
+
+
 class NesaPlan:
     """Device plan of one (tree, operators, precision) triple.
 
@@ -96,10 +117,17 @@ class NesaPlan:
     dtype : "f64" (float64 / complex128 vectors) or "f32" (float32 / complex64).
     device : CUDA device ordinal.
     leaf_range : (begin, end) leaf ids of this rank's targets (multi-GPU).
+    v_on_host : assemble the radiation blocks V = fit @ K(check, pts) on the
+        host, per leaf, exactly as operators.py:107-112 does (default for
+        float64 plans).  V goes through the ill-conditioned pinv fit, which
+        amplifies 1-ulp differences between the device and numpy ``log`` to
+        ~1e-12 at Q >= 32; the host route keeps float64 parity at ~1e-14.
+        Near and U blocks are direct kernel entries and always assemble on
+        the device.
     """
 
     def __init__(self, tree: Tree, ops, dtype: str = "f64", device: int = 0,
-                 leaf_range: tuple[int, int] | None = None):
+                 leaf_range: tuple[int, int] | None = None, v_on_host: bool | None = None):
         self.lib = _capi.load()
         if dtype not in _DTYPES:
             raise ValueError(f"unknown dtype {dtype!r}")
@@ -160,6 +188,11 @@ class NesaPlan:
             d.U_blob = _ptr(arr("Ub", U_b, np.float64), f64)
         else:
             nl = a.level_count[L]
+            if v_on_host is None:
+                v_on_host = self.dtype == "f64"
+            if v_on_host:
+                d.V_blob = _ptr(arr("Vb", _radiation_blob(tree, tables, leaf_range),
+                                    np.float64), f64)
             d.points_tree = _ptr(arr("pts", tree.points, np.float64), f64)
             d.leaf_center = _ptr(arr("ctr", tables.leaf_center, np.float64), f64)
             # radii exactly as circle_points receives them: rho * h (operators.py:86-94)
