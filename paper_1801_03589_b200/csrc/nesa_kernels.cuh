@@ -33,12 +33,26 @@ namespace nesa {
 // shared memory.  Rows are owned by threads (r = t % m) with column lanes
 // (cl = t / m) reduced in a fixed order at the end of the item.
 
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, T v[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+
 struct BlockItem {
-  int64_t a_off;     // element offset of the column-major block in blob
+  int64_t a_off;     // element offset of the column-major block in blob (multiple of 4)
   int32_t m, n;      // rows, columns
+  int32_t ld;        // leading dimension: m rounded up to 4 (pad rows are zero)
   int32_t y_row0;    // first output row
   int32_t seg_begin; // segments [seg_begin, seg_begin + seg_count)
   int32_t seg_count;
+  int32_t x0;        // radiation items: first point of the leaf (device assembly)
   int32_t pad;
 };
 struct BlockSeg {
@@ -50,7 +64,7 @@ struct BlockSeg {
 // fetches it with ONE coalesced load (lane l <- word l) and prefetches the
 // next one while the current is in flight: no dependent metadata loads on
 // the streaming path.
-constexpr int kRecSegs = 12;
+constexpr int kRecSegs = 11;
 struct __align__(128) ChunkRec {
   int64_t src_off;   // element offset of the chunk's first element in blob
   int32_t m;         // rows of the item
@@ -58,19 +72,21 @@ struct __align__(128) ChunkRec {
   int32_t y_row0;    // first output row of the item
   int32_t flags;     // bit0 first chunk of its item, bit1 last chunk
   int32_t nseg;      // x segments of this chunk (<= kRecSegs)
-  int32_t pad;
+  int32_t ld;        // leading dimension (multiple of 4)
+  uint32_t magic;    // ceil(2^32 / (ld/4)): thread -> (row quad, column lane) without division
+  int32_t CL;        // column lanes = consumer threads / (ld/4)
   int32_t seg[2 * kRecSegs];  // (x_row0, first column within the chunk) pairs
 };
 static_assert(sizeof(ChunkRec) == 128, "ChunkRec must be 128 bytes");
 
-constexpr int kStages = 4;
-constexpr int kABytes = 24 * 1024;         // payload per stage
-constexpr int kAStride = kABytes + 128;    // + alignment slack, keeps 128 B alignment
+constexpr int kStages = 3;
+constexpr int kABytes = 16 * 1024;         // payload per stage
 constexpr int kMaxC = 256;                 // columns per chunk
 constexpr int kNCW = 8;                    // consumer warps
 constexpr int kNCT = kNCW * 32;            // consumer threads
 constexpr int kBGThreads = kNCT + 32;      // + producer warp
 constexpr int kMaxRows = 2 * kNCT;         // rows per item (taller blocks are paneled)
+constexpr int kBGPerSM = 2;                // resident CTAs per SM
 
 enum { kModeStore = 0, kModeScatter = 1 };
 
@@ -86,21 +102,24 @@ struct BlockGemvArgs {
 };
 
 struct StageHdr {
-  int32_t m, ncols, delta, flags, y_row0, pad[3];
+  int32_t m, ncols, ld, flags, y_row0, CL;
+  uint32_t magic;
+  int32_t pad;
 };
 
 // Per-stage shared memory: [A | X | header | (scatter) perm | base]
 template <typename T, int R, int MODE>
 struct BGLayout {
+  static constexpr size_t kA = kABytes;
   static constexpr size_t kX = size_t(kMaxC) * R * sizeof(T);
   static constexpr size_t kFinPerm = MODE == kModeScatter ? size_t(kMaxRows) * 8 : 0;
   static constexpr size_t kFinBase = MODE == kModeScatter ? size_t(kMaxRows) * R * sizeof(T) : 0;
   static constexpr size_t kStage =
-      ((kAStride + kX + sizeof(StageHdr) + kFinPerm + kFinBase) + 127) & ~size_t(127);
-  static constexpr size_t kRed = size_t(kNCT) * R * sizeof(T);
+      ((kA + kX + sizeof(StageHdr) + kFinPerm + kFinBase) + 127) & ~size_t(127);
+  static constexpr size_t kRed = size_t(4) * kNCT * R * sizeof(T);
   static constexpr size_t kBytes = kStages * kStage + kRed + 2 * kStages * sizeof(uint64_t) + 16;
-  static constexpr size_t offX = kAStride;
-  static constexpr size_t offHdr = kAStride + kX;
+  static constexpr size_t offX = kA;
+  static constexpr size_t offHdr = kA + kX;
   static constexpr size_t offPerm = offHdr + sizeof(StageHdr);
   static constexpr size_t offBase = offPerm + kFinPerm;
 };
@@ -110,13 +129,38 @@ constexpr size_t blockgemv_smem_bytes() {
   return BGLayout<T, R, MODE>::kBytes;
 }
 
+template <typename T, int R>
+__device__ __forceinline__ void ldx(const T* p, T v[R]) {
+  if constexpr (R * sizeof(T) == 8) {
+    if constexpr (sizeof(T) == 4) {
+      const float2 t = *reinterpret_cast<const float2*>(p);
+      v[0] = t.x;
+      v[1] = t.y;
+    } else {
+      v[0] = p[0];
+    }
+  } else if constexpr (R * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 t = *reinterpret_cast<const float4*>(p);
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+      const double2 t = *reinterpret_cast<const double2*>(p);
+      v[0] = t.x;
+      v[1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) v[rr] = p[rr];
+  }
+}
+
 template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGemvArgs<T> a) {
+__global__ void __launch_bounds__(kBGThreads, kBGPerSM) blockgemv_kernel(const BlockGemvArgs<T> a) {
   using Lay = BGLayout<T, R, MODE>;
   extern __shared__ __align__(128) unsigned char smem[];
   T* sRed = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(sRed + kNCT * R) + 15) & ~uintptr_t(15));
+      (reinterpret_cast<uintptr_t>(sRed + 4 * kNCT * R) + 15) & ~uintptr_t(15));
   uint64_t* empty = full + kStages;
 
   const int c0 = a.cta_chunk_ptr[blockIdx.x];
@@ -150,26 +194,28 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
       const int y_row0 = __shfl_sync(0xffffffffu, w, 4);
       const int flags = __shfl_sync(0xffffffffu, w, 5);
       const int nseg = __shfl_sync(0xffffffffu, w, 6);
-      const uintptr_t src = reinterpret_cast<uintptr_t>(a.blob + src_off);
-      const uint32_t bytes = uint32_t(ncols) * uint32_t(m) * uint32_t(sizeof(T));
-      const uintptr_t s0 = src & ~uintptr_t(15);
-      const uintptr_t s1 = (src + bytes + 15) & ~uintptr_t(15);
+      const int ld = __shfl_sync(0xffffffffu, w, 7);
+      const uint32_t magic = uint32_t(__shfl_sync(0xffffffffu, w, 8));
+      const int CLv = __shfl_sync(0xffffffffu, w, 9);
+      const uint32_t bytes = uint32_t(ncols) * uint32_t(ld) * uint32_t(sizeof(T));
       mbar_wait(&empty[st], (round & 1u) ^ 1u);
       if (lane == 0) {
         StageHdr* h = reinterpret_cast<StageHdr*>(stg + Lay::offHdr);
         h->m = m;
         h->ncols = ncols;
-        h->delta = int(src - s0);
+        h->ld = ld;
         h->flags = flags;
         h->y_row0 = y_row0;
-        mbar_arrive_expect_tx(&full[st], uint32_t(s1 - s0));
-        bulk_g2s(stg, reinterpret_cast<const void*>(s0), uint32_t(s1 - s0), &full[st]);
+        h->magic = magic;
+        h->CL = CLv;
+        mbar_arrive_expect_tx(&full[st], bytes);
+        bulk_g2s(stg, a.blob + src_off, bytes, &full[st]);
       }
       T* xs = reinterpret_cast<T*>(stg + Lay::offX);
       for (int sg = 0; sg < nseg; ++sg) {
-        const int xr = __shfl_sync(0xffffffffu, w, 8 + 2 * sg);
-        const int cs = __shfl_sync(0xffffffffu, w, 9 + 2 * sg);
-        const int ce = sg + 1 < nseg ? __shfl_sync(0xffffffffu, w, 11 + 2 * sg) : ncols;
+        const int xr = __shfl_sync(0xffffffffu, w, 10 + 2 * sg);
+        const int cs = __shfl_sync(0xffffffffu, w, 11 + 2 * sg);
+        const int ce = sg + 1 < nseg ? __shfl_sync(0xffffffffu, w, 13 + 2 * sg) : ncols;
         for (int c = cs + lane; c < ce; c += 32)
           cp_async_n<R * sizeof(T)>(xs + c * R, a.x + int64_t(xr + (c - cs)) * R);
       }
@@ -187,64 +233,65 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
     }
   } else {
     // ------------------------------ consumers -----------------------------
+    // Thread (rq, cl): rows 4rq..4rq+3 of the item, columns cl, cl+CL, ...;
+    // one 16-byte shared load of A per column; column lanes are reduced in
+    // a fixed order at the end of the item.
     const int tid = threadIdx.x;
-    T acc0[R], acc1[R], accB[R];
+    T acc[4][R];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = T(0);
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[i][rr] = T(0);
     for (int i = c0; i < c1; ++i) {
       const int k = i - c0, st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
       const unsigned char* stg = smem + size_t(st) * Lay::kStage;
       mbar_wait(&full[st], round & 1u);
       const StageHdr h = *reinterpret_cast<const StageHdr*>(stg + Lay::offHdr);
-      const int m = h.m, nc = h.ncols;
-      const T* A = reinterpret_cast<const T*>(stg + h.delta);
+      const int m = h.m, nc = h.ncols, ld = h.ld, CL = h.CL;
+      const int RQ = ld >> 2;
+      const int cl = RQ == 1 ? tid : int(__umulhi(uint32_t(tid), h.magic));
+      const int rq = tid - cl * RQ;
+      const T* A = reinterpret_cast<const T*>(stg);
       const T* X = reinterpret_cast<const T*>(stg + Lay::offX);
       if (h.flags & 1) {
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) acc0[rr] = acc1[rr] = T(0);
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) acc[q][rr] = T(0);
       }
-      if (m <= kNCT) {
-        const int CL = kNCT / m;
-        const int r = tid % m, cl = tid / m;
-        if (cl < CL) {
+      if (cl < CL) {
+        const T* Ap = A + 4 * rq;
+#pragma unroll 4
+        for (int c = cl; c < nc; c += CL) {
+          T a4[4], xv[R];
+          ld4(Ap + c * ld, a4);
+          ldx<T, R>(X + c * R, xv);
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) accB[rr] = T(0);
-          int c = cl;
-          for (; c + CL < nc; c += 2 * CL) {
-            const T a0 = A[c * m + r], a1 = A[(c + CL) * m + r];
+          for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-              acc0[rr] = fma(a0, X[c * R + rr], acc0[rr]);
-              accB[rr] = fma(a1, X[(c + CL) * R + rr], accB[rr]);
-            }
-          }
-          if (c < nc) {
-            const T a0 = A[c * m + r];
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) acc0[rr] = fma(a0, X[c * R + rr], acc0[rr]);
-          }
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) acc0[rr] += accB[rr];
-        }
-      } else {
-        const int r1 = tid + kNCT;
-        for (int c = 0; c < nc; ++c) {
-          const T a0 = A[c * m + tid];
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) acc0[rr] = fma(a0, X[c * R + rr], acc0[rr]);
-          if (r1 < m) {
-            const T a1 = A[c * m + r1];
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) acc1[rr] = fma(a1, X[c * R + rr], acc1[rr]);
-          }
+            for (int rr = 0; rr < R; ++rr) acc[q][rr] = fma(a4[q], xv[rr], acc[q][rr]);
         }
       }
 
-      if (h.flags & 2) {  // last chunk of the item: reduce + write
+      if (h.flags & 2) {  // last chunk of the item: reduce column lanes + write
         const int64_t* sperm = reinterpret_cast<const int64_t*>(stg + Lay::offPerm);
         const T* sbase = reinterpret_cast<const T*>(stg + Lay::offBase);
-        auto write = [&](int row, const T* v) {
+        if (cl < CL) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) sRed[(cl * ld + 4 * rq + q) * R + rr] = acc[q][rr];
+        }
+        named_bar_sync(1, kNCT);
+        for (int row = tid; row < m; row += kNCT) {
+          T v[R];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) v[rr] = sRed[row * R + rr];
+          for (int l = 1; l < CL; ++l) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) v[rr] += sRed[(l * ld + row) * R + rr];
+          }
           if constexpr (MODE == kModeStore) {
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) a.y[int64_t(h.y_row0 + row) * R + rr] = v[rr];
@@ -254,34 +301,10 @@ __global__ void __launch_bounds__(kBGThreads, 1) blockgemv_kernel(const BlockGem
             for (int rr = 0; rr < R; ++rr)
               a.y[dst * R + rr] = (a.base ? sbase[row * R + rr] : T(0)) + v[rr];
           }
-        };
-        if (m <= kNCT / 2) {
-          const int CL = kNCT / m;
-          const int r = tid % m, cl = tid / m;
-          if (cl < CL) {
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) sRed[(cl * m + r) * R + rr] = acc0[rr];
-          }
-          named_bar_sync(1, kNCT);
-          if (tid < m) {
-            T v[R];
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) v[rr] = sRed[tid * R + rr];
-            for (int l = 1; l < CL; ++l) {
-#pragma unroll
-              for (int rr = 0; rr < R; ++rr) v[rr] += sRed[(l * m + tid) * R + rr];
-            }
-            write(tid, v);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[st]);
-          named_bar_sync(1, kNCT);
-        } else {
-          if (tid < m) write(tid, acc0);
-          if (tid + kNCT < m) write(tid + kNCT, acc1);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[st]);
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        named_bar_sync(1, kNCT);
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -349,18 +372,6 @@ template <>
 struct Vec4<double> {
   using type = double4;
 };
-
-template <typename T>
-__device__ __forceinline__ void ld4(const T* p, T v[4]) {
-  if constexpr (sizeof(T) == 4) {
-    const float4 t = *reinterpret_cast<const float4*>(p);
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else {
-    const double2 a = *reinterpret_cast<const double2*>(p);
-    const double2 b = *reinterpret_cast<const double2*>(p + 2);
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-  }
-}
 
 // acc[r][c] += sum_{j in [jb, je)} MT[j*Qp + k0 + r] * X[j*NC + c0 + c]
 template <typename T>
@@ -473,10 +484,9 @@ size_t level_smem_bytes(int Q, int qs) {
 template <typename T, int R>
 __global__ void __launch_bounds__(kFarThreads) upward_kernel(
     const T* __restrict__ CT, const int32_t* __restrict__ slot, int64_t pf, int64_t pc, T* s,
-    int Q, int QS) {
+    int Q, int QS, int TP) {
   extern __shared__ __align__(128) unsigned char smem[];
   const FarGeom G = far_geom(Q);
-  const int TP = G.NC / R;
   const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
   unsigned char* Mbase = smem;
   unsigned char* Xbase = smem + QS * mb;
@@ -542,10 +552,10 @@ template <typename T, int R>
 __global__ void __launch_bounds__(kFarThreads) downward_kernel(
     const T* __restrict__ BT, const int32_t* __restrict__ quad, const int32_t* __restrict__ order,
     const int32_t* __restrict__ opar, const int64_t* __restrict__ int_ptr,
-    const T* __restrict__ Y, int64_t cc, T* o, int Q, int QS, int has_parent) {
+    const T* __restrict__ Y, int64_t cc, T* o, int Q, int QS, int has_parent, int TC) {
   extern __shared__ __align__(128) unsigned char smem[];
   const FarGeom G = far_geom(Q);
-  const int TC = G.NC / R, QR = Q * R;
+  const int QR = Q * R;
   const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
   unsigned char* Xp = smem;            // parent amplitudes, column layout
   unsigned char* Ys = smem + xb;       // translation sums, column layout

@@ -107,15 +107,19 @@ void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
   for (size_t i = 0; i < hs.items.size(); ++i) {
     const BlockItem& it = hs.items[i];
     item_first_chunk[i] = int64_t(hs.recs.size());
-    int per = int(std::min<int64_t>(kMaxC, kABytes / (int64_t(it.m) * int64_t(elem_bytes))));
+    int per = int(std::min<int64_t>(kMaxC, kABytes / (int64_t(it.ld) * int64_t(elem_bytes))));
     per = std::max(per, 1);
+    const int RQ = it.ld / 4;
     const int seg_end = it.seg_begin + it.seg_count;
     int c = 0;
     while (c < it.n) {
       ChunkRec r{};
-      r.src_off = it.a_off + int64_t(c) * it.m;
+      r.src_off = it.a_off + int64_t(c) * it.ld;
       r.m = it.m;
+      r.ld = it.ld;
       r.y_row0 = it.y_row0;
+      r.magic = RQ == 1 ? 0u : uint32_t(((uint64_t(1) << 32) + RQ - 1) / RQ);
+      r.CL = kNCT / RQ;
       int ce = std::min(it.n, c + per);
       // segments overlapping [c, ce); cut the chunk if more than kRecSegs
       int ns = 0;
@@ -138,7 +142,7 @@ void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
       hs.recs.push_back(r);
       c = ce;
     }
-    item_bytes[i] = double(it.m) * it.n * elem_bytes + 256.0;  // + per-item overhead
+    item_bytes[i] = double(it.ld) * it.n * elem_bytes + 256.0;  // + per-item overhead
   }
   item_first_chunk[hs.items.size()] = int64_t(hs.recs.size());
   const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_grid, int64_t(hs.items.size()))));
@@ -199,7 +203,7 @@ __global__ void assemble_near_kernel(const BlockItem* items, const BlockSeg* seg
       const int64_t i = it.y_row0 + r, j = S.x_row0 + (c - S.col0);
       const double v = (i == j) ? 0.0
                                 : kernel_entry(pts[2 * i], pts[2 * i + 1], pts[2 * j], pts[2 * j + 1]);
-      blob[it.a_off + int64_t(c) * it.m + r] = T(v);
+      blob[it.a_off + int64_t(c) * it.ld + r] = T(v);
     }
   }
 }
@@ -216,7 +220,7 @@ __global__ void assemble_V_kernel(const BlockItem* items, const int64_t* item_le
   const double cx = center[2 * leaf], cy = center[2 * leaf + 1], rc = r_check[leaf];
   for (int c = 0; c < it.n; ++c) {
     // column c is point (segment x_row0 + c); V items carry one segment.
-    const int64_t j = int64_t(it.pad) + c;  // pad holds the leaf's first point
+    const int64_t j = int64_t(it.x0) + c;
     const double px = pts[2 * j], py = pts[2 * j + 1];
     __syncthreads();
     for (int i = threadIdx.x; i < n_check; i += blockDim.x) {
@@ -228,7 +232,7 @@ __global__ void assemble_V_kernel(const BlockItem* items, const int64_t* item_le
     for (int k = threadIdx.x; k < Q; k += blockDim.x) {
       double acc = 0.0;
       for (int i = 0; i < n_check; ++i) acc = fma(fit[int64_t(k) * n_check + i], kc[i], acc);
-      blob[it.a_off + int64_t(c) * Q + k] = T(acc);
+      blob[it.a_off + int64_t(c) * it.ld + k] = T(acc);
     }
   }
 }
@@ -247,7 +251,7 @@ __global__ void assemble_U_kernel(const BlockItem* items, const int64_t* item_le
     const int64_t i = it.y_row0 + r;
     const double ax = __dadd_rn(cx, __dmul_rn(ra, acos_[k]));
     const double ay = __dadd_rn(cy, __dmul_rn(ra, asin_[k]));
-    blob[it.a_off + int64_t(k) * it.m + r] = T(kernel_entry(pts[2 * i], pts[2 * i + 1], ax, ay));
+    blob[it.a_off + int64_t(k) * it.ld + r] = T(kernel_entry(pts[2 * i], pts[2 * i + 1], ax, ay));
   }
 }
 
@@ -374,7 +378,7 @@ void upload_host_blob(DevBlockSet& d, const HostBlockSet& h, const double* src,
     const int32_t ld = item_src_rows[i], r0 = item_row0[i];
     for (int c = 0; c < it.n; ++c)
       for (int r = 0; r < it.m; ++r)
-        stage[it.a_off + int64_t(c) * it.m + r] = T(src[so + int64_t(c) * ld + r0 + r]);
+        stage[it.a_off + int64_t(c) * it.ld + r] = T(src[so + int64_t(c) * ld + r0 + r]);
   }
   if (!stage.empty())
     CUDA_OK(cudaMemcpy(d.blob.p, stage.data(), stage.size() * sizeof(T), cudaMemcpyHostToDevice));
@@ -516,26 +520,28 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         const int32_t seg_count = int32_t(hn.segs.size()) - seg_begin;
         for (int64_t r0 = 0; r0 < na; r0 += kMaxRows) {
           const int32_t m = int32_t(std::min<int64_t>(kMaxRows, na - r0));
-          hn.items.push_back(BlockItem{hn.blob_elems, m, int32_t(W),
-                                       int32_t(d->group_start[a] + r0), seg_begin, seg_count, 0});
+          const int32_t ld = (m + 3) / 4 * 4;
+          hn.items.push_back(BlockItem{hn.blob_elems, m, int32_t(W), ld,
+                                       int32_t(d->group_start[a] + r0), seg_begin, seg_count, 0, 0});
           near_src_off.push_back(near_off);
           near_src_rows.push_back(int32_t(na));
           near_row0.push_back(int32_t(r0));
-          hn.blob_elems += int64_t(m) * W;
+          hn.blob_elems += int64_t(ld) * W;
           hn.entries += int64_t(m) * W;
         }
         // V: Q x na, x = qt rows of the leaf, y = s rows of leaf a
         {
           const int32_t sb = int32_t(hv.segs.size());
           hv.segs.push_back(BlockSeg{int32_t(d->group_start[a]), 0});
-          BlockItem it{hv.blob_elems, Q, int32_t(na), int32_t(a * Q), sb, 1,
-                       int32_t(d->group_start[a])};
+          const int32_t ld = (Q + 3) / 4 * 4;
+          BlockItem it{hv.blob_elems, Q, int32_t(na), ld, int32_t(a * Q), sb, 1,
+                       int32_t(d->group_start[a]), 0};
           hv.items.push_back(it);
           v_src_off.push_back(v_off);
           v_src_rows.push_back(Q);
           v_row0.push_back(0);
           v_leaf.push_back(a);
-          hv.blob_elems += int64_t(Q) * na;
+          hv.blob_elems += int64_t(ld) * na;
           hv.entries += int64_t(Q) * na;
         }
         // U: na x Q, x = o rows of leaf a, y = phi rows
@@ -544,13 +550,14 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           hu.segs.push_back(BlockSeg{int32_t(a * Q), 0});
           for (int64_t r0 = 0; r0 < na; r0 += kMaxRows) {
             const int32_t m = int32_t(std::min<int64_t>(kMaxRows, na - r0));
-            hu.items.push_back(BlockItem{hu.blob_elems, m, Q,
-                                         int32_t(d->group_start[a] + r0), sb, 1, 0});
+            const int32_t ld = (m + 3) / 4 * 4;
+            hu.items.push_back(BlockItem{hu.blob_elems, m, Q, ld,
+                                         int32_t(d->group_start[a] + r0), sb, 1, 0, 0});
             u_src_off.push_back(u_off);
             u_src_rows.push_back(int32_t(na));
             u_row0.push_back(int32_t(r0));
             u_leaf.push_back(a);
-            hu.blob_elems += int64_t(m) * Q;
+            hu.blob_elems += int64_t(ld) * Q;
             hu.entries += int64_t(m) * Q;
           }
         }
@@ -561,9 +568,9 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
   }
-  chunk_and_balance(hn, es, P->n_sm);
-  chunk_and_balance(hv, es, P->n_sm);
-  chunk_and_balance(hu, es, P->n_sm);
+  chunk_and_balance(hn, es, kBGPerSM * P->n_sm);
+  chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
+  chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
   upload_blockset<T>(P->Vset, hv);
   upload_blockset<T>(P->Uset, hu);
@@ -725,14 +732,21 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   const size_t mstride = P->mbytes / sizeof(T);
   const FarGeom FG = far_geom(Q);
   const size_t lvl_sm = level_smem_bytes<T>(Q, P->qs);
+  // groups per CTA: fill the column tile only when the level is big enough to
+  // occupy every SM twice; coarse levels get one group per CTA
+  auto tile_for = [&](int64_t count) {
+    const int64_t want = (count + 2 * P->n_sm - 1) / (2 * P->n_sm);
+    return int(std::max<int64_t>(1, std::min<int64_t>(FG.NC / R, want)));
+  };
   auto up_pass = [&]() {
-    const int TP = FG.NC / R;
     for (int lv = P->L; lv > P->l0; --lv) {
       const int ci = lv - P->l0, pi = ci - 1;
       const int64_t pc = P->loc_count[pi];
       if (pc == 0) continue;
+      const int TP = tile_for(pc);
       upward_kernel<T, R><<<int((pc + TP - 1) / TP), kFarThreads, lvl_sm, s0>>>(
-          CT + size_t(ci - 1) * 4 * mstride, P->up_slot[ci].p, P->loc_first[pi], pc, s, Q, P->qs);
+          CT + size_t(ci - 1) * 4 * mstride, P->up_slot[ci].p, P->loc_first[pi], pc, s, Q, P->qs,
+          TP);
       nk++;
     }
   };
@@ -743,16 +757,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
           P->tunits.p, P->tents.p, reinterpret_cast<const T*>(P->DT.p), s, Y, Q);
       nk++;
     }
-    const int TC = FG.NC / R;
     const size_t dsm = down_smem_bytes<T>(Q, P->qs);
     for (int lv = P->l0; lv <= P->L; ++lv) {
       const int ci = lv - P->l0;
       const int64_t cc = P->loc_count[ci];
       if (cc == 0) continue;
+      const int TC = tile_for(cc);
       const T* Bl = ci > 0 ? BT + size_t(ci - 1) * 4 * mstride : BT;
       downward_kernel<T, R><<<int((cc + TC - 1) / TC), kFarThreads, dsm, s0>>>(
           Bl, P->quad.p, P->down_order[ci].p, P->down_par[ci].p, P->int_ptr.p, Y, cc, o, Q, P->qs,
-          ci > 0 ? 1 : 0);
+          ci > 0 ? 1 : 0, TC);
       nk++;
     }
   };
