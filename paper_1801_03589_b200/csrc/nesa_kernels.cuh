@@ -470,182 +470,193 @@ __device__ __forceinline__ void tile_reduce(const FarGeom& G, const TileMap& m, 
   }
 }
 
+// ----------------------------------------------------------------------------
+// Level transfer kernels (one launch per level).  The level's groups are
+// visited in `order` (sorted by child quadrant, then id), NC/R per CTA, so a
+// CTA needs one quadrant matrix (two at a boundary).  Children-major form:
+//   kLvlUpLeaf  T[c] = C_{quad c} s[c]                 (leaf level, s from V)
+//   kLvlUpSum   s[c] = sum_k T[first child of c + k];  T[c] = C_{quad c} s[c]
+//   kLvlDown    o[c] += B_{quad c} o[parent c]
+// The parent's s is the ordered sum of its children's T (fastmvp.py:160-162
+// accumulates s[parent] += C s[child] in child-id order); o[c] already holds
+// its translation sum (reduce_kernel) when the downward kernel runs, matching
+// fastmvp.py:163-169 (translations first, then potential transfer).
+// Matrices arrive by bulk copy; amplitudes by cp.async or summed in staging.
+// ----------------------------------------------------------------------------
+enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2 };
+
 template <typename T>
 size_t level_smem_bytes(int Q, int qs) {
-  return size_t(qs) * (mat_bytes(Q, sizeof(T)) + xblk_bytes<T>(Q)) +
+  return size_t(qs) * mat_bytes(Q, sizeof(T)) + xblk_bytes<T>(Q) +
          size_t(16) * kFarThreads * sizeof(T) + 64;
 }
 
-// ----------------------------------------------------------------------------
-// Upward pass, one level: s[p] = sum_q C_q s[slot[p][q]] for local parents
-// pf .. pf+pc-1 (slot = -1: no child in that quadrant).  Matrices by bulk
-// copy, children by zero-filling cp.async, QS quadrants per round.
-// ----------------------------------------------------------------------------
 template <typename T, int R>
-__global__ void __launch_bounds__(kFarThreads) upward_kernel(
-    const T* __restrict__ CT, const int32_t* __restrict__ slot, int64_t pf, int64_t pc, T* s,
-    int Q, int QS, int TP) {
+struct LevelArgs {
+  const T* MT4;               // this level's four quadrant matrices (padded, transposed)
+  const int32_t* quad;        // [G]
+  const int32_t* order;       // level ids sorted by quadrant
+  const int32_t* opar;        // kLvlDown: parent of order[i]
+  const int64_t* child_first; // kLvlUpSum
+  const int32_t* n_child;
+  int64_t cf_lo, cf_hi;       // kLvlUpSum: local child id range (finer level)
+  const T* Tin;               // kLvlUpSum: finer level's transfers
+  T* s;                       // up: amplitudes (read leaf / written sum)
+  T* Tout;                    // up: transfers out
+  T* o;                       // down: incoming amplitudes
+  int64_t count;
+  int Q, QS, TC;
+};
+
+template <typename T, int R, int MODE>
+__global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R> a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const FarGeom G = far_geom(Q);
+  const FarGeom G = far_geom(a.Q);
+  const int Q = a.Q, QR = Q * R, TC = a.TC;
   const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
-  unsigned char* Mbase = smem;
-  unsigned char* Xbase = smem + QS * mb;
-  T* red = reinterpret_cast<T*>(Xbase + QS * xb);
+  T* X = reinterpret_cast<T*>(smem);
+  unsigned char* Mbase = smem + xb;
+  T* red = reinterpret_cast<T*>(Mbase + a.QS * mb);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 16 * kFarThreads);
-  const int64_t t0 = int64_t(blockIdx.x) * TP;
-  const int np = int(pc - t0 < TP ? pc - t0 : TP);
-  const int tid = threadIdx.x;
-  const TileMap tm = tile_map(G, np * R, tid);
+  const int64_t t0 = int64_t(blockIdx.x) * TC;
+  const int nc = int(a.count - t0 < TC ? a.count - t0 : TC);
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const TileMap tm = tile_map(G, nc * R, tid);
+  const int q_lo = a.quad[a.order[t0]], q_hi = a.quad[a.order[t0 + nc - 1]];
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
+    const int nq0 = min(a.QS, q_hi - q_lo + 1);
+    mbar_arrive_expect_tx(bar, uint32_t(nq0 * mb));
+    bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(a.MT4) + q_lo * mb, uint32_t(nq0 * mb),
+             bar);
   }
-  __syncthreads();
-  T acc[4][4];
-  zero4x4(acc);
-  for (int q0 = 0; q0 < 4; q0 += QS) {
-    if (q0) __syncthreads();  // previous slots consumed
-    if (tid == 0) {
-      mbar_arrive_expect_tx(bar, uint32_t(QS * mb));
-      bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(CT) + q0 * mb, uint32_t(QS * mb), bar);
+  __syncthreads();  // barrier initialised before anyone waits on it
+  // ---- stage the input amplitudes, one warp per column group
+  if constexpr (MODE == kLvlUpSum) {
+    for (int cc = wid; cc < nc; cc += kFarThreads / 32) {
+      const int64_t c = a.order[t0 + cc];
+      const int64_t k_lo = max(a.child_first[c], a.cf_lo);
+      const int64_t k_hi = min(a.child_first[c] + a.n_child[c], a.cf_hi);
+      for (int w = lane; w < QR; w += 32) {
+        T v = T(0);
+        for (int64_t k = k_lo; k < k_hi; ++k) v += a.Tin[k * QR + w];
+        a.s[c * QR + w] = v;
+        X[(w / R) * G.NC + cc * R + (w % R)] = v;
+      }
     }
-    // X_q[j][pp*R + rr] = s[child][j][rr]  (zeros for absent children)
-    for (int i = tid; i < QS * G.Q * np; i += kFarThreads) {
-      const int pp = i % np, j = (i / np) % G.Q, qq = i / (np * G.Q);
-      const int c = slot[(t0 + pp) * 4 + q0 + qq];
-      T* dst = reinterpret_cast<T*>(Xbase + qq * xb) + j * G.NC + pp * R;
-      cp_async_zfill_n<R * sizeof(T)>(dst, s + (int64_t(c < 0 ? 0 : c) * G.Q + j) * R, c >= 0);
+  } else {
+    for (int cc = wid; cc < nc; cc += kFarThreads / 32) {
+      const T* src = MODE == kLvlDown ? a.o + int64_t(a.opar[t0 + cc]) * QR
+                                      : a.s + int64_t(a.order[t0 + cc]) * QR;
+      for (int j = lane; j < Q; j += 32) cp_async_n<R * sizeof(T)>(X + j * G.NC + cc * R, src + j * R);
     }
     cp_async_commit();
     cp_async_wait_all();
-    mbar_wait(bar, uint32_t(q0 / QS) & 1u);
-    __syncthreads();
-    if (tm.live)
-      for (int qq = 0; qq < QS; ++qq)
-        mm4x4(reinterpret_cast<const T*>(Mbase + qq * mb),
-              reinterpret_cast<const T*>(Xbase + qq * xb), G, 4 * tm.rg, 4 * tm.cgi, acc, tm.jb,
-              tm.je);
+  }
+  int colq[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int cc = (4 * tm.cgi + c) / R;
+    colq[c] = (tm.live && cc < nc) ? a.quad[a.order[t0 + cc]] : -1;
+  }
+  T acc[4][4];
+  zero4x4(acc);
+  int round = 0;
+  for (int q0 = q_lo; q0 <= q_hi; q0 += a.QS, ++round) {
+    const int nq = min(a.QS, q_hi - q0 + 1);
+    if (round) {
+      __syncthreads();  // slots consumed
+      if (tid == 0) {
+        mbar_arrive_expect_tx(bar, uint32_t(nq * mb));
+        bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(a.MT4) + q0 * mb, uint32_t(nq * mb),
+                 bar);
+      }
+    }
+    mbar_wait(bar, uint32_t(round) & 1u);
+    __syncthreads();  // staging complete (first round)
+    if (tm.live) {
+      for (int qq = 0; qq < nq; ++qq) {
+        bool any = false;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) any |= colq[c] == q0 + qq;
+        if (!any) continue;
+        T part[4][4];
+        zero4x4(part);
+        mm4x4(reinterpret_cast<const T*>(Mbase + qq * mb), X, G, 4 * tm.rg, 4 * tm.cgi, part,
+              tm.jb, tm.je);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (colq[c] == q0 + qq)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][c] += part[r][c];
+      }
+    }
   }
   tile_reduce(G, tm, acc, red, tid);
   if (tm.live && tm.js == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int col = 4 * tm.cgi + c, pp = col / R, rr = col % R;
-      if (pp >= np) continue;
-      T* dst = s + (pf + t0 + pp) * int64_t(Q) * R + rr;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (4 * tm.rg + r < Q) dst[(4 * tm.rg + r) * R] = acc[r][c];
-    }
-  }
-}
-
-// ----------------------------------------------------------------------------
-// Downward pass fused with the translation reduce, one level:
-//   o[c] = sum_{e in interaction entries of c} Y[e]  +  B_{quad c} o[parent c]
-// (reference order: translation sums over c's interaction list, then the
-// potential transfer adds; fastmvp.py:163-169).  Children are visited in
-// `order` (sorted by quadrant, then id); `opar` are their parents.  With
-// has_parent = 0 (level l0) only the reduce runs.
-// ----------------------------------------------------------------------------
-template <typename T, int R>
-__global__ void __launch_bounds__(kFarThreads) downward_kernel(
-    const T* __restrict__ BT, const int32_t* __restrict__ quad, const int32_t* __restrict__ order,
-    const int32_t* __restrict__ opar, const int64_t* __restrict__ int_ptr,
-    const T* __restrict__ Y, int64_t cc, T* o, int Q, int QS, int has_parent, int TC) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const FarGeom G = far_geom(Q);
-  const int QR = Q * R;
-  const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
-  unsigned char* Xp = smem;            // parent amplitudes, column layout
-  unsigned char* Ys = smem + xb;       // translation sums, column layout
-  unsigned char* Mbase = smem + 2 * xb;
-  T* red = reinterpret_cast<T*>(Mbase + QS * mb);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 16 * kFarThreads);
-  const int64_t t0 = int64_t(blockIdx.x) * TC;
-  const int nc = int(cc - t0 < TC ? cc - t0 : TC);
-  const int tid = threadIdx.x;
-  const TileMap tm = tile_map(G, nc * R, tid);
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (has_parent) {
-    for (int i = tid; i < G.Q * nc; i += kFarThreads) {
-      const int cc_ = i % nc, j = i / nc;
-      cp_async_n<R * sizeof(T)>(reinterpret_cast<T*>(Xp) + j * G.NC + cc_ * R,
-                                o + (int64_t(opar[t0 + cc_]) * G.Q + j) * R);
-    }
-    cp_async_commit();
-  }
-  // Ys[j][cc*R + rr] = sum_e Y[e][j][rr] in entry order
-  for (int i = tid; i < nc * QR; i += kFarThreads) {
-    const int cc_ = i / QR, w = i % QR;
-    const int64_t c = order[t0 + cc_];
-    T v = T(0);
-    for (int64_t e = int_ptr[c]; e < int_ptr[c + 1]; ++e) v += Y[e * QR + w];
-    reinterpret_cast<T*>(Ys)[(w / R) * G.NC + cc_ * R + (w % R)] = v;
-  }
-  int colq[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int cc_ = (4 * tm.cgi + c) / R;
-    colq[c] = (tm.live && cc_ < nc) ? quad[order[t0 + cc_]] : -1;
-  }
-  T acc[4][4];
-  zero4x4(acc);
-  if (has_parent) {
-    const int q_lo = quad[order[t0]], q_hi = quad[order[t0 + nc - 1]];
-    int round = 0;
-    for (int q0 = q_lo; q0 <= q_hi; q0 += QS, ++round) {
-      const int nq = min(QS, q_hi - q0 + 1);
-      if (round) __syncthreads();
-      if (tid == 0) {
-        mbar_arrive_expect_tx(bar, uint32_t(nq * mb));
-        bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(BT) + q0 * mb, uint32_t(nq * mb),
-                 bar);
-      }
-      cp_async_wait_all();
-      mbar_wait(bar, uint32_t(round) & 1u);
-      __syncthreads();
-      if (tm.live) {
-        for (int qq = 0; qq < nq; ++qq) {
-          T part[4][4];
-          zero4x4(part);
-          mm4x4(reinterpret_cast<const T*>(Mbase + qq * mb), reinterpret_cast<const T*>(Xp), G,
-                4 * tm.rg, 4 * tm.cgi, part, tm.jb, tm.je);
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (colq[c] == q0 + qq)
-#pragma unroll
-              for (int r = 0; r < 4; ++r) acc[r][c] += part[r][c];
-        }
-      }
-    }
-    tile_reduce(G, tm, acc, red, tid);
-  }
-  __syncthreads();  // Ys complete
-  if (tm.live && tm.js == 0) {
-    const T* ys = reinterpret_cast<const T*>(Ys);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
       if (colq[c] < 0) continue;
       const int col = 4 * tm.cgi + c;
-      T* dst = o + int64_t(order[t0 + col / R]) * QR + (col % R);
+      const int64_t g = a.order[t0 + col / R];
+      T* dst = (MODE == kLvlDown ? a.o : a.Tout) + g * QR + (col % R);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int k = 4 * tm.rg + r;
-        if (k < Q) dst[k * R] = ys[k * G.NC + col] + acc[r][c];
+        if (k < Q) {
+          if constexpr (MODE == kLvlDown)
+            dst[k * R] += acc[r][c];
+          else
+            dst[k * R] = acc[r][c];
+        }
       }
     }
   }
 }
 
-template <typename T>
-size_t down_smem_bytes(int Q, int qs) {
-  return 2 * xblk_bytes<T>(Q) + size_t(qs) * mat_bytes(Q, sizeof(T)) +
-         size_t(16) * kFarThreads * sizeof(T) + 64;
+// s[c] = sum_k T[first child + k] for the coarsest level (no transfer above).
+template <typename T, int R>
+__global__ void sum_children_kernel(const int64_t* __restrict__ child_first,
+                                    const int32_t* __restrict__ n_child, int64_t first,
+                                    int64_t count, int64_t cf_lo, int64_t cf_hi,
+                                    const T* __restrict__ Tin, T* s, int Q) {
+  const int QR = Q * R;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count * QR;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = first + i / QR;
+    const int w = int(i % QR);
+    const int64_t k_lo = max(child_first[c], cf_lo), k_hi = min(child_first[c] + n_child[c], cf_hi);
+    T v = T(0);
+    for (int64_t k = k_lo; k < k_hi; ++k) v += Tin[k * QR + w];
+    s[c * QR + w] = v;
+  }
+}
+
+// o[g] = sum_{e in interaction entries of g} Y[e] (entry order) for the
+// listed groups: the translation sums of every level, one warp per group.
+template <typename T, int R>
+__global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
+                              const int64_t* __restrict__ int_ptr, const T* __restrict__ Y, T* o,
+                              int Q) {
+  const int QR = Q * R;
+  const int lane = threadIdx.x & 31;
+  for (int64_t wg = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; wg < n_ids;
+       wg += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t g = ids[wg];
+    const int64_t e0 = int_ptr[g], e1 = int_ptr[g + 1];
+    for (int w = lane; w < QR; w += 32) {
+      T v = T(0);
+      int64_t e = e0;
+      for (; e + 2 <= e1; e += 2) {
+        const T y0 = Y[e * QR + w], y1 = Y[(e + 1) * QR + w];
+        v += y0;
+        v += y1;
+      }
+      if (e < e1) v += Y[e * QR + w];
+      o[g * QR + w] = v;
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -656,7 +667,7 @@ size_t down_smem_bytes(int Q, int qs) {
 // buffered across passes); results go straight to Y (the per-target sums
 // happen in the fused downward kernel, in reference order).
 // ----------------------------------------------------------------------------
-constexpr int kTUnitPasses = 4;
+constexpr int kTUnitPasses = 8;
 
 struct TUnit {
   int32_t dtab;

@@ -297,14 +297,15 @@ struct nesa_plan {
   DevBuf<int64_t> int_ptr;  // [G+1] interaction CSR (Y rows of each target)
   int64_t nnz = 0;
   size_t mbytes = 0;                       // padded matrix stride (bytes)
-  std::vector<DevBuf<int32_t>> up_slot;     // per child level (lv-l0): parent x quadrant -> child
+  DevBuf<int32_t> red_ids;                  // local groups (translation-sum targets)
+  int64_t n_red = 0;
   std::vector<DevBuf<int32_t>> down_order;  // per level (index lv-l0): children by quadrant
   std::vector<DevBuf<int32_t>> down_par;    // parents of down_order
   int qs = 4;                               // quadrant slots staged per round
 
   // workspace for R real columns
   int ws_R = 0;
-  DevBuf<unsigned char> qt, phin, s, o, Y;
+  DevBuf<unsigned char> qt, phin, s, o, Y, Tup;
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -445,28 +446,20 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   // quadrant slots per round: keep the level kernels <= ~96 KB so they can
   // co-reside with the persistent near-field CTAs (~110 KB) on one SM
   P->qs = 2;
-  while (P->qs > 1 && (level_smem_bytes<T>(Q, P->qs) > 96 * 1024 ||
-                       down_smem_bytes<T>(Q, P->qs) > 96 * 1024))
-    P->qs /= 2;
-  require(level_smem_bytes<T>(Q, 1) <= 200 * 1024 && down_smem_bytes<T>(Q, 1) <= 200 * 1024 &&
-              tgemm_smem_bytes<T>(Q) <= 200 * 1024,
+  while (P->qs > 1 && level_smem_bytes<T>(Q, P->qs) > 96 * 1024) P->qs /= 2;
+  require(level_smem_bytes<T>(Q, 1) <= 200 * 1024 && tgemm_smem_bytes<T>(Q) <= 200 * 1024,
           "Q too large for the far-field kernels");
   // per-level gather tables (see nesa_kernels.cuh "Level transfers")
-  P->up_slot.resize(nlev);
   P->down_order.resize(nlev);
   P->down_par.resize(nlev);
   for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
     const int li = lv - P->l0;
     const int64_t cf = P->loc_first[li], cn = P->loc_count[li];
     const int64_t pf = P->loc_first[li - 1], pn = P->loc_count[li - 1];
-    std::vector<int32_t> slot(size_t(pn) * 4, -1);
     for (int64_t c = cf; c < cf + cn; ++c) {
       const int64_t pl = d->parent[c] - pf;
       require(pl >= 0 && pl < pn, "local child with a non-local parent");
-      require(slot[pl * 4 + d->quad[c]] < 0, "two children in one quadrant");
-      slot[pl * 4 + d->quad[c]] = int32_t(c);
     }
-    P->up_slot[li].upload(slot);
     std::vector<int32_t> ord(static_cast<size_t>(cn)), par(static_cast<size_t>(cn));
     for (int64_t i = 0; i < cn; ++i) ord[i] = int32_t(cf + i);
     std::stable_sort(ord.begin(), ord.end(),
@@ -475,13 +468,14 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->down_order[li].upload(ord);
     P->down_par[li].upload(par);
   }
-  {  // level l0: reduce-only pass over its local groups
-    std::vector<int32_t> ord(static_cast<size_t>(P->loc_count[0])), par(ord.size(), 0);
-    for (size_t i = 0; i < ord.size(); ++i) ord[i] = int32_t(P->loc_first[0] + int64_t(i));
-    P->down_order[0].upload(ord);
-    P->down_par[0].upload(par);
+  {
+    std::vector<int32_t> ids;
+    for (int li = 0; li < nlev; ++li)
+      for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
+        ids.push_back(int32_t(g));
+    P->n_red = int64_t(ids.size());
+    P->red_ids.upload(ids);
   }
-
   // ---- near / V / U block sets (local leaves)
   HostBlockSet hn, hv, hu;
   std::vector<int64_t> near_src_off, v_src_off, u_src_off;
@@ -667,6 +661,7 @@ void ensure_workspace(nesa_plan* P, int R) {
   P->s.alloc(size_t(P->G) * P->Q * R * es);
   P->o.alloc(size_t(P->G) * P->Q * R * es);
   P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
+  P->Tup.alloc(size_t(P->G) * P->Q * R * es);
   P->ws_R = R;
 }
 
@@ -697,8 +692,9 @@ void set_smem_attrs() {
                                int(blockgemv_smem_bytes<T, R, kModeScatter>())));
   const int lim = 220 * 1024;
   CUDA_OK(cudaFuncSetAttribute(tgemm_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(upward_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(downward_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   done = true;
 }
 
@@ -738,15 +734,47 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const int64_t want = (count + 2 * P->n_sm - 1) / (2 * P->n_sm);
     return int(std::max<int64_t>(1, std::min<int64_t>(FG.NC / R, want)));
   };
+  T* Tup = reinterpret_cast<T*>(P->Tup.p);
+  auto level_args = [&](int li, const T* M) {
+    LevelArgs<T, R> la{};
+    la.MT4 = M;
+    la.quad = P->quad.p;
+    la.order = P->down_order[li].p;
+    la.opar = P->down_par[li].p;
+    la.child_first = P->child_first.p;
+    la.n_child = P->n_child.p;
+    if (li + 1 < int(P->loc_first.size())) {
+      la.cf_lo = P->loc_first[li + 1];
+      la.cf_hi = P->loc_first[li + 1] + P->loc_count[li + 1];
+    }
+    la.Tin = Tup;
+    la.s = s;
+    la.Tout = Tup;
+    la.o = o;
+    la.count = P->loc_count[li];
+    la.Q = Q;
+    la.QS = P->qs;
+    la.TC = tile_for(la.count);
+    return la;
+  };
   auto up_pass = [&]() {
+    // children-major: T[c] = C s[c]; s[parent] = sum of its children's T
     for (int lv = P->L; lv > P->l0; --lv) {
-      const int ci = lv - P->l0, pi = ci - 1;
-      const int64_t pc = P->loc_count[pi];
-      if (pc == 0) continue;
-      const int TP = tile_for(pc);
-      upward_kernel<T, R><<<int((pc + TP - 1) / TP), kFarThreads, lvl_sm, s0>>>(
-          CT + size_t(ci - 1) * 4 * mstride, P->up_slot[ci].p, P->loc_first[pi], pc, s, Q, P->qs,
-          TP);
+      const int ci = lv - P->l0;
+      if (P->loc_count[ci] == 0) continue;
+      const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
+      const int grid = int((la.count + la.TC - 1) / la.TC);
+      if (lv == P->L)
+        level_kernel<T, R, kLvlUpLeaf><<<grid, kFarThreads, lvl_sm, s0>>>(la);
+      else
+        level_kernel<T, R, kLvlUpSum><<<grid, kFarThreads, lvl_sm, s0>>>(la);
+      nk++;
+    }
+    if (P->L > P->l0 && P->loc_count[0] > 0) {
+      const int64_t n = P->loc_count[0] * Q * R;
+      sum_children_kernel<T, R><<<grid_for(n, 256, cap), 256, 0, s0>>>(
+          P->child_first.p, P->n_child.p, P->loc_first[0], P->loc_count[0], P->loc_first[1],
+          P->loc_first[1] + P->loc_count[1], Tup, s, Q);
       nk++;
     }
   };
@@ -757,16 +785,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
           P->tunits.p, P->tents.p, reinterpret_cast<const T*>(P->DT.p), s, Y, Q);
       nk++;
     }
-    const size_t dsm = down_smem_bytes<T>(Q, P->qs);
-    for (int lv = P->l0; lv <= P->L; ++lv) {
+    // o[g] = translation sum of every local group (all levels, one launch)
+    reduce_kernel<T, R><<<grid_for(P->n_red * 32, 256, cap), 256, 0, s0>>>(
+        P->red_ids.p, P->n_red, P->int_ptr.p, Y, o, Q);
+    nk++;
+    for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
       const int ci = lv - P->l0;
-      const int64_t cc = P->loc_count[ci];
-      if (cc == 0) continue;
-      const int TC = tile_for(cc);
-      const T* Bl = ci > 0 ? BT + size_t(ci - 1) * 4 * mstride : BT;
-      downward_kernel<T, R><<<int((cc + TC - 1) / TC), kFarThreads, dsm, s0>>>(
-          Bl, P->quad.p, P->down_order[ci].p, P->down_par[ci].p, P->int_ptr.p, Y, cc, o, Q, P->qs,
-          ci > 0 ? 1 : 0, TC);
+      if (P->loc_count[ci] == 0) continue;
+      const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
+      level_kernel<T, R, kLvlDown><<<int((la.count + la.TC - 1) / la.TC), kFarThreads, lvl_sm, s0>>>(
+          la);
       nk++;
     }
   };
@@ -791,8 +819,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   };
 
   if (stage == 0) {
+    // gather -> radiation (full bandwidth) -> fork {near | up, translate,
+    // down: compute-bound, overlaps the memory-bound near field} -> join ->
+    // reception + scatter
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
     gather();
+    if (far) {
+      prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
+      launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
+      nk++;
+    }
     CUDA_OK(cudaEventRecord(P->ev_fork, s0));
     CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
     if (near) {
@@ -802,9 +838,6 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
     }
     if (far) {
-      prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
-      launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
-      nk++;
       up_pass();
       down_pass();
       prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
