@@ -594,23 +594,51 @@ __global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R
     }
   }
   tile_reduce(G, tm, acc, red, tid);
+  // stage the tile group-major in the consumed X buffer, then write every
+  // group's contiguous QR block with coalesced stores
+  __syncthreads();
   if (tm.live && tm.js == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       if (colq[c] < 0) continue;
-      const int col = 4 * tm.cgi + c;
-      const int64_t g = a.order[t0 + col / R];
-      T* dst = (MODE == kLvlDown ? a.o : a.Tout) + g * QR + (col % R);
+      const int col = 4 * tm.cgi + c, cc = col / R, rr = col % R;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int k = 4 * tm.rg + r;
-        if (k < Q) {
-          if constexpr (MODE == kLvlDown)
-            dst[k * R] += acc[r][c];
-          else
-            dst[k * R] = acc[r][c];
-        }
+        if (k < Q) X[cc * QR + k * R + rr] = acc[r][c];
       }
+    }
+  }
+  __syncthreads();
+  T* outb = MODE == kLvlDown ? a.o : a.Tout;
+  if ((QR % 4) == 0) {
+    const int nv = QR / 4;
+    for (int i = tid; i < nc * nv; i += kFarThreads) {
+      const int cc = i / nv, v = i - cc * nv;
+      T* dst = outb + int64_t(a.order[t0 + cc]) * QR + 4 * v;
+      T val[4];
+      ld4(X + cc * QR + 4 * v, val);
+      if constexpr (MODE == kLvlDown) {
+        T cur[4];
+        ld4(dst, cur);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) val[q] += cur[q];
+      }
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(dst) = make_float4(val[0], val[1], val[2], val[3]);
+      } else {
+        reinterpret_cast<double2*>(dst)[0] = make_double2(val[0], val[1]);
+        reinterpret_cast<double2*>(dst)[1] = make_double2(val[2], val[3]);
+      }
+    }
+  } else {
+    for (int i = tid; i < nc * QR; i += kFarThreads) {
+      const int cc = i / QR, w = i - cc * QR;
+      T* dst = outb + int64_t(a.order[t0 + cc]) * QR + w;
+      if constexpr (MODE == kLvlDown)
+        *dst += X[cc * QR + w];
+      else
+        *dst = X[cc * QR + w];
     }
   }
 }
@@ -641,20 +669,37 @@ __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
                               int Q) {
   const int QR = Q * R;
   const int lane = threadIdx.x & 31;
+  const bool vec = (QR % 4) == 0;
   for (int64_t wg = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; wg < n_ids;
        wg += (int64_t(gridDim.x) * blockDim.x) >> 5) {
     const int64_t g = ids[wg];
     const int64_t e0 = int_ptr[g], e1 = int_ptr[g + 1];
-    for (int w = lane; w < QR; w += 32) {
-      T v = T(0);
-      int64_t e = e0;
-      for (; e + 2 <= e1; e += 2) {
-        const T y0 = Y[e * QR + w], y1 = Y[(e + 1) * QR + w];
-        v += y0;
-        v += y1;
+    if (vec) {
+      for (int w = 4 * lane; w < QR; w += 128) {
+        T v[4] = {T(0), T(0), T(0), T(0)};
+        int64_t e = e0;
+        for (; e + 2 <= e1; e += 2) {
+          T a[4], b[4];
+          ld4(Y + e * QR + w, a);
+          ld4(Y + (e + 1) * QR + w, b);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = (v[i] + a[i]) + b[i];
+        }
+        if (e < e1) {
+          T a[4];
+          ld4(Y + e * QR + w, a);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] += a[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[g * QR + w + i] = v[i];
       }
-      if (e < e1) v += Y[e * QR + w];
-      o[g * QR + w] = v;
+    } else {
+      for (int w = lane; w < QR; w += 32) {
+        T v = T(0);
+        for (int64_t e = e0; e < e1; ++e) v += Y[e * QR + w];
+        o[g * QR + w] = v;
+      }
     }
   }
 }
@@ -680,73 +725,297 @@ struct TEnt {
   int32_t e;    // interaction entry (Y row)
 };
 
+// Translation GEMM geometry: 128 threads, 8 x 4 register tile per thread
+// (rows 8rg.., columns 4cg..): per j two 16-byte loads of D and one of the
+// sources feed 32 FMAs.
+constexpr int kTGThreads = 128;
+
+struct TGGeom {
+  int Q, Qp, RG, CG, NC;
+};
+__host__ __device__ inline TGGeom tg_geom(int Q) {
+  TGGeom g;
+  g.Q = Q;
+  g.Qp = (Q + 3) / 4 * 4;               // table row stride
+  g.RG = (Q + 7) / 8;                   // 8-row groups (rows >= Q are discarded)
+  g.CG = kTGThreads / g.RG;
+  g.NC = g.CG * 4;
+  return g;
+}
+
+// Entry-major staging: source vector p lives at X + p * XS (XS = QR padded to
+// 16 bytes plus 16 bytes, so column groups of one warp hit distinct banks);
+// each vector arrives as ONE bulk copy when QR * sizeof(T) is a multiple of
+// 16 (the usual case), else by 4/8-byte cp.async.
 template <typename T>
+__host__ __device__ inline int tg_xstride(int QR) {
+  const int per16 = 16 / int(sizeof(T));
+  return (QR + per16 - 1) / per16 * per16 + per16;
+}
+
+template <typename T, int R>
 size_t tgemm_smem_bytes(int Q) {
-  return mat_bytes(Q, sizeof(T)) + 2 * xblk_bytes<T>(Q) + 64;
+  const TGGeom G = tg_geom(Q);
+  const size_t xb = (size_t(G.NC / R) * tg_xstride<T>(Q * R) * sizeof(T) + 127) & ~size_t(127);
+  return mat_bytes(Q, sizeof(T)) + 64 /* row overrun pad */ + 2 * xb + 2 * 4 * size_t(G.NC) + 64;
 }
 
 template <typename T, int R>
 __device__ __forceinline__ void tgemm_stage(const TEnt* ents, int eb, int n, const T* s,
-                                            const FarGeom& G, T* X, int tid) {
-  for (int i = tid; i < n * G.Q; i += kFarThreads) {
-    const int p = i % n, j = i / n;
-    cp_async_n<R * sizeof(T)>(X + j * G.NC + p * R, s + (int64_t(ents[eb + p].src) * G.Q + j) * R);
+                                            const TGGeom& G, T* X, int XS, int32_t* eid,
+                                            uint64_t* bar, int tid) {
+  const int QR = G.Q * R;
+  const uint32_t vb = uint32_t(QR * sizeof(T));
+  if ((vb & 15u) == 0) {
+    if (tid < 32) {
+      if (tid == 0) mbar_arrive_expect_tx(bar, vb * uint32_t(n));
+      __syncwarp();
+      for (int p = tid; p < n; p += 32) {
+        const TEnt te = ents[eb + p];
+        eid[p] = te.e;
+        bulk_g2s(X + p * XS, s + int64_t(te.src) * QR, vb, bar);
+      }
+    }
+  } else {
+    for (int p = tid >> 5; p < n; p += kTGThreads / 32) {
+      const TEnt te = ents[eb + p];
+      if ((tid & 31) == 0) eid[p] = te.e;
+      const T* src = s + int64_t(te.src) * QR;
+      for (int w = tid & 31; w < QR; w += 32) cp_async<sizeof(T)>(X + p * XS + w, src + w);
+    }
+    cp_async_commit();
+    if (tid == 0) mbar_arrive(bar);
   }
-  cp_async_commit();
 }
 
 template <typename T, int R>
-__global__ void __launch_bounds__(kFarThreads) tgemm_kernel(const TUnit* __restrict__ units,
-                                                            const TEnt* __restrict__ ents,
-                                                            const T* __restrict__ DT,
-                                                            const T* __restrict__ s, T* Y, int Q) {
+__global__ void __launch_bounds__(kTGThreads) tgemm_kernel(const TUnit* __restrict__ units,
+                                                           const TEnt* __restrict__ ents,
+                                                           const T* __restrict__ DT,
+                                                           const T* __restrict__ s, T* Y, int Q) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const FarGeom G = far_geom(Q);
+  const TGGeom G = tg_geom(Q);
   const int QR = Q * R, per = G.NC / R;
-  const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
+  const int XS = tg_xstride<T>(QR);
+  const size_t mb = mat_bytes(Q, sizeof(T));
+  const size_t xb = (size_t(per) * XS * sizeof(T) + 127) & ~size_t(127);
   T* Dm = reinterpret_cast<T*>(smem);
-  T* X0 = reinterpret_cast<T*>(smem + mb);
-  T* X1 = reinterpret_cast<T*>(smem + mb + xb);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + 2 * xb);
+  T* Xb[2] = {reinterpret_cast<T*>(smem + mb + 64), reinterpret_cast<T*>(smem + mb + 64 + xb)};
+  int32_t* Eb[2] = {reinterpret_cast<int32_t*>(smem + mb + 64 + 2 * xb), nullptr};
+  Eb[1] = Eb[0] + G.NC;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Eb[1] + G.NC);  // [0] D, [1] X0, [2] X1
   const TUnit u = units[blockIdx.x];
   const int tid = threadIdx.x;
   const int rg = tid % G.RG, cg = tid / G.RG;
+  const bool bulk = ((QR * sizeof(T)) & 15) == 0;
   if (tid == 0) {
-    mbar_init(bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(bar, uint32_t(mb));
+    mbar_arrive_expect_tx(&bar[0], uint32_t(mb));
     bulk_g2s(Dm, reinterpret_cast<const unsigned char*>(DT) + size_t(u.dtab) * mb, uint32_t(mb),
-             bar);
+             &bar[0]);
   }
+  __syncthreads();
   const int n_all = u.ent_end - u.ent_begin;
   const int npass = (n_all + per - 1) / per;
-  tgemm_stage<T, R>(ents, u.ent_begin, min(per, n_all), s, G, X0, tid);
-  __syncthreads();  // barrier init visible before anyone waits
-  mbar_wait(bar, 0);
+  tgemm_stage<T, R>(ents, u.ent_begin, min(per, n_all), s, G, Xb[0], XS, Eb[0], &bar[1], tid);
+  mbar_wait(&bar[0], 0);
   for (int ps = 0; ps < npass; ++ps) {
-    T* X = (ps & 1) ? X1 : X0;
+    const int b = ps & 1;
+    const T* X = b ? Xb[1] : Xb[0];
+    const int32_t* eid = b ? Eb[1] : Eb[0];
     const int eb = u.ent_begin + ps * per;
     const int n = min(per, u.ent_end - eb);
     if (ps + 1 < npass) {
       const int eb2 = eb + per;
-      tgemm_stage<T, R>(ents, eb2, min(per, u.ent_end - eb2), s, G, (ps & 1) ? X0 : X1, tid);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      cp_async_wait_all();
+      tgemm_stage<T, R>(ents, eb2, min(per, u.ent_end - eb2), s, G, b ? Xb[0] : Xb[1], XS,
+                        b ? Eb[0] : Eb[1], &bar[1 + (b ^ 1)], tid);
     }
+    if (!bulk) {
+      if (ps + 1 < npass)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else
+        cp_async_wait_all();
+    }
+    mbar_wait(&bar[1 + b], uint32_t(ps >> 1) & 1u);
     __syncthreads();
     if (cg < G.CG && 4 * cg < n * R) {
-      T acc[4][4];
-      zero4x4(acc);
-      mm4x4(Dm, X, G, 4 * rg, 4 * cg, acc);
+      T acc[8][4];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
+      const T* mp = Dm + 8 * rg;
+      // column c of this thread = entry (4cg + c) / R, component (4cg + c) % R
+      const T* xq[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int col = 4 * cg + c;
+        xq[c] = X + (col / R) * XS + (col % R);
+      }
+#pragma unroll 2
+      for (int j = 0; j < G.Q; ++j) {
+        T m0[4], m1[4], x[4];
+        ld4(mp + j * G.Qp, m0);
+        ld4(mp + j * G.Qp + 4, m1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) x[c] = xq[c][j * R];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            acc[r][c] = fma(m0[r], x[c], acc[r][c]);
+            acc[r + 4][c] = fma(m1[r], x[c], acc[r + 4][c]);
+          }
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int col = 4 * cg + c, p = col / R, rr = col % R;
         if (p >= n) continue;
-        T* dst = Y + int64_t(ents[eb + p].e) * QR + rr;
+        T* dst = Y + int64_t(eid[p]) * QR + rr;
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (4 * rg + r < Q) dst[(4 * rg + r) * R] = acc[r][c];
+        for (int r = 0; r < 8; ++r)
+          if (8 * rg + r < Q) dst[(8 * rg + r) * R] = acc[r][c];
+      }
+    }
+    __syncthreads();  // X buffer reuse
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Warp-tiled translation GEMM for Q in {32, 64, 128} (the benchmark uses 64).
+// 128 threads = RW row-warps x CW column-warps, each warp a 32 x 32 tile of
+// Y = D S: lane (tr = lane / 8, tc = lane % 8) owns rows 8tr..8tr+7 and
+// columns 4tc..4tc+3.  Per j the 8 lanes of a row group read the same D
+// words (broadcast) and the four row groups one contiguous 128-byte line, so
+// a warp issues ~4 shared wavefronts per 32 FMAs.
+// ----------------------------------------------------------------------------
+template <typename T, int R, int QT>
+struct TGW {
+  static constexpr int RW = QT / 32;
+  static constexpr int CW = 4 / RW;
+  static constexpr int NC = 32 * CW;       // real columns per pass
+  static constexpr int PER = NC / R;       // entries per pass
+  static constexpr int QR = QT * R;
+  static constexpr int XS = (QR + 16 / int(sizeof(T)) - 1) / (16 / int(sizeof(T))) * (16 / int(sizeof(T))) +
+                            16 / int(sizeof(T));
+  static constexpr size_t MB = size_t(QT) * QT * sizeof(T);
+  static constexpr size_t XB = (size_t(PER) * XS * sizeof(T) + 127) & ~size_t(127);
+  static constexpr size_t SMEM = MB + 2 * XB + 2 * 4 * PER + 64;
+};
+
+template <typename T, int R, int QT>
+__global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__ units,
+                                                       const TEnt* __restrict__ ents,
+                                                       const T* __restrict__ DT,
+                                                       const T* __restrict__ s, T* Y) {
+  using W = TGW<T, R, QT>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* Dm = reinterpret_cast<T*>(smem);
+  T* Xb0 = reinterpret_cast<T*>(smem + W::MB);
+  T* Xb1 = reinterpret_cast<T*>(smem + W::MB + W::XB);
+  int32_t* Eb0 = reinterpret_cast<int32_t*>(smem + W::MB + 2 * W::XB);
+  int32_t* Eb1 = Eb0 + W::PER;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Eb1 + W::PER);  // [0] D, [1] X0, [2] X1
+  const TUnit u = units[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp % W::RW, wc = warp / W::RW;
+  const int tr = lane >> 3, tc = lane & 7;
+  const int row0 = 32 * wr + 8 * tr;   // first output row of this thread
+  const int col0 = 32 * wc + 4 * tc;   // first real column of this thread
+  constexpr uint32_t kVB = uint32_t(W::QR * sizeof(T));
+  const size_t mb = mat_bytes(QT, sizeof(T));
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bar[0], uint32_t(mb));
+    bulk_g2s(Dm, reinterpret_cast<const unsigned char*>(DT) + size_t(u.dtab) * mb, uint32_t(mb),
+             &bar[0]);
+  }
+  __syncthreads();
+  auto stage = [&](int eb, int n, T* X, int32_t* eid, uint64_t* b) {
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(b, kVB * uint32_t(n));
+      __syncwarp();
+      for (int p = lane; p < n; p += 32) {
+        const TEnt te = ents[eb + p];
+        eid[p] = te.e;
+        bulk_g2s(X + p * W::XS, s + int64_t(te.src) * W::QR, kVB, b);
+      }
+    }
+  };
+  const int n_all = u.ent_end - u.ent_begin;
+  const int npass = (n_all + W::PER - 1) / W::PER;
+  stage(u.ent_begin, min(W::PER, n_all), Xb0, Eb0, &bar[1]);
+  mbar_wait(&bar[0], 0);
+  for (int ps = 0; ps < npass; ++ps) {
+    const int b = ps & 1;
+    const T* X = b ? Xb1 : Xb0;
+    const int32_t* eid = b ? Eb1 : Eb0;
+    const int eb = u.ent_begin + ps * W::PER;
+    const int n = min(W::PER, u.ent_end - eb);
+    if (ps + 1 < npass)
+      stage(eb + W::PER, min(W::PER, u.ent_end - eb - W::PER), b ? Xb0 : Xb1, b ? Eb0 : Eb1,
+            &bar[1 + (b ^ 1)]);
+    mbar_wait(&bar[1 + b], uint32_t(ps >> 1) & 1u);
+    __syncthreads();  // eid visible
+    const bool active = col0 < n * R;
+    T acc[8][4];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
+    if (active) {
+      const T* mp = Dm + row0;
+      const T* xp = X + (col0 / R) * W::XS;  // first entry of this thread
+#pragma unroll 4
+      for (int j = 0; j < QT; ++j) {
+        T m0[4], m1[4], x[4];
+        ld4(mp + j * QT, m0);
+        ld4(mp + j * QT + 4, m1);
+        if constexpr (R == 1) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) x[c] = xp[c * W::XS + j];
+        } else if constexpr (R == 2) {
+          ldx<T, 2>(xp + 2 * j, x);
+          ldx<T, 2>(xp + W::XS + 2 * j, x + 2);
+        } else {
+          ldx<T, 4>(xp + 4 * j, x);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            acc[r][c] = fma(m0[r], x[c], acc[r][c]);
+            acc[r + 4][c] = fma(m1[r], x[c], acc[r + 4][c]);
+          }
+      }
+    }
+    // stage the tile entry-major in the consumed X buffer, then write each
+    // entry's contiguous QR block with 16-byte stores (no partial sectors)
+    __syncthreads();
+    T* O = (b ? Xb1 : Xb0);
+    if (active) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int col = col0 + c, p = col / R, rr = col % R;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) O[p * W::XS + (row0 + r) * R + rr] = acc[r][c];
+      }
+    }
+    __syncthreads();
+    {
+      constexpr int V = 16 / int(sizeof(T));  // elements per 16-byte store
+      constexpr int NV = W::QR / V;
+      for (int i = tid; i < n * NV; i += 128) {
+        const int p = i / NV, v = i - p * NV;
+        const float4 val = *reinterpret_cast<const float4*>(O + p * W::XS + v * V);
+        *reinterpret_cast<float4*>(Y + int64_t(eid[p]) * W::QR + v * V) = val;
       }
     }
     __syncthreads();  // X buffer reuse

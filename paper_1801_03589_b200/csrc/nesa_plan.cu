@@ -447,7 +447,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   // co-reside with the persistent near-field CTAs (~110 KB) on one SM
   P->qs = 2;
   while (P->qs > 1 && level_smem_bytes<T>(Q, P->qs) > 96 * 1024) P->qs /= 2;
-  require(level_smem_bytes<T>(Q, 1) <= 200 * 1024 && tgemm_smem_bytes<T>(Q) <= 200 * 1024,
+  require(level_smem_bytes<T>(Q, 1) <= 200 * 1024 && tgemm_smem_bytes<T, 4>(Q) <= 200 * 1024,
           "Q too large for the far-field kernels");
   // per-level gather tables (see nesa_kernels.cuh "Level transfers")
   P->down_order.resize(nlev);
@@ -634,7 +634,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
     }
     require(P->nnz < (int64_t(1) << 31), "too many interaction entries");
-    const int per = kTUnitPasses * (far_geom(Q).NC / 4);  // sized for R = 4; smaller R packs more
+    const int per = kTUnitPasses * (tg_geom(Q).NC / 4);  // sized for R = 4; smaller R packs more
     std::vector<TEnt> ents;
     std::vector<TUnit> units;
     for (int64_t dt = 0; dt < d->n_dtab; ++dt) {
@@ -692,6 +692,8 @@ void set_smem_attrs() {
                                int(blockgemv_smem_bytes<T, R, kModeScatter>())));
   const int lim = 220 * 1024;
   CUDA_OK(cudaFuncSetAttribute(tgemm_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
@@ -781,8 +783,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   auto down_pass = [&]() {
     T* Y = reinterpret_cast<T*>(P->Y.p);
     if (P->n_tunits > 0) {
-      tgemm_kernel<T, R><<<P->n_tunits, kFarThreads, tgemm_smem_bytes<T>(Q), s0>>>(
-          P->tunits.p, P->tents.p, reinterpret_cast<const T*>(P->DT.p), s, Y, Q);
+      const T* DTp = reinterpret_cast<const T*>(P->DT.p);
+      if (Q == 64)
+        tgemm_wt_kernel<T, R, 64><<<P->n_tunits, 128, TGW<T, R, 64>::SMEM, s0>>>(
+            P->tunits.p, P->tents.p, DTp, s, Y);
+      else if (Q == 32)
+        tgemm_wt_kernel<T, R, 32><<<P->n_tunits, 128, TGW<T, R, 32>::SMEM, s0>>>(
+            P->tunits.p, P->tents.p, DTp, s, Y);
+      else
+        tgemm_kernel<T, R><<<P->n_tunits, kTGThreads, tgemm_smem_bytes<T, R>(Q), s0>>>(
+            P->tunits.p, P->tents.p, DTp, s, Y, Q);
       nk++;
     }
     // o[g] = translation sum of every local group (all levels, one launch)

@@ -160,3 +160,16 @@ def test_plan_stats(golden):
     assert plan.stat("v_entries") == tree.n_points * params.Q
     assert plan.stat("d_refs") == int(a.int_ptr[-1])
     plan.close()
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_q64_bench_geometry_vs_oracle(dtype, tol):
+    # the benchmark's configuration family (ellipse + plates, P=64, Q=64) at a
+    # size the oracle finishes in seconds; exercises the Q=64 fast paths
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=3), 30000)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    q = geo.random_rhs(30000, 3)
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    qq = q if dtype == "f64" else q.astype(np.complex64)
+    assert rel_l2(mvp(tree, params, qq), ref) <= tol
