@@ -497,9 +497,7 @@ struct LevelArgs {
   const int32_t* quad;        // [G]
   const int32_t* order;       // level ids sorted by quadrant
   const int32_t* opar;        // kLvlDown: parent of order[i]
-  const int64_t* child_first; // kLvlUpSum
-  const int32_t* n_child;
-  int64_t cf_lo, cf_hi;       // kLvlUpSum: local child id range (finer level)
+  const int2* ochild;         // kLvlUpSum: (first local child, count) of order[i]
   const T* Tin;               // kLvlUpSum: finer level's transfers
   T* s;                       // up: amplitudes (read leaf / written sum)
   T* Tout;                    // up: transfers out
@@ -534,15 +532,37 @@ __global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R
   __syncthreads();  // barrier initialised before anyone waits on it
   // ---- stage the input amplitudes, one warp per column group
   if constexpr (MODE == kLvlUpSum) {
+    // s[c] = ordered sum of <= 4 children's T: all child loads in flight
+    // together, 4 consecutive elements per lane
     for (int cc = wid; cc < nc; cc += kFarThreads / 32) {
       const int64_t c = a.order[t0 + cc];
-      const int64_t k_lo = max(a.child_first[c], a.cf_lo);
-      const int64_t k_hi = min(a.child_first[c] + a.n_child[c], a.cf_hi);
-      for (int w = lane; w < QR; w += 32) {
-        T v = T(0);
-        for (int64_t k = k_lo; k < k_hi; ++k) v += a.Tin[k * QR + w];
-        a.s[c * QR + w] = v;
-        X[(w / R) * G.NC + cc * R + (w % R)] = v;
+      const int2 kr = a.ochild[t0 + cc];  // (first local child, count)
+      const bool vec = (QR % 4) == 0;
+      if (vec) {
+        for (int w = 4 * lane; w < QR; w += 128) {
+          T v[4] = {T(0), T(0), T(0), T(0)};
+          T t[4][4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < kr.y) ld4(a.Tin + (int64_t(kr.x) + k) * QR + w, t[k]);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < kr.y)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) v[i] += t[k][i];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            a.s[c * QR + w + i] = v[i];
+            X[((w + i) / R) * G.NC + cc * R + ((w + i) % R)] = v[i];
+          }
+        }
+      } else {
+        for (int w = lane; w < QR; w += 32) {
+          T v = T(0);
+          for (int k = 0; k < kr.y; ++k) v += a.Tin[(int64_t(kr.x) + k) * QR + w];
+          a.s[c * QR + w] = v;
+          X[(w / R) * G.NC + cc * R + (w % R)] = v;
+        }
       }
     }
   } else {
@@ -925,7 +945,10 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
   const int wr = warp % W::RW, wc = warp / W::RW;
   const int tr = lane >> 3, tc = lane & 7;
   const int row0 = 32 * wr + 8 * tr;   // first output row of this thread
-  const int col0 = 32 * wc + 4 * tc;   // first real column of this thread
+  // this thread's entries: e_i = E0 + tc + 8 i (i < 4/R), components rr < R;
+  // the 8 lanes of a row group read 8 consecutive entries (conflict-free)
+  constexpr int NE = 4 / R;
+  const int E0 = 32 * wc / R;
   constexpr uint32_t kVB = uint32_t(W::QR * sizeof(T));
   const size_t mb = mat_bytes(QT, sizeof(T));
   if (tid == 0) {
@@ -964,7 +987,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
             &bar[1 + (b ^ 1)]);
     mbar_wait(&bar[1 + b], uint32_t(ps >> 1) & 1u);
     __syncthreads();  // eid visible
-    const bool active = col0 < n * R;
+    const bool active = E0 + tc < n;
     T acc[8][4];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -972,21 +995,14 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
       for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
     if (active) {
       const T* mp = Dm + row0;
-      const T* xp = X + (col0 / R) * W::XS;  // first entry of this thread
+      const T* xp = X + (E0 + tc) * W::XS;
 #pragma unroll 4
       for (int j = 0; j < QT; ++j) {
         T m0[4], m1[4], x[4];
         ld4(mp + j * QT, m0);
         ld4(mp + j * QT + 4, m1);
-        if constexpr (R == 1) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) x[c] = xp[c * W::XS + j];
-        } else if constexpr (R == 2) {
-          ldx<T, 2>(xp + 2 * j, x);
-          ldx<T, 2>(xp + W::XS + 2 * j, x + 2);
-        } else {
-          ldx<T, 4>(xp + 4 * j, x);
-        }
+        for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -1003,7 +1019,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
     if (active) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int col = col0 + c, p = col / R, rr = col % R;
+        const int p = E0 + tc + 8 * (c / R), rr = c % R;
 #pragma unroll
         for (int r = 0; r < 8; ++r) O[p * W::XS + (row0 + r) * R + rr] = acc[r][c];
       }
@@ -1019,6 +1035,162 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
       }
     }
     __syncthreads();  // X buffer reuse
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Warp-tiled level transfer for Q in {32, 64} on the large levels (same
+// roles as level_kernel).  The tile's groups (sorted by quadrant, so one or
+// two quadrant matrices) are staged group-major by bulk copy (UpLeaf, Down)
+// or summed from the children (UpSum); each warp computes a 32 x 32 block
+// with the conflict-free lane layout of tgemm_wt_kernel.
+// ----------------------------------------------------------------------------
+template <typename T, int R, int QT>
+struct LVW {
+  using W = TGW<T, R, QT>;
+  static constexpr size_t SMEM = 4 * W::MB + W::XB + 3 * 64;
+};
+
+template <typename T, int R, int QT, int MODE>
+__global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) {
+  using W = TGW<T, R, QT>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  T* M = reinterpret_cast<T*>(smem);                         // up to 4 quadrant matrices
+  T* X = reinterpret_cast<T*>(smem + 4 * W::MB);             // group-major inputs / outputs
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * W::MB + W::XB);  // [0] M, [1] X
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t t0 = int64_t(blockIdx.x) * W::PER;
+  const int n = int(a.count - t0 < W::PER ? a.count - t0 : W::PER);
+  const int q_lo = a.quad[a.order[t0]], q_hi = a.quad[a.order[t0 + n - 1]];
+  constexpr uint32_t kVB = uint32_t(W::QR * sizeof(T));
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    const uint32_t mbytes = uint32_t((q_hi - q_lo + 1) * W::MB);
+    mbar_arrive_expect_tx(&bar[0], mbytes);
+    bulk_g2s(M, reinterpret_cast<const unsigned char*>(a.MT4) + q_lo * W::MB, mbytes, &bar[0]);
+  }
+  __syncthreads();
+  if constexpr (MODE == kLvlUpSum) {
+    // X[p] = s[order p] = ordered sum of its children's T (also stored to s)
+    for (int p = warp; p < n; p += 4) {
+      const int64_t c = a.order[t0 + p];
+      const int2 kr = a.ochild[t0 + p];
+      for (int w = 4 * lane; w < W::QR; w += 128) {
+        T v[4] = {T(0), T(0), T(0), T(0)};
+        T t[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < kr.y) ld4(a.Tin + (int64_t(kr.x) + k) * W::QR + w, t[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < kr.y)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] += t[k][i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a.s[c * W::QR + w + i] = v[i];
+          X[p * W::XS + w + i] = v[i];
+        }
+      }
+    }
+  } else {
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(&bar[1], kVB * uint32_t(n));
+      __syncwarp();
+      for (int p = lane; p < n; p += 32) {
+        const int64_t g = MODE == kLvlDown ? a.opar[t0 + p] : a.order[t0 + p];
+        bulk_g2s(X + p * W::XS, (MODE == kLvlDown ? a.o : a.s) + g * W::QR, kVB, &bar[1]);
+      }
+    }
+    mbar_wait(&bar[1], 0);
+  }
+  mbar_wait(&bar[0], 0);
+  __syncthreads();
+
+  const int wr = warp % W::RW, wc = warp / W::RW;
+  const int tr = lane >> 3, tc = lane & 7;
+  const int row0 = 32 * wr + 8 * tr;
+  constexpr int NE = 4 / R;
+  const int E0 = 32 * wc / R;
+  int eq[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int e = E0 + tc + 8 * i;
+    eq[i] = e < n ? a.quad[a.order[t0 + e]] : -1;
+  }
+  T acc[8][4];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
+  if (E0 + tc < n) {
+    const T* xp = X + (E0 + tc) * W::XS;
+    for (int qd = q_lo; qd <= q_hi; ++qd) {
+      bool any = false;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) any |= eq[i] == qd;
+      if (!any) continue;
+      const T* mp = M + (qd - q_lo) * (W::MB / sizeof(T)) + row0;
+      T part[8][4];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) part[r][c] = T(0);
+#pragma unroll 4
+      for (int j = 0; j < QT; ++j) {
+        T m0[4], m1[4], x[4];
+        ld4(mp + j * QT, m0);
+        ld4(mp + j * QT + 4, m1);
+#pragma unroll
+        for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            part[r][c] = fma(m0[r], x[c], part[r][c]);
+            part[r + 4][c] = fma(m1[r], x[c], part[r + 4][c]);
+          }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (eq[c / R] == qd)
+#pragma unroll
+          for (int r = 0; r < 8; ++r) acc[r][c] = part[r][c];
+    }
+  }
+  __syncthreads();  // inputs consumed
+  if (E0 + tc < n) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int p = E0 + tc + 8 * (c / R), rr = c % R;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) X[p * W::XS + (row0 + r) * R + rr] = acc[r][c];
+    }
+  }
+  __syncthreads();
+  T* outb = MODE == kLvlDown ? a.o : a.Tout;
+  constexpr int V = 16 / int(sizeof(T));
+  constexpr int NV = W::QR / V;
+  for (int i = tid; i < n * NV; i += 128) {
+    const int p = i / NV, v = i - p * NV;
+    T* dst = outb + int64_t(a.order[t0 + p]) * W::QR + v * V;
+    if constexpr (sizeof(T) == 4) {
+      float4 val = *reinterpret_cast<const float4*>(X + p * W::XS + v * V);
+      if constexpr (MODE == kLvlDown) {
+        const float4 cur = *reinterpret_cast<const float4*>(dst);
+        val.x += cur.x; val.y += cur.y; val.z += cur.z; val.w += cur.w;
+      }
+      *reinterpret_cast<float4*>(dst) = val;
+    } else {
+      double2 val = *reinterpret_cast<const double2*>(X + p * W::XS + v * V);
+      if constexpr (MODE == kLvlDown) {
+        const double2 cur = *reinterpret_cast<const double2*>(dst);
+        val.x += cur.x; val.y += cur.y;
+      }
+      *reinterpret_cast<double2*>(dst) = val;
+    }
   }
 }
 

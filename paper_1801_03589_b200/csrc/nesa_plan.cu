@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -301,7 +302,9 @@ struct nesa_plan {
   int64_t n_red = 0;
   std::vector<DevBuf<int32_t>> down_order;  // per level (index lv-l0): children by quadrant
   std::vector<DevBuf<int32_t>> down_par;    // parents of down_order
+  std::vector<DevBuf<int2>> down_child;     // local child range of down_order entries
   int qs = 4;                               // quadrant slots staged per round
+  int64_t wide_level = 2048;                // warp-tiled level kernels from this size
 
   // workspace for R real columns
   int ws_R = 0;
@@ -452,6 +455,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   // per-level gather tables (see nesa_kernels.cuh "Level transfers")
   P->down_order.resize(nlev);
   P->down_par.resize(nlev);
+  P->down_child.resize(nlev);
   for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
     const int li = lv - P->l0;
     const int64_t cf = P->loc_first[li], cn = P->loc_count[li];
@@ -467,6 +471,26 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     for (int64_t i = 0; i < cn; ++i) par[i] = int32_t(d->parent[ord[i]]);
     P->down_order[li].upload(ord);
     P->down_par[li].upload(par);
+    // children of each ordered group, clipped to the local range of level lv+1
+    std::vector<int2> och(static_cast<size_t>(cn), int2{0, 0});
+    if (lv < P->L) {
+      std::vector<int64_t> first(static_cast<size_t>(cn), -1), cnt(static_cast<size_t>(cn), 0);
+      const int64_t lo = P->loc_first[li + 1], hi = lo + P->loc_count[li + 1];
+      std::vector<int64_t> pos(static_cast<size_t>(P->G), -1);
+      for (int64_t i = 0; i < cn; ++i) pos[ord[i]] = i;
+      for (int64_t k = lo; k < hi; ++k) {
+        const int64_t i = pos[d->parent[k]];
+        require(i >= 0, "child of a non-local parent");
+        if (first[i] < 0) first[i] = k;
+        require(k == first[i] + cnt[i], "children must be consecutive ids");
+        cnt[i]++;
+      }
+      for (int64_t i = 0; i < cn; ++i) {
+        require(cnt[i] <= 4, "more than four children");
+        och[i] = int2{int(std::max<int64_t>(first[i], 0)), int(cnt[i])};
+      }
+    }
+    P->down_child[li].upload(och);
   }
   {
     std::vector<int32_t> ids;
@@ -652,6 +676,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
 }
 
+
+
 template <typename T>
 void ensure_workspace(nesa_plan* P, int R) {
   if (P->ws_R >= R) return;
@@ -694,6 +720,9 @@ void set_smem_attrs() {
   CUDA_OK(cudaFuncSetAttribute(tgemm_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(level_wt_kernel<T, R, 64, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(level_wt_kernel<T, R, 64, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  CUDA_OK(cudaFuncSetAttribute(level_wt_kernel<T, R, 64, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
@@ -743,12 +772,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     la.quad = P->quad.p;
     la.order = P->down_order[li].p;
     la.opar = P->down_par[li].p;
-    la.child_first = P->child_first.p;
-    la.n_child = P->n_child.p;
-    if (li + 1 < int(P->loc_first.size())) {
-      la.cf_lo = P->loc_first[li + 1];
-      la.cf_hi = P->loc_first[li + 1] + P->loc_count[li + 1];
-    }
+    la.ochild = P->down_child[li].p;
     la.Tin = Tup;
     la.s = s;
     la.Tout = Tup;
@@ -766,10 +790,17 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       if (P->loc_count[ci] == 0) continue;
       const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
       const int grid = int((la.count + la.TC - 1) / la.TC);
-      if (lv == P->L)
+      if (Q == 64 && la.count >= P->wide_level) {
+        const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
+        if (lv == P->L)
+          level_wt_kernel<T, R, 64, kLvlUpLeaf><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+        else
+          level_wt_kernel<T, R, 64, kLvlUpSum><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+      } else if (lv == P->L) {
         level_kernel<T, R, kLvlUpLeaf><<<grid, kFarThreads, lvl_sm, s0>>>(la);
-      else
+      } else {
         level_kernel<T, R, kLvlUpSum><<<grid, kFarThreads, lvl_sm, s0>>>(la);
+      }
       nk++;
     }
     if (P->L > P->l0 && P->loc_count[0] > 0) {
@@ -803,8 +834,13 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       const int ci = lv - P->l0;
       if (P->loc_count[ci] == 0) continue;
       const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
-      level_kernel<T, R, kLvlDown><<<int((la.count + la.TC - 1) / la.TC), kFarThreads, lvl_sm, s0>>>(
-          la);
+      if (Q == 64 && la.count >= P->wide_level) {
+        const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
+        level_wt_kernel<T, R, 64, kLvlDown><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+      } else {
+        level_kernel<T, R, kLvlDown><<<int((la.count + la.TC - 1) / la.TC), kFarThreads, lvl_sm,
+                                       s0>>>(la);
+      }
       nk++;
     }
   };
@@ -1000,6 +1036,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->N = d->N;
     P->NL = d->n_leaves;
     P->G = d->n_groups;
+    if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     if (P->leaf_end <= P->leaf_begin) {

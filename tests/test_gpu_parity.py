@@ -173,3 +173,22 @@ def test_q64_bench_geometry_vs_oracle(dtype, tol):
     ref = oracle_mvp(tree, build_all(tree, params), q)
     qq = q if dtype == "f64" else q.astype(np.complex64)
     assert rel_l2(mvp(tree, params, qq), ref) <= tol
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_q64_wide_level_kernels(monkeypatch, dtype, tol):
+    # force the warp-tiled level kernels onto a tree the oracle can check
+    monkeypatch.setenv("NESA_WIDE_LEVEL", "32")
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=5), 40000)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    plan = NesaPlan(tree, params, dtype=dtype)
+    q = geo.random_rhs(40000, 5)
+    qq = q if dtype == "f64" else q.astype(np.complex64)
+    qd = torch.from_numpy(qq).cuda()
+    phi = torch.empty_like(qd)
+    plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 1, True,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    assert rel_l2(phi.cpu().numpy(), ref) <= tol
+    plan.close()
