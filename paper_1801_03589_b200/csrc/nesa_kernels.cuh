@@ -79,7 +79,7 @@ struct __align__(128) ChunkRec {
 };
 static_assert(sizeof(ChunkRec) == 128, "ChunkRec must be 128 bytes");
 
-constexpr int kStages = 3;
+constexpr int kStages = 3;                 // default ring depth (2 CTAs / SM)
 constexpr int kABytes = 16 * 1024;         // payload per stage
 constexpr int kMaxC = 256;                 // columns per chunk
 constexpr int kNCW = 8;                    // consumer warps
@@ -108,7 +108,7 @@ struct StageHdr {
 };
 
 // Per-stage shared memory: [A | X | header | (scatter) perm | base]
-template <typename T, int R, int MODE>
+template <typename T, int R, int MODE, int NST = kStages>
 struct BGLayout {
   static constexpr size_t kA = kABytes;
   static constexpr size_t kX = size_t(kMaxC) * R * sizeof(T);
@@ -117,16 +117,16 @@ struct BGLayout {
   static constexpr size_t kStage =
       ((kA + kX + sizeof(StageHdr) + kFinPerm + kFinBase) + 127) & ~size_t(127);
   static constexpr size_t kRed = size_t(4) * kNCT * R * sizeof(T);
-  static constexpr size_t kBytes = kStages * kStage + kRed + 2 * kStages * sizeof(uint64_t) + 16;
+  static constexpr size_t kBytes = NST * kStage + kRed + 2 * NST * sizeof(uint64_t) + 16;
   static constexpr size_t offX = kA;
   static constexpr size_t offHdr = kA + kX;
   static constexpr size_t offPerm = offHdr + sizeof(StageHdr);
   static constexpr size_t offBase = offPerm + kFinPerm;
 };
 
-template <typename T, int R, int MODE>
+template <typename T, int R, int MODE, int NST = kStages>
 constexpr size_t blockgemv_smem_bytes() {
-  return BGLayout<T, R, MODE>::kBytes;
+  return BGLayout<T, R, MODE, NST>::kBytes;
 }
 
 template <typename T, int R>
@@ -154,9 +154,10 @@ __device__ __forceinline__ void ldx(const T* p, T v[R]) {
   }
 }
 
-template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(kBGThreads, kBGPerSM) blockgemv_kernel(const BlockGemvArgs<T> a) {
-  using Lay = BGLayout<T, R, MODE>;
+template <typename T, int R, int MODE, int NST = kStages>
+__global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel(const BlockGemvArgs<T> a) {
+  using Lay = BGLayout<T, R, MODE, NST>;
+  constexpr int kStages = NST;
   extern __shared__ __align__(128) unsigned char smem[];
   T* sRed = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
   uint64_t* full = reinterpret_cast<uint64_t*>(

@@ -305,6 +305,9 @@ struct nesa_plan {
   std::vector<DevBuf<int2>> down_child;     // local child range of down_order entries
   int qs = 4;                               // quadrant slots staged per round
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
+  int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
+  bool priority = true;                     // far-field stream scheduled first
+  bool split = false;                       // fine-level translation on a side stream
 
   // workspace for R real columns
   int ws_R = 0;
@@ -312,6 +315,11 @@ struct nesa_plan {
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s2 = nullptr;                 // fine-level translation branch
+  cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
+  int split_lv = 0;                          // levels >= split_lv: translated on s2
+  int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
+  int64_t n_red_fine = 0;                    // red_ids [0, n_red_fine) are fine levels
 
   struct GraphKey {
     const void* q;
@@ -346,6 +354,9 @@ struct nesa_plan {
       for (auto e : v) cudaEventDestroy(e);
     for (auto e : cap_events)
       if (e) cudaEventDestroy(e);
+    if (ev_sfine) cudaEventDestroy(ev_sfine);
+    if (ev_tfine) cudaEventDestroy(ev_tfine);
+    if (s2) cudaStreamDestroy(s2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (s0) cudaStreamDestroy(s0);
@@ -492,11 +503,18 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     P->down_child[li].upload(och);
   }
+  // wide levels (>= split_lv) get their translation on a side stream as soon
+  // as their source amplitudes are final (see enqueue_T)
+  P->split_lv = P->L + 1;
+  for (int lv = P->L; lv >= P->l0 && P->loc_count[lv - P->l0] >= P->wide_level; --lv) P->split_lv = lv;
   {
-    std::vector<int32_t> ids;
-    for (int li = 0; li < nlev; ++li)
+    std::vector<int32_t> ids;  // fine levels first
+    for (int lv = P->L; lv >= P->l0; --lv) {
+      const int li = lv - P->l0;
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         ids.push_back(int32_t(g));
+      if (lv == P->split_lv) P->n_red_fine = int64_t(ids.size());
+    }
     P->n_red = int64_t(ids.size());
     P->red_ids.upload(ids);
   }
@@ -586,7 +604,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
   }
-  chunk_and_balance(hn, es, kBGPerSM * P->n_sm);
+  chunk_and_balance(hn, es, P->near_ctas * P->n_sm);
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
@@ -646,29 +664,35 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   {
     P->nnz = d->int_ptr[G];
     P->int_ptr.upload(std::vector<int64_t>(d->int_ptr, d->int_ptr + G + 1));
+    require(P->nnz < (int64_t(1) << 31), "too many interaction entries");
+    const int per = kTUnitPasses * (tg_geom(Q).NC / 4);  // sized for R = 4; smaller R packs more
+    std::vector<TEnt> ents;
+    std::vector<TUnit> units;
     std::vector<std::vector<TEnt>> by_d(size_t(std::max<int64_t>(d->n_dtab, 1)));
-    for (int lv = P->l0; lv <= P->L; ++lv) {
+    // levels fine -> coarse; within a level grouped by unique D
+    for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
+      std::vector<int64_t> used;
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
           const int64_t dt = d->int_dtab[e];
           require(dt >= 0 && dt < d->n_dtab, "D index out of range");
           require(d->int_idx[e] >= 0 && d->int_idx[e] < G, "interaction id out of range");
+          if (by_d[dt].empty()) used.push_back(dt);
           by_d[dt].push_back(TEnt{int32_t(d->int_idx[e]), int32_t(e)});
         }
-    }
-    require(P->nnz < (int64_t(1) << 31), "too many interaction entries");
-    const int per = kTUnitPasses * (tg_geom(Q).NC / 4);  // sized for R = 4; smaller R packs more
-    std::vector<TEnt> ents;
-    std::vector<TUnit> units;
-    for (int64_t dt = 0; dt < d->n_dtab; ++dt) {
-      const auto& v = by_d[dt];
-      for (size_t i = 0; i < v.size(); i += size_t(per)) {
-        const size_t j = std::min(v.size(), i + size_t(per));
-        units.push_back(TUnit{int32_t(dt), int32_t(ents.size()), int32_t(ents.size() + (j - i)), 0});
-        ents.insert(ents.end(), v.begin() + i, v.begin() + j);
+      std::sort(used.begin(), used.end());
+      for (int64_t dt : used) {
+        auto& v = by_d[dt];
+        for (size_t i = 0; i < v.size(); i += size_t(per)) {
+          const size_t j = std::min(v.size(), i + size_t(per));
+          units.push_back(TUnit{int32_t(dt), int32_t(ents.size()), int32_t(ents.size() + (j - i)), 0});
+          ents.insert(ents.end(), v.begin() + i, v.begin() + j);
+        }
+        P->d_refs += int64_t(v.size());
+        v.clear();
       }
-      P->d_refs += int64_t(v.size());
+      if (lv == P->split_lv) P->n_tunits_fine = int(units.size());
     }
     P->tunits.upload(units);
     P->tents.upload(ents);
@@ -695,15 +719,15 @@ inline int grid_for(int64_t n, int threads, int cap) {
   return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap)));
 }
 
-template <typename T, int R, int MODE>
+template <typename T, int R, int MODE, int NST = kStages>
 void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
                       int64_t perm_offset, cudaStream_t st) {
   if (bs.n_items == 0) return;
   BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p, x, y, base,
                      perm};
   (void)perm_offset;
-  constexpr size_t sm = blockgemv_smem_bytes<T, R, MODE>();
-  blockgemv_kernel<T, R, MODE><<<bs.grid, kBGThreads, sm, st>>>(a);
+  constexpr size_t sm = blockgemv_smem_bytes<T, R, MODE, NST>();
+  blockgemv_kernel<T, R, MODE, NST><<<bs.grid, kBGThreads, sm, st>>>(a);
 }
 
 template <typename T, int R>
@@ -716,6 +740,9 @@ void set_smem_attrs() {
   CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeScatter>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(blockgemv_smem_bytes<T, R, kModeScatter>())));
+  CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeStore, 6>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(blockgemv_smem_bytes<T, R, kModeStore, 6>())));
   const int lim = 220 * 1024;
   CUDA_OK(cudaFuncSetAttribute(tgemm_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
@@ -783,26 +810,26 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     la.TC = tile_for(la.count);
     return la;
   };
-  auto up_pass = [&]() {
+  auto up_level = [&](int lv) {
     // children-major: T[c] = C s[c]; s[parent] = sum of its children's T
-    for (int lv = P->L; lv > P->l0; --lv) {
-      const int ci = lv - P->l0;
-      if (P->loc_count[ci] == 0) continue;
-      const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
-      const int grid = int((la.count + la.TC - 1) / la.TC);
-      if (Q == 64 && la.count >= P->wide_level) {
-        const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-        if (lv == P->L)
-          level_wt_kernel<T, R, 64, kLvlUpLeaf><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
-        else
-          level_wt_kernel<T, R, 64, kLvlUpSum><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
-      } else if (lv == P->L) {
-        level_kernel<T, R, kLvlUpLeaf><<<grid, kFarThreads, lvl_sm, s0>>>(la);
-      } else {
-        level_kernel<T, R, kLvlUpSum><<<grid, kFarThreads, lvl_sm, s0>>>(la);
-      }
-      nk++;
+    const int ci = lv - P->l0;
+    if (P->loc_count[ci] == 0) return;
+    const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
+    const int grid = int((la.count + la.TC - 1) / la.TC);
+    if (Q == 64 && la.count >= P->wide_level) {
+      const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
+      if (lv == P->L)
+        level_wt_kernel<T, R, 64, kLvlUpLeaf><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+      else
+        level_wt_kernel<T, R, 64, kLvlUpSum><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+    } else if (lv == P->L) {
+      level_kernel<T, R, kLvlUpLeaf><<<grid, kFarThreads, lvl_sm, s0>>>(la);
+    } else {
+      level_kernel<T, R, kLvlUpSum><<<grid, kFarThreads, lvl_sm, s0>>>(la);
     }
+    nk++;
+  };
+  auto top_sum = [&]() {
     if (P->L > P->l0 && P->loc_count[0] > 0) {
       const int64_t n = P->loc_count[0] * Q * R;
       sum_children_kernel<T, R><<<grid_for(n, 256, cap), 256, 0, s0>>>(
@@ -811,38 +838,81 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       nk++;
     }
   };
-  auto down_pass = [&]() {
-    T* Y = reinterpret_cast<T*>(P->Y.p);
-    if (P->n_tunits > 0) {
-      const T* DTp = reinterpret_cast<const T*>(P->DT.p);
-      if (Q == 64)
-        tgemm_wt_kernel<T, R, 64><<<P->n_tunits, 128, TGW<T, R, 64>::SMEM, s0>>>(
-            P->tunits.p, P->tents.p, DTp, s, Y);
-      else if (Q == 32)
-        tgemm_wt_kernel<T, R, 32><<<P->n_tunits, 128, TGW<T, R, 32>::SMEM, s0>>>(
-            P->tunits.p, P->tents.p, DTp, s, Y);
-      else
-        tgemm_kernel<T, R><<<P->n_tunits, kTGThreads, tgemm_smem_bytes<T, R>(Q), s0>>>(
-            P->tunits.p, P->tents.p, DTp, s, Y, Q);
-      nk++;
-    }
-    // o[g] = translation sum of every local group (all levels, one launch)
-    reduce_kernel<T, R><<<grid_for(P->n_red * 32, 256, cap), 256, 0, s0>>>(
-        P->red_ids.p, P->n_red, P->int_ptr.p, Y, o, Q);
+  T* Y = reinterpret_cast<T*>(P->Y.p);
+  auto translate = [&](int u0, int u1, cudaStream_t st) {
+    if (u1 <= u0) return;
+    const T* DTp = reinterpret_cast<const T*>(P->DT.p);
+    const TUnit* up = P->tunits.p + u0;
+    if (Q == 64)
+      tgemm_wt_kernel<T, R, 64><<<u1 - u0, 128, TGW<T, R, 64>::SMEM, st>>>(up, P->tents.p, DTp, s, Y);
+    else if (Q == 32)
+      tgemm_wt_kernel<T, R, 32><<<u1 - u0, 128, TGW<T, R, 32>::SMEM, st>>>(up, P->tents.p, DTp, s, Y);
+    else
+      tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp,
+                                                                                s, Y, Q);
     nk++;
-    for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
-      const int ci = lv - P->l0;
-      if (P->loc_count[ci] == 0) continue;
-      const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
-      if (Q == 64 && la.count >= P->wide_level) {
-        const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-        level_wt_kernel<T, R, 64, kLvlDown><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
-      } else {
-        level_kernel<T, R, kLvlDown><<<int((la.count + la.TC - 1) / la.TC), kFarThreads, lvl_sm,
-                                       s0>>>(la);
-      }
-      nk++;
+  };
+  auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st) {
+    // o[g] = translation sum of the listed local groups
+    if (i1 <= i0) return;
+    reduce_kernel<T, R><<<grid_for((i1 - i0) * 32, 256, cap), 256, 0, st>>>(
+        P->red_ids.p + i0, i1 - i0, P->int_ptr.p, Y, o, Q);
+    nk++;
+  };
+  auto down_level = [&](int lv) {
+    const int ci = lv - P->l0;
+    if (P->loc_count[ci] == 0) return;
+    const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
+    if (Q == 64 && la.count >= P->wide_level) {
+      const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
+      level_wt_kernel<T, R, 64, kLvlDown><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+    } else {
+      level_kernel<T, R, kLvlDown><<<int((la.count + la.TC - 1) / la.TC), kFarThreads, lvl_sm, s0>>>(
+          la);
     }
+    nk++;
+  };
+  // Far field.  The wide (fine) levels' translation + reduce run on s2 as
+  // soon as their s is final, concurrently with the coarse end of the
+  // upward chain, the coarse translations and the coarse downward levels.
+  auto far_pass = [&](bool split) {
+    const bool fine = split && P->split_lv <= P->L;
+    for (int lv = P->L; lv > P->l0; --lv) {
+      up_level(lv);
+      if (fine && lv == P->split_lv) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+    }
+    if (P->L == P->split_lv && fine && P->L == P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+    top_sum();
+    if (fine && P->split_lv == P->l0 && P->L > P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+    if (fine) {
+      CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
+      translate(0, P->n_tunits_fine, P->s2);
+      reduce(0, P->n_red_fine, P->s2);
+      CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
+      translate(P->n_tunits_fine, P->n_tunits, s0);
+      reduce(P->n_red_fine, P->n_red, s0);
+    } else {
+      translate(0, P->n_tunits, s0);
+      reduce(0, P->n_red, s0);
+    }
+    bool joined = !fine;
+    for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
+      if (!joined && lv >= P->split_lv) {
+        CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
+        joined = true;
+      }
+      down_level(lv);
+    }
+    if (!joined) CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
+  };
+  auto up_pass = [&]() {
+    for (int lv = P->L; lv > P->l0; --lv) up_level(lv);
+    top_sum();
+  };
+  auto down_pass = [&]() {
+    translate(0, P->n_tunits, s0);
+    reduce(0, P->n_red, s0);
+    for (int lv = P->l0 + 1; lv <= P->L; ++lv) down_level(lv);
   };
   auto gather = [&]() {
     gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N);
@@ -879,13 +949,15 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
     if (near) {
       prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
-      launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
+      if (P->near_ctas == 1)
+        launch_blockgemv<T, R, kModeStore, 6>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
+      else
+        launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       nk++;
       prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
     }
     if (far) {
-      up_pass();
-      down_pass();
+      far_pass(P->split);
       prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
     }
     CUDA_OK(cudaEventRecord(P->ev_join, s1));
@@ -1037,6 +1109,9 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->NL = d->n_leaves;
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
+    if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
+    if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
+    if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     if (P->leaf_end <= P->leaf_begin) {
@@ -1055,8 +1130,16 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       build_plan_T<double>(P.get(), d);
     else
       build_plan_T<float>(P.get(), d);
-    CUDA_OK(cudaStreamCreateWithFlags(&P->s0, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamCreateWithFlags(&P->s1, cudaStreamNonBlocking));
+    {
+      int lo = 0;  // numerically lower = higher priority
+      int hi = 0;
+      CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s0, cudaStreamNonBlocking, P->priority ? hi : lo));
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s1, cudaStreamNonBlocking, lo));
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, P->priority ? hi : lo));
+    }
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_sfine, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_tfine, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
     for (auto& e : P->cap_events) CUDA_OK(cudaEventCreate(&e));
