@@ -192,3 +192,44 @@ def test_q64_wide_level_kernels(monkeypatch, dtype, tol):
     ref = oracle_mvp(tree, build_all(tree, params), q)
     assert rel_l2(phi.cpu().numpy(), ref) <= tol
     plan.close()
+
+
+@pytest.mark.parametrize("world,dtype,tol", [(2, "f64", 1e-12), (3, "f32", 1e-5)])
+def test_subplans_with_exchange_on_one_gpu(world, dtype, tol):
+    # the multi-GPU path's kernels: per-rank sub-plans (leaf ranges, partial
+    # upward sums, stage 1 / stage 2 graphs) run one after another on one
+    # device; the all_gather is a concatenation of the ranks' send buffers
+    from paper_1801_03589_b200.dist import (build_exchange, combine_s, exchange_tensors, pack_s,
+                                            partition_leaves)
+    from paper_1801_03589_b200.dist import _tensor_from_ptr
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=2), 20000)
+    tree = build_tree(pts, TreeParams(P=32))
+    params = NesaParams(Q=24)
+    ranges = partition_leaves(tree, world, params.Q)
+    q = geo.random_rhs(20000, 2)
+    cdt = np.complex128 if dtype == "f64" else np.complex64
+    qd = torch.from_numpy(q.astype(cdt)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    plans, phis, xps, tens, svs = [], [], [], [], []
+    G = tree.arrays.n_groups
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    for r in range(world):
+        p = NesaPlan(tree, params, dtype=dtype, leaf_range=ranges[r])
+        phi = torch.zeros_like(qd)
+        p.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 1, True, stream=st, stage=1)
+        sv = _tensor_from_ptr(p.s_dev_ptr(2), (G, params.Q * 2), tdt, 0)
+        xp = build_exchange(tree, ranges, r)
+        plans.append(p), phis.append(phi), xps.append(xp), svs.append(sv)
+        tens.append(exchange_tensors(xp, sv.device))
+    sends = [pack_s(svs[r], xps[r], tens[r]) for r in range(world)]
+    recv = torch.cat(sends, 0)
+    for r in range(world):
+        combine_s(svs[r], xps[r], recv, tens[r])
+    total = torch.zeros_like(qd)
+    for r in range(world):
+        plans[r].matvec_ptr(qd.data_ptr(), phis[r].data_ptr(), 1, True, stream=st, stage=2)
+        total += phis[r]
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    assert rel_l2(total.cpu().numpy(), ref) <= tol
+    for p in plans:
+        p.close()
