@@ -134,16 +134,22 @@ def mvp(tree, ops, q, runtime=None, vec=None, near: bool = True, far: bool = Tru
     tdt = {("f64", False): torch.float64, ("f64", True): torch.complex128,
            ("f32", False): torch.float32, ("f32", True): torch.complex64}[(dtype, is_complex)]
     with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        on_host = (not is_torch) or not q.is_cuda
         if is_torch:
-            qd = q.to(device=f"cuda:{dev}", dtype=tdt).contiguous()
+            qd = q.to(device=f"cuda:{dev}", dtype=tdt, non_blocking=True).contiguous()
         else:
             qd = torch.from_numpy(np.ascontiguousarray(q)).to(f"cuda:{dev}", dtype=tdt)
         phi = torch.empty_like(qd)
-        stream = torch.cuda.current_stream(dev)
         plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), nrhs, is_complex, near=near, far=far,
                         stream=stream.cuda_stream)
-        if is_torch:
+        if not on_host:
             return phi
+        if is_torch:        # CPU tensor in -> CPU tensor out (pinned if the input was)
+            out = torch.empty(phi.shape, dtype=phi.dtype, pin_memory=q.is_pinned())
+            out.copy_(phi, non_blocking=True)
+            stream.synchronize()
+            return out
         return phi.cpu().numpy()
 
 

@@ -233,3 +233,12 @@ def test_subplans_with_exchange_on_one_gpu(world, dtype, tol):
     assert rel_l2(total.cpu().numpy(), ref) <= tol
     for p in plans:
         p.close()
+
+
+def test_pinned_host_tensor_roundtrip(golden):
+    g = golden("c1_circle_2000")
+    tree, params = _problem(g)
+    qh = torch.from_numpy(g["q"].astype(np.complex64)).pin_memory()
+    phi = mvp(tree, params, qh)
+    assert not phi.is_cuda and phi.is_pinned() and phi.dtype == torch.complex64
+    assert rel_l2(phi.numpy(), g["phi"]) <= 1e-5
