@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
   if (warp == kNCW) {
     // ------------------------------ producer ------------------------------
     const int32_t* recw = reinterpret_cast<const int32_t*>(a.recs);
+    const uint64_t pol = l2_evict_first_policy();
     int32_t w_next = c0 < c1 ? __ldg(recw + int64_t(c0) * 32 + lane) : 0;
     for (int i = c0; i < c1; ++i) {
       const int32_t w = w_next;
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
         h->magic = magic;
         h->CL = CLv;
         mbar_arrive_expect_tx(&full[st], bytes);
-        bulk_g2s(stg, a.blob + src_off, bytes, &full[st]);
+        bulk_g2s_hint(stg, a.blob + src_off, bytes, &full[st], pol);
       }
       T* xs = reinterpret_cast<T*>(stg + Lay::offX);
       for (int sg = 0; sg < nseg; ++sg) {

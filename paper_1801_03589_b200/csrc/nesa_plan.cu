@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -308,6 +309,8 @@ struct nesa_plan {
   int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
   bool priority = true;                     // far-field stream scheduled first
   bool split = false;                       // fine-level translation on a side stream
+  int near_after = 1;                       // where the near branch forks (see enqueue_T)
+  cudaEvent_t ev_mark = nullptr;            // no-op event-record node ahead of the near kernel
 
   // workspace for R real columns
   int ws_R = 0;
@@ -355,6 +358,7 @@ struct nesa_plan {
     for (auto e : cap_events)
       if (e) cudaEventDestroy(e);
     if (ev_sfine) cudaEventDestroy(ev_sfine);
+    if (ev_mark) cudaEventDestroy(ev_mark);
     if (ev_tfine) cudaEventDestroy(ev_tfine);
     if (s2) cudaStreamDestroy(s2);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -875,14 +879,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   // Far field.  The wide (fine) levels' translation + reduce run on s2 as
   // soon as their s is final, concurrently with the coarse end of the
   // upward chain, the coarse translations and the coarse downward levels.
-  auto far_pass = [&](bool split) {
+  auto far_pass = [&](bool split, const std::function<void(int)>& hook) {
     const bool fine = split && P->split_lv <= P->L;
     for (int lv = P->L; lv > P->l0; --lv) {
       up_level(lv);
+      if (lv == P->L) hook(2);
       if (fine && lv == P->split_lv) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     }
     if (P->L == P->split_lv && fine && P->L == P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     top_sum();
+    hook(3);
     if (fine && P->split_lv == P->l0 && P->L > P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     if (fine) {
       CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
@@ -895,6 +901,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       translate(0, P->n_tunits, s0);
       reduce(0, P->n_red, s0);
     }
+    hook(4);
     bool joined = !fine;
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
       if (!joined && lv >= P->split_lv) {
@@ -945,19 +952,35 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
       nk++;
     }
-    CUDA_OK(cudaEventRecord(P->ev_fork, s0));
-    CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
-    if (near) {
-      prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
+    // Near branch: forks from s0 at position `near_after` (0/1: after
+    // radiation, 1 adds a no-op event node so the first far-field kernel is
+    // launched -- and resident -- before the persistent near-field CTAs;
+    // 2: after the leaf-level upward kernel; 3: after the upward pass;
+    // 4: after translation).
+    bool forked = false;
+    auto launch_near = [&]() {
+      if (forked) return;
+      forked = true;
+      CUDA_OK(cudaEventRecord(P->ev_fork, s0));
+      CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
+      if (!near) return;
+      if (prof)
+        prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
+      else if (P->near_after == 1)
+        CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
       if (P->near_ctas == 1)
         launch_blockgemv<T, R, kModeStore, 6>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       else
         launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       nk++;
       prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
-    }
+    };
+    if (!far || P->near_after <= 1) launch_near();
     if (far) {
-      far_pass(P->split);
+      far_pass(P->split, [&](int pos) {
+        if (pos == P->near_after) launch_near();
+      });
+      launch_near();
       prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
     }
     CUDA_OK(cudaEventRecord(P->ev_join, s1));
@@ -1112,6 +1135,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
+    if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     if (P->leaf_end <= P->leaf_begin) {
@@ -1139,6 +1163,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       CUDA_OK(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, P->priority ? hi : lo));
     }
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_sfine, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_mark, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_tfine, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));

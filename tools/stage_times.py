@@ -28,18 +28,21 @@ def main():
     q = torch.from_numpy(nesa.random_rhs(a.n, 3).astype(cdt)).cuda()
     phi = torch.empty_like(q)
     st = torch.cuda.current_stream()
-    for name, near, far in (("full", True, True), ("near", True, False), ("far", False, True)):
+    for name, near, far, prof in (("full", True, True, False), ("full+prof", True, True, True),
+                                  ("near", True, False, False), ("far", False, True, False)):
         for _ in range(10):
             plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, near=near, far=far,
-                            stream=st.cuda_stream)
+                            stream=st.cuda_stream, profile=prof)
+        if prof:
+            plan.profile_reset()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for _ in range(a.reps):
             plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, near=near, far=far,
-                            stream=st.cuda_stream)
+                            stream=st.cuda_stream, profile=prof)
         e1.record(st)
         e1.synchronize()
-        print(f"{name:5s} {e0.elapsed_time(e1) / a.reps * 1e3:8.1f} us  "
+        print(f"{name:9s} {e0.elapsed_time(e1) / a.reps * 1e3:8.1f} us  "
               f"(NESA_WIDE_LEVEL={os.environ.get('NESA_WIDE_LEVEL', '2048')})")
 
 
