@@ -1196,4 +1196,55 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
   }
 }
 
+// ----------------------------------------------------------------------------
+// Matrix-free reception (float32 plans):
+//   phi[perm i] = phin[i] + sum_k -0.5 log|p_i - a_k|^2 o[leaf i][k]
+// with the incoming aux circle a_k = c + r (cos, sin)(2 pi k / Q) of the
+// point's leaf (operators.py:147-149 builds U = kernel_matrix(pts, in_aux)).
+// Evaluated from leaf-relative coordinates p_i - c (the aux circle lies
+// >= 1.38 h from every point of the leaf, so float32 loses nothing that
+// matters at the 1e-5 tolerance), log via MUFU lg2, scaled once.  Streams
+// ~36 bytes per point instead of the 4Q-byte stored row of U.
+// ----------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(128) reception_mf_kernel(
+    const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
+    const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
+    const float2* __restrict__ unit_circle, const float* __restrict__ o,
+    const float* __restrict__ phin, const int64_t* __restrict__ perm, float* __restrict__ phi,
+    int64_t leaf0, int Q) {
+  // one CTA per leaf: its aux circle and incoming amplitudes live in smem
+  extern __shared__ float4 sm4[];
+  float2* aux = reinterpret_cast<float2*>(sm4);        // Q relative aux points
+  float* os = reinterpret_cast<float*>(aux + Q);       // Q * R amplitudes
+  const int64_t leaf = leaf0 + blockIdx.x;
+  const float r = leaf_r[leaf];
+  for (int k = threadIdx.x; k < Q; k += blockDim.x) {
+    const float2 c = unit_circle[k];
+    aux[k] = make_float2(r * c.x, r * c.y);
+  }
+  for (int k = threadIdx.x; k < Q * R; k += blockDim.x) os[k] = o[leaf * Q * R + k];
+  __syncthreads();
+  const int64_t b = leaf_start[leaf], e = leaf_stop[leaf];
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    const float2 p = prel[i];
+    float acc[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) acc[rr] = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < Q; ++k) {
+      const float2 a = aux[k];
+      const float dx = p.x - a.x, dy = p.y - a.y;
+      const float l2 = __log2f(fmaf(dx, dx, dy * dy));
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(l2, os[k * R + rr], acc[rr]);
+    }
+    constexpr float kScale = -0.5f * 0.69314718055994531f;  // -0.5 ln 2
+    const int64_t dst = perm[i];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr)
+      phi[dst * R + rr] = (phin ? phin[i * R + rr] : 0.f) + kScale * acc[rr];
+  }
+}
+
 }  // namespace nesa

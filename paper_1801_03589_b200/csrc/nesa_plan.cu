@@ -21,6 +21,7 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/nesa_b200.h"
@@ -310,6 +311,11 @@ struct nesa_plan {
   bool priority = true;                     // far-field stream scheduled first
   bool split = false;                       // fine-level translation on a side stream
   int near_after = 1;                       // where the near branch forks (see enqueue_T)
+  bool u_mf = false;                        // matrix-free reception (float32 plans)
+  DevBuf<float2> mf_prel;                   // [N] point - leaf center (float32)
+  DevBuf<int64_t> gstart, gstop;            // [NL] leaf point ranges
+  DevBuf<float> mf_leaf_r;                  // [NL] rho_in_aux * half side
+  DevBuf<float2> mf_circle;                 // [Q] unit circle (cos, sin)
   cudaEvent_t ev_mark = nullptr;            // no-op event-record node ahead of the near kernel
 
   // workspace for R real columns
@@ -584,8 +590,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           hv.blob_elems += int64_t(ld) * na;
           hv.entries += int64_t(Q) * na;
         }
-        // U: na x Q, x = o rows of leaf a, y = phi rows
-        {
+        // U: na x Q, x = o rows of leaf a, y = phi rows (stored mode only)
+        if (!P->u_mf) {
           const int32_t sb = int32_t(hu.segs.size());
           hu.segs.push_back(BlockSeg{int32_t(a * Q), 0});
           for (int64_t r0 = 0; r0 < na; r0 += kMaxRows) {
@@ -655,7 +661,26 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         P->Vset.items.p, vleaf.p, pts.p, center.p, rck.p, fit.p, cc.p, cs.p, Q, P->n_check, vblob);
     CUDA_OK(cudaGetLastError());
   }
-  if (d->U_blob) {
+  if (P->u_mf) {
+    // matrix-free reception inputs: leaf-relative float32 coordinates
+    std::vector<float2> prel(static_cast<size_t>(P->N));
+
+    std::vector<float> lr(static_cast<size_t>(NL));
+    for (int64_t a = 0; a < NL; ++a) {
+      const double cx = d->leaf_center[2 * a], cy = d->leaf_center[2 * a + 1];
+      lr[a] = float(d->leaf_r_inaux[a]);
+      for (int64_t i = d->group_start[a]; i < d->group_stop[a]; ++i) {
+        prel[i] = float2{float(d->points_tree[2 * i] - cx), float(d->points_tree[2 * i + 1] - cy)};
+      }
+    }
+    std::vector<float2> circ(static_cast<size_t>(Q));
+    for (int k = 0; k < Q; ++k) circ[k] = float2{float(d->aux_cos[k]), float(d->aux_sin[k])};
+    P->mf_prel.upload(prel);
+    P->gstart.upload(std::vector<int64_t>(d->group_start, d->group_start + NL));
+    P->gstop.upload(std::vector<int64_t>(d->group_stop, d->group_stop + NL));
+    P->mf_leaf_r.upload(lr);
+    P->mf_circle.upload(circ);
+  } else if (d->U_blob) {
     upload_host_blob<T>(P->Uset, hu, d->U_blob, u_src_off, u_src_rows, u_row0);
   } else if (!hu.items.empty()) {
     assemble_U_kernel<T><<<int(hu.items.size()), 256>>>(P->Uset.items.p, uleaf.p, pts.p, center.p,
@@ -927,7 +952,15 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   };
   auto finish = [&]() {
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
-    if (far) {
+    if (far && P->u_mf) {
+      if constexpr (std::is_same<T, float>::value) {
+        const size_t sm = size_t(Q) * (sizeof(float2) + R * sizeof(float));
+        reception_mf_kernel<R><<<int(P->leaf_end - P->leaf_begin), 128, sm, s0>>>(
+            P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->mf_circle.p, o,
+            near ? phin : nullptr, P->perm.p, phi, P->leaf_begin, Q);
+      }
+      nk++;
+    } else if (far) {
       launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p, 0,
                                            s0);
       nk++;
@@ -1136,6 +1169,8 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
+    P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
+    if (const char* us = std::getenv("NESA_U_STORED")) P->u_mf = P->u_mf && std::atoi(us) == 0;
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     if (P->leaf_end <= P->leaf_begin) {
