@@ -532,6 +532,8 @@ __global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R
              bar);
   }
   __syncthreads();  // barrier initialised before anyone waits on it
+  pdl_trigger();
+  pdl_wait();       // inputs below come from the previous kernel in the chain
   // ---- stage the input amplitudes, one warp per column group
   if constexpr (MODE == kLvlUpSum) {
     // s[c] = ordered sum of <= 4 children's T: all child loads in flight
@@ -671,6 +673,8 @@ __global__ void sum_children_kernel(const int64_t* __restrict__ child_first,
                                     const int32_t* __restrict__ n_child, int64_t first,
                                     int64_t count, int64_t cf_lo, int64_t cf_hi,
                                     const T* __restrict__ Tin, T* s, int Q) {
+  pdl_trigger();
+  pdl_wait();
   const int QR = Q * R;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count * QR;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -689,6 +693,8 @@ template <typename T, int R>
 __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
                               const int64_t* __restrict__ int_ptr, const T* __restrict__ Y, T* o,
                               int Q) {
+  pdl_trigger();
+  pdl_wait();
   const int QR = Q * R;
   const int lane = threadIdx.x & 31;
   const bool vec = (QR % 4) == 0;
@@ -840,6 +846,8 @@ __global__ void __launch_bounds__(kTGThreads) tgemm_kernel(const TUnit* __restri
              &bar[0]);
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();
   const int n_all = u.ent_end - u.ent_begin;
   const int npass = (n_all + per - 1) / per;
   tgemm_stage<T, R>(ents, u.ent_begin, min(per, n_all), s, G, Xb[0], XS, Eb[0], &bar[1], tid);
@@ -963,6 +971,8 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
              &bar[0]);
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // s comes from the upward pass
   auto stage = [&](int eb, int n, T* X, int32_t* eid, uint64_t* b) {
     if (warp == 0) {
       if (lane == 0) mbar_arrive_expect_tx(b, kVB * uint32_t(n));
@@ -1074,6 +1084,8 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
     bulk_g2s(M, reinterpret_cast<const unsigned char*>(a.MT4) + q_lo * W::MB, mbytes, &bar[0]);
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // amplitudes come from the previous kernel in the chain
   if constexpr (MODE == kLvlUpSum) {
     // X[p] = s[order p] = ordered sum of its children's T (also stored to s)
     for (int p = warp; p < n; p += 4) {

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <utility>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -312,6 +313,7 @@ struct nesa_plan {
   bool split = false;                       // fine-level translation on a side stream
   int near_after = 1;                       // where the near branch forks (see enqueue_T)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
+  bool pdl = true;                          // programmatic dependent launch in the far chain
   DevBuf<float2> mf_prel;                   // [N] point - leaf center (float32)
   DevBuf<int64_t> gstart, gstop;            // [NL] leaf point ranges
   DevBuf<float> mf_leaf_r;                  // [NL] rho_in_aux * half side
@@ -793,6 +795,25 @@ void prof_mark(nesa_plan* P, bool profile, int slot, cudaStream_t st) {
   CUDA_OK(cudaEventRecordWithFlags(P->cap_events[slot], st, cudaEventRecordExternal));
 }
 
+// Launch with programmatic dependent launch (PDL): the kernel may start its
+// prologue while the previous kernel of the stream drains; it calls
+// pdl_wait() before touching that kernel's outputs.
+template <typename... KArgs, typename... Args>
+void launch_pdl(bool pdl, void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // Enqueue one product, or one of its two stages (multi-GPU), on P->s0/P->s1.
 //   stage 0: gather, fork{near | V, up, translate, down}, join, reception
 //   stage 1: gather, V, up                  (before the s halo exchange)
@@ -848,22 +869,23 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
       if (lv == P->L)
-        level_wt_kernel<T, R, 64, kLvlUpLeaf><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64>::SMEM, s0, la);
       else
-        level_wt_kernel<T, R, 64, kLvlUpSum><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64>::SMEM, s0, la);
     } else if (lv == P->L) {
-      level_kernel<T, R, kLvlUpLeaf><<<grid, kFarThreads, lvl_sm, s0>>>(la);
+      launch_pdl(P->pdl, level_kernel<T, R, kLvlUpLeaf>, grid, kFarThreads, lvl_sm, s0, la);
     } else {
-      level_kernel<T, R, kLvlUpSum><<<grid, kFarThreads, lvl_sm, s0>>>(la);
+      launch_pdl(P->pdl, level_kernel<T, R, kLvlUpSum>, grid, kFarThreads, lvl_sm, s0, la);
     }
     nk++;
   };
   auto top_sum = [&]() {
     if (P->L > P->l0 && P->loc_count[0] > 0) {
       const int64_t n = P->loc_count[0] * Q * R;
-      sum_children_kernel<T, R><<<grid_for(n, 256, cap), 256, 0, s0>>>(
-          P->child_first.p, P->n_child.p, P->loc_first[0], P->loc_count[0], P->loc_first[1],
-          P->loc_first[1] + P->loc_count[1], Tup, s, Q);
+      launch_pdl(P->pdl, sum_children_kernel<T, R>, grid_for(n, 256, cap), 256, 0, s0,
+                 (const int64_t*)P->child_first.p, (const int32_t*)P->n_child.p, P->loc_first[0],
+                 P->loc_count[0], P->loc_first[1], P->loc_first[1] + P->loc_count[1],
+                 (const T*)Tup, s, Q);
       nk++;
     }
   };
@@ -873,9 +895,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const T* DTp = reinterpret_cast<const T*>(P->DT.p);
     const TUnit* up = P->tunits.p + u0;
     if (Q == 64)
-      tgemm_wt_kernel<T, R, 64><<<u1 - u0, 128, TGW<T, R, 64>::SMEM, st>>>(up, P->tents.p, DTp, s, Y);
+      launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 64>, u1 - u0, 128, TGW<T, R, 64>::SMEM, st,
+                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y);
     else if (Q == 32)
-      tgemm_wt_kernel<T, R, 32><<<u1 - u0, 128, TGW<T, R, 32>::SMEM, st>>>(up, P->tents.p, DTp, s, Y);
+      launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 32>, u1 - u0, 128, TGW<T, R, 32>::SMEM, st,
+                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y);
     else
       tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp,
                                                                                 s, Y, Q);
@@ -884,8 +908,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st) {
     // o[g] = translation sum of the listed local groups
     if (i1 <= i0) return;
-    reduce_kernel<T, R><<<grid_for((i1 - i0) * 32, 256, cap), 256, 0, st>>>(
-        P->red_ids.p + i0, i1 - i0, P->int_ptr.p, Y, o, Q);
+    launch_pdl(P->pdl && st == s0, reduce_kernel<T, R>, grid_for((i1 - i0) * 32, 256, cap), 256, 0,
+               st, (const int32_t*)(P->red_ids.p + i0), i1 - i0, (const int64_t*)P->int_ptr.p,
+               (const T*)Y, o, Q);
     nk++;
   };
   auto down_level = [&](int lv) {
@@ -894,10 +919,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-      level_wt_kernel<T, R, 64, kLvlDown><<<gw, 128, LVW<T, R, 64>::SMEM, s0>>>(la);
+      launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64>::SMEM, s0, la);
     } else {
-      level_kernel<T, R, kLvlDown><<<int((la.count + la.TC - 1) / la.TC), kFarThreads, lvl_sm, s0>>>(
-          la);
+      launch_pdl(P->pdl, level_kernel<T, R, kLvlDown>, int((la.count + la.TC - 1) / la.TC),
+                 kFarThreads, lvl_sm, s0, la);
     }
     nk++;
   };
@@ -1169,6 +1194,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
+    if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
     P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
     if (const char* us = std::getenv("NESA_U_STORED")) P->u_mf = P->u_mf && std::atoi(us) == 0;
     P->leaf_begin = d->leaf_begin;
