@@ -99,6 +99,7 @@ struct BlockGemvArgs {
   T* y;                          // store: y rows; scatter: output in original order
   const T* base;                 // scatter: added per tree row (may be null)
   const int64_t* perm;           // scatter: tree row -> original row
+  int ldy;                       // scatter: row stride of y (elements)
 };
 
 struct StageHdr {
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
             const int64_t dst = sperm[row];
 #pragma unroll
             for (int rr = 0; rr < R; ++rr)
-              a.y[dst * R + rr] = (a.base ? sbase[row * R + rr] : T(0)) + v[rr];
+              a.y[dst * a.ldy + rr] = (a.base ? sbase[row * R + rr] : T(0)) + v[rr];
           }
         }
         __syncwarp();
@@ -320,23 +321,24 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
 // ----------------------------------------------------------------------------
 template <typename T, int R>
 __global__ void gather_kernel(const T* __restrict__ q, const int64_t* __restrict__ perm,
-                              T* __restrict__ qt, int64_t n) {
+                              T* __restrict__ qt, int64_t n, int ldq) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = perm[i];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) qt[i * R + rr] = q[j * R + rr];
+    for (int rr = 0; rr < R; ++rr) qt[i * R + rr] = q[j * ldq + rr];
   }
 }
 
+// phi[perm[i]] = phin[i] (phin == nullptr: zeros), phi rows of stride ldp
 template <typename T, int R>
 __global__ void scatter_kernel(const T* __restrict__ phin, const int64_t* __restrict__ perm,
-                               T* __restrict__ phi, int64_t row0, int64_t n) {
+                               T* __restrict__ phi, int64_t row0, int64_t n, int ldp) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = perm[i];
+    const int64_t j = perm[row0 + i];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) phi[j * R + rr] = phin[(row0 + i) * R + rr];
+    for (int rr = 0; rr < R; ++rr) phi[j * ldp + rr] = phin ? phin[(row0 + i) * R + rr] : T(0);
   }
 }
 
@@ -1224,7 +1226,7 @@ __global__ void __launch_bounds__(128) reception_mf_kernel(
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ unit_circle, const float* __restrict__ o,
     const float* __restrict__ phin, const int64_t* __restrict__ perm, float* __restrict__ phi,
-    int64_t leaf0, int Q) {
+    int64_t leaf0, int Q, int ldp) {
   // one CTA per leaf: its aux circle and incoming amplitudes live in smem
   extern __shared__ float4 sm4[];
   float2* aux = reinterpret_cast<float2*>(sm4);        // Q relative aux points
@@ -1255,7 +1257,7 @@ __global__ void __launch_bounds__(128) reception_mf_kernel(
     const int64_t dst = perm[i];
 #pragma unroll
     for (int rr = 0; rr < R; ++rr)
-      phi[dst * R + rr] = (phin ? phin[i * R + rr] : 0.f) + kScale * acc[rr];
+      phi[dst * ldp + rr] = (phin ? phin[i * R + rr] : 0.f) + kScale * acc[rr];
   }
 }
 

@@ -322,6 +322,7 @@ struct nesa_plan {
 
   // workspace for R real columns
   int ws_R = 0;
+  int ldv = 1;  // row stride of the caller's q / phi (elements) for the current capture
   DevBuf<unsigned char> qt, phin, s, o, Y, Tup;
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
@@ -338,8 +339,10 @@ struct nesa_plan {
     int R;
     uint32_t flags;
     int stage;
+    int ldv;
     bool operator<(const GraphKey& o) const {
-      return std::tie(q, phi, R, flags, stage) < std::tie(o.q, o.phi, o.R, o.flags, o.stage);
+      return std::tie(q, phi, R, flags, stage, ldv) <
+             std::tie(o.q, o.phi, o.R, o.flags, o.stage, o.ldv);
     }
   };
   struct GraphEntry {
@@ -755,8 +758,7 @@ void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, co
                       int64_t perm_offset, cudaStream_t st) {
   if (bs.n_items == 0) return;
   BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p, x, y, base,
-                     perm};
-  (void)perm_offset;
+                     perm, int(perm_offset)};
   constexpr size_t sm = blockgemv_smem_bytes<T, R, MODE, NST>();
   blockgemv_kernel<T, R, MODE, NST><<<bs.grid, kBGThreads, sm, st>>>(a);
 }
@@ -972,7 +974,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) down_level(lv);
   };
   auto gather = [&]() {
-    gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N);
+    gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N, P->ldv);
     nk++;
   };
   auto finish = [&]() {
@@ -982,19 +984,21 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         const size_t sm = size_t(Q) * (sizeof(float2) + R * sizeof(float));
         reception_mf_kernel<R><<<int(P->leaf_end - P->leaf_begin), 128, sm, s0>>>(
             P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->mf_circle.p, o,
-            near ? phin : nullptr, P->perm.p, phi, P->leaf_begin, Q);
+            near ? phin : nullptr, P->perm.p, phi, P->leaf_begin, Q, P->ldv);
       }
       nk++;
     } else if (far) {
-      launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p, 0,
-                                           s0);
+      launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p,
+                                           P->ldv, s0);
       nk++;
     } else if (near) {
       scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
-          phin, P->perm.p + P->pt_begin, phi, P->pt_begin, nloc);
+          phin, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
       nk++;
     } else {
-      CUDA_OK(cudaMemsetAsync(phi, 0, size_t(P->N) * R * sizeof(T), s0));
+      scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
+          nullptr, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
+      nk++;
     }
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
   };
@@ -1084,19 +1088,40 @@ int enqueue_dispatch(nesa_plan* P, const void* q, void* phi, int R, uint32_t fla
   }
 }
 
+int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t flags, void* stream,
+              int stage);
+
+// One product of nrhs right-hand sides: real columns are processed in blocks
+// of <= 4 (one captured graph per block; rows of q / phi keep their stride).
 int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_complex,
                uint32_t flags, void* stream, int stage) {
   require(P != nullptr, "null plan");
   require(nrhs >= 1, "nrhs must be >= 1");
   require(q != nullptr && phi != nullptr, "null vector");
   require(stage == 0 || !(flags & NESA_PROFILE), "profiling needs a full product");
-  const int R = nrhs * (is_complex ? 2 : 1);
+  const int Rt = nrhs * (is_complex ? 2 : 1);
+  if (Rt == 1 || Rt == 2 || Rt == 4) return run_block(P, q, phi, Rt, Rt, flags, stream, stage);
+  require(stage == 0, "the staged (multi-GPU) product takes at most 4 real columns");
+  require(!(flags & NESA_PROFILE), "profiling takes at most 4 real columns");
+  const size_t es = P->esz;
+  for (int c0 = 0; c0 < Rt;) {
+    const int Rb = Rt - c0 >= 4 ? 4 : (Rt - c0 >= 2 ? 2 : 1);
+    run_block(P, static_cast<const char*>(q) + c0 * es, static_cast<char*>(phi) + c0 * es, Rb, Rt,
+              flags, stream, stage);
+    c0 += Rb;
+  }
+  return NESA_OK;
+}
+
+int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t flags, void* stream,
+              int stage) {
   CUDA_OK(cudaSetDevice(P->device));
   if (P->dtype == NESA_F64)
     ensure_workspace<double>(P, R);
   else
     ensure_workspace<float>(P, R);
-  nesa_plan::GraphKey key{q, phi, R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE), stage};
+  nesa_plan::GraphKey key{q, phi, R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE), stage, ldv};
+  P->ldv = ldv;
   auto itg = P->graphs.find(key);
   if (itg == P->graphs.end()) {
     cudaGraph_t g = nullptr;

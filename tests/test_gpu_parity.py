@@ -242,3 +242,21 @@ def test_pinned_host_tensor_roundtrip(golden):
     phi = mvp(tree, params, qh)
     assert not phi.is_cuda and phi.is_pinned() and phi.dtype == torch.complex64
     assert rel_l2(phi.numpy(), g["phi"]) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype,tol,nrhs,cplx", [("f64", 1e-12, 7, True), ("f32", 1e-5, 5, False),
+                                                 ("f32", 1e-5, 16, True)])
+def test_many_rhs_column_blocks(dtype, tol, nrhs, cplx):
+    # C5: many right-hand sides (plane waves) run as column blocks of <= 4 reals
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=4), 8000)
+    tree = build_tree(pts, TreeParams(P=32))
+    params = NesaParams(Q=24)
+    k = geo.wavenumber(geo.CurveSpec(kind="ellipse-plates", seed=4), 8000)
+    Qm = geo.plane_wave_rhs(pts, k, n_waves=nrhs)
+    if not cplx:
+        Qm = Qm.real.copy()
+    ref = oracle_mvp(tree, build_all(tree, params), Qm)
+    qq = Qm if dtype == "f64" else Qm.astype(np.complex64 if cplx else np.float32)
+    phi = mvp(tree, params, qq)
+    assert phi.shape == Qm.shape
+    assert rel_l2(phi, ref) <= tol
