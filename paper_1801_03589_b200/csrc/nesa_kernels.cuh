@@ -700,6 +700,7 @@ __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
   const int QR = Q * R;
   const int lane = threadIdx.x & 31;
   const bool vec = (QR % 4) == 0;
+  const uint64_t drop = l2_evict_first_policy();  // last use of Y
   for (int64_t wg = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; wg < n_ids;
        wg += (int64_t(gridDim.x) * blockDim.x) >> 5) {
     const int64_t g = ids[wg];
@@ -710,8 +711,14 @@ __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
         int64_t e = e0;
         for (; e + 2 <= e1; e += 2) {
           T a[4], b[4];
-          ld4(Y + e * QR + w, a);
-          ld4(Y + (e + 1) * QR + w, b);
+          if constexpr (sizeof(T) == 4) {
+            const float4 fa = ld16_hint(Y + e * QR + w, drop), fb = ld16_hint(Y + (e + 1) * QR + w, drop);
+            a[0] = fa.x; a[1] = fa.y; a[2] = fa.z; a[3] = fa.w;
+            b[0] = fb.x; b[1] = fb.y; b[2] = fb.z; b[3] = fb.w;
+          } else {
+            ld4(Y + e * QR + w, a);
+            ld4(Y + (e + 1) * QR + w, b);
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) v[i] = (v[i] + a[i]) + b[i];
         }
@@ -1042,10 +1049,11 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
     {
       constexpr int V = 16 / int(sizeof(T));  // elements per 16-byte store
       constexpr int NV = W::QR / V;
+      const uint64_t keep = l2_evict_last_policy();  // Y is re-read by reduce_kernel
       for (int i = tid; i < n * NV; i += 128) {
         const int p = i / NV, v = i - p * NV;
         const float4 val = *reinterpret_cast<const float4*>(O + p * W::XS + v * V);
-        *reinterpret_cast<float4*>(Y + int64_t(eid[p]) * W::QR + v * V) = val;
+        st16_hint(Y + int64_t(eid[p]) * W::QR + v * V, val, keep);
       }
     }
     __syncthreads();  // X buffer reuse
