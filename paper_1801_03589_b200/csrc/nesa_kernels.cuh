@@ -1070,16 +1070,19 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
 template <typename T, int R, int QT>
 struct LVW {
   using W = TGW<T, R, QT>;
-  static constexpr size_t SMEM = 4 * W::MB + W::XB + 3 * 64;
+  static constexpr int kSlots = 2;  // quadrant matrices per round (sorted tiles need <= 2)
+  static constexpr size_t SMEM = kSlots * W::MB + 2 * W::XB + 3 * 64;
 };
 
 template <typename T, int R, int QT, int MODE>
 __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) {
   using W = TGW<T, R, QT>;
+  using LV = LVW<T, R, QT>;
   extern __shared__ __align__(128) unsigned char smem[];
-  T* M = reinterpret_cast<T*>(smem);                         // up to 4 quadrant matrices
-  T* X = reinterpret_cast<T*>(smem + 4 * W::MB);             // group-major inputs / outputs
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * W::MB + W::XB);  // [0] M, [1] X
+  T* M = reinterpret_cast<T*>(smem);                                  // kSlots matrices
+  T* X = reinterpret_cast<T*>(smem + LV::kSlots * W::MB);             // inputs / outputs
+  T* Oc = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + W::XB);    // down: o[c] (reduce output)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LV::kSlots * W::MB + 2 * W::XB);  // M, X
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t t0 = int64_t(blockIdx.x) * W::PER;
   const int n = int(a.count - t0 < W::PER ? a.count - t0 : W::PER);
@@ -1089,9 +1092,10 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
-    const uint32_t mbytes = uint32_t((q_hi - q_lo + 1) * W::MB);
-    mbar_arrive_expect_tx(&bar[0], mbytes);
-    bulk_g2s(M, reinterpret_cast<const unsigned char*>(a.MT4) + q_lo * W::MB, mbytes, &bar[0]);
+    const int nq = min(LV::kSlots, q_hi - q_lo + 1);
+    mbar_arrive_expect_tx(&bar[0], uint32_t(nq * W::MB));
+    bulk_g2s(M, reinterpret_cast<const unsigned char*>(a.MT4) + q_lo * W::MB, uint32_t(nq * W::MB),
+             &bar[0]);
   }
   __syncthreads();
   pdl_trigger();
@@ -1121,17 +1125,18 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
     }
   } else {
     if (warp == 0) {
-      if (lane == 0) mbar_arrive_expect_tx(&bar[1], kVB * uint32_t(n));
+      const uint32_t nb = (MODE == kLvlDown ? 2u : 1u) * kVB * uint32_t(n);
+      if (lane == 0) mbar_arrive_expect_tx(&bar[1], nb);
       __syncwarp();
       for (int p = lane; p < n; p += 32) {
         const int64_t g = MODE == kLvlDown ? a.opar[t0 + p] : a.order[t0 + p];
         bulk_g2s(X + p * W::XS, (MODE == kLvlDown ? a.o : a.s) + g * W::QR, kVB, &bar[1]);
+        if constexpr (MODE == kLvlDown)
+          bulk_g2s(Oc + p * W::XS, a.o + int64_t(a.order[t0 + p]) * W::QR, kVB, &bar[1]);
       }
     }
     mbar_wait(&bar[1], 0);
   }
-  mbar_wait(&bar[0], 0);
-  __syncthreads();
 
   const int wr = warp % W::RW, wc = warp / W::RW;
   const int tr = lane >> 3, tc = lane & 7;
@@ -1149,39 +1154,54 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = T(0);
-  if (E0 + tc < n) {
-    const T* xp = X + (E0 + tc) * W::XS;
-    for (int qd = q_lo; qd <= q_hi; ++qd) {
-      bool any = false;
+  int round = 0;
+  for (int q0 = q_lo; q0 <= q_hi; q0 += LV::kSlots, ++round) {
+    const int nq = min(LV::kSlots, q_hi - q0 + 1);
+    if (round) {
+      __syncthreads();  // previous slots consumed
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&bar[0], uint32_t(nq * W::MB));
+        bulk_g2s(M, reinterpret_cast<const unsigned char*>(a.MT4) + q0 * W::MB,
+                 uint32_t(nq * W::MB), &bar[0]);
+      }
+    }
+    mbar_wait(&bar[0], uint32_t(round) & 1u);
+    __syncthreads();  // staged inputs visible (first round)
+    if (E0 + tc < n) {
+      const T* xp = X + (E0 + tc) * W::XS;
+      for (int qq = 0; qq < nq; ++qq) {
+        const int qd = q0 + qq;
+        bool any = false;
 #pragma unroll
-      for (int i = 0; i < NE; ++i) any |= eq[i] == qd;
-      if (!any) continue;
-      const T* mp = M + (qd - q_lo) * (W::MB / sizeof(T)) + row0;
-      T part[8][4];
+        for (int i = 0; i < NE; ++i) any |= eq[i] == qd;
+        if (!any) continue;
+        const T* mp = M + qq * (W::MB / sizeof(T)) + row0;
+        T part[8][4];
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) part[r][c] = T(0);
+          for (int c = 0; c < 4; ++c) part[r][c] = T(0);
 #pragma unroll 4
-      for (int j = 0; j < QT; ++j) {
-        T m0[4], m1[4], x[4];
-        ld4(mp + j * QT, m0);
-        ld4(mp + j * QT + 4, m1);
+        for (int j = 0; j < QT; ++j) {
+          T m0[4], m1[4], x[4];
+          ld4(mp + j * QT, m0);
+          ld4(mp + j * QT + 4, m1);
 #pragma unroll
-        for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
+          for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              part[r][c] = fma(m0[r], x[c], part[r][c]);
+              part[r + 4][c] = fma(m1[r], x[c], part[r + 4][c]);
+            }
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c)
+          if (eq[c / R] == qd)
 #pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            part[r][c] = fma(m0[r], x[c], part[r][c]);
-            part[r + 4][c] = fma(m1[r], x[c], part[r + 4][c]);
-          }
+            for (int r = 0; r < 8; ++r) acc[r][c] = part[r][c];
       }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (eq[c / R] == qd)
-#pragma unroll
-          for (int r = 0; r < 8; ++r) acc[r][c] = part[r][c];
     }
   }
   __syncthreads();  // inputs consumed
@@ -1190,7 +1210,13 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
     for (int c = 0; c < 4; ++c) {
       const int p = E0 + tc + 8 * (c / R), rr = c % R;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) X[p * W::XS + (row0 + r) * R + rr] = acc[r][c];
+      for (int r = 0; r < 8; ++r) {
+        const int idx = p * W::XS + (row0 + r) * R + rr;
+        if constexpr (MODE == kLvlDown)
+          X[idx] = Oc[idx] + acc[r][c];  // translation sum + potential transfer
+        else
+          X[idx] = acc[r][c];
+      }
     }
   }
   __syncthreads();
@@ -1200,21 +1226,10 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
   for (int i = tid; i < n * NV; i += 128) {
     const int p = i / NV, v = i - p * NV;
     T* dst = outb + int64_t(a.order[t0 + p]) * W::QR + v * V;
-    if constexpr (sizeof(T) == 4) {
-      float4 val = *reinterpret_cast<const float4*>(X + p * W::XS + v * V);
-      if constexpr (MODE == kLvlDown) {
-        const float4 cur = *reinterpret_cast<const float4*>(dst);
-        val.x += cur.x; val.y += cur.y; val.z += cur.z; val.w += cur.w;
-      }
-      *reinterpret_cast<float4*>(dst) = val;
-    } else {
-      double2 val = *reinterpret_cast<const double2*>(X + p * W::XS + v * V);
-      if constexpr (MODE == kLvlDown) {
-        const double2 cur = *reinterpret_cast<const double2*>(dst);
-        val.x += cur.x; val.y += cur.y;
-      }
-      *reinterpret_cast<double2*>(dst) = val;
-    }
+    if constexpr (sizeof(T) == 4)
+      *reinterpret_cast<float4*>(dst) = *reinterpret_cast<const float4*>(X + p * W::XS + v * V);
+    else
+      *reinterpret_cast<double2*>(dst) = *reinterpret_cast<const double2*>(X + p * W::XS + v * V);
   }
 }
 
