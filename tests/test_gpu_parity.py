@@ -260,3 +260,24 @@ def test_many_rhs_column_blocks(dtype, tol, nrhs, cplx):
     phi = mvp(tree, params, qq)
     assert phi.shape == Qm.shape
     assert rel_l2(phi, ref) <= tol
+
+
+@pytest.mark.parametrize("name", ["fastmvp_1500", "c1_wave_2000", "c2_circle_20000",
+                                  "ellipse_plates_20000"])
+def test_f32_near_and_far_parts(golden, name):
+    # float32 plans compute the near field and the reception matrix-free
+    g = golden(name)
+    tree, params = _problem(g)
+    q = g["q"].astype(np.complex64 if np.iscomplexobj(g["q"]) else np.float32)
+    assert rel_l2(mvp(tree, params, q, far=False), g["phi_near"]) <= 1e-5
+    assert rel_l2(mvp(tree, params, q, near=False), g["phi_far"]) <= 1e-5
+
+
+def test_f32_tall_leaves_matrix_free():
+    pts = geo.generate_sources(geo.CurveSpec(), 6000)
+    tree = build_tree(pts, TreeParams(P=700))
+    assert max(g.n_points for g in tree.leaves()) > 160
+    params = NesaParams(Q=12)
+    q = np.random.default_rng(3).standard_normal(6000)
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    assert rel_l2(mvp(tree, params, q.astype(np.float32)), ref) <= 1e-5
