@@ -164,6 +164,8 @@ int nesa_abi_version(void);
 #define NESA_STAT_DEVICE_BYTES 5
 #define NESA_STAT_NEAR_CTAS 6
 #define NESA_STAT_KERNELS_PER_MATVEC 7
+#define NESA_STAT_V_MOMENTS 8        /* outgoing moments per leaf (0: stored V)   */
+#define NESA_STAT_U_TERMS 9          /* incoming expansion terms (0: stored U)    */
 int64_t nesa_plan_stat(nesa_plan* plan, int32_t which);
 
 /* Profiling: with NESA_PROFILE in flags each nesa_matvec records CUDA
@@ -176,6 +178,12 @@ int64_t nesa_plan_stat(nesa_plan* plan, int32_t which);
 int nesa_profile_reset(nesa_plan* plan);
 /* Synchronises; fills up to max durations (ms) of `stage`, returns count. */
 int nesa_profile_read(nesa_plan* plan, int32_t stage, float* ms, int32_t max);
+/* Diagnostics: with NESA_TRACE=1 in the environment at plan creation, a
+ * profiled product records an event after every kernel.  Fills up to max
+ * times (ms from the product's start) of the last profiled product and
+ * returns the count; nesa_trace_name(i) names the kernel of entry i. */
+int nesa_trace_read(nesa_plan* plan, float* ms, int32_t max);
+const char* nesa_trace_name(nesa_plan* plan, int32_t i);
 
 #ifdef __cplusplus
 }

@@ -25,13 +25,14 @@ NESA_FAR = 2
 NESA_PROFILE = 16
 
 STAT = {"near_entries": 0, "v_entries": 1, "u_entries": 2, "d_refs": 3, "n_dtab": 4,
-        "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7}
+        "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7, "v_moments": 8,
+        "u_terms": 9}
 STAGE = {"total": 0, "near": 1, "far": 2, "reception": 3}
 
 EXPORTED_SYMBOLS = (
     "nesa_plan_create", "nesa_matvec", "nesa_matvec_stage", "nesa_plan_s_dev",
     "nesa_plan_destroy", "nesa_last_error", "nesa_abi_version", "nesa_plan_stat",
-    "nesa_profile_reset", "nesa_profile_read",
+    "nesa_profile_reset", "nesa_profile_read", "nesa_trace_read", "nesa_trace_name",
 )
 
 _p = ctypes.c_void_p
@@ -98,6 +99,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_profile_read.argtypes = [_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_float),
                                       ctypes.c_int32]
     lib.nesa_profile_read.restype = ctypes.c_int
+    lib.nesa_trace_read.argtypes = [_p, ctypes.POINTER(ctypes.c_float), ctypes.c_int32]
+    lib.nesa_trace_read.restype = ctypes.c_int
+    lib.nesa_trace_name.argtypes = [_p, ctypes.c_int32]
+    lib.nesa_trace_name.restype = ctypes.c_char_p
     if lib.nesa_abi_version() != NESA_ABI_VERSION:
         raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
     _lib = lib

@@ -330,15 +330,18 @@ __global__ void gather_kernel(const T* __restrict__ q, const int64_t* __restrict
   }
 }
 
-// phi[perm[i]] = phin[i] (phin == nullptr: zeros), phi rows of stride ldp
+// phi[perm[i]] = phin[i] + phif[i] (a null term is zero), phi rows of stride ldp
 template <typename T, int R>
-__global__ void scatter_kernel(const T* __restrict__ phin, const int64_t* __restrict__ perm,
-                               T* __restrict__ phi, int64_t row0, int64_t n, int ldp) {
+__global__ void scatter_kernel(const T* __restrict__ phin, const T* __restrict__ phif,
+                               const int64_t* __restrict__ perm, T* __restrict__ phi, int64_t row0,
+                               int64_t n, int ldp) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = perm[row0 + i];
+    const int64_t k = (row0 + i) * R;
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) phi[j * ldp + rr] = phin ? phin[(row0 + i) * R + rr] : T(0);
+    for (int rr = 0; rr < R; ++rr)
+      phi[j * ldp + rr] = (phin ? phin[k + rr] : T(0)) + (phif ? phif[k + rr] : T(0));
   }
 }
 
@@ -1234,53 +1237,307 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
 }
 
 // ----------------------------------------------------------------------------
-// Matrix-free reception (float32 plans):
-//   phi[perm i] = phin[i] + sum_k -0.5 log|p_i - a_k|^2 o[leaf i][k]
-// with the incoming aux circle a_k = c + r (cos, sin)(2 pi k / Q) of the
-// point's leaf (operators.py:147-149 builds U = kernel_matrix(pts, in_aux)).
-// Evaluated from leaf-relative coordinates p_i - c (the aux circle lies
-// >= 1.38 h from every point of the leaf, so float32 loses nothing that
-// matters at the 1e-5 tolerance), log via MUFU lg2, scaled once.  Streams
-// ~36 bytes per point instead of the 4Q-byte stored row of U.
+// Radiation and reception through circle expansions (float32 plans built
+// from geometry).  With w = (p - c) / r for a point p of a leaf with center
+// c and a circle of radius r > |p - c| through x_l = c + r e^{i phi_l}:
+//   -0.5 log|x_l - p|^2 = -log r + Re sum_{m>=1} (1/m) w^m e^{-i m phi_l}
+// (|w| <= sqrt2 h / r: 0.57 for the outgoing check circle, 0.51 for the
+// incoming aux circle, so the series converges geometrically).
+//
+// Radiation V = fit K(out_check, pts) (operators.py:107-112):
+//   s_k = -log(r) F_k mu_0 + sum_{m>=1} Re(A_km mu_m),
+//   mu_m = sum_j w_j^m q_j,  A_km = sum_l fit_kl (1/m) e^{-i m phi_l},
+//   F_k = sum_l fit_kl   (A, F formed once per plan in float64).
+// Reception U = K(pts, in_aux) (operators.py:147-149):
+//   phi_j = -log(r) sum_k o_k + Re sum_{m>=1} beta_m w_j^m,
+//   beta_m = sum_k (1/m) e^{-i m theta_k} o_k.
+// Both replace a streamed Q x n operator (4Q bytes per point each way) by
+// ~8 FP32 instructions per point and term; the plan picks the number of
+// terms from the largest |w| of its points (truncation below float32
+// rounding).  One warp per leaf; moment sums over the leaf's points use a
+// fixed transpose-reduction tree (deterministic).
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+// Sum 32 per-lane values over the warp: afterwards lane l returns the sum of
+// value l (31 shuffles; fixed pairing, so bitwise reproducible).
+__device__ __forceinline__ float warp_transpose_sum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int sft = 16; sft >= 1; sft >>= 1) {
+    const bool up = lane & sft;
+#pragma unroll
+    for (int j = 0; j < sft; ++j) {
+      const float send = up ? v[j] : v[j + sft];
+      const float keep = up ? v[j + sft] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+    }
+  }
+  return v[0];
+}
+
+constexpr int kExpWarps = 4;   // warps per CTA of the expansion kernels
+constexpr int kMomLanes = 4;   // radiation: lanes per leaf
+constexpr int kMomLeavesPerWarp = 32 / kMomLanes;
+
+// w^e (e >= 0) by binary powering
+__device__ __forceinline__ float2 cpowf(float2 w, int e) {
+  float2 r = make_float2(1.f, 0.f);
+  while (e) {
+    if (e & 1) r = cmulf(r, w);
+    w = cmulf(w, w);
+    e >>= 1;
+  }
+  return r;
+}
+
+// Radiation through outgoing moments.  Lane group of kMomLanes lanes per
+// leaf, kMomLeavesPerWarp leaves per warp.  Each lane accumulates the moments
+// of every kMomLanes-th point of its leaf in registers (passes of MP moments,
+// 2 R MP = 80 accumulators; the next point's data is prefetched), the group
+// combines them with a transpose reduction (fixed pairing), then the warp
+// applies A (read through L1, it is shared by every leaf) to its leaves'
+// moments.  smem: per warp mu [leaves][nm][R] float2 (16-byte aligned).
 template <int R>
-__global__ void __launch_bounds__(128) reception_mf_kernel(
+__global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
-    const float2* __restrict__ unit_circle, const float* __restrict__ o,
-    const float* __restrict__ phin, const int64_t* __restrict__ perm, float* __restrict__ phi,
-    int64_t leaf0, int Q, int ldp) {
-  // one CTA per leaf: its aux circle and incoming amplitudes live in smem
+    const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
+    int64_t leaf0, int64_t nleaf, int Q, int nm) {
+  constexpr int MP = 40 / R;           // moments per pass
+  constexpr int NV = 2 * R * MP;       // 80 accumulators
+  constexpr int NV2 = NV / 2, NV4 = NV / 4;
+  constexpr int LW = kMomLeavesPerWarp;
   extern __shared__ float4 sm4[];
-  float2* aux = reinterpret_cast<float2*>(sm4);        // Q relative aux points
-  float* os = reinterpret_cast<float*>(aux + Q);       // Q * R amplitudes
-  const int64_t leaf = leaf0 + blockIdx.x;
-  const float r = leaf_r[leaf];
-  for (int k = threadIdx.x; k < Q; k += blockDim.x) {
-    const float2 c = unit_circle[k];
-    aux[k] = make_float2(r * c.x, r * c.y);
-  }
-  for (int k = threadIdx.x; k < Q * R; k += blockDim.x) os[k] = o[leaf * Q * R + k];
-  __syncthreads();
-  const int64_t b = leaf_start[leaf], e = leaf_stop[leaf];
-  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-    const float2 p = prel[i];
-    float acc[R];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mu_stride = (nm * R + 1) & ~1;  // float2 per leaf, even => 16-byte rows
+  float2* mu = reinterpret_cast<float2*>(sm4) + warp * LW * mu_stride;
+  const int slot = lane / kMomLanes, g = lane % kMomLanes;
+  for (int64_t lw = (int64_t(blockIdx.x) * kExpWarps + warp) * LW; lw < nleaf;
+       lw += int64_t(gridDim.x) * kExpWarps * LW) {
+    const int64_t li = lw + slot;
+    const bool live = li < nleaf;
+    const int64_t leaf = leaf0 + (live ? li : 0);
+    const int64_t b = leaf_start[leaf];
+    const int n = live ? int(leaf_stop[leaf] - b) : 0;
+    const float inv = 1.f / leaf_r[leaf];
+    float* muf = reinterpret_cast<float*>(mu + slot * mu_stride);
+    for (int m0 = 0; m0 < nm; m0 += MP) {
+      float v[NV];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) acc[rr] = 0.f;
-#pragma unroll 8
-    for (int k = 0; k < Q; ++k) {
-      const float2 a = aux[k];
-      const float dx = p.x - a.x, dy = p.y - a.y;
-      const float l2 = __log2f(fmaf(dx, dx, dy * dy));
+      for (int t = 0; t < NV; ++t) v[t] = 0.f;
+      float2 pn = make_float2(0.f, 0.f);
+      float qn[R];
+      if (g < n) {
+        pn = prel[b + g];
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(l2, os[k * R + rr], acc[rr]);
+        for (int rr = 0; rr < R; ++rr) qn[rr] = qt[(b + g) * R + rr];
+      }
+      for (int j = g; j < n; j += kMomLanes) {
+        const float2 w = make_float2(pn.x * inv, pn.y * inv);
+        float qv[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) qv[rr] = qn[rr];
+        if (j + kMomLanes < n) {  // prefetch the next point
+          pn = prel[b + j + kMomLanes];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) qn[rr] = qt[(b + j + kMomLanes) * R + rr];
+        }
+        float2 z = m0 ? cpowf(w, m0) : make_float2(1.f, 0.f);
+#pragma unroll
+        for (int mm = 0; mm < MP; ++mm) {
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            v[(mm * R + rr) * 2] = fmaf(z.x, qv[rr], v[(mm * R + rr) * 2]);
+            v[(mm * R + rr) * 2 + 1] = fmaf(z.y, qv[rr], v[(mm * R + rr) * 2 + 1]);
+          }
+          z = cmulf(z, w);
+        }
+      }
+      // transpose reduction over the 4 lanes of the group: lane g ends with
+      // values [vb, vb + NV4)
+      {
+        const bool up = g & 2;
+#pragma unroll
+        for (int t = 0; t < NV2; ++t) {
+          const float send = up ? v[t] : v[t + NV2];
+          const float keep = up ? v[t + NV2] : v[t];
+          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+      }
+      {
+        const bool up = g & 1;
+#pragma unroll
+        for (int t = 0; t < NV4; ++t) {
+          const float send = up ? v[t] : v[t + NV4];
+          const float keep = up ? v[t + NV4] : v[t];
+          v[t] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+      }
+      const int vb = ((g & 2) ? NV2 : 0) + ((g & 1) ? NV4 : 0);
+      const int lim = (nm - m0) * R * 2;  // values of moments < nm
+#pragma unroll
+      for (int t = 0; t < NV4; ++t)
+        if (vb + t < lim) muf[m0 * R * 2 + vb + t] = v[t];
     }
-    constexpr float kScale = -0.5f * 0.69314718055994531f;  // -0.5 ln 2
-    const int64_t dst = perm[i];
+    __syncwarp();
+    // s_k = -log(r) F_k mu_0 + sum_m Re(A_km mu_m): lane owns k = kb + lane
+    // and kb + 32 + lane for all the warp's leaves
+    for (int kb = 0; kb < Q; kb += 64) {
+      const int k0 = kb + lane, k1 = kb + 32 + lane;
+      const bool h0 = k0 < Q, h1 = k1 < Q;
+      float acc[2][LW][R];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr)
-      phi[dst * ldp + rr] = (phin ? phin[i * R + rr] : 0.f) + kScale * acc[rr];
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int l = 0; l < LW; ++l)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) acc[h][l][rr] = 0.f;
+      for (int m = 1; m < nm; ++m) {
+        const float2 a0 = h0 ? __ldg(A + m * Q + k0) : make_float2(0.f, 0.f);
+        const float2 a1 = h1 ? __ldg(A + m * Q + k1) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int l = 0; l < LW; ++l) {
+          float2 u[R];
+          if constexpr (R == 2) {
+            const float4 t = *reinterpret_cast<const float4*>(mu + l * mu_stride + m * R);
+            u[0] = make_float2(t.x, t.y);
+            u[1] = make_float2(t.z, t.w);
+          } else {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) u[rr] = mu[l * mu_stride + m * R + rr];
+          }
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            acc[0][l][rr] = fmaf(a0.x, u[rr].x, fmaf(-a0.y, u[rr].y, acc[0][l][rr]));
+            acc[1][l][rr] = fmaf(a1.x, u[rr].x, fmaf(-a1.y, u[rr].y, acc[1][l][rr]));
+          }
+        }
+      }
+      const float f0 = h0 ? __ldg(A + k0).x : 0.f, f1 = h1 ? __ldg(A + k1).x : 0.f;
+#pragma unroll
+      for (int l = 0; l < LW; ++l) {
+        const int64_t li2 = lw + l;
+        if (li2 >= nleaf) break;
+        const int64_t lf = leaf0 + li2;
+        const float nl = -logf(leaf_r[lf]);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const float u0 = mu[l * mu_stride + rr].x;
+          if (h0) s[(lf * Q + k0) * R + rr] = fmaf(nl * f0, u0, acc[0][l][rr]);
+          if (h1) s[(lf * Q + k1) * R + rr] = fmaf(nl * f1, u0, acc[1][l][rr]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// Reception through the incoming expansion.  One warp per leaf, one lane per
+// point; the point data and the leaf's amplitudes are loaded before the
+// coefficient phase so their latency overlaps it.  E [Q][nt + 1] float2
+// (column 0 = 1, column m = (1/m) e^{-i m theta_k}) is read through L1.
+// smem per warp: beta [nt + 1][R] float2 (16-byte aligned), o [Q][R].
+template <int R>
+__global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
+    const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
+    const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
+    const float2* __restrict__ E, const float* __restrict__ o, const float* __restrict__ phin,
+    const int64_t* __restrict__ perm, float* __restrict__ phi, int64_t leaf0, int64_t nleaf, int Q,
+    int nt, int ldp) {
+  extern __shared__ float4 sm4[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = ((nt + 1) * R + 1) & ~1;            // beta float2, even
+  const int per_warp = nb + ((Q * R + 3) & ~3) / 2;  // + o floats, 16-byte multiple
+  float2* beta = reinterpret_cast<float2*>(sm4) + warp * per_warp;
+  float* os = reinterpret_cast<float*>(beta + nb);
+  const int ne = nt + 1;
+  constexpr int kSlots = 4;
+  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf;
+       li += int64_t(gridDim.x) * kExpWarps) {
+    const int64_t leaf = leaf0 + li;
+    const int64_t b = leaf_start[leaf];
+    const int n = int(leaf_stop[leaf] - b);
+    const float r = leaf_r[leaf];
+    // prefetch: amplitudes and the first kSlots * 32 points
+    float ov[4];
+    const int nq = Q * R;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) ov[t] = lane + 32 * t < nq ? o[leaf * nq + lane + 32 * t] : 0.f;
+    float2 pp[kSlots];
+    int64_t dd[kSlots];
+    float bb[kSlots][R];
+#pragma unroll
+    for (int i = 0; i < kSlots; ++i) {
+      const int j = lane + 32 * i;
+      if (j < n) {
+        pp[i] = prel[b + j];
+        dd[i] = perm ? perm[b + j] : b + j;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) bb[i][rr] = phin ? phin[(b + j) * R + rr] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (lane + 32 * t < nq) os[lane + 32 * t] = ov[t];
+    for (int t = lane + 128; t < nq; t += 32) os[t] = o[leaf * nq + t];
+    __syncwarp();
+    const float nlr = -logf(r);
+    for (int m = lane; m < ne; m += 32) {
+      float2 acc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = make_float2(0.f, 0.f);
+#pragma unroll 4
+      for (int k = 0; k < Q; ++k) {
+        const float2 e = __ldg(E + k * ne + m);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const float ok = os[k * R + rr];
+          acc[rr].x = fmaf(e.x, ok, acc[rr].x);
+          acc[rr].y = fmaf(e.y, ok, acc[rr].y);
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        beta[m * R + rr] = m ? acc[rr] : make_float2(nlr * acc[rr].x, 0.f);
+    }
+    __syncwarp();
+    const float inv = 1.f / r;
+    auto eval = [&](float2 p, int64_t dst, const float* base) {
+      const float2 w = make_float2(p.x * inv, p.y * inv);
+      float2 z = w;
+      float acc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = beta[rr].x;
+#pragma unroll 4
+      for (int m = 1; m <= nt; ++m) {
+        float2 bt[R];
+        if constexpr (R == 2) {
+          const float4 t = *reinterpret_cast<const float4*>(beta + m * 2);
+          bt[0] = make_float2(t.x, t.y);
+          bt[1] = make_float2(t.z, t.w);
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) bt[rr] = beta[m * R + rr];
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(bt[rr].x, z.x, fmaf(-bt[rr].y, z.y, acc[rr]));
+        z = cmulf(z, w);
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) phi[dst * ldp + rr] = base[rr] + acc[rr];
+    };
+#pragma unroll
+    for (int i = 0; i < kSlots; ++i)
+      if (lane + 32 * i < n) eval(pp[i], dd[i], bb[i]);
+    for (int j = lane + 32 * kSlots; j < n; j += 32) {
+      float base[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) base[rr] = phin ? phin[(b + j) * R + rr] : 0.f;
+      eval(prel[b + j], perm ? perm[b + j] : b + j, base);
+    }
+    __syncwarp();
   }
 }
 

@@ -18,6 +18,7 @@
 #include <functional>
 #include <utility>
 #include <map>
+#include <string>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -271,6 +272,8 @@ __global__ void convert_kernel(const double* src, T* dst, int64_t n) {
 // ---------------------------------------------------------------------------
 // Plan
 // ---------------------------------------------------------------------------
+constexpr int kTraceSlots = 64;
+
 struct nesa_plan {
   int device = 0;
   int dtype = NESA_F64;
@@ -309,21 +312,29 @@ struct nesa_plan {
   int qs = 4;                               // quadrant slots staged per round
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
   int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
+  int near_waves = 1;                       // near-field grid = waves x resident CTAs
   bool priority = true;                     // far-field stream scheduled first
   bool split = false;                       // fine-level translation on a side stream
   int near_after = 1;                       // where the near branch forks (see enqueue_T)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
+  bool recv_far = false;                    // reception in the far branch (u_mf only)
   bool pdl = true;                          // programmatic dependent launch in the far chain
   DevBuf<float2> mf_prel;                   // [N] point - leaf center (float32)
   DevBuf<int64_t> gstart, gstop;            // [NL] leaf point ranges
-  DevBuf<float> mf_leaf_r;                  // [NL] rho_in_aux * half side
-  DevBuf<float2> mf_circle;                 // [Q] unit circle (cos, sin)
+  DevBuf<float> mf_leaf_r;                  // [NL] rho_in_aux * half side (float32)
+  // radiation through outgoing moments (float32 plans from geometry)
+  bool v_mom = false;
+  int v_nm = 0;                             // moments m = 0 .. v_nm - 1
+  int u_nt = 0;                             // reception terms m = 1 .. u_nt
+  DevBuf<float2> mom_A;                     // [v_nm][Q]: row 0 = (F_k, 0), row m = A_km
+  DevBuf<float2> exp_E;                     // [Q][u_nt + 1]: 1, (1/m) e^{-i m theta_k}
+  DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
   cudaEvent_t ev_mark = nullptr;            // no-op event-record node ahead of the near kernel
 
   // workspace for R real columns
   int ws_R = 0;
   int ldv = 1;  // row stride of the caller's q / phi (elements) for the current capture
-  DevBuf<unsigned char> qt, phin, s, o, Y, Tup;
+  DevBuf<unsigned char> qt, phin, phif, s, o, Y, Tup;
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -356,7 +367,9 @@ struct nesa_plan {
   // profiling: per matvec a set of 2*NESA_N_STAGES events
   std::vector<std::vector<cudaEvent_t>> prof_events;
   size_t prof_used = 0;
-  cudaEvent_t cap_events[2 * NESA_N_STAGES] = {};
+  cudaEvent_t cap_events[2 * NESA_N_STAGES + kTraceSlots] = {};
+  bool trace = false;                       // NESA_TRACE: an event after every kernel
+  std::vector<std::string> trace_names;
 
   ~nesa_plan() {
     cudaSetDevice(device);
@@ -533,6 +546,38 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->n_red = int64_t(ids.size());
     P->red_ids.upload(ids);
   }
+  // ---- circle expansions (float32 plans from geometry): the number of
+  // terms follows the largest |p - c| / r of the plan's points
+  {
+    const bool geom = d->points_tree && d->leaf_center && d->leaf_r_check && d->leaf_r_inaux &&
+                      d->out_fit_leaf && d->check_cos && d->check_sin && d->aux_cos && d->aux_sin;
+    const bool f32 = std::is_same<T, float>::value;
+    P->v_mom = P->v_mom && f32 && !d->V_blob && geom;
+    P->u_mf = P->u_mf && f32 && !d->U_blob && geom;
+    if (P->v_mom || P->u_mf) {
+      double rv = 0, ru = 0;
+      for (int64_t a = lb; a < le; ++a) {
+        const double cx = d->leaf_center[2 * a], cy = d->leaf_center[2 * a + 1];
+        double dm = 0;
+        for (int64_t i = d->group_start[a]; i < d->group_stop[a]; ++i)
+          dm = std::max(dm, std::hypot(d->points_tree[2 * i] - cx, d->points_tree[2 * i + 1] - cy));
+        rv = std::max(rv, dm / d->leaf_r_check[a]);
+        ru = std::max(ru, dm / d->leaf_r_inaux[a]);
+      }
+      // smallest M with rho^(M+1) / (1 - rho) <= tol
+      auto terms = [](double rho, double tol) {
+        int M = 1;
+        while (M < 96 && std::pow(rho, M + 1) / (1.0 - rho) > tol) ++M;
+        return M;
+      };
+      if (rv >= 0.9) P->v_mom = false;  // stored V for (non-quadtree) geometry this far out
+      if (ru >= 0.9) P->u_mf = false;
+      P->v_nm = terms(rv, 1e-9) + 1;     // V: the fit amplifies truncation; keep a margin
+      P->u_nt = terms(ru, 1e-8);
+      if (const char* e = std::getenv("NESA_V_MOMENTS")) P->v_nm = std::max(2, std::atoi(e));
+      if (const char* e = std::getenv("NESA_U_TERMS")) P->u_nt = std::max(1, std::atoi(e));
+    }
+  }
   // ---- near / V / U block sets (local leaves)
   HostBlockSet hn, hv, hu;
   std::vector<int64_t> near_src_off, v_src_off, u_src_off;
@@ -619,11 +664,11 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
   }
-  chunk_and_balance(hn, es, P->near_ctas * P->n_sm);
+  chunk_and_balance(hn, es, P->near_waves * P->near_ctas * P->n_sm);
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
-  upload_blockset<T>(P->Vset, hv);
+  if (!P->v_mom) upload_blockset<T>(P->Vset, hv);
   upload_blockset<T>(P->Uset, hu);
 
   // ---- fill the blobs: from host operators or assembled on the device
@@ -661,30 +706,63 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
   if (d->V_blob) {
     upload_host_blob<T>(P->Vset, hv, d->V_blob, v_src_off, v_src_rows, v_row0);
-  } else if (!hv.items.empty()) {
+  } else if (!hv.items.empty() && !P->v_mom) {
     assemble_V_kernel<T><<<int(hv.items.size()), 128, P->n_check * sizeof(double)>>>(
         P->Vset.items.p, vleaf.p, pts.p, center.p, rck.p, fit.p, cc.p, cs.p, Q, P->n_check, vblob);
     CUDA_OK(cudaGetLastError());
   }
-  if (P->u_mf) {
-    // matrix-free reception inputs: leaf-relative float32 coordinates
+  if (P->u_mf || P->v_mom) {
+    // expansion inputs: leaf-relative float32 coordinates, radii, and the
+    // per-plan coefficient tables (formed in float64)
     std::vector<float2> prel(static_cast<size_t>(P->N));
-
-    std::vector<float> lr(static_cast<size_t>(NL));
+    std::vector<float> lr(static_cast<size_t>(NL)), lrc(static_cast<size_t>(NL));
     for (int64_t a = 0; a < NL; ++a) {
       const double cx = d->leaf_center[2 * a], cy = d->leaf_center[2 * a + 1];
       lr[a] = float(d->leaf_r_inaux[a]);
+      lrc[a] = float(d->leaf_r_check[a]);
       for (int64_t i = d->group_start[a]; i < d->group_stop[a]; ++i) {
         prel[i] = float2{float(d->points_tree[2 * i] - cx), float(d->points_tree[2 * i + 1] - cy)};
       }
     }
-    std::vector<float2> circ(static_cast<size_t>(Q));
-    for (int k = 0; k < Q; ++k) circ[k] = float2{float(d->aux_cos[k]), float(d->aux_sin[k])};
     P->mf_prel.upload(prel);
     P->gstart.upload(std::vector<int64_t>(d->group_start, d->group_start + NL));
     P->gstop.upload(std::vector<int64_t>(d->group_stop, d->group_stop + NL));
     P->mf_leaf_r.upload(lr);
-    P->mf_circle.upload(circ);
+    P->mf_leaf_rc.upload(lrc);
+    const int nc = P->n_check;
+    if (P->v_mom) {
+      std::vector<float2> A(size_t(P->v_nm) * Q);
+      std::vector<double> ang(nc);
+      for (int l = 0; l < nc; ++l) ang[l] = std::atan2(d->check_sin[l], d->check_cos[l]);
+      for (int k = 0; k < Q; ++k) {
+        const double* f = d->out_fit_leaf + int64_t(k) * nc;
+        double F = 0;
+        for (int l = 0; l < nc; ++l) F += f[l];
+        A[k] = float2{float(F), 0.f};
+        for (int m = 1; m < P->v_nm; ++m) {
+          double re = 0, im = 0;
+          for (int l = 0; l < nc; ++l) {
+            re += f[l] * std::cos(m * ang[l]);
+            im -= f[l] * std::sin(m * ang[l]);
+          }
+          A[size_t(m) * Q + k] = float2{float(re / m), float(im / m)};
+        }
+      }
+      P->mom_A.upload(A);
+    }
+    if (P->u_mf) {
+      const int ne = P->u_nt + 1;
+      std::vector<float2> E(size_t(Q) * ne);
+      for (int k = 0; k < Q; ++k) {
+        const double th = std::atan2(d->aux_sin[k], d->aux_cos[k]);
+        E[size_t(k) * ne] = float2{1.f, 0.f};
+        for (int m = 1; m <= P->u_nt; ++m)
+          E[size_t(k) * ne + m] = float2{float(std::cos(m * th) / m), float(-std::sin(m * th) / m)};
+      }
+      P->exp_E.upload(E);
+    }
+  }
+  if (P->u_mf) {
   } else if (d->U_blob) {
     upload_host_blob<T>(P->Uset, hu, d->U_blob, u_src_off, u_src_rows, u_row0);
   } else if (!hu.items.empty()) {
@@ -742,6 +820,7 @@ void ensure_workspace(nesa_plan* P, int R) {
   const size_t es = sizeof(T);
   P->qt.alloc(size_t(P->N) * R * es);
   P->phin.alloc(size_t(P->N) * R * es);
+  if (P->u_mf && P->recv_far) P->phif.alloc(size_t(P->N) * R * es);
   P->s.alloc(size_t(P->G) * P->Q * R * es);
   P->o.alloc(size_t(P->G) * P->Q * R * es);
   P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
@@ -786,6 +865,10 @@ void set_smem_attrs() {
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  if constexpr (std::is_same<T, float>::value) {
+    CUDA_OK(cudaFuncSetAttribute(radiation_mom_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    CUDA_OK(cudaFuncSetAttribute(reception_exp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  }
   done = true;
 }
 
@@ -816,6 +899,43 @@ void launch_pdl(bool pdl, void (*kernel)(KArgs...), int grid, int block, size_t 
   CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+constexpr int kExpCtasPerSM = 12;  // reception: leaves are latency-bound, keep many warps
+constexpr int kMomCtasPerSM = 4;
+
+// s = V qt: outgoing moments (float32 plans from geometry) or stored V
+template <typename T, int R>
+void launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (P->v_mom) {
+      const int64_t nleaf = P->leaf_end - P->leaf_begin;
+      const int64_t per_cta = int64_t(kExpWarps) * kMomLeavesPerWarp;
+      const int grid = int(std::max<int64_t>(
+          1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(kMomCtasPerSM) * P->n_sm)));
+      const size_t sm = size_t(kExpWarps) * kMomLeavesPerWarp * ((P->v_nm * R + 1) & ~1) * sizeof(float2);
+      radiation_mom_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
+          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, s, P->leaf_begin,
+          nleaf, P->Q, P->v_nm);
+      return;
+    }
+  }
+  launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, st);
+}
+
+// phi[perm] = phin + U o through the incoming expansion (float32 plans)
+template <int R>
+void launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const int64_t* perm,
+                          float* phi, int ldp, cudaStream_t st) {
+  const int64_t nleaf = P->leaf_end - P->leaf_begin;
+  const int grid = int(std::max<int64_t>(
+      1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(kExpCtasPerSM) * P->n_sm)));
+  const int Q = P->Q, nt = P->u_nt;
+  const size_t nb = ((size_t(nt) + 1) * R + 1) & ~size_t(1);
+  const size_t sm = size_t(kExpWarps) * (nb + ((size_t(Q) * R + 3) & ~size_t(3)) / 2) * sizeof(float2);
+  reception_exp_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
+      P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, o, phin, perm, phi,
+      P->leaf_begin, nleaf, Q, nt, ldp);
+}
+
 // Enqueue one product, or one of its two stages (multi-GPU), on P->s0/P->s1.
 //   stage 0: gather, fork{near | V, up, translate, down}, join, reception
 //   stage 1: gather, V, up                  (before the s halo exchange)
@@ -834,6 +954,13 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   const int cap = P->n_sm * 8;
   const int64_t nloc = P->pt_end - P->pt_begin;
   int nk = 0;
+  if (prof) P->trace_names.clear();
+  // NESA_TRACE diagnostics: an event-record node after each kernel
+  auto tr = [&](const char* name, cudaStream_t st) {
+    if (!prof || !P->trace || P->trace_names.size() >= size_t(kTraceSlots)) return;
+    prof_mark(P, true, 2 * NESA_N_STAGES + int(P->trace_names.size()), st);
+    P->trace_names.emplace_back(name);
+  };
 
   const size_t mstride = P->mbytes / sizeof(T);
   const FarGeom FG = far_geom(Q);
@@ -880,6 +1007,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       launch_pdl(P->pdl, level_kernel<T, R, kLvlUpSum>, grid, kFarThreads, lvl_sm, s0, la);
     }
     nk++;
+    tr(la.count >= P->wide_level && Q == 64 ? "up_wt" : "up", s0);
   };
   auto top_sum = [&]() {
     if (P->L > P->l0 && P->loc_count[0] > 0) {
@@ -889,6 +1017,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
                  P->loc_count[0], P->loc_first[1], P->loc_first[1] + P->loc_count[1],
                  (const T*)Tup, s, Q);
       nk++;
+      tr("top_sum", s0);
     }
   };
   T* Y = reinterpret_cast<T*>(P->Y.p);
@@ -906,6 +1035,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp,
                                                                                 s, Y, Q);
     nk++;
+    tr("translate", st);
   };
   auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st) {
     // o[g] = translation sum of the listed local groups
@@ -914,6 +1044,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
                st, (const int32_t*)(P->red_ids.p + i0), i1 - i0, (const int64_t*)P->int_ptr.p,
                (const T*)Y, o, Q);
     nk++;
+    tr("reduce", st);
   };
   auto down_level = [&](int lv) {
     const int ci = lv - P->l0;
@@ -927,6 +1058,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
                  kFarThreads, lvl_sm, s0, la);
     }
     nk++;
+    tr(la.count >= P->wide_level && Q == 64 ? "down_wt" : "down", s0);
   };
   // Far field.  The wide (fine) levels' translation + reduce run on s2 as
   // soon as their s is final, concurrently with the coarse end of the
@@ -976,16 +1108,13 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   auto gather = [&]() {
     gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N, P->ldv);
     nk++;
+    tr("gather", s0);
   };
   auto finish = [&]() {
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
     if (far && P->u_mf) {
-      if constexpr (std::is_same<T, float>::value) {
-        const size_t sm = size_t(Q) * (sizeof(float2) + R * sizeof(float));
-        reception_mf_kernel<R><<<int(P->leaf_end - P->leaf_begin), 128, sm, s0>>>(
-            P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->mf_circle.p, o,
-            near ? phin : nullptr, P->perm.p, phi, P->leaf_begin, Q, P->ldv);
-      }
+      if constexpr (std::is_same<T, float>::value)
+        launch_reception_exp<R>(P, o, near ? phin : nullptr, P->perm.p, phi, P->ldv, s0);
       nk++;
     } else if (far) {
       launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p,
@@ -993,13 +1122,14 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       nk++;
     } else if (near) {
       scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
-          phin, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
+          phin, nullptr, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
       nk++;
     } else {
       scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
-          nullptr, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
+          nullptr, nullptr, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
       nk++;
     }
+    tr("finish", s0);
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
   };
 
@@ -1011,8 +1141,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     gather();
     if (far) {
       prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
-      launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
+      launch_radiation<T, R>(P, qt, s, s0);
       nk++;
+      tr("radiation", s0);
     }
     // Near branch: forks from s0 at position `near_after` (0/1: after
     // radiation, 1 adds a no-op event node so the first far-field kernel is
@@ -1026,8 +1157,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       CUDA_OK(cudaEventRecord(P->ev_fork, s0));
       CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
       if (!near) return;
-      if (prof)
+      if (prof) {
         prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
+        tr("near_begin", s1);
+      }
       else if (P->near_after == 1)
         CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
       if (P->near_ctas == 1)
@@ -1036,23 +1169,44 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       nk++;
       prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
+      tr("near", s1);
     };
     if (!far || P->near_after <= 1) launch_near();
+    // float32 + near + far: the (compute-bound) matrix-free reception runs at
+    // the end of the far branch into phif, overlapping the near field; the
+    // join is followed by one combining scatter phi[perm] = phin + phif.
+    const bool rfar = far && near && P->u_mf && P->recv_far && std::is_same<T, float>::value;
     if (far) {
       far_pass(P->split, [&](int pos) {
         if (pos == P->near_after) launch_near();
       });
       launch_near();
       prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
+      if (rfar) {
+        if constexpr (std::is_same<T, float>::value) {
+          prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
+          launch_reception_exp<R>(P, o, nullptr, nullptr, reinterpret_cast<float*>(P->phif.p), R, s0);
+          nk++;
+          tr("reception", s0);
+          prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
+        }
+      }
     }
     CUDA_OK(cudaEventRecord(P->ev_join, s1));
     CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
-    finish();
+    if (rfar) {
+      scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
+          phin, reinterpret_cast<const T*>(P->phif.p), P->perm.p, phi, P->pt_begin, nloc, P->ldv);
+      nk++;
+      tr("combine", s0);
+    } else {
+      finish();
+    }
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL + 1, s0);
   } else if (stage == 1) {
     gather();
     if (far) {
-      launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, s0);
+      launch_radiation<T, R>(P, qt, s, s0);
       nk++;
       up_pass();
     }
@@ -1149,7 +1303,7 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
         if (ty != cudaGraphNodeTypeEventRecord) continue;
         cudaEvent_t ev;
         CUDA_OK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
-        for (int slot = 0; slot < 2 * NESA_N_STAGES; ++slot)
+        for (int slot = 0; slot < 2 * NESA_N_STAGES + kTraceSlots; ++slot)
           if (P->cap_events[slot] == ev) ent.ev_nodes.emplace_back(nd, slot);
       }
     }
@@ -1159,7 +1313,7 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
   }
   if (flags & NESA_PROFILE) {
     if (P->prof_used == P->prof_events.size()) {
-      std::vector<cudaEvent_t> evs(2 * NESA_N_STAGES);
+      std::vector<cudaEvent_t> evs(2 * NESA_N_STAGES + kTraceSlots);
       for (auto& e : evs) CUDA_OK(cudaEventCreate(&e));
       P->prof_events.push_back(evs);
     }
@@ -1216,12 +1370,17 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
     if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
+    if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
     P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
     if (const char* us = std::getenv("NESA_U_STORED")) P->u_mf = P->u_mf && std::atoi(us) == 0;
+    P->v_mom = d->op_dtype == NESA_F32 && !d->V_blob;
+    if (const char* vs = std::getenv("NESA_V_STORED")) P->v_mom = P->v_mom && std::atoi(vs) == 0;
+    if (const char* tr = std::getenv("NESA_TRACE")) P->trace = std::atoi(tr) != 0;
+    if (const char* rf = std::getenv("NESA_RECV_FAR")) P->recv_far = std::atoi(rf) != 0;
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     if (P->leaf_end <= P->leaf_begin) {
@@ -1320,6 +1479,10 @@ NESA_API int64_t nesa_plan_stat(nesa_plan* P, int32_t which) {
       return P->nearset.grid;
     case NESA_STAT_KERNELS_PER_MATVEC:
       return P->kernels_per_matvec;
+    case NESA_STAT_V_MOMENTS:
+      return P->v_mom ? P->v_nm : 0;
+    case NESA_STAT_U_TERMS:
+      return P->u_mf ? P->u_nt : 0;
     default:
       return -1;
   }
@@ -1333,6 +1496,36 @@ NESA_API int nesa_profile_reset(nesa_plan* P) {
     P->prof_used = 0;
     return NESA_OK;
   })
+}
+
+// Diagnostics (NESA_TRACE=1 plans, profiled products): time of the event
+// after each traced kernel of the LAST profiled product, in ms from its start.
+NESA_API int nesa_trace_read(nesa_plan* P, float* ms, int32_t max) {
+  try {
+    require(P != nullptr && ms != nullptr, "null argument");
+    CUDA_OK(cudaSetDevice(P->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    if (P->prof_used == 0) return 0;
+    const auto& evs = P->prof_events[P->prof_used - 1];
+    int n = 0;
+    for (size_t i = 0; i < P->trace_names.size() && n < max; ++i) {
+      float t = -1.f;
+      if (cudaEventElapsedTime(&t, evs[2 * NESA_STAGE_TOTAL], evs[2 * NESA_N_STAGES + i]) != cudaSuccess) {
+        cudaGetLastError();
+        t = -1.f;
+      }
+      ms[n++] = t;
+    }
+    return n;
+  } catch (const NesaError& e) {
+    g_last_error = e.what();
+    return -e.code;
+  }
+}
+
+NESA_API const char* nesa_trace_name(nesa_plan* P, int32_t i) {
+  if (P == nullptr || i < 0 || size_t(i) >= P->trace_names.size()) return "";
+  return P->trace_names[size_t(i)].c_str();
 }
 
 NESA_API int nesa_profile_read(nesa_plan* P, int32_t stage, float* ms, int32_t max) {

@@ -272,6 +272,15 @@ class NesaPlan:
             raise RuntimeError(self.lib.nesa_last_error().decode())
         return np.frombuffer(buf, dtype=np.float32, count=n).astype(np.float64)
 
+    def trace_read(self, max_n: int = 64) -> list[tuple[str, float]]:
+        """(kernel, ms from the product start) after each kernel of the last
+        profiled product; needs NESA_TRACE=1 when the plan was created."""
+        buf = (ctypes.c_float * max_n)()
+        n = self.lib.nesa_trace_read(self.handle, buf, max_n)
+        if n < 0:
+            raise RuntimeError(self.lib.nesa_last_error().decode())
+        return [(self.lib.nesa_trace_name(self.handle, i).decode(), float(buf[i])) for i in range(n)]
+
 
 def algorithmic_bytes(plan: NesaPlan, nrhs_real: int, near: bool = True,
                       far: bool = True) -> dict:

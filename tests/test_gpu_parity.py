@@ -157,8 +157,16 @@ def test_plan_stats(golden):
     e_near = sum(int(sizes[i]) * int(sizes[a.nbr_idx[a.nbr_ptr[i]:a.nbr_ptr[i + 1]]].sum())
                  for i in range(a.level_count[tree.L]))
     assert plan.stat("near_entries") == e_near
-    assert plan.stat("v_entries") == tree.n_points * params.Q
+    # float32 plans from geometry: radiation and reception through circle
+    # expansions, no stored V / U
+    assert plan.stat("v_entries") == 0 and plan.stat("u_entries") == 0
+    assert 8 <= plan.stat("v_moments") <= 96 and 4 <= plan.stat("u_terms") <= 96
     assert plan.stat("d_refs") == int(a.int_ptr[-1])
+    plan.close()
+    plan = NesaPlan(tree, params, dtype="f64")
+    assert plan.stat("v_entries") == tree.n_points * params.Q
+    assert plan.stat("u_entries") == tree.n_points * params.Q
+    assert plan.stat("v_moments") == 0 and plan.stat("u_terms") == 0
     plan.close()
 
 
@@ -281,3 +289,35 @@ def test_f32_tall_leaves_matrix_free():
     q = np.random.default_rng(3).standard_normal(6000)
     ref = oracle_mvp(tree, build_all(tree, params), q)
     assert rel_l2(mvp(tree, params, q.astype(np.float32)), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["c1_wave_2000", "c2_circle_20000", "ellipse_plates_20000"])
+def test_f32_stored_v_u_paths(monkeypatch, golden, name):
+    # the stored-operator float32 paths (blockgemv V / U) stay correct when the
+    # circle expansions are switched off
+    monkeypatch.setenv("NESA_V_STORED", "1")
+    monkeypatch.setenv("NESA_U_STORED", "1")
+    g = golden(name)
+    tree, params = _problem(g)
+    q = g["q"].astype(np.complex64 if np.iscomplexobj(g["q"]) else np.float32)
+    plan = NesaPlan(tree, params, dtype="f32")
+    assert plan.stat("v_moments") == 0 and plan.stat("u_terms") == 0
+    assert plan.stat("v_entries") == tree.n_points * params.Q
+    plan.close()
+    assert rel_l2(mvp(tree, params, q), g["phi"]) <= 1e-5
+
+
+@pytest.mark.parametrize("nm,nt", [(8, 4), (96, 96)])
+def test_f32_expansion_term_counts(monkeypatch, golden, nm, nt):
+    # forced term counts: too few terms must show up as error, many terms
+    # must stay within the float32 tolerance (no overflow / breakdown)
+    monkeypatch.setenv("NESA_V_MOMENTS", str(nm))
+    monkeypatch.setenv("NESA_U_TERMS", str(nt))
+    g = golden("ellipse_plates_20000")
+    tree, params = _problem(g)
+    q = g["q"].astype(np.complex64 if np.iscomplexobj(g["q"]) else np.float32)
+    err = rel_l2(mvp(tree, params, q, near=False), g["phi_far"])
+    if nm >= 64:
+        assert err <= 1e-5
+    else:
+        assert err > 1e-5

@@ -1,6 +1,8 @@
 """Top stall lines of one kernel in an ncu report (CUDA source view).
 
-    python tools/ncu_source.py REPORT.ncu-rep KERNEL_REGEX [launch_skip] [top]
+    python tools/ncu_source.py REPORT.ncu-rep KERNEL_REGEX [launch_skip] [top] [inst]
+
+(``inst``: rank lines by executed warp instructions instead of stall samples)
 """
 import csv
 import io
@@ -27,6 +29,8 @@ def main():
             d["Source"] = r[1]
             recs.append(d)
     key = "Warp Stall Sampling (All Samples)"
+    if len(sys.argv) > 5 and sys.argv[5] == "inst":
+        key = "Instructions Executed"
     tot = sum(float(x[key] or 0) for x in recs) or 1.0
     stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
     for x in sorted(recs, key=lambda x: -float(x[key] or 0))[:top]:
