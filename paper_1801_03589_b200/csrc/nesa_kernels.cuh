@@ -672,6 +672,188 @@ __global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R
   }
 }
 
+// ----------------------------------------------------------------------------
+// Fused coarse levels.  The levels l0+1 .. lf (too small to fill the GPU) run
+// as ONE kernel per pass instead of one launch per level:
+//
+//  fused_up_kernel    one CTA per level-lf group.  A CTA computes
+//                     s[g] = sum of its children's T (fixed child order) and
+//                     T[g] = C_{lv, quad g} s[g], then counts itself in at its
+//                     parent; the LAST child to arrive continues with the
+//                     parent (fence + atomic: the parent's sum is formed once,
+//                     by one CTA, in child order -> deterministic).  At level
+//                     l0 only s is formed (the old top-level sum).  No CTA
+//                     ever waits, so residency does not matter.
+//  fused_down_kernel  one CTA per level-lf group walks its ancestor chain top
+//                     down.  Each ancestor is CLAIMED by one CTA (CAS 0 -> 1),
+//                     which computes o[a] += B_{lv, quad a} o[parent a] and
+//                     publishes it (state 2); other CTAs needing it wait.  A
+//                     claimer only ever reads finished parents, so every wait
+//                     ends (no deadlock even if CTAs are not co-resident).
+//
+// The up kernel also resets the down-claim state of every group it passes
+// and the last arriver resets the parent's counter, so no memset is needed
+// between products.
+// ----------------------------------------------------------------------------
+template <typename T>
+struct FusedArgs {
+  const T* MT;            // C (up) / B (down) tables, padded + transposed
+  size_t mstride;         // elements per matrix; level ci = lv - l0 >= 1: ((ci-1)*4 + quad)
+  const int32_t* quad;    // [G]
+  const int64_t* parent;  // [G]
+  const int2* uchild;     // [G] local children (first id, count)
+  const int32_t* anc;     // down: [count][D] ancestors of the level-lf groups (level lf-1 first)
+  int* cnt;               // up: arrivals per group
+  int* state;             // down: 0 free, 1 claimed, 2 done
+  T* Tup;
+  T* s;
+  T* o;
+  int64_t first, count;   // level-lf groups (local)
+  int lf, l0, L, Q, D;
+};
+
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+constexpr int kFusedThreads = 128;
+
+template <typename T>
+__host__ __device__ inline size_t fused_smem_bytes(int Q, int R) {
+  return mat_bytes(Q, sizeof(T)) + ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 64;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
+  const size_t mb = mat_bytes(Q, sizeof(T));
+  T* M = reinterpret_cast<T*>(smem);
+  T* X = reinterpret_cast<T*>(smem + mb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + ((size_t(QR) * sizeof(T) + 15) & ~size_t(15)));
+  int64_t* nxt = reinterpret_cast<int64_t*>(bar + 1);
+  int64_t g = a.first + blockIdx.x;
+  int lv = a.lf;
+  auto load_mat = [&](int lvx, int64_t gx) {
+    mbar_arrive_expect_tx(bar, uint32_t(mb));
+    bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * 4 + a.quad[gx]) * a.mstride, uint32_t(mb), bar);
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    if (lv > a.l0) load_mat(lv, g);   // constant data: before the dependency wait
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  uint32_t phase = 0;
+  while (true) {
+    if (tid == 0) a.state[g] = 0;
+    const int2 uc = a.uchild[g];
+    for (int w = tid; w < QR; w += kFusedThreads) {
+      T v;
+      if (lv == a.L) {
+        v = __ldcg(a.s + g * QR + w);
+      } else {
+        v = T(0);
+        for (int k = 0; k < uc.y; ++k) v += __ldcg(a.Tup + (int64_t(uc.x) + k) * QR + w);
+        a.s[g * QR + w] = v;
+      }
+      X[w] = v;
+    }
+    if (lv == a.l0) break;
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    for (int w = tid; w < QR; w += kFusedThreads) {
+      const int k = w / R, rr = w - (w / R) * R;
+      T acc = T(0);
+#pragma unroll 8
+      for (int j = 0; j < Q; ++j) acc = fma(M[j * Qp + k], X[j * R + rr], acc);
+      a.Tup[g * QR + w] = acc;
+    }
+    __syncthreads();  // T[g] written, M and X consumed
+    if (tid == 0) {
+      const int64_t p = a.parent[g];
+      __threadfence();
+      const int old = atomicAdd(a.cnt + p, 1);
+      const bool last = old == a.uchild[p].y - 1;
+      if (last) {
+        a.cnt[p] = 0;
+        __threadfence();
+        if (lv - 1 > a.l0) load_mat(lv - 1, p);
+      }
+      *nxt = last ? p : -1;
+    }
+    __syncthreads();
+    const int64_t p = *nxt;
+    if (p < 0) break;
+    g = p;
+    --lv;
+  }
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
+  const size_t mb = mat_bytes(Q, sizeof(T));
+  T* M = reinterpret_cast<T*>(smem);
+  T* X = reinterpret_cast<T*>(smem + mb);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + ((size_t(QR) * sizeof(T) + 15) & ~size_t(15)));
+  int* flag = reinterpret_cast<int*>(bar + 1);
+  const int64_t g = a.first + blockIdx.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // o holds the translation sums
+  uint32_t phase = 0;
+  for (int i = a.D - 1; i >= -1; --i) {
+    const int64_t x = i >= 0 ? int64_t(a.anc[blockIdx.x * int64_t(a.D) + i]) : g;
+    const int lvx = a.lf - 1 - i;
+    if (i >= 0) {
+      __syncthreads();  // everyone has read the previous flag
+      if (tid == 0) {
+        int st = atomicCAS(a.state + x, 0, 1);
+        if (st == 1) {
+          while (ld_acquire_s32(a.state + x) != 2) __nanosleep(128);
+          st = 2;
+        }
+        *flag = st;
+      }
+      __syncthreads();
+      if (*flag != 0) continue;  // finished by another CTA
+    }
+    // o[x] += B_{lvx, quad x} o[parent x]
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar, uint32_t(mb));
+      bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * 4 + a.quad[x]) * a.mstride, uint32_t(mb), bar);
+    }
+    const int64_t px = a.parent[x];
+    for (int w = tid; w < QR; w += kFusedThreads) X[w] = __ldcg(a.o + px * QR + w);
+    __syncthreads();
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    for (int w = tid; w < QR; w += kFusedThreads) {
+      const int k = w / R, rr = w - (w / R) * R;
+      T acc = T(0);
+#pragma unroll 8
+      for (int j = 0; j < Q; ++j) acc = fma(M[j * Qp + k], X[j * R + rr], acc);
+      a.o[x * QR + w] = __ldcg(a.o + x * QR + w) + acc;
+    }
+    __syncthreads();  // o[x] written, M and X consumed
+    if (i >= 0 && tid == 0) {
+      __threadfence();
+      atomicExch(a.state + x, 2);
+    }
+  }
+}
+
 // s[c] = sum_k T[first child + k] for the coarsest level (no transfer above).
 template <typename T, int R>
 __global__ void sum_children_kernel(const int64_t* __restrict__ child_first,
@@ -1104,25 +1286,46 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
   pdl_trigger();
   pdl_wait();  // amplitudes come from the previous kernel in the chain
   if constexpr (MODE == kLvlUpSum) {
-    // X[p] = s[order p] = ordered sum of its children's T (also stored to s)
-    for (int p = warp; p < n; p += 4) {
-      const int64_t c = a.order[t0 + p];
-      const int2 kr = a.ochild[t0 + p];
-      for (int w = 4 * lane; w < W::QR; w += 128) {
-        T v[4] = {T(0), T(0), T(0), T(0)};
-        T t[4][4];
+    // X[p] = s[order p] = ordered sum of its children's T (also stored to s).
+    // Warp w sums groups w, w+4, ...: in batches of GB groups, every child
+    // load of the batch is issued before any sum (one memory round trip per
+    // batch instead of one per group).
+    constexpr int GB = 4;
+    constexpr int NW = W::QR / 128 > 0 ? W::QR / 128 : 1;  // 4-element slices per lane
+    for (int p0 = warp; p0 < n; p0 += 4 * GB) {
+      int64_t cid[GB];
+      int2 kr[GB];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < kr.y) ld4(a.Tin + (int64_t(kr.x) + k) * W::QR + w, t[k]);
+      for (int b = 0; b < GB; ++b) {
+        const int p = p0 + 4 * b;
+        cid[b] = p < n ? int64_t(a.order[t0 + p]) : 0;
+        kr[b] = p < n ? a.ochild[t0 + p] : make_int2(0, 0);
+      }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < kr.y)
+      for (int sl = 0; sl < NW; ++sl) {
+        const int w = 4 * lane + 128 * sl;
+        if (w >= W::QR) break;
+        T t[GB][4][4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] += t[k][i];
+        for (int b = 0; b < GB; ++b)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          a.s[c * W::QR + w + i] = v[i];
-          X[p * W::XS + w + i] = v[i];
+          for (int k = 0; k < 4; ++k)
+            if (k < kr[b].y) ld4(a.Tin + (int64_t(kr[b].x) + k) * W::QR + w, t[b][k]);
+#pragma unroll
+        for (int b = 0; b < GB; ++b) {
+          const int p = p0 + 4 * b;
+          if (p >= n) break;
+          T v[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < kr[b].y)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) v[i] += t[b][k][i];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            a.s[cid[b] * W::QR + w + i] = v[i];
+            X[p * W::XS + w + i] = v[i];
+          }
         }
       }
     }

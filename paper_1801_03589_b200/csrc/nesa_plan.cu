@@ -309,12 +309,19 @@ struct nesa_plan {
   std::vector<DevBuf<int32_t>> down_order;  // per level (index lv-l0): children by quadrant
   std::vector<DevBuf<int32_t>> down_par;    // parents of down_order
   std::vector<DevBuf<int2>> down_child;     // local child range of down_order entries
+  // fused coarse levels l0+1 .. fused_lf (one kernel per pass; see
+  // nesa_kernels.cuh "Fused coarse levels"); fused_lf == l0: off
+  bool fused = true;
+  int fused_lf = 0;
+  DevBuf<int2> uchild;                      // [G] local children (first, count)
+  DevBuf<int32_t> fused_anc;                // [count(lf)][lf - l0 - 1] ancestors
+  DevBuf<int> fused_cnt, fused_state;       // [G] arrival counters / claim states
   int qs = 4;                               // quadrant slots staged per round
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
   int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
   int near_waves = 1;                       // near-field grid = waves x resident CTAs
   bool priority = true;                     // far-field stream scheduled first
-  bool split = false;                       // fine-level translation on a side stream
+  bool split = true;                        // fine-level translation on a side stream
   int near_after = 1;                       // where the near branch forks (see enqueue_T)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
   bool recv_far = false;                    // reception in the far branch (u_mf only)
@@ -531,6 +538,43 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     P->down_child[li].upload(och);
   }
+  // fused coarse levels: l0+1 .. fused_lf are the levels the wide kernels do
+  // not take (contiguous from the top)
+  P->fused_lf = P->l0;
+  if (P->fused) {
+    for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
+      const bool wide = Q == 64 && P->loc_count[lv - P->l0] >= P->wide_level;
+      if (wide || P->loc_count[lv - P->l0] == 0) break;
+      P->fused_lf = lv;
+    }
+  }
+  if (P->fused_lf > P->l0) {
+    std::vector<int2> uc(static_cast<size_t>(G), int2{0, 0});
+    for (int lv = P->l0; lv < P->L; ++lv) {
+      const int li = lv - P->l0;
+      const int64_t lo = P->loc_first[li + 1], hi = lo + P->loc_count[li + 1];
+      for (int64_t k = lo; k < hi; ++k) {
+        const int64_t p = d->parent[k];
+        if (uc[p].y == 0) uc[p].x = int(k);
+        require(k == uc[p].x + uc[p].y, "children must be consecutive ids");
+        uc[p].y += 1;
+      }
+    }
+    P->uchild.upload(uc);
+    const int li = P->fused_lf - P->l0;
+    const int D = P->fused_lf - P->l0 - 1;
+    std::vector<int32_t> anc(static_cast<size_t>(std::max<int64_t>(1, P->loc_count[li] * D)), 0);
+    for (int64_t i = 0; i < P->loc_count[li]; ++i) {
+      int64_t x = P->loc_first[li] + i;
+      for (int k = 0; k < D; ++k) {
+        x = d->parent[x];
+        anc[size_t(i * D + k)] = int32_t(x);
+      }
+    }
+    P->fused_anc.upload(anc);
+    P->fused_cnt.alloc(size_t(G));    // zero-filled
+    P->fused_state.alloc(size_t(G));
+  }
   // wide levels (>= split_lv) get their translation on a side stream as soon
   // as their source amplitudes are final (see enqueue_T)
   P->split_lv = P->L + 1;
@@ -664,7 +708,11 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
   }
-  chunk_and_balance(hn, es, P->near_waves * P->near_ctas * P->n_sm);
+  {
+    int ng = P->near_waves * P->near_ctas * P->n_sm;
+    if (const char* e = std::getenv("NESA_NEAR_GRID")) ng = std::max(1, std::atoi(e));
+    chunk_and_balance(hn, es, ng);
+  }
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
@@ -846,28 +894,38 @@ template <typename T, int R>
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeStore>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(blockgemv_smem_bytes<T, R, kModeStore>())));
-  CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeScatter>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(blockgemv_smem_bytes<T, R, kModeScatter>())));
-  CUDA_OK(cudaFuncSetAttribute(blockgemv_kernel<T, R, kModeStore, 6>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(blockgemv_smem_bytes<T, R, kModeStore, 6>())));
+  // NESA_CARVEOUT=c (0..100): every kernel asks for the same shared-memory
+  // carveout (measured: the driver default is faster for this schedule)
+  int carve = -1;
+  if (const char* e = std::getenv("NESA_CARVEOUT")) carve = std::atoi(e);
+  auto attr = [carve](auto* fn, int smem) {
+    if (smem >= 0)
+      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (carve >= 0)
+      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  };
+  attr(blockgemv_kernel<T, R, kModeStore>, int(blockgemv_smem_bytes<T, R, kModeStore>()));
+  attr(blockgemv_kernel<T, R, kModeScatter>, int(blockgemv_smem_bytes<T, R, kModeScatter>()));
+  attr(blockgemv_kernel<T, R, kModeStore, 6>, int(blockgemv_smem_bytes<T, R, kModeStore, 6>()));
   const int lim = 220 * 1024;
-  CUDA_OK(cudaFuncSetAttribute(tgemm_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(tgemm_wt_kernel<T, R, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(level_wt_kernel<T, R, 64, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(level_wt_kernel<T, R, 64, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(level_wt_kernel<T, R, 64, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpLeaf>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlUpSum>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  CUDA_OK(cudaFuncSetAttribute(level_kernel<T, R, kLvlDown>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  attr(tgemm_kernel<T, R>, lim);
+  attr(tgemm_wt_kernel<T, R, 64>, lim);
+  attr(tgemm_wt_kernel<T, R, 32>, lim);
+  attr(level_wt_kernel<T, R, 64, kLvlUpLeaf>, lim);
+  attr(level_wt_kernel<T, R, 64, kLvlUpSum>, lim);
+  attr(level_wt_kernel<T, R, 64, kLvlDown>, lim);
+  attr(level_kernel<T, R, kLvlUpLeaf>, lim);
+  attr(level_kernel<T, R, kLvlUpSum>, lim);
+  attr(level_kernel<T, R, kLvlDown>, lim);
+  attr(gather_kernel<T, R>, -1);
+  attr(scatter_kernel<T, R>, -1);
+  attr(reduce_kernel<T, R>, -1);
+  attr(sum_children_kernel<T, R>, -1);
+  attr(fused_up_kernel<T, R>, lim);
+  attr(fused_down_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
-    CUDA_OK(cudaFuncSetAttribute(radiation_mom_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-    CUDA_OK(cudaFuncSetAttribute(reception_exp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    attr(radiation_mom_kernel<R>, lim);
+    attr(reception_exp_kernel<R>, lim);
   }
   done = true;
 }
@@ -1060,18 +1118,62 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     nk++;
     tr(la.count >= P->wide_level && Q == 64 ? "down_wt" : "down", s0);
   };
+  auto fused_args = [&](const T* MT) {
+    FusedArgs<T> fa{};
+    fa.MT = MT;
+    fa.mstride = mstride;
+    fa.quad = P->quad.p;
+    fa.parent = P->parent.p;
+    fa.uchild = P->uchild.p;
+    fa.anc = P->fused_anc.p;
+    fa.cnt = P->fused_cnt.p;
+    fa.state = P->fused_state.p;
+    fa.Tup = Tup;
+    fa.s = s;
+    fa.o = o;
+    const int li = P->fused_lf - P->l0;
+    fa.first = P->loc_first[li];
+    fa.count = P->loc_count[li];
+    fa.lf = P->fused_lf;
+    fa.l0 = P->l0;
+    fa.L = P->L;
+    fa.Q = Q;
+    fa.D = P->fused_lf - P->l0 - 1;
+    return fa;
+  };
+  const bool fused = P->fused_lf > P->l0;
+  const size_t fsm = fused_smem_bytes<T>(Q, R);
+  // upward transfers of the fused coarse levels + the top-level sum
+  auto fused_up = [&]() {
+    const FusedArgs<T> fa = fused_args(CT);
+    launch_pdl(P->pdl, fused_up_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
+    nk++;
+    tr("up_fused", s0);
+  };
+  auto fused_down = [&]() {
+    const FusedArgs<T> fa = fused_args(BT);
+    launch_pdl(P->pdl, fused_down_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
+    nk++;
+    tr("down_fused", s0);
+  };
   // Far field.  The wide (fine) levels' translation + reduce run on s2 as
   // soon as their s is final, concurrently with the coarse end of the
   // upward chain, the coarse translations and the coarse downward levels.
   auto far_pass = [&](bool split, const std::function<void(int)>& hook) {
     const bool fine = split && P->split_lv <= P->L;
     for (int lv = P->L; lv > P->l0; --lv) {
+      if (fused && lv <= P->fused_lf) break;
       up_level(lv);
       if (lv == P->L) hook(2);
       if (fine && lv == P->split_lv) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     }
     if (P->L == P->split_lv && fine && P->L == P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
-    top_sum();
+    if (fused) {
+      fused_up();
+      if (P->fused_lf == P->L) hook(2);
+    } else {
+      top_sum();
+    }
     hook(3);
     if (fine && P->split_lv == P->l0 && P->L > P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     if (fine) {
@@ -1087,7 +1189,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     }
     hook(4);
     bool joined = !fine;
+    if (fused) fused_down();
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
+      if (fused && lv <= P->fused_lf) continue;
       if (!joined && lv >= P->split_lv) {
         CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
         joined = true;
@@ -1097,13 +1201,21 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (!joined) CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
   };
   auto up_pass = [&]() {
-    for (int lv = P->L; lv > P->l0; --lv) up_level(lv);
-    top_sum();
+    for (int lv = P->L; lv > P->l0; --lv) {
+      if (fused && lv <= P->fused_lf) break;
+      up_level(lv);
+    }
+    if (fused)
+      fused_up();
+    else
+      top_sum();
   };
   auto down_pass = [&]() {
     translate(0, P->n_tunits, s0);
     reduce(0, P->n_red, s0);
-    for (int lv = P->l0 + 1; lv <= P->L; ++lv) down_level(lv);
+    if (fused) fused_down();
+    for (int lv = P->l0 + 1; lv <= P->L; ++lv)
+      if (!fused || lv > P->fused_lf) down_level(lv);
   };
   auto gather = [&]() {
     gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N, P->ldv);
@@ -1138,18 +1250,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     // down: compute-bound, overlaps the memory-bound near field} -> join ->
     // reception + scatter
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
-    gather();
-    if (far) {
-      prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
-      launch_radiation<T, R>(P, qt, s, s0);
-      nk++;
-      tr("radiation", s0);
-    }
-    // Near branch: forks from s0 at position `near_after` (0/1: after
-    // radiation, 1 adds a no-op event node so the first far-field kernel is
-    // launched -- and resident -- before the persistent near-field CTAs;
-    // 2: after the leaf-level upward kernel; 3: after the upward pass;
-    // 4: after translation).
+    // Near branch: forks from s0 at position `near_after` (-1/-2: before the
+    // radiation; 0/1: after it; -1 and 1 add a no-op event node so the
+    // far-field kernel is launched -- and resident -- before the persistent
+    // near-field CTAs; 2: after the leaf-level upward kernel; 3: after the
+    // upward pass; 4: after translation).
     bool forked = false;
     auto launch_near = [&]() {
       if (forked) return;
@@ -1157,11 +1262,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       CUDA_OK(cudaEventRecord(P->ev_fork, s0));
       CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
       if (!near) return;
-      if (prof) {
+      if (prof)
         prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
-        tr("near_begin", s1);
-      }
-      else if (P->near_after == 1)
+      else if (P->near_after == 1 || P->near_after == -1)
         CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
       if (P->near_ctas == 1)
         launch_blockgemv<T, R, kModeStore, 6>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
@@ -1171,6 +1274,14 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
       tr("near", s1);
     };
+    gather();
+    if (far && P->near_after < 0) launch_near();
+    if (far) {
+      prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
+      launch_radiation<T, R>(P, qt, s, s0);
+      nk++;
+      tr("radiation", s0);
+    }
     if (!far || P->near_after <= 1) launch_near();
     // float32 + near + far: the (compute-bound) matrix-free reception runs at
     // the end of the far branch into phif, overlapping the near field; the
@@ -1370,6 +1481,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
     if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
+    if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
     if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
