@@ -117,7 +117,12 @@ struct BGLayout {
   static constexpr size_t kFinBase = MODE == kModeScatter ? size_t(kMaxRows) * R * sizeof(T) : 0;
   static constexpr size_t kStage =
       ((kA + kX + sizeof(StageHdr) + kFinPerm + kFinBase) + 127) & ~size_t(127);
-  static constexpr size_t kRed = size_t(4) * kNCT * R * sizeof(T);
+  // the end-of-item column-lane reduction reuses the finished chunk's A
+  // buffer when it fits (keeps 2 CTAs/SM at ~57 KB, leaving room for the
+  // concurrent far-field kernels); otherwise it gets its own area
+  static constexpr size_t kRedNeed = size_t(4) * kNCT * R * sizeof(T);
+  static constexpr bool kRedInA = kRedNeed <= kA;
+  static constexpr size_t kRed = kRedInA ? 0 : kRedNeed;
   static constexpr size_t kBytes = NST * kStage + kRed + 2 * NST * sizeof(uint64_t) + 16;
   static constexpr size_t offX = kA;
   static constexpr size_t offHdr = kA + kX;
@@ -160,9 +165,9 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
   using Lay = BGLayout<T, R, MODE, NST>;
   constexpr int kStages = NST;
   extern __shared__ __align__(128) unsigned char smem[];
-  T* sRed = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
+  T* const sRedOwn = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(sRed + 4 * kNCT * R) + 15) & ~uintptr_t(15));
+      (reinterpret_cast<uintptr_t>(smem + kStages * Lay::kStage + Lay::kRed) + 15) & ~uintptr_t(15));
   uint64_t* empty = full + kStages;
 
   const int c0 = a.cta_chunk_ptr[blockIdx.x];
@@ -280,6 +285,11 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
       if (h.flags & 2) {  // last chunk of the item: reduce column lanes + write
         const int64_t* sperm = reinterpret_cast<const int64_t*>(stg + Lay::offPerm);
         const T* sbase = reinterpret_cast<const T*>(stg + Lay::offBase);
+        T* sRed = sRedOwn;
+        if constexpr (Lay::kRedInA) {
+          sRed = reinterpret_cast<T*>(const_cast<unsigned char*>(stg));
+          named_bar_sync(1, kNCT);  // every consumer is done reading this chunk's A
+        }
         if (cl < CL) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -1117,26 +1127,29 @@ __global__ void __launch_bounds__(kTGThreads) tgemm_kernel(const TUnit* __restri
 // words (broadcast) and the four row groups one contiguous 128-byte line, so
 // a warp issues ~4 shared wavefronts per 32 FMAs.
 // ----------------------------------------------------------------------------
-template <typename T, int R, int QT>
+// QT output rows; KT input length (KT = QT for the square far-field
+// operators; the radiation's moment map uses KT > QT).
+template <typename T, int R, int QT, int KT = QT>
 struct TGW {
   static constexpr int RW = QT / 32;
   static constexpr int CW = 4 / RW;
   static constexpr int NC = 32 * CW;       // real columns per pass
   static constexpr int PER = NC / R;       // entries per pass
-  static constexpr int QR = QT * R;
-  static constexpr int XS = (QR + 16 / int(sizeof(T)) - 1) / (16 / int(sizeof(T))) * (16 / int(sizeof(T))) +
-                            16 / int(sizeof(T));
-  static constexpr size_t MB = size_t(QT) * QT * sizeof(T);
+  static constexpr int QR = QT * R;        // output values per entry
+  static constexpr int KR = KT * R;        // input values per entry
+  static constexpr int XS = ((KR > QR ? KR : QR) + 16 / int(sizeof(T)) - 1) / (16 / int(sizeof(T))) *
+                                (16 / int(sizeof(T))) + 16 / int(sizeof(T));
+  static constexpr size_t MB = size_t(KT) * QT * sizeof(T);
   static constexpr size_t XB = (size_t(PER) * XS * sizeof(T) + 127) & ~size_t(127);
   static constexpr size_t SMEM = MB + 2 * XB + 2 * 4 * PER + 64;
 };
 
-template <typename T, int R, int QT>
+template <typename T, int R, int QT, int KT = QT>
 __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__ units,
                                                        const TEnt* __restrict__ ents,
                                                        const T* __restrict__ DT,
                                                        const T* __restrict__ s, T* Y) {
-  using W = TGW<T, R, QT>;
+  using W = TGW<T, R, QT, KT>;
   extern __shared__ __align__(128) unsigned char smem[];
   T* Dm = reinterpret_cast<T*>(smem);
   T* Xb0 = reinterpret_cast<T*>(smem + W::MB);
@@ -1153,8 +1166,8 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
   // the 8 lanes of a row group read 8 consecutive entries (conflict-free)
   constexpr int NE = 4 / R;
   const int E0 = 32 * wc / R;
-  constexpr uint32_t kVB = uint32_t(W::QR * sizeof(T));
-  const size_t mb = mat_bytes(QT, sizeof(T));
+  constexpr uint32_t kVB = uint32_t(W::KR * sizeof(T));
+  const size_t mb = W::MB;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -1174,7 +1187,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
       for (int p = lane; p < n; p += 32) {
         const TEnt te = ents[eb + p];
         eid[p] = te.e;
-        bulk_g2s(X + p * W::XS, s + int64_t(te.src) * W::QR, kVB, b);
+        bulk_g2s(X + p * W::XS, s + int64_t(te.src) * W::KR, kVB, b);
       }
     }
   };
@@ -1203,7 +1216,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
       const T* mp = Dm + row0;
       const T* xp = X + (E0 + tc) * W::XS;
 #pragma unroll 4
-      for (int j = 0; j < QT; ++j) {
+      for (int j = 0; j < KT; ++j) {
         T m0[4], m1[4], x[4];
         ld4(mp + j * QT, m0);
         ld4(mp + j * QT + 4, m1);
@@ -1252,22 +1265,29 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
 // or summed from the children (UpSum); each warp computes a 32 x 32 block
 // with the conflict-free lane layout of tgemm_wt_kernel.
 // ----------------------------------------------------------------------------
-template <typename T, int R, int QT>
+#ifndef LVW_SLOTS
+#define LVW_SLOTS 1
+#endif
+template <typename T, int R, int QT, int MODE>
 struct LVW {
   using W = TGW<T, R, QT>;
-  static constexpr int kSlots = 2;  // quadrant matrices per round (sorted tiles need <= 2)
-  static constexpr size_t SMEM = kSlots * W::MB + 2 * W::XB + 3 * 64;
+  // quadrant matrices per round: tiles are quadrant-sorted, so only the (at
+  // most 3) boundary tiles of a level need a second round; one slot keeps the
+  // kernel small enough to run 2-3 CTAs per SM beside the near field
+  static constexpr int kSlots = LVW_SLOTS;
+  static constexpr int kXBufs = MODE == 2 ? 2 : 1;  // kLvlDown also stages o[c]
+  static constexpr size_t SMEM = kSlots * W::MB + kXBufs * W::XB + 3 * 64;
 };
 
 template <typename T, int R, int QT, int MODE>
 __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) {
   using W = TGW<T, R, QT>;
-  using LV = LVW<T, R, QT>;
+  using LV = LVW<T, R, QT, MODE>;
   extern __shared__ __align__(128) unsigned char smem[];
   T* M = reinterpret_cast<T*>(smem);                                  // kSlots matrices
   T* X = reinterpret_cast<T*>(smem + LV::kSlots * W::MB);             // inputs / outputs
   T* Oc = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + W::XB);    // down: o[c] (reduce output)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LV::kSlots * W::MB + 2 * W::XB);  // M, X
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LV::kSlots * W::MB + LV::kXBufs * W::XB);  // M, X
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t t0 = int64_t(blockIdx.x) * W::PER;
   const int n = int(a.count - t0 < W::PER ? a.count - t0 : W::PER);
@@ -1495,19 +1515,42 @@ __device__ __forceinline__ float2 cpowf(float2 w, int e) {
   return r;
 }
 
+// w^E for a compile-time E (unrolled square-and-multiply)
+template <int E>
+__device__ __forceinline__ float2 cpow_const(float2 w) {
+  if constexpr (E == 0) {
+    return make_float2(1.f, 0.f);
+  } else if constexpr (E == 1) {
+    return w;
+  } else {
+    const float2 h = cpow_const<E / 2>(w);
+    const float2 h2 = cmulf(h, h);
+    if constexpr (E % 2) return cmulf(h2, w);
+    else return h2;
+  }
+}
+
+constexpr int kMomBufPts = 800;  // staged points per warp batch (8 leaves)
+
 // Radiation through outgoing moments.  Lane group of kMomLanes lanes per
-// leaf, kMomLeavesPerWarp leaves per warp.  Each lane accumulates the moments
-// of every kMomLanes-th point of its leaf in registers (passes of MP moments,
-// 2 R MP = 80 accumulators; the next point's data is prefetched), the group
+// leaf, kMomLeavesPerWarp leaves per warp.  The batch's points (contiguous)
+// are staged in shared memory by cp.async; the next batch's copy is issued
+// as soon as the moments are formed, so it overlaps the A-phase.  Each lane
+// accumulates the moments of every kMomLanes-th point of its leaf in
+// registers (passes of MP moments, 2 R MP = 80 accumulators), the group
 // combines them with a transpose reduction (fixed pairing), then the warp
-// applies A (read through L1, it is shared by every leaf) to its leaves'
-// moments.  smem: per warp mu [leaves][nm][R] float2 (16-byte aligned).
-template <int R>
+// applies A (read through L1, shared by every leaf) to its leaves' moments.
+// smem per warp: points [kMomBufPts] float2, q [kMomBufPts][R], mu
+// [leaves][nm][R] float2 (16-byte rows).
+// MU_OUT: instead of applying A, write the leaf's real moment vector
+// mu^[leaf][kt][R] (row 0 = -log(r) mu_0, rows 2m-1 / 2m = Re / Im mu_m,
+// zero padding) for the warp-tiled GEMM s = A^ mu^ (tgemm_wt_kernel).
+template <int R, bool MU_OUT = false>
 __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
-    int64_t leaf0, int64_t nleaf, int Q, int nm) {
+    int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0) {
   constexpr int MP = 40 / R;           // moments per pass
   constexpr int NV = 2 * R * MP;       // 80 accumulators
   constexpr int NV2 = NV / 2, NV4 = NV / 4;
@@ -1515,39 +1558,64 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
   extern __shared__ float4 sm4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mu_stride = (nm * R + 1) & ~1;  // float2 per leaf, even => 16-byte rows
-  float2* mu = reinterpret_cast<float2*>(sm4) + warp * LW * mu_stride;
+  const size_t per_warp = size_t(kMomBufPts) * (2 + R) + size_t(LW) * mu_stride * 2;  // floats
+  float* wbase = reinterpret_cast<float*>(sm4) + warp * per_warp;
+  float2* Pb = reinterpret_cast<float2*>(wbase);
+  float* Qb = wbase + 2 * kMomBufPts;
+  float2* mu = reinterpret_cast<float2*>(wbase + size_t(kMomBufPts) * (2 + R));
   const int slot = lane / kMomLanes, g = lane % kMomLanes;
-  for (int64_t lw = (int64_t(blockIdx.x) * kExpWarps + warp) * LW; lw < nleaf;
-       lw += int64_t(gridDim.x) * kExpWarps * LW) {
+  const int64_t stride = int64_t(gridDim.x) * kExpWarps * LW;
+  // stage the points of batch lw (if they fit); returns whether staged
+  auto stage = [&](int64_t lw) -> bool {
+    if (lw >= nleaf) return false;
+    const int64_t le = lw + LW < nleaf ? lw + LW : nleaf;
+    const int64_t b0 = leaf_start[leaf0 + lw], b1 = leaf_stop[leaf0 + le - 1];
+    const int np = int(b1 - b0);
+    if (np > kMomBufPts) return false;
+    for (int t = lane; t < np; t += 32) {
+      cp_async<8>(Pb + t, prel + b0 + t);
+      cp_async_n<R * 4>(Qb + t * R, qt + (b0 + t) * R);
+    }
+    cp_async_commit();
+    return true;
+  };
+  int64_t lw = (int64_t(blockIdx.x) * kExpWarps + warp) * LW;
+  bool staged = stage(lw);
+  for (; lw < nleaf; lw += stride) {
     const int64_t li = lw + slot;
     const bool live = li < nleaf;
     const int64_t leaf = leaf0 + (live ? li : 0);
     const int64_t b = leaf_start[leaf];
     const int n = live ? int(leaf_stop[leaf] - b) : 0;
     const float inv = 1.f / leaf_r[leaf];
+    const int64_t b0 = leaf_start[leaf0 + lw];
+    if (staged) cp_async_wait_all();
+    __syncwarp();
     float* muf = reinterpret_cast<float*>(mu + slot * mu_stride);
     for (int m0 = 0; m0 < nm; m0 += MP) {
       float v[NV];
 #pragma unroll
       for (int t = 0; t < NV; ++t) v[t] = 0.f;
-      float2 pn = make_float2(0.f, 0.f);
-      float qn[R];
-      if (g < n) {
-        pn = prel[b + g];
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) qn[rr] = qt[(b + g) * R + rr];
-      }
       for (int j = g; j < n; j += kMomLanes) {
-        const float2 w = make_float2(pn.x * inv, pn.y * inv);
+        float2 p;
         float qv[R];
+        if (staged) {
+          const int t = int(b + j - b0);
+          p = Pb[t];
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) qv[rr] = qn[rr];
-        if (j + kMomLanes < n) {  // prefetch the next point
-          pn = prel[b + j + kMomLanes];
+          for (int rr = 0; rr < R; ++rr) qv[rr] = Qb[t * R + rr];
+        } else {
+          p = prel[b + j];
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) qn[rr] = qt[(b + j + kMomLanes) * R + rr];
+          for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(b + j) * R + rr];
         }
-        float2 z = m0 ? cpowf(w, m0) : make_float2(1.f, 0.f);
+        const float2 w = make_float2(p.x * inv, p.y * inv);
+        float2 z = make_float2(1.f, 0.f);
+        if (m0) {
+          const float2 wp = cpow_const<MP>(w);
+          z = wp;
+          for (int e = MP; e < m0; e += MP) z = cmulf(z, wp);
+        }
 #pragma unroll
         for (int mm = 0; mm < MP; ++mm) {
 #pragma unroll
@@ -1584,7 +1652,30 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
       for (int t = 0; t < NV4; ++t)
         if (vb + t < lim) muf[m0 * R * 2 + vb + t] = v[t];
     }
-    __syncwarp();
+    __syncwarp();  // moments visible; the point buffer is free
+    staged = stage(lw + stride);
+    if constexpr (MU_OUT) {
+#pragma unroll 1
+      for (int l = 0; l < LW; ++l) {
+        const int64_t li2 = lw + l;
+        if (li2 >= nleaf) break;
+        const int64_t lf = leaf0 + li2;
+        const float nl = -logf(leaf_r[lf]);
+        const float2* ml = mu + l * mu_stride;
+        float* dst = s + lf * int64_t(kt) * R;
+        for (int t = lane; t < kt * R; t += 32) {
+          const int row = t / R, rr = t - (t / R) * R;
+          const int m = (row + 1) >> 1;
+          float v = 0.f;
+          if (row == 0)
+            v = nl * ml[rr].x;
+          else if (m < nm)
+            v = (row & 1) ? ml[m * R + rr].x : ml[m * R + rr].y;
+          dst[t] = v;
+        }
+      }
+      __syncwarp();
+    } else {
     // s_k = -log(r) F_k mu_0 + sum_m Re(A_km mu_m): lane owns k = kb + lane
     // and kb + 32 + lane for all the warp's leaves
     for (int kb = 0; kb < Q; kb += 64) {
@@ -1634,7 +1725,9 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
       }
     }
     __syncwarp();
+    }  // !MU_OUT
   }
+  cp_async_wait_all();
 }
 
 // Reception through the incoming expansion.  One warp per leaf, one lane per

@@ -56,18 +56,26 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool own = true;  // false: a view into another buffer
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), own(o.own) {
     o.p = nullptr;
     o.n = 0;
   }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
+  }
+  void view(T* ptr, size_t count) {
+    if (p && own) cudaFree(p);
+    p = ptr;
+    n = count;
+    own = false;
   }
   void alloc(size_t count, size_t pad_bytes = 0) {
-    if (p) cudaFree(p);
+    if (p && own) cudaFree(p);
+    own = true;
     p = nullptr;
     n = count;
     size_t bytes = count * sizeof(T) + pad_bytes;
@@ -322,7 +330,7 @@ struct nesa_plan {
   int near_waves = 1;                       // near-field grid = waves x resident CTAs
   bool priority = true;                     // far-field stream scheduled first
   bool split = true;                        // fine-level translation on a side stream
-  int near_after = 1;                       // where the near branch forks (see enqueue_T)
+  int near_after = -1;                      // where the near branch forks (see enqueue_T)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
   bool recv_far = false;                    // reception in the far branch (u_mf only)
   bool pdl = true;                          // programmatic dependent launch in the far chain
@@ -336,12 +344,21 @@ struct nesa_plan {
   DevBuf<float2> mom_A;                     // [v_nm][Q]: row 0 = (F_k, 0), row m = A_km
   DevBuf<float2> exp_E;                     // [Q][u_nt + 1]: 1, (1/m) e^{-i m theta_k}
   DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
+  // Q = 64: s = A^ mu^ as a warp-tiled GEMM over the leaves (KT = mom_kt)
+  int mom_kt = 0;
+  DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
+  DevBuf<TUnit> mom_units;
+  DevBuf<TEnt> mom_ents;
+  int n_mom_units = 0;
+  DevBuf<unsigned char> mu;                 // [NL][mom_kt][R] moments
   cudaEvent_t ev_mark = nullptr;            // no-op event-record node ahead of the near kernel
 
   // workspace for R real columns
   int ws_R = 0;
   int ldv = 1;  // row stride of the caller's q / phi (elements) for the current capture
   DevBuf<unsigned char> qt, phin, phif, s, o, Y, Tup;
+  DevBuf<unsigned char> farws;              // s | Tup | o, contiguous (one L2 window)
+  size_t l2_persist = 0;                    // bytes of L2 set aside for farws (NESA_L2_PERSIST MB)
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -797,6 +814,32 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
       }
       P->mom_A.upload(A);
+      if (Q == 64 && !std::getenv("NESA_MOM_INKERNEL")) {
+        const int need = 2 * P->v_nm - 1;
+        P->mom_kt = need <= 80 ? 80 : (need <= 127 ? 128 : 0);  // nm <= 64 (16 per lane)
+      }
+      if (P->mom_kt) {
+        // rows: 0 -> F_k (times -log r mu_0), 2m-1 -> Re A_km, 2m -> -Im A_km
+        std::vector<float> AT(size_t(P->mom_kt) * Q, 0.f);
+        for (int k = 0; k < Q; ++k) {
+          AT[k] = A[k].x;
+          for (int m = 1; m < P->v_nm; ++m) {
+            AT[size_t(2 * m - 1) * Q + k] = A[size_t(m) * Q + k].x;
+            AT[size_t(2 * m) * Q + k] = -A[size_t(m) * Q + k].y;
+          }
+        }
+        P->momAT.upload(AT);
+        std::vector<TUnit> units;
+        std::vector<TEnt> ents;
+        for (int64_t a = lb; a < le; ++a) ents.push_back(TEnt{int32_t(a), int32_t(a)});
+        int per = 32;  // one pass of 32 leaves per CTA: the GEMM is latency-bound
+        if (const char* e = std::getenv("NESA_MOM_PER")) per = std::max(1, std::atoi(e));
+        for (size_t i = 0; i < ents.size(); i += per)
+          units.push_back(TUnit{0, int32_t(i), int32_t(std::min(ents.size(), i + per)), 0});
+        P->mom_units.upload(units);
+        P->mom_ents.upload(ents);
+        P->n_mom_units = int(units.size());
+      }
     }
     if (P->u_mf) {
       const int ne = P->u_nt + 1;
@@ -869,10 +912,15 @@ void ensure_workspace(nesa_plan* P, int R) {
   P->qt.alloc(size_t(P->N) * R * es);
   P->phin.alloc(size_t(P->N) * R * es);
   if (P->u_mf && P->recv_far) P->phif.alloc(size_t(P->N) * R * es);
-  P->s.alloc(size_t(P->G) * P->Q * R * es);
-  P->o.alloc(size_t(P->G) * P->Q * R * es);
+  if (P->mom_kt) P->mu.alloc(size_t(P->NL) * P->mom_kt * R * es);
+  {
+    const size_t fb = (size_t(P->G) * P->Q * R * es + 255) & ~size_t(255);
+    P->farws.alloc(3 * fb);
+    P->s.view(P->farws.p, fb);
+    P->Tup.view(P->farws.p + fb, fb);
+    P->o.view(P->farws.p + 2 * fb, fb);
+  }
   P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
-  P->Tup.alloc(size_t(P->G) * P->Q * R * es);
   P->ws_R = R;
 }
 
@@ -925,6 +973,9 @@ void set_smem_attrs() {
   attr(fused_down_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
     attr(radiation_mom_kernel<R>, lim);
+    attr(radiation_mom_kernel<R, true>, lim);
+    attr(tgemm_wt_kernel<float, R, 64, 80>, lim);
+    attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
   }
   done = true;
@@ -962,21 +1013,37 @@ constexpr int kMomCtasPerSM = 4;
 
 // s = V qt: outgoing moments (float32 plans from geometry) or stored V
 template <typename T, int R>
-void launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
+int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value) {
     if (P->v_mom) {
       const int64_t nleaf = P->leaf_end - P->leaf_begin;
       const int64_t per_cta = int64_t(kExpWarps) * kMomLeavesPerWarp;
       const int grid = int(std::max<int64_t>(
           1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(kMomCtasPerSM) * P->n_sm)));
-      const size_t sm = size_t(kExpWarps) * kMomLeavesPerWarp * ((P->v_nm * R + 1) & ~1) * sizeof(float2);
+      const size_t sm = size_t(kExpWarps) *
+                        (size_t(kMomBufPts) * (2 + R) + size_t(kMomLeavesPerWarp) * ((P->v_nm * R + 1) & ~1) * 2) *
+                        sizeof(float);
+      if (P->mom_kt) {
+        float* mu = reinterpret_cast<float*>(P->mu.p);
+        radiation_mom_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
+            P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, mu, P->leaf_begin,
+            nleaf, P->Q, P->v_nm, P->mom_kt);
+        if (P->mom_kt == 80)
+          tgemm_wt_kernel<float, R, 64, 80><<<P->n_mom_units, 128, TGW<float, R, 64, 80>::SMEM, st>>>(
+              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s);
+        else
+          tgemm_wt_kernel<float, R, 64, 128><<<P->n_mom_units, 128, TGW<float, R, 64, 128>::SMEM, st>>>(
+              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s);
+        return 2;
+      }
       radiation_mom_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
           P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, s, P->leaf_begin,
           nleaf, P->Q, P->v_nm);
-      return;
+      return 1;
     }
   }
   launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, st);
+  return 1;
 }
 
 // phi[perm] = phin + U o through the incoming expansion (float32 plans)
@@ -1056,9 +1123,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
       if (lv == P->L)
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64>::SMEM, s0, la);
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64, kLvlUpLeaf>::SMEM, s0, la);
       else
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64>::SMEM, s0, la);
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64, kLvlUpSum>::SMEM, s0, la);
     } else if (lv == P->L) {
       launch_pdl(P->pdl, level_kernel<T, R, kLvlUpLeaf>, grid, kFarThreads, lvl_sm, s0, la);
     } else {
@@ -1110,7 +1177,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-      launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64>::SMEM, s0, la);
+      launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64, kLvlDown>::SMEM, s0, la);
     } else {
       launch_pdl(P->pdl, level_kernel<T, R, kLvlDown>, int((la.count + la.TC - 1) / la.TC),
                  kFarThreads, lvl_sm, s0, la);
@@ -1278,8 +1345,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (far && P->near_after < 0) launch_near();
     if (far) {
       prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
-      launch_radiation<T, R>(P, qt, s, s0);
-      nk++;
+      nk += launch_radiation<T, R>(P, qt, s, s0);
       tr("radiation", s0);
     }
     if (!far || P->near_after <= 1) launch_near();
@@ -1317,8 +1383,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   } else if (stage == 1) {
     gather();
     if (far) {
-      launch_radiation<T, R>(P, qt, s, s0);
-      nk++;
+      nk += launch_radiation<T, R>(P, qt, s, s0);
       up_pass();
     }
   } else {
@@ -1401,6 +1466,26 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
       throw;
     }
     CUDA_OK(cudaStreamEndCapture(P->s0, &g));
+    if (P->l2_persist > 0) {
+      // s / T / o stay L2-resident while the near field streams past them
+      cudaKernelNodeAttrValue av = {};
+      av.accessPolicyWindow.base_ptr = P->farws.p;
+      av.accessPolicyWindow.num_bytes = P->farws.n;
+      av.accessPolicyWindow.hitRatio =
+          float(std::min(1.0, double(P->l2_persist) / double(std::max<size_t>(P->farws.n, 1))));
+      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      size_t nn = 0;
+      CUDA_OK(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      CUDA_OK(cudaGraphGetNodes(g, nodes.data(), &nn));
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        CUDA_OK(cudaGraphNodeGetType(nd, &ty));
+        if (ty == cudaGraphNodeTypeKernel)
+          CUDA_OK(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &av));
+      }
+    }
     nesa_plan::GraphEntry ent;
     CUDA_OK(cudaGraphInstantiate(&ent.exec, g, 0));
     if (flags & NESA_PROFILE) {
@@ -1481,6 +1566,12 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
     if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
+    if (const char* lp = std::getenv("NESA_L2_PERSIST")) {
+      int maxp = 0;
+      CUDA_OK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
+      P->l2_persist = std::min<size_t>(size_t(std::max(0, std::atoi(lp))) << 20, size_t(maxp));
+      if (P->l2_persist > 0) CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, P->l2_persist));
+    }
     if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
     if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
