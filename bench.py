@@ -253,7 +253,7 @@ def run_ours(args):
             engine.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream)
         else:
             plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream,
-                            profile=profile)
+                            profile="near" if profile else False)
 
     prof = engine is None
     for _ in range(max(args.warmup, 3)):
@@ -301,7 +301,7 @@ def run_ours(args):
     roofline = None
     stages = {}
     if prof:
-        for st in ("total", "near", "far", "reception"):
+        for st in ("near",):   # only the near-field events are in the timed graph
             d = plan.profile_read(st)
             stages[st] = float(np.mean(d)) if d.size else None
         near_ms = stages["near"]
@@ -317,25 +317,47 @@ def run_ours(args):
                     "peak_source": peak_src}
     matvec_bw = alg["total"] / (ms_step * 1e-3) / 1e9
 
-    # end to end through the public API with pinned host buffers
+    # end to end through the public API with pinned host buffers: the
+    # pipelined API (H2D of step k+1 and D2H of step k-1 overlap product k;
+    # every step still uploads its q and downloads its phi), and the
+    # synchronous mvp() call for reference
     e2e = None
     if not args.no_e2e and world == 1:
         qh = torch.from_numpy(q).pin_memory()
+        k2 = max(10, min(args.steps, 100))
+        pipe = nesa.MvpPipeline(tree, tables, dtype="f32", is_complex=True)
+        outs = [torch.empty_like(qh).pin_memory() for _ in range(2)]
+        for i in range(4):
+            pipe.submit(qh, outs[i % 2])
+        pipe.synchronize()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(pipe.s_h2d)
+        for i in range(k2):
+            pipe.submit(qh, outs[i % 2])
+        e1.record(pipe.s_d2h)
+        e1.synchronize()
+        e_ms = e0.elapsed_time(e1) / k2
+        # synchronous call
         for _ in range(3):
             nesa.mvp(tree, tables, qh)
         torch.cuda.synchronize()
-        k2 = max(10, min(args.steps, 100))
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
         for _ in range(k2):
             out = nesa.mvp(tree, tables, qh)
-        e1.record(stream)
-        e1.synchronize()
-        e_ms = e0.elapsed_time(e1) / k2
+        s1.record(stream)
+        s1.synchronize()
+        s_ms = s0.elapsed_time(s1) / k2
         e2e = {"value": 1e3 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(qh.numel() * 8),
                "d2h_bytes_per_step": int(out.numel() * 8), "ms_per_step": e_ms,
-               "api": "paper_1801_03589_b200.mvp(tree, tables, pinned torch.complex64 (N,))"}
+               "api": "paper_1801_03589_b200.MvpPipeline(tree, tables).submit(pinned q, pinned phi) "
+                      "x K, synchronize(): every step uploads q and downloads phi; transfers of "
+                      "neighbouring steps overlap the product",
+               "sync_call": {"value": 1e3 / s_ms, "ms_per_step": s_ms,
+                             "api": "paper_1801_03589_b200.mvp(tree, tables, pinned torch.complex64 (N,))"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

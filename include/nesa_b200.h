@@ -61,6 +61,8 @@ typedef enum { NESA_F64 = 0, NESA_F32 = 1 } nesa_dtype;
 #define NESA_NEAR 1u
 #define NESA_FAR 2u
 #define NESA_PROFILE 16u /* record per-stage CUDA events (nesa_profile_*) */
+#define NESA_PROFILE_NEAR 32u /* with NESA_PROFILE: only the near-field stage (its events
+                                 sit on the near branch, off the critical path) */
 
 typedef struct nesa_plan nesa_plan;
 

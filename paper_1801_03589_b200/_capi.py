@@ -23,6 +23,7 @@ NESA_F32 = 1
 NESA_NEAR = 1
 NESA_FAR = 2
 NESA_PROFILE = 16
+NESA_PROFILE_NEAR = 32
 
 STAT = {"near_entries": 0, "v_entries": 1, "u_entries": 2, "d_refs": 3, "n_dtab": 4,
         "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7, "v_moments": 8,

@@ -1067,7 +1067,8 @@ void launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const
 //   stage 2: fork{near | translate, down}, join, reception
 template <typename T, int R>
 int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
-  const bool near = flags & NESA_NEAR, far = flags & NESA_FAR, prof = flags & NESA_PROFILE;
+  const bool near = flags & NESA_NEAR, far = flags & NESA_FAR, profn = flags & NESA_PROFILE;
+  const bool prof = profn && !(flags & NESA_PROFILE_NEAR);  // stage marks on the far path
   cudaStream_t s0 = P->s0, s1 = P->s1;
   T* qt = reinterpret_cast<T*>(P->qt.p);
   T* phin = reinterpret_cast<T*>(P->phin.p);
@@ -1329,8 +1330,8 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       CUDA_OK(cudaEventRecord(P->ev_fork, s0));
       CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
       if (!near) return;
-      if (prof)
-        prof_mark(P, prof, 2 * NESA_STAGE_NEAR, s1);
+      if (profn)
+        prof_mark(P, profn, 2 * NESA_STAGE_NEAR, s1);
       else if (P->near_after == 1 || P->near_after == -1)
         CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
       if (P->near_ctas == 1)
@@ -1338,7 +1339,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       else
         launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       nk++;
-      prof_mark(P, prof, 2 * NESA_STAGE_NEAR + 1, s1);
+      prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, s1);
       tr("near", s1);
     };
     gather();
@@ -1450,7 +1451,8 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
     ensure_workspace<double>(P, R);
   else
     ensure_workspace<float>(P, R);
-  nesa_plan::GraphKey key{q, phi, R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE), stage, ldv};
+  nesa_plan::GraphKey key{q, phi, R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE | NESA_PROFILE_NEAR),
+                          stage, ldv};
   P->ldv = ldv;
   auto itg = P->graphs.find(key);
   if (itg == P->graphs.end()) {

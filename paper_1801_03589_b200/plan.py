@@ -241,11 +241,17 @@ class NesaPlan:
 
     def matvec_ptr(self, q_ptr: int, phi_ptr: int, nrhs: int, is_complex: bool,
                    near: bool = True, far: bool = True, stream: int = 0,
-                   profile: bool = False, stage: int = 0) -> None:
-        """Raw device-pointer product (the C ABI call, stream-ordered)."""
+                   profile=False, stage: int = 0) -> None:
+        """Raw device-pointer product (the C ABI call, stream-ordered).
+
+        ``profile``: True records every stage's events; "near" only the
+        near-field kernel's (no event nodes on the critical path).
+        """
         flags = (_capi.NESA_NEAR if near else 0) | (_capi.NESA_FAR if far else 0)
         if profile:
             flags |= _capi.NESA_PROFILE
+            if profile == "near":
+                flags |= _capi.NESA_PROFILE_NEAR
         if stage == 0:
             rc = self.lib.nesa_matvec(self.handle, ctypes.c_void_p(q_ptr),
                                       ctypes.c_void_p(phi_ptr), nrhs, int(is_complex),

@@ -321,3 +321,25 @@ def test_f32_expansion_term_counts(monkeypatch, golden, nm, nt):
         assert err <= 1e-5
     else:
         assert err > 1e-5
+
+
+def test_pipeline_matches_sync_calls(golden):
+    # overlapped host-to-host products give exactly the synchronous results
+    import torch
+    from paper_1801_03589_b200 import MvpPipeline
+    g = golden("ellipse_plates_20000")
+    tree, params = _problem(g)
+    rng = np.random.default_rng(5)
+    n = tree.n_points
+    qs = [torch.from_numpy((rng.standard_normal(n) + 1j * rng.standard_normal(n))
+                           .astype(np.complex64)).pin_memory() for _ in range(5)]
+    outs = [torch.empty_like(q).pin_memory() for q in qs]
+    pipe = MvpPipeline(tree, params, dtype="f32", is_complex=True)
+    for q, o in zip(qs, outs):
+        pipe.submit(q, o)
+    pipe.synchronize()
+    for q, o in zip(qs, outs):
+        ref = mvp(tree, params, q.numpy())
+        assert np.array_equal(o.numpy(), ref)
+    with pytest.raises(ValueError):
+        pipe.submit(qs[0][:-1], outs[0])
