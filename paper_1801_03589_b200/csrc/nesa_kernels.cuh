@@ -1259,6 +1259,243 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
 }
 
 // ----------------------------------------------------------------------------
+// Translation GEMM on the 5th-generation tensor cores (float32 plans, Q = 64).
+//   Y_e = D_{dtab} s_src(e) for the <= 128 / R entries of a unit, as ONE
+//   M = 128 tile: A = the unit's sources, one row per (entry, component)
+//   (K = 64 = source coefficients), B = D (N = 64 output rows, K-major =
+//   D row-major), accumulator 128 lanes x 64 columns fp32 in TMEM.
+// float32 accuracy from TF32 operands by the 3-term split
+//   D s ~= D_hi s_hi + D_hi s_lo + D_lo s_hi   (x_hi = tf32(x), x_lo = tf32(x - x_hi))
+// (the dropped D_lo s_lo term is ~2^-22 relative): 3 x 8 tcgen05.mma (K = 8
+// each) issued by one thread.  D_hi / D_lo arrive pre-split in the canonical
+// no-swizzle K-major layout (core matrices of 8 rows x 16 bytes; the two K
+// chunks of a core-matrix pair 128 B apart (LBO), 8-row groups 2048 B apart
+// (SBO)) by one bulk copy; the sources are split while being staged.  The
+// epilogue moves TMEM -> registers (tcgen05.ld 32x32b: thread = lane = row)
+// -> smem -> coalesced 16-byte stores of Y.
+// ----------------------------------------------------------------------------
+constexpr int kTcLBO = 128;                  // bytes between the K-adjacent core matrices
+constexpr int kTcSBO = 2048;                 // bytes between 8-row groups (16 K chunks)
+constexpr uint32_t kTcBBytes = 64 * 64 * 4;  // one 64 x 64 tf32 operand (16 KB)
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t y;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
+  return __uint_as_float(y);
+}
+
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((kTcLBO >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((kTcSBO >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // sm100 descriptor version; base offset 0, no swizzle
+  return d;
+}
+
+// kind::tf32, D = F32, A = B = TF32, both K-major, N = 64, M = 128
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
+}
+
+template <int R>
+__global__ void __launch_bounds__(128) tgemm_tc_kernel(const TUnit* __restrict__ units,
+                                                       const TEnt* __restrict__ ents,
+                                                       const float* __restrict__ DTC,
+                                                       const float* __restrict__ s, float* Y) {
+  constexpr int QT = 64, QR = QT * R;
+  constexpr int EPT = 128 / R;  // entries per M = 128 tile
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Bhi = reinterpret_cast<float*>(smem);        // 16 KB
+  float* Blo = Bhi + 4096;                             // 16 KB
+  unsigned char* Ahi = smem + 2 * kTcBBytes;           // 32 KB (128 rows)
+  unsigned char* Alo = Ahi + 2 * kTcBBytes;            // 32 KB
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Alo + 2 * kTcBBytes);  // [0] D, [1] MMA done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  const TUnit u = units[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bar[0], 2 * kTcBBytes);
+    bulk_g2s(Bhi, DTC + size_t(u.dtab) * (2 * 4096), 2 * kTcBBytes, &bar[0]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  pdl_trigger();
+  pdl_wait();  // s comes from the upward pass
+  const int n_all = u.ent_end - u.ent_begin;
+  const int m = tid, e = m / R, rr = m - (m / R) * R;
+  const uint32_t rowoff = uint32_t(m >> 3) * kTcSBO + uint32_t(m & 7) * 16;
+  // this thread's share of tile t0: the R lanes of an entry each hold a
+  // contiguous 1/R of its vector (16 float4: all in flight at once)
+  float4 c[16];
+  int32_t eid = -1;
+  auto load = [&](int t0) {
+    const bool live = t0 + e < n_all;
+    eid = -1;
+    int64_t srcg = 0;
+    if (live) {
+      const TEnt te = ents[u.ent_begin + t0 + e];
+      eid = te.e;
+      srcg = te.src;
+    }
+    const float4* src4 = reinterpret_cast<const float4*>(s + srcg * QR) + rr * 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = live ? src4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto put = [&](int kb, float4 v) {
+    float4 h, l;
+    h.x = tf32_rna(v.x);
+    h.y = tf32_rna(v.y);
+    h.z = tf32_rna(v.z);
+    h.w = tf32_rna(v.w);
+    l.x = tf32_rna(v.x - h.x);
+    l.y = tf32_rna(v.y - h.y);
+    l.z = tf32_rna(v.z - h.z);
+    l.w = tf32_rna(v.w - h.w);
+    *reinterpret_cast<float4*>(Ahi + rowoff + kb * kTcLBO) = h;
+    *reinterpret_cast<float4*>(Alo + rowoff + kb * kTcLBO) = l;
+  };
+  const uint64_t keep = l2_evict_last_policy();  // Y is re-read by reduce_kernel
+  uint32_t phase = 0;
+  load(0);
+  for (int t0 = 0; t0 < n_all; t0 += EPT) {
+    const int eid_t = eid;
+    // ---- A = split(sources): row m = (entry e, component rr), k along K
+    if constexpr (R == 1) {
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb) put(kb, c[kb]);
+    } else if constexpr (R == 2) {
+      // chunk i holds (k, 0), (k, 1), (k+1, 0), (k+1, 1) for k = 2i + 32 rr:
+      // swap the partner's component with the partner lane
+      float mine[32], other[32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        mine[2 * i] = rr ? c[i].y : c[i].x;
+        mine[2 * i + 1] = rr ? c[i].w : c[i].z;
+        other[2 * i] = rr ? c[i].x : c[i].y;
+        other[2 * i + 1] = rr ? c[i].z : c[i].w;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
+#pragma unroll
+      for (int kb = 0; kb < 8; ++kb) {
+        put(rr * 8 + kb, make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]));
+        put((1 - rr) * 8 + kb, make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]));
+      }
+    } else {
+      // R = 4: chunk i = (k, 0..3) for k = i + 16 rr; gather component rr
+      // of every k through the 4 lanes of the entry
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 4 * kb + j, owner = k >> 4, ci = k & 15;
+          // lane (e, owner) holds chunk ci; everyone reads component rr of it
+          const float4 mine4 = c[ci];
+          const float x0 = __shfl_sync(0xffffffffu, mine4.x, (tid & ~3) + owner);
+          const float x1 = __shfl_sync(0xffffffffu, mine4.y, (tid & ~3) + owner);
+          const float x2 = __shfl_sync(0xffffffffu, mine4.z, (tid & ~3) + owner);
+          const float x3 = __shfl_sync(0xffffffffu, mine4.w, (tid & ~3) + owner);
+          v[j] = rr == 0 ? x0 : (rr == 1 ? x1 : (rr == 2 ? x2 : x3));
+        }
+        put(kb, make_float4(v[0], v[1], v[2], v[3]));
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    // ---- MMA: one thread issues 3 x 8 instructions
+    if (tid == 0) {
+      if (t0 == 0) mbar_wait(&bar[0], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t ah = smem_u32(Ahi), al = smem_u32(Alo);
+      const uint32_t bh = smem_u32(Bhi), bl = smem_u32(Blo);
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) {
+        const uint32_t a0 = cc == 2 ? al : ah, b0 = cc == 1 ? bl : bh;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          umma_tf32(tmem, umma_desc_kmajor(a0 + ks * 2 * kTcLBO), umma_desc_kmajor(b0 + ks * 2 * kTcLBO),
+                    (cc | ks) != 0);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&bar[1]))
+                   : "memory");
+    }
+    // ---- prefetch the next tile while the tensor core works
+    if (t0 + EPT < n_all) load(t0 + EPT);
+    mbar_wait(&bar[1], phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- epilogue: lane m of TMEM = row m (entry e, component rr); 64 columns
+    uint32_t r[64];
+    {
+      const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+          "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+          "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+            "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+            "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]),
+            "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
+            "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+            "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+            "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]),
+            "=r"(r[63])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    // stage the tile entry-major in smem (A is consumed), then coalesced
+    // 16-byte stores of whole Y rows
+    constexpr int OS = QR + 4;
+    float* stage = reinterpret_cast<float*>(Ahi);
+    if (eid_t >= 0)
+#pragma unroll
+      for (int k = 0; k < 64; ++k) stage[e * OS + k * R + rr] = __uint_as_float(r[k]);
+    if (rr == 0) reinterpret_cast<int32_t*>(tslot + 4)[e] = eid_t;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    {
+      constexpr int NV = QR / 4;
+      const int32_t* eids = reinterpret_cast<const int32_t*>(tslot + 4);
+      const int n = min(EPT, n_all - t0);
+      for (int i = tid; i < n * NV; i += 128) {
+        const int ee = i / NV, v = i - (i / NV) * NV;
+        const float4 val = *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
+        st16_hint(Y + int64_t(eids[ee]) * QR + 4 * v, val, keep);
+      }
+    }
+    __syncthreads();  // stage (= A) read before the next tile is split into it
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
+// bytes of dynamic shared memory of tgemm_tc_kernel
+constexpr size_t kTcSmem = 6 * size_t(kTcBBytes) + 64 + 4 * 128 + 1024;
+
+// ----------------------------------------------------------------------------
 // Warp-tiled level transfer for Q in {32, 64} on the large levels (same
 // roles as level_kernel).  The tile's groups (sorted by quadrant, so one or
 // two quadrant matrices) are staged group-major by bulk copy (UpLeaf, Down)

@@ -347,6 +347,8 @@ struct nesa_plan {
   // Q = 64: s = A^ mu^ as a warp-tiled GEMM over the leaves (KT = mom_kt)
   int mom_kt = 0;
   DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
+  bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
+  DevBuf<float> DTC;                        // [n_dtab][hi | lo][64 x 64] canonical tf32 D
   DevBuf<TUnit> mom_units;
   DevBuf<TEnt> mom_ents;
   int n_mom_units = 0;
@@ -509,6 +511,31 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
   P->n_dtab = d->n_dtab;
   upload_table_T<T>(P->DT, d->D, d->n_dtab, Q);
+  // tensor-core translation (float32, Q = 64): D split into tf32 hi / lo in
+  // the canonical K-major core-matrix layout (see tgemm_tc_kernel)
+  if (std::is_same<T, float>::value && Q == 64 && P->tc && d->n_dtab > 0) {
+    std::vector<float> h(size_t(d->n_dtab) * 8192);
+    auto tf32 = [](float x) {
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u = (u + 0x1000u) & ~0x1FFFu;  // round to nearest (ties away), 10-bit mantissa
+      float y;
+      std::memcpy(&y, &u, 4);
+      return y;
+    };
+    for (int64_t t = 0; t < d->n_dtab; ++t)
+      for (int nn = 0; nn < 64; ++nn)
+        for (int k = 0; k < 64; ++k) {
+          const float x = float(d->D[(t * 64 + nn) * 64 + k]);
+          const float hi = tf32(x), lo = tf32(x - hi);
+          const size_t off = size_t(nn / 8) * 512 + size_t(k / 4) * 32 + size_t(nn % 8) * 4 + (k % 4);
+          h[size_t(t) * 8192 + off] = hi;
+          h[size_t(t) * 8192 + 4096 + off] = lo;
+        }
+    P->DTC.upload(h);
+  } else {
+    P->tc = false;
+  }
   // quadrant slots per round: keep the level kernels <= ~96 KB so they can
   // co-reside with the persistent near-field CTAs (~110 KB) on one SM
   P->qs = 2;
@@ -868,7 +895,14 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->nnz = d->int_ptr[G];
     P->int_ptr.upload(std::vector<int64_t>(d->int_ptr, d->int_ptr + G + 1));
     require(P->nnz < (int64_t(1) << 31), "too many interaction entries");
-    const int per = kTUnitPasses * (tg_geom(Q).NC / 4);  // sized for R = 4; smaller R packs more
+    // entries per unit: the FFMA kernel runs kTUnitPasses passes (sized for
+    // R = 4); the tensor-core kernel loops over M = 128 tiles and amortises
+    // its D load and TMEM allocation over longer units
+    int per = kTUnitPasses * (tg_geom(Q).NC / 4);
+    if (P->tc) {
+      per = 128;
+      if (const char* e = std::getenv("NESA_TC_PER")) per = std::max(32, std::atoi(e));
+    }
     std::vector<TEnt> ents;
     std::vector<TUnit> units;
     std::vector<std::vector<TEnt>> by_d(size_t(std::max<int64_t>(d->n_dtab, 1)));
@@ -975,6 +1009,7 @@ void set_smem_attrs() {
     attr(radiation_mom_kernel<R>, lim);
     attr(radiation_mom_kernel<R, true>, lim);
     attr(tgemm_wt_kernel<float, R, 64, 80>, lim);
+    attr(tgemm_tc_kernel<R>, int(kTcSmem));
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
   }
@@ -1151,7 +1186,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (u1 <= u0) return;
     const T* DTp = reinterpret_cast<const T*>(P->DT.p);
     const TUnit* up = P->tunits.p + u0;
-    if (Q == 64)
+    if (P->tc) {
+      if constexpr (std::is_same<T, float>::value)
+        launch_pdl(P->pdl && st == s0, tgemm_tc_kernel<R>, u1 - u0, 128, kTcSmem, st, up,
+                   (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+    } else if (Q == 64)
       launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 64>, u1 - u0, 128, TGW<T, R, 64>::SMEM, st,
                  up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y);
     else if (Q == 32)
@@ -1574,6 +1613,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       P->l2_persist = std::min<size_t>(size_t(std::max(0, std::atoi(lp))) << 20, size_t(maxp));
       if (P->l2_persist > 0) CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, P->l2_persist));
     }
+    if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
     if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
     if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;

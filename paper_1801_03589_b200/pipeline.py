@@ -4,25 +4,29 @@ calls overlap.
 ``fastmvp.mvp`` is synchronous: each call copies q in, runs the product and
 copies phi out before returning, so the PCIe transfers (16 MB each way at
 N = 2M complex64) serialise with the product.  A caller with a stream of
-right-hand sides -- an iterative solver on several systems, a serving loop --
-uses this class instead:
+independent right-hand sides -- several systems solved side by side, a
+serving loop -- uses this class instead:
 
     pipe = MvpPipeline(tree, ops, dtype="f32", is_complex=True)
     for q_host, phi_host in pairs:          # pinned CPU tensors
         pipe.submit(q_host, phi_host)       # returns at once
     pipe.synchronize()                      # every phi_host is written
 
-Three CUDA streams: H2D copies (``depth`` device input slots), the product
-(the plan's CUDA graph, strictly in submission order: the plan's workspace
-is shared), and D2H copies.  While product k runs, the input of k+1 is
-uploaded and the result of k-1 downloaded.  Events order slot reuse, so a
-slot is never overwritten while a product or a download still reads it.
-Results are identical to ``mvp`` (same plan, same graph).
+Streams: one for H2D copies, one per compute slot, one for D2H copies.
+Submission k uses slot k % slots.  A slot is a complete plan (its own
+workspace and CUDA graph; the operator data is uploaded per slot), so with
+slots >= 2 the products of consecutive submissions may also overlap each
+other: the latency-bound far-field chain of one product runs beside the
+bandwidth-bound near field of the next.  Events order reuse of every
+buffer (an upload never overwrites an input a product still reads, a
+product never overwrites a result still being downloaded).  Each result is
+bitwise identical to ``mvp`` for the same plan parameters.
 """
 
 from __future__ import annotations
 
 from .fastmvp import as_tree, get_plan
+from .plan import NesaPlan
 
 __all__ = ["MvpPipeline"]
 
@@ -31,16 +35,20 @@ class MvpPipeline:
     """Overlapped host-to-host products for one (tree, ops) pair."""
 
     def __init__(self, tree, ops, dtype: str = "f32", is_complex: bool = True, nrhs: int = 1,
-                 device: int = 0, depth: int = 2):
+                 device: int = 0, slots: int = 2):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("MvpPipeline needs a CUDA device (no CPU fallback)")
-        if depth < 2:
-            raise ValueError("depth must be >= 2")
+        if slots < 1:
+            raise ValueError("slots must be >= 1")
         self.tree = as_tree(tree)
-        self.plan = get_plan(self.tree, ops, dtype=dtype, device=device)
+        # slot 0 shares the cached plan of mvp(); further slots are private
+        self.plans = [get_plan(self.tree, ops, dtype=dtype, device=device)]
+        for _ in range(slots - 1):
+            self.plans.append(NesaPlan(self.tree, self.plans[0].ops_in, dtype=dtype,
+                                       device=device))
         self.device = device
-        self.depth = depth
+        self.slots = slots
         self.nrhs = nrhs
         self.is_complex = is_complex
         n = self.tree.n_points
@@ -50,14 +58,16 @@ class MvpPipeline:
         shape = (n,) if nrhs == 1 else (n, nrhs)
         self.shape = shape
         dev = f"cuda:{device}"
-        self.q_dev = [torch.empty(shape, dtype=tdt, device=dev) for _ in range(depth)]
-        self.phi_dev = [torch.empty(shape, dtype=tdt, device=dev) for _ in range(depth)]
+        # two input / output buffers per slot: the upload of k + slots overlaps product k
+        nb = 2 * slots
+        self.q_dev = [torch.empty(shape, dtype=tdt, device=dev) for _ in range(nb)]
+        self.phi_dev = [torch.empty(shape, dtype=tdt, device=dev) for _ in range(nb)]
         self.s_h2d = torch.cuda.Stream(device)
-        self.s_comp = torch.cuda.Stream(device)
+        self.s_comp = [torch.cuda.Stream(device) for _ in range(slots)]
         self.s_d2h = torch.cuda.Stream(device)
-        self.ev_in = [torch.cuda.Event() for _ in range(depth)]     # upload k done
-        self.ev_used = [torch.cuda.Event() for _ in range(depth)]   # product k done
-        self.ev_out = [torch.cuda.Event() for _ in range(depth)]    # download k done
+        self.ev_in = [torch.cuda.Event() for _ in range(nb)]     # upload done
+        self.ev_used = [torch.cuda.Event() for _ in range(nb)]   # product done
+        self.ev_out = [torch.cuda.Event() for _ in range(nb)]    # download done
         self.k = 0
 
     def submit(self, q_host, phi_host) -> None:
@@ -68,27 +78,30 @@ class MvpPipeline:
             raise ValueError("q must have one charge per point")
         if q_host.dtype != self.dtype or phi_host.dtype != self.dtype:
             raise ValueError(f"expected {self.dtype}")
-        slot = self.k % self.depth
-        first = self.k < self.depth
-        qd, pd = self.q_dev[slot], self.phi_dev[slot]
-        # upload into the slot once product k - depth has consumed it
-        if not first:
-            self.s_h2d.wait_event(self.ev_used[slot])
+        nb = len(self.q_dev)
+        b = self.k % nb
+        slot = self.k % self.slots
+        reuse = self.k >= nb
+        qd, pd = self.q_dev[b], self.phi_dev[b]
+        comp = self.s_comp[slot]
+        # upload into buffer b once the product that last read it is done
+        if reuse:
+            self.s_h2d.wait_event(self.ev_used[b])
         with torch.cuda.stream(self.s_h2d):
             qd.copy_(q_host, non_blocking=True)
-            self.ev_in[slot].record(self.s_h2d)
-        # product k after its upload and after download k - depth left the slot
-        self.s_comp.wait_event(self.ev_in[slot])
-        if not first:
-            self.s_comp.wait_event(self.ev_out[slot])
-        self.plan.matvec_ptr(qd.data_ptr(), pd.data_ptr(), self.nrhs, self.is_complex,
-                             stream=self.s_comp.cuda_stream)
-        self.ev_used[slot].record(self.s_comp)
+            self.ev_in[b].record(self.s_h2d)
+        # product after its upload and after the download that last read phi b
+        comp.wait_event(self.ev_in[b])
+        if reuse:
+            comp.wait_event(self.ev_out[b])
+        self.plans[slot].matvec_ptr(qd.data_ptr(), pd.data_ptr(), self.nrhs, self.is_complex,
+                                    stream=comp.cuda_stream)
+        self.ev_used[b].record(comp)
         # download once the product is done
-        self.s_d2h.wait_event(self.ev_used[slot])
+        self.s_d2h.wait_event(self.ev_used[b])
         with torch.cuda.stream(self.s_d2h):
             phi_host.copy_(pd, non_blocking=True)
-            self.ev_out[slot].record(self.s_d2h)
+            self.ev_out[b].record(self.s_d2h)
         self.k += 1
 
     def synchronize(self) -> None:

@@ -132,6 +132,7 @@ class NesaPlan:
         if dtype not in _DTYPES:
             raise ValueError(f"unknown dtype {dtype!r}")
         self.tree = tree
+        self.ops_in = ops      # what the plan was built from (MvpPipeline builds siblings)
         self.dtype = "f64" if _DTYPES[dtype] == _capi.NESA_F64 else "f32"
         self.device = int(device)
         if isinstance(ops, OperatorSet):
