@@ -6,6 +6,8 @@ complex128 plans, <= 1e-5 for float32 / complex64 plans, near field alone
 <= 1e-13 (test_fastmvp.py:35-40 bar) in float64.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -343,3 +345,38 @@ def test_pipeline_matches_sync_calls(golden):
         assert np.array_equal(o.numpy(), ref)
     with pytest.raises(ValueError):
         pipe.submit(qs[0][:-1], outs[0])
+
+
+@pytest.mark.parametrize("env", [{"NESA_TC": "0"}, {"NESA_TC": "1"}, {"NESA_MOM_INKERNEL": "1"},
+                                 {"NESA_FUSED": "0", "NESA_SPLIT": "0"}])
+def test_q64_f32_path_variants(monkeypatch, env):
+    # every float32 Q = 64 code path (FFMA / tensor-core translation, in-kernel
+    # or GEMM moment map, fused / per-level coarse kernels) against the oracle
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=7), 30000)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    q = geo.random_rhs(30000, 7)
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    plan = NesaPlan(tree, params, dtype="f32")
+    qd = torch.from_numpy(q.astype(np.complex64)).cuda()
+    phi = torch.empty_like(qd)
+    plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 1, True,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    assert rel_l2(phi.cpu().numpy(), ref) <= 1e-5
+    plan.close()
+
+
+def test_tensor_core_translation_kernel_standalone(tmp_path):
+    # tools/tc_test.cu: the tcgen05 tf32x3 GEMM against a float64 host
+    # reference for R = 1, 2, 4 (single- and multi-tile units)
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "tc_test")
+    subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17",
+                    "-o", exe, os.path.join(root, "tools", "tc_test.cu")], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "PASS" in out.stdout, out.stdout
