@@ -1545,7 +1545,7 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
       }
     }
     ent.graph = g;
-    if (stage == 0) P->kernels_per_matvec = nk;
+    if (stage == 0 && (flags & NESA_NEAR) && (flags & NESA_FAR)) P->kernels_per_matvec = nk;  // full product
     itg = P->graphs.emplace(key, ent).first;
   }
   if (flags & NESA_PROFILE) {
