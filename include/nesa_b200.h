@@ -143,8 +143,9 @@ int nesa_matvec(nesa_plan* plan, const void* q_dev, void* phi_dev,
                 int32_t nrhs, int32_t is_complex, uint32_t flags, void* stream);
 
 /* Multi-GPU pieces of one product (used by the Python dist layer):
- * stage 1 = gather + near + radiation + source transfer (up to the exchange),
- * stage 2 = translation + potential transfer + reception + scatter.
+ * stage 1 = gather + radiation + source transfer (up to the exchange),
+ * stage 2 = near field (concurrent) + translation + potential transfer +
+ *           reception + scatter.
  * s_dev() exposes the (G, Q, nrhs_real) source-amplitude workspace for the
  * halo exchange between the two stages. */
 int nesa_matvec_stage(nesa_plan* plan, int32_t stage, const void* q_dev,
