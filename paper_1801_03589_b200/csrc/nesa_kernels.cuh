@@ -1787,7 +1787,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
-    int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0) {
+    int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0, int bufpts = kMomBufPts) {
   constexpr int MP = 40 / R;           // moments per pass
   constexpr int NV = 2 * R * MP;       // 80 accumulators
   constexpr int NV2 = NV / 2, NV4 = NV / 4;
@@ -1795,11 +1795,11 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
   extern __shared__ float4 sm4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mu_stride = (nm * R + 1) & ~1;  // float2 per leaf, even => 16-byte rows
-  const size_t per_warp = size_t(kMomBufPts) * (2 + R) + size_t(LW) * mu_stride * 2;  // floats
+  const size_t per_warp = size_t(bufpts) * (2 + R) + size_t(LW) * mu_stride * 2;  // floats
   float* wbase = reinterpret_cast<float*>(sm4) + warp * per_warp;
   float2* Pb = reinterpret_cast<float2*>(wbase);
-  float* Qb = wbase + 2 * kMomBufPts;
-  float2* mu = reinterpret_cast<float2*>(wbase + size_t(kMomBufPts) * (2 + R));
+  float* Qb = wbase + 2 * bufpts;
+  float2* mu = reinterpret_cast<float2*>(wbase + size_t(bufpts) * (2 + R));
   const int slot = lane / kMomLanes, g = lane % kMomLanes;
   const int64_t stride = int64_t(gridDim.x) * kExpWarps * LW;
   // stage the points of batch lw (if they fit); returns whether staged
@@ -1808,7 +1808,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
     const int64_t le = lw + LW < nleaf ? lw + LW : nleaf;
     const int64_t b0 = leaf_start[leaf0 + lw], b1 = leaf_stop[leaf0 + le - 1];
     const int np = int(b1 - b0);
-    if (np > kMomBufPts) return false;
+    if (np > bufpts) return false;
     for (int t = lane; t < np; t += 32) {
       cp_async<8>(Pb + t, prel + b0 + t);
       cp_async_n<R * 4>(Qb + t * R, qt + (b0 + t) * R);

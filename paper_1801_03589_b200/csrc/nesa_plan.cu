@@ -346,6 +346,7 @@ struct nesa_plan {
   DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
   // Q = 64: s = A^ mu^ as a warp-tiled GEMM over the leaves (KT = mom_kt)
   int mom_kt = 0;
+  int mom_buf = 800;                        // staged points per warp in the moment kernel
   DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
   DevBuf<float> DTC;                        // [n_dtab][hi | lo][64 x 64] canonical tf32 D
@@ -1055,14 +1056,18 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
       const int64_t per_cta = int64_t(kExpWarps) * kMomLeavesPerWarp;
       const int grid = int(std::max<int64_t>(
           1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(kMomCtasPerSM) * P->n_sm)));
+      // point staging (cp.async) helps alone but costs shared memory the
+      // concurrent near field needs; NESA_MOM_BUF sets the staged points
+      // per warp (0: none)
+      int bufpts = P->mom_buf;
       const size_t sm = size_t(kExpWarps) *
-                        (size_t(kMomBufPts) * (2 + R) + size_t(kMomLeavesPerWarp) * ((P->v_nm * R + 1) & ~1) * 2) *
+                        (size_t(bufpts) * (2 + R) + size_t(kMomLeavesPerWarp) * ((P->v_nm * R + 1) & ~1) * 2) *
                         sizeof(float);
       if (P->mom_kt) {
         float* mu = reinterpret_cast<float*>(P->mu.p);
         radiation_mom_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
             P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, mu, P->leaf_begin,
-            nleaf, P->Q, P->v_nm, P->mom_kt);
+            nleaf, P->Q, P->v_nm, P->mom_kt, bufpts);
         if (P->mom_kt == 80)
           tgemm_wt_kernel<float, R, 64, 80><<<P->n_mom_units, 128, TGW<float, R, 64, 80>::SMEM, st>>>(
               P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s);
@@ -1073,7 +1078,7 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
       }
       radiation_mom_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
           P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, s, P->leaf_begin,
-          nleaf, P->Q, P->v_nm);
+          nleaf, P->Q, P->v_nm, 0, bufpts);
       return 1;
     }
   }
@@ -1613,6 +1618,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       P->l2_persist = std::min<size_t>(size_t(std::max(0, std::atoi(lp))) << 20, size_t(maxp));
       if (P->l2_persist > 0) CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, P->l2_persist));
     }
+    if (const char* mb = std::getenv("NESA_MOM_BUF")) P->mom_buf = std::max(0, std::atoi(mb));
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
     if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
     if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
