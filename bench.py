@@ -208,6 +208,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "ms_per_matvec": 1e3 / value,   # a step is a 1/16 sample of one product
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.n, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
