@@ -1972,7 +1972,10 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
 // coefficient phase so their latency overlaps it.  E [Q][nt + 1] float2
 // (column 0 = 1, column m = (1/m) e^{-i m theta_k}) is read through L1.
 // smem per warp: beta [nt + 1][R] float2 (16-byte aligned), o [Q][R].
-template <int R>
+// BETA_IN: `o` holds beta^[leaf][64][R] (row 0 = sum_k o_k, rows 2m-1 / 2m =
+// Re / Im beta_m) from the tensor-core GEMM beta^ = E^ o; the coefficient
+// phase is skipped.
+template <int R, bool BETA_IN = false>
 __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
@@ -1993,11 +1996,12 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
     const int64_t b = leaf_start[leaf];
     const int n = int(leaf_stop[leaf] - b);
     const float r = leaf_r[leaf];
-    // prefetch: amplitudes and the first kSlots * 32 points
-    float ov[4];
-    const int nq = Q * R;
+    // prefetch: amplitudes (or coefficients) and the first kSlots * 32 points
+    const int nq = BETA_IN ? 64 * R : Q * R;
+    constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
+    float ov[NOV];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) ov[t] = lane + 32 * t < nq ? o[leaf * nq + lane + 32 * t] : 0.f;
+    for (int t = 0; t < NOV; ++t) ov[t] = lane + 32 * t < nq ? o[leaf * nq + lane + 32 * t] : 0.f;
     float2 pp[kSlots];
     int64_t dd[kSlots];
     float bb[kSlots][R];
@@ -2011,31 +2015,50 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
         for (int rr = 0; rr < R; ++rr) bb[i][rr] = phin ? phin[(b + j) * R + rr] : 0.f;
       }
     }
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (lane + 32 * t < nq) os[lane + 32 * t] = ov[t];
-    for (int t = lane + 128; t < nq; t += 32) os[t] = o[leaf * nq + t];
-    __syncwarp();
     const float nlr = -logf(r);
-    for (int m = lane; m < ne; m += 32) {
-      float2 acc[R];
+    if constexpr (BETA_IN) {
+      // beta^ row 0 -> beta_0 = -log(r) sum o; rows (2m-1, 2m) -> beta_m
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] = make_float2(0.f, 0.f);
-#pragma unroll 4
-      for (int k = 0; k < Q; ++k) {
-        const float2 e = __ldg(E + k * ne + m);
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) {
-          const float ok = os[k * R + rr];
-          acc[rr].x = fmaf(e.x, ok, acc[rr].x);
-          acc[rr].y = fmaf(e.y, ok, acc[rr].y);
+      for (int t = 0; t < NOV; ++t) {
+        const int idx = lane + 32 * t;
+        if (idx < nq) {
+          const int row = idx / R, rr = idx - (idx / R) * R;
+          const int m = (row + 1) >> 1;
+          if (row == 0)
+            beta[rr] = make_float2(nlr * ov[t], 0.f);
+          else if (m <= nt) {
+            float* bf = reinterpret_cast<float*>(beta + m * R + rr);
+            bf[(row & 1) ? 0 : 1] = ov[t];
+          }
         }
       }
+      __syncwarp();
+    } else {
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr)
-        beta[m * R + rr] = m ? acc[rr] : make_float2(nlr * acc[rr].x, 0.f);
+      for (int t = 0; t < NOV; ++t)
+        if (lane + 32 * t < nq) os[lane + 32 * t] = ov[t];
+      for (int t = lane + 32 * NOV; t < nq; t += 32) os[t] = o[leaf * nq + t];
+      __syncwarp();
+      for (int m = lane; m < ne; m += 32) {
+        float2 acc[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) acc[rr] = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int k = 0; k < Q; ++k) {
+          const float2 e = __ldg(E + k * ne + m);
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) {
+            const float ok = os[k * R + rr];
+            acc[rr].x = fmaf(e.x, ok, acc[rr].x);
+            acc[rr].y = fmaf(e.y, ok, acc[rr].y);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+          beta[m * R + rr] = m ? acc[rr] : make_float2(nlr * acc[rr].x, 0.f);
+      }
+      __syncwarp();
     }
-    __syncwarp();
     const float inv = 1.f / r;
     auto eval = [&](float2 p, int64_t dst, const float* base) {
       const float2 w = make_float2(p.x * inv, p.y * inv);

@@ -353,6 +353,9 @@ struct nesa_plan {
   DevBuf<TUnit> mom_units;
   DevBuf<TEnt> mom_ents;
   int n_mom_units = 0;
+  bool beta_tc = false;                     // reception coefficients by tgemm_tc (E^ o)
+  DevBuf<float> ETC;                        // [hi | lo][64 x 64] canonical tf32 E^
+  DevBuf<unsigned char> beta;               // [NL][64][R] reception coefficients
   DevBuf<unsigned char> mu;                 // [NL][mom_kt][R] moments
   cudaEvent_t ev_mark = nullptr;            // no-op event-record node ahead of the near kernel
 
@@ -842,7 +845,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
       }
       P->mom_A.upload(A);
-      if (Q == 64 && !std::getenv("NESA_MOM_INKERNEL")) {
+      const char* mi = std::getenv("NESA_MOM_INKERNEL");
+      if (Q == 64 && !(mi && std::atoi(mi) != 0)) {
         const int need = 2 * P->v_nm - 1;
         P->mom_kt = need <= 80 ? 80 : (need <= 127 ? 128 : 0);  // nm <= 64 (16 per lane)
       }
@@ -857,16 +861,6 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           }
         }
         P->momAT.upload(AT);
-        std::vector<TUnit> units;
-        std::vector<TEnt> ents;
-        for (int64_t a = lb; a < le; ++a) ents.push_back(TEnt{int32_t(a), int32_t(a)});
-        int per = 32;  // one pass of 32 leaves per CTA: the GEMM is latency-bound
-        if (const char* e = std::getenv("NESA_MOM_PER")) per = std::max(1, std::atoi(e));
-        for (size_t i = 0; i < ents.size(); i += per)
-          units.push_back(TUnit{0, int32_t(i), int32_t(std::min(ents.size(), i + per)), 0});
-        P->mom_units.upload(units);
-        P->mom_ents.upload(ents);
-        P->n_mom_units = int(units.size());
       }
     }
     if (P->u_mf) {
@@ -879,6 +873,47 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           E[size_t(k) * ne + m] = float2{float(std::cos(m * th) / m), float(-std::sin(m * th) / m)};
       }
       P->exp_E.upload(E);
+      // Q = 64 with tensor cores: beta^ = E^ o for all leaves as one GEMM;
+      // E^ rows 0 -> 1 (sum of o), 2m-1 / 2m -> Re / Im of (1/m) e^{-i m theta_k}
+      const char* ri = std::getenv("NESA_RECV_INKERNEL");
+      if (Q == 64 && P->tc && 2 * P->u_nt + 1 <= 64 && !(ri && std::atoi(ri) != 0)) {
+        auto tf32 = [](float x) {
+          uint32_t u;
+          std::memcpy(&u, &x, 4);
+          u = (u + 0x1000u) & ~0x1FFFu;
+          float y;
+          std::memcpy(&y, &u, 4);
+          return y;
+        };
+        std::vector<float> h(8192, 0.f);
+        for (int row = 0; row < 64; ++row)
+          for (int k = 0; k < 64; ++k) {
+            float x = 0.f;
+            if (row == 0)
+              x = 1.f;
+            else if (row <= 2 * P->u_nt)
+              x = (row & 1) ? E[size_t(k) * ne + (row + 1) / 2].x : E[size_t(k) * ne + row / 2].y;
+            const float hi = tf32(x), lo = tf32(x - hi);
+            const size_t off = size_t(row / 8) * 512 + size_t(k / 4) * 32 + size_t(row % 8) * 4 + (k % 4);
+            h[off] = hi;
+            h[4096 + off] = lo;
+          }
+        P->ETC.upload(h);
+        P->beta_tc = true;
+      }
+    }
+    if (P->mom_kt || P->beta_tc) {
+      // one entry per local leaf (src = dst = leaf), 32 leaves per unit
+      std::vector<TUnit> units;
+      std::vector<TEnt> ents;
+      for (int64_t a = lb; a < le; ++a) ents.push_back(TEnt{int32_t(a), int32_t(a)});
+      int per = 32;  // one pass of 32 leaves per CTA: the GEMM is latency-bound
+      if (const char* e = std::getenv("NESA_MOM_PER")) per = std::max(1, std::atoi(e));
+      for (size_t i = 0; i < ents.size(); i += per)
+        units.push_back(TUnit{0, int32_t(i), int32_t(std::min(ents.size(), i + per)), 0});
+      P->mom_units.upload(units);
+      P->mom_ents.upload(ents);
+      P->n_mom_units = int(units.size());
     }
   }
   if (P->u_mf) {
@@ -948,6 +983,7 @@ void ensure_workspace(nesa_plan* P, int R) {
   P->phin.alloc(size_t(P->N) * R * es);
   if (P->u_mf && P->recv_far) P->phif.alloc(size_t(P->N) * R * es);
   if (P->mom_kt) P->mu.alloc(size_t(P->NL) * P->mom_kt * R * es);
+  if (P->beta_tc) P->beta.alloc(size_t(P->NL) * 64 * R * es);
   {
     const size_t fb = (size_t(P->G) * P->Q * R * es + 255) & ~size_t(255);
     P->farws.alloc(3 * fb);
@@ -1013,6 +1049,7 @@ void set_smem_attrs() {
     attr(tgemm_tc_kernel<R>, int(kTcSmem));
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
+    attr(reception_exp_kernel<R, true>, lim);
   }
   done = true;
 }
@@ -1088,17 +1125,28 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
 
 // phi[perm] = phin + U o through the incoming expansion (float32 plans)
 template <int R>
-void launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const int64_t* perm,
-                          float* phi, int ldp, cudaStream_t st) {
+int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const int64_t* perm,
+                         float* phi, int ldp, cudaStream_t st) {
   const int64_t nleaf = P->leaf_end - P->leaf_begin;
   const int grid = int(std::max<int64_t>(
       1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(kExpCtasPerSM) * P->n_sm)));
   const int Q = P->Q, nt = P->u_nt;
   const size_t nb = ((size_t(nt) + 1) * R + 1) & ~size_t(1);
   const size_t sm = size_t(kExpWarps) * (nb + ((size_t(Q) * R + 3) & ~size_t(3)) / 2) * sizeof(float2);
+  if (P->beta_tc) {
+    // beta^ = E^ o for every leaf on the tensor cores, then the per-point series
+    float* beta = reinterpret_cast<float*>(P->beta.p);
+    tgemm_tc_kernel<R><<<P->n_mom_units, 128, kTcSmem, st>>>(P->mom_units.p, P->mom_ents.p,
+                                                            P->ETC.p, o, beta);
+    reception_exp_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
+        P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
+        P->leaf_begin, nleaf, Q, nt, ldp);
+    return 2;
+  }
   reception_exp_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
       P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, o, phin, perm, phi,
       P->leaf_begin, nleaf, Q, nt, ldp);
+  return 1;
 }
 
 // Enqueue one product, or one of its two stages (multi-GPU), on P->s0/P->s1.
@@ -1338,8 +1386,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
     if (far && P->u_mf) {
       if constexpr (std::is_same<T, float>::value)
-        launch_reception_exp<R>(P, o, near ? phin : nullptr, P->perm.p, phi, P->ldv, s0);
-      nk++;
+        nk += launch_reception_exp<R>(P, o, near ? phin : nullptr, P->perm.p, phi, P->ldv, s0);
     } else if (far) {
       launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p,
                                            P->ldv, s0);
@@ -1407,8 +1454,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       if (rfar) {
         if constexpr (std::is_same<T, float>::value) {
           prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
-          launch_reception_exp<R>(P, o, nullptr, nullptr, reinterpret_cast<float*>(P->phif.p), R, s0);
-          nk++;
+          nk += launch_reception_exp<R>(P, o, nullptr, nullptr, reinterpret_cast<float*>(P->phif.p), R, s0);
           tr("reception", s0);
           prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
         }
