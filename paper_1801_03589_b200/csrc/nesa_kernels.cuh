@@ -1144,11 +1144,13 @@ struct TGW {
   static constexpr size_t SMEM = MB + 2 * XB + 2 * 4 * PER + 64;
 };
 
-template <typename T, int R, int QT, int KT = QT>
+// SPLITQ > 0: output rows [0, SPLITQ) go to Y, rows [SPLITQ, QT) to Y2 (the
+// radiation's stacked [A^; C_q A^] map writes s and the leaf transfers T).
+template <typename T, int R, int QT, int KT = QT, int SPLITQ = 0>
 __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__ units,
                                                        const TEnt* __restrict__ ents,
                                                        const T* __restrict__ DT,
-                                                       const T* __restrict__ s, T* Y) {
+                                                       const T* __restrict__ s, T* Y, T* Y2) {
   using W = TGW<T, R, QT, KT>;
   extern __shared__ __align__(128) unsigned char smem[];
   T* Dm = reinterpret_cast<T*>(smem);
@@ -1251,7 +1253,16 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
       for (int i = tid; i < n * NV; i += 128) {
         const int p = i / NV, v = i - p * NV;
         const float4 val = *reinterpret_cast<const float4*>(O + p * W::XS + v * V);
-        st16_hint(Y + int64_t(eid[p]) * W::QR + v * V, val, keep);
+        if constexpr (SPLITQ > 0) {
+          constexpr int S1 = SPLITQ * R, S2 = (QT - SPLITQ) * R;
+          const int w = v * V;
+          if (w < S1)
+            *reinterpret_cast<float4*>(Y + int64_t(eid[p]) * S1 + w) = val;
+          else
+            *reinterpret_cast<float4*>(Y2 + int64_t(eid[p]) * S2 + (w - S1)) = val;
+        } else {
+          st16_hint(Y + int64_t(eid[p]) * W::QR + v * V, val, keep);
+        }
       }
     }
     __syncthreads();  // X buffer reuse

@@ -353,6 +353,11 @@ struct nesa_plan {
   DevBuf<TUnit> mom_units;
   DevBuf<TEnt> mom_ents;
   int n_mom_units = 0;
+  bool rad_up = false;                      // radiation GEMM also writes the leaf transfers T
+  DevBuf<float> radT;                       // [4 quadrants][80][128] stacked [A^; C_q A^]^T
+  DevBuf<TUnit> rad_units;
+  DevBuf<TEnt> rad_ents;
+  int n_rad_units = 0;
   bool beta_tc = false;                     // reception coefficients by tgemm_tc (E^ o)
   DevBuf<float> ETC;                        // [hi | lo][64 x 64] canonical tf32 E^
   DevBuf<unsigned char> beta;               // [NL][64][R] reception coefficients
@@ -828,6 +833,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     const int nc = P->n_check;
     if (P->v_mom) {
       std::vector<float2> A(size_t(P->v_nm) * Q);
+      std::vector<double> Ad(size_t(P->v_nm) * Q * 2);  // float64 (re, im) for the stacked map
       std::vector<double> ang(nc);
       for (int l = 0; l < nc; ++l) ang[l] = std::atan2(d->check_sin[l], d->check_cos[l]);
       for (int k = 0; k < Q; ++k) {
@@ -835,6 +841,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         double F = 0;
         for (int l = 0; l < nc; ++l) F += f[l];
         A[k] = float2{float(F), 0.f};
+        Ad[2 * size_t(k)] = F;
+        Ad[2 * size_t(k) + 1] = 0;
         for (int m = 1; m < P->v_nm; ++m) {
           double re = 0, im = 0;
           for (int l = 0; l < nc; ++l) {
@@ -842,6 +850,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
             im -= f[l] * std::sin(m * ang[l]);
           }
           A[size_t(m) * Q + k] = float2{float(re / m), float(im / m)};
+          Ad[2 * (size_t(m) * Q + k)] = re / m;
+          Ad[2 * (size_t(m) * Q + k) + 1] = im / m;
         }
       }
       P->mom_A.upload(A);
@@ -861,6 +871,55 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           }
         }
         P->momAT.upload(AT);
+        // leaf level wide (warp-tiled level kernels): fold the leaf transfer
+        // into the same GEMM, Y = [A^; C_q A^] mu^ -> s and T in one pass
+        // (one stacked 128 x 80 map per child quadrant q, formed in float64)
+        const int li = P->L - P->l0;
+        const bool leaf_wide = P->L > P->l0 && P->loc_count[li] >= P->wide_level;
+        // (measured neutral at C4: the 128-row GEMM costs what the leaf level
+        // kernel did; opt in with NESA_RAD_UP=1)
+        const char* ru = std::getenv("NESA_RAD_UP");
+        if (P->mom_kt == 80 && leaf_wide && ru && std::atoi(ru) != 0) {
+          const int kt = 80;
+          std::vector<double> ATd(size_t(kt) * Q, 0.0);  // ATd[j][i] = A^[i][j]
+          for (int i = 0; i < Q; ++i) {
+            ATd[i] = Ad[2 * size_t(i)];
+            for (int m = 1; m < P->v_nm; ++m) {
+              ATd[size_t(2 * m - 1) * Q + i] = Ad[2 * (size_t(m) * Q + i)];
+              ATd[size_t(2 * m) * Q + i] = -Ad[2 * (size_t(m) * Q + i) + 1];
+            }
+          }
+          std::vector<float> RT(size_t(4) * kt * 128, 0.f);
+          for (int q = 0; q < 4; ++q) {
+            const double* Cq = d->C + (size_t(li - 1) * 4 + q) * Q * Q;
+            float* M = RT.data() + size_t(q) * kt * 128;
+            for (int j = 0; j < kt; ++j) {
+              for (int k = 0; k < Q; ++k) M[size_t(j) * 128 + k] = float(ATd[size_t(j) * Q + k]);
+              for (int k = 0; k < Q; ++k) {
+                double acc = 0;
+                for (int i = 0; i < Q; ++i) acc += Cq[size_t(k) * Q + i] * ATd[size_t(j) * Q + i];
+                M[size_t(j) * 128 + Q + k] = float(acc);
+              }
+            }
+          }
+          P->radT.upload(RT);
+          std::vector<TUnit> units;
+          std::vector<TEnt> ents;
+          for (int q = 0; q < 4; ++q) {
+            std::vector<TEnt> v;
+            for (int64_t a = lb; a < le; ++a)
+              if (d->quad[a] == q) v.push_back(TEnt{int32_t(a), int32_t(a)});
+            for (size_t i = 0; i < v.size(); i += 32) {
+              const size_t j = std::min(v.size(), i + 32);
+              units.push_back(TUnit{q, int32_t(ents.size()), int32_t(ents.size() + (j - i)), 0});
+              ents.insert(ents.end(), v.begin() + i, v.begin() + j);
+            }
+          }
+          P->rad_units.upload(units);
+          P->rad_ents.upload(ents);
+          P->n_rad_units = int(units.size());
+          P->rad_up = true;
+        }
       }
     }
     if (P->u_mf) {
@@ -1046,6 +1105,7 @@ void set_smem_attrs() {
     attr(radiation_mom_kernel<R>, lim);
     attr(radiation_mom_kernel<R, true>, lim);
     attr(tgemm_wt_kernel<float, R, 64, 80>, lim);
+    attr(tgemm_wt_kernel<float, R, 128, 80, 64>, lim);
     attr(tgemm_tc_kernel<R>, int(kTcSmem));
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
@@ -1105,12 +1165,15 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
         radiation_mom_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
             P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, mu, P->leaf_begin,
             nleaf, P->Q, P->v_nm, P->mom_kt, bufpts);
-        if (P->mom_kt == 80)
+        if (P->rad_up)
+          tgemm_wt_kernel<float, R, 128, 80, 64><<<P->n_rad_units, 128, TGW<float, R, 128, 80>::SMEM, st>>>(
+              P->rad_units.p, P->rad_ents.p, P->radT.p, mu, s, reinterpret_cast<float*>(P->Tup.p));
+        else if (P->mom_kt == 80)
           tgemm_wt_kernel<float, R, 64, 80><<<P->n_mom_units, 128, TGW<float, R, 64, 80>::SMEM, st>>>(
-              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s);
+              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s, nullptr);
         else
           tgemm_wt_kernel<float, R, 64, 128><<<P->n_mom_units, 128, TGW<float, R, 64, 128>::SMEM, st>>>(
-              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s);
+              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s, nullptr);
         return 2;
       }
       radiation_mom_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
@@ -1207,6 +1270,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     // children-major: T[c] = C s[c]; s[parent] = sum of its children's T
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
+    if (lv == P->L && P->rad_up) return;  // the radiation GEMM wrote the leaf T
     const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
     const int grid = int((la.count + la.TC - 1) / la.TC);
     if (Q == 64 && la.count >= P->wide_level) {
@@ -1245,10 +1309,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
                    (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
     } else if (Q == 64)
       launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 64>, u1 - u0, 128, TGW<T, R, 64>::SMEM, st,
-                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y);
+                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y, (T*)nullptr);
     else if (Q == 32)
       launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 32>, u1 - u0, 128, TGW<T, R, 32>::SMEM, st,
-                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y);
+                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y, (T*)nullptr);
     else
       tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp,
                                                                                 s, Y, Q);
