@@ -13,16 +13,18 @@ from .geometry import (BBox, CurveSpec, bounding_box, generate_sources, parse_cu
 from .linalg import circle_points, gemv, kernel_eval, kernel_matrix, pinv
 from .operators import NesaParams, OperatorSet, OperatorTables, build_all, build_tables
 from .pipeline import MvpPipeline
+from .serialize import load_problem, save_problem
+from .solver import GmresResult, gmres
 from .plan import NesaPlan, algorithmic_bytes, algorithmic_flops
 from .quadtree import Tree, TreeParams, build_tree, interaction_list, neighbor_list, tree_stats
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BBox", "CurveSpec", "MvpPipeline", "NesaParams", "NesaPlan", "OperatorSet", "OperatorTables", "Tree",
+    "BBox", "CurveSpec", "GmresResult", "MvpPipeline", "NesaParams", "NesaPlan", "OperatorSet", "OperatorTables", "Tree",
     "TreeParams", "algorithmic_bytes", "algorithmic_flops", "as_tree", "bounding_box",
     "build_all", "build_tables", "build_tree", "circle_points", "gemv", "generate_sources",
-    "get_plan", "interaction_list", "kernel_eval", "kernel_matrix", "mvp", "mvp_serial",
-    "neighbor_list", "parse_curve_spec", "pinv", "plane_wave_rhs", "random_rhs",
+    "get_plan", "gmres", "interaction_list", "kernel_eval", "load_problem", "kernel_matrix", "mvp", "mvp_serial",
+    "neighbor_list", "parse_curve_spec", "pinv", "plane_wave_rhs", "random_rhs", "save_problem",
     "task_counts", "tree_stats", "wavenumber",
 ]

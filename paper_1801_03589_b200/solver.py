@@ -1,0 +1,168 @@
+"""Iterative solver around the GPU NESA product.
+
+The reference only multiplies (no solver); the paper names the
+product as the inner kernel of an iterative solver.  This
+is restarted GMRES for
+
+    (shift * I + K~) x = b
+
+with every product on the GPU (``NesaPlan.matvec_ptr`` on device tensors, no
+host copies of the N-vectors) and several right-hand sides solved side by
+side: the columns run independent Arnoldi processes in lockstep, so each
+iteration is ONE multi-column product (the plan streams the near-field
+operator once for up to 4 real columns, see nesa_plan.cu run_matvec).
+
+Only the small Hessenberg / Givens bookkeeping (restart x restart per
+column) lives on the host.  ``shift`` turns the first-kind log-kernel system
+into a second-kind one when wanted (the first-kind system is ill conditioned
+and converges slowly, as for any first-kind integral equation).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .fastmvp import as_tree, get_plan
+
+__all__ = ["gmres", "GmresResult"]
+
+
+@dataclass
+class GmresResult:
+    x: object                 # solution, same kind (numpy / torch) and shape as b
+    iterations: int           # inner iterations (products) performed
+    residuals: np.ndarray     # final relative residual per column (true, recomputed)
+    converged: np.ndarray     # per column
+    history: list             # estimated relative residual per iteration, (n_iter, m)
+
+
+def _givens(a: complex, b: complex):
+    """(c, s) with [c, s; -conj(s), c] [a; b] = [r; 0]."""
+    if b == 0:
+        return 1.0, 0.0
+    if a == 0:
+        return 0.0, 1.0
+    r = np.hypot(abs(a), abs(b))
+    c = abs(a) / r
+    s = (a / abs(a)) * np.conj(b) / r
+    return c, s
+
+
+def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40,
+          maxiter: int = 400, x0=None, device: int | None = None) -> GmresResult:
+    """Restarted GMRES on the GPU for (shift I + K~) x = b.
+
+    b: (N,) or (N, m), numpy or torch (CPU or CUDA); real or complex; float32
+    / complex64 use the float32 plan, float64 / complex128 the float64 plan.
+    Columns stop updating once their relative residual is below ``tol``.
+    """
+    import torch
+    t = as_tree(tree)
+    is_torch = isinstance(b, torch.Tensor)
+    on_host = (not is_torch) or not b.is_cuda
+    if is_torch:
+        dev = b.device.index if b.is_cuda else (device or 0)
+        bd = b.to(f"cuda:{dev}")
+    else:
+        dev = device or 0
+        bd = torch.from_numpy(np.ascontiguousarray(b)).to(f"cuda:{dev}")
+    if bd.shape[0] != t.n_points or bd.dim() not in (1, 2):
+        raise ValueError("b must have one value per point")
+    vec = bd.dim() == 1
+    B = bd.reshape(t.n_points, -1).contiguous()
+    m = B.shape[1]
+    single = B.dtype in (torch.float32, torch.complex64)
+    is_complex = B.is_complex()
+    plan = get_plan(t, ops, dtype="f32" if single else "f64", device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def A(X):
+        Y = torch.empty_like(X)
+        plan.matvec_ptr(X.data_ptr(), Y.data_ptr(), m, is_complex, stream=stream.cuda_stream)
+        if shift:
+            Y.add_(X, alpha=shift)
+        return Y
+
+    def cnorm(X):                      # per-column 2-norms, float64 on host
+        return torch.linalg.vector_norm(X, dim=0).double().cpu().numpy()
+
+    X = torch.zeros_like(B) if x0 is None else (
+        x0 if isinstance(x0, torch.Tensor) else torch.from_numpy(np.asarray(x0))
+    ).to(B.device, B.dtype).reshape(B.shape).clone()
+    bnorm = cnorm(B)
+    bnorm[bnorm == 0] = 1.0
+    hdt = np.complex128 if is_complex else np.float64
+    history = []
+    iters = 0
+    done = np.zeros(m, bool)
+    while iters < maxiter and not done.all():
+        Rv = B - A(X) if iters or x0 is not None else B.clone()
+        if iters or x0 is not None:
+            iters += 1
+        beta = cnorm(Rv)
+        done |= beta / bnorm <= tol
+        if done.all():
+            break
+        k_max = min(restart, maxiter - iters)
+        if k_max <= 0:
+            break
+        V = torch.empty((k_max + 1,) + tuple(B.shape), dtype=B.dtype, device=B.device)
+        scale = torch.as_tensor(np.where(beta > 0, 1.0 / np.maximum(beta, 1e-300), 0.0),
+                                device=B.device, dtype=B.real.dtype if is_complex else B.dtype)
+        V[0] = Rv * scale
+        H = np.zeros((k_max + 1, k_max, m), hdt)
+        cs = np.zeros((k_max, m))
+        sn = np.zeros((k_max, m), hdt)
+        g = np.zeros((k_max + 1, m), hdt)
+        g[0] = beta
+        k_used = 0
+        for k in range(k_max):
+            W = A(V[k])
+            iters += 1
+            # modified Gram-Schmidt, all columns at once
+            for j in range(k + 1):
+                hj = (V[j].conj() * W).sum(dim=0) if is_complex else (V[j] * W).sum(dim=0)
+                W -= V[j] * hj
+                H[j, k] = hj.cpu().numpy()
+            hn = cnorm(W)
+            H[k + 1, k] = hn
+            V[k + 1] = W * torch.as_tensor(np.where(hn > 0, 1.0 / np.maximum(hn, 1e-300), 0.0),
+                                           device=B.device, dtype=W.real.dtype if is_complex else W.dtype)
+            # Givens rotations per column
+            for c in range(m):
+                for j in range(k):
+                    a0, a1 = H[j, k, c], H[j + 1, k, c]
+                    H[j, k, c] = cs[j, c] * a0 + sn[j, c] * a1
+                    H[j + 1, k, c] = -np.conj(sn[j, c]) * a0 + cs[j, c] * a1
+                cc, ss = _givens(H[k, k, c], H[k + 1, k, c])
+                cs[k, c], sn[k, c] = cc, ss
+                H[k, k, c] = cc * H[k, k, c] + ss * H[k + 1, k, c]
+                H[k + 1, k, c] = 0
+                g[k + 1, c] = -np.conj(ss) * g[k, c]
+                g[k, c] = cc * g[k, c]
+            k_used = k + 1
+            est = np.abs(g[k + 1]) / bnorm
+            est[done] = 0.0
+            history.append(est.copy())
+            if (est <= tol).all() or iters >= maxiter:
+                break
+        # x += V y, y from the triangular system, per column (finished columns keep x)
+        Y = np.zeros((k_used, m), hdt)
+        for c in range(m):
+            if done[c]:
+                continue
+            Rm = H[:k_used, :k_used, c]
+            Y[:, c] = np.linalg.solve(np.triu(Rm), g[:k_used, c])
+        Yd = torch.as_tensor(Y, device=B.device, dtype=B.dtype)
+        X += torch.einsum("knm,km->nm", V[:k_used], Yd)
+    R = B - A(X)
+    res = cnorm(R) / bnorm
+    out = X.reshape(bd.shape)
+    if on_host:
+        out = out.cpu()
+        if not is_torch:
+            out = out.numpy()
+    return GmresResult(x=out, iterations=iters, residuals=res, converged=res <= tol * 1.01,
+                       history=history)
