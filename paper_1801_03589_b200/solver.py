@@ -12,8 +12,10 @@ side: the columns run independent Arnoldi processes in lockstep, so each
 iteration is ONE multi-column product (the plan streams the near-field
 operator once for up to 4 real columns, see nesa_plan.cu run_matvec).
 
-Only the small Hessenberg / Givens bookkeeping (restart x restart per
-column) lives on the host.  ``shift`` turns the first-kind log-kernel system
+Orthogonalisation is classical Gram-Schmidt applied twice (CGS2: two
+batched projections against the basis per iteration).  Only the small
+Hessenberg / Givens bookkeeping (restart x restart per column) lives on the
+host.  ``shift`` turns the first-kind log-kernel system
 into a second-kind one when wanted (the first-kind system is ill conditioned
 and converges slowly, as for any first-kind integral equation).
 """
@@ -121,11 +123,24 @@ def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40
         for k in range(k_max):
             W = A(V[k])
             iters += 1
-            # modified Gram-Schmidt, all columns at once
-            for j in range(k + 1):
-                hj = (V[j].conj() * W).sum(dim=0) if is_complex else (V[j] * W).sum(dim=0)
-                W -= V[j] * hj
-                H[j, k] = hj.cpu().numpy()
+            # classical Gram-Schmidt, twice (CGS2): two batched projections
+            # against the whole basis per iteration, one host transfer
+            Vk = V[:k + 1]
+            if m == 1:   # GEMV (cuBLAS) on the (k+1, N) basis
+                V2, w = Vk.reshape(k + 1, -1), W.reshape(-1)
+                Vc = V2.conj() if is_complex else V2
+                h1 = torch.mv(Vc, w)
+                w -= torch.mv(V2.t(), h1)
+                h2 = torch.mv(Vc, w)
+                w -= torch.mv(V2.t(), h2)
+                h1, h2 = h1[:, None], h2[:, None]
+            else:
+                Vc = Vk.conj() if is_complex else Vk
+                h1 = torch.einsum("knm,nm->km", Vc, W)
+                W -= torch.einsum("knm,km->nm", Vk, h1)
+                h2 = torch.einsum("knm,nm->km", Vc, W)
+                W -= torch.einsum("knm,km->nm", Vk, h2)
+            H[:k + 1, k] = (h1 + h2).cpu().numpy()
             hn = cnorm(W)
             H[k + 1, k] = hn
             V[k + 1] = W * torch.as_tensor(np.where(hn > 0, 1.0 / np.maximum(hn, 1e-300), 0.0),
