@@ -374,6 +374,12 @@ struct nesa_plan {
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t s2 = nullptr;                 // fine-level translation branch
+  cudaStream_t s3 = nullptr;                 // second near-field launch (near_split)
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+  int near_split = 0;                        // far-pass hook position of the 2nd near launch (0: one
+                                             // launch; measured slower: half the CTAs stream at
+                                             // about half the bandwidth)
+  double near_frac = 0.5;                    // share of near-field CTAs in the first launch
   cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
@@ -420,6 +426,9 @@ struct nesa_plan {
     if (ev_mark) cudaEventDestroy(ev_mark);
     if (ev_tfine) cudaEventDestroy(ev_tfine);
     if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
+    if (ev_fork2) cudaEventDestroy(ev_fork2);
+    if (ev_join2) cudaEventDestroy(ev_join2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (s0) cudaStreamDestroy(s0);
@@ -1060,12 +1069,14 @@ inline int grid_for(int64_t n, int threads, int cap) {
 
 template <typename T, int R, int MODE, int NST = kStages>
 void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
-                      int64_t perm_offset, cudaStream_t st) {
+                      int64_t perm_offset, cudaStream_t st, int cta0 = 0, int ncta = -1) {
   if (bs.n_items == 0) return;
-  BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p, x, y, base,
-                     perm, int(perm_offset)};
+  if (ncta < 0) ncta = bs.grid - cta0;
+  if (ncta <= 0) return;
+  BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p + cta0, x, y,
+                     base, perm, int(perm_offset)};
   constexpr size_t sm = blockgemv_smem_bytes<T, R, MODE, NST>();
-  blockgemv_kernel<T, R, MODE, NST><<<bs.grid, kBGThreads, sm, st>>>(a);
+  blockgemv_kernel<T, R, MODE, NST><<<ncta, kBGThreads, sm, st>>>(a);
 }
 
 template <typename T, int R>
@@ -1479,6 +1490,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     // near-field CTAs; 2: after the leaf-level upward kernel; 3: after the
     // upward pass; 4: after translation).
     bool forked = false;
+    const bool nsplit = near && far && P->near_split > 0 && P->near_ctas != 1 && P->nearset.grid > 1;
+    const int n_a = nsplit ? std::max(1, std::min(P->nearset.grid - 1,
+                                                   int(P->near_frac * P->nearset.grid + 0.5)))
+                           : P->nearset.grid;
     auto launch_near = [&]() {
       if (forked) return;
       forked = true;
@@ -1491,11 +1506,27 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
       if (P->near_ctas == 1)
         launch_blockgemv<T, R, kModeStore, 6>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
+      else if (nsplit)
+        launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1, 0, n_a);
       else
         launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       nk++;
-      prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, s1);
+      if (!nsplit) prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, s1);
       tr("near", s1);
+    };
+    // optional second near-field launch (the remaining CTAs' items) forked
+    // from the far chain at hook position near_split, on its own stream
+    bool forked2 = false;
+    auto launch_near2 = [&]() {
+      if (!nsplit || forked2) return;
+      forked2 = true;
+      CUDA_OK(cudaEventRecord(P->ev_fork2, s0));
+      CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_fork2, 0));
+      launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, P->s3, n_a);
+      nk++;
+      CUDA_OK(cudaEventRecord(P->ev_join2, P->s1));
+      CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_join2, 0));
+      prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, P->s3);
     };
     gather();
     if (far && P->near_after < 0) launch_near();
@@ -1512,7 +1543,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (far) {
       far_pass(P->split, [&](int pos) {
         if (pos == P->near_after) launch_near();
+        if (pos == P->near_split) launch_near2();
       });
+      launch_near2();
       launch_near();
       prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
       if (rfar) {
@@ -1524,7 +1557,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         }
       }
     }
-    CUDA_OK(cudaEventRecord(P->ev_join, s1));
+    CUDA_OK(cudaEventRecord(P->ev_join, nsplit ? P->s3 : s1));
     CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
     if (rfar) {
       scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
@@ -1731,6 +1764,8 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* mb = std::getenv("NESA_MOM_BUF")) P->mom_buf = std::max(0, std::atoi(mb));
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
     if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
+    if (const char* ns = std::getenv("NESA_NEAR_SPLIT")) P->near_split = std::atoi(ns);
+    if (const char* nf = std::getenv("NESA_NEAR_FRAC")) P->near_frac = std::atof(nf);
     if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
@@ -1767,7 +1802,10 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       CUDA_OK(cudaStreamCreateWithPriority(&P->s0, cudaStreamNonBlocking, P->priority ? hi : lo));
       CUDA_OK(cudaStreamCreateWithPriority(&P->s1, cudaStreamNonBlocking, lo));
       CUDA_OK(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, P->priority ? hi : lo));
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s3, cudaStreamNonBlocking, lo));
     }
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork2, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_join2, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_sfine, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_mark, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_tfine, cudaEventDisableTiming));

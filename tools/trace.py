@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--near", type=int, default=1)
     ap.add_argument("--far", type=int, default=1)
+    ap.add_argument("--chrome", default="", help="also write a Chrome trace (chrome://tracing) here")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -52,6 +53,17 @@ def main():
         last[stream] = v
     tot = plan.profile_read("total")
     print(f"total (median) {np.median(tot) * 1e3:.1f} us")
+    if a.chrome:
+        # one complete event per kernel: from the previous event on its stream
+        import json
+        ev, last = [], {}
+        for n, v in zip(names, t):
+            stream = "s1" if n.startswith("near") else "s0"
+            t0 = last.get(stream, 0.0)
+            ev.append({"name": n, "ph": "X", "ts": t0, "dur": max(v - t0, 0.0), "pid": 0,
+                       "tid": 1 if stream == "s1" else 0})
+            last[stream] = v
+        json.dump({"traceEvents": ev, "displayTimeUnit": "ns"}, open(a.chrome, "w"))
 
 
 if __name__ == "__main__":
