@@ -641,6 +641,9 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   // as their source amplitudes are final (see enqueue_T)
   P->split_lv = P->L + 1;
   for (int lv = P->L; lv >= P->l0 && P->loc_count[lv - P->l0] >= P->wide_level; --lv) P->split_lv = lv;
+  // the split point must be a per-level kernel's output: levels inside the
+  // fused coarse range are all produced by one kernel at its end
+  if (P->fused_lf > P->l0 && P->split_lv <= P->fused_lf) P->split_lv = P->fused_lf + 1;
   {
     std::vector<int32_t> ids;  // fine levels first
     for (int lv = P->L; lv >= P->l0; --lv) {

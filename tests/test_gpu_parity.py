@@ -419,3 +419,17 @@ def test_loaded_problem_gives_identical_products(tmp_path):
     t2, tab2 = load_problem(str(tmp_path / "p.npz"))
     q = geo.random_rhs(30000, 9).astype(np.complex64)
     assert np.array_equal(mvp(tree, tables, q), mvp(t2, tab2, q))
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_q48_split_and_fused_levels(monkeypatch, dtype, tol):
+    # Q != 64 with several "wide" levels: the side-stream translation split
+    # must sit outside the fused coarse range (regression: C3 capture error)
+    monkeypatch.setenv("NESA_WIDE_LEVEL", "64")
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=2), 30000)
+    tree = build_tree(pts, TreeParams(P=48))
+    params = NesaParams(Q=48)
+    q = geo.random_rhs(30000, 2)
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    qq = q if dtype == "f64" else q.astype(np.complex64)
+    assert rel_l2(mvp(tree, params, qq), ref) <= tol

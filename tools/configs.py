@@ -1,0 +1,72 @@
+"""Products/s on the BASELINE configurations C1-C4 (2D analogs).
+
+    python tools/configs.py [--reps 200]
+
+C1: unit circle (random angles, seed 0), N = 2 000,   P = 32, Q = 24
+C2: unit circle (seed 1),                N = 20 000,  P = 32, Q = 32
+C3: ellipse (5, 0.5) + 2 plates, seed 2, N = 200 000, P = 48, Q = 48
+C4: ellipse (5, 0.5) + 2 plates, seed 3, N = 2M,      P = 64, Q = 64
+Each with a float32 plan / complex64 vector and a float64 plan / complex128
+vector; device-resident, CUDA events around `reps` back-to-back products.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, HERE)
+
+CONFIGS = [
+    ("C1", "circle-random", 2_000, 0, 32, 24),
+    ("C2", "circle-random", 20_000, 1, 32, 32),
+    ("C3", "ellipse-plates", 200_000, 2, 48, 48),
+    ("C4", "ellipse-plates", 2_000_000, 3, 64, 64),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--only", default="")
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.plan import NesaPlan
+    out = []
+    for name, kind, n, seed, P, Q in CONFIGS:
+        if a.only and name not in a.only.split(","):
+            continue
+        t0 = time.perf_counter()
+        pts = nesa.generate_sources(nesa.CurveSpec(kind=kind, seed=seed), n)
+        tree = nesa.build_tree(pts, nesa.TreeParams(P=P))
+        tables = nesa.build_tables(tree, nesa.NesaParams(Q=Q))
+        t_build = time.perf_counter() - t0
+        q = nesa.random_rhs(n, seed)
+        for dt, cdt in (("f32", np.complex64), ("f64", np.complex128)):
+            plan = NesaPlan(tree, tables, dtype=dt)
+            qd = torch.from_numpy(q.astype(cdt)).cuda()
+            phi = torch.empty_like(qd)
+            st = torch.cuda.current_stream()
+            for _ in range(10):
+                plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 1, True, stream=st.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(a.reps):
+                plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 1, True, stream=st.cuda_stream)
+            e1.record(st)
+            e1.synchronize()
+            us = e0.elapsed_time(e1) / a.reps * 1e3
+            rec = {"config": name, "N": n, "P": P, "Q": Q, "levels": tree.L - tree.l0 + 1,
+                   "plan": dt, "us_per_product": round(us, 1), "products_per_s": round(1e6 / us, 1),
+                   "kernels": plan.stat("kernels_per_matvec"), "host_build_s": round(t_build, 2)}
+            print(json.dumps(rec), flush=True)
+            out.append(rec)
+            plan.close()
+    return out
+
+
+if __name__ == "__main__":
+    main()
