@@ -187,6 +187,12 @@ int nesa_profile_read(nesa_plan* plan, int32_t stage, float* ms, int32_t max);
  * returns the count; nesa_trace_name(i) names the kernel of entry i. */
 int nesa_trace_read(nesa_plan* plan, float* ms, int32_t max);
 const char* nesa_trace_name(nesa_plan* plan, int32_t i);
+/* Diagnostics: per-CTA kernel timeline without graph nodes.  enable(cap)
+ * makes every instrumented CTA append {tag, grid, start_ns, end_ns}
+ * (process-wide; cap 0 turns it off); read copies up to max records
+ * (4 x uint64 each), resets the log and returns the count. */
+int nesa_ktrace_enable(nesa_plan* plan, int64_t capacity);
+int64_t nesa_ktrace_read(nesa_plan* plan, unsigned long long* out, int64_t max_records);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,42 @@
 namespace nesa {
 
 // ----------------------------------------------------------------------------
+// Kernel timeline (diagnostics, NESA_KTRACE): when g_kt_buf is set, thread 0
+// of every CTA of an instrumented kernel appends {tag, grid, start, end}
+// (%globaltimer, ns) -- a non-perturbing view of the concurrent schedule that
+// graph event nodes cannot give.  One global load + branch per CTA when off.
+// ----------------------------------------------------------------------------
+__device__ unsigned long long* g_kt_buf = nullptr;
+__device__ unsigned int* g_kt_cnt = nullptr;
+__device__ unsigned int g_kt_cap = 0;
+
+__device__ __forceinline__ unsigned long long kt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct KtScope {
+  unsigned long long t0;
+  int tag;
+  __device__ __forceinline__ explicit KtScope(int t) : t0(0), tag(t) {
+    if (threadIdx.x == 0 && g_kt_buf) t0 = kt_now();
+  }
+  __device__ __forceinline__ ~KtScope() {
+    if (threadIdx.x == 0 && g_kt_buf) {
+      const unsigned int i = atomicAdd(g_kt_cnt, 1u);
+      if (i < g_kt_cap) {
+        unsigned long long* r = g_kt_buf + 4ull * i;
+        r[0] = (unsigned long long)tag;
+        r[1] = gridDim.x;
+        r[2] = t0;
+        r[3] = kt_now();
+      }
+    }
+  }
+};
+
+// ----------------------------------------------------------------------------
 // Block GEMV engine (near field, radiation V, reception U)
 // ----------------------------------------------------------------------------
 // A work item is a dense m x n block stored column-major at blob[a_off]; its
@@ -162,6 +198,7 @@ __device__ __forceinline__ void ldx(const T* p, T v[R]) {
 
 template <typename T, int R, int MODE, int NST = kStages>
 __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel(const BlockGemvArgs<T> a) {
+  KtScope kt_(10 + MODE);
   using Lay = BGLayout<T, R, MODE, NST>;
   constexpr int kStages = NST;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -332,6 +369,7 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
 template <typename T, int R>
 __global__ void gather_kernel(const T* __restrict__ q, const int64_t* __restrict__ perm,
                               T* __restrict__ qt, int64_t n, int ldq) {
+  KtScope kt_(1);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = perm[i];
@@ -345,6 +383,7 @@ template <typename T, int R>
 __global__ void scatter_kernel(const T* __restrict__ phin, const T* __restrict__ phif,
                                const int64_t* __restrict__ perm, T* __restrict__ phi, int64_t row0,
                                int64_t n, int ldp) {
+  KtScope kt_(2);
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t j = perm[row0 + i];
@@ -525,6 +564,7 @@ struct LevelArgs {
 
 template <typename T, int R, int MODE>
 __global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R> a) {
+  KtScope kt_(20 + MODE);
   extern __shared__ __align__(128) unsigned char smem[];
   const FarGeom G = far_geom(a.Q);
   const int Q = a.Q, QR = Q * R, TC = a.TC;
@@ -737,6 +777,7 @@ __host__ __device__ inline size_t fused_smem_bytes(int Q, int R) {
 
 template <typename T, int R>
 __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs<T> a) {
+  KtScope kt_(30);
   extern __shared__ __align__(128) unsigned char smem[];
   const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
   const size_t mb = mat_bytes(Q, sizeof(T));
@@ -807,6 +848,7 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
 
 template <typename T, int R>
 __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedArgs<T> a) {
+  KtScope kt_(31);
   extern __shared__ __align__(128) unsigned char smem[];
   const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
   const size_t mb = mat_bytes(Q, sizeof(T));
@@ -870,6 +912,7 @@ __global__ void sum_children_kernel(const int64_t* __restrict__ child_first,
                                     const int32_t* __restrict__ n_child, int64_t first,
                                     int64_t count, int64_t cf_lo, int64_t cf_hi,
                                     const T* __restrict__ Tin, T* s, int Q) {
+  KtScope kt_(32);
   pdl_trigger();
   pdl_wait();
   const int QR = Q * R;
@@ -890,6 +933,7 @@ template <typename T, int R>
 __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
                               const int64_t* __restrict__ int_ptr, const T* __restrict__ Y, T* o,
                               int Q) {
+  KtScope kt_(33);
   pdl_trigger();
   pdl_wait();
   const int QR = Q * R;
@@ -1025,6 +1069,7 @@ __global__ void __launch_bounds__(kTGThreads) tgemm_kernel(const TUnit* __restri
                                                            const TEnt* __restrict__ ents,
                                                            const T* __restrict__ DT,
                                                            const T* __restrict__ s, T* Y, int Q) {
+  KtScope kt_(40);
   extern __shared__ __align__(128) unsigned char smem[];
   const TGGeom G = tg_geom(Q);
   const int QR = Q * R, per = G.NC / R;
@@ -1151,6 +1196,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
                                                        const TEnt* __restrict__ ents,
                                                        const T* __restrict__ DT,
                                                        const T* __restrict__ s, T* Y, T* Y2) {
+  KtScope kt_(41);
   using W = TGW<T, R, QT, KT>;
   extern __shared__ __align__(128) unsigned char smem[];
   T* Dm = reinterpret_cast<T*>(smem);
@@ -1321,6 +1367,7 @@ __global__ void __launch_bounds__(128) tgemm_tc_kernel(const TUnit* __restrict__
                                                        const TEnt* __restrict__ ents,
                                                        const float* __restrict__ DTC,
                                                        const float* __restrict__ s, float* Y) {
+  KtScope kt_(42);
   constexpr int QT = 64, QR = QT * R;
   constexpr int EPT = 128 / R;  // entries per M = 128 tile
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1529,6 +1576,7 @@ struct LVW {
 
 template <typename T, int R, int QT, int MODE>
 __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) {
+  KtScope kt_(50 + MODE);
   using W = TGW<T, R, QT>;
   using LV = LVW<T, R, QT, MODE>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1799,6 +1847,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
     int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0, int bufpts = kMomBufPts) {
+  KtScope kt_(60 + int(MU_OUT));
   constexpr int MP = 40 / R;           // moments per pass
   constexpr int NV = 2 * R * MP;       // 80 accumulators
   constexpr int NV2 = NV / 2, NV4 = NV / 4;
@@ -1993,6 +2042,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
     const float2* __restrict__ E, const float* __restrict__ o, const float* __restrict__ phin,
     const int64_t* __restrict__ perm, float* __restrict__ phi, int64_t leaf0, int64_t nleaf, int Q,
     int nt, int ldp) {
+  KtScope kt_(70 + int(BETA_IN));
   extern __shared__ float4 sm4[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = ((nt + 1) * R + 1) & ~1;            // beta float2, even

@@ -1900,6 +1900,57 @@ NESA_API int nesa_profile_reset(nesa_plan* P) {
   })
 }
 
+// Kernel timeline diagnostics (see KtScope in nesa_kernels.cuh): capacity
+// records of {tag, grid, start_ns, end_ns}; capacity 0 turns it off.
+namespace {
+DevBuf<unsigned long long> g_kt_host_buf;
+DevBuf<unsigned int> g_kt_host_cnt;
+}  // namespace
+
+NESA_API int nesa_ktrace_enable(nesa_plan* P, int64_t capacity) {
+  NESA_GUARD({
+    require(P != nullptr && capacity >= 0, "bad argument");
+    CUDA_OK(cudaSetDevice(P->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    unsigned long long* bp = nullptr;
+    unsigned int* cp = nullptr;
+    unsigned int cap = 0;
+    if (capacity > 0) {
+      g_kt_host_buf.alloc(size_t(capacity) * 4);
+      g_kt_host_cnt.alloc(1);
+      bp = g_kt_host_buf.p;
+      cp = g_kt_host_cnt.p;
+      cap = unsigned(capacity);
+    }
+    CUDA_OK(cudaMemcpyToSymbol(nesa::g_kt_buf, &bp, sizeof(bp)));
+    CUDA_OK(cudaMemcpyToSymbol(nesa::g_kt_cnt, &cp, sizeof(cp)));
+    CUDA_OK(cudaMemcpyToSymbol(nesa::g_kt_cap, &cap, sizeof(cap)));
+    return NESA_OK;
+  })
+}
+
+// Copies up to max_records records (4 x uint64 each) and resets the log;
+// returns the number of records written (< 0: error).
+NESA_API int64_t nesa_ktrace_read(nesa_plan* P, unsigned long long* out, int64_t max_records) {
+  try {
+    require(P != nullptr && out != nullptr, "null argument");
+    CUDA_OK(cudaSetDevice(P->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    if (!g_kt_host_cnt.p) return 0;
+    unsigned int n = 0;
+    CUDA_OK(cudaMemcpy(&n, g_kt_host_cnt.p, sizeof(n), cudaMemcpyDeviceToHost));
+    const int64_t cnt = std::min<int64_t>({int64_t(n), max_records, int64_t(g_kt_host_buf.n / 4)});
+    if (cnt > 0)
+      CUDA_OK(cudaMemcpy(out, g_kt_host_buf.p, size_t(cnt) * 4 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemset(g_kt_host_cnt.p, 0, sizeof(unsigned int)));
+    return cnt;
+  } catch (const NesaError& e) {
+    g_last_error = e.what();
+    return -e.code;
+  }
+}
+
 // Diagnostics (NESA_TRACE=1 plans, profiled products): time of the event
 // after each traced kernel of the LAST profiled product, in ms from its start.
 NESA_API int nesa_trace_read(nesa_plan* P, float* ms, int32_t max) {

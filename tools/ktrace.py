@@ -1,0 +1,86 @@
+"""Concurrent kernel timeline of one product from in-kernel %globaltimer
+records (no graph nodes added, schedule unperturbed).
+
+    python tools/ktrace.py [--n 2000000] [--reps 5] [--chrome out.json]
+
+Per kernel launch (tag, grid): first CTA start, last CTA end (us from the
+product's first CTA), span, CTA count; medians over reps.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, HERE)
+
+TAGS = {1: "gather", 2: "scatter", 10: "blockgemv(store: near)", 11: "blockgemv(scatter: U)",
+        20: "level_kernel up-leaf", 21: "level_kernel up-sum", 22: "level_kernel down",
+        30: "fused_up", 31: "fused_down", 32: "sum_children", 33: "reduce", 40: "tgemm",
+        41: "tgemm_wt (FFMA)", 42: "tgemm_tc (tcgen05)", 50: "level_wt up-leaf",
+        51: "level_wt up-sum", 52: "level_wt down", 60: "radiation moments (in-kernel A)",
+        61: "radiation moments", 70: "reception (in-kernel beta)", 71: "reception series"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=2_000_000)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--chrome", default="")
+    ap.add_argument("--near", type=int, default=1)
+    ap.add_argument("--far", type=int, default=1)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.plan import NesaPlan
+    pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=3), a.n)
+    tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
+    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype="f32")
+    q = torch.from_numpy(nesa.random_rhs(a.n, 3).astype(np.complex64)).cuda()
+    phi = torch.empty_like(q)
+    st = torch.cuda.current_stream()
+    lib = plan.lib
+    cap = 1 << 16
+    for _ in range(5):
+        plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, near=bool(a.near), far=bool(a.far),
+                        stream=st.cuda_stream)
+    lib.nesa_ktrace_enable(plan.handle, cap)
+    buf = (ctypes.c_uint64 * (4 * cap))()
+    runs = []
+    for _ in range(a.reps):
+        plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, near=bool(a.near), far=bool(a.far),
+                        stream=st.cuda_stream)
+        torch.cuda.synchronize()
+        n = lib.nesa_ktrace_read(plan.handle, buf, cap)
+        rec = np.frombuffer(buf, dtype=np.uint64, count=4 * n).reshape(n, 4).astype(np.int64)
+        t0 = rec[:, 2].min()
+        launches = {}
+        for tag, grid, s, e in rec:
+            k = (int(tag), int(grid))
+            lo, hi, c = launches.get(k, (1 << 62, 0, 0))
+            launches[k] = (min(lo, s - t0), max(hi, e - t0), c + 1)
+        runs.append(launches)
+    lib.nesa_ktrace_enable(plan.handle, 0)
+    keys = sorted(runs[0], key=lambda k: runs[0][k][0])
+    rows = []
+    print(f"{'kernel':34s} {'grid':>6s} {'start':>8s} {'end':>8s} {'span':>8s} {'CTAs':>6s}")
+    for k in keys:
+        st_ = np.median([r[k][0] for r in runs if k in r]) / 1e3
+        en = np.median([r[k][1] for r in runs if k in r]) / 1e3
+        c = runs[0][k][2]
+        name = TAGS.get(k[0], str(k[0]))
+        rows.append((name, k[1], st_, en))
+        print(f"{name:34s} {k[1]:6d} {st_:8.1f} {en:8.1f} {en - st_:8.1f} {c:6d}")
+    tot = np.median([max(v[1] for v in r.values()) for r in runs]) / 1e3
+    print(f"product span (first CTA start -> last CTA end): {tot:.1f} us")
+    if a.chrome:
+        ev = [{"name": n, "ph": "X", "ts": s, "dur": e - s, "pid": 0,
+               "tid": 1 if n.startswith("blockgemv") else 0, "args": {"grid": g}}
+              for n, g, s, e in rows]
+        json.dump({"traceEvents": ev}, open(a.chrome, "w"))
+
+
+if __name__ == "__main__":
+    main()
