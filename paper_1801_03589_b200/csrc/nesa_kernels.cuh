@@ -36,6 +36,11 @@ __device__ __forceinline__ unsigned long long kt_now() {
   return t;
 }
 
+// complex multiply on float2 (re, im)
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
 struct KtScope {
   unsigned long long t0;
   int tag;
@@ -539,7 +544,22 @@ __device__ __forceinline__ void tile_reduce(const FarGeom& G, const TileMap& m, 
 // fastmvp.py:163-169 (translations first, then potential transfer).
 // Matrices arrive by bulk copy; amplitudes by cp.async or summed in staging.
 // ----------------------------------------------------------------------------
-enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2 };
+enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2, kLvlDownRecv = 3 };
+
+// kLvlDownRecv (leaf level, float32 expansion plans): the leaf-level
+// downward transfer, the reception coefficients and the reception itself in
+// one kernel (see level_wt_kernel).
+struct RecvArgs {
+  const float* ET;          // [64][64]: ET[j * 64 + row] = E^[row][j] (row 0 = 1, 2m-1 / 2m = Re / Im (1/m) e^{-i m theta_j})
+  const float2* prel;       // [N] point - leaf center
+  const int64_t* gstart;    // [NL] leaf point ranges
+  const int64_t* gstop;
+  const float* leaf_r;      // [NL] incoming aux radius
+  const float* phin;        // [N][R] near field (tree order) or null
+  const int64_t* perm;      // tree row -> original row
+  float* phi;               // output, original order, rows of stride ldp
+  int ldp, nt;
+};
 
 template <typename T>
 size_t level_smem_bytes(int Q, int qs) {
@@ -1550,6 +1570,207 @@ __global__ void __launch_bounds__(128) tgemm_tc_kernel(const TUnit* __restrict__
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
+// Variant with the A operand (sources, split hi / lo) in TMEM instead of
+// shared memory (tcgen05.mma ... [d], [a_tmem], b_desc): thread m = TMEM
+// lane m writes its row with tcgen05.st, and the epilogue stages half a
+// tile at a time, so the kernel needs ~50 KB of shared memory and two CTAs
+// fit beside the near field's two on an SM.  TMEM: 256 columns =
+// accumulator [0, 64) | A_hi [64, 128) | A_lo [128, 192).
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(kTcIdesc), "r"(0u));
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, float4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+               "r"(__float_as_uint(v.w))
+               : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(128) tgemm_tc2_kernel(const TUnit* __restrict__ units,
+                                                        const TEnt* __restrict__ ents,
+                                                        const float* __restrict__ DTC,
+                                                        const float* __restrict__ s, float* Y) {
+  KtScope kt_(43);
+  constexpr int QT = 64, QR = QT * R;
+  constexpr int EPT = 128 / R;   // entries per M = 128 tile
+  constexpr int HALF = EPT / 2;  // entries staged per epilogue round
+  constexpr int OS = QR + 4;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Bhi = reinterpret_cast<float*>(smem);        // 16 KB
+  float* Blo = Bhi + 4096;                             // 16 KB
+  float* stage = Blo + 4096;                           // HALF x OS floats
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + ((HALF * OS + 3) & ~3));  // [0] D, [1] MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  int32_t* eids = reinterpret_cast<int32_t*>(tslot + 4);
+  const TUnit u = units[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bar[0], 2 * kTcBBytes);
+    bulk_g2s(Bhi, DTC + size_t(u.dtab) * (2 * 4096), 2 * kTcBBytes, &bar[0]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const uint32_t t_acc = tmem + lane_base, t_hi = tmem + lane_base + 64, t_lo = tmem + lane_base + 128;
+  pdl_trigger();
+  pdl_wait();  // s comes from the upward pass
+  const int n_all = u.ent_end - u.ent_begin;
+  const int m = tid, e = m / R, rr = m - (m / R) * R;
+  float4 c[16];
+  int32_t eid = -1;
+  auto load = [&](int t0) {
+    const bool live = t0 + e < n_all;
+    eid = -1;
+    int64_t srcg = 0;
+    if (live) {
+      const TEnt te = ents[u.ent_begin + t0 + e];
+      eid = te.e;
+      srcg = te.src;
+    }
+    if constexpr (R == 1 || R == 2) {
+      const float4* src4 = reinterpret_cast<const float4*>(s + srcg * QR) + rr * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c[i] = live ? src4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float* src = s + srcg * QR + rr;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        c[i] = live ? make_float4(src[(4 * i) * R], src[(4 * i + 1) * R], src[(4 * i + 2) * R],
+                                  src[(4 * i + 3) * R])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto put = [&](int kb, float4 v) {  // columns 4kb..4kb+3 of this thread's row
+    float4 h, l;
+    h.x = tf32_rna(v.x);
+    h.y = tf32_rna(v.y);
+    h.z = tf32_rna(v.z);
+    h.w = tf32_rna(v.w);
+    l.x = tf32_rna(v.x - h.x);
+    l.y = tf32_rna(v.y - h.y);
+    l.z = tf32_rna(v.z - h.z);
+    l.w = tf32_rna(v.w - h.w);
+    tmem_st4(t_hi + 4 * kb, h);
+    tmem_st4(t_lo + 4 * kb, l);
+  };
+  uint32_t phase = 0;
+  load(0);
+  for (int t0 = 0; t0 < n_all; t0 += EPT) {
+    const int eid_t = eid;
+    if constexpr (R == 1 || R == 4) {
+      // R = 1: c[i] = k 4i..4i+3 of this row; R = 4: the loader fetched the
+      // component rr strided (one float4 = 4 consecutive k)
+#pragma unroll
+      for (int kb = 0; kb < 16; ++kb) put(kb, c[kb]);
+    } else {
+      float mine[32], other[32];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        mine[2 * i] = rr ? c[i].y : c[i].x;
+        mine[2 * i + 1] = rr ? c[i].w : c[i].z;
+        other[2 * i] = rr ? c[i].x : c[i].y;
+        other[2 * i + 1] = rr ? c[i].z : c[i].w;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
+      // tcgen05.st is warp-collective (one column address per warp): lane rr
+      // owns k in [32 rr, 32 rr + 32) as `mine`, the rest as `other`
+#pragma unroll
+      for (int kb = 0; kb < 8; ++kb) {
+        const float4 a = make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]);
+        const float4 b = make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]);
+        put(kb, rr ? b : a);       // k in [0, 32)
+        put(8 + kb, rr ? a : b);   // k in [32, 64)
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      if (t0 == 0) mbar_wait(&bar[0], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t bh = smem_u32(Bhi), bl = smem_u32(Blo);
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) {
+        const uint32_t a0 = tmem + (cc == 2 ? 128u : 64u), b0 = cc == 1 ? bl : bh;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          umma_tf32_ts(tmem, a0 + ks * 8, umma_desc_kmajor(b0 + ks * 2 * kTcLBO), (cc | ks) != 0);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&bar[1]))
+                   : "memory");
+    }
+    if (t0 + EPT < n_all) load(t0 + EPT);  // overlaps the tensor core
+    mbar_wait(&bar[1], phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+        "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+        "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]),
+          "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
+          "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+          "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+          "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]),
+          "=r"(r[63])
+        : "r"(t_acc));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (rr == 0) eids[e] = eid_t;
+    const int n = min(EPT, n_all - t0);
+    const uint64_t keep = l2_evict_last_policy();  // Y is re-read by reduce_kernel
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e0 = h * HALF;
+      if (e >= e0 && e < e0 + HALF && eid_t >= 0)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
+      __syncthreads();
+      constexpr int NV = QR / 4;
+      const int nh = max(0, min(HALF, n - e0));
+      for (int i = tid; i < nh * NV; i += 128) {
+        const int ee = i / NV, v = i - (i / NV) * NV;
+        const float4 val = *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
+        st16_hint(Y + int64_t(eids[e0 + ee]) * QR + 4 * v, val, keep);
+      }
+      __syncthreads();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int R>
+constexpr size_t tc2_smem_bytes() {
+  constexpr int HALF = 64 / R, OS = 64 * R + 4;
+  return 2 * size_t(kTcBBytes) + size_t((HALF * OS + 3) & ~3) * 4 + 64 + 4 * 128 + 256;
+}
+
 // bytes of dynamic shared memory of tgemm_tc_kernel
 constexpr size_t kTcSmem = 6 * size_t(kTcBBytes) + 64 + 4 * 128 + 1024;
 
@@ -1570,20 +1791,25 @@ struct LVW {
   // most 3) boundary tiles of a level need a second round; one slot keeps the
   // kernel small enough to run 2-3 CTAs per SM beside the near field
   static constexpr int kSlots = LVW_SLOTS;
-  static constexpr int kXBufs = MODE == 2 ? 2 : 1;  // kLvlDown also stages o[c]
-  static constexpr size_t SMEM = kSlots * W::MB + kXBufs * W::XB + 3 * 64;
+  static constexpr bool kDown = MODE == 2 || MODE == 3;
+  static constexpr int kXBufs = kDown ? 2 : 1;      // the downward modes also stage o[c]
+  static constexpr int kEMat = MODE == 3 ? 1 : 0;   // kLvlDownRecv: the E^ matrix
+  static constexpr size_t SMEM = (kSlots + kEMat) * W::MB + kXBufs * W::XB + 3 * 64;
 };
 
 template <typename T, int R, int QT, int MODE>
-__global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) {
+__global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, const RecvArgs rv) {
   KtScope kt_(50 + MODE);
   using W = TGW<T, R, QT>;
   using LV = LVW<T, R, QT, MODE>;
+  constexpr bool kDown = LV::kDown;
   extern __shared__ __align__(128) unsigned char smem[];
   T* M = reinterpret_cast<T*>(smem);                                  // kSlots matrices
   T* X = reinterpret_cast<T*>(smem + LV::kSlots * W::MB);             // inputs / outputs
   T* Oc = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + W::XB);    // down: o[c] (reduce output)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LV::kSlots * W::MB + LV::kXBufs * W::XB);  // M, X
+  T* Em = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + LV::kXBufs * W::XB);  // kLvlDownRecv: E^
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (LV::kSlots + LV::kEMat) * W::MB +
+                                               LV::kXBufs * W::XB);  // M, X
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t t0 = int64_t(blockIdx.x) * W::PER;
   const int n = int(a.count - t0 < W::PER ? a.count - t0 : W::PER);
@@ -1647,13 +1873,17 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
     }
   } else {
     if (warp == 0) {
-      const uint32_t nb = (MODE == kLvlDown ? 2u : 1u) * kVB * uint32_t(n);
-      if (lane == 0) mbar_arrive_expect_tx(&bar[1], nb);
+      const uint32_t nb = (kDown ? 2u : 1u) * kVB * uint32_t(n) + (MODE == kLvlDownRecv ? uint32_t(W::MB) : 0u);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bar[1], nb);
+        if constexpr (MODE == kLvlDownRecv)
+          if constexpr (sizeof(T) == 4) bulk_g2s(Em, rv.ET, uint32_t(W::MB), &bar[1]);
+      }
       __syncwarp();
       for (int p = lane; p < n; p += 32) {
-        const int64_t g = MODE == kLvlDown ? a.opar[t0 + p] : a.order[t0 + p];
-        bulk_g2s(X + p * W::XS, (MODE == kLvlDown ? a.o : a.s) + g * W::QR, kVB, &bar[1]);
-        if constexpr (MODE == kLvlDown)
+        const int64_t g = kDown ? a.opar[t0 + p] : a.order[t0 + p];
+        bulk_g2s(X + p * W::XS, (kDown ? a.o : a.s) + g * W::QR, kVB, &bar[1]);
+        if constexpr (kDown)
           bulk_g2s(Oc + p * W::XS, a.o + int64_t(a.order[t0 + p]) * W::QR, kVB, &bar[1]);
       }
     }
@@ -1734,7 +1964,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int idx = p * W::XS + (row0 + r) * R + rr;
-        if constexpr (MODE == kLvlDown)
+        if constexpr (kDown)
           X[idx] = Oc[idx] + acc[r][c];  // translation sum + potential transfer
         else
           X[idx] = acc[r][c];
@@ -1742,7 +1972,76 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
     }
   }
   __syncthreads();
-  T* outb = MODE == kLvlDown ? a.o : a.Tout;
+  if constexpr (MODE == kLvlDownRecv) {
+    if constexpr (sizeof(T) == 4 && QT == 64) {
+      // ---- reception coefficients of the tile's leaves: beta^ = E^ o (same
+      // warp tiling; E^ is one matrix for every column), into the Oc buffer
+      if (E0 + tc < n) {
+        const T* xp = X + (E0 + tc) * W::XS;
+        const T* mp = Em + row0;
+        T part[8][4];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) part[r][c] = T(0);
+#pragma unroll 4
+        for (int j = 0; j < QT; ++j) {
+          T m0[4], m1[4], x[4];
+          ld4(mp + j * QT, m0);
+          ld4(mp + j * QT + 4, m1);
+#pragma unroll
+          for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              part[r][c] = fma(m0[r], x[c], part[r][c]);
+              part[r + 4][c] = fma(m1[r], x[c], part[r + 4][c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int p = E0 + tc + 8 * (c / R), rr = c % R;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) Oc[p * W::XS + (row0 + r) * R + rr] = part[r][c];
+        }
+      }
+      __syncthreads();
+      // ---- reception of the tile's leaves: warp w takes leaves w, w+4, ...;
+      // lane = point; phi[perm] = phin + beta_0 + Re sum_m beta_m w^m
+      for (int p = warp; p < n; p += 4) {
+        const int64_t leaf = a.order[t0 + p];
+        const int64_t b = rv.gstart[leaf];
+        const int np = int(rv.gstop[leaf] - b);
+        const float rad = rv.leaf_r[leaf];
+        const float inv = 1.f / rad, nlr = -logf(rad);
+        const T* bt = Oc + p * W::XS;  // row r, component rr at r * R + rr
+        for (int j = lane; j < np; j += 32) {
+          const int64_t i = b + j;
+          const float2 pt = rv.prel[i];
+          const int64_t dst = rv.perm[i];
+          float accv[R];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) accv[rr] = (rv.phin ? rv.phin[i * R + rr] : 0.f) + nlr * bt[rr];
+          const float2 w = make_float2(pt.x * inv, pt.y * inv);
+          float2 z = w;
+#pragma unroll 4
+          for (int m = 1; m <= rv.nt; ++m) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              const float br = bt[(2 * m - 1) * R + rr], bi = bt[(2 * m) * R + rr];
+              accv[rr] = fmaf(br, z.x, fmaf(-bi, z.y, accv[rr]));
+            }
+            z = cmulf(z, w);
+          }
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) rv.phi[dst * rv.ldp + rr] = accv[rr];
+        }
+      }
+    }
+    return;
+  }
+  T* outb = kDown ? a.o : a.Tout;
   constexpr int V = 16 / int(sizeof(T));
   constexpr int NV = W::QR / V;
   for (int i = tid; i < n * NV; i += 128) {
@@ -1776,9 +2075,6 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a) 
 // rounding).  One warp per leaf; moment sums over the leaf's points use a
 // fixed transpose-reduction tree (deterministic).
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-}
 
 // Sum 32 per-lane values over the warp: afterwards lane l returns the sum of
 // value l (31 shuffles; fixed pairing, so bitwise reproducible).

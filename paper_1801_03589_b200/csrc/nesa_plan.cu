@@ -349,6 +349,7 @@ struct nesa_plan {
   int mom_buf = 800;                        // staged points per warp in the moment kernel
   DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
+  bool tc2 = true;                          // ... with the A operand in TMEM (~50 KB smem)
   DevBuf<float> DTC;                        // [n_dtab][hi | lo][64 x 64] canonical tf32 D
   DevBuf<TUnit> mom_units;
   DevBuf<TEnt> mom_ents;
@@ -359,6 +360,8 @@ struct nesa_plan {
   DevBuf<TEnt> rad_ents;
   int n_rad_units = 0;
   bool beta_tc = false;                     // reception coefficients by tgemm_tc (E^ o)
+  bool recv_fused = false;                  // leaf down + beta + reception in one kernel
+  DevBuf<float> ET;                         // [64][64] E^ transposed for the warp-tiled GEMM
   DevBuf<float> ETC;                        // [hi | lo][64 x 64] canonical tf32 E^
   DevBuf<unsigned char> beta;               // [NL][64][R] reception coefficients
   DevBuf<unsigned char> mu;                 // [NL][mom_kt][R] moments
@@ -972,6 +975,27 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         P->ETC.upload(h);
         P->beta_tc = true;
       }
+      // leaf level handled by the wide kernels: fuse its downward transfer,
+      // beta^ = E^ o and the reception into one kernel (no o / beta round trip)
+      const char* rf = std::getenv("NESA_RECV_FUSED");
+      const bool leaf_wide = P->L > P->l0 && P->loc_count[P->L - P->l0] >= P->wide_level;
+      // (measured slower at C4, 641 vs 627 us: 8 warps per SM cannot hide the
+      // point loads the separate 48-warp reception kernel hides; opt in with
+      // NESA_RECV_FUSED=1)
+      if (Q == 64 && leaf_wide && 2 * P->u_nt + 1 <= 64 && rf && std::atoi(rf) != 0) {
+        std::vector<float> et(64 * 64, 0.f);
+        for (int row = 0; row < 64; ++row)
+          for (int k = 0; k < 64; ++k) {
+            float x = 0.f;
+            if (row == 0)
+              x = 1.f;
+            else if (row <= 2 * P->u_nt)
+              x = (row & 1) ? E[size_t(k) * ne + (row + 1) / 2].x : E[size_t(k) * ne + row / 2].y;
+            et[size_t(k) * 64 + row] = x;
+          }
+        P->ET.upload(et);
+        P->recv_fused = true;
+      }
     }
     if (P->mom_kt || P->beta_tc) {
       // one entry per local leaf (src = dst = leaf), 32 leaves per unit
@@ -1106,6 +1130,7 @@ void set_smem_attrs() {
   attr(level_wt_kernel<T, R, 64, kLvlUpLeaf>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlUpSum>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDown>, lim);
+  attr(level_wt_kernel<T, R, 64, kLvlDownRecv>, lim);
   attr(level_kernel<T, R, kLvlUpLeaf>, lim);
   attr(level_kernel<T, R, kLvlUpSum>, lim);
   attr(level_kernel<T, R, kLvlDown>, lim);
@@ -1121,6 +1146,7 @@ void set_smem_attrs() {
     attr(tgemm_wt_kernel<float, R, 64, 80>, lim);
     attr(tgemm_wt_kernel<float, R, 128, 80, 64>, lim);
     attr(tgemm_tc_kernel<R>, int(kTcSmem));
+    attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
     attr(reception_exp_kernel<R, true>, lim);
@@ -1213,8 +1239,12 @@ int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const 
   if (P->beta_tc) {
     // beta^ = E^ o for every leaf on the tensor cores, then the per-point series
     float* beta = reinterpret_cast<float*>(P->beta.p);
-    tgemm_tc_kernel<R><<<P->n_mom_units, 128, kTcSmem, st>>>(P->mom_units.p, P->mom_ents.p,
-                                                            P->ETC.p, o, beta);
+    if (P->tc2)
+      tgemm_tc2_kernel<R><<<P->n_mom_units, 128, tc2_smem_bytes<R>(), st>>>(P->mom_units.p, P->mom_ents.p,
+                                                                           P->ETC.p, o, beta);
+    else
+      tgemm_tc_kernel<R><<<P->n_mom_units, 128, kTcSmem, st>>>(P->mom_units.p, P->mom_ents.p,
+                                                              P->ETC.p, o, beta);
     reception_exp_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
         P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
         P->leaf_begin, nleaf, Q, nt, ldp);
@@ -1235,6 +1265,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   const bool near = flags & NESA_NEAR, far = flags & NESA_FAR, profn = flags & NESA_PROFILE;
   const bool prof = profn && !(flags & NESA_PROFILE_NEAR);  // stage marks on the far path
   cudaStream_t s0 = P->s0, s1 = P->s1;
+  cudaStream_t join_stream = s1;  // the near branch's last stream (s3 with a split near launch)
   T* qt = reinterpret_cast<T*>(P->qt.p);
   T* phin = reinterpret_cast<T*>(P->phin.p);
   T* s = reinterpret_cast<T*>(P->s.p);
@@ -1290,9 +1321,9 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
       if (lv == P->L)
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64, kLvlUpLeaf>::SMEM, s0, la);
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64, kLvlUpLeaf>::SMEM, s0, la, RecvArgs{});
       else
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64, kLvlUpSum>::SMEM, s0, la);
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64, kLvlUpSum>::SMEM, s0, la, RecvArgs{});
     } else if (lv == P->L) {
       launch_pdl(P->pdl, level_kernel<T, R, kLvlUpLeaf>, grid, kFarThreads, lvl_sm, s0, la);
     } else {
@@ -1318,9 +1349,14 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const T* DTp = reinterpret_cast<const T*>(P->DT.p);
     const TUnit* up = P->tunits.p + u0;
     if (P->tc) {
-      if constexpr (std::is_same<T, float>::value)
-        launch_pdl(P->pdl && st == s0, tgemm_tc_kernel<R>, u1 - u0, 128, kTcSmem, st, up,
-                   (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+      if constexpr (std::is_same<T, float>::value) {
+        if (P->tc2)
+          launch_pdl(P->pdl && st == s0, tgemm_tc2_kernel<R>, u1 - u0, 128, tc2_smem_bytes<R>(), st, up,
+                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+        else
+          launch_pdl(P->pdl && st == s0, tgemm_tc_kernel<R>, u1 - u0, 128, kTcSmem, st, up,
+                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+      }
     } else if (Q == 64)
       launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 64>, u1 - u0, 128, TGW<T, R, 64>::SMEM, st,
                  up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y, (T*)nullptr);
@@ -1342,13 +1378,38 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     nk++;
     tr("reduce", st);
   };
+  // the near field's completion joins the far stream once: before the fused
+  // leaf-level reception (recv_fused) or before finish()
+  bool near_joined = false, recv_done = false;
+  const bool far_recv = far && (stage == 0 || stage == 2);
+  auto join_near = [&]() {
+    if (near_joined) return;
+    near_joined = true;
+    CUDA_OK(cudaEventRecord(P->ev_join, join_stream));
+    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
+  };
   auto down_level = [&](int lv) {
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
     const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-      launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64, kLvlDown>::SMEM, s0, la);
+      if (lv == P->L && P->recv_fused && far_recv) {
+        // leaf level + reception coefficients + reception in one kernel: the
+        // near field must be complete (phin)
+        join_near();
+        if constexpr (std::is_same<T, float>::value) {
+          RecvArgs rv{P->ET.p, P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p,
+                      near ? reinterpret_cast<const float*>(phin) : nullptr, P->perm.p,
+                      reinterpret_cast<float*>(phi), P->ldv, P->u_nt};
+          launch_pdl(false, level_wt_kernel<T, R, 64, kLvlDownRecv>, gw, 128,
+                     LVW<T, R, 64, kLvlDownRecv>::SMEM, s0, la, rv);
+        }
+        recv_done = true;
+      } else {
+        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64, kLvlDown>::SMEM, s0, la,
+                   RecvArgs{});
+      }
     } else {
       launch_pdl(P->pdl, level_kernel<T, R, kLvlDown>, int((la.count + la.TC - 1) / la.TC),
                  kFarThreads, lvl_sm, s0, la);
@@ -1461,6 +1522,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     tr("gather", s0);
   };
   auto finish = [&]() {
+    if (recv_done) return;  // the fused leaf-level kernel wrote phi
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
     if (far && P->u_mf) {
       if constexpr (std::is_same<T, float>::value)
@@ -1497,6 +1559,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const int n_a = nsplit ? std::max(1, std::min(P->nearset.grid - 1,
                                                    int(P->near_frac * P->nearset.grid + 0.5)))
                            : P->nearset.grid;
+    if (nsplit) join_stream = P->s3;
     auto launch_near = [&]() {
       if (forked) return;
       forked = true;
@@ -1542,7 +1605,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     // float32 + near + far: the (compute-bound) matrix-free reception runs at
     // the end of the far branch into phif, overlapping the near field; the
     // join is followed by one combining scatter phi[perm] = phin + phif.
-    const bool rfar = far && near && P->u_mf && P->recv_far && std::is_same<T, float>::value;
+    const bool rfar = far && near && P->u_mf && P->recv_far && !P->recv_fused && std::is_same<T, float>::value;
     if (far) {
       far_pass(P->split, [&](int pos) {
         if (pos == P->near_after) launch_near();
@@ -1560,8 +1623,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         }
       }
     }
-    CUDA_OK(cudaEventRecord(P->ev_join, nsplit ? P->s3 : s1));
-    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
+    join_near();
     if (rfar) {
       scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
           phin, reinterpret_cast<const T*>(P->phif.p), P->perm.p, phi, P->pt_begin, nloc, P->ldv);
@@ -1585,8 +1647,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       nk++;
     }
     if (far) down_pass();
-    CUDA_OK(cudaEventRecord(P->ev_join, s1));
-    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
+    join_near();
     finish();
   }
   return nk;
@@ -1766,6 +1827,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     }
     if (const char* mb = std::getenv("NESA_MOM_BUF")) P->mom_buf = std::max(0, std::atoi(mb));
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
+    if (const char* tc2 = std::getenv("NESA_TC2")) P->tc2 = std::atoi(tc2) != 0;
     if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
     if (const char* ns = std::getenv("NESA_NEAR_SPLIT")) P->near_split = std::atoi(ns);
     if (const char* nf = std::getenv("NESA_NEAR_FRAC")) P->near_frac = std::atof(nf);

@@ -17,7 +17,7 @@ static float tf32h(float x) {  // host round-to-nearest-away tf32
   float y; memcpy(&y, &u, 4); return y;
 }
 
-template <int R>
+template <int R, int V>
 int run() {
   const int Q = 64, QR = Q * R, EPT = 128 / R;
   const int ndt = 3, G = 300, nunits = 7;
@@ -55,8 +55,14 @@ int run() {
   CK(cudaMemcpy(dU, units.data(), units.size() * sizeof(TUnit), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dE, ents.data(), ents.size() * sizeof(TEnt), cudaMemcpyHostToDevice));
   CK(cudaMemset(dY, 0, size_t(eidx) * QR * 4));
-  CK(cudaFuncSetAttribute(tgemm_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmem)));
-  tgemm_tc_kernel<R><<<nunits, 128, kTcSmem>>>(dU, dE, dD, dS, dY);
+  if (V == 1) {
+    CK(cudaFuncSetAttribute(tgemm_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmem)));
+    tgemm_tc_kernel<R><<<nunits, 128, kTcSmem>>>(dU, dE, dD, dS, dY);
+  } else {
+    CK(cudaFuncSetAttribute(tgemm_tc2_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(tc2_smem_bytes<R>())));
+    tgemm_tc2_kernel<R><<<nunits, 128, tc2_smem_bytes<R>()>>>(dU, dE, dD, dS, dY);
+  }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   std::vector<float> Y(size_t(eidx) * QR);
@@ -74,15 +80,18 @@ int run() {
           rmax = std::max(rmax, std::fabs(ref));
         }
     }
-  printf("R=%d max abs err %.3e (max |ref| %.3e, rel %.3e)\n", R, emax, rmax, emax / rmax);
+  printf("kernel %s R=%d max abs err %.3e (max |ref| %.3e, rel %.3e)\n", V == 1 ? "tc (A in smem)" : "tc2 (A in TMEM)", R, emax, rmax, emax / rmax);
   return emax / rmax < 1e-5 ? 0 : 2;
 }
 
 int main() {
   int rc = 0;
-  rc |= run<2>();
-  rc |= run<1>();
-  rc |= run<4>();
+  rc |= run<2, 1>();
+  rc |= run<1, 1>();
+  rc |= run<4, 1>();
+  rc |= run<2, 2>();
+  rc |= run<1, 2>();
+  rc |= run<4, 2>();
   printf(rc ? "FAIL\n" : "PASS\n");
   return rc;
 }
