@@ -387,6 +387,12 @@ struct nesa_plan {
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
   int64_t n_red_fine = 0;                    // red_ids [0, n_red_fine) are fine levels
+  std::vector<int> tu_start;                 // [lv - l0]: first translation unit of level lv
+  std::vector<int64_t> red_start;            // [lv - l0]: first red_ids entry of level lv
+  std::vector<cudaEvent_t> ev_lv;            // [lv - l0]: level lv's s is final
+  bool split_levels = false;                 // fine levels translated one by one as their s is final
+                                             // (NESA_SPLIT_LEVELS=1; measured slower: the translation
+                                             // CTAs delay the up chain)
 
   struct GraphKey {
     const void* q;
@@ -431,6 +437,8 @@ struct nesa_plan {
     if (s2) cudaStreamDestroy(s2);
     if (s3) cudaStreamDestroy(s3);
     if (ev_fork2) cudaEventDestroy(ev_fork2);
+    for (auto e : ev_lv)
+      if (e) cudaEventDestroy(e);
     if (ev_join2) cudaEventDestroy(ev_join2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -649,8 +657,10 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   if (P->fused_lf > P->l0 && P->split_lv <= P->fused_lf) P->split_lv = P->fused_lf + 1;
   {
     std::vector<int32_t> ids;  // fine levels first
+    P->red_start.assign(size_t(nlev) + 1, 0);
     for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
+      P->red_start[li] = int64_t(ids.size());
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         ids.push_back(int32_t(g));
       if (lv == P->split_lv) P->n_red_fine = int64_t(ids.size());
@@ -1038,8 +1048,10 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     std::vector<TUnit> units;
     std::vector<std::vector<TEnt>> by_d(size_t(std::max<int64_t>(d->n_dtab, 1)));
     // levels fine -> coarse; within a level grouped by unique D
+    P->tu_start.assign(size_t(P->L - P->l0 + 2), 0);
     for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
+      P->tu_start[li] = int(units.size());
       std::vector<int64_t> used;
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
@@ -1460,11 +1472,30 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   // upward chain, the coarse translations and the coarse downward levels.
   auto far_pass = [&](bool split, const std::function<void(int)>& hook) {
     const bool fine = split && P->split_lv <= P->L;
+    // per-level split: each fine level's translation + reduce goes to s2 as
+    // soon as that level's s is final (overlapping the rest of the up pass);
+    // units / red_ids are ordered fine -> coarse, level lv's range ends where
+    // level lv - 1's begins (or at the fine / total boundary)
+    const bool per_level = fine && P->split_levels;
+    auto unit_end = [&](int lv) {
+      return lv == P->split_lv ? P->n_tunits_fine : P->tu_start[lv - 1 - P->l0];
+    };
+    auto red_end = [&](int lv) {
+      return lv == P->split_lv ? P->n_red_fine : P->red_start[lv - 1 - P->l0];
+    };
     for (int lv = P->L; lv > P->l0; --lv) {
       if (fused && lv <= P->fused_lf) break;
       up_level(lv);
       if (lv == P->L) hook(2);
-      if (fine && lv == P->split_lv) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+      if (per_level && lv >= P->split_lv) {
+        const int li = lv - P->l0;
+        CUDA_OK(cudaEventRecord(P->ev_lv[li], s0));
+        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_lv[li], 0));
+        translate(P->tu_start[li], unit_end(lv), P->s2);
+        reduce(P->red_start[li], red_end(lv), P->s2);
+      } else if (fine && lv == P->split_lv) {
+        CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+      }
     }
     if (P->L == P->split_lv && fine && P->L == P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     if (fused) {
@@ -1476,9 +1507,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     hook(3);
     if (fine && P->split_lv == P->l0 && P->L > P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     if (fine) {
-      CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
-      translate(0, P->n_tunits_fine, P->s2);
-      reduce(0, P->n_red_fine, P->s2);
+      if (!per_level) {
+        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
+        translate(0, P->n_tunits_fine, P->s2);
+        reduce(0, P->n_red_fine, P->s2);
+      }
       CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
       translate(P->n_tunits_fine, P->n_tunits, s0);
       reduce(P->n_red_fine, P->n_red, s0);
@@ -1834,6 +1867,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
+    if (const char* sl = std::getenv("NESA_SPLIT_LEVELS")) P->split_levels = std::atoi(sl) != 0;
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
     P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
@@ -1866,10 +1900,21 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       CUDA_OK(cudaStreamCreateWithPriority(&P->s0, cudaStreamNonBlocking, P->priority ? hi : lo));
       CUDA_OK(cudaStreamCreateWithPriority(&P->s1, cudaStreamNonBlocking, lo));
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, P->priority ? hi : lo));
+      // s2 (side-stream translation) one step below the far chain so the
+      // latency-bound level kernels are scheduled first (NESA_S2_PRIO:
+      // 0 = same as the chain, 1 = middle, 2 = lowest)
+      int s2p = P->priority ? hi : lo;
+      if (const char* e = std::getenv("NESA_S2_PRIO")) {
+        const int v = std::atoi(e);
+        if (v == 1) s2p = (hi + lo) / 2 == hi ? std::min(lo, hi + 1) : (hi + lo) / 2;
+        if (v >= 2) s2p = lo;
+      }
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, s2p));
       CUDA_OK(cudaStreamCreateWithPriority(&P->s3, cudaStreamNonBlocking, lo));
     }
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork2, cudaEventDisableTiming));
+    P->ev_lv.assign(size_t(P->L - P->l0 + 1), nullptr);
+    for (auto& e : P->ev_lv) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join2, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_sfine, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_mark, cudaEventDisableTiming));
