@@ -1765,6 +1765,202 @@ __global__ void __launch_bounds__(128) tgemm_tc2_kernel(const TUnit* __restrict_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
+// Persistent form of tgemm_tc2_kernel: a CTA loops over units (grid-stride),
+// allocates TMEM once, and fetches the next unit's D as soon as the last MMA
+// of the current one has consumed the D buffer, so the D copy, the next
+// sources and the epilogue overlap instead of paying one CTA start per unit.
+template <int R>
+__global__ void __launch_bounds__(128) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
+                                                        const TEnt* __restrict__ ents,
+                                                        const float* __restrict__ DTC,
+                                                        const float* __restrict__ s, float* Y) {
+  KtScope kt_(44);
+  constexpr int QT = 64, QR = QT * R;
+  constexpr int EPT = 128 / R;
+  constexpr int HALF = EPT / 2;
+  constexpr int OS = QR + 4;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Bhi = reinterpret_cast<float*>(smem);
+  float* Blo = Bhi + 4096;
+  float* stage = Blo + 4096;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + ((HALF * OS + 3) & ~3));  // [0] D, [1] MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  int32_t* eids = reinterpret_cast<int32_t*>(tslot + 4);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  int ui = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    if (ui < n_units) {
+      mbar_arrive_expect_tx(&bar[0], 2 * kTcBBytes);
+      bulk_g2s(Bhi, DTC + size_t(units[ui].dtab) * (2 * 4096), 2 * kTcBBytes, &bar[0]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const uint32_t t_acc = tmem + lane_base, t_hi = tmem + lane_base + 64, t_lo = tmem + lane_base + 128;
+  pdl_trigger();
+  pdl_wait();  // s comes from the upward pass
+  const int m = tid, e = m / R, rr = m - (m / R) * R;
+  float4 c[16];
+  int32_t eid = -1;
+  auto load = [&](const TUnit& uu, int t0) {
+    const int na = uu.ent_end - uu.ent_begin;
+    const bool live = t0 + e < na;
+    eid = -1;
+    int64_t srcg = 0;
+    if (live) {
+      const TEnt te = ents[uu.ent_begin + t0 + e];
+      eid = te.e;
+      srcg = te.src;
+    }
+    if constexpr (R == 1 || R == 2) {
+      const float4* src4 = reinterpret_cast<const float4*>(s + srcg * QR) + rr * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c[i] = live ? src4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float* src = s + srcg * QR + rr;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        c[i] = live ? make_float4(src[(4 * i) * R], src[(4 * i + 1) * R], src[(4 * i + 2) * R],
+                                  src[(4 * i + 3) * R])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto put = [&](int kb, float4 v) {
+    float4 h, l;
+    h.x = tf32_rna(v.x);
+    h.y = tf32_rna(v.y);
+    h.z = tf32_rna(v.z);
+    h.w = tf32_rna(v.w);
+    l.x = tf32_rna(v.x - h.x);
+    l.y = tf32_rna(v.y - h.y);
+    l.z = tf32_rna(v.z - h.z);
+    l.w = tf32_rna(v.w - h.w);
+    tmem_st4(t_hi + 4 * kb, h);
+    tmem_st4(t_lo + 4 * kb, l);
+  };
+  const uint64_t keep = l2_evict_last_policy();  // Y is re-read by reduce_kernel
+  uint32_t phase = 0, dphase = 0;
+  TUnit u = ui < n_units ? units[ui] : TUnit{0, 0, 0, 0};
+  if (ui < n_units) load(u, 0);
+  while (ui < n_units) {
+    const int n_all = u.ent_end - u.ent_begin;
+    const int next = ui + int(gridDim.x);
+    const TUnit un = next < n_units ? units[next] : TUnit{0, 0, 0, 0};
+    for (int t0 = 0; t0 < n_all; t0 += EPT) {
+      const bool last_tile = t0 + EPT >= n_all;
+      const int eid_t = eid;
+      if constexpr (R == 1 || R == 4) {
+#pragma unroll
+        for (int kb = 0; kb < 16; ++kb) put(kb, c[kb]);
+      } else {
+        float mine[32], other[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          mine[2 * i] = rr ? c[i].y : c[i].x;
+          mine[2 * i + 1] = rr ? c[i].w : c[i].z;
+          other[2 * i] = rr ? c[i].x : c[i].y;
+          other[2 * i + 1] = rr ? c[i].z : c[i].w;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
+#pragma unroll
+        for (int kb = 0; kb < 8; ++kb) {
+          const float4 a = make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]);
+          const float4 b = make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]);
+          put(kb, rr ? b : a);
+          put(8 + kb, rr ? a : b);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        if (t0 == 0) {
+          mbar_wait(&bar[0], dphase);
+          dphase ^= 1u;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bh = smem_u32(Bhi), bl = smem_u32(Blo);
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const uint32_t a0 = tmem + (cc == 2 ? 128u : 64u), b0 = cc == 1 ? bl : bh;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            umma_tf32_ts(tmem, a0 + ks * 8, umma_desc_kmajor(b0 + ks * 2 * kTcLBO), (cc | ks) != 0);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar[1]))
+                     : "memory");
+      }
+      // prefetch the next tile's sources (this unit's or the next unit's first)
+      if (!last_tile)
+        load(u, t0 + EPT);
+      else if (next < n_units)
+        load(un, 0);
+      mbar_wait(&bar[1], phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // D consumed: fetch the next unit's D while the epilogue runs
+      if (last_tile && tid == 0 && next < n_units) {
+        mbar_arrive_expect_tx(&bar[0], 2 * kTcBBytes);
+        bulk_g2s(Bhi, DTC + size_t(un.dtab) * (2 * 4096), 2 * kTcBBytes, &bar[0]);
+      }
+      uint32_t r[64];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+          "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+          "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+            "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+            "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]),
+            "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
+            "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+            "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+            "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]),
+            "=r"(r[63])
+          : "r"(t_acc));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (rr == 0) eids[e] = eid_t;
+      const int n = min(EPT, n_all - t0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e0 = h * HALF;
+        if (e >= e0 && e < e0 + HALF && eid_t >= 0)
+#pragma unroll
+          for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
+        __syncthreads();
+        constexpr int NV = QR / 4;
+        const int nh = max(0, min(HALF, n - e0));
+        for (int i = tid; i < nh * NV; i += 128) {
+          const int ee = i / NV, v = i - (i / NV) * NV;
+          const float4 val = *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
+          st16_hint(Y + int64_t(eids[e0 + ee]) * QR + 4 * v, val, keep);
+        }
+        __syncthreads();
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    ui = next;
+    u = un;
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
 template <int R>
 constexpr size_t tc2_smem_bytes() {
   constexpr int HALF = 64 / R, OS = 64 * R + 4;

@@ -350,6 +350,7 @@ struct nesa_plan {
   DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
   bool tc2 = true;                          // ... with the A operand in TMEM (~50 KB smem)
+  int tc3_ctas = 2;                         // ... persistent, this many CTAs per SM (0: one CTA per unit)
   DevBuf<float> DTC;                        // [n_dtab][hi | lo][64 x 64] canonical tf32 D
   DevBuf<TUnit> mom_units;
   DevBuf<TEnt> mom_ents;
@@ -1159,6 +1160,7 @@ void set_smem_attrs() {
     attr(tgemm_wt_kernel<float, R, 128, 80, 64>, lim);
     attr(tgemm_tc_kernel<R>, int(kTcSmem));
     attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
+    attr(tgemm_tc3_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
     attr(reception_exp_kernel<R, true>, lim);
@@ -1362,7 +1364,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const TUnit* up = P->tunits.p + u0;
     if (P->tc) {
       if constexpr (std::is_same<T, float>::value) {
-        if (P->tc2)
+        if (P->tc2 && P->tc3_ctas > 0)
+          launch_pdl(P->pdl && st == s0, tgemm_tc3_kernel<R>,
+                     std::min(u1 - u0, P->tc3_ctas * P->n_sm), 128, tc2_smem_bytes<R>(), st, up, u1 - u0,
+                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+        else if (P->tc2)
           launch_pdl(P->pdl && st == s0, tgemm_tc2_kernel<R>, u1 - u0, 128, tc2_smem_bytes<R>(), st, up,
                      (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
         else
@@ -1861,6 +1867,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* mb = std::getenv("NESA_MOM_BUF")) P->mom_buf = std::max(0, std::atoi(mb));
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
     if (const char* tc2 = std::getenv("NESA_TC2")) P->tc2 = std::atoi(tc2) != 0;
+    if (const char* t3 = std::getenv("NESA_TC3_CTAS")) P->tc3_ctas = std::max(0, std::atoi(t3));
     if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
     if (const char* ns = std::getenv("NESA_NEAR_SPLIT")) P->near_split = std::atoi(ns);
     if (const char* nf = std::getenv("NESA_NEAR_FRAC")) P->near_frac = std::atof(nf);

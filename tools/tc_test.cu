@@ -58,10 +58,14 @@ int run() {
   if (V == 1) {
     CK(cudaFuncSetAttribute(tgemm_tc_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmem)));
     tgemm_tc_kernel<R><<<nunits, 128, kTcSmem>>>(dU, dE, dD, dS, dY);
-  } else {
+  } else if (V == 2) {
     CK(cudaFuncSetAttribute(tgemm_tc2_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(tc2_smem_bytes<R>())));
     tgemm_tc2_kernel<R><<<nunits, 128, tc2_smem_bytes<R>()>>>(dU, dE, dD, dS, dY);
+  } else {
+    CK(cudaFuncSetAttribute(tgemm_tc3_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(tc2_smem_bytes<R>())));
+    tgemm_tc3_kernel<R><<<3, 128, tc2_smem_bytes<R>()>>>(dU, nunits, dE, dD, dS, dY);  // persistent
   }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
@@ -80,7 +84,7 @@ int run() {
           rmax = std::max(rmax, std::fabs(ref));
         }
     }
-  printf("kernel %s R=%d max abs err %.3e (max |ref| %.3e, rel %.3e)\n", V == 1 ? "tc (A in smem)" : "tc2 (A in TMEM)", R, emax, rmax, emax / rmax);
+  printf("kernel %s R=%d max abs err %.3e (max |ref| %.3e, rel %.3e)\n", V == 1 ? "tc (A in smem)" : (V == 2 ? "tc2 (A in TMEM)" : "tc3 (persistent)"), R, emax, rmax, emax / rmax);
   return emax / rmax < 1e-5 ? 0 : 2;
 }
 
@@ -92,6 +96,9 @@ int main() {
   rc |= run<2, 2>();
   rc |= run<1, 2>();
   rc |= run<4, 2>();
+  rc |= run<2, 3>();
+  rc |= run<1, 3>();
+  rc |= run<4, 3>();
   printf(rc ? "FAIL\n" : "PASS\n");
   return rc;
 }
