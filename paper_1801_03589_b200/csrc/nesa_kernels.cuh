@@ -544,7 +544,7 @@ __device__ __forceinline__ void tile_reduce(const FarGeom& G, const TileMap& m, 
 // fastmvp.py:163-169 (translations first, then potential transfer).
 // Matrices arrive by bulk copy; amplitudes by cp.async or summed in staging.
 // ----------------------------------------------------------------------------
-enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2, kLvlDownRecv = 3 };
+enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2, kLvlDownRecv = 3, kLvlDownBeta = 4 };
 
 // kLvlDownRecv (leaf level, float32 expansion plans): the leaf-level
 // downward transfer, the reception coefficients and the reception itself in
@@ -559,6 +559,7 @@ struct RecvArgs {
   const int64_t* perm;      // tree row -> original row
   float* phi;               // output, original order, rows of stride ldp
   int ldp, nt;
+  float* beta;              // kLvlDownBeta: [NL][64][R] reception coefficients out
 };
 
 template <typename T>
@@ -1987,9 +1988,9 @@ struct LVW {
   // most 3) boundary tiles of a level need a second round; one slot keeps the
   // kernel small enough to run 2-3 CTAs per SM beside the near field
   static constexpr int kSlots = LVW_SLOTS;
-  static constexpr bool kDown = MODE == 2 || MODE == 3;
+  static constexpr bool kDown = MODE == 2 || MODE == 3 || MODE == 4;
   static constexpr int kXBufs = kDown ? 2 : 1;      // the downward modes also stage o[c]
-  static constexpr int kEMat = MODE == 3 ? 1 : 0;   // kLvlDownRecv: the E^ matrix
+  static constexpr int kEMat = MODE >= 3 ? 1 : 0;   // kLvlDownRecv / Beta: the E^ matrix
   static constexpr size_t SMEM = (kSlots + kEMat) * W::MB + kXBufs * W::XB + 3 * 64;
 };
 
@@ -2069,10 +2070,10 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
     }
   } else {
     if (warp == 0) {
-      const uint32_t nb = (kDown ? 2u : 1u) * kVB * uint32_t(n) + (MODE == kLvlDownRecv ? uint32_t(W::MB) : 0u);
+      const uint32_t nb = (kDown ? 2u : 1u) * kVB * uint32_t(n) + (LV::kEMat ? uint32_t(W::MB) : 0u);
       if (lane == 0) {
         mbar_arrive_expect_tx(&bar[1], nb);
-        if constexpr (MODE == kLvlDownRecv)
+        if constexpr (LV::kEMat)
           if constexpr (sizeof(T) == 4) bulk_g2s(Em, rv.ET, uint32_t(W::MB), &bar[1]);
       }
       __syncwarp();
@@ -2168,7 +2169,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
     }
   }
   __syncthreads();
-  if constexpr (MODE == kLvlDownRecv) {
+  if constexpr (MODE == kLvlDownRecv || MODE == kLvlDownBeta) {
     if constexpr (sizeof(T) == 4 && QT == 64) {
       // ---- reception coefficients of the tile's leaves: beta^ = E^ o (same
       // warp tiling; E^ is one matrix for every column), into the Oc buffer
@@ -2203,6 +2204,17 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
         }
       }
       __syncthreads();
+      if constexpr (MODE == kLvlDownBeta) {
+        // beta^ rows of the tile's leaves -> global, coalesced
+        constexpr int V = 4;
+        constexpr int NV = W::QR / V;
+        for (int i = tid; i < n * NV; i += 128) {
+          const int p = i / NV, v = i - p * NV;
+          *reinterpret_cast<float4*>(rv.beta + int64_t(a.order[t0 + p]) * W::QR + v * V) =
+              *reinterpret_cast<const float4*>(Oc + p * W::XS + v * V);
+        }
+        return;
+      }
       // ---- reception of the tile's leaves: warp w takes leaves w, w+4, ...;
       // lane = point; phi[perm] = phin + beta_0 + Re sum_m beta_m w^m
       for (int p = warp; p < n; p += 4) {

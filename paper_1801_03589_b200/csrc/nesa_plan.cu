@@ -362,6 +362,7 @@ struct nesa_plan {
   int n_rad_units = 0;
   bool beta_tc = false;                     // reception coefficients by tgemm_tc (E^ o)
   bool recv_fused = false;                  // leaf down + beta + reception in one kernel
+  bool beta_fused = false;                  // leaf down + beta in one kernel (reception separate)
   DevBuf<float> ET;                         // [64][64] E^ transposed for the warp-tiled GEMM
   DevBuf<float> ETC;                        // [hi | lo][64 x 64] canonical tf32 E^
   DevBuf<unsigned char> beta;               // [NL][64][R] reception coefficients
@@ -993,7 +994,10 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       // (measured slower at C4, 641 vs 627 us: 8 warps per SM cannot hide the
       // point loads the separate 48-warp reception kernel hides; opt in with
       // NESA_RECV_FUSED=1)
-      if (Q == 64 && leaf_wide && 2 * P->u_nt + 1 <= 64 && rf && std::atoi(rf) != 0) {
+      const char* bf = std::getenv("NESA_BETA_FUSED");
+      const bool want_recv = rf && std::atoi(rf) != 0;
+      const bool want_beta = !want_recv && P->beta_tc && !(bf && std::atoi(bf) == 0);
+      if (Q == 64 && leaf_wide && 2 * P->u_nt + 1 <= 64 && (want_recv || want_beta)) {
         std::vector<float> et(64 * 64, 0.f);
         for (int row = 0; row < 64; ++row)
           for (int k = 0; k < 64; ++k) {
@@ -1005,7 +1009,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
             et[size_t(k) * 64 + row] = x;
           }
         P->ET.upload(et);
-        P->recv_fused = true;
+        P->recv_fused = want_recv;
+        P->beta_fused = want_beta;
       }
     }
     if (P->mom_kt || P->beta_tc) {
@@ -1144,6 +1149,7 @@ void set_smem_attrs() {
   attr(level_wt_kernel<T, R, 64, kLvlUpSum>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDown>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDownRecv>, lim);
+  attr(level_wt_kernel<T, R, 64, kLvlDownBeta>, lim);
   attr(level_kernel<T, R, kLvlUpLeaf>, lim);
   attr(level_kernel<T, R, kLvlUpSum>, lim);
   attr(level_kernel<T, R, kLvlDown>, lim);
@@ -1251,9 +1257,12 @@ int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const 
   const size_t nb = ((size_t(nt) + 1) * R + 1) & ~size_t(1);
   const size_t sm = size_t(kExpWarps) * (nb + ((size_t(Q) * R + 3) & ~size_t(3)) / 2) * sizeof(float2);
   if (P->beta_tc) {
-    // beta^ = E^ o for every leaf on the tensor cores, then the per-point series
+    // beta^ = E^ o for every leaf on the tensor cores (or already by the fused
+    // leaf-level kernel), then the per-point series
     float* beta = reinterpret_cast<float*>(P->beta.p);
-    if (P->tc2)
+    if (P->beta_fused)
+      ;
+    else if (P->tc2)
       tgemm_tc2_kernel<R><<<P->n_mom_units, 128, tc2_smem_bytes<R>(), st>>>(P->mom_units.p, P->mom_ents.p,
                                                                            P->ETC.p, o, beta);
     else
@@ -1262,7 +1271,7 @@ int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const 
     reception_exp_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
         P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
         P->leaf_begin, nleaf, Q, nt, ldp);
-    return 2;
+    return P->beta_fused ? 1 : 2;
   }
   reception_exp_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
       P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, o, phin, perm, phi,
@@ -1412,7 +1421,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-      if (lv == P->L && P->recv_fused && far_recv) {
+      if (lv == P->L && P->beta_fused && far_recv) {
+        // leaf level + reception coefficients beta^ = E^ o in one kernel
+        if constexpr (std::is_same<T, float>::value) {
+          RecvArgs rv{};
+          rv.ET = P->ET.p;
+          rv.beta = reinterpret_cast<float*>(P->beta.p);
+          launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDownBeta>, gw, 128,
+                     LVW<T, R, 64, kLvlDownBeta>::SMEM, s0, la, rv);
+        }
+      } else if (lv == P->L && P->recv_fused && far_recv) {
         // leaf level + reception coefficients + reception in one kernel: the
         // near field must be complete (phin)
         join_near();

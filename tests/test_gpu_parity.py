@@ -348,7 +348,7 @@ def test_pipeline_matches_sync_calls(golden):
 
 
 @pytest.mark.parametrize("env", [{"NESA_TC": "0"}, {"NESA_TC": "1"}, {"NESA_TC2": "0"}, {"NESA_TC3_CTAS": "0"}, {"NESA_MOM_INKERNEL": "1"},
-                                 {"NESA_RECV_INKERNEL": "1"}, {"NESA_RECV_FUSED": "1"}, {"NESA_FUSED": "0", "NESA_SPLIT": "0"},
+                                 {"NESA_RECV_INKERNEL": "1"}, {"NESA_RECV_FUSED": "1"}, {"NESA_BETA_FUSED": "0"}, {"NESA_FUSED": "0", "NESA_SPLIT": "0"},
                                  {"NESA_NEAR_AFTER": "1", "NESA_MOM_BUF": "0"}, {"NESA_RAD_UP": "1"}])
 def test_q64_f32_path_variants(monkeypatch, env):
     # every float32 Q = 64 code path (FFMA / tensor-core translation, in-kernel
