@@ -141,6 +141,13 @@ struct BlockGemvArgs {
   const T* base;                 // scatter: added per tree row (may be null)
   const int64_t* perm;           // scatter: tree row -> original row
   int ldy;                       // scatter: row stride of y (elements)
+  // dynamic mode (wq != null): CTAs claim units [cta_chunk_ptr[u], [u+1])
+  // from the queue wq[0] (wq[1] counts exited CTAs; the last one resets
+  // both); CTAs resident on SMs with %smid < sm_skip exit at once, leaving
+  // those SMs to the concurrent far-field chain
+  int* wq;
+  int n_units;
+  int sm_skip;
 };
 
 struct StageHdr {
@@ -150,9 +157,11 @@ struct StageHdr {
 };
 
 // Per-stage shared memory: [A | X | header | (scatter) perm | base]
-template <typename T, int R, int MODE, int NST = kStages>
+template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB = kABytes>
 struct BGLayout {
-  static constexpr size_t kA = kABytes;
+  static constexpr int kNCT = NCW * 32;
+  static constexpr int kMaxC = AB / 64;  // columns per chunk
+  static constexpr size_t kA = AB;
   static constexpr size_t kX = size_t(kMaxC) * R * sizeof(T);
   static constexpr size_t kFinPerm = MODE == kModeScatter ? size_t(kMaxRows) * 8 : 0;
   static constexpr size_t kFinBase = MODE == kModeScatter ? size_t(kMaxRows) * R * sizeof(T) : 0;
@@ -171,9 +180,9 @@ struct BGLayout {
   static constexpr size_t offBase = offPerm + kFinPerm;
 };
 
-template <typename T, int R, int MODE, int NST = kStages>
+template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB = kABytes>
 constexpr size_t blockgemv_smem_bytes() {
-  return BGLayout<T, R, MODE, NST>::kBytes;
+  return BGLayout<T, R, MODE, NST, NCW, AB>::kBytes;
 }
 
 template <typename T, int R>
@@ -201,10 +210,30 @@ __device__ __forceinline__ void ldx(const T* p, T v[R]) {
   }
 }
 
-template <typename T, int R, int MODE, int NST = kStages>
-__global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel(const BlockGemvArgs<T> a) {
+__device__ __forceinline__ uint32_t smid_u32() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+// one exited CTA of a dynamic launch; the last one resets the queue for the
+// next launch (launches of one plan are stream-ordered)
+__device__ __forceinline__ void bg_exit_count(int* wq) {
+  __threadfence();
+  if (atomicAdd(wq + 1, 1) == int(gridDim.x) - 1) {
+    wq[0] = 0;
+    wq[1] = 0;
+    __threadfence();
+  }
+}
+
+template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB = kABytes>
+__global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
+    blockgemv_kernel(const BlockGemvArgs<T> a) {
   KtScope kt_(10 + MODE);
-  using Lay = BGLayout<T, R, MODE, NST>;
+  using Lay = BGLayout<T, R, MODE, NST, NCW, AB>;
+  constexpr int kNCW = NCW;
+  constexpr int kNCT = NCW * 32;
+  constexpr int kABytes = AB;
   constexpr int kStages = NST;
   extern __shared__ __align__(128) unsigned char smem[];
   T* const sRedOwn = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
@@ -212,8 +241,13 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
       (reinterpret_cast<uintptr_t>(smem + kStages * Lay::kStage + Lay::kRed) + 15) & ~uintptr_t(15));
   uint64_t* empty = full + kStages;
 
-  const int c0 = a.cta_chunk_ptr[blockIdx.x];
-  const int c1 = a.cta_chunk_ptr[blockIdx.x + 1];
+  const bool dyn = a.wq != nullptr;
+  if (dyn && int(smid_u32()) < a.sm_skip) {
+    if (threadIdx.x == 0) bg_exit_count(a.wq);
+    return;
+  }
+  const int c0 = dyn ? 0 : a.cta_chunk_ptr[blockIdx.x];
+  const int c1 = dyn ? 0 : a.cta_chunk_ptr[blockIdx.x + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -229,12 +263,36 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
     // ------------------------------ producer ------------------------------
     const int32_t* recw = reinterpret_cast<const int32_t*>(a.recs);
     const uint64_t pol = l2_evict_first_policy();
-    int32_t w_next = c0 < c1 ? __ldg(recw + int64_t(c0) * 32 + lane) : 0;
-    for (int i = c0; i < c1; ++i) {
+    // static: one range [c0, c1); dynamic: claimed units, one claim ahead
+    int u_cur = 0, u_next = 0, i0 = c0, i1 = c1;
+    if (dyn) {
+      u_cur = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(a.wq, 1) : 0, 0);
+      u_next = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(a.wq, 1) : 0, 0);
+      if (u_cur < a.n_units) {
+        i0 = __ldg(a.cta_chunk_ptr + u_cur);
+        i1 = __ldg(a.cta_chunk_ptr + u_cur + 1);
+      }
+    }
+    int k = 0;
+    int32_t w_next = i0 < i1 ? __ldg(recw + int64_t(i0) * 32 + lane) : 0;
+    for (;;) {
+      if (dyn && i0 >= i1) {
+        // unit done: move to the claimed one, claim the next
+        if (u_cur >= a.n_units || u_next >= a.n_units) break;
+        u_cur = u_next;
+        u_next = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(a.wq, 1) : 0, 0);
+        i0 = __ldg(a.cta_chunk_ptr + u_cur);
+        i1 = __ldg(a.cta_chunk_ptr + u_cur + 1);
+        if (i0 >= i1) continue;
+        w_next = __ldg(recw + int64_t(i0) * 32 + lane);
+      }
+      if (i0 >= i1) break;
+      const int i = i0++;
       const int32_t w = w_next;
-      if (i + 1 < c1) w_next = __ldg(recw + int64_t(i + 1) * 32 + lane);
-      const int k = i - c0, st = k % kStages;
+      if (i + 1 < i1) w_next = __ldg(recw + int64_t(i + 1) * 32 + lane);
+      const int st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
+      ++k;
       unsigned char* stg = smem + size_t(st) * Lay::kStage;
       const uint32_t lo = uint32_t(__shfl_sync(0xffffffffu, w, 0));
       const uint32_t hi = uint32_t(__shfl_sync(0xffffffffu, w, 1));
@@ -281,6 +339,18 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
       }
       cp_async_mbar_arrive_noinc(&full[st]);
     }
+    if (dyn) {
+      // end marker for the consumers
+      const int st = k % kStages;
+      const uint32_t round = uint32_t(k / kStages);
+      unsigned char* stg = smem + size_t(st) * Lay::kStage;
+      mbar_wait(&empty[st], (round & 1u) ^ 1u);
+      if (lane == 0) {
+        reinterpret_cast<StageHdr*>(stg + Lay::offHdr)->flags = 4;
+        mbar_arrive_expect_tx(&full[st], 0);
+      }
+      cp_async_mbar_arrive_noinc(&full[st]);
+    }
   } else {
     // ------------------------------ consumers -----------------------------
     // Thread (rq, cl): rows 4rq..4rq+3 of the item, columns cl, cl+CL, ...;
@@ -292,12 +362,13 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) acc[i][rr] = T(0);
-    for (int i = c0; i < c1; ++i) {
-      const int k = i - c0, st = k % kStages;
+    for (int k = 0; dyn || k < c1 - c0; ++k) {
+      const int st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
       const unsigned char* stg = smem + size_t(st) * Lay::kStage;
       mbar_wait(&full[st], round & 1u);
       const StageHdr h = *reinterpret_cast<const StageHdr*>(stg + Lay::offHdr);
+      if (dyn && (h.flags & 4)) break;
       const int m = h.m, nc = h.ncols, ld = h.ld, CL = h.CL;
       const int RQ = ld >> 2;
       const int cl = RQ == 1 ? tid : int(__umulhi(uint32_t(tid), h.magic));
@@ -365,6 +436,10 @@ __global__ void __launch_bounds__(kBGThreads, NST <= 3 ? 2 : 1) blockgemv_kernel
         if (lane == 0) mbar_arrive(&empty[st]);
       }
     }
+  }
+  if (dyn) {
+    __syncthreads();
+    if (threadIdx.x == 0) bg_exit_count(a.wq);
   }
 }
 

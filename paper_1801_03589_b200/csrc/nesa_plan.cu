@@ -107,20 +107,31 @@ struct DevBlockSet {
   DevBuf<int32_t> cta_ptr;
   int grid = 0;
   int64_t n_items = 0;
+  // dynamic launch (n_units > 0): cta_ptr holds n_units claimable ranges,
+  // launch_grid CTAs claim them from wq; CTAs on SMs < sm_skip exit at once
+  DevBuf<int> wq;
+  int n_units = 0;
+  int launch_grid = 0;
+  int sm_skip = 0;
+  size_t smem = 0;  // dynamic shared memory per CTA (0: the layout's own)
+  int ncw = kNCW;    // consumer warps of the block-GEMV launch (store mode: 8 or 4)
+  int ab = kABytes;  // bytes per ring stage (16 or 32 KB)
+  int nst = kStages; // ring stages
   int64_t entries = 0;
 };
 
 // Split items into bulk-copy chunks and give each CTA a contiguous,
 // byte-balanced range of whole items (a target row is never split across
 // CTAs, so it has exactly one writer).
-void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
+void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid, int ab = kABytes,
+                       int nct = kNCT) {
   hs.recs.clear();
   std::vector<int64_t> item_first_chunk(hs.items.size() + 1);
   std::vector<double> item_bytes(hs.items.size());
   for (size_t i = 0; i < hs.items.size(); ++i) {
     const BlockItem& it = hs.items[i];
     item_first_chunk[i] = int64_t(hs.recs.size());
-    int per = int(std::min<int64_t>(kMaxC, kABytes / (int64_t(it.ld) * int64_t(elem_bytes))));
+    int per = int(std::min<int64_t>(ab / 64, ab / (int64_t(it.ld) * int64_t(elem_bytes))));
     per = std::max(per, 1);
     const int RQ = it.ld / 4;
     const int seg_end = it.seg_begin + it.seg_count;
@@ -132,7 +143,7 @@ void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid) {
       r.ld = it.ld;
       r.y_row0 = it.y_row0;
       r.magic = RQ == 1 ? 0u : uint32_t(((uint64_t(1) << 32) + RQ - 1) / RQ);
-      r.CL = kNCT / RQ;
+      r.CL = nct / RQ;
       int ce = std::min(it.n, c + per);
       // segments overlapping [c, ce); cut the chunk if more than kRecSegs
       int ns = 0;
@@ -328,6 +339,10 @@ struct nesa_plan {
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
   int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
   int near_waves = 1;                       // near-field grid = waves x resident CTAs
+  int near_units = 0;                       // >0: dynamic near launch over this many ranges
+  int near_sm_skip = 0;                     // dynamic: SMs [0, skip) left to the far chain
+  size_t near_smem = 0;                     // dynamic: shared memory per near CTA (padding)
+  int near_ncw = 4, near_ab = 24576, near_nst = 2;  // near-field kernel variant (NESA_BG_VARIANTS)
   bool priority = true;                     // far-field stream scheduled first
   bool split = true;                        // fine-level translation on a side stream
   int near_after = -1;                      // where the near branch forks (see enqueue_T)
@@ -791,11 +806,22 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   {
     int ng = P->near_waves * P->near_ctas * P->n_sm;
     if (const char* e = std::getenv("NESA_NEAR_GRID")) ng = std::max(1, std::atoi(e));
-    chunk_and_balance(hn, es, ng);
+    if (P->near_units > 0) ng = P->near_units;
+    chunk_and_balance(hn, es, ng, P->near_ab, P->near_ncw * 32);
   }
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
+  P->nearset.ncw = P->near_ncw;
+  P->nearset.ab = P->near_ab;
+  P->nearset.nst = P->near_nst;
+  if (P->near_units > 0 && P->near_ctas == 2) {
+    P->nearset.n_units = P->nearset.grid;
+    P->nearset.launch_grid = kBGPerSM * P->n_sm;
+    P->nearset.sm_skip = P->near_sm_skip;
+    P->nearset.smem = P->near_smem;
+    P->nearset.wq.alloc(2);
+  }
   if (!P->v_mom) upload_blockset<T>(P->Vset, hv);
   upload_blockset<T>(P->Uset, hu);
 
@@ -1112,16 +1138,52 @@ inline int grid_for(int64_t n, int threads, int cap) {
   return int(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap)));
 }
 
-template <typename T, int R, int MODE, int NST = kStages>
-void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
+template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB = kABytes>
+void launch_blockgemv_v(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
                       int64_t perm_offset, cudaStream_t st, int cta0 = 0, int ncta = -1) {
   if (bs.n_items == 0) return;
   if (ncta < 0) ncta = bs.grid - cta0;
   if (ncta <= 0) return;
   BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p + cta0, x, y,
-                     base, perm, int(perm_offset)};
-  constexpr size_t sm = blockgemv_smem_bytes<T, R, MODE, NST>();
-  blockgemv_kernel<T, R, MODE, NST><<<ncta, kBGThreads, sm, st>>>(a);
+                     base, perm, int(perm_offset), nullptr, 0, 0};
+  size_t sm = blockgemv_smem_bytes<T, R, MODE, NST, NCW, AB>();
+  if (bs.n_units > 0 && cta0 == 0 && ncta == bs.grid) {
+    a.wq = bs.wq.p;
+    a.n_units = bs.n_units;
+    a.sm_skip = bs.sm_skip;
+    ncta = bs.launch_grid;
+    sm = std::max(sm, bs.smem);
+  }
+  blockgemv_kernel<T, R, MODE, NST, NCW, AB><<<ncta, NCW * 32 + 32, sm, st>>>(a);
+}
+
+// near-field variants (store mode): (consumer warps, stage bytes, stages)
+// (measured in the full C4 product: 4 warps x 24 KB x 2 stages 555 us, 4 x 16 KB x 3 556,
+// 4 x 32 KB x 2 580, 8 x 16 KB x 3 (the generic default) 633; fewer consumer threads and
+// larger stages amortise the per-chunk consumer overhead that bounds an SM's share)
+#define NESA_BG_VARIANTS(X) X(4, 24576, 2) X(4, 16384, 3) X(4, 32768, 2) X(8, 32768, 2)
+
+bool bg_variant_known(int w, int b, int n) {
+  bool known = w == kNCW && b == kABytes && n == kStages;
+#define NESA_BG_KNOWN(W, B, S) known = known || (w == W && b == B && n == S);
+  NESA_BG_VARIANTS(NESA_BG_KNOWN)
+#undef NESA_BG_KNOWN
+  return known;
+}
+
+template <typename T, int R, int MODE, int NST = kStages>
+void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
+                      int64_t perm_offset, cudaStream_t st, int cta0 = 0, int ncta = -1) {
+  if constexpr (MODE == kModeStore && NST == kStages) {
+#define NESA_BG_CASE(W, B, S)                                                                      \
+  if (bs.ncw == W && bs.ab == B && bs.nst == S) {                                                  \
+    launch_blockgemv_v<T, R, MODE, S, W, B>(bs, x, y, base, perm, perm_offset, st, cta0, ncta); \
+    return;                                                                                        \
+  }
+    NESA_BG_VARIANTS(NESA_BG_CASE)
+#undef NESA_BG_CASE
+  }
+  launch_blockgemv_v<T, R, MODE, NST>(bs, x, y, base, perm, perm_offset, st, cta0, ncta);
 }
 
 template <typename T, int R>
@@ -1138,7 +1200,10 @@ void set_smem_attrs() {
     if (carve >= 0)
       CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
   };
-  attr(blockgemv_kernel<T, R, kModeStore>, int(blockgemv_smem_bytes<T, R, kModeStore>()));
+  attr(blockgemv_kernel<T, R, kModeStore>, 113 * 1024);
+#define NESA_BG_ATTR(W, B, S) attr(blockgemv_kernel<T, R, kModeStore, S, W, B>, 113 * 1024);
+  NESA_BG_VARIANTS(NESA_BG_ATTR)
+#undef NESA_BG_ATTR
   attr(blockgemv_kernel<T, R, kModeScatter>, int(blockgemv_smem_bytes<T, R, kModeScatter>()));
   attr(blockgemv_kernel<T, R, kModeStore, 6>, int(blockgemv_smem_bytes<T, R, kModeStore, 6>()));
   const int lim = 220 * 1024;
@@ -1876,6 +1941,24 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
     if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
+    if (const char* e = std::getenv("NESA_NEAR_UNITS")) P->near_units = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("NESA_NEAR_SKIP")) P->near_sm_skip = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("NESA_NEAR_SMEM")) P->near_smem = size_t(std::max(0, std::atoi(e)));
+    if (const char* e = std::getenv("NESA_NEAR_VARIANT")) {  // "warps,stage_bytes,stages"
+      int w = kNCW;
+      int b = kABytes;
+      int n = kStages;
+      if (std::sscanf(e, "%d,%d,%d", &w, &b, &n) == 3 && bg_variant_known(w, b, n)) {
+        P->near_ncw = w;
+        P->near_ab = b;
+        P->near_nst = n;
+      }
+    }
+    if (P->near_ctas == 1) {  // the one-CTA-per-SM 6-stage ring uses the generic geometry
+      P->near_ncw = kNCW;
+      P->near_ab = kABytes;
+      P->near_nst = kStages;
+    }
     if (const char* lp = std::getenv("NESA_L2_PERSIST")) {
       int maxp = 0;
       CUDA_OK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
