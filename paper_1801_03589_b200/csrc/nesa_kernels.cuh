@@ -389,9 +389,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
           ld4(Ap + c * ld, a4);
           ldx<T, R>(X + c * R, xv);
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) acc[q][rr] = fma(a4[q], xv[rr], acc[q][rr]);
+          for (int q = 0; q < 4; ++q) fma_row<T, R>(acc[q], a4[q], xv);
         }
       }
 
@@ -1237,14 +1235,7 @@ __global__ void __launch_bounds__(kTGThreads) tgemm_kernel(const TUnit* __restri
         ld4(mp + j * G.Qp + 4, m1);
 #pragma unroll
         for (int c = 0; c < 4; ++c) x[c] = xq[c][j * R];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            acc[r][c] = fma(m0[r], x[c], acc[r][c]);
-            acc[r + 4][c] = fma(m1[r], x[c], acc[r + 4][c]);
-          }
-        }
+        tile_fma8x4<T>(acc, m0, m1, x);
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -1366,13 +1357,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
         ld4(mp + j * QT + 4, m1);
 #pragma unroll
         for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            acc[r][c] = fma(m0[r], x[c], acc[r][c]);
-            acc[r + 4][c] = fma(m1[r], x[c], acc[r + 4][c]);
-          }
+        tile_fma8x4<T>(acc, m0, m1, x);
       }
     }
     // stage the tile entry-major in the consumed X buffer, then write each
@@ -2212,13 +2197,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
           ld4(mp + j * QT + 4, m1);
 #pragma unroll
           for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              part[r][c] = fma(m0[r], x[c], part[r][c]);
-              part[r + 4][c] = fma(m1[r], x[c], part[r + 4][c]);
-            }
+          tile_fma8x4<T>(part, m0, m1, x);
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -2263,13 +2242,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
           ld4(mp + j * QT + 4, m1);
 #pragma unroll
           for (int i = 0; i < NE; ++i) ldx<T, R>(xp + i * 8 * W::XS + j * R, x + i * R);
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-              part[r][c] = fma(m0[r], x[c], part[r][c]);
-              part[r + 4][c] = fma(m1[r], x[c], part[r + 4][c]);
-            }
+          tile_fma8x4<T>(part, m0, m1, x);
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -2486,6 +2459,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
           for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(b + j) * R + rr];
         }
         const float2 w = make_float2(p.x * inv, p.y * inv);
+        const float2 W1 = w, W2 = make_float2(-w.y, w.x);
         float2 z = make_float2(1.f, 0.f);
         if (m0) {
           const float2 wp = cpow_const<MP>(w);
@@ -2495,11 +2469,9 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
 #pragma unroll
         for (int mm = 0; mm < MP; ++mm) {
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) {
-            v[(mm * R + rr) * 2] = fmaf(z.x, qv[rr], v[(mm * R + rr) * 2]);
-            v[(mm * R + rr) * 2 + 1] = fmaf(z.y, qv[rr], v[(mm * R + rr) * 2 + 1]);
-          }
-          z = cmulf(z, w);
+          for (int rr = 0; rr < R; ++rr)
+            ffma2(v[(mm * R + rr) * 2], v[(mm * R + rr) * 2 + 1], qv[rr], z.x, z.y);
+          z = cmul_pk(z, W1, W2);
         }
       }
       // transpose reduction over the 4 lanes of the group: lane g ends with
@@ -2702,6 +2674,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
     const float inv = 1.f / r;
     auto eval = [&](float2 p, int64_t dst, const float* base) {
       const float2 w = make_float2(p.x * inv, p.y * inv);
+      const float2 W1 = w, W2 = make_float2(-w.y, w.x);
       float2 z = w;
       float acc[R];
 #pragma unroll
@@ -2719,7 +2692,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
         }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(bt[rr].x, z.x, fmaf(-bt[rr].y, z.y, acc[rr]));
-        z = cmulf(z, w);
+        z = cmul_pk(z, W1, W2);
       }
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) phi[dst * ldp + rr] = base[rr] + acc[rr];

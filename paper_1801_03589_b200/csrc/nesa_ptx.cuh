@@ -176,4 +176,79 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Paired FP32 FMA (Blackwell FFMA2): (c.x, c.y) += a * (x.x, x.y), each lane
+// rounded exactly like fmaf, so results are bitwise those of two FFMAs.
+__device__ __forceinline__ void ffma2(float& c0, float& c1, float a, float x0, float x1) {
+  unsigned long long c, x, aa;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "f"(c0), "f"(c1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(aa) : "f"(a));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(aa), "l"(x));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
+}
+// elementwise a * b + c and a * b on float2 pairs (FFMA2 / FMUL2)
+__device__ __forceinline__ float2 ffma2v(float2 a, float2 b, float2 c) {
+  unsigned long long pa, pb, pc;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(pc) : "l"(pa), "l"(pb));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(pc));
+  return r;
+}
+__device__ __forceinline__ float2 fmul2v(float2 a, float2 b) {
+  unsigned long long pa, pb, pc;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pb) : "f"(b.x), "f"(b.y));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(pc) : "l"(pa), "l"(pb));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(pc));
+  return r;
+}
+// complex z * w with the loop-invariant pairs W1 = (w.x, w.y), W2 = (-w.y, w.x):
+// z.x W1 + z.y W2 (one FMUL2 + one FFMA2)
+__device__ __forceinline__ float2 cmul_pk(float2 z, float2 W1, float2 W2) {
+  return ffma2v(make_float2(z.y, z.y), W2, fmul2v(make_float2(z.x, z.x), W1));
+}
+
+// 8 x 4 register tile: acc[r][c] += m[r] x[c] (float: column pairs share one FFMA2)
+template <typename T>
+__device__ __forceinline__ void tile_fma8x4(T (&acc)[8][4], const T (&m0)[4], const T (&m1)[4],
+                                            const T (&x)[4]) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int c = 0; c < 4; c += 2)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        ffma2(reinterpret_cast<float&>(acc[r][c]), reinterpret_cast<float&>(acc[r][c + 1]), float(m0[r]),
+              float(x[c]), float(x[c + 1]));
+        ffma2(reinterpret_cast<float&>(acc[r + 4][c]), reinterpret_cast<float&>(acc[r + 4][c + 1]),
+              float(m1[r]), float(x[c]), float(x[c + 1]));
+      }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        acc[r][c] = fma(m0[r], x[c], acc[r][c]);
+        acc[r + 4][c] = fma(m1[r], x[c], acc[r + 4][c]);
+      }
+  }
+}
+
+// acc[rr] += a * x[rr] for rr < R (float: paired FMAs; double: scalar)
+template <typename T, int R>
+__device__ __forceinline__ void fma_row(T (&acc)[R], T a, const T (&x)[R]) {
+  if constexpr (sizeof(T) == 4 && R % 2 == 0) {
+#pragma unroll
+    for (int rr = 0; rr < R; rr += 2)
+      ffma2(reinterpret_cast<float&>(acc[rr]), reinterpret_cast<float&>(acc[rr + 1]), float(a),
+            float(x[rr]), float(x[rr + 1]));
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) acc[rr] = fma(a, x[rr], acc[rr]);
+  }
+}
+
 }  // namespace nesa
