@@ -64,7 +64,7 @@ def parse_args(argv=None):
     ap.add_argument("--n", type=int, default=N_POINTS, help="points (default 2M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--pipe-slots", type=int, default=2,
+    ap.add_argument("--pipe-slots", type=int, default=1,
                     help="compute slots of the pipelined e2e API (independent plans)")
     return ap.parse_args(argv)
 

@@ -345,7 +345,8 @@ struct nesa_plan {
   int near_ncw = 4, near_ab = 24576, near_nst = 2;  // near-field kernel variant (NESA_BG_VARIANTS)
   bool priority = true;                     // far-field stream scheduled first
   bool split = true;                        // fine-level translation on a side stream
-  int near_after = -1;                      // where the near branch forks (see enqueue_T)
+  int near_after = 0;                       // where the near branch forks (see enqueue_T;
+                                            // 0: after the radiation, measured best at C4)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
   bool recv_far = false;                    // reception in the far branch (u_mf only)
   bool pdl = true;                          // programmatic dependent launch in the far chain
@@ -908,8 +909,11 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
       }
       P->mom_A.upload(A);
+      // default: A^ applied inside the moment kernel (MU_OUT = false; measured 531 vs
+      // 545 us at C4 with FFMA2: one launch less on the critical path);
+      // NESA_MOM_INKERNEL=0 selects the separate 64 x 80 moment-map GEMM
       const char* mi = std::getenv("NESA_MOM_INKERNEL");
-      if (Q == 64 && !(mi && std::atoi(mi) != 0)) {
+      if (Q == 64 && mi && std::atoi(mi) == 0) {
         const int need = 2 * P->v_nm - 1;
         P->mom_kt = need <= 80 ? 80 : (need <= 127 ? 128 : 0);  // nm <= 64 (16 per lane)
       }
