@@ -2028,6 +2028,225 @@ constexpr size_t tc2_smem_bytes() {
   return 2 * size_t(kTcBBytes) + size_t((HALF * OS + 3) & ~3) * 4 + 64 + 4 * 128 + 256;
 }
 
+// ----------------------------------------------------------------------------
+// Target-major translation on the tensor cores (float32, Q = 64):
+//   o_t = sum_j D_j s_src(t, j)      (operators.py:225-239; fastmvp.py:163-166)
+// for a unit of <= 128 targets of one level that share one interaction
+// pattern (the sorted list of their D matrices).  An M = 128 tile holds 128/R
+// targets (row = (target, component)); the K-loop runs over the pattern's
+// D matrices, every step one tf32x3 product (3 x 8 tcgen05.mma, A = the
+// tile's sources in TMEM, B = D in shared memory) accumulated in TMEM, so the
+// per-target sum happens on the tensor core and o is written once: no
+// per-entry partials Y, no reduce pass.  D matrices are double-buffered and
+// fetched one step ahead (bulk copies); the next step's sources load while
+// the tensor core runs.  Summation order = pattern order: deterministic.
+// ----------------------------------------------------------------------------
+struct PUnit {
+  int32_t tgt_begin;  // into ptgt
+  int32_t n_tgt;      // <= 128
+  int32_t off_begin;  // into pdid: the pattern's D indices (K-loop order)
+  int32_t n_off;      // >= 1 (targets without entries use the zero matrix)
+  int32_t src_begin;  // into psrc: [j][t], n_off x n_tgt source groups
+  int32_t pad[3];
+};
+
+template <int R>
+constexpr size_t pat_smem_bytes() {
+  constexpr int HALF = 64 / R, OS = 64 * R + 4;
+  return 4 * size_t(kTcBBytes) + size_t((HALF * OS + 3) & ~3) * 4 + 64 + 4 * 128 + 256;
+}
+
+template <int R>
+__global__ void __launch_bounds__(128) tgemm_pat_kernel(const PUnit* __restrict__ units, int n_units,
+                                                        const int32_t* __restrict__ ptgt,
+                                                        const int32_t* __restrict__ pdid,
+                                                        const int32_t* __restrict__ psrc,
+                                                        const float* __restrict__ DTC,
+                                                        const float* __restrict__ s, float* o) {
+  KtScope kt_(45);
+  constexpr int QT = 64, QR = QT * R;
+  constexpr int EPT = 128 / R;   // targets per M = 128 tile
+  constexpr int HALF = EPT / 2;  // targets staged per epilogue round
+  constexpr int OS = QR + 4;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Bb = reinterpret_cast<float*>(smem);  // 2 buffers x [hi | lo] (32 KB each)
+  float* stage = Bb + 2 * 8192;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + ((HALF * OS + 3) & ~3));  // [0,1] D, [2] MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  int32_t* tids = reinterpret_cast<int32_t*>(tslot + 4);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  auto issue_d = [&](int buf, int dt) {
+    mbar_arrive_expect_tx(&bar[buf], 2 * kTcBBytes);
+    bulk_g2s(Bb + buf * 8192, DTC + size_t(dt) * 8192, 2 * kTcBBytes, &bar[buf]);
+  };
+  int ui = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+    if (ui < n_units) issue_d(0, pdid[units[ui].off_begin]);  // constant data: before the wait
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const uint32_t t_acc = tmem + lane_base, t_hi = tmem + lane_base + 64, t_lo = tmem + lane_base + 128;
+  pdl_trigger();
+  pdl_wait();  // s comes from the upward pass
+  const int m = tid, e = m / R, rr = m - (m / R) * R;
+  float4 c[16];
+  auto load = [&](const PUnit& uu, int t0, int j) {
+    const bool live = t0 + e < uu.n_tgt;
+    const int64_t srcg = live ? int64_t(psrc[uu.src_begin + j * uu.n_tgt + t0 + e]) : 0;
+    if constexpr (R == 1 || R == 2) {
+      const float4* src4 = reinterpret_cast<const float4*>(s + srcg * QR) + rr * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c[i] = live ? src4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float* src = s + srcg * QR + rr;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        c[i] = live ? make_float4(src[(4 * i) * R], src[(4 * i + 1) * R], src[(4 * i + 2) * R],
+                                  src[(4 * i + 3) * R])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto put = [&](int kb, float4 v) {
+    float4 h, l;
+    h.x = tf32_rna(v.x);
+    h.y = tf32_rna(v.y);
+    h.z = tf32_rna(v.z);
+    h.w = tf32_rna(v.w);
+    l.x = tf32_rna(v.x - h.x);
+    l.y = tf32_rna(v.y - h.y);
+    l.z = tf32_rna(v.z - h.z);
+    l.w = tf32_rna(v.w - h.w);
+    tmem_st4(t_hi + 4 * kb, h);
+    tmem_st4(t_lo + 4 * kb, l);
+  };
+  uint32_t mph = 0, dph = 0;  // MMA barrier phase; bit b: phase of D buffer b
+  int gs = 0;                 // step counter: D buffer = gs & 1
+  PUnit u = ui < n_units ? units[ui] : PUnit{};
+  if (ui < n_units) load(u, 0, 0);
+  while (ui < n_units) {
+    const int next = ui + int(gridDim.x);
+    const PUnit un = next < n_units ? units[next] : PUnit{};
+    for (int t0 = 0; t0 < u.n_tgt; t0 += EPT) {
+      for (int j = 0; j < u.n_off; ++j, ++gs) {
+        // ---- A = split(sources of step j) into TMEM
+        if constexpr (R == 1 || R == 4) {
+#pragma unroll
+          for (int kb = 0; kb < 16; ++kb) put(kb, c[kb]);
+        } else {
+          float mine[32], other[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            mine[2 * i] = rr ? c[i].y : c[i].x;
+            mine[2 * i + 1] = rr ? c[i].w : c[i].z;
+            other[2 * i] = rr ? c[i].x : c[i].y;
+            other[2 * i + 1] = rr ? c[i].z : c[i].w;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
+#pragma unroll
+          for (int kb = 0; kb < 8; ++kb) {
+            const float4 a = make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]);
+            const float4 b = make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]);
+            put(kb, rr ? b : a);
+            put(8 + kb, rr ? a : b);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        // ---- the step after this one (for the D prefetch and the source loads)
+        int nu = -1, nt = 0, nj = 0;  // 0: this unit, 1: next unit
+        if (j + 1 < u.n_off) {
+          nu = 0; nt = t0; nj = j + 1;
+        } else if (t0 + EPT < u.n_tgt) {
+          nu = 0; nt = t0 + EPT; nj = 0;
+        } else if (next < n_units) {
+          nu = 1; nt = 0; nj = 0;
+        }
+        const int buf = gs & 1;
+        if (tid == 0) {
+          mbar_wait(&bar[buf], (dph >> buf) & 1u);
+          dph ^= 1u << buf;
+          // D of the next step into the other buffer (its last reader, the
+          // previous step's MMA, has completed)
+          if (nu >= 0) issue_d(buf ^ 1, pdid[(nu ? un : u).off_begin + nj]);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t bh = smem_u32(Bb + buf * 8192), bl = bh + kTcBBytes;
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            const uint32_t a0 = tmem + (cc == 2 ? 128u : 64u), b0 = cc == 1 ? bl : bh;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              umma_tf32_ts(tmem, a0 + ks * 8, umma_desc_kmajor(b0 + ks * 2 * kTcLBO), (j | cc | ks) != 0);
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(&bar[2]))
+                       : "memory");
+        }
+        // the next step's sources load while the tensor core runs
+        if (nu >= 0) load(nu ? un : u, nt, nj);
+        mbar_wait(&bar[2], mph);
+        mph ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      // ---- epilogue: TMEM lane m = row m (target e, component rr), 64 columns
+      uint32_t r[64];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+          "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+          "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+            "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+            "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]),
+            "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
+            "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+            "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+            "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]),
+            "=r"(r[63])
+          : "r"(t_acc));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int n = min(EPT, u.n_tgt - t0);
+      if (rr == 0) tids[e] = e < n ? ptgt[u.tgt_begin + t0 + e] : -1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e0 = h * HALF;
+        if (e >= e0 && e < e0 + HALF && e < n)
+#pragma unroll
+          for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
+        __syncthreads();
+        constexpr int NV = QR / 4;
+        const int nh = max(0, min(HALF, n - e0));
+        for (int i = tid; i < nh * NV; i += 128) {
+          const int ee = i / NV, v = i - (i / NV) * NV;
+          const float4 val = *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
+          *reinterpret_cast<float4*>(o + int64_t(tids[e0 + ee]) * QR + 4 * v) = val;
+        }
+        __syncthreads();
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    ui = next;
+    u = un;
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
 // bytes of dynamic shared memory of tgemm_tc_kernel
 constexpr size_t kTcSmem = 6 * size_t(kTcBBytes) + 64 + 4 * 128 + 1024;
 
@@ -2459,19 +2678,36 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
           for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(b + j) * R + rr];
         }
         const float2 w = make_float2(p.x * inv, p.y * inv);
-        const float2 W1 = w, W2 = make_float2(-w.y, w.x);
-        float2 z = make_float2(1.f, 0.f);
+        // two interleaved power chains (even / odd terms, each stepping by w^2)
+        // halve the dependent complex-multiply latency per point
+        const float2 w2 = cmulf(w, w);
+        const float2 W1 = w2, W2 = make_float2(-w2.y, w2.x);
+        float2 zc[2];
+        zc[0] = make_float2(1.f, 0.f);
         if (m0) {
           const float2 wp = cpow_const<MP>(w);
-          z = wp;
-          for (int e = MP; e < m0; e += MP) z = cmulf(z, wp);
+          zc[0] = wp;
+          for (int e = MP; e < m0; e += MP) zc[0] = cmulf(zc[0], wp);
         }
+        zc[1] = cmulf(zc[0], w);
 #pragma unroll
         for (int mm = 0; mm < MP; ++mm) {
+          const float2 z = zc[mm & 1];
+          // v layout [moment][re, im][rhs column] (column pairs share an FFMA2)
+          if constexpr (R % 2 == 0) {
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr)
-            ffma2(v[(mm * R + rr) * 2], v[(mm * R + rr) * 2 + 1], qv[rr], z.x, z.y);
-          z = cmul_pk(z, W1, W2);
+            for (int rr = 0; rr < R; rr += 2) {
+              ffma2(v[(mm * 2) * R + rr], v[(mm * 2) * R + rr + 1], z.x, qv[rr], qv[rr + 1]);
+              ffma2(v[(mm * 2 + 1) * R + rr], v[(mm * 2 + 1) * R + rr + 1], z.y, qv[rr], qv[rr + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              v[(mm * 2) * R + rr] = fmaf(z.x, qv[rr], v[(mm * 2) * R + rr]);
+              v[(mm * 2 + 1) * R + rr] = fmaf(z.y, qv[rr], v[(mm * 2 + 1) * R + rr]);
+            }
+          }
+          zc[mm & 1] = cmul_pk(z, W1, W2);
         }
       }
       // transpose reduction over the 4 lanes of the group: lane g ends with
@@ -2509,16 +2745,16 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
         if (li2 >= nleaf) break;
         const int64_t lf = leaf0 + li2;
         const float nl = -logf(leaf_r[lf]);
-        const float2* ml = mu + l * mu_stride;
+        const float* ml = reinterpret_cast<const float*>(mu + l * mu_stride);  // [m][re, im][rr]
         float* dst = s + lf * int64_t(kt) * R;
         for (int t = lane; t < kt * R; t += 32) {
           const int row = t / R, rr = t - (t / R) * R;
           const int m = (row + 1) >> 1;
           float v = 0.f;
           if (row == 0)
-            v = nl * ml[rr].x;
+            v = nl * ml[rr];
           else if (m < nm)
-            v = (row & 1) ? ml[m * R + rr].x : ml[m * R + rr].y;
+            v = (row & 1) ? ml[(m * 2) * R + rr] : ml[(m * 2 + 1) * R + rr];
           dst[t] = v;
         }
       }
@@ -2541,19 +2777,33 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
         const float2 a1 = h1 ? __ldg(A + m * Q + k1) : make_float2(0.f, 0.f);
 #pragma unroll
         for (int l = 0; l < LW; ++l) {
-          float2 u[R];
+          // mu_m: re[R] then im[R]
+          const float* um = reinterpret_cast<const float*>(mu + l * mu_stride) + (m * 2) * R;
+          float ur[R], ui[R];
           if constexpr (R == 2) {
-            const float4 t = *reinterpret_cast<const float4*>(mu + l * mu_stride + m * R);
-            u[0] = make_float2(t.x, t.y);
-            u[1] = make_float2(t.z, t.w);
+            const float4 t = *reinterpret_cast<const float4*>(um);
+            ur[0] = t.x; ur[1] = t.y; ui[0] = t.z; ui[1] = t.w;
           } else {
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) u[rr] = mu[l * mu_stride + m * R + rr];
+            for (int rr = 0; rr < R; ++rr) {
+              ur[rr] = um[rr];
+              ui[rr] = um[R + rr];
+            }
           }
+          if constexpr (R % 2 == 0) {
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) {
-            acc[0][l][rr] = fmaf(a0.x, u[rr].x, fmaf(-a0.y, u[rr].y, acc[0][l][rr]));
-            acc[1][l][rr] = fmaf(a1.x, u[rr].x, fmaf(-a1.y, u[rr].y, acc[1][l][rr]));
+            for (int rr = 0; rr < R; rr += 2) {
+              ffma2(acc[0][l][rr], acc[0][l][rr + 1], -a0.y, ui[rr], ui[rr + 1]);
+              ffma2(acc[0][l][rr], acc[0][l][rr + 1], a0.x, ur[rr], ur[rr + 1]);
+              ffma2(acc[1][l][rr], acc[1][l][rr + 1], -a1.y, ui[rr], ui[rr + 1]);
+              ffma2(acc[1][l][rr], acc[1][l][rr + 1], a1.x, ur[rr], ur[rr + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+              acc[0][l][rr] = fmaf(a0.x, ur[rr], fmaf(-a0.y, ui[rr], acc[0][l][rr]));
+              acc[1][l][rr] = fmaf(a1.x, ur[rr], fmaf(-a1.y, ui[rr], acc[1][l][rr]));
+            }
           }
         }
       }
@@ -2566,7 +2816,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
         const float nl = -logf(leaf_r[lf]);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
-          const float u0 = mu[l * mu_stride + rr].x;
+          const float u0 = reinterpret_cast<const float*>(mu + l * mu_stride)[rr];
           if (h0) s[(lf * Q + k0) * R + rr] = fmaf(nl * f0, u0, acc[0][l][rr]);
           if (h1) s[(lf * Q + k1) * R + rr] = fmaf(nl * f1, u0, acc[1][l][rr]);
         }

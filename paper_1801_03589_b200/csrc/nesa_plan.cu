@@ -367,7 +367,17 @@ struct nesa_plan {
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
   bool tc2 = true;                          // ... with the A operand in TMEM (~50 KB smem)
   int tc3_ctas = 2;                         // ... persistent, this many CTAs per SM (0: one CTA per unit)
-  DevBuf<float> DTC;                        // [n_dtab][hi | lo][64 x 64] canonical tf32 D
+  DevBuf<float> DTC;                        // [n_dtab + 1][hi | lo][64 x 64] canonical tf32 D (+ zero)
+  // target-major translation (float32, Q = 64, tensor cores): units of <= 128
+  // targets of one level sharing one interaction pattern (the sorted list of
+  // their D matrices); o is written directly, no Y and no reduce
+  // (measured 561 vs 527 us at C4: the shared patterns pad the K-loop ~2x and
+  // each step's D load is serial in a CTA; NESA_PAT=1 enables it)
+  bool pat = false;
+  int pat_ctas = 1;                         // persistent CTAs per SM of the pattern kernel
+  DevBuf<PUnit> punits;
+  DevBuf<int32_t> ptgt, pdid, psrc;
+  int n_punits = 0, n_punits_fine = 0;
   DevBuf<TUnit> mom_units;
   DevBuf<TEnt> mom_ents;
   int n_mom_units = 0;
@@ -403,6 +413,8 @@ struct nesa_plan {
   double near_frac = 0.5;                    // share of near-field CTAs in the first launch
   cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
   int split_lv = 0;                          // levels >= split_lv: translated on s2
+  int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
+  int coarse_tc = 1;                         // coarse translation: 0 FFMA, 1 as fine, 2 one CTA per unit
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
   int64_t n_red_fine = 0;                    // red_ids [0, n_red_fine) are fine levels
   std::vector<int> tu_start;                 // [lv - l0]: first translation unit of level lv
@@ -561,7 +573,9 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   // tensor-core translation (float32, Q = 64): D split into tf32 hi / lo in
   // the canonical K-major core-matrix layout (see tgemm_tc_kernel)
   if (std::is_same<T, float>::value && Q == 64 && P->tc && d->n_dtab > 0) {
-    std::vector<float> h(size_t(d->n_dtab) * 8192);
+    // + one zero matrix at index n_dtab (the pattern of targets without
+    // interaction entries, so their translation sum is written as 0)
+    std::vector<float> h(size_t(d->n_dtab + 1) * 8192, 0.f);
     auto tf32 = [](float x) {
       uint32_t u;
       std::memcpy(&u, &x, 4);
@@ -1113,6 +1127,55 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->tunits.upload(units);
     P->tents.upload(ents);
     P->n_tunits = int(units.size());
+    if (P->pat && P->tc && std::is_same<T, float>::value && Q == 64 && !P->split_levels) {
+      std::vector<PUnit> pu;
+      std::vector<int32_t> tg, did, src;
+      for (int lv = P->L; lv >= P->l0; --lv) {
+        const int li = lv - P->l0;
+        std::map<std::vector<int32_t>, std::vector<int64_t>> pats;
+        for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g) {
+          std::vector<int32_t> key;
+          for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) key.push_back(int32_t(d->int_dtab[e]));
+          std::sort(key.begin(), key.end());
+          require(std::adjacent_find(key.begin(), key.end()) == key.end(), "repeated D in one interaction list");
+          if (key.empty()) key.push_back(int32_t(d->n_dtab));  // zero matrix
+          pats[key].push_back(g);
+        }
+        for (auto& kv : pats) {
+          const std::vector<int32_t>& key = kv.first;
+          const std::vector<int64_t>& gs = kv.second;
+          for (size_t i = 0; i < gs.size(); i += 128) {
+            const size_t j = std::min(gs.size(), i + 128);
+            PUnit u{};
+            u.tgt_begin = int32_t(tg.size());
+            u.n_tgt = int32_t(j - i);
+            u.off_begin = int32_t(did.size());
+            u.n_off = int32_t(key.size());
+            u.src_begin = int32_t(src.size());
+            for (size_t t = i; t < j; ++t) tg.push_back(int32_t(gs[t]));
+            did.insert(did.end(), key.begin(), key.end());
+            for (int32_t dt : key)
+              for (size_t t = i; t < j; ++t) {
+                const int64_t g = gs[t];
+                int32_t sg = int32_t(g);  // zero pattern: any valid group
+                for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e)
+                  if (d->int_dtab[e] == dt) sg = int32_t(d->int_idx[e]);
+                src.push_back(sg);
+              }
+            pu.push_back(u);
+          }
+        }
+        if (lv == P->split_lv) P->n_punits_fine = int(pu.size());
+      }
+      require(src.size() < (size_t(1) << 31), "too many pattern sources");
+      P->punits.upload(pu);
+      P->ptgt.upload(tg);
+      P->pdid.upload(did);
+      P->psrc.upload(src);
+      P->n_punits = int(pu.size());
+    } else {
+      P->pat = false;
+    }
   }
 }
 
@@ -1134,7 +1197,7 @@ void ensure_workspace(nesa_plan* P, int R) {
     P->Tup.view(P->farws.p + fb, fb);
     P->o.view(P->farws.p + 2 * fb, fb);
   }
-  P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
+  P->Y.alloc(size_t(P->pat ? 1 : std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
   P->ws_R = R;
 }
 
@@ -1226,6 +1289,7 @@ void set_smem_attrs() {
   attr(scatter_kernel<T, R>, -1);
   attr(reduce_kernel<T, R>, -1);
   attr(sum_children_kernel<T, R>, -1);
+  if constexpr (std::is_same<T, float>::value) attr(tgemm_pat_kernel<R>, int(pat_smem_bytes<R>()));
   attr(fused_up_kernel<T, R>, lim);
   attr(fused_down_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
@@ -1280,8 +1344,10 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
     if (P->v_mom) {
       const int64_t nleaf = P->leaf_end - P->leaf_begin;
       const int64_t per_cta = int64_t(kExpWarps) * kMomLeavesPerWarp;
+      int mcta = kMomCtasPerSM;
+      if (const char* e = std::getenv("NESA_MOM_CTAS")) mcta = std::max(1, std::atoi(e));
       const int grid = int(std::max<int64_t>(
-          1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(kMomCtasPerSM) * P->n_sm)));
+          1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(mcta) * P->n_sm)));
       // point staging (cp.async) helps alone but costs shared memory the
       // concurrent near field needs; NESA_MOM_BUF sets the staged points
       // per warp (0: none)
@@ -1438,11 +1504,27 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   T* Y = reinterpret_cast<T*>(P->Y.p);
   auto translate = [&](int u0, int u1, cudaStream_t st) {
     if (u1 <= u0) return;
+    if constexpr (std::is_same<T, float>::value) {
+      if (P->pat) {
+        // unit ranges map to the fine / coarse pattern units
+        const int p0 = u0 == 0 ? 0 : P->n_punits_fine;
+        const int p1 = u1 == P->n_tunits ? P->n_punits : P->n_punits_fine;
+        if (p1 > p0)
+          launch_pdl(P->pdl && st == s0, tgemm_pat_kernel<R>, std::min(p1 - p0, P->pat_ctas * P->n_sm), 128,
+                     pat_smem_bytes<R>(), st, (const PUnit*)(P->punits.p + p0), p1 - p0,
+                     (const int32_t*)P->ptgt.p, (const int32_t*)P->pdid.p, (const int32_t*)P->psrc.p,
+                     (const float*)P->DTC.p, (const float*)s, o);
+        nk++;
+        tr("translate", st);
+        return;
+      }
+    }
     const T* DTp = reinterpret_cast<const T*>(P->DT.p);
     const TUnit* up = P->tunits.p + u0;
-    if (P->tc) {
+    const bool coarse = u0 >= P->n_tunits_fine && P->split_lv <= P->L;
+    if (P->tc && !(coarse && P->coarse_tc == 0)) {
       if constexpr (std::is_same<T, float>::value) {
-        if (P->tc2 && P->tc3_ctas > 0)
+        if (P->tc2 && P->tc3_ctas > 0 && !(coarse && P->coarse_tc == 2))
           launch_pdl(P->pdl && st == s0, tgemm_tc3_kernel<R>,
                      std::min(u1 - u0, P->tc3_ctas * P->n_sm), 128, tc2_smem_bytes<R>(), st, up, u1 - u0,
                      (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
@@ -1467,7 +1549,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
   };
   auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st) {
     // o[g] = translation sum of the listed local groups
-    if (i1 <= i0) return;
+    if (i1 <= i0 || P->pat) return;
     launch_pdl(P->pdl && st == s0, reduce_kernel<T, R>, grid_for((i1 - i0) * 32, 256, cap), 256, 0,
                st, (const int32_t*)(P->red_ids.p + i0), i1 - i0, (const int64_t*)P->int_ptr.p,
                (const T*)Y, o, Q);
@@ -1586,7 +1668,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_lv[li], 0));
         translate(P->tu_start[li], unit_end(lv), P->s2);
         reduce(P->red_start[li], red_end(lv), P->s2);
-      } else if (fine && lv == P->split_lv) {
+      } else if (fine && lv == P->split_lv && !P->fine_after_up) {
         CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
       }
     }
@@ -1598,16 +1680,29 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       top_sum();
     }
     hook(3);
-    if (fine && P->split_lv == P->l0 && P->L > P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+    if (fine && ((P->split_lv == P->l0 && P->L > P->l0) || (P->fine_after_up == 1 && !per_level)))
+      CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     if (fine) {
-      if (!per_level) {
+      if (P->fine_after_up >= 2 && !per_level) {
+        // coarse translation first (it is on the critical path and needs
+        // the SM slots the fine one would hold), then the fine one on s2
+        translate(P->n_tunits_fine, P->n_tunits, s0);
+        reduce(P->n_red_fine, P->n_red, s0);
+        CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
         CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
         translate(0, P->n_tunits_fine, P->s2);
         reduce(0, P->n_red_fine, P->s2);
+        CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
+      } else {
+        if (!per_level) {
+          CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
+          translate(0, P->n_tunits_fine, P->s2);
+          reduce(0, P->n_red_fine, P->s2);
+        }
+        CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
+        translate(P->n_tunits_fine, P->n_tunits, s0);
+        reduce(P->n_red_fine, P->n_red, s0);
       }
-      CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
-      translate(P->n_tunits_fine, P->n_tunits, s0);
-      reduce(P->n_red_fine, P->n_red, s0);
     } else {
       translate(0, P->n_tunits, s0);
       reduce(0, P->n_red, s0);
@@ -1980,6 +2075,10 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
     if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
     if (const char* sl = std::getenv("NESA_SPLIT_LEVELS")) P->split_levels = std::atoi(sl) != 0;
+    if (const char* fa = std::getenv("NESA_FINE_AFTER_UP")) P->fine_after_up = std::atoi(fa);
+    if (const char* ct = std::getenv("NESA_COARSE_TC")) P->coarse_tc = std::atoi(ct);
+    if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
+    if (const char* pc = std::getenv("NESA_PAT_CTAS")) P->pat_ctas = std::max(1, std::atoi(pc));
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
     P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
