@@ -2886,11 +2886,13 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
         if (idx < nq) {
           const int row = idx / R, rr = idx - (idx / R) * R;
           const int m = (row + 1) >> 1;
-          if (row == 0)
-            beta[rr] = make_float2(nlr * ov[t], 0.f);
-          else if (m <= nt) {
-            float* bf = reinterpret_cast<float*>(beta + m * R + rr);
-            bf[(row & 1) ? 0 : 1] = ov[t];
+          // beta layout (floats): [m][re | -im][rr] (column pairs share an FFMA2)
+          float* bf = reinterpret_cast<float*>(beta);
+          if (row == 0) {
+            bf[rr] = nlr * ov[t];
+            bf[R + rr] = 0.f;
+          } else if (m <= nt) {
+            bf[m * 2 * R + ((row & 1) ? 0 : R) + rr] = (row & 1) ? ov[t] : -ov[t];
           }
         }
       }
@@ -2915,9 +2917,12 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
             acc[rr].y = fmaf(e.y, ok, acc[rr].y);
           }
         }
+        float* bf = reinterpret_cast<float*>(beta) + m * 2 * R;
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr)
-          beta[m * R + rr] = m ? acc[rr] : make_float2(nlr * acc[rr].x, 0.f);
+        for (int rr = 0; rr < R; ++rr) {
+          bf[rr] = m ? acc[rr].x : nlr * acc[rr].x;
+          bf[R + rr] = m ? -acc[rr].y : 0.f;
+        }
       }
       __syncwarp();
     }
@@ -2926,22 +2931,34 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
       const float2 w = make_float2(p.x * inv, p.y * inv);
       const float2 W1 = w, W2 = make_float2(-w.y, w.x);
       float2 z = w;
+      const float* bf = reinterpret_cast<const float*>(beta);
       float acc[R];
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] = beta[rr].x;
+      for (int rr = 0; rr < R; ++rr) acc[rr] = bf[rr];
 #pragma unroll 4
       for (int m = 1; m <= nt; ++m) {
-        float2 bt[R];
+        float br[R], nbi[R];  // re and -im of beta_m per column
         if constexpr (R == 2) {
-          const float4 t = *reinterpret_cast<const float4*>(beta + m * 2);
-          bt[0] = make_float2(t.x, t.y);
-          bt[1] = make_float2(t.z, t.w);
+          const float4 t = *reinterpret_cast<const float4*>(bf + m * 4);
+          br[0] = t.x; br[1] = t.y; nbi[0] = t.z; nbi[1] = t.w;
         } else {
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) bt[rr] = beta[m * R + rr];
+          for (int rr = 0; rr < R; ++rr) {
+            br[rr] = bf[m * 2 * R + rr];
+            nbi[rr] = bf[m * 2 * R + R + rr];
+          }
         }
+        // acc += Re(beta_m z) = re z.x - im z.y (the -im term first, as before)
+        if constexpr (R % 2 == 0) {
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(bt[rr].x, z.x, fmaf(-bt[rr].y, z.y, acc[rr]));
+          for (int rr = 0; rr < R; rr += 2) {
+            ffma2(acc[rr], acc[rr + 1], z.y, nbi[rr], nbi[rr + 1]);
+            ffma2(acc[rr], acc[rr + 1], z.x, br[rr], br[rr + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(br[rr], z.x, fmaf(nbi[rr], z.y, acc[rr]));
+        }
         z = cmul_pk(z, W1, W2);
       }
 #pragma unroll
