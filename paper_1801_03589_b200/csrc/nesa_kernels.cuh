@@ -448,11 +448,24 @@ template <typename T, int R>
 __global__ void gather_kernel(const T* __restrict__ q, const int64_t* __restrict__ perm,
                               T* __restrict__ qt, int64_t n, int ldq) {
   KtScope kt_(1);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t j = perm[i];
+  // four independent rows per thread per round: the random reads of q are
+  // latency-bound, so keep several in flight
+  constexpr int U = 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < n; i0 += U * stride) {
+    int64_t j[U];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) qt[i * R + rr] = q[j * ldq + rr];
+    for (int u = 0; u < U; ++u) j[u] = i0 + u * stride < n ? perm[i0 + u * stride] : -1;
+    T v[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) v[u][rr] = j[u] >= 0 ? q[j[u] * ldq + rr] : T(0);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j[u] >= 0)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) qt[(i0 + u * stride) * R + rr] = v[u][rr];
   }
 }
 
@@ -2852,18 +2865,32 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
   float* os = reinterpret_cast<float*>(beta + nb);
   const int ne = nt + 1;
   constexpr int kSlots = 4;
-  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf;
-       li += int64_t(gridDim.x) * kExpWarps) {
+  const int nq = BETA_IN ? 64 * R : Q * R;
+  constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
+  // the next leaf's extent, radius and amplitude (or coefficient) words are
+  // loaded one leaf ahead, so only the point loads are exposed per leaf
+  const int64_t lstride = int64_t(gridDim.x) * kExpWarps;
+  int64_t nx_b = 0;
+  int nx_n = 0;
+  float nx_r = 1.f, nx_ov[NOV];
+  auto fetch = [&](int64_t lj) {
+    if (lj >= nleaf) return;
+    const int64_t lf = leaf0 + lj;
+    nx_b = leaf_start[lf];
+    nx_n = int(leaf_stop[lf] - nx_b);
+    nx_r = leaf_r[lf];
+#pragma unroll
+    for (int t = 0; t < NOV; ++t) nx_ov[t] = lane + 32 * t < nq ? o[lf * nq + lane + 32 * t] : 0.f;
+  };
+  fetch(int64_t(blockIdx.x) * kExpWarps + warp);
+  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf; li += lstride) {
     const int64_t leaf = leaf0 + li;
-    const int64_t b = leaf_start[leaf];
-    const int n = int(leaf_stop[leaf] - b);
-    const float r = leaf_r[leaf];
-    // prefetch: amplitudes (or coefficients) and the first kSlots * 32 points
-    const int nq = BETA_IN ? 64 * R : Q * R;
-    constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
+    const int64_t b = nx_b;
+    const int n = nx_n;
+    const float r = nx_r;
     float ov[NOV];
 #pragma unroll
-    for (int t = 0; t < NOV; ++t) ov[t] = lane + 32 * t < nq ? o[leaf * nq + lane + 32 * t] : 0.f;
+    for (int t = 0; t < NOV; ++t) ov[t] = nx_ov[t];
     float2 pp[kSlots];
     int64_t dd[kSlots];
     float bb[kSlots][R];
@@ -2877,6 +2904,7 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
         for (int rr = 0; rr < R; ++rr) bb[i][rr] = phin ? phin[(b + j) * R + rr] : 0.f;
       }
     }
+    fetch(li + lstride);
     const float nlr = -logf(r);
     if constexpr (BETA_IN) {
       // beta^ row 0 -> beta_0 = -log(r) sum o; rows (2m-1, 2m) -> beta_m

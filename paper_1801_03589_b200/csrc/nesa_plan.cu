@@ -1228,7 +1228,9 @@ void launch_blockgemv_v(const DevBlockSet& bs, const T* x, T* y, const T* base, 
 // (measured in the full C4 product: 4 warps x 24 KB x 2 stages 555 us, 4 x 16 KB x 3 556,
 // 4 x 32 KB x 2 580, 8 x 16 KB x 3 (the generic default) 633; fewer consumer threads and
 // larger stages amortise the per-chunk consumer overhead that bounds an SM's share)
-#define NESA_BG_VARIANTS(X) X(4, 24576, 2) X(4, 16384, 3) X(4, 32768, 2) X(8, 32768, 2)
+#define NESA_BG_VARIANTS(X)                                                                 \
+  X(4, 24576, 2) X(4, 16384, 3) X(4, 32768, 2) X(8, 32768, 2) X(4, 32768, 3) X(8, 32768, 3) \
+  X(4, 49152, 2) X(8, 24576, 4)
 
 bool bg_variant_known(int w, int b, int n) {
   bool known = w == kNCW && b == kABytes && n == kStages;
@@ -1791,7 +1793,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         prof_mark(P, profn, 2 * NESA_STAGE_NEAR, s1);
       else if (P->near_after == 1 || P->near_after == -1)
         CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
-      if (P->near_ctas == 1)
+      if (P->near_ctas == 1 && P->near_nst == kStages && P->near_ncw == kNCW && P->near_ab == kABytes)
         launch_blockgemv<T, R, kModeStore, 6>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       else if (nsplit)
         launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1, 0, n_a);
@@ -2053,7 +2055,8 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
         P->near_nst = n;
       }
     }
-    if (P->near_ctas == 1) {  // the one-CTA-per-SM 6-stage ring uses the generic geometry
+    if (P->near_ctas == 1 && !std::getenv("NESA_NEAR_VARIANT")) {
+      // one CTA per SM: the generic geometry with a 6-stage ring
       P->near_ncw = kNCW;
       P->near_ab = kABytes;
       P->near_nst = kStages;
