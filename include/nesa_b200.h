@@ -194,6 +194,16 @@ const char* nesa_trace_name(nesa_plan* plan, int32_t i);
 int nesa_ktrace_enable(nesa_plan* plan, int64_t capacity);
 int64_t nesa_ktrace_read(nesa_plan* plan, unsigned long long* out, int64_t max_records);
 
+/* Exact O(N^2) potential sum (reference: dense.dense_matvec, dense.py:14-33)
+ * on the device, float64: phi_i = sum_{j != i} -0.5 log|x_i - x_j|^2 q_j.
+ * points_dev: (n, 2) row-major; q_dev / phi_dev: (n, ncols) row-major,
+ * ncols real columns (a complex vector = 2).  Synchronises the stream.
+ * Coincident distinct points -> NESA_ERR_INVALID "coincident points"
+ * (the reference's ValueError).  The approximation-error oracle at sizes
+ * the CPU cannot reach. */
+int nesa_dense_matvec(const double* points_dev, const double* q_dev, double* phi_dev, int64_t n,
+                      int32_t ncols, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

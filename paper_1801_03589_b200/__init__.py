@@ -7,6 +7,8 @@ itself runs in libnesa_b200.so (hand-written sm_100a CUDA, C ABI in
 include/nesa_b200.h); there is no CPU fallback.
 """
 
+from .benchmark import BenchConfig, run_benchmark
+from .dense import dense_matvec_gpu
 from .fastmvp import as_tree, get_plan, mvp, mvp_serial, task_counts
 from .geometry import (BBox, CurveSpec, bounding_box, generate_sources, parse_curve_spec,
                        plane_wave_rhs, random_rhs, wavenumber)
@@ -21,7 +23,7 @@ from .quadtree import Tree, TreeParams, build_tree, interaction_list, neighbor_l
 __version__ = "0.1.0"
 
 __all__ = [
-    "BBox", "CurveSpec", "GmresResult", "MvpPipeline", "NesaParams", "NesaPlan", "OperatorSet", "OperatorTables", "Tree",
+    "BBox", "BenchConfig", "CurveSpec", "dense_matvec_gpu", "run_benchmark", "GmresResult", "MvpPipeline", "NesaParams", "NesaPlan", "OperatorSet", "OperatorTables", "Tree",
     "TreeParams", "algorithmic_bytes", "algorithmic_flops", "as_tree", "bounding_box",
     "build_all", "build_tables", "build_tree", "circle_points", "gemv", "generate_sources",
     "get_plan", "gmres", "interaction_list", "kernel_eval", "load_problem", "kernel_matrix", "mvp", "mvp_serial",

@@ -2176,6 +2176,95 @@ NESA_API int nesa_plan_destroy(nesa_plan* plan) {
   })
 }
 
+// ---------------------------------------------------------------------------
+// Exact O(N^2) potential sum on the GPU (dense.py:14-33): the approximation
+// error oracle at sizes the CPU cannot reach.
+// phi_i = sum_{j != i} -0.5 log(d2_ij) q_j with d2 = dx*dx + dy*dy formed
+// without contraction as the reference's einsum does, float64 throughout.
+// One thread per target; sources stream through shared memory in tiles.
+// Coincident distinct points are counted (the reference raises ValueError).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kDenseTile = 256;
+
+template <int R>
+__global__ void __launch_bounds__(kDenseTile) dense_kernel(const double* __restrict__ pts,
+                                                           const double* __restrict__ q,
+                                                           double* __restrict__ phi, int64_t n,
+                                                           unsigned long long* coincident) {
+  __shared__ double sx[kDenseTile], sy[kDenseTile], sq[kDenseTile * R];
+  const int64_t i = int64_t(blockIdx.x) * kDenseTile + threadIdx.x;
+  const bool live = i < n;
+  const double xi = live ? pts[2 * i] : 0.0, yi = live ? pts[2 * i + 1] : 0.0;
+  double acc[R];
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) acc[rr] = 0.0;
+  unsigned long long bad = 0;
+  for (int64_t j0 = 0; j0 < n; j0 += kDenseTile) {
+    const int64_t j = j0 + threadIdx.x;
+    __syncthreads();
+    if (j < n) {
+      sx[threadIdx.x] = pts[2 * j];
+      sy[threadIdx.x] = pts[2 * j + 1];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) sq[threadIdx.x * R + rr] = q[j * R + rr];
+    }
+    __syncthreads();
+    const int m = n - j0 < kDenseTile ? int(n - j0) : kDenseTile;
+    if (!live) continue;
+    for (int t = 0; t < m; ++t) {
+      if (j0 + t == i) continue;
+      const double dx = __dsub_rn(xi, sx[t]), dy = __dsub_rn(yi, sy[t]);
+      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      if (d2 == 0.0) {
+        ++bad;
+        continue;
+      }
+      const double k = -0.5 * log(d2);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = fma(k, sq[t * R + rr], acc[rr]);
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) phi[i * R + rr] = acc[rr];
+  }
+  if (bad) atomicAdd(coincident, bad);
+}
+}  // namespace
+
+int dense_run(const double* points_dev, const double* q_dev, double* phi_dev, int64_t n,
+              int32_t ncols, void* stream) {
+  require(n >= 2, "n must be >= 2");
+  require(points_dev && q_dev && phi_dev, "null pointer");
+  require(ncols >= 1 && ncols <= 4, "ncols must be 1..4 (real columns; complex = 2)");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* cnt = nullptr;
+  CUDA_OK(cudaMallocAsync(&cnt, sizeof(unsigned long long), st));
+  CUDA_OK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+  const int grid = int((n + kDenseTile - 1) / kDenseTile);
+  if (ncols == 1)
+    dense_kernel<1><<<grid, kDenseTile, 0, st>>>(points_dev, q_dev, phi_dev, n, cnt);
+  else if (ncols == 2)
+    dense_kernel<2><<<grid, kDenseTile, 0, st>>>(points_dev, q_dev, phi_dev, n, cnt);
+  else if (ncols == 3)
+    dense_kernel<3><<<grid, kDenseTile, 0, st>>>(points_dev, q_dev, phi_dev, n, cnt);
+  else
+    dense_kernel<4><<<grid, kDenseTile, 0, st>>>(points_dev, q_dev, phi_dev, n, cnt);
+  CUDA_OK(cudaGetLastError());
+  unsigned long long h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  CUDA_OK(cudaFree(cnt));
+  require(h == 0, "coincident points");
+  return NESA_OK;
+}
+
+NESA_API int nesa_dense_matvec(const double* points_dev, const double* q_dev, double* phi_dev,
+                               int64_t n, int32_t ncols, void* stream) {
+  NESA_GUARD(return dense_run(points_dev, q_dev, phi_dev, n, ncols, stream));
+}
+
 NESA_API const char* nesa_last_error(void) { return g_last_error.c_str(); }
 
 NESA_API int nesa_abi_version(void) { return NESA_ABI_VERSION; }
