@@ -381,6 +381,41 @@ def run_ours(args):
                "sync_call": {"value": 1e3 / s_ms, "ms_per_step": s_ms,
                              "api": "paper_1801_03589_b200.mvp(tree, tables, pinned torch.complex64 (N,))"}}
 
+    if not args.no_e2e and world > 1:
+        # every rank: its q (the full vector, original order) from pinned host
+        # memory, the distributed product, its phi back (its points' entries;
+        # the ranks' outputs are disjoint); time = max over ranks
+        qh = torch.from_numpy(q).pin_memory()
+        ph = torch.empty_like(qh).pin_memory()
+        qd2 = torch.empty_like(qd)
+        phd2 = torch.zeros_like(qd)
+        k2 = max(10, min(args.steps, 100))
+
+        def e2e_step():
+            qd2.copy_(qh, non_blocking=True)
+            engine.matvec_ptr(qd2.data_ptr(), phd2.data_ptr(), 1, True, stream=stream.cuda_stream)
+            ph.copy_(phd2, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / k2], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+        e2e = {"value": 1e3 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(qh.numel() * 8) * world,
+               "d2h_bytes_per_step": int(ph.numel() * 8) * world, "ms_per_step": e_ms,
+               "api": "paper_1801_03589_b200.dist.DistNesa.matvec_ptr per rank: H2D of q from pinned "
+                      "memory, product (stage 1, NCCL all_gather of partial source amplitudes, "
+                      "stage 2), D2H of the rank's phi; max over ranks"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(tree, params, q)

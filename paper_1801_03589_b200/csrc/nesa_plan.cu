@@ -1857,20 +1857,24 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     }
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL + 1, s0);
   } else if (stage == 1) {
+    // multi-GPU stage 1: the near field (local leaves) runs beside the
+    // radiation and the upward pass, before the halo exchange; stage 2 is
+    // the far field's second half and the reception
     gather();
-    if (far) {
-      nk += launch_radiation<T, R>(P, qt, s, s0);
-      up_pass();
-    }
-  } else {
     CUDA_OK(cudaEventRecord(P->ev_fork, s0));
     CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
     if (near) {
       launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
       nk++;
     }
-    if (far) down_pass();
+    if (far) {
+      nk += launch_radiation<T, R>(P, qt, s, s0);
+      up_pass();
+    }
     join_near();
+  } else {
+    near_joined = true;  // phin was completed in stage 1
+    if (far) down_pass();
     finish();
   }
   return nk;
