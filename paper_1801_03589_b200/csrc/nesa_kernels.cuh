@@ -1843,8 +1843,8 @@ __global__ void __launch_bounds__(128) tgemm_tc2_kernel(const TUnit* __restrict_
 // allocates TMEM once, and fetches the next unit's D as soon as the last MMA
 // of the current one has consumed the D buffer, so the D copy, the next
 // sources and the epilogue overlap instead of paying one CTA start per unit.
-template <int R>
-__global__ void __launch_bounds__(128) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
+template <int R, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
                                                         const TEnt* __restrict__ ents,
                                                         const float* __restrict__ DTC,
                                                         const float* __restrict__ s, float* Y) {
@@ -2625,14 +2625,14 @@ constexpr int kMomBufPts = 800;  // staged points per warp batch (8 leaves)
 // MU_OUT: instead of applying A, write the leaf's real moment vector
 // mu^[leaf][kt][R] (row 0 = -log(r) mu_0, rows 2m-1 / 2m = Re / Im mu_m,
 // zero padding) for the warp-tiled GEMM s = A^ mu^ (tgemm_wt_kernel).
-template <int R, bool MU_OUT = false>
-__global__ void __launch_bounds__(32 * kExpWarps) radiation_mom_kernel(
+template <int R, bool MU_OUT = false, int MPX = 0, int MINB = 1>
+__global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
     int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0, int bufpts = kMomBufPts) {
   KtScope kt_(60 + int(MU_OUT));
-  constexpr int MP = 40 / R;           // moments per pass
+  constexpr int MP = MPX > 0 ? MPX : 40 / R;  // moments per pass
   constexpr int NV = 2 * R * MP;       // 80 accumulators
   constexpr int NV2 = NV / 2, NV4 = NV / 4;
   constexpr int LW = kMomLeavesPerWarp;

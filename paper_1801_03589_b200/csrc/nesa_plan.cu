@@ -363,6 +363,7 @@ struct nesa_plan {
   // Q = 64: s = A^ mu^ as a warp-tiled GEMM over the leaves (KT = mom_kt)
   int mom_kt = 0;
   int mom_buf = 800;                        // staged points per warp in the moment kernel
+  int mom_variant = 0;                      // moment kernel instantiation (launch_radiation)
   DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
   bool tc2 = true;                          // ... with the A operand in TMEM (~50 KB smem)
@@ -414,6 +415,7 @@ struct nesa_plan {
   cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
+  int tc3_minb = 0;                          // tgemm_tc3 register budget (3: <= 168 registers)
   int coarse_tc = 1;                         // coarse translation: 0 FFMA, 1 as fine, 2 one CTA per unit
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
   int64_t n_red_fine = 0;                    // red_ids [0, n_red_fine) are fine levels
@@ -1296,12 +1298,15 @@ void set_smem_attrs() {
   attr(fused_down_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
     attr(radiation_mom_kernel<R>, lim);
+    attr(radiation_mom_kernel<R, false, 0, 4>, lim);
+    attr(radiation_mom_kernel<R, false, 20 / R, 4>, lim);
     attr(radiation_mom_kernel<R, true>, lim);
     attr(tgemm_wt_kernel<float, R, 64, 80>, lim);
     attr(tgemm_wt_kernel<float, R, 128, 80, 64>, lim);
     attr(tgemm_tc_kernel<R>, int(kTcSmem));
     attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_tc3_kernel<R>, int(tc2_smem_bytes<R>()));
+    attr(tgemm_tc3_kernel<R, 3>, int(tc2_smem_bytes<R>()));
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
     attr(reception_exp_kernel<R, true>, lim);
@@ -1373,9 +1378,19 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
               P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s, nullptr);
         return 2;
       }
-      radiation_mom_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
-          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, s, P->leaf_begin,
-          nleaf, P->Q, P->v_nm, 0, bufpts);
+      // register budget for 4 CTAs / SM (<= 128 registers, no spills): at the
+      // natural 169 registers only 2 CTAs fit (measured 531 vs 537 us at C4);
+      // NESA_MOM_VARIANT=1: uncapped, 3: half the moments per pass (capped)
+      auto go = [&](auto kern) {
+        kern<<<grid, 32 * kExpWarps, sm, st>>>(P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p,
+                                                P->mom_A.p, qt, s, P->leaf_begin, nleaf, P->Q, P->v_nm, 0,
+                                                bufpts);
+      };
+      switch (P->mom_variant) {
+        case 1: go(radiation_mom_kernel<R>); break;
+        case 3: go(radiation_mom_kernel<R, false, 20 / R, 4>); break;
+        default: go(radiation_mom_kernel<R, false, 0, 4>); break;
+      }
       return 1;
     }
   }
@@ -1526,7 +1541,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     const bool coarse = u0 >= P->n_tunits_fine && P->split_lv <= P->L;
     if (P->tc && !(coarse && P->coarse_tc == 0)) {
       if constexpr (std::is_same<T, float>::value) {
-        if (P->tc2 && P->tc3_ctas > 0 && !(coarse && P->coarse_tc == 2))
+        if (P->tc2 && P->tc3_ctas > 0 && !(coarse && P->coarse_tc == 2) && P->tc3_minb >= 3)
+          launch_pdl(P->pdl && st == s0, tgemm_tc3_kernel<R, 3>,
+                     std::min(u1 - u0, P->tc3_ctas * P->n_sm), 128, tc2_smem_bytes<R>(), st, up, u1 - u0,
+                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+        else if (P->tc2 && P->tc3_ctas > 0 && !(coarse && P->coarse_tc == 2))
           launch_pdl(P->pdl && st == s0, tgemm_tc3_kernel<R>,
                      std::min(u1 - u0, P->tc3_ctas * P->n_sm), 128, tc2_smem_bytes<R>(), st, up, u1 - u0,
                      (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
@@ -2072,6 +2091,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       if (P->l2_persist > 0) CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, P->l2_persist));
     }
     if (const char* mb = std::getenv("NESA_MOM_BUF")) P->mom_buf = std::max(0, std::atoi(mb));
+    if (const char* mv = std::getenv("NESA_MOM_VARIANT")) P->mom_variant = std::atoi(mv);
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
     if (const char* tc2 = std::getenv("NESA_TC2")) P->tc2 = std::atoi(tc2) != 0;
     if (const char* t3 = std::getenv("NESA_TC3_CTAS")) P->tc3_ctas = std::max(0, std::atoi(t3));
@@ -2084,6 +2104,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* sl = std::getenv("NESA_SPLIT_LEVELS")) P->split_levels = std::atoi(sl) != 0;
     if (const char* fa = std::getenv("NESA_FINE_AFTER_UP")) P->fine_after_up = std::atoi(fa);
     if (const char* ct = std::getenv("NESA_COARSE_TC")) P->coarse_tc = std::atoi(ct);
+    if (const char* tm = std::getenv("NESA_TC3_MINB")) P->tc3_minb = std::atoi(tm);
     if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
     if (const char* pc = std::getenv("NESA_PAT_CTAS")) P->pat_ctas = std::max(1, std::atoi(pc));
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
