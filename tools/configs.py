@@ -8,6 +8,9 @@ C3: ellipse (5, 0.5) + 2 plates, seed 2, N = 200 000, P = 48, Q = 48
 C4: ellipse (5, 0.5) + 2 plates, seed 3, N = 2M,      P = 64, Q = 64
 Each with a float32 plan / complex64 vector and a float64 plan / complex128
 vector; device-resident, CUDA events around `reps` back-to-back products.
+C5 (--c5): ellipse + plates, seed 4, N = 200 000, 64 plane waves
+exp(-j k d_m . r) (k at 10 points per wavelength), Q in {24, 48, 96} x leaf
+P in {32, 64, 128}, complex64: one product of all 64 right-hand sides.
 """
 import argparse
 import json
@@ -30,7 +33,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--only", default="")
+    ap.add_argument("--c5", action="store_true")
     a = ap.parse_args()
+    if a.c5:
+        return c5(a)
     import numpy as np
     import torch
     import paper_1801_03589_b200 as nesa
@@ -66,6 +72,40 @@ def main():
             out.append(rec)
             plan.close()
     return out
+
+
+def c5(a):
+    import numpy as np
+    import torch
+    import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.plan import NesaPlan
+    n = 200_000
+    spec = nesa.CurveSpec(kind="ellipse-plates", seed=4)
+    pts = nesa.generate_sources(spec, n)
+    k = nesa.wavenumber(spec, n)
+    q = nesa.plane_wave_rhs(pts, k, 64).astype(np.complex64)
+    qd = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    phi = torch.empty_like(qd)
+    st = torch.cuda.current_stream()
+    for P in (32, 64, 128):
+        tree = nesa.build_tree(pts, nesa.TreeParams(P=P))
+        for Q in (24, 48, 96):
+            plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=Q)), dtype="f32")
+            for _ in range(3):
+                plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(3, a.reps // 20)
+            e0.record(st)
+            for _ in range(reps):
+                plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
+            e1.record(st)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            rec = {"config": "C5", "N": n, "P": P, "Q": Q, "rhs": 64, "levels": tree.L - tree.l0 + 1,
+                   "plan": "f32", "ms_per_64rhs_product": round(ms, 3),
+                   "rhs_products_per_s": round(64e3 / ms, 1)}
+            print(json.dumps(rec), flush=True)
+            plan.close()
 
 
 if __name__ == "__main__":
