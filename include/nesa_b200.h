@@ -153,6 +153,14 @@ int nesa_matvec_stage(nesa_plan* plan, int32_t stage, const void* q_dev,
                       uint32_t flags, void* stream);
 void* nesa_plan_s_dev(nesa_plan* plan, int32_t nrhs_real);
 
+/* Columns [col0, col0 + ncols_real) of an (N, ld_real) row-major real block
+ * (a complex right-hand side is 2 adjacent real columns) -- the same product
+ * as nesa_matvec on that column range, in blocks of <= 4 columns.  Lets a
+ * caller spread many right-hand sides over several plans on several streams
+ * (reference: mvp_serial on a multi-column q, fastmvp.py:142-172). */
+int nesa_matvec_cols(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t ld_real,
+                     int32_t col0, int32_t ncols_real, uint32_t flags, void* stream);
+
 int nesa_plan_destroy(nesa_plan* plan);
 
 const char* nesa_last_error(void);

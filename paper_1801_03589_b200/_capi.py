@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "nesa_plan_create", "nesa_matvec", "nesa_matvec_stage", "nesa_plan_s_dev",
     "nesa_plan_destroy", "nesa_last_error", "nesa_abi_version", "nesa_plan_stat",
     "nesa_profile_reset", "nesa_profile_read", "nesa_trace_read", "nesa_trace_name",
-    "nesa_ktrace_enable", "nesa_ktrace_read", "nesa_dense_matvec",
+    "nesa_ktrace_enable", "nesa_ktrace_read", "nesa_dense_matvec", "nesa_matvec_cols",
 )
 
 _p = ctypes.c_void_p
@@ -111,6 +111,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_ktrace_read.restype = ctypes.c_int64
     lib.nesa_dense_matvec.argtypes = [_p, _p, _p, ctypes.c_int64, ctypes.c_int32, _p]
     lib.nesa_dense_matvec.restype = ctypes.c_int
+    lib.nesa_matvec_cols.argtypes = [_p, _p, _p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_uint32, _p]
+    lib.nesa_matvec_cols.restype = ctypes.c_int
     if lib.nesa_abi_version() != NESA_ABI_VERSION:
         raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
     _lib = lib

@@ -2171,6 +2171,28 @@ NESA_API int nesa_matvec(nesa_plan* plan, const void* q_dev, void* phi_dev, int3
   NESA_GUARD(return run_matvec(plan, q_dev, phi_dev, nrhs, is_complex, flags, stream, 0));
 }
 
+int run_cols(nesa_plan* P, const void* q, void* phi, int32_t ld, int32_t col0, int32_t ncols,
+             uint32_t flags, void* stream) {
+  require(P != nullptr, "null plan");
+  require(q != nullptr && phi != nullptr, "null vector");
+  require(ld >= 1 && col0 >= 0 && ncols >= 1 && col0 + ncols <= ld, "bad column range");
+  require(!(flags & NESA_PROFILE), "profiling takes one block");
+  const size_t es = P->esz;
+  for (int c0 = col0; c0 < col0 + ncols;) {
+    const int left = col0 + ncols - c0;
+    const int Rb = left >= 4 ? 4 : (left >= 2 ? 2 : 1);
+    run_block(P, static_cast<const char*>(q) + c0 * es, static_cast<char*>(phi) + c0 * es, Rb, ld,
+              flags, stream, 0);
+    c0 += Rb;
+  }
+  return NESA_OK;
+}
+
+NESA_API int nesa_matvec_cols(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t ld_real,
+                              int32_t col0, int32_t ncols_real, uint32_t flags, void* stream) {
+  NESA_GUARD(return run_cols(plan, q_dev, phi_dev, ld_real, col0, ncols_real, flags, stream));
+}
+
 NESA_API int nesa_matvec_stage(nesa_plan* plan, int32_t stage, const void* q_dev, void* phi_dev,
                                int32_t nrhs, int32_t is_complex, uint32_t flags, void* stream) {
   NESA_GUARD({

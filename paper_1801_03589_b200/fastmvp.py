@@ -27,7 +27,7 @@ from .operators import NesaParams, OperatorSet, OperatorTables
 from .plan import NesaPlan
 from .quadtree import Tree, TreeArrays
 
-__all__ = ["mvp", "mvp_serial", "task_counts", "get_plan", "as_tree"]
+__all__ = ["mvp", "mvp_serial", "task_counts", "get_plan", "get_lanes", "as_tree", "RhsLanes"]
 
 
 def as_tree(tree) -> Tree:
@@ -88,6 +88,64 @@ def get_plan(tree, ops, dtype: str = "f64", device: int = 0) -> NesaPlan:
     return ent[1]
 
 
+class RhsLanes:
+    """Many right-hand sides spread over ``lanes`` plans of the same problem
+    (each with its own workspace and CUDA graphs) on ``lanes`` streams.
+
+    One plan runs a multi-column product as blocks of <= 4 real columns one
+    after another; every block walks the latency-bound far-field chain again.
+    Blocks of different lanes run concurrently, so their far chains overlap
+    each other and the near-field streams (C5's 64 plane waves).  The column
+    ranges are multiples of 4, so the block decomposition -- and every result
+    bit -- is that of the single-plan product.
+    """
+
+    def __init__(self, plan: NesaPlan, lanes: int):
+        import torch
+        self.plans = [plan] + [NesaPlan(plan.tree, plan.ops_in, dtype=plan.dtype,
+                                        device=plan.device) for _ in range(lanes - 1)]
+        self.streams = [torch.cuda.Stream(plan.device) for _ in range(lanes)]
+        self.events = [torch.cuda.Event() for _ in range(lanes)]
+
+    def matvec_ptr(self, q_ptr: int, phi_ptr: int, nrhs: int, is_complex: bool,
+                   near: bool = True, far: bool = True, stream: int = 0) -> None:
+        import torch
+        rt = nrhs * (2 if is_complex else 1)
+        blocks = -(-rt // 4)
+        lanes = min(len(self.plans), blocks)
+        per = -(-blocks // lanes) * 4
+        caller = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        fork = torch.cuda.Event()
+        fork.record(caller)
+        used = []
+        for k in range(lanes):
+            c0 = k * per
+            n = min(per, rt - c0)
+            if n <= 0:
+                break
+            s = self.streams[k]
+            s.wait_event(fork)
+            self.plans[k].matvec_cols_ptr(q_ptr, phi_ptr, rt, c0, n, near=near, far=far,
+                                          stream=s.cuda_stream)
+            self.events[k].record(s)
+            used.append(k)
+        for k in used:
+            caller.wait_event(self.events[k])
+
+
+def get_lanes(tree, ops, dtype: str = "f64", device: int = 0, lanes: int | None = None) -> RhsLanes:
+    """Cached RhsLanes for (tree, ops, dtype, device); lane 0 is get_plan's."""
+    import os
+    if lanes is None:
+        lanes = max(1, int(os.environ.get("NESA_RHS_LANES", "4")))
+    plan = get_plan(tree, ops, dtype=dtype, device=device)
+    ent = getattr(plan, "_lanes", None)
+    if ent is None or len(ent.plans) != lanes:
+        ent = RhsLanes(plan, lanes)
+        plan._lanes = ent
+    return ent
+
+
 def _adopt_opset(ops) -> OperatorSet:
     """A reference taskfmm OperatorSet -> ours (same dicts, shared matrices)."""
     p = ops.params
@@ -141,8 +199,13 @@ def mvp(tree, ops, q, runtime=None, vec=None, near: bool = True, far: bool = Tru
         else:
             qd = torch.from_numpy(np.ascontiguousarray(q)).to(f"cuda:{dev}", dtype=tdt)
         phi = torch.empty_like(qd)
-        plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), nrhs, is_complex, near=near, far=far,
-                        stream=stream.cuda_stream)
+        if nrhs * (2 if is_complex else 1) > 4:   # several blocks: spread over lanes
+            get_lanes(t, ops, dtype=dtype, device=dev).matvec_ptr(
+                qd.data_ptr(), phi.data_ptr(), nrhs, is_complex, near=near, far=far,
+                stream=stream.cuda_stream)
+        else:
+            plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), nrhs, is_complex, near=near, far=far,
+                            stream=stream.cuda_stream)
         if not on_host:
             return phi
         if is_torch:        # CPU tensor in -> CPU tensor out (pinned if the input was)

@@ -263,6 +263,14 @@ class NesaPlan:
                                             flags, ctypes.c_void_p(stream))
         _capi.check(rc)
 
+    def matvec_cols_ptr(self, q_ptr: int, phi_ptr: int, ld_real: int, col0: int, ncols: int,
+                        near: bool = True, far: bool = True, stream: int = 0) -> None:
+        """Columns [col0, col0 + ncols) of (N, ld_real) real device blocks."""
+        flags = (_capi.NESA_NEAR if near else 0) | (_capi.NESA_FAR if far else 0)
+        _capi.check(self.lib.nesa_matvec_cols(self.handle, ctypes.c_void_p(q_ptr),
+                                              ctypes.c_void_p(phi_ptr), ld_real, col0, ncols, flags,
+                                              ctypes.c_void_p(stream)))
+
     def s_dev_ptr(self, nrhs_real: int) -> int:
         p = self.lib.nesa_plan_s_dev(self.handle, nrhs_real)
         if not p:

@@ -433,3 +433,31 @@ def test_q48_split_and_fused_levels(monkeypatch, dtype, tol):
     ref = oracle_mvp(tree, build_all(tree, params), q)
     qq = q if dtype == "f64" else q.astype(np.complex64)
     assert rel_l2(mvp(tree, params, qq), ref) <= tol
+
+
+@pytest.mark.parametrize("dtype,cdt", [("f32", np.complex64), ("f64", np.complex128)])
+def test_rhs_lanes_bitwise_and_vs_oracle(dtype, cdt):
+    # many right-hand sides spread over 3 plans on 3 streams: every bit equals
+    # the single-plan multi-column product, and each column the oracle
+    from paper_1801_03589_b200.fastmvp import RhsLanes
+    pts = geo.generate_sources(geo.CurveSpec(kind="circle-random", seed=1), 20000)
+    tree = build_tree(pts, TreeParams(P=32))
+    params = NesaParams(Q=32)
+    rng = np.random.default_rng(5)
+    q = (rng.standard_normal((20000, 11)) + 1j * rng.standard_normal((20000, 11))).astype(cdt)
+    plan = NesaPlan(tree, params, dtype=dtype)
+    lanes = RhsLanes(plan, 3)
+    qd = torch.from_numpy(q).cuda()
+    a, b = torch.empty_like(qd), torch.empty_like(qd)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.matvec_ptr(qd.data_ptr(), a.data_ptr(), 11, True, stream=st)
+    lanes.matvec_ptr(qd.data_ptr(), b.data_ptr(), 11, True, stream=st)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    ops = build_all(tree, params)
+    tol = 1e-12 if dtype == "f64" else 1e-5
+    for j in (0, 5, 10):
+        assert rel_l2(b[:, j].cpu().numpy(), oracle_mvp(tree, ops, q[:, j].astype(np.complex128))) <= tol
+    for p in lanes.plans[1:]:
+        p.close()
+    plan.close()

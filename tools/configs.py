@@ -78,6 +78,7 @@ def c5(a):
     import numpy as np
     import torch
     import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.fastmvp import RhsLanes
     from paper_1801_03589_b200.plan import NesaPlan
     n = 200_000
     spec = nesa.CurveSpec(kind="ellipse-plates", seed=4)
@@ -91,20 +92,25 @@ def c5(a):
         tree = nesa.build_tree(pts, nesa.TreeParams(P=P))
         for Q in (24, 48, 96):
             plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=Q)), dtype="f32")
-            for _ in range(3):
-                plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = max(3, a.reps // 20)
-            e0.record(st)
-            for _ in range(reps):
-                plan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
-            e1.record(st)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / reps
             rec = {"config": "C5", "N": n, "P": P, "Q": Q, "rhs": 64, "levels": tree.L - tree.l0 + 1,
-                   "plan": "f32", "ms_per_64rhs_product": round(ms, 3),
-                   "rhs_products_per_s": round(64e3 / ms, 1)}
+                   "plan": "f32"}
+            lanes = RhsLanes(plan, 4)
+            for tag, eng in (("one_plan", plan), ("lanes4", lanes)):
+                for _ in range(3):
+                    eng.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = max(3, a.reps // 20)
+                e0.record(st)
+                for _ in range(reps):
+                    eng.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
+                e1.record(st)
+                e1.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                rec[f"ms_per_64rhs_product_{tag}"] = round(ms, 3)
+                rec[f"rhs_products_per_s_{tag}"] = round(64e3 / ms, 1)
             print(json.dumps(rec), flush=True)
+            for p_ in lanes.plans[1:]:
+                p_.close()
             plan.close()
 
 
