@@ -212,6 +212,25 @@ int64_t nesa_ktrace_read(nesa_plan* plan, unsigned long long* out, int64_t max_r
 int nesa_dense_matvec(const double* points_dev, const double* q_dev, double* phi_dev, int64_t n,
                       int32_t ncols, void* stream);
 
+/* Native bit-exact quadtree build (reference: build_tree + _fill_lists,
+ * quadtree.py:123-245).  points: (n, 2) row-major HOST doubles.  Returns 0,
+ * 1 for invalid input (the reference's ValueError; text in
+ * nesa_tree_error) or 2; *out is set in every case and must be freed.
+ * nesa_tree_size(what): 0 groups, 1 leaves, 2 neighbor entries,
+ * 3 interaction entries, 4 l0, 5 L, 6 points.  nesa_tree_copy(field, dst)
+ * copies one array into caller memory: 0 level (int32), 1 ix, 2 iy,
+ * 3 start, 4 stop, 5 parent, 6 child_first, 7 n_children (int64, per group),
+ * 8 box (double, groups x 4), 9 level_first, 10 level_count (int64, index
+ * level - l0), 11 nbr_ptr, 12 nbr_idx, 13 int_ptr, 14 int_idx, 15 perm
+ * (int64), 16 origin x, origin y, side (3 doubles). */
+typedef struct nesa_tree nesa_tree;
+int nesa_tree_build(const double* points, int64_t n, double P, int32_t l0_groups_longest,
+                    nesa_tree** out);
+const char* nesa_tree_error(nesa_tree* tree);
+int64_t nesa_tree_size(nesa_tree* tree, int32_t what);
+int nesa_tree_copy(nesa_tree* tree, int32_t field, void* dst);
+void nesa_tree_free(nesa_tree* tree);
+
 #ifdef __cplusplus
 }
 #endif

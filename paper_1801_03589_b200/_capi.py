@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "nesa_plan_destroy", "nesa_last_error", "nesa_abi_version", "nesa_plan_stat",
     "nesa_profile_reset", "nesa_profile_read", "nesa_trace_read", "nesa_trace_name",
     "nesa_ktrace_enable", "nesa_ktrace_read", "nesa_dense_matvec", "nesa_matvec_cols",
+    "nesa_tree_build", "nesa_tree_error", "nesa_tree_size", "nesa_tree_copy", "nesa_tree_free",
 )
 
 _p = ctypes.c_void_p
@@ -114,6 +115,17 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_matvec_cols.argtypes = [_p, _p, _p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                      ctypes.c_uint32, _p]
     lib.nesa_matvec_cols.restype = ctypes.c_int
+    lib.nesa_tree_build.argtypes = [_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_void_p)]
+    lib.nesa_tree_build.restype = ctypes.c_int
+    lib.nesa_tree_error.argtypes = [_p]
+    lib.nesa_tree_error.restype = ctypes.c_char_p
+    lib.nesa_tree_size.argtypes = [_p, ctypes.c_int32]
+    lib.nesa_tree_size.restype = ctypes.c_int64
+    lib.nesa_tree_copy.argtypes = [_p, ctypes.c_int32, _p]
+    lib.nesa_tree_copy.restype = ctypes.c_int
+    lib.nesa_tree_free.argtypes = [_p]
+    lib.nesa_tree_free.restype = None
     if lib.nesa_abi_version() != NESA_ABI_VERSION:
         raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
     _lib = lib

@@ -231,9 +231,74 @@ def _sorted_rows_to_csr(cand: np.ndarray):
     return ptr, idx
 
 
-def build_tree(points: np.ndarray, params: TreeParams) -> Tree:
-    """Build the quadtree and its lists (quadtree.py:123-205)."""
+def _build_tree_native(points: np.ndarray, params: TreeParams):
+    """The same build in C++ (csrc/nesa_tree.cpp via the C ABI); None when
+    the library is not built.  Bit-identical arrays (tests/test_host_tree.py)."""
+    import ctypes
+    try:
+        from . import _capi
+        lib = _capi.load()
+    except (OSError, RuntimeError):
+        return None
+    n = points.shape[0]
+    h = ctypes.c_void_p()
+    rc = lib.nesa_tree_build(points.ctypes.data, n, float(params.P), int(params.l0_groups_longest),
+                             ctypes.byref(h))
+    try:
+        if rc != 0:
+            msg = lib.nesa_tree_error(h).decode()
+            if rc == 1:
+                raise ValueError(msg)
+            raise RuntimeError(msg)
+        size = lambda w: int(lib.nesa_tree_size(h, w))  # noqa: E731
+        G, NL, nn, ni, l0, L = (size(w) for w in range(6))
+
+        def get(field, count, dtype, shape=None):
+            out = np.empty(count, dtype)
+            if count:
+                lib.nesa_tree_copy(h, field, out.ctypes.data)
+            return out if shape is None else out.reshape(shape)
+
+        nlev = L - l0 + 1
+        lf = get(9, nlev, np.int64)
+        lc = get(10, nlev, np.int64)
+        geo = get(16, 3, np.float64)
+        arrays = TreeArrays(level=get(0, G, np.int32), ix=get(1, G, np.int64), iy=get(2, G, np.int64),
+                            start=get(3, G, np.int64), stop=get(4, G, np.int64),
+                            parent=get(5, G, np.int64), child_first=get(6, G, np.int64),
+                            n_children=get(7, G, np.int64), box=get(8, 4 * G, np.float64, (G, 4)),
+                            level_first={l0 + i: int(lf[i]) for i in range(nlev)},
+                            level_count={l0 + i: int(lc[i]) for i in range(nlev)},
+                            nbr_ptr=get(11, NL + 1, np.int64), nbr_idx=get(12, nn, np.int64),
+                            int_ptr=get(13, G + 1, np.int64), int_idx=get(14, ni, np.int64))
+        perm = get(15, n, np.int64)
+    finally:
+        lib.nesa_tree_free(h)
+    return Tree(params=params, l0=l0, L=L, root_origin=(float(geo[0]), float(geo[1])),
+                root_side=float(geo[2]), arrays=arrays, perm=perm, points=points[perm])
+
+
+def build_tree(points: np.ndarray, params: TreeParams, native: bool | None = None) -> Tree:
+    """Build the quadtree and its lists (quadtree.py:123-205).
+
+    ``native`` (default: the C++ build when the library is built,
+    NESA_TREE_NATIVE=0 forces numpy) selects csrc/nesa_tree.cpp; both give
+    bit-identical trees.
+    """
+    import os
     points = np.ascontiguousarray(points, dtype=float)
+    if points.ndim != 2 or points.shape[1] != 2 or points.shape[0] == 0:
+        raise ValueError("points must be a nonempty (n, 2) array")
+    if native is None:
+        native = os.environ.get("NESA_TREE_NATIVE", "1") != "0"
+    if native:
+        t = _build_tree_native(points, params)
+        if t is not None:
+            return t
+    return _build_tree_numpy(points, params)
+
+
+def _build_tree_numpy(points: np.ndarray, params: TreeParams) -> Tree:
     n = points.shape[0]
     if n < params.l0_groups_longest:
         raise ValueError("too few points for the coarsest level")

@@ -124,3 +124,37 @@ def test_reference_tree_adapter_roundtrip():
     for f in ("level", "ix", "iy", "start", "stop", "parent", "child_first", "n_children",
               "box", "nbr_ptr", "nbr_idx", "int_ptr", "int_idx"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+@pytest.mark.parametrize("spec,n,P", [
+    (geo.CurveSpec(), 1500, 40),
+    (geo.CurveSpec(kind="circle-random", seed=1), 20000, 32),
+    (geo.CurveSpec(kind="ellipse-plates", seed=2), 200000, 48),
+    (geo.CurveSpec(kind="circle", seed=3), 5000, 20),
+])
+def test_native_tree_build_bit_identical_to_numpy(spec, n, P):
+    # csrc/nesa_tree.cpp (the C++ build, default) against the numpy restatement
+    from oracle.gen_golden import tree_arrays as ta
+    pts = geo.generate_sources(spec, n)
+    a = build_tree(pts, TreeParams(P=P), native=True)
+    b = build_tree(pts, TreeParams(P=P), native=False)
+    A, B = ta(a), ta(b)
+    assert set(A) == set(B)
+    for k in B:
+        assert np.array_equal(A[k], B[k]), k
+    assert (a.l0, a.L, a.root_side, a.root_origin) == (b.l0, b.L, b.root_side, b.root_origin)
+    assert np.array_equal(a.points, b.points)
+
+
+@pytest.mark.parametrize("native", [True, False])
+def test_tree_build_errors(native):
+    pts = geo.generate_sources(geo.CurveSpec(), 500)
+    dup = pts.copy()
+    dup[3] = dup[100]
+    with pytest.raises(ValueError, match="distinct"):
+        build_tree(dup, TreeParams(P=20), native=native)
+    with pytest.raises(ValueError):
+        build_tree(pts[:3], TreeParams(P=2, l0_groups_longest=4), native=native)
+    same = np.zeros((4, 2))
+    with pytest.raises(ValueError):
+        build_tree(same, TreeParams(P=1), native=native)
