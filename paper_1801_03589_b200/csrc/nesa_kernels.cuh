@@ -2785,9 +2785,27 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
         for (int l = 0; l < LW; ++l)
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) acc[h][l][rr] = 0.f;
-      for (int m = 1; m < nm; ++m) {
-        const float2 a0 = h0 ? __ldg(A + m * Q + k0) : make_float2(0.f, 0.f);
-        const float2 a1 = h1 ? __ldg(A + m * Q + k1) : make_float2(0.f, 0.f);
+      // A rows prefetched PF steps ahead (the A-apply was stalled on these
+      // L1/L2 loads: ncu long-scoreboard at the first use)
+      constexpr int PF = 4;
+      float2 ap0[PF], ap1[PF];
+#pragma unroll
+      for (int i = 0; i < PF; ++i) {
+        const int mm = 1 + i;
+        ap0[i] = (h0 && mm < nm) ? __ldg(A + mm * Q + k0) : make_float2(0.f, 0.f);
+        ap1[i] = (h1 && mm < nm) ? __ldg(A + mm * Q + k1) : make_float2(0.f, 0.f);
+      }
+      for (int mb = 1; mb < nm; mb += PF) {
+#pragma unroll
+        for (int i = 0; i < PF; ++i) {
+        const int m = mb + i;
+        if (m >= nm) break;
+        const float2 a0 = ap0[i], a1 = ap1[i];
+        {
+          const int mn = m + PF;
+          ap0[i] = (h0 && mn < nm) ? __ldg(A + mn * Q + k0) : make_float2(0.f, 0.f);
+          ap1[i] = (h1 && mn < nm) ? __ldg(A + mn * Q + k1) : make_float2(0.f, 0.f);
+        }
 #pragma unroll
         for (int l = 0; l < LW; ++l) {
           // mu_m: re[R] then im[R]
@@ -2818,6 +2836,7 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
               acc[1][l][rr] = fmaf(a1.x, ur[rr], fmaf(-a1.y, ui[rr], acc[1][l][rr]));
             }
           }
+        }
         }
       }
       const float f0 = h0 ? __ldg(A + k0).x : 0.f, f1 = h1 ? __ldg(A + k1).x : 0.f;
