@@ -469,6 +469,27 @@ __global__ void gather_kernel(const T* __restrict__ q, const int64_t* __restrict
   }
 }
 
+// qt[iperm[j]] = q[j]: the same gather walked in the original order --
+// coalesced reads of q and iperm, scattered 8-byte writes that merge in L2
+// (random 8-byte reads would each fetch a whole sector from DRAM)
+template <typename T, int R>
+__global__ void gather_inv_kernel(const T* __restrict__ q, const int32_t* __restrict__ iperm,
+                                  T* __restrict__ qt, int64_t n, int ldq) {
+  KtScope kt_(3);
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
+       j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = iperm[j];
+    if constexpr (R == 2 && sizeof(T) == 4) {
+      const float2 v = ldq == 2 ? *reinterpret_cast<const float2*>(q + j * 2)
+                                : make_float2(q[j * ldq], q[j * ldq + 1]);
+      *reinterpret_cast<float2*>(qt + i * 2) = v;
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) qt[i * R + rr] = q[j * ldq + rr];
+    }
+  }
+}
+
 // phi[perm[i]] = phin[i] + phif[i] (a null term is zero), phi rows of stride ldp
 template <typename T, int R>
 __global__ void scatter_kernel(const T* __restrict__ phin, const T* __restrict__ phif,
@@ -2630,7 +2651,12 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
-    int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0, int bufpts = kMomBufPts) {
+    int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0, int bufpts = kMomBufPts,
+    const int64_t* __restrict__ qperm = nullptr) {
+  // qperm != null: qt is q in the ORIGINAL order (row stride R) and point
+  // b's charges are qt[qperm[b]] -- the gather into tree order is then off
+  // the far chain's critical path (it runs beside this kernel for the near
+  // field only)
   KtScope kt_(60 + int(MU_OUT));
   constexpr int MP = MPX > 0 ? MPX : 40 / R;  // moments per pass
   constexpr int NV = 2 * R * MP;       // 80 accumulators
@@ -2655,7 +2681,8 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
     if (np > bufpts) return false;
     for (int t = lane; t < np; t += 32) {
       cp_async<8>(Pb + t, prel + b0 + t);
-      cp_async_n<R * 4>(Qb + t * R, qt + (b0 + t) * R);
+      const int64_t src = qperm ? qperm[b0 + t] : b0 + t;
+      cp_async_n<R * 4>(Qb + t * R, qt + src * R);
     }
     cp_async_commit();
     return true;
@@ -2688,7 +2715,7 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
         } else {
           p = prel[b + j];
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(b + j) * R + rr];
+          for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(qperm ? qperm[b + j] : b + j) * R + rr];
         }
         const float2 w = make_float2(p.x * inv, p.y * inv);
         // two interleaved power chains (even / odd terms, each stepping by w^2)

@@ -307,6 +307,8 @@ struct nesa_plan {
   std::vector<int64_t> loc_first, loc_count;  // local (ancestors of local leaves)
 
   DevBuf<int64_t> perm;        // [N]
+  DevBuf<int32_t> iperm;       // [N] original index -> tree index
+  bool gather_inv = true;      // gather walked in the original order (gather_inv_kernel; ~same time)
   DevBuf<int32_t> quad;        // [G]
   DevBuf<int64_t> parent;      // [G]
   DevBuf<int64_t> child_first; // [G]
@@ -408,6 +410,9 @@ struct nesa_plan {
   cudaStream_t s2 = nullptr;                 // fine-level translation branch
   cudaStream_t s3 = nullptr;                 // second near-field launch (near_split)
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+  cudaEvent_t ev_gfork = nullptr;           // gather on the near stream (rad_direct)
+  bool rad_direct = false;                  // radiation reads q through perm (see enqueue_T;
+                                            // measured slower: 556 vs 539 us, random q reads)
   int near_split = 0;                        // far-pass hook position of the 2nd near launch (0: one
                                              // launch; measured slower: half the CTAs stream at
                                              // about half the bandwidth)
@@ -469,6 +474,7 @@ struct nesa_plan {
     if (s2) cudaStreamDestroy(s2);
     if (s3) cudaStreamDestroy(s3);
     if (ev_fork2) cudaEventDestroy(ev_fork2);
+    if (ev_gfork) cudaEventDestroy(ev_gfork);
     for (auto e : ev_lv)
       if (e) cudaEventDestroy(e);
     if (ev_join2) cudaEventDestroy(ev_join2);
@@ -526,6 +532,14 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     std::vector<int64_t> perm(d->perm, d->perm + P->N);  // full: near halo columns
     for (auto v : perm) require(v >= 0 && v < P->N, "perm out of range");
     P->perm.upload(perm);
+    {
+      std::vector<int32_t> iperm(P->N, -1);
+      for (int64_t i = 0; i < P->N; ++i) {
+        require(iperm[perm[i]] < 0, "perm is not a permutation");
+        iperm[perm[i]] = int32_t(i);
+      }
+      P->iperm.upload(iperm);
+    }
     std::vector<int32_t> quad(d->quad, d->quad + G);
     P->quad.upload(quad);
     std::vector<int64_t> parent(d->parent, d->parent + G);
@@ -1346,7 +1360,8 @@ constexpr int kMomCtasPerSM = 4;
 
 // s = V qt: outgoing moments (float32 plans from geometry) or stored V
 template <typename T, int R>
-int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
+int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st,
+                     const int64_t* qperm = nullptr) {
   if constexpr (std::is_same<T, float>::value) {
     if (P->v_mom) {
       const int64_t nleaf = P->leaf_end - P->leaf_begin;
@@ -1384,7 +1399,7 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
       auto go = [&](auto kern) {
         kern<<<grid, 32 * kExpWarps, sm, st>>>(P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p,
                                                 P->mom_A.p, qt, s, P->leaf_begin, nleaf, P->Q, P->v_nm, 0,
-                                                bufpts);
+                                                bufpts, qperm);
       };
       switch (P->mom_variant) {
         case 1: go(radiation_mom_kernel<R>); break;
@@ -1759,7 +1774,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       if (!fused || lv > P->fused_lf) down_level(lv);
   };
   auto gather = [&]() {
-    gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N, P->ldv);
+    if (P->gather_inv)
+      gather_inv_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->iperm.p, qt, P->N, P->ldv);
+    else
+      gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N, P->ldv);
     nk++;
     tr("gather", s0);
   };
@@ -1836,11 +1854,25 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_join2, 0));
       prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, P->s3);
     };
-    gather();
+    // float32 moment radiation reading q in the original order: the gather
+    // (only the near field needs tree-ordered q) moves to the near stream
+    const bool rad_direct = std::is_same<T, float>::value && far && near && P->v_mom && P->rad_direct &&
+                            P->near_after == 0 && !nsplit && P->ldv == R && P->mom_kt == 0;
+    if (rad_direct) {
+      CUDA_OK(cudaEventRecord(P->ev_gfork, s0));
+      CUDA_OK(cudaStreamWaitEvent(s1, P->ev_gfork, 0));
+      if (P->gather_inv)
+        gather_inv_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s1>>>(q, P->iperm.p, qt, P->N, P->ldv);
+      else
+        gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s1>>>(q, P->perm.p, qt, P->N, P->ldv);
+      nk++;
+    } else {
+      gather();
+    }
     if (far && P->near_after < 0) launch_near();
     if (far) {
       prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
-      nk += launch_radiation<T, R>(P, qt, s, s0);
+      nk += rad_direct ? launch_radiation<T, R>(P, q, s, s0, P->perm.p) : launch_radiation<T, R>(P, qt, s, s0);
       tr("radiation", s0);
     }
     if (!far || P->near_after <= 1) launch_near();
@@ -2106,6 +2138,8 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* ct = std::getenv("NESA_COARSE_TC")) P->coarse_tc = std::atoi(ct);
     if (const char* tm = std::getenv("NESA_TC3_MINB")) P->tc3_minb = std::atoi(tm);
     if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
+    if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
+    if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;
     if (const char* pc = std::getenv("NESA_PAT_CTAS")) P->pat_ctas = std::max(1, std::atoi(pc));
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
@@ -2152,6 +2186,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       CUDA_OK(cudaStreamCreateWithPriority(&P->s3, cudaStreamNonBlocking, lo));
     }
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork2, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_gfork, cudaEventDisableTiming));
     P->ev_lv.assign(size_t(P->L - P->l0 + 1), nullptr);
     for (auto& e : P->ev_lv) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join2, cudaEventDisableTiming));
