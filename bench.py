@@ -51,7 +51,7 @@ def workload_config(n=N_POINTS, world=1):
         "N": n, "P": LEAF_P, "Q": Q_AUX, "geometry": "ellipse-plates", "seed": SEED,
         "vectors": "complex64", "operators": "float32",
         "parallelism": f"morton-partition x{world}" if world > 1 else "single-gpu",
-        "l2": "no flush needed: each step streams ~3.3 GB of operators (> 126 MB L2)",
+        "l2": "no flush needed: each step streams the 2.13 GB near-field operator (> 126 MB L2)",
     }
 
 
