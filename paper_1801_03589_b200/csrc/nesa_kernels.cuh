@@ -888,6 +888,7 @@ struct FusedArgs {
   T* o;
   int64_t first, count;   // level-lf groups (local)
   int lf, l0, L, Q, D;
+  int spec;               // up: prefetch the parent's matrix before the arrival count
 };
 
 __device__ __forceinline__ int ld_acquire_s32(const int* p) {
@@ -956,13 +957,20 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
     __syncthreads();  // T[g] written, M and X consumed
     if (tid == 0) {
       const int64_t p = a.parent[g];
+      // the parent's matrix, fetched before knowing whether this CTA is the
+      // last child (a.spec): the continuing CTA then finds it in flight
+      // instead of paying one more round trip on the chain
+      const bool spec = a.spec && lv - 1 > a.l0;
+      if (spec) load_mat(lv - 1, p);
       __threadfence();
       const int old = atomicAdd(a.cnt + p, 1);
       const bool last = old == a.uchild[p].y - 1;
       if (last) {
         a.cnt[p] = 0;
         __threadfence();
-        if (lv - 1 > a.l0) load_mat(lv - 1, p);
+        if (!spec && lv - 1 > a.l0) load_mat(lv - 1, p);
+      } else if (spec) {
+        mbar_wait(bar, phase);  // no bulk copy may outlive the CTA
       }
       *nxt = last ? p : -1;
     }

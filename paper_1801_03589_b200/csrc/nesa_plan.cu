@@ -420,6 +420,7 @@ struct nesa_plan {
   cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
+  bool fused_spec = false;                   // fused up: speculative parent-matrix prefetch (neutral)
   int tc3_minb = 0;                          // tgemm_tc3 register budget (3: <= 168 registers)
   int coarse_tc = 1;                         // coarse translation: 0 FFMA, 1 as fine, 2 one CTA per unit
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
@@ -1661,6 +1662,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     fa.L = P->L;
     fa.Q = Q;
     fa.D = P->fused_lf - P->l0 - 1;
+    fa.spec = P->fused_spec ? 1 : 0;
     return fa;
   };
   const bool fused = P->fused_lf > P->l0;
@@ -2140,6 +2142,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
     if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
     if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;
+    if (const char* fs = std::getenv("NESA_FUSED_SPEC")) P->fused_spec = std::atoi(fs) != 0;
     if (const char* pc = std::getenv("NESA_PAT_CTAS")) P->pat_ctas = std::max(1, std::atoi(pc));
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
