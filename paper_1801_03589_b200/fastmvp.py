@@ -137,7 +137,9 @@ def get_lanes(tree, ops, dtype: str = "f64", device: int = 0, lanes: int | None 
     """Cached RhsLanes for (tree, ops, dtype, device); lane 0 is get_plan's."""
     import os
     if lanes is None:
-        lanes = max(1, int(os.environ.get("NESA_RHS_LANES", "4")))
+        # C5 (200k points, 64 plane waves): 1 / 2 / 4 / 8 / 16 lanes ->
+        # 10.5 / 8.9 / 6.0 / 5.1 / 5.0 ms (tools/lanes_sweep.py)
+        lanes = max(1, int(os.environ.get("NESA_RHS_LANES", "8")))
     plan = get_plan(tree, ops, dtype=dtype, device=device)
     ent = getattr(plan, "_lanes", None)
     if ent is None or len(ent.plans) != lanes:
