@@ -212,6 +212,20 @@ int64_t nesa_ktrace_read(nesa_plan* plan, unsigned long long* out, int64_t max_r
 int nesa_dense_matvec(const double* points_dev, const double* q_dev, double* phi_dev, int64_t n,
                       int32_t ncols, void* stream);
 
+/* Multi-GPU halo exchange of partial source amplitudes (
+ * the reference has no distributed layer).  Device pointers; s is the
+ * (G, qr) amplitude block of nesa_plan_s_dev.  pack: send[r] =
+ * s[export_ids[r]] for r < n_export, zero rows up to send_rows.  combine:
+ * for each imported group i, s[import_ids[i]] = sum over k of row
+ * contrib[i][k] (k ascending, -1 = none) of [recv rows | s rows], a row
+ * c < n_recv_rows reading recv[c], c >= n_recv_rows reading s[c - n_recv_rows]
+ * (only the group's own row).  Stream-ordered, no synchronisation. */
+int nesa_exchange_pack(const void* s_dev, const int64_t* export_ids_dev, int64_t n_export,
+                       int64_t send_rows, int32_t qr, int32_t is_f64, void* send_dev, void* stream);
+int nesa_exchange_combine(void* s_dev, const void* recv_dev, const int64_t* import_ids_dev,
+                          const int64_t* contrib_dev, int64_t n_import, int32_t max_contrib,
+                          int64_t n_recv_rows, int32_t qr, int32_t is_f64, void* stream);
+
 /* Native bit-exact quadtree build (reference: build_tree + _fill_lists,
  * quadtree.py:123-245).  points: (n, 2) row-major HOST doubles.  Returns 0,
  * 1 for invalid input (the reference's ValueError; text in

@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "nesa_profile_reset", "nesa_profile_read", "nesa_trace_read", "nesa_trace_name",
     "nesa_ktrace_enable", "nesa_ktrace_read", "nesa_dense_matvec", "nesa_matvec_cols",
     "nesa_tree_build", "nesa_tree_error", "nesa_tree_size", "nesa_tree_copy", "nesa_tree_free",
+    "nesa_exchange_pack", "nesa_exchange_combine",
 )
 
 _p = ctypes.c_void_p
@@ -126,6 +127,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_tree_copy.restype = ctypes.c_int
     lib.nesa_tree_free.argtypes = [_p]
     lib.nesa_tree_free.restype = None
+    lib.nesa_exchange_pack.argtypes = [_p, _p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                       ctypes.c_int32, _p, _p]
+    lib.nesa_exchange_pack.restype = ctypes.c_int
+    lib.nesa_exchange_combine.argtypes = [_p, _p, _p, _p, ctypes.c_int64, ctypes.c_int32,
+                                          ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _p]
+    lib.nesa_exchange_combine.restype = ctypes.c_int
     if lib.nesa_abi_version() != NESA_ABI_VERSION:
         raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
     _lib = lib

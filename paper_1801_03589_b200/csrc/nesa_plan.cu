@@ -2350,6 +2350,87 @@ NESA_API int nesa_dense_matvec(const double* points_dev, const double* q_dev, do
   NESA_GUARD(return dense_run(points_dev, q_dev, phi_dev, n, ncols, stream));
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU halo exchange (paper_1801_03589_b200/dist.py):
+// pack this rank's partial source amplitudes that other ranks need into the
+// all_gather send buffer, and complete the needed groups' amplitudes as the
+// rank-ordered sum of their contributors' partials (contrib rows < n_recv
+// index the gathered buffer, rows >= n_recv this rank's own s[row - n_recv]).
+// One kernel each instead of a dozen torch ops per product.
+// ---------------------------------------------------------------------------
+namespace {
+template <typename T>
+__global__ void xpack_kernel(const T* __restrict__ s, const int64_t* __restrict__ ids, int64_t n_ids,
+                             int64_t rows, int qr, T* __restrict__ send) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < rows * qr;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = t / qr, w = t - r * qr;
+    send[t] = r < n_ids ? s[ids[r] * qr + w] : T(0);
+  }
+}
+
+template <typename T>
+__global__ void xcombine_kernel(T* s, const T* __restrict__ recv, const int64_t* __restrict__ imp,
+                                const int64_t* __restrict__ contrib, int64_t n_imp, int max_c,
+                                int64_t n_recv, int qr) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_imp * qr;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / qr, w = t - i * qr;
+    T acc = T(0);
+    for (int k = 0; k < max_c; ++k) {  // fixed rank order: deterministic
+      const int64_t c = contrib[i * max_c + k];
+      if (c < 0) continue;
+      acc += c < n_recv ? recv[c * qr + w] : s[(c - n_recv) * qr + w];
+    }
+    s[imp[i] * qr + w] = acc;  // the only local row read is imp[i]'s own
+  }
+}
+
+int xpack_run(const void* s, const int64_t* ids, int64_t n_ids, int64_t rows, int32_t qr, int32_t f64,
+              void* send, void* stream) {
+  require(s && send && (ids || n_ids == 0) && rows >= n_ids && qr > 0, "bad exchange pack arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>((rows * qr + 255) / 256, 4096)));
+  if (f64)
+    xpack_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(s), ids, n_ids, rows, qr,
+                                               static_cast<double*>(send));
+  else
+    xpack_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(s), ids, n_ids, rows, qr,
+                                              static_cast<float*>(send));
+  CUDA_OK(cudaGetLastError());
+  return NESA_OK;
+}
+
+int xcombine_run(void* s, const void* recv, const int64_t* imp, const int64_t* contrib, int64_t n_imp,
+                 int32_t max_c, int64_t n_recv, int32_t qr, int32_t f64, void* stream) {
+  require(s && recv && qr > 0 && max_c >= 1 && (n_imp == 0 || (imp && contrib)), "bad exchange combine arguments");
+  if (n_imp == 0) return NESA_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>((n_imp * qr + 255) / 256, 4096)));
+  if (f64)
+    xcombine_kernel<double><<<grid, 256, 0, st>>>(static_cast<double*>(s), static_cast<const double*>(recv),
+                                                  imp, contrib, n_imp, max_c, n_recv, qr);
+  else
+    xcombine_kernel<float><<<grid, 256, 0, st>>>(static_cast<float*>(s), static_cast<const float*>(recv),
+                                                 imp, contrib, n_imp, max_c, n_recv, qr);
+  CUDA_OK(cudaGetLastError());
+  return NESA_OK;
+}
+}  // namespace
+
+NESA_API int nesa_exchange_pack(const void* s_dev, const int64_t* export_ids_dev, int64_t n_export,
+                                int64_t send_rows, int32_t qr, int32_t is_f64, void* send_dev,
+                                void* stream) {
+  NESA_GUARD(return xpack_run(s_dev, export_ids_dev, n_export, send_rows, qr, is_f64, send_dev, stream));
+}
+
+NESA_API int nesa_exchange_combine(void* s_dev, const void* recv_dev, const int64_t* import_ids_dev,
+                                   const int64_t* contrib_dev, int64_t n_import, int32_t max_contrib,
+                                   int64_t n_recv_rows, int32_t qr, int32_t is_f64, void* stream) {
+  NESA_GUARD(return xcombine_run(s_dev, recv_dev, import_ids_dev, contrib_dev, n_import, max_contrib,
+                                 n_recv_rows, qr, is_f64, stream));
+}
+
 NESA_API const char* nesa_last_error(void) { return g_last_error.c_str(); }
 
 NESA_API int nesa_abi_version(void) { return NESA_ABI_VERSION; }

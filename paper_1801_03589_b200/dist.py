@@ -134,10 +134,23 @@ def build_exchange(tree: Tree, ranges: list[tuple[int, int]], rank: int) -> Exch
                         contrib=contrib, n_recv_rows=world * max_export)
 
 
+def _native(s) -> bool:
+    return s.is_cuda and s.dtype in (__import__("torch").float32, __import__("torch").float64)
+
+
 def pack_s(s, xp: ExchangePlan, tensors):
-    """This rank's send buffer (max_export, Q*R): its partials others need."""
+    """This rank's send buffer (max_export, Q*R): its partials others need.
+    CUDA: one kernel (nesa_exchange_pack); CPU (gloo tests): torch ops."""
     import torch
     exp_ids = tensors[0]
+    if _native(s):
+        from . import _capi
+        send = torch.empty((xp.max_export, s.shape[1]), dtype=s.dtype, device=s.device)
+        _capi.check(_capi.load().nesa_exchange_pack(
+            s.data_ptr(), exp_ids.data_ptr() if exp_ids.numel() else None, exp_ids.numel(),
+            xp.max_export, s.shape[1], int(s.dtype == torch.float64), send.data_ptr(),
+            torch.cuda.current_stream(s.device).cuda_stream))
+        return send
     send = torch.zeros((xp.max_export, s.shape[1]), dtype=s.dtype, device=s.device)
     if exp_ids.numel():
         send[:exp_ids.numel()] = s.index_select(0, exp_ids)
@@ -149,6 +162,13 @@ def combine_s(s, xp: ExchangePlan, recv, tensors) -> None:
     import torch
     _, imp_ids, contrib = tensors
     if imp_ids.numel() == 0:
+        return
+    if _native(s):
+        from . import _capi
+        _capi.check(_capi.load().nesa_exchange_combine(
+            s.data_ptr(), recv.data_ptr(), imp_ids.data_ptr(), contrib.data_ptr(), imp_ids.numel(),
+            contrib.shape[1], recv.shape[0], s.shape[1], int(s.dtype == torch.float64),
+            torch.cuda.current_stream(s.device).cuda_stream))
         return
     pool = torch.cat((recv, s), 0)                      # rows: recv | local s (all G)
     acc = torch.zeros((imp_ids.numel(), s.shape[1]), dtype=s.dtype, device=s.device)

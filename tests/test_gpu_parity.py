@@ -461,3 +461,33 @@ def test_rhs_lanes_bitwise_and_vs_oracle(dtype, cdt):
     for p in lanes.plans[1:]:
         p.close()
     plan.close()
+
+
+@pytest.mark.parametrize("tdt", ["float32", "float64"])
+def test_exchange_kernels_match_torch_ops(tdt):
+    # nesa_exchange_pack / _combine (CUDA) bitwise against the torch-op
+    # version the gloo tests run on CPU
+    from paper_1801_03589_b200.dist import (build_exchange, combine_s, exchange_tensors, pack_s,
+                                            partition_leaves)
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=2), 20000)
+    tree = build_tree(pts, TreeParams(P=32))
+    world = 4
+    ranges = partition_leaves(tree, world, 24)
+    G = tree.arrays.n_groups
+    dt = getattr(torch, tdt)
+    gen = torch.Generator().manual_seed(3)
+    s_cpu = [torch.randn((G, 48), generator=gen, dtype=dt) for _ in range(world)]
+    xps = [build_exchange(tree, ranges, r) for r in range(world)]
+    outs = {}
+    for dev in ("cpu", "cuda"):
+        ss = [x.clone().to(dev) for x in s_cpu]
+        tens = [exchange_tensors(xp, ss[0].device) for xp in xps]
+        sends = [pack_s(ss[r], xps[r], tens[r]) for r in range(world)]
+        recv = torch.cat(sends, 0)
+        for r in range(world):
+            combine_s(ss[r], xps[r], recv, tens[r])
+        outs[dev] = ([x.cpu() for x in sends], [x.cpu() for x in ss])
+    for a, b in zip(outs["cpu"][0], outs["cuda"][0]):
+        assert torch.equal(a, b)
+    for a, b in zip(outs["cpu"][1], outs["cuda"][1]):
+        assert torch.equal(a, b)
