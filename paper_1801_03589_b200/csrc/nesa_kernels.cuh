@@ -1043,6 +1043,245 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
 }
 
 // s[c] = sum_k T[first child + k] for the coarsest level (no transfer above).
+// ----------------------------------------------------------------------------
+// Coarse far field in ONE persistent kernel: the upward pass of the coarse
+// levels (fused_up_kernel's last-arriver chains), their translation sums
+// o_x = sum_e D_e s_src(e) (operators.py:225-239; fastmvp.py:163-166) and the
+// downward pass (fused_down_kernel's claim chains), scheduled from a device
+// work queue instead of four kernel launches.  The paper's task graph
+// on the GPU: items are claimed in dependency order
+// (up items, then translation targets coarse level by level from the finest,
+// then down items), and an item only waits on work that is already claimed
+// by a running CTA -- a level's completion counter, a target's epoch flag, an
+// ancestor's claim state -- so every wait ends even though CTAs are not all
+// co-resident.  Sums keep the reference order (children in order, entries in
+// interaction-list order), one writer per output: deterministic.
+// ----------------------------------------------------------------------------
+template <typename T>
+struct CoarseArgs {
+  FusedArgs<T> f;          // up: MT = C tables; anc / state / cnt / Tup / s / o / level lf range
+  const T* BT;             // B tables (same layout as C)
+  const T* DT;             // D tables (same layout), by D index
+  const int64_t* int_ptr;  // [G + 1] interaction CSR
+  const int32_t* e_src;    // [nnz] source group of entry e
+  const int32_t* e_dt;     // [nnz] D index of entry e
+  const int32_t* glevel;   // [G] level of each group
+  const int32_t* tq;       // translation items: coarse targets, level lf first ... l0 last
+  int64_t n_t;
+  const int32_t* lvl_count;  // [lf - l0 + 1] groups per coarse level (index lv - l0)
+  int* head;               // work queue head
+  int* lvl_done;           // [lf - l0 + 1] finalized amplitudes per level
+  int* tdone;              // [G] epoch of the written translation sum
+  int* ctl;                // [0] epoch, [1] exited CTAs, [2] wait-timeout flag
+};
+
+__device__ __forceinline__ void st_release_s32(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// spin (one thread) until *p reaches v (>= for counters); bounded
+__device__ __forceinline__ void coarse_wait_ge(const int* p, int v, int* err) {
+  for (long long it = 0; ld_acquire_s32(p) < v; ++it) {
+    if (it > (1ll << 24)) {  // ~seconds: give up instead of hanging the GPU
+      atomicExch(err, 1);
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+template <typename T>
+__host__ __device__ inline size_t coarse_smem_bytes(int Q, int R) {
+  return 2 * mat_bytes(Q, sizeof(T)) + 2 * ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 128;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const CoarseArgs<T> c) {
+  KtScope kt_(35);
+  const FusedArgs<T>& a = c.f;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
+  const size_t mb = mat_bytes(Q, sizeof(T));
+  const size_t xb = (size_t(QR) * sizeof(T) + 15) & ~size_t(15);
+  T* Mb[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem + mb)};
+  T* Xb[2] = {reinterpret_cast<T*>(smem + 2 * mb), reinterpret_cast<T*>(smem + 2 * mb + xb)};
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * mb + 2 * xb);  // [0], [1]: M buffers
+  int* sh = reinterpret_cast<int*>(bar + 2);                           // [0] item, [1] flag
+  int64_t* nxt = reinterpret_cast<int64_t*>(sh + 2);
+  const int n_lf = int(a.count);
+  const int n_items = 2 * n_lf + int(c.n_t);
+  const int ep = ld_acquire_s32(c.ctl) + 1;  // this launch's epoch
+  uint32_t ph[2] = {0u, 0u};
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();  // the finer levels' transfers are complete
+  auto load_m = [&](int b, const T* table, size_t idx) {  // one thread
+    mbar_arrive_expect_tx(&bar[b], uint32_t(mb));
+    bulk_g2s(Mb[b], table + idx * a.mstride, uint32_t(mb), &bar[b]);
+  };
+  auto wait_m = [&](int b) {
+    mbar_wait(&bar[b], ph[b]);
+    ph[b] ^= 1u;
+  };
+  // y[w] (w = k R + rr) = sum_j M[j Qp + k] X[j R + rr], one output per thread slot
+  auto gemv = [&](const T* M, const T* X, int w) {
+    const int k = w / R, rr = w - (w / R) * R;
+    T acc = T(0);
+#pragma unroll 8
+    for (int j = 0; j < Q; ++j) acc = fma(M[j * Qp + k], X[j * R + rr], acc);
+    return acc;
+  };
+  constexpr int NW = (64 * 4 + kFusedThreads - 1) / kFusedThreads;  // outputs per thread (QR <= 256)
+  for (;;) {
+    if (tid == 0) sh[0] = atomicAdd(c.head, 1);
+    __syncthreads();
+    const int item = sh[0];
+    __syncthreads();
+    if (item >= n_items) break;
+    if (item < n_lf) {
+      // ---------------- upward chain from a level-lf group (fused_up_kernel)
+      int64_t g = a.first + item;
+      int lv = a.lf;
+      if (tid == 0 && lv > a.l0) load_m(0, a.MT, size_t(lv - a.l0 - 1) * 4 + a.quad[g]);
+      while (true) {
+        if (tid == 0) a.state[g] = 0;  // claim state for the downward pass
+        const int2 uc = a.uchild[g];
+        T* X = Xb[0];
+        for (int w = tid; w < QR; w += kFusedThreads) {
+          T v;
+          if (lv == a.L) {
+            v = __ldcg(a.s + g * QR + w);
+          } else {
+            v = T(0);
+            for (int k = 0; k < uc.y; ++k) v += __ldcg(a.Tup + (int64_t(uc.x) + k) * QR + w);
+            a.s[g * QR + w] = v;
+          }
+          X[w] = v;
+        }
+        __syncthreads();  // s[g] written by every thread
+        if (tid == 0) {
+          __threadfence();
+          atomicAdd(c.lvl_done + (lv - a.l0), 1);  // s[g] final
+        }
+        if (lv == a.l0) break;
+        wait_m(0);
+        for (int w = tid; w < QR; w += kFusedThreads) a.Tup[g * QR + w] = gemv(Mb[0], X, w);
+        __syncthreads();  // T[g] written, M and X consumed
+        if (tid == 0) {
+          const int64_t p = a.parent[g];
+          __threadfence();
+          const int old = atomicAdd(a.cnt + p, 1);
+          const bool last = old == a.uchild[p].y - 1;
+          if (last) {
+            a.cnt[p] = 0;
+            __threadfence();
+            if (lv - 1 > a.l0) load_m(0, a.MT, size_t(lv - 1 - a.l0 - 1) * 4 + a.quad[p]);
+          }
+          *nxt = last ? p : -1;
+        }
+        __syncthreads();
+        const int64_t p = *nxt;
+        if (p < 0) break;
+        g = p;
+        --lv;
+      }
+    } else if (item < n_lf + c.n_t) {
+      // ---------------- translation sum of one coarse target
+      const int64_t x = c.tq[item - n_lf];
+      const int lv = c.glevel[x];
+      if (tid == 0) coarse_wait_ge(c.lvl_done + (lv - a.l0), c.lvl_count[lv - a.l0], c.ctl + 2);
+      __syncthreads();
+      const int64_t e0 = c.int_ptr[x], e1 = c.int_ptr[x + 1];
+      T acc[NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) acc[i] = T(0);
+      if (tid == 0 && e0 < e1) load_m(0, c.DT, size_t(c.e_dt[e0]));
+      for (int64_t e = e0; e < e1; ++e) {
+        const int b = int(e - e0) & 1;
+        // next entry's D into the other buffer (its last reader finished)
+        if (tid == 0 && e + 1 < e1) load_m(b ^ 1, c.DT, size_t(c.e_dt[e + 1]));
+        const int64_t src = c.e_src[e];
+        for (int w = tid; w < QR; w += kFusedThreads) Xb[b][w] = __ldcg(a.s + src * QR + w);
+        wait_m(b);
+        __syncthreads();
+        int i = 0;
+        for (int w = tid; w < QR; w += kFusedThreads, ++i) acc[i] += gemv(Mb[b], Xb[b], w);
+        __syncthreads();  // buffer b consumed
+      }
+      int i = 0;
+      for (int w = tid; w < QR; w += kFusedThreads, ++i) a.o[x * QR + w] = acc[i];
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release_s32(c.tdone + x, ep);
+      }
+    } else {
+      // ---------------- downward chain to one level-lf group (fused_down_kernel)
+      const int di = item - n_lf - int(c.n_t);
+      const int64_t g = a.first + di;
+      // every amplitude (and so every claim-state reset) is in place once
+      // the top level is complete
+      if (tid == 0) coarse_wait_ge(c.lvl_done, c.lvl_count[0], c.ctl + 2);
+      __syncthreads();
+      for (int i = a.D - 1; i >= -1; --i) {
+        const int64_t x = i >= 0 ? int64_t(a.anc[int64_t(di) * a.D + i]) : g;
+        const int lvx = a.lf - 1 - i;
+        if (i >= 0) {
+          if (tid == 0) {
+            int st = atomicCAS(a.state + x, 0, 1);
+            if (st == 1) {
+              coarse_wait_ge(a.state + x, 2, c.ctl + 2);
+              st = 2;
+            }
+            sh[1] = st;
+          }
+          __syncthreads();
+          const int fl = sh[1];
+          __syncthreads();
+          if (fl != 0) continue;  // finished by another CTA
+        }
+        const int64_t px = a.parent[x];
+        if (tid == 0) {
+          load_m(0, c.BT, size_t(lvx - a.l0 - 1) * 4 + a.quad[x]);
+          coarse_wait_ge(c.tdone + x, ep, c.ctl + 2);                      // o[x] = translation sum
+          if (lvx - 1 == a.l0) coarse_wait_ge(c.tdone + px, ep, c.ctl + 2);  // top parent: final
+        }
+        __syncthreads();
+        for (int w = tid; w < QR; w += kFusedThreads) Xb[0][w] = __ldcg(a.o + px * QR + w);
+        wait_m(0);
+        __syncthreads();
+        T res[NW];
+        int k = 0;
+        for (int w = tid; w < QR; w += kFusedThreads, ++k) res[k] = __ldcg(a.o + x * QR + w) + gemv(Mb[0], Xb[0], w);
+        __syncthreads();
+        k = 0;
+        for (int w = tid; w < QR; w += kFusedThreads, ++k) a.o[x * QR + w] = res[k];
+        __syncthreads();
+        if (i >= 0 && tid == 0) {
+          __threadfence();
+          atomicExch(a.state + x, 2);
+        }
+      }
+    }
+  }
+  // the last CTA out resets the queue for the next launch and publishes the epoch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(c.ctl + 1, 1) == int(gridDim.x) - 1) {
+      *c.head = 0;
+      for (int l = 0; l <= a.lf - a.l0; ++l) c.lvl_done[l] = 0;
+      c.ctl[1] = 0;
+      __threadfence();
+      st_release_s32(c.ctl, ep);
+    }
+  }
+}
+
 template <typename T, int R>
 __global__ void sum_children_kernel(const int64_t* __restrict__ child_first,
                                     const int32_t* __restrict__ n_child, int64_t first,

@@ -337,6 +337,14 @@ struct nesa_plan {
   DevBuf<int2> uchild;                      // [G] local children (first, count)
   DevBuf<int32_t> fused_anc;                // [count(lf)][lf - l0 - 1] ancestors
   DevBuf<int> fused_cnt, fused_state;       // [G] arrival counters / claim states
+  // coarse far field as one persistent kernel (coarse_kernel): coarse
+  // up + translation + down from a device work queue
+  bool coarse_mega = false;                 // (measured slower: items serialise inside CTAs)
+  int mega_ctas = 2;                        // persistent CTAs per SM
+  bool mega_ready = false;
+  DevBuf<int32_t> e_src, e_dt, glevel, mega_tq, mega_lcount;
+  DevBuf<int> mega_head, mega_ldone, mega_tdone, mega_ctl;
+  int64_t mega_nt = 0;
   int qs = 4;                               // quadrant slots staged per round
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
   int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
@@ -696,6 +704,37 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->fused_anc.upload(anc);
     P->fused_cnt.alloc(size_t(G));    // zero-filled
     P->fused_state.alloc(size_t(G));
+    if (P->coarse_mega && P->leaf_begin == 0 && P->leaf_end == P->NL) {
+      const int64_t nnz = d->int_ptr[G];
+      std::vector<int32_t> es(static_cast<size_t>(std::max<int64_t>(nnz, 1)), 0),
+          ed(static_cast<size_t>(std::max<int64_t>(nnz, 1)), 0);
+      for (int64_t e = 0; e < nnz; ++e) {
+        es[size_t(e)] = int32_t(d->int_idx[e]);
+        ed[size_t(e)] = int32_t(d->int_dtab[e]);
+      }
+      P->e_src.upload(es);
+      P->e_dt.upload(ed);
+      std::vector<int32_t> gl(static_cast<size_t>(G), -1), tq, lc;
+      for (int lv = P->l0; lv <= P->L; ++lv) {
+        const int lj = lv - P->l0;
+        for (int64_t g = P->loc_first[lj]; g < P->loc_first[lj] + P->loc_count[lj]; ++g) gl[size_t(g)] = lv;
+      }
+      for (int lv = P->fused_lf; lv >= P->l0; --lv) {
+        const int lj = lv - P->l0;
+        for (int64_t g = P->loc_first[lj]; g < P->loc_first[lj] + P->loc_count[lj]; ++g)
+          tq.push_back(int32_t(g));
+      }
+      for (int lv = P->l0; lv <= P->fused_lf; ++lv) lc.push_back(int32_t(P->loc_count[lv - P->l0]));
+      P->glevel.upload(gl);
+      P->mega_tq.upload(tq);
+      P->mega_lcount.upload(lc);
+      P->mega_nt = int64_t(tq.size());
+      P->mega_head.alloc(1);
+      P->mega_ldone.alloc(lc.size());
+      P->mega_tdone.alloc(size_t(G));
+      P->mega_ctl.alloc(4);
+      P->mega_ready = true;
+    }
   }
   // wide levels (>= split_lv) get their translation on a side stream as soon
   // as their source amplitudes are final (see enqueue_T)
@@ -1311,6 +1350,7 @@ void set_smem_attrs() {
   if constexpr (std::is_same<T, float>::value) attr(tgemm_pat_kernel<R>, int(pat_smem_bytes<R>()));
   attr(fused_up_kernel<T, R>, lim);
   attr(fused_down_kernel<T, R>, lim);
+  attr(coarse_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
     attr(radiation_mom_kernel<R>, lim);
     attr(radiation_mom_kernel<R, false, 0, 4>, lim);
@@ -1680,6 +1720,28 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     nk++;
     tr("down_fused", s0);
   };
+  auto coarse_mega = [&]() {
+    CoarseArgs<T> ca{};
+    ca.f = fused_args(CT);
+    ca.BT = BT;
+    ca.DT = reinterpret_cast<const T*>(P->DT.p);
+    ca.int_ptr = P->int_ptr.p;
+    ca.e_src = P->e_src.p;
+    ca.e_dt = P->e_dt.p;
+    ca.glevel = P->glevel.p;
+    ca.tq = P->mega_tq.p;
+    ca.n_t = P->mega_nt;
+    ca.lvl_count = P->mega_lcount.p;
+    ca.head = P->mega_head.p;
+    ca.lvl_done = P->mega_ldone.p;
+    ca.tdone = P->mega_tdone.p;
+    ca.ctl = P->mega_ctl.p;
+    const int items = int(2 * ca.f.count + ca.n_t);
+    launch_pdl(P->pdl, coarse_kernel<T, R>, std::max(1, std::min(items, P->mega_ctas * P->n_sm)),
+               kFusedThreads, coarse_smem_bytes<T>(Q, R), s0, ca);
+    nk++;
+    tr("coarse", s0);
+  };
   // Far field.  The wide (fine) levels' translation + reduce run on s2 as
   // soon as their s is final, concurrently with the coarse end of the
   // upward chain, the coarse translations and the coarse downward levels.
@@ -1711,7 +1773,12 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
       }
     }
     if (P->L == P->split_lv && fine && P->L == P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
-    if (fused) {
+    // the coarse levels' up, translation and down in one persistent kernel
+    const bool mega = fused && fine && !per_level && P->fine_after_up == 0 && P->coarse_mega && P->mega_ready &&
+                      P->split_lv == P->fused_lf + 1 && Q * R <= 256;
+    if (mega) {
+      coarse_mega();
+    } else if (fused) {
       fused_up();
       if (P->fused_lf == P->L) hook(2);
     } else {
@@ -1738,8 +1805,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
           reduce(0, P->n_red_fine, P->s2);
         }
         CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
-        translate(P->n_tunits_fine, P->n_tunits, s0);
-        reduce(P->n_red_fine, P->n_red, s0);
+        if (!mega) {
+          translate(P->n_tunits_fine, P->n_tunits, s0);
+          reduce(P->n_red_fine, P->n_red, s0);
+        }
       }
     } else {
       translate(0, P->n_tunits, s0);
@@ -1747,7 +1816,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     }
     hook(4);
     bool joined = !fine;
-    if (fused) fused_down();
+    if (fused && !mega) fused_down();
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
       if (fused && lv <= P->fused_lf) continue;
       if (!joined && lv >= P->split_lv) {
@@ -2143,6 +2212,8 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
     if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;
     if (const char* fs = std::getenv("NESA_FUSED_SPEC")) P->fused_spec = std::atoi(fs) != 0;
+    if (const char* cm = std::getenv("NESA_COARSE_MEGA")) P->coarse_mega = std::atoi(cm) != 0;
+    if (const char* mc = std::getenv("NESA_MEGA_CTAS")) P->mega_ctas = std::max(1, std::atoi(mc));
     if (const char* pc = std::getenv("NESA_PAT_CTAS")) P->pat_ctas = std::max(1, std::atoi(pc));
     if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
     if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;

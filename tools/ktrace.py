@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, HERE)
 
-TAGS = {1: "gather", 2: "scatter", 3: "gather (original order)", 10: "blockgemv(store: near)", 11: "blockgemv(scatter: U)",
+TAGS = {1: "gather", 2: "scatter", 3: "gather (original order)", 35: "coarse far (up + translation + down)", 10: "blockgemv(store: near)", 11: "blockgemv(scatter: U)",
         20: "level_kernel up-leaf", 21: "level_kernel up-sum", 22: "level_kernel down",
         30: "fused_up", 31: "fused_down", 32: "sum_children", 33: "reduce", 40: "tgemm",
         41: "tgemm_wt (FFMA)", 42: "tgemm_tc (tcgen05)", 43: "tgemm_tc2 (tcgen05, A in TMEM)", 44: "tgemm_tc3 (persistent)", 45: "tgemm_pat (target-major, tcgen05)", 50: "level_wt up-leaf",
