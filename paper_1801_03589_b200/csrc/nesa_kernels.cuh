@@ -3142,8 +3142,8 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
 // BETA_IN: `o` holds beta^[leaf][64][R] (row 0 = sum_k o_k, rows 2m-1 / 2m =
 // Re / Im beta_m) from the tensor-core GEMM beta^ = E^ o; the coefficient
 // phase is skipped.
-template <int R, bool BETA_IN = false>
-__global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
+template <int R, bool BETA_IN = false, int MINB = 1>
+__global__ void __launch_bounds__(32 * kExpWarps, MINB) reception_exp_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ E, const float* __restrict__ o, const float* __restrict__ phin,
@@ -3158,32 +3158,18 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
   float* os = reinterpret_cast<float*>(beta + nb);
   const int ne = nt + 1;
   constexpr int kSlots = 4;
-  const int nq = BETA_IN ? 64 * R : Q * R;
-  constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
-  // the next leaf's extent, radius and amplitude (or coefficient) words are
-  // loaded one leaf ahead, so only the point loads are exposed per leaf
-  const int64_t lstride = int64_t(gridDim.x) * kExpWarps;
-  int64_t nx_b = 0;
-  int nx_n = 0;
-  float nx_r = 1.f, nx_ov[NOV];
-  auto fetch = [&](int64_t lj) {
-    if (lj >= nleaf) return;
-    const int64_t lf = leaf0 + lj;
-    nx_b = leaf_start[lf];
-    nx_n = int(leaf_stop[lf] - nx_b);
-    nx_r = leaf_r[lf];
-#pragma unroll
-    for (int t = 0; t < NOV; ++t) nx_ov[t] = lane + 32 * t < nq ? o[lf * nq + lane + 32 * t] : 0.f;
-  };
-  fetch(int64_t(blockIdx.x) * kExpWarps + warp);
-  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf; li += lstride) {
+  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf;
+       li += int64_t(gridDim.x) * kExpWarps) {
     const int64_t leaf = leaf0 + li;
-    const int64_t b = nx_b;
-    const int n = nx_n;
-    const float r = nx_r;
+    const int64_t b = leaf_start[leaf];
+    const int n = int(leaf_stop[leaf] - b);
+    const float r = leaf_r[leaf];
+    // prefetch: amplitudes (or coefficients) and the first kSlots * 32 points
+    const int nq = BETA_IN ? 64 * R : Q * R;
+    constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
     float ov[NOV];
 #pragma unroll
-    for (int t = 0; t < NOV; ++t) ov[t] = nx_ov[t];
+    for (int t = 0; t < NOV; ++t) ov[t] = lane + 32 * t < nq ? o[leaf * nq + lane + 32 * t] : 0.f;
     float2 pp[kSlots];
     int64_t dd[kSlots];
     float bb[kSlots][R];
@@ -3197,7 +3183,6 @@ __global__ void __launch_bounds__(32 * kExpWarps) reception_exp_kernel(
         for (int rr = 0; rr < R; ++rr) bb[i][rr] = phin ? phin[(b + j) * R + rr] : 0.f;
       }
     }
-    fetch(li + lstride);
     const float nlr = -logf(r);
     if constexpr (BETA_IN) {
       // beta^ row 0 -> beta_0 = -log(r) sum o; rows (2m-1, 2m) -> beta_m

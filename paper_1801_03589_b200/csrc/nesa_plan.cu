@@ -429,6 +429,7 @@ struct nesa_plan {
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
   bool fused_spec = false;                   // fused up: speculative parent-matrix prefetch (neutral)
+  int recv_minb = 6;                         // reception register budget (6 / 8 CTAs per SM; 6: 37 vs 39 us)
   int tc3_minb = 0;                          // tgemm_tc3 register budget (3: <= 168 registers)
   int coarse_tc = 1;                         // coarse translation: 0 FFMA, 1 as fine, 2 one CTA per unit
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
@@ -1365,6 +1366,8 @@ void set_smem_attrs() {
     attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
     attr(reception_exp_kernel<R>, lim);
     attr(reception_exp_kernel<R, true>, lim);
+    attr(reception_exp_kernel<R, true, 6>, lim);
+    attr(reception_exp_kernel<R, true, 8>, lim);
   }
   done = true;
 }
@@ -1476,9 +1479,18 @@ int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const 
     else
       tgemm_tc_kernel<R><<<P->n_mom_units, 128, kTcSmem, st>>>(P->mom_units.p, P->mom_ents.p,
                                                               P->ETC.p, o, beta);
-    reception_exp_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
-        P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
-        P->leaf_begin, nleaf, Q, nt, ldp);
+    if (P->recv_minb >= 8)
+      reception_exp_kernel<R, true, 8><<<grid, 32 * kExpWarps, sm, st>>>(
+          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
+          P->leaf_begin, nleaf, Q, nt, ldp);
+    else if (P->recv_minb >= 6)
+      reception_exp_kernel<R, true, 6><<<grid, 32 * kExpWarps, sm, st>>>(
+          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
+          P->leaf_begin, nleaf, Q, nt, ldp);
+    else
+      reception_exp_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
+          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
+          P->leaf_begin, nleaf, Q, nt, ldp);
     return P->beta_fused ? 1 : 2;
   }
   reception_exp_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
@@ -2208,6 +2220,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* fa = std::getenv("NESA_FINE_AFTER_UP")) P->fine_after_up = std::atoi(fa);
     if (const char* ct = std::getenv("NESA_COARSE_TC")) P->coarse_tc = std::atoi(ct);
     if (const char* tm = std::getenv("NESA_TC3_MINB")) P->tc3_minb = std::atoi(tm);
+    if (const char* rm = std::getenv("NESA_RECV_MINB")) P->recv_minb = std::atoi(rm);
     if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
     if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
     if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;
