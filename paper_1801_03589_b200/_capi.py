@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnesa_b200.so")
+LIB_PATH = os.environ.get("NESA_LIB") or os.path.join(_HERE, "libnesa_b200.so")  # NESA_LIB: A/B builds
 
 NESA_ABI_VERSION = 1
 NESA_OK = 0
