@@ -165,7 +165,6 @@ def run_benchmark(config: BenchConfig) -> dict:
     phi_gpu = None
     spans = None
     if "gpu" in config.modes or "verify" in config.modes:
-        t0 = torch.cuda.Event(enable_timing=True)
         tree = build_tree(points, TreeParams(P=config.p_avg))
         tables = build_tables(tree, NesaParams(Q=config.q_aux))
         report["tree_stats"] = tree_stats(tree)
@@ -194,9 +193,7 @@ def run_benchmark(config: BenchConfig) -> dict:
             samples.append(t0.elapsed_time(t1) / config.matvecs_per_sample)
         t_ms = min(samples)
         R = 2 if config.complex_rhs else 1
-        alg = algorithmic_bytes(plan, R, near=near, far=far)
-        total = float(alg["total"]) if isinstance(alg, dict) and "total" in alg else float(
-            sum(v for v in alg.values() if isinstance(v, (int, float))))
+        total = float(algorithmic_bytes(plan, R, near=near, far=far)["total"])
         report["gpu"] = {"samples_ms": samples, "T_ms": t_ms, "matvecs_per_s": 1e3 / t_ms,
                          "alg_bytes": total, "GB_s": total / (t_ms * 1e-3) / 1e9}
         spans = kernel_timeline(plan, qd.data_ptr(), phid.data_ptr(), 1, config.complex_rhs,

@@ -3,7 +3,7 @@ the right-hand-side blocks spread over 1..16 plans / streams (RhsLanes).
 
     python tools/lanes_sweep.py
 """
-import sys, os, json
+import sys
 sys.path.insert(0, '/root/repo')
 import numpy as np, torch
 import paper_1801_03589_b200 as nesa
