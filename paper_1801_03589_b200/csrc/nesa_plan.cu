@@ -429,6 +429,7 @@ struct nesa_plan {
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
   bool fused_spec = false;                   // fused up: speculative parent-matrix prefetch (neutral)
+  bool node_prio = false;                    // graphs honour the captured stream priorities (measured worse)
   int recv_minb = 6;                         // reception register budget (6 / 8 CTAs per SM; 6: 37 vs 39 us)
   int tc3_minb = 0;                          // tgemm_tc3 register budget (3: <= 168 registers)
   int coarse_tc = 1;                         // coarse translation: 0 FFMA, 1 as fine, 2 one CTA per unit
@@ -2101,7 +2102,9 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
       }
     }
     nesa_plan::GraphEntry ent;
-    CUDA_OK(cudaGraphInstantiate(&ent.exec, g, 0));
+    // node priorities: the captured kernels keep their streams' priorities
+    // (far chain above the near field) only with this flag
+    CUDA_OK(cudaGraphInstantiate(&ent.exec, g, P->node_prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
     if (flags & NESA_PROFILE) {
       size_t n = 0;
       CUDA_OK(cudaGraphGetNodes(g, nullptr, &n));
@@ -2221,6 +2224,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* ct = std::getenv("NESA_COARSE_TC")) P->coarse_tc = std::atoi(ct);
     if (const char* tm = std::getenv("NESA_TC3_MINB")) P->tc3_minb = std::atoi(tm);
     if (const char* rm = std::getenv("NESA_RECV_MINB")) P->recv_minb = std::atoi(rm);
+    if (const char* np = std::getenv("NESA_NODE_PRIO")) P->node_prio = std::atoi(np) != 0;
     if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
     if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
     if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;
@@ -2258,8 +2262,10 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       int lo = 0;  // numerically lower = higher priority
       int hi = 0;
       CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s0, cudaStreamNonBlocking, P->priority ? hi : lo));
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s1, cudaStreamNonBlocking, lo));
+      // NESA_NEAR_PRIO=1: the near-field stream above the far chain
+      const bool nprio = std::getenv("NESA_NEAR_PRIO") && std::atoi(std::getenv("NESA_NEAR_PRIO")) != 0;
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s0, cudaStreamNonBlocking, P->priority && !nprio ? hi : lo));
+      CUDA_OK(cudaStreamCreateWithPriority(&P->s1, cudaStreamNonBlocking, nprio ? hi : lo));
       // s2 (side-stream translation) one step below the far chain so the
       // latency-bound level kernels are scheduled first (NESA_S2_PRIO:
       // 0 = same as the chain, 1 = middle, 2 = lowest)
