@@ -113,3 +113,29 @@ def test_nesa_vs_exact_sum_200k():
                                     curve=geo.CurveSpec(kind="ellipse-plates", seed=2),
                                     modes=("gpu", "verify"), repeats=1, matvecs_per_sample=3))
     assert rep["accuracy_rel_l2"] <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,cdt", [("f64", np.float64), ("f32", np.float32)])
+def test_reference_accuracy_suite_on_gpu(dtype, cdt):
+    # test_fastmvp.py:35-54 with the product and the exact sum on the GPU:
+    # near exact, far == dense - near (<= 5e-4), full vs dense (<= 1e-4)
+    _cuda()
+    from oracle.mvp_oracle import near_mask_dense
+    from paper_1801_03589_b200 import dense_matvec_gpu, mvp
+    from paper_1801_03589_b200.operators import NesaParams, build_all
+    from paper_1801_03589_b200.quadtree import TreeParams, build_tree
+    pts = geo.generate_sources(geo.CurveSpec(), 1500)
+    tree = build_tree(pts, TreeParams(P=40))
+    ops = build_all(tree, NesaParams(Q=12))
+    q = np.random.default_rng(0).standard_normal(1500)
+    qq = q.astype(cdt)
+    near = mvp(tree, ops, qq, far=False)
+    far = mvp(tree, ops, qq, near=False)
+    full = mvp(tree, ops, qq)
+    exact = dense_matvec_gpu(pts, q)
+    near_ref = near_mask_dense(tree, pts) @ q
+    tol_near = 1e-13 if dtype == "f64" else 1e-6
+    assert rel_l2(near, near_ref) <= tol_near
+    assert rel_l2(far, exact - near_ref) <= 5e-4
+    assert rel_l2(full, exact) <= 1e-4
