@@ -1463,8 +1463,10 @@ template <int R>
 int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const int64_t* perm,
                          float* phi, int ldp, cudaStream_t st) {
   const int64_t nleaf = P->leaf_end - P->leaf_begin;
+  int rcta = kExpCtasPerSM;
+  if (const char* e = std::getenv("NESA_RECV_CTAS")) rcta = std::max(1, std::atoi(e));
   const int grid = int(std::max<int64_t>(
-      1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(kExpCtasPerSM) * P->n_sm)));
+      1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(rcta) * P->n_sm)));
   const int Q = P->Q, nt = P->u_nt;
   const size_t nb = ((size_t(nt) + 1) * R + 1) & ~size_t(1);
   const size_t sm = size_t(kExpWarps) * (nb + ((size_t(Q) * R + 3) & ~size_t(3)) / 2) * sizeof(float2);
