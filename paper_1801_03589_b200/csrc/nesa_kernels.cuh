@@ -688,6 +688,8 @@ struct LevelArgs {
   T* o;                       // down: incoming amplitudes
   int64_t count;
   int Q, QS, TC;
+  const T* Y;                 // down (level_wt): != null -> translation sums formed here from
+  const int64_t* yptr;        //   the per-entry partials Y[yptr[c] .. yptr[c+1]) (no reduce pass)
 };
 
 template <typename T, int R, int MODE>
@@ -2629,8 +2631,9 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
       }
     }
   } else {
+    const bool ysum = kDown && a.Y != nullptr;
     if (warp == 0) {
-      const uint32_t nb = (kDown ? 2u : 1u) * kVB * uint32_t(n) + (LV::kEMat ? uint32_t(W::MB) : 0u);
+      const uint32_t nb = ((kDown && !ysum) ? 2u : 1u) * kVB * uint32_t(n) + (LV::kEMat ? uint32_t(W::MB) : 0u);
       if (lane == 0) {
         mbar_arrive_expect_tx(&bar[1], nb);
         if constexpr (LV::kEMat)
@@ -2641,7 +2644,40 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
         const int64_t g = kDown ? a.opar[t0 + p] : a.order[t0 + p];
         bulk_g2s(X + p * W::XS, (kDown ? a.o : a.s) + g * W::QR, kVB, &bar[1]);
         if constexpr (kDown)
-          bulk_g2s(Oc + p * W::XS, a.o + int64_t(a.order[t0 + p]) * W::QR, kVB, &bar[1]);
+          if (!ysum) bulk_g2s(Oc + p * W::XS, a.o + int64_t(a.order[t0 + p]) * W::QR, kVB, &bar[1]);
+      }
+    }
+    if constexpr (kDown) {
+      if (ysum) {
+        // Oc[p] = sum of the child's translation partials, in entry order
+        // (reduce_kernel's order): warp w sums children w, w + 4, ...
+        constexpr int NW = W::QR / 128 > 0 ? W::QR / 128 : 1;
+        for (int p = warp; p < n; p += 4) {
+          const int64_t c = a.order[t0 + p];
+          const int64_t e0 = a.yptr[c], e1 = a.yptr[c + 1];
+#pragma unroll
+          for (int sl = 0; sl < NW; ++sl) {
+            const int w = 4 * lane + 128 * sl;
+            if (w >= W::QR) break;
+            T v[4] = {T(0), T(0), T(0), T(0)};
+            int64_t e = e0;
+            for (; e + 2 <= e1; e += 2) {
+              T y0[4], y1[4];
+              ld4(a.Y + e * W::QR + w, y0);
+              ld4(a.Y + (e + 1) * W::QR + w, y1);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) v[i] = (v[i] + y0[i]) + y1[i];
+            }
+            if (e < e1) {
+              T y0[4];
+              ld4(a.Y + e * W::QR + w, y0);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) v[i] += y0[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) Oc[p * W::XS + w + i] = v[i];
+          }
+        }
       }
     }
     mbar_wait(&bar[1], 0);

@@ -429,6 +429,7 @@ struct nesa_plan {
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
   bool fused_spec = false;                   // fused up: speculative parent-matrix prefetch (neutral)
+  bool down_ysum = false;                    // wide down kernels sum Y (no fine reduce; measured slower)
   bool node_prio = false;                    // graphs honour the captured stream priorities (measured worse)
   int recv_minb = 6;                         // reception register budget (6 / 8 CTAs per SM; 6: 37 vs 39 us)
   int tc3_minb = 0;                          // tgemm_tc3 register budget (3: <= 168 registers)
@@ -1658,10 +1659,17 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     CUDA_OK(cudaEventRecord(P->ev_join, join_stream));
     CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
   };
+  // fine levels: the wide downward kernels sum the translation partials Y
+  // themselves (no fine reduce pass; NESA_DOWN_YSUM=0 restores it)
+  bool ysum_down = false;
   auto down_level = [&](int lv) {
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
-    const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
+    LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
+    if (ysum_down && lv >= P->split_lv) {  // translation sums formed in the down kernel
+      la.Y = Y;
+      la.yptr = P->int_ptr.p;
+    }
     if (Q == 64 && la.count >= P->wide_level) {
       const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
       if (lv == P->L && P->beta_fused && far_recv) {
@@ -1817,7 +1825,8 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
         if (!per_level) {
           CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
           translate(0, P->n_tunits_fine, P->s2);
-          reduce(0, P->n_red_fine, P->s2);
+          ysum_down = P->down_ysum && Q == 64 && !P->pat && P->split_lv >= P->l0 + 1;
+          if (!ysum_down) reduce(0, P->n_red_fine, P->s2);
         }
         CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
         if (!mega) {
@@ -2227,6 +2236,7 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     if (const char* tm = std::getenv("NESA_TC3_MINB")) P->tc3_minb = std::atoi(tm);
     if (const char* rm = std::getenv("NESA_RECV_MINB")) P->recv_minb = std::atoi(rm);
     if (const char* np = std::getenv("NESA_NODE_PRIO")) P->node_prio = std::atoi(np) != 0;
+    if (const char* dy = std::getenv("NESA_DOWN_YSUM")) P->down_ysum = std::atoi(dy) != 0;
     if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
     if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
     if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;

@@ -347,7 +347,7 @@ def test_pipeline_matches_sync_calls(golden):
         pipe.submit(qs[0][:-1], outs[0])
 
 
-@pytest.mark.parametrize("env", [{"NESA_TC": "0"}, {"NESA_TC": "1"}, {"NESA_TC2": "0"}, {"NESA_TC3_CTAS": "0"}, {"NESA_MOM_INKERNEL": "0"}, {"NESA_NEAR_AFTER": "-1"}, {"NESA_NEAR_VARIANT": "8,16384,3"}, {"NESA_NEAR_VARIANT": "4,16384,3"}, {"NESA_NEAR_UNITS": "300"}, {"NESA_NEAR_UNITS": "300", "NESA_NEAR_SKIP": "8", "NESA_NEAR_SMEM": "115712"}, {"NESA_PAT": "1"}, {"NESA_PAT": "1", "NESA_PAT_CTAS": "2"}, {"NESA_RAD_DIRECT": "1"}, {"NESA_FUSED_SPEC": "1"}, {"NESA_COARSE_MEGA": "1"}, {"NESA_COARSE_MEGA": "1", "NESA_MEGA_CTAS": "1"}, {"NESA_RECV_MINB": "0"}, {"NESA_RECV_MINB": "8"}, {"NESA_GATHER_INV": "0"}, {"NESA_MOM_VARIANT": "1"}, {"NESA_FINE_AFTER_UP": "2", "NESA_COARSE_TC": "2"}, {"NESA_COARSE_TC": "0"},
+@pytest.mark.parametrize("env", [{"NESA_TC": "0"}, {"NESA_TC": "1"}, {"NESA_TC2": "0"}, {"NESA_TC3_CTAS": "0"}, {"NESA_MOM_INKERNEL": "0"}, {"NESA_NEAR_AFTER": "-1"}, {"NESA_NEAR_VARIANT": "8,16384,3"}, {"NESA_NEAR_VARIANT": "4,16384,3"}, {"NESA_NEAR_UNITS": "300"}, {"NESA_NEAR_UNITS": "300", "NESA_NEAR_SKIP": "8", "NESA_NEAR_SMEM": "115712"}, {"NESA_PAT": "1"}, {"NESA_PAT": "1", "NESA_PAT_CTAS": "2"}, {"NESA_RAD_DIRECT": "1"}, {"NESA_FUSED_SPEC": "1"}, {"NESA_COARSE_MEGA": "1"}, {"NESA_COARSE_MEGA": "1", "NESA_MEGA_CTAS": "1"}, {"NESA_RECV_MINB": "0"}, {"NESA_RECV_MINB": "8"}, {"NESA_DOWN_YSUM": "1"}, {"NESA_DOWN_YSUM": "1", "NESA_RECV_FUSED": "1"}, {"NESA_GATHER_INV": "0"}, {"NESA_MOM_VARIANT": "1"}, {"NESA_FINE_AFTER_UP": "2", "NESA_COARSE_TC": "2"}, {"NESA_COARSE_TC": "0"},
                                  {"NESA_RECV_INKERNEL": "1"}, {"NESA_RECV_FUSED": "1"}, {"NESA_BETA_FUSED": "0"}, {"NESA_FUSED": "0", "NESA_SPLIT": "0"},
                                  {"NESA_NEAR_AFTER": "1", "NESA_MOM_BUF": "0"}, {"NESA_RAD_UP": "1"}])
 def test_q64_f32_path_variants(monkeypatch, env):
