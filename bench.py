@@ -14,9 +14,10 @@ buffers, host<->device copies inside the timed region.
 
 ``--impl reference`` times the reference's CPU algorithm -- the oracle port
 (oracle/mvp_oracle.py, the restated taskfmm mvp_serial; the reference itself
-is pure Python and not present on the GPU box) -- on a bounded sample of the
-same workload (first 1/16 of every stage loop, Re and Im as two real calls),
-scaled to matvecs/s.
+is pure Python and not present on the GPU box) -- one WHOLE complex product
+per step (Re and Im as two real calls), on the host's cores, in a process
+that never loads the product library; plus one product of the reference's
+task-parallel form (oracle/task_mvp.py).
 """
 
 from __future__ import annotations
@@ -38,7 +39,6 @@ N_POINTS = 2_000_000
 SEED = 3
 LEAF_P = 64
 Q_AUX = 64
-SAMPLE_FRACTION = 1.0 / 16.0
 METRIC = "NESA matvecs/sec at N=2M (1/2/4/8 B200); achieved HBM GB/s vs roofline"
 UNIT = "matvecs/s"
 
@@ -62,7 +62,10 @@ def parse_args(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_POINTS, help="points (default 2M)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-task-form", action="store_true",
+                    help="reference arm: skip the task-parallel form's timing")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c128", action="store_true", help="skip the complex128 product timing")
     ap.add_argument("--pipe-slots", type=int, default=1,
                     help="compute slots of the pipelined e2e API (independent plans)")
     return ap.parse_args(argv)
@@ -162,13 +165,8 @@ def load_traffic():
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port on a bounded sample)
+# CPU baseline / reference arm: the oracle port of the reference's product
 # ---------------------------------------------------------------------------
-def cpu_sample_setup(tree, params):
-    from oracle.sample import build_sampled_opset
-    return build_sampled_opset(tree, params, SAMPLE_FRACTION)
-
-
 def cpu_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -177,51 +175,164 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def run_cpu_baseline(tree, params, q, repeats=2):
-    from oracle.sample import time_sample
-    ops = cpu_sample_setup(tree, params)
-    ts = [time_sample(tree, ops, q, SAMPLE_FRACTION) for _ in range(repeats)]
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def reference_problem(n):
+    """Tree and OperatorSet exactly as the reference builds them, on the host,
+    WITHOUT the product library: the numpy tree restatement (bit-identical to
+    the reference's build_tree, tests/test_host_tree.py) and the host operator
+    assembly (build_all, pinned to the reference's checksums)."""
+    import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.quadtree import build_tree
+    pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=SEED), n)
+    t0 = time.perf_counter()
+    tree = build_tree(pts, nesa.TreeParams(P=LEAF_P), native=False)
+    params = nesa.NesaParams(Q=Q_AUX)
+    ops = nesa.build_all(tree, params)
+    q = nesa.random_rhs(n, SEED).astype(np.complex64)
+    return tree, ops, q, time.perf_counter() - t0
+
+
+def reference_product(tree, ops, q):
+    """One complex product as the reference computes it: mvp_serial on Re q
+    and on Im q (float64; the operator is real)."""
+    from oracle.mvp_oracle import mvp_serial
+    t0 = time.perf_counter()
+    mvp_serial(tree, ops, q.real.astype(np.float64))
+    mvp_serial(tree, ops, q.imag.astype(np.float64))
+    return time.perf_counter() - t0
+
+
+def reference_task_product(tree, ops, q, workers):
+    """The reference's task-parallel form (mvp with a Runtime of `workers`
+    threads, fastmvp.py:124-139), restated in oracle/task_mvp.py."""
+    from oracle.task_mvp import TaskRuntime, mvp_tasks
+    with TaskRuntime(workers) as rt:
+        t0 = time.perf_counter()
+        mvp_tasks(tree, ops, q.real.astype(np.float64), rt)
+        mvp_tasks(tree, ops, q.imag.astype(np.float64), rt)
+        return time.perf_counter() - t0
+
+
+def loaded_native_libs():
+    try:
+        return sorted({ln.split()[-1] for ln in open("/proc/self/maps") if "libnesa" in ln})
+    except OSError:
+        return []
+
+
+def run_cpu_baseline(tree_unused, n, repeats=2):
+    """cpu_baseline of our arm: whole complex products of the oracle port at
+    the bench workload, min of `repeats`."""
+    tree, ops, q, build_s = reference_problem(n)
+    ts = [reference_product(tree, ops, q) for _ in range(repeats)]
     t = min(ts)
-    return {"value": SAMPLE_FRACTION / t, "unit": UNIT, "cores": cpu_threads(),
-            "kind": "port",
-            "sample": f"oracle port of taskfmm mvp_serial (fastmvp.py:142-172) on the first "
-                      f"1/{int(1 / SAMPLE_FRACTION)} of every stage loop at N={tree.n_points:,}; "
-                      f"complex q as two real calls (Re, Im); min of {repeats}; "
-                      f"{t:.3f} s per sample; value = fraction / time",
-            "seconds_per_sample": t}
+    return {"value": 1.0 / t, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+            "sample": f"whole products at N={n:,}: oracle port of taskfmm mvp_serial "
+                      f"(fastmvp.py:142-172), float64, complex q as two real calls (Re, Im); "
+                      f"min of {repeats}: {t:.3f} s per product (all {len(ts)}: "
+                      f"{', '.join(f'{x:.3f}' for x in ts)} s); host build {build_s:.1f} s untimed",
+            "seconds_per_product": t, "cpu_model": cpu_model()}
 
 
 def run_reference(args):
+    """--impl reference: the reference's CPU product (the oracle port; the
+    reference is pure Python and absent on the GPU box) on the host cores,
+    every step one WHOLE complex product of the bench workload.  This process
+    never loads libnesa_b200.so (checked and reported)."""
     rank, _, world = dist_env()
     if world > 1 and rank != 0:
         return
-    pts, tree, params, tables, q, _ = build_problem(args.n)
-    from oracle.sample import time_sample
-    ops = cpu_sample_setup(tree, params)
+    tree, ops, q, build_s = reference_problem(args.n)
     for _ in range(args.warmup):
-        time_sample(tree, ops, q, SAMPLE_FRACTION)
-    times = [time_sample(tree, ops, q, SAMPLE_FRACTION) for _ in range(args.steps)]
+        reference_product(tree, ops, q)
+    times = [reference_product(tree, ops, q) for _ in range(args.steps)]
     tot = float(np.sum(times))
-    value = args.steps * SAMPLE_FRACTION / tot
+    value = args.steps / tot
+    workers = os.cpu_count() or 1
+    t_task = reference_task_product(tree, ops, q, workers) if not args.no_task_form else None
+    cores = cpu_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-        "ms_per_matvec": 1e3 / value,   # a step is a 1/16 sample of one product
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.n, 1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                         "sample": f"each step: first 1/{int(1 / SAMPLE_FRACTION)} of every "
-                                   "stage loop of the oracle port of mvp_serial "
-                                   "(float64, complex q as Re+Im real calls); "
-                                   "matvecs/s = steps * fraction / time"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "every step one whole complex product at the bench workload: "
+                                   "oracle port of taskfmm mvp_serial (fastmvp.py:142-172, "
+                                   "float64, Re and Im as two real calls, numpy/OpenBLAS on all "
+                                   "host threads)",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_s": {"min": float(np.min(times)), "median": float(np.median(times)),
+                   "max": float(np.max(times))},
+        "task_parallel": None if t_task is None else {
+            "value": 1.0 / t_task, "unit": UNIT, "workers": workers, "seconds_per_product": t_task,
+            "form": "reference mvp(tree, ops, q, Runtime(RuntimeConfig(workers=os.cpu_count()))) "
+                    "restated in oracle/task_mvp.py (fastmvp.py:124-139, runtime.py); one whole "
+                    "complex product; GIL-bound as in BASELINE.md §2"},
+        "host_build_s": build_s,
+        "native_libs_loaded": loaded_native_libs(),
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
 # GPU arm
+# ---------------------------------------------------------------------------
+def time_c128(args, tree, tables, q, dev, stream):
+    """complex128 products with a float64 plan (BASELINE north_star's 1e-12
+    precision), timed like the headline: CUDA events around K graph launches,
+    device-resident q / phi; plus the near kernel's in-graph roofline."""
+    import torch
+    from paper_1801_03589_b200.plan import NesaPlan, algorithmic_bytes
+    plan = NesaPlan(tree, tables, dtype="f64", device=dev.index)
+    qd = torch.from_numpy(q.astype(np.complex128)).to(dev)
+    phid = torch.empty_like(qd)
+
+    def step():
+        plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream,
+                        profile="near")
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    plan.profile_reset()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    near_ms = float(np.mean(plan.profile_read("near")))
+    alg = algorithmic_bytes(plan, 2)
+    peak, _ = load_peaks()
+    out = {"value": 1e3 / ms, "unit": UNIT, "ms_per_step": ms, "steps": args.steps,
+           "dtype": "c128", "operators": "float64",
+           "near_roofline": {"achieved": alg["near"] / (near_ms * 1e-3) / 1e9, "peak": peak,
+                             "frac": alg["near"] / (near_ms * 1e-3) / 1e9 / peak,
+                             "avg_launch_ms": near_ms, "alg_bytes_per_launch": alg["near"]},
+           "matvec_alg_bytes": alg["total"], "matvec_achieved_gbs": alg["total"] / (ms * 1e-3) / 1e9,
+           "gpu_launches": plan.stat("kernels_per_matvec") * args.steps}
+    plan.close()
+    del qd, phid
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# (our arm)
 # ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
@@ -335,6 +446,12 @@ def run_ours(args):
                                 "note": "near-only product, nothing concurrent"}
     matvec_bw = alg["total"] / (ms_step * 1e-3) / 1e9
 
+    # the reference's own precision: a complex128 product (float64 plan,
+    # operators assembled on the device as for the headline), same workload
+    c128 = None
+    if world == 1 and not args.no_c128:
+        c128 = time_c128(args, tree, tables, q, dev, stream)
+
     # end to end through the public API with pinned host buffers: the
     # pipelined API (H2D of step k+1 and D2H of step k-1 overlap product k;
     # every step still uploads its q and downloads its phi), and the
@@ -417,7 +534,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = run_cpu_baseline(tree, params, q)
+        cpu = run_cpu_baseline(tree, args.n)
 
     if rank == 0:
         line = {
@@ -426,7 +543,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c64", "data": "synthetic (seeded ellipse+plates geometry, N(0,1) rhs)",
             "config": workload_config(args.n, world),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "c128": c128,
             "gpu_launches": plan.stat("kernels_per_matvec") * args.steps,
             "clocks": clocks,
             "matvec_alg_bytes": alg["total"], "matvec_achieved_gbs": matvec_bw,

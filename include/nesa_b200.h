@@ -177,6 +177,8 @@ int nesa_abi_version(void);
 #define NESA_STAT_KERNELS_PER_MATVEC 7
 #define NESA_STAT_V_MOMENTS 8        /* outgoing moments per leaf (0: stored V)   */
 #define NESA_STAT_U_TERMS 9          /* incoming expansion terms (0: stored U)    */
+#define NESA_STAT_GRAPH_CAPTURES 10  /* stream captures so far (one per schedule)  */
+#define NESA_STAT_GRAPHS_CACHED 11   /* instantiated graphs held by the plan       */
 int64_t nesa_plan_stat(nesa_plan* plan, int32_t which);
 
 /* Profiling: with NESA_PROFILE in flags each nesa_matvec records CUDA

@@ -2,7 +2,8 @@
 
 Run in the build container (needs /root/reference, read-only):
 
-    python oracle/gen_golden.py
+    python oracle/gen_golden.py          # the small cases + tree digests
+    python oracle/gen_golden.py c3       # BASELINE C3 (200k points), phi only
 
 For each case the reference's own ``build_tree`` / ``build_all`` /
 ``mvp_serial`` / ``dense_matvec`` (taskfmm, /root/reference/pkg/src) are
@@ -108,6 +109,34 @@ def make_case(name, pts, P, Q, q, with_dense=True, full_tree=True):
     print(f"{name}: N={len(pts)} L={tree.L} G={len(tree.groups)}")
 
 
+def make_phi_case(name, pts, P, Q, q):
+    """A large case stored compactly: the reference's full product only (its
+    inputs are regenerated from the seeds), the tree digest and the counts."""
+    from taskfmm import fastmvp, operators, quadtree
+    tree = quadtree.build_tree(pts, quadtree.TreeParams(P=P))
+    ops = operators.build_all(tree, operators.NesaParams(Q=Q))
+    phi = (fastmvp.mvp_serial(tree, ops, q.real.copy())
+           + 1j * fastmvp.mvp_serial(tree, ops, q.imag.copy()))
+    d = dict(P=np.int64(P), Q=np.int64(Q), phi=phi,
+             tree_sha256=np.array(tree_digest(tree_arrays(tree))),
+             task_counts=np.array([fastmvp.task_counts(tree)[k] for k in (
+                 "near", "radiation", "source-transfer", "translation",
+                 "potential-transfer", "reception")], np.int64))
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(f"{name}: N={len(pts)} L={tree.L} G={len(tree.groups)}")
+
+
+def main_c3():
+    """BASELINE configs[2] (C3) 2D analog: 200k points on ellipse + plates
+    (seed 2), P = 48, Q = 48, complex q (seed 2)."""
+    sys.path.insert(0, REF)
+    sys.path.insert(0, REPO)
+    from paper_1801_03589_b200 import geometry as mine
+    n = 200000
+    pts = mine.generate_sources(mine.CurveSpec(kind="ellipse-plates", seed=2), n)
+    make_phi_case("c3_ellipse_plates_200000", pts, 48, 48, mine.random_rhs(n, 2))
+
+
 def tree_only(name, pts, P):
     from taskfmm import quadtree
     tree = quadtree.build_tree(pts, quadtree.TreeParams(P=P))
@@ -168,4 +197,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "c3":
+        main_c3()
+    else:
+        main()

@@ -27,7 +27,7 @@ NESA_PROFILE_NEAR = 32
 
 STAT = {"near_entries": 0, "v_entries": 1, "u_entries": 2, "d_refs": 3, "n_dtab": 4,
         "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7, "v_moments": 8,
-        "u_terms": 9}
+        "u_terms": 9, "graph_captures": 10, "graphs_cached": 11}
 STAGE = {"total": 0, "near": 1, "far": 2, "reception": 3}
 
 EXPORTED_SYMBOLS = (

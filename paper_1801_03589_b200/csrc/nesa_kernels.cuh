@@ -128,6 +128,13 @@ constexpr int kNCT = kNCW * 32;            // consumer threads
 constexpr int kBGThreads = kNCT + 32;      // + producer warp
 constexpr int kMaxRows = 2 * kNCT;         // rows per item (taller blocks are paneled)
 constexpr int kBGPerSM = 2;                // resident CTAs per SM
+// near-field geometry (measured in the full C4 product: 4 warps x 24 KB x 2
+// stages 555 us, 4 x 16 KB x 3 556, 4 x 32 KB x 2 580, 8 x 16 KB x 3 633;
+// fewer consumer threads and larger stages amortise the per-chunk consumer
+// overhead that bounds an SM's share)
+constexpr int kNearNCW = 4;
+constexpr int kNearABytes = 24 * 1024;
+constexpr int kNearStages = 2;
 
 enum { kModeStore = 0, kModeScatter = 1 };
 
@@ -141,13 +148,6 @@ struct BlockGemvArgs {
   const T* base;                 // scatter: added per tree row (may be null)
   const int64_t* perm;           // scatter: tree row -> original row
   int ldy;                       // scatter: row stride of y (elements)
-  // dynamic mode (wq != null): CTAs claim units [cta_chunk_ptr[u], [u+1])
-  // from the queue wq[0] (wq[1] counts exited CTAs; the last one resets
-  // both); CTAs resident on SMs with %smid < sm_skip exit at once, leaving
-  // those SMs to the concurrent far-field chain
-  int* wq;
-  int n_units;
-  int sm_skip;
 };
 
 struct StageHdr {
@@ -210,21 +210,6 @@ __device__ __forceinline__ void ldx(const T* p, T v[R]) {
   }
 }
 
-__device__ __forceinline__ uint32_t smid_u32() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-// one exited CTA of a dynamic launch; the last one resets the queue for the
-// next launch (launches of one plan are stream-ordered)
-__device__ __forceinline__ void bg_exit_count(int* wq) {
-  __threadfence();
-  if (atomicAdd(wq + 1, 1) == int(gridDim.x) - 1) {
-    wq[0] = 0;
-    wq[1] = 0;
-    __threadfence();
-  }
-}
 
 template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB = kABytes>
 __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
@@ -233,7 +218,6 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
   using Lay = BGLayout<T, R, MODE, NST, NCW, AB>;
   constexpr int kNCW = NCW;
   constexpr int kNCT = NCW * 32;
-  constexpr int kABytes = AB;
   constexpr int kStages = NST;
   extern __shared__ __align__(128) unsigned char smem[];
   T* const sRedOwn = reinterpret_cast<T*>(smem + kStages * Lay::kStage);
@@ -241,13 +225,8 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
       (reinterpret_cast<uintptr_t>(smem + kStages * Lay::kStage + Lay::kRed) + 15) & ~uintptr_t(15));
   uint64_t* empty = full + kStages;
 
-  const bool dyn = a.wq != nullptr;
-  if (dyn && int(smid_u32()) < a.sm_skip) {
-    if (threadIdx.x == 0) bg_exit_count(a.wq);
-    return;
-  }
-  const int c0 = dyn ? 0 : a.cta_chunk_ptr[blockIdx.x];
-  const int c1 = dyn ? 0 : a.cta_chunk_ptr[blockIdx.x + 1];
+  const int c0 = a.cta_chunk_ptr[blockIdx.x];
+  const int c1 = a.cta_chunk_ptr[blockIdx.x + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -263,30 +242,11 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
     // ------------------------------ producer ------------------------------
     const int32_t* recw = reinterpret_cast<const int32_t*>(a.recs);
     const uint64_t pol = l2_evict_first_policy();
-    // static: one range [c0, c1); dynamic: claimed units, one claim ahead
-    int u_cur = 0, u_next = 0, i0 = c0, i1 = c1;
-    if (dyn) {
-      u_cur = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(a.wq, 1) : 0, 0);
-      u_next = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(a.wq, 1) : 0, 0);
-      if (u_cur < a.n_units) {
-        i0 = __ldg(a.cta_chunk_ptr + u_cur);
-        i1 = __ldg(a.cta_chunk_ptr + u_cur + 1);
-      }
-    }
+    int i0 = c0;
+    const int i1 = c1;
     int k = 0;
     int32_t w_next = i0 < i1 ? __ldg(recw + int64_t(i0) * 32 + lane) : 0;
-    for (;;) {
-      if (dyn && i0 >= i1) {
-        // unit done: move to the claimed one, claim the next
-        if (u_cur >= a.n_units || u_next >= a.n_units) break;
-        u_cur = u_next;
-        u_next = __shfl_sync(0xffffffffu, lane == 0 ? atomicAdd(a.wq, 1) : 0, 0);
-        i0 = __ldg(a.cta_chunk_ptr + u_cur);
-        i1 = __ldg(a.cta_chunk_ptr + u_cur + 1);
-        if (i0 >= i1) continue;
-        w_next = __ldg(recw + int64_t(i0) * 32 + lane);
-      }
-      if (i0 >= i1) break;
+    while (i0 < i1) {
       const int i = i0++;
       const int32_t w = w_next;
       if (i + 1 < i1) w_next = __ldg(recw + int64_t(i + 1) * 32 + lane);
@@ -339,18 +299,6 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
       }
       cp_async_mbar_arrive_noinc(&full[st]);
     }
-    if (dyn) {
-      // end marker for the consumers
-      const int st = k % kStages;
-      const uint32_t round = uint32_t(k / kStages);
-      unsigned char* stg = smem + size_t(st) * Lay::kStage;
-      mbar_wait(&empty[st], (round & 1u) ^ 1u);
-      if (lane == 0) {
-        reinterpret_cast<StageHdr*>(stg + Lay::offHdr)->flags = 4;
-        mbar_arrive_expect_tx(&full[st], 0);
-      }
-      cp_async_mbar_arrive_noinc(&full[st]);
-    }
   } else {
     // ------------------------------ consumers -----------------------------
     // Thread (rq, cl): rows 4rq..4rq+3 of the item, columns cl, cl+CL, ...;
@@ -362,13 +310,12 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) acc[i][rr] = T(0);
-    for (int k = 0; dyn || k < c1 - c0; ++k) {
+    for (int k = 0; k < c1 - c0; ++k) {
       const int st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
       const unsigned char* stg = smem + size_t(st) * Lay::kStage;
       mbar_wait(&full[st], round & 1u);
       const StageHdr h = *reinterpret_cast<const StageHdr*>(stg + Lay::offHdr);
-      if (dyn && (h.flags & 4)) break;
       const int m = h.m, nc = h.ncols, ld = h.ld, CL = h.CL;
       const int RQ = ld >> 2;
       const int cl = RQ == 1 ? tid : int(__umulhi(uint32_t(tid), h.magic));
@@ -435,41 +382,12 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
       }
     }
   }
-  if (dyn) {
-    __syncthreads();
-    if (threadIdx.x == 0) bg_exit_count(a.wq);
-  }
 }
 
 // ----------------------------------------------------------------------------
 // gather qt[i] = q[perm[i]]; scatter phi[perm[i]] = phin[i]
 // ----------------------------------------------------------------------------
-template <typename T, int R>
-__global__ void gather_kernel(const T* __restrict__ q, const int64_t* __restrict__ perm,
-                              T* __restrict__ qt, int64_t n, int ldq) {
-  KtScope kt_(1);
-  // four independent rows per thread per round: the random reads of q are
-  // latency-bound, so keep several in flight
-  constexpr int U = 4;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i0 < n; i0 += U * stride) {
-    int64_t j[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) j[u] = i0 + u * stride < n ? perm[i0 + u * stride] : -1;
-    T v[U][R];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) v[u][rr] = j[u] >= 0 ? q[j[u] * ldq + rr] : T(0);
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (j[u] >= 0)
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) qt[(i0 + u * stride) * R + rr] = v[u][rr];
-  }
-}
-
-// qt[iperm[j]] = q[j]: the same gather walked in the original order --
+// qt[iperm[j]] = q[j]: the gather walked in the original order --
 // coalesced reads of q and iperm, scattered 8-byte writes that merge in L2
 // (random 8-byte reads would each fetch a whole sector from DRAM)
 template <typename T, int R>
@@ -573,72 +491,6 @@ __host__ __device__ inline size_t mat_bytes(int Q, size_t es) {
 }
 
 // ----------------------------------------------------------------------------
-// Level transfers.  Per level the host precomputes flat index tables so a
-// CTA issues all its gathers at once (no dependent metadata loads):
-//   upward   slot[(p - pf) * 4 + q] = child of local parent p in quadrant q
-//            (-1 if absent);  s[p] = sum_q C_q s[slot]      (operators.py C)
-//   downward order[i] = children sorted by (quadrant, id), opar[i] = their
-//            parents;          o[c] += B_{quad c} o[parent c]
-// The needed quadrant matrices arrive by bulk copy (TMA bulk engine) and the
-// amplitudes by zero-filling cp.async, all on one mbarrier / group, then the
-// 4 x 4 micro-kernel runs without further synchronisation.  QS quadrant
-// slots are staged at a time (4 in float32 at Q <= 64; fewer if the shared
-// memory would not fit).
-// ----------------------------------------------------------------------------
-template <typename T>
-__host__ __device__ inline size_t xblk_bytes(int Q) {
-  const FarGeom G = far_geom(Q);
-  return (size_t(G.Q) * G.NC * sizeof(T) + 127) & ~size_t(127);
-}
-
-// Thread roles for one CTA whose tile has only ncol live columns: row group
-// rg, column group cgi < CGn and reduction slice js < JS of the j loop (small
-// coarse-level tiles split the Q-long dot products over idle threads).
-struct TileMap {
-  int rg, cgi, js, JS, CGn, jb, je;
-  bool live;
-};
-
-__device__ __forceinline__ TileMap tile_map(const FarGeom& G, int ncol, int tid) {
-  TileMap m;
-  m.CGn = (ncol + 3) / 4;
-  m.JS = 1;
-  while (m.JS < 16 && m.CGn * m.JS * 2 <= G.CG && G.Q / (m.JS * 2) >= 4) m.JS *= 2;
-  m.rg = tid % G.RG;
-  const int rest = tid / G.RG;
-  m.js = rest % m.JS;
-  m.cgi = rest / m.JS;
-  m.live = tid < G.RG * G.CG && m.cgi < m.CGn;
-  m.jb = m.js * G.Q / m.JS;
-  m.je = (m.js + 1) * G.Q / m.JS;
-  return m;
-}
-
-// Sum the JS partial tiles into the js == 0 thread (fixed order; deterministic).
-template <typename T>
-__device__ __forceinline__ void tile_reduce(const FarGeom& G, const TileMap& m, T acc[4][4],
-                                            T* red, int tid) {
-  if (m.JS == 1) return;
-  __syncthreads();
-  if (m.live && m.js) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) red[(r * 4 + c) * kFarThreads + tid] = acc[r][c];
-  }
-  __syncthreads();
-  if (m.live && m.js == 0) {
-    for (int js = 1; js < m.JS; ++js) {
-      const int t2 = tid + js * G.RG;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] += red[(r * 4 + c) * kFarThreads + t2];
-    }
-  }
-}
-
-// ----------------------------------------------------------------------------
 // Level transfer kernels (one launch per level).  The level's groups are
 // visited in `order` (sorted by child quadrant, then id), NC/R per CTA, so a
 // CTA needs one quadrant matrix (two at a boundary).  Children-major form:
@@ -651,29 +503,14 @@ __device__ __forceinline__ void tile_reduce(const FarGeom& G, const TileMap& m, 
 // fastmvp.py:163-169 (translations first, then potential transfer).
 // Matrices arrive by bulk copy; amplitudes by cp.async or summed in staging.
 // ----------------------------------------------------------------------------
-enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2, kLvlDownRecv = 3, kLvlDownBeta = 4 };
+//   kLvlDownBeta  (leaf level, float32 expansion plans) kLvlDown plus the
+//                 reception coefficients beta^ = E^ o of the leaves
+enum { kLvlUpLeaf = 0, kLvlUpSum = 1, kLvlDown = 2, kLvlDownBeta = 4 };
 
-// kLvlDownRecv (leaf level, float32 expansion plans): the leaf-level
-// downward transfer, the reception coefficients and the reception itself in
-// one kernel (see level_wt_kernel).
 struct RecvArgs {
   const float* ET;          // [64][64]: ET[j * 64 + row] = E^[row][j] (row 0 = 1, 2m-1 / 2m = Re / Im (1/m) e^{-i m theta_j})
-  const float2* prel;       // [N] point - leaf center
-  const int64_t* gstart;    // [NL] leaf point ranges
-  const int64_t* gstop;
-  const float* leaf_r;      // [NL] incoming aux radius
-  const float* phin;        // [N][R] near field (tree order) or null
-  const int64_t* perm;      // tree row -> original row
-  float* phi;               // output, original order, rows of stride ldp
-  int ldp, nt;
   float* beta;              // kLvlDownBeta: [NL][64][R] reception coefficients out
 };
-
-template <typename T>
-size_t level_smem_bytes(int Q, int qs) {
-  return size_t(qs) * mat_bytes(Q, sizeof(T)) + xblk_bytes<T>(Q) +
-         size_t(16) * kFarThreads * sizeof(T) + 64;
-}
 
 template <typename T, int R>
 struct LevelArgs {
@@ -687,170 +524,8 @@ struct LevelArgs {
   T* Tout;                    // up: transfers out
   T* o;                       // down: incoming amplitudes
   int64_t count;
-  int Q, QS, TC;
-  const T* Y;                 // down (level_wt): != null -> translation sums formed here from
-  const int64_t* yptr;        //   the per-entry partials Y[yptr[c] .. yptr[c+1]) (no reduce pass)
+  int Q;
 };
-
-template <typename T, int R, int MODE>
-__global__ void __launch_bounds__(kFarThreads) level_kernel(const LevelArgs<T, R> a) {
-  KtScope kt_(20 + MODE);
-  extern __shared__ __align__(128) unsigned char smem[];
-  const FarGeom G = far_geom(a.Q);
-  const int Q = a.Q, QR = Q * R, TC = a.TC;
-  const size_t mb = mat_bytes(Q, sizeof(T)), xb = xblk_bytes<T>(Q);
-  T* X = reinterpret_cast<T*>(smem);
-  unsigned char* Mbase = smem + xb;
-  T* red = reinterpret_cast<T*>(Mbase + a.QS * mb);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 16 * kFarThreads);
-  const int64_t t0 = int64_t(blockIdx.x) * TC;
-  const int nc = int(a.count - t0 < TC ? a.count - t0 : TC);
-  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const TileMap tm = tile_map(G, nc * R, tid);
-  const int q_lo = a.quad[a.order[t0]], q_hi = a.quad[a.order[t0 + nc - 1]];
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    const int nq0 = min(a.QS, q_hi - q_lo + 1);
-    mbar_arrive_expect_tx(bar, uint32_t(nq0 * mb));
-    bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(a.MT4) + q_lo * mb, uint32_t(nq0 * mb),
-             bar);
-  }
-  __syncthreads();  // barrier initialised before anyone waits on it
-  pdl_trigger();
-  pdl_wait();       // inputs below come from the previous kernel in the chain
-  // ---- stage the input amplitudes, one warp per column group
-  if constexpr (MODE == kLvlUpSum) {
-    // s[c] = ordered sum of <= 4 children's T: all child loads in flight
-    // together, 4 consecutive elements per lane
-    for (int cc = wid; cc < nc; cc += kFarThreads / 32) {
-      const int64_t c = a.order[t0 + cc];
-      const int2 kr = a.ochild[t0 + cc];  // (first local child, count)
-      const bool vec = (QR % 4) == 0;
-      if (vec) {
-        for (int w = 4 * lane; w < QR; w += 128) {
-          T v[4] = {T(0), T(0), T(0), T(0)};
-          T t[4][4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < kr.y) ld4(a.Tin + (int64_t(kr.x) + k) * QR + w, t[k]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (k < kr.y)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) v[i] += t[k][i];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            a.s[c * QR + w + i] = v[i];
-            X[((w + i) / R) * G.NC + cc * R + ((w + i) % R)] = v[i];
-          }
-        }
-      } else {
-        for (int w = lane; w < QR; w += 32) {
-          T v = T(0);
-          for (int k = 0; k < kr.y; ++k) v += a.Tin[(int64_t(kr.x) + k) * QR + w];
-          a.s[c * QR + w] = v;
-          X[(w / R) * G.NC + cc * R + (w % R)] = v;
-        }
-      }
-    }
-  } else {
-    for (int cc = wid; cc < nc; cc += kFarThreads / 32) {
-      const T* src = MODE == kLvlDown ? a.o + int64_t(a.opar[t0 + cc]) * QR
-                                      : a.s + int64_t(a.order[t0 + cc]) * QR;
-      for (int j = lane; j < Q; j += 32) cp_async_n<R * sizeof(T)>(X + j * G.NC + cc * R, src + j * R);
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-  }
-  int colq[4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int cc = (4 * tm.cgi + c) / R;
-    colq[c] = (tm.live && cc < nc) ? a.quad[a.order[t0 + cc]] : -1;
-  }
-  T acc[4][4];
-  zero4x4(acc);
-  int round = 0;
-  for (int q0 = q_lo; q0 <= q_hi; q0 += a.QS, ++round) {
-    const int nq = min(a.QS, q_hi - q0 + 1);
-    if (round) {
-      __syncthreads();  // slots consumed
-      if (tid == 0) {
-        mbar_arrive_expect_tx(bar, uint32_t(nq * mb));
-        bulk_g2s(Mbase, reinterpret_cast<const unsigned char*>(a.MT4) + q0 * mb, uint32_t(nq * mb),
-                 bar);
-      }
-    }
-    mbar_wait(bar, uint32_t(round) & 1u);
-    __syncthreads();  // staging complete (first round)
-    if (tm.live) {
-      for (int qq = 0; qq < nq; ++qq) {
-        bool any = false;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) any |= colq[c] == q0 + qq;
-        if (!any) continue;
-        T part[4][4];
-        zero4x4(part);
-        mm4x4(reinterpret_cast<const T*>(Mbase + qq * mb), X, G, 4 * tm.rg, 4 * tm.cgi, part,
-              tm.jb, tm.je);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (colq[c] == q0 + qq)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc[r][c] += part[r][c];
-      }
-    }
-  }
-  tile_reduce(G, tm, acc, red, tid);
-  // stage the tile group-major in the consumed X buffer, then write every
-  // group's contiguous QR block with coalesced stores
-  __syncthreads();
-  if (tm.live && tm.js == 0) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (colq[c] < 0) continue;
-      const int col = 4 * tm.cgi + c, cc = col / R, rr = col % R;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int k = 4 * tm.rg + r;
-        if (k < Q) X[cc * QR + k * R + rr] = acc[r][c];
-      }
-    }
-  }
-  __syncthreads();
-  T* outb = MODE == kLvlDown ? a.o : a.Tout;
-  if ((QR % 4) == 0) {
-    const int nv = QR / 4;
-    for (int i = tid; i < nc * nv; i += kFarThreads) {
-      const int cc = i / nv, v = i - cc * nv;
-      T* dst = outb + int64_t(a.order[t0 + cc]) * QR + 4 * v;
-      T val[4];
-      ld4(X + cc * QR + 4 * v, val);
-      if constexpr (MODE == kLvlDown) {
-        T cur[4];
-        ld4(dst, cur);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) val[q] += cur[q];
-      }
-      if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<float4*>(dst) = make_float4(val[0], val[1], val[2], val[3]);
-      } else {
-        reinterpret_cast<double2*>(dst)[0] = make_double2(val[0], val[1]);
-        reinterpret_cast<double2*>(dst)[1] = make_double2(val[2], val[3]);
-      }
-    }
-  } else {
-    for (int i = tid; i < nc * QR; i += kFarThreads) {
-      const int cc = i / QR, w = i - cc * QR;
-      T* dst = outb + int64_t(a.order[t0 + cc]) * QR + w;
-      if constexpr (MODE == kLvlDown)
-        *dst += X[cc * QR + w];
-      else
-        *dst = X[cc * QR + w];
-    }
-  }
-}
 
 // ----------------------------------------------------------------------------
 // Fused coarse levels.  The levels l0+1 .. lf (too small to fill the GPU) run
@@ -890,7 +565,6 @@ struct FusedArgs {
   T* o;
   int64_t first, count;   // level-lf groups (local)
   int lf, l0, L, Q, D;
-  int spec;               // up: prefetch the parent's matrix before the arrival count
 };
 
 __device__ __forceinline__ int ld_acquire_s32(const int* p) {
@@ -959,20 +633,13 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
     __syncthreads();  // T[g] written, M and X consumed
     if (tid == 0) {
       const int64_t p = a.parent[g];
-      // the parent's matrix, fetched before knowing whether this CTA is the
-      // last child (a.spec): the continuing CTA then finds it in flight
-      // instead of paying one more round trip on the chain
-      const bool spec = a.spec && lv - 1 > a.l0;
-      if (spec) load_mat(lv - 1, p);
       __threadfence();
       const int old = atomicAdd(a.cnt + p, 1);
       const bool last = old == a.uchild[p].y - 1;
       if (last) {
         a.cnt[p] = 0;
         __threadfence();
-        if (!spec && lv - 1 > a.l0) load_mat(lv - 1, p);
-      } else if (spec) {
-        mbar_wait(bar, phase);  // no bulk copy may outlive the CTA
+        if (lv - 1 > a.l0) load_mat(lv - 1, p);
       }
       *nxt = last ? p : -1;
     }
@@ -1044,265 +711,6 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   }
 }
 
-// s[c] = sum_k T[first child + k] for the coarsest level (no transfer above).
-// ----------------------------------------------------------------------------
-// Coarse far field in ONE persistent kernel: the upward pass of the coarse
-// levels (fused_up_kernel's last-arriver chains), their translation sums
-// o_x = sum_e D_e s_src(e) (operators.py:225-239; fastmvp.py:163-166) and the
-// downward pass (fused_down_kernel's claim chains), scheduled from a device
-// work queue instead of four kernel launches.  The paper's task graph
-// on the GPU: items are claimed in dependency order
-// (up items, then translation targets coarse level by level from the finest,
-// then down items), and an item only waits on work that is already claimed
-// by a running CTA -- a level's completion counter, a target's epoch flag, an
-// ancestor's claim state -- so every wait ends even though CTAs are not all
-// co-resident.  Sums keep the reference order (children in order, entries in
-// interaction-list order), one writer per output: deterministic.
-// ----------------------------------------------------------------------------
-template <typename T>
-struct CoarseArgs {
-  FusedArgs<T> f;          // up: MT = C tables; anc / state / cnt / Tup / s / o / level lf range
-  const T* BT;             // B tables (same layout as C)
-  const T* DT;             // D tables (same layout), by D index
-  const int64_t* int_ptr;  // [G + 1] interaction CSR
-  const int32_t* e_src;    // [nnz] source group of entry e
-  const int32_t* e_dt;     // [nnz] D index of entry e
-  const int32_t* glevel;   // [G] level of each group
-  const int32_t* tq;       // translation items: coarse targets, level lf first ... l0 last
-  int64_t n_t;
-  const int32_t* lvl_count;  // [lf - l0 + 1] groups per coarse level (index lv - l0)
-  int* head;               // work queue head
-  int* lvl_done;           // [lf - l0 + 1] finalized amplitudes per level
-  int* tdone;              // [G] epoch of the written translation sum
-  int* ctl;                // [0] epoch, [1] exited CTAs, [2] wait-timeout flag
-};
-
-__device__ __forceinline__ void st_release_s32(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// spin (one thread) until *p reaches v (>= for counters); bounded
-__device__ __forceinline__ void coarse_wait_ge(const int* p, int v, int* err) {
-  for (long long it = 0; ld_acquire_s32(p) < v; ++it) {
-    if (it > (1ll << 24)) {  // ~seconds: give up instead of hanging the GPU
-      atomicExch(err, 1);
-      return;
-    }
-    __nanosleep(64);
-  }
-}
-
-template <typename T>
-__host__ __device__ inline size_t coarse_smem_bytes(int Q, int R) {
-  return 2 * mat_bytes(Q, sizeof(T)) + 2 * ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 128;
-}
-
-template <typename T, int R>
-__global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const CoarseArgs<T> c) {
-  KtScope kt_(35);
-  const FusedArgs<T>& a = c.f;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
-  const size_t mb = mat_bytes(Q, sizeof(T));
-  const size_t xb = (size_t(QR) * sizeof(T) + 15) & ~size_t(15);
-  T* Mb[2] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem + mb)};
-  T* Xb[2] = {reinterpret_cast<T*>(smem + 2 * mb), reinterpret_cast<T*>(smem + 2 * mb + xb)};
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * mb + 2 * xb);  // [0], [1]: M buffers
-  int* sh = reinterpret_cast<int*>(bar + 2);                           // [0] item, [1] flag
-  int64_t* nxt = reinterpret_cast<int64_t*>(sh + 2);
-  const int n_lf = int(a.count);
-  const int n_items = 2 * n_lf + int(c.n_t);
-  const int ep = ld_acquire_s32(c.ctl) + 1;  // this launch's epoch
-  uint32_t ph[2] = {0u, 0u};
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_trigger();
-  pdl_wait();  // the finer levels' transfers are complete
-  auto load_m = [&](int b, const T* table, size_t idx) {  // one thread
-    mbar_arrive_expect_tx(&bar[b], uint32_t(mb));
-    bulk_g2s(Mb[b], table + idx * a.mstride, uint32_t(mb), &bar[b]);
-  };
-  auto wait_m = [&](int b) {
-    mbar_wait(&bar[b], ph[b]);
-    ph[b] ^= 1u;
-  };
-  // y[w] (w = k R + rr) = sum_j M[j Qp + k] X[j R + rr], one output per thread slot
-  auto gemv = [&](const T* M, const T* X, int w) {
-    const int k = w / R, rr = w - (w / R) * R;
-    T acc = T(0);
-#pragma unroll 8
-    for (int j = 0; j < Q; ++j) acc = fma(M[j * Qp + k], X[j * R + rr], acc);
-    return acc;
-  };
-  constexpr int NW = (64 * 4 + kFusedThreads - 1) / kFusedThreads;  // outputs per thread (QR <= 256)
-  for (;;) {
-    if (tid == 0) sh[0] = atomicAdd(c.head, 1);
-    __syncthreads();
-    const int item = sh[0];
-    __syncthreads();
-    if (item >= n_items) break;
-    if (item < n_lf) {
-      // ---------------- upward chain from a level-lf group (fused_up_kernel)
-      int64_t g = a.first + item;
-      int lv = a.lf;
-      if (tid == 0 && lv > a.l0) load_m(0, a.MT, size_t(lv - a.l0 - 1) * 4 + a.quad[g]);
-      while (true) {
-        if (tid == 0) a.state[g] = 0;  // claim state for the downward pass
-        const int2 uc = a.uchild[g];
-        T* X = Xb[0];
-        for (int w = tid; w < QR; w += kFusedThreads) {
-          T v;
-          if (lv == a.L) {
-            v = __ldcg(a.s + g * QR + w);
-          } else {
-            v = T(0);
-            for (int k = 0; k < uc.y; ++k) v += __ldcg(a.Tup + (int64_t(uc.x) + k) * QR + w);
-            a.s[g * QR + w] = v;
-          }
-          X[w] = v;
-        }
-        __syncthreads();  // s[g] written by every thread
-        if (tid == 0) {
-          __threadfence();
-          atomicAdd(c.lvl_done + (lv - a.l0), 1);  // s[g] final
-        }
-        if (lv == a.l0) break;
-        wait_m(0);
-        for (int w = tid; w < QR; w += kFusedThreads) a.Tup[g * QR + w] = gemv(Mb[0], X, w);
-        __syncthreads();  // T[g] written, M and X consumed
-        if (tid == 0) {
-          const int64_t p = a.parent[g];
-          __threadfence();
-          const int old = atomicAdd(a.cnt + p, 1);
-          const bool last = old == a.uchild[p].y - 1;
-          if (last) {
-            a.cnt[p] = 0;
-            __threadfence();
-            if (lv - 1 > a.l0) load_m(0, a.MT, size_t(lv - 1 - a.l0 - 1) * 4 + a.quad[p]);
-          }
-          *nxt = last ? p : -1;
-        }
-        __syncthreads();
-        const int64_t p = *nxt;
-        if (p < 0) break;
-        g = p;
-        --lv;
-      }
-    } else if (item < n_lf + c.n_t) {
-      // ---------------- translation sum of one coarse target
-      const int64_t x = c.tq[item - n_lf];
-      const int lv = c.glevel[x];
-      if (tid == 0) coarse_wait_ge(c.lvl_done + (lv - a.l0), c.lvl_count[lv - a.l0], c.ctl + 2);
-      __syncthreads();
-      const int64_t e0 = c.int_ptr[x], e1 = c.int_ptr[x + 1];
-      T acc[NW];
-#pragma unroll
-      for (int i = 0; i < NW; ++i) acc[i] = T(0);
-      if (tid == 0 && e0 < e1) load_m(0, c.DT, size_t(c.e_dt[e0]));
-      for (int64_t e = e0; e < e1; ++e) {
-        const int b = int(e - e0) & 1;
-        // next entry's D into the other buffer (its last reader finished)
-        if (tid == 0 && e + 1 < e1) load_m(b ^ 1, c.DT, size_t(c.e_dt[e + 1]));
-        const int64_t src = c.e_src[e];
-        for (int w = tid; w < QR; w += kFusedThreads) Xb[b][w] = __ldcg(a.s + src * QR + w);
-        wait_m(b);
-        __syncthreads();
-        int i = 0;
-        for (int w = tid; w < QR; w += kFusedThreads, ++i) acc[i] += gemv(Mb[b], Xb[b], w);
-        __syncthreads();  // buffer b consumed
-      }
-      int i = 0;
-      for (int w = tid; w < QR; w += kFusedThreads, ++i) a.o[x * QR + w] = acc[i];
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        st_release_s32(c.tdone + x, ep);
-      }
-    } else {
-      // ---------------- downward chain to one level-lf group (fused_down_kernel)
-      const int di = item - n_lf - int(c.n_t);
-      const int64_t g = a.first + di;
-      // every amplitude (and so every claim-state reset) is in place once
-      // the top level is complete
-      if (tid == 0) coarse_wait_ge(c.lvl_done, c.lvl_count[0], c.ctl + 2);
-      __syncthreads();
-      for (int i = a.D - 1; i >= -1; --i) {
-        const int64_t x = i >= 0 ? int64_t(a.anc[int64_t(di) * a.D + i]) : g;
-        const int lvx = a.lf - 1 - i;
-        if (i >= 0) {
-          if (tid == 0) {
-            int st = atomicCAS(a.state + x, 0, 1);
-            if (st == 1) {
-              coarse_wait_ge(a.state + x, 2, c.ctl + 2);
-              st = 2;
-            }
-            sh[1] = st;
-          }
-          __syncthreads();
-          const int fl = sh[1];
-          __syncthreads();
-          if (fl != 0) continue;  // finished by another CTA
-        }
-        const int64_t px = a.parent[x];
-        if (tid == 0) {
-          load_m(0, c.BT, size_t(lvx - a.l0 - 1) * 4 + a.quad[x]);
-          coarse_wait_ge(c.tdone + x, ep, c.ctl + 2);                      // o[x] = translation sum
-          if (lvx - 1 == a.l0) coarse_wait_ge(c.tdone + px, ep, c.ctl + 2);  // top parent: final
-        }
-        __syncthreads();
-        for (int w = tid; w < QR; w += kFusedThreads) Xb[0][w] = __ldcg(a.o + px * QR + w);
-        wait_m(0);
-        __syncthreads();
-        T res[NW];
-        int k = 0;
-        for (int w = tid; w < QR; w += kFusedThreads, ++k) res[k] = __ldcg(a.o + x * QR + w) + gemv(Mb[0], Xb[0], w);
-        __syncthreads();
-        k = 0;
-        for (int w = tid; w < QR; w += kFusedThreads, ++k) a.o[x * QR + w] = res[k];
-        __syncthreads();
-        if (i >= 0 && tid == 0) {
-          __threadfence();
-          atomicExch(a.state + x, 2);
-        }
-      }
-    }
-  }
-  // the last CTA out resets the queue for the next launch and publishes the epoch
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(c.ctl + 1, 1) == int(gridDim.x) - 1) {
-      *c.head = 0;
-      for (int l = 0; l <= a.lf - a.l0; ++l) c.lvl_done[l] = 0;
-      c.ctl[1] = 0;
-      __threadfence();
-      st_release_s32(c.ctl, ep);
-    }
-  }
-}
-
-template <typename T, int R>
-__global__ void sum_children_kernel(const int64_t* __restrict__ child_first,
-                                    const int32_t* __restrict__ n_child, int64_t first,
-                                    int64_t count, int64_t cf_lo, int64_t cf_hi,
-                                    const T* __restrict__ Tin, T* s, int Q) {
-  KtScope kt_(32);
-  pdl_trigger();
-  pdl_wait();
-  const int QR = Q * R;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count * QR;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t c = first + i / QR;
-    const int w = int(i % QR);
-    const int64_t k_lo = max(child_first[c], cf_lo), k_hi = min(child_first[c] + n_child[c], cf_hi);
-    T v = T(0);
-    for (int64_t k = k_lo; k < k_hi; ++k) v += Tin[k * QR + w];
-    s[c * QR + w] = v;
-  }
-}
 
 // o[g] = sum_{e in interaction entries of g} Y[e] (entry order) for the
 // listed groups: the translation sums of every level, one warp per group.
@@ -1559,13 +967,11 @@ struct TGW {
   static constexpr size_t SMEM = MB + 2 * XB + 2 * 4 * PER + 64;
 };
 
-// SPLITQ > 0: output rows [0, SPLITQ) go to Y, rows [SPLITQ, QT) to Y2 (the
-// radiation's stacked [A^; C_q A^] map writes s and the leaf transfers T).
-template <typename T, int R, int QT, int KT = QT, int SPLITQ = 0>
+template <typename T, int R, int QT, int KT = QT>
 __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__ units,
                                                        const TEnt* __restrict__ ents,
                                                        const T* __restrict__ DT,
-                                                       const T* __restrict__ s, T* Y, T* Y2) {
+                                                       const T* __restrict__ s, T* Y) {
   KtScope kt_(41);
   using W = TGW<T, R, QT, KT>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1663,16 +1069,7 @@ __global__ void __launch_bounds__(128) tgemm_wt_kernel(const TUnit* __restrict__
       for (int i = tid; i < n * NV; i += 128) {
         const int p = i / NV, v = i - p * NV;
         const float4 val = *reinterpret_cast<const float4*>(O + p * W::XS + v * V);
-        if constexpr (SPLITQ > 0) {
-          constexpr int S1 = SPLITQ * R, S2 = (QT - SPLITQ) * R;
-          const int w = v * V;
-          if (w < S1)
-            *reinterpret_cast<float4*>(Y + int64_t(eid[p]) * S1 + w) = val;
-          else
-            *reinterpret_cast<float4*>(Y2 + int64_t(eid[p]) * S2 + (w - S1)) = val;
-        } else {
-          st16_hint(Y + int64_t(eid[p]) * W::QR + v * V, val, keep);
-        }
+        st16_hint(Y + int64_t(eid[p]) * W::QR + v * V, val, keep);
       }
     }
     __syncthreads();  // X buffer reuse
@@ -1726,193 +1123,6 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
       "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
 }
 
-template <int R>
-__global__ void __launch_bounds__(128) tgemm_tc_kernel(const TUnit* __restrict__ units,
-                                                       const TEnt* __restrict__ ents,
-                                                       const float* __restrict__ DTC,
-                                                       const float* __restrict__ s, float* Y) {
-  KtScope kt_(42);
-  constexpr int QT = 64, QR = QT * R;
-  constexpr int EPT = 128 / R;  // entries per M = 128 tile
-  extern __shared__ __align__(128) unsigned char smem[];
-  float* Bhi = reinterpret_cast<float*>(smem);        // 16 KB
-  float* Blo = Bhi + 4096;                             // 16 KB
-  unsigned char* Ahi = smem + 2 * kTcBBytes;           // 32 KB (128 rows)
-  unsigned char* Alo = Ahi + 2 * kTcBBytes;            // 32 KB
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Alo + 2 * kTcBBytes);  // [0] D, [1] MMA done
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
-  const TUnit u = units[blockIdx.x];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-    mbar_arrive_expect_tx(&bar[0], 2 * kTcBBytes);
-    bulk_g2s(Bhi, DTC + size_t(u.dtab) * (2 * 4096), 2 * kTcBBytes, &bar[0]);
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tslot;
-  pdl_trigger();
-  pdl_wait();  // s comes from the upward pass
-  const int n_all = u.ent_end - u.ent_begin;
-  const int m = tid, e = m / R, rr = m - (m / R) * R;
-  const uint32_t rowoff = uint32_t(m >> 3) * kTcSBO + uint32_t(m & 7) * 16;
-  // this thread's share of tile t0: the R lanes of an entry each hold a
-  // contiguous 1/R of its vector (16 float4: all in flight at once)
-  float4 c[16];
-  int32_t eid = -1;
-  auto load = [&](int t0) {
-    const bool live = t0 + e < n_all;
-    eid = -1;
-    int64_t srcg = 0;
-    if (live) {
-      const TEnt te = ents[u.ent_begin + t0 + e];
-      eid = te.e;
-      srcg = te.src;
-    }
-    const float4* src4 = reinterpret_cast<const float4*>(s + srcg * QR) + rr * 16;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) c[i] = live ? src4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  auto put = [&](int kb, float4 v) {
-    float4 h, l;
-    h.x = tf32_rna(v.x);
-    h.y = tf32_rna(v.y);
-    h.z = tf32_rna(v.z);
-    h.w = tf32_rna(v.w);
-    l.x = tf32_rna(v.x - h.x);
-    l.y = tf32_rna(v.y - h.y);
-    l.z = tf32_rna(v.z - h.z);
-    l.w = tf32_rna(v.w - h.w);
-    *reinterpret_cast<float4*>(Ahi + rowoff + kb * kTcLBO) = h;
-    *reinterpret_cast<float4*>(Alo + rowoff + kb * kTcLBO) = l;
-  };
-  const uint64_t keep = l2_evict_last_policy();  // Y is re-read by reduce_kernel
-  uint32_t phase = 0;
-  load(0);
-  for (int t0 = 0; t0 < n_all; t0 += EPT) {
-    const int eid_t = eid;
-    // ---- A = split(sources): row m = (entry e, component rr), k along K
-    if constexpr (R == 1) {
-#pragma unroll
-      for (int kb = 0; kb < 16; ++kb) put(kb, c[kb]);
-    } else if constexpr (R == 2) {
-      // chunk i holds (k, 0), (k, 1), (k+1, 0), (k+1, 1) for k = 2i + 32 rr:
-      // swap the partner's component with the partner lane
-      float mine[32], other[32];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        mine[2 * i] = rr ? c[i].y : c[i].x;
-        mine[2 * i + 1] = rr ? c[i].w : c[i].z;
-        other[2 * i] = rr ? c[i].x : c[i].y;
-        other[2 * i + 1] = rr ? c[i].z : c[i].w;
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
-#pragma unroll
-      for (int kb = 0; kb < 8; ++kb) {
-        put(rr * 8 + kb, make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]));
-        put((1 - rr) * 8 + kb, make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]));
-      }
-    } else {
-      // R = 4: chunk i = (k, 0..3) for k = i + 16 rr; gather component rr
-      // of every k through the 4 lanes of the entry
-#pragma unroll
-      for (int kb = 0; kb < 16; ++kb) {
-        float v[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = 4 * kb + j, owner = k >> 4, ci = k & 15;
-          // lane (e, owner) holds chunk ci; everyone reads component rr of it
-          const float4 mine4 = c[ci];
-          const float x0 = __shfl_sync(0xffffffffu, mine4.x, (tid & ~3) + owner);
-          const float x1 = __shfl_sync(0xffffffffu, mine4.y, (tid & ~3) + owner);
-          const float x2 = __shfl_sync(0xffffffffu, mine4.z, (tid & ~3) + owner);
-          const float x3 = __shfl_sync(0xffffffffu, mine4.w, (tid & ~3) + owner);
-          v[j] = rr == 0 ? x0 : (rr == 1 ? x1 : (rr == 2 ? x2 : x3));
-        }
-        put(kb, make_float4(v[0], v[1], v[2], v[3]));
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    // ---- MMA: one thread issues 3 x 8 instructions
-    if (tid == 0) {
-      if (t0 == 0) mbar_wait(&bar[0], 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t ah = smem_u32(Ahi), al = smem_u32(Alo);
-      const uint32_t bh = smem_u32(Bhi), bl = smem_u32(Blo);
-#pragma unroll
-      for (int cc = 0; cc < 3; ++cc) {
-        const uint32_t a0 = cc == 2 ? al : ah, b0 = cc == 1 ? bl : bh;
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)
-          umma_tf32(tmem, umma_desc_kmajor(a0 + ks * 2 * kTcLBO), umma_desc_kmajor(b0 + ks * 2 * kTcLBO),
-                    (cc | ks) != 0);
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(&bar[1]))
-                   : "memory");
-    }
-    // ---- prefetch the next tile while the tensor core works
-    if (t0 + EPT < n_all) load(t0 + EPT);
-    mbar_wait(&bar[1], phase);
-    phase ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // ---- epilogue: lane m of TMEM = row m (entry e, component rr); 64 columns
-    uint32_t r[64];
-    {
-      const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
-          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
-          "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
-          "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
-            "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
-            "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]),
-            "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
-            "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
-            "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
-            "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]),
-            "=r"(r[63])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    }
-    // stage the tile entry-major in smem (A is consumed), then coalesced
-    // 16-byte stores of whole Y rows
-    constexpr int OS = QR + 4;
-    float* stage = reinterpret_cast<float*>(Ahi);
-    if (eid_t >= 0)
-#pragma unroll
-      for (int k = 0; k < 64; ++k) stage[e * OS + k * R + rr] = __uint_as_float(r[k]);
-    if (rr == 0) reinterpret_cast<int32_t*>(tslot + 4)[e] = eid_t;
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    {
-      constexpr int NV = QR / 4;
-      const int32_t* eids = reinterpret_cast<const int32_t*>(tslot + 4);
-      const int n = min(EPT, n_all - t0);
-      for (int i = tid; i < n * NV; i += 128) {
-        const int ee = i / NV, v = i - (i / NV) * NV;
-        const float4 val = *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
-        st16_hint(Y + int64_t(eids[ee]) * QR + 4 * v, val, keep);
-      }
-    }
-    __syncthreads();  // stage (= A) read before the next tile is split into it
-  }
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
-}
 
 // Variant with the A operand (sources, split hi / lo) in TMEM instead of
 // shared memory (tcgen05.mma ... [d], [a_tmem], b_desc): thread m = TMEM
@@ -2109,12 +1319,14 @@ __global__ void __launch_bounds__(128) tgemm_tc2_kernel(const TUnit* __restrict_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
+constexpr int kTc3CtasPerSM = 2;  // persistent translation CTAs per SM
+
 // Persistent form of tgemm_tc2_kernel: a CTA loops over units (grid-stride),
 // allocates TMEM once, and fetches the next unit's D as soon as the last MMA
 // of the current one has consumed the D buffer, so the D copy, the next
 // sources and the epilogue overlap instead of paying one CTA start per unit.
-template <int R, int MINB = 1>
-__global__ void __launch_bounds__(128, MINB) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
+template <int R>
+__global__ void __launch_bounds__(128) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
                                                         const TEnt* __restrict__ ents,
                                                         const float* __restrict__ DTC,
                                                         const float* __restrict__ s, float* Y) {
@@ -2311,227 +1523,6 @@ constexpr size_t tc2_smem_bytes() {
   return 2 * size_t(kTcBBytes) + size_t((HALF * OS + 3) & ~3) * 4 + 64 + 4 * 128 + 256;
 }
 
-// ----------------------------------------------------------------------------
-// Target-major translation on the tensor cores (float32, Q = 64):
-//   o_t = sum_j D_j s_src(t, j)      (operators.py:225-239; fastmvp.py:163-166)
-// for a unit of <= 128 targets of one level that share one interaction
-// pattern (the sorted list of their D matrices).  An M = 128 tile holds 128/R
-// targets (row = (target, component)); the K-loop runs over the pattern's
-// D matrices, every step one tf32x3 product (3 x 8 tcgen05.mma, A = the
-// tile's sources in TMEM, B = D in shared memory) accumulated in TMEM, so the
-// per-target sum happens on the tensor core and o is written once: no
-// per-entry partials Y, no reduce pass.  D matrices are double-buffered and
-// fetched one step ahead (bulk copies); the next step's sources load while
-// the tensor core runs.  Summation order = pattern order: deterministic.
-// ----------------------------------------------------------------------------
-struct PUnit {
-  int32_t tgt_begin;  // into ptgt
-  int32_t n_tgt;      // <= 128
-  int32_t off_begin;  // into pdid: the pattern's D indices (K-loop order)
-  int32_t n_off;      // >= 1 (targets without entries use the zero matrix)
-  int32_t src_begin;  // into psrc: [j][t], n_off x n_tgt source groups
-  int32_t pad[3];
-};
-
-template <int R>
-constexpr size_t pat_smem_bytes() {
-  constexpr int HALF = 64 / R, OS = 64 * R + 4;
-  return 4 * size_t(kTcBBytes) + size_t((HALF * OS + 3) & ~3) * 4 + 64 + 4 * 128 + 256;
-}
-
-template <int R>
-__global__ void __launch_bounds__(128) tgemm_pat_kernel(const PUnit* __restrict__ units, int n_units,
-                                                        const int32_t* __restrict__ ptgt,
-                                                        const int32_t* __restrict__ pdid,
-                                                        const int32_t* __restrict__ psrc,
-                                                        const float* __restrict__ DTC,
-                                                        const float* __restrict__ s, float* o) {
-  KtScope kt_(45);
-  constexpr int QT = 64, QR = QT * R;
-  constexpr int EPT = 128 / R;   // targets per M = 128 tile
-  constexpr int HALF = EPT / 2;  // targets staged per epilogue round
-  constexpr int OS = QR + 4;
-  extern __shared__ __align__(128) unsigned char smem[];
-  float* Bb = reinterpret_cast<float*>(smem);  // 2 buffers x [hi | lo] (32 KB each)
-  float* stage = Bb + 2 * 8192;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + ((HALF * OS + 3) & ~3));  // [0,1] D, [2] MMA
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
-  int32_t* tids = reinterpret_cast<int32_t*>(tslot + 4);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  auto issue_d = [&](int buf, int dt) {
-    mbar_arrive_expect_tx(&bar[buf], 2 * kTcBBytes);
-    bulk_g2s(Bb + buf * 8192, DTC + size_t(dt) * 8192, 2 * kTcBBytes, &bar[buf]);
-  };
-  int ui = blockIdx.x;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
-    fence_mbar_init();
-    if (ui < n_units) issue_d(0, pdid[units[ui].off_begin]);  // constant data: before the wait
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tslot;
-  const uint32_t lane_base = uint32_t(warp * 32) << 16;
-  const uint32_t t_acc = tmem + lane_base, t_hi = tmem + lane_base + 64, t_lo = tmem + lane_base + 128;
-  pdl_trigger();
-  pdl_wait();  // s comes from the upward pass
-  const int m = tid, e = m / R, rr = m - (m / R) * R;
-  float4 c[16];
-  auto load = [&](const PUnit& uu, int t0, int j) {
-    const bool live = t0 + e < uu.n_tgt;
-    const int64_t srcg = live ? int64_t(psrc[uu.src_begin + j * uu.n_tgt + t0 + e]) : 0;
-    if constexpr (R == 1 || R == 2) {
-      const float4* src4 = reinterpret_cast<const float4*>(s + srcg * QR) + rr * 16;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) c[i] = live ? src4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
-      const float* src = s + srcg * QR + rr;
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        c[i] = live ? make_float4(src[(4 * i) * R], src[(4 * i + 1) * R], src[(4 * i + 2) * R],
-                                  src[(4 * i + 3) * R])
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  auto put = [&](int kb, float4 v) {
-    float4 h, l;
-    h.x = tf32_rna(v.x);
-    h.y = tf32_rna(v.y);
-    h.z = tf32_rna(v.z);
-    h.w = tf32_rna(v.w);
-    l.x = tf32_rna(v.x - h.x);
-    l.y = tf32_rna(v.y - h.y);
-    l.z = tf32_rna(v.z - h.z);
-    l.w = tf32_rna(v.w - h.w);
-    tmem_st4(t_hi + 4 * kb, h);
-    tmem_st4(t_lo + 4 * kb, l);
-  };
-  uint32_t mph = 0, dph = 0;  // MMA barrier phase; bit b: phase of D buffer b
-  int gs = 0;                 // step counter: D buffer = gs & 1
-  PUnit u = ui < n_units ? units[ui] : PUnit{};
-  if (ui < n_units) load(u, 0, 0);
-  while (ui < n_units) {
-    const int next = ui + int(gridDim.x);
-    const PUnit un = next < n_units ? units[next] : PUnit{};
-    for (int t0 = 0; t0 < u.n_tgt; t0 += EPT) {
-      for (int j = 0; j < u.n_off; ++j, ++gs) {
-        // ---- A = split(sources of step j) into TMEM
-        if constexpr (R == 1 || R == 4) {
-#pragma unroll
-          for (int kb = 0; kb < 16; ++kb) put(kb, c[kb]);
-        } else {
-          float mine[32], other[32];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            mine[2 * i] = rr ? c[i].y : c[i].x;
-            mine[2 * i + 1] = rr ? c[i].w : c[i].z;
-            other[2 * i] = rr ? c[i].x : c[i].y;
-            other[2 * i + 1] = rr ? c[i].z : c[i].w;
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
-#pragma unroll
-          for (int kb = 0; kb < 8; ++kb) {
-            const float4 a = make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]);
-            const float4 b = make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]);
-            put(kb, rr ? b : a);
-            put(8 + kb, rr ? a : b);
-          }
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncthreads();
-        // ---- the step after this one (for the D prefetch and the source loads)
-        int nu = -1, nt = 0, nj = 0;  // 0: this unit, 1: next unit
-        if (j + 1 < u.n_off) {
-          nu = 0; nt = t0; nj = j + 1;
-        } else if (t0 + EPT < u.n_tgt) {
-          nu = 0; nt = t0 + EPT; nj = 0;
-        } else if (next < n_units) {
-          nu = 1; nt = 0; nj = 0;
-        }
-        const int buf = gs & 1;
-        if (tid == 0) {
-          mbar_wait(&bar[buf], (dph >> buf) & 1u);
-          dph ^= 1u << buf;
-          // D of the next step into the other buffer (its last reader, the
-          // previous step's MMA, has completed)
-          if (nu >= 0) issue_d(buf ^ 1, pdid[(nu ? un : u).off_begin + nj]);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t bh = smem_u32(Bb + buf * 8192), bl = bh + kTcBBytes;
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) {
-            const uint32_t a0 = tmem + (cc == 2 ? 128u : 64u), b0 = cc == 1 ? bl : bh;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
-              umma_tf32_ts(tmem, a0 + ks * 8, umma_desc_kmajor(b0 + ks * 2 * kTcLBO), (j | cc | ks) != 0);
-          }
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           smem_u32(&bar[2]))
-                       : "memory");
-        }
-        // the next step's sources load while the tensor core runs
-        if (nu >= 0) load(nu ? un : u, nt, nj);
-        mbar_wait(&bar[2], mph);
-        mph ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      }
-      // ---- epilogue: TMEM lane m = row m (target e, component rr), 64 columns
-      uint32_t r[64];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
-          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
-          "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
-          "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-            "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
-            "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
-            "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]),
-            "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]),
-            "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
-            "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
-            "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]),
-            "=r"(r[63])
-          : "r"(t_acc));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int n = min(EPT, u.n_tgt - t0);
-      if (rr == 0) tids[e] = e < n ? ptgt[u.tgt_begin + t0 + e] : -1;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e0 = h * HALF;
-        if (e >= e0 && e < e0 + HALF && e < n)
-#pragma unroll
-          for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
-        __syncthreads();
-        constexpr int NV = QR / 4;
-        const int nh = max(0, min(HALF, n - e0));
-        for (int i = tid; i < nh * NV; i += 128) {
-          const int ee = i / NV, v = i - (i / NV) * NV;
-          const float4 val = *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
-          *reinterpret_cast<float4*>(o + int64_t(tids[e0 + ee]) * QR + 4 * v) = val;
-        }
-        __syncthreads();
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    }
-    ui = next;
-    u = un;
-  }
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
-}
-
-// bytes of dynamic shared memory of tgemm_tc_kernel
-constexpr size_t kTcSmem = 6 * size_t(kTcBBytes) + 64 + 4 * 128 + 1024;
 
 // ----------------------------------------------------------------------------
 // Warp-tiled level transfer for Q in {32, 64} on the large levels (same
@@ -2540,19 +1531,16 @@ constexpr size_t kTcSmem = 6 * size_t(kTcBBytes) + 64 + 4 * 128 + 1024;
 // or summed from the children (UpSum); each warp computes a 32 x 32 block
 // with the conflict-free lane layout of tgemm_wt_kernel.
 // ----------------------------------------------------------------------------
-#ifndef LVW_SLOTS
-#define LVW_SLOTS 1
-#endif
 template <typename T, int R, int QT, int MODE>
 struct LVW {
   using W = TGW<T, R, QT>;
   // quadrant matrices per round: tiles are quadrant-sorted, so only the (at
   // most 3) boundary tiles of a level need a second round; one slot keeps the
   // kernel small enough to run 2-3 CTAs per SM beside the near field
-  static constexpr int kSlots = LVW_SLOTS;
-  static constexpr bool kDown = MODE == 2 || MODE == 3 || MODE == 4;
+  static constexpr int kSlots = 1;
+  static constexpr bool kDown = MODE == kLvlDown || MODE == kLvlDownBeta;
   static constexpr int kXBufs = kDown ? 2 : 1;      // the downward modes also stage o[c]
-  static constexpr int kEMat = MODE >= 3 ? 1 : 0;   // kLvlDownRecv / Beta: the E^ matrix
+  static constexpr int kEMat = MODE == kLvlDownBeta ? 1 : 0;  // the E^ matrix
   static constexpr size_t SMEM = (kSlots + kEMat) * W::MB + kXBufs * W::XB + 3 * 64;
 };
 
@@ -2566,7 +1554,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
   T* M = reinterpret_cast<T*>(smem);                                  // kSlots matrices
   T* X = reinterpret_cast<T*>(smem + LV::kSlots * W::MB);             // inputs / outputs
   T* Oc = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + W::XB);    // down: o[c] (reduce output)
-  T* Em = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + LV::kXBufs * W::XB);  // kLvlDownRecv: E^
+  T* Em = reinterpret_cast<T*>(smem + LV::kSlots * W::MB + LV::kXBufs * W::XB);  // kLvlDownBeta: E^
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (LV::kSlots + LV::kEMat) * W::MB +
                                                LV::kXBufs * W::XB);  // M, X
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -2631,9 +1619,8 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
       }
     }
   } else {
-    const bool ysum = kDown && a.Y != nullptr;
     if (warp == 0) {
-      const uint32_t nb = ((kDown && !ysum) ? 2u : 1u) * kVB * uint32_t(n) + (LV::kEMat ? uint32_t(W::MB) : 0u);
+      const uint32_t nb = (kDown ? 2u : 1u) * kVB * uint32_t(n) + (LV::kEMat ? uint32_t(W::MB) : 0u);
       if (lane == 0) {
         mbar_arrive_expect_tx(&bar[1], nb);
         if constexpr (LV::kEMat)
@@ -2644,40 +1631,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
         const int64_t g = kDown ? a.opar[t0 + p] : a.order[t0 + p];
         bulk_g2s(X + p * W::XS, (kDown ? a.o : a.s) + g * W::QR, kVB, &bar[1]);
         if constexpr (kDown)
-          if (!ysum) bulk_g2s(Oc + p * W::XS, a.o + int64_t(a.order[t0 + p]) * W::QR, kVB, &bar[1]);
-      }
-    }
-    if constexpr (kDown) {
-      if (ysum) {
-        // Oc[p] = sum of the child's translation partials, in entry order
-        // (reduce_kernel's order): warp w sums children w, w + 4, ...
-        constexpr int NW = W::QR / 128 > 0 ? W::QR / 128 : 1;
-        for (int p = warp; p < n; p += 4) {
-          const int64_t c = a.order[t0 + p];
-          const int64_t e0 = a.yptr[c], e1 = a.yptr[c + 1];
-#pragma unroll
-          for (int sl = 0; sl < NW; ++sl) {
-            const int w = 4 * lane + 128 * sl;
-            if (w >= W::QR) break;
-            T v[4] = {T(0), T(0), T(0), T(0)};
-            int64_t e = e0;
-            for (; e + 2 <= e1; e += 2) {
-              T y0[4], y1[4];
-              ld4(a.Y + e * W::QR + w, y0);
-              ld4(a.Y + (e + 1) * W::QR + w, y1);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) v[i] = (v[i] + y0[i]) + y1[i];
-            }
-            if (e < e1) {
-              T y0[4];
-              ld4(a.Y + e * W::QR + w, y0);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) v[i] += y0[i];
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) Oc[p * W::XS + w + i] = v[i];
-          }
-        }
+          bulk_g2s(Oc + p * W::XS, a.o + int64_t(a.order[t0 + p]) * W::QR, kVB, &bar[1]);
       }
     }
     mbar_wait(&bar[1], 0);
@@ -2759,7 +1713,7 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
     }
   }
   __syncthreads();
-  if constexpr (MODE == kLvlDownRecv || MODE == kLvlDownBeta) {
+  if constexpr (MODE == kLvlDownBeta) {
     if constexpr (sizeof(T) == 4 && QT == 64) {
       // ---- reception coefficients of the tile's leaves: beta^ = E^ o (same
       // warp tiling; E^ is one matrix for every column), into the Oc buffer
@@ -2788,46 +1742,15 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
         }
       }
       __syncthreads();
-      if constexpr (MODE == kLvlDownBeta) {
-        // beta^ rows of the tile's leaves -> global, coalesced
+      {
+        // beta^ rows of the tile's leaves -> global, coalesced (the leaf
+        // level's o is only ever read through beta^, so it is not stored)
         constexpr int V = 4;
         constexpr int NV = W::QR / V;
         for (int i = tid; i < n * NV; i += 128) {
           const int p = i / NV, v = i - p * NV;
           *reinterpret_cast<float4*>(rv.beta + int64_t(a.order[t0 + p]) * W::QR + v * V) =
               *reinterpret_cast<const float4*>(Oc + p * W::XS + v * V);
-        }
-        return;
-      }
-      // ---- reception of the tile's leaves: warp w takes leaves w, w+4, ...;
-      // lane = point; phi[perm] = phin + beta_0 + Re sum_m beta_m w^m
-      for (int p = warp; p < n; p += 4) {
-        const int64_t leaf = a.order[t0 + p];
-        const int64_t b = rv.gstart[leaf];
-        const int np = int(rv.gstop[leaf] - b);
-        const float rad = rv.leaf_r[leaf];
-        const float inv = 1.f / rad, nlr = -logf(rad);
-        const T* bt = Oc + p * W::XS;  // row r, component rr at r * R + rr
-        for (int j = lane; j < np; j += 32) {
-          const int64_t i = b + j;
-          const float2 pt = rv.prel[i];
-          const int64_t dst = rv.perm[i];
-          float accv[R];
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) accv[rr] = (rv.phin ? rv.phin[i * R + rr] : 0.f) + nlr * bt[rr];
-          const float2 w = make_float2(pt.x * inv, pt.y * inv);
-          float2 z = w;
-#pragma unroll 4
-          for (int m = 1; m <= rv.nt; ++m) {
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-              const float br = bt[(2 * m - 1) * R + rr], bi = bt[(2 * m) * R + rr];
-              accv[rr] = fmaf(br, z.x, fmaf(-bi, z.y, accv[rr]));
-            }
-            z = cmulf(z, w);
-          }
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) rv.phi[dst * rv.ldp + rr] = accv[rr];
         }
       }
     }
@@ -2914,7 +1837,6 @@ __device__ __forceinline__ float2 cpow_const(float2 w) {
   }
 }
 
-constexpr int kMomBufPts = 800;  // staged points per warp batch (8 leaves)
 
 // Radiation through outgoing moments.  Lane group of kMomLanes lanes per
 // leaf, kMomLeavesPerWarp leaves per warp.  The batch's points (contiguous)
@@ -2924,24 +1846,18 @@ constexpr int kMomBufPts = 800;  // staged points per warp batch (8 leaves)
 // registers (passes of MP moments, 2 R MP = 80 accumulators), the group
 // combines them with a transpose reduction (fixed pairing), then the warp
 // applies A (read through L1, shared by every leaf) to its leaves' moments.
-// smem per warp: points [kMomBufPts] float2, q [kMomBufPts][R], mu
+// smem per warp: points [bufpts] float2, q [bufpts][R], mu
 // [leaves][nm][R] float2 (16-byte rows).
-// MU_OUT: instead of applying A, write the leaf's real moment vector
-// mu^[leaf][kt][R] (row 0 = -log(r) mu_0, rows 2m-1 / 2m = Re / Im mu_m,
-// zero padding) for the warp-tiled GEMM s = A^ mu^ (tgemm_wt_kernel).
-template <int R, bool MU_OUT = false, int MPX = 0, int MINB = 1>
-__global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
+// Register budget for 4 CTAs / SM (<= 128 registers, no spills): at the
+// natural 169 registers only 2 CTAs fit (measured 531 vs 537 us at C4).
+template <int R>
+__global__ void __launch_bounds__(32 * kExpWarps, 4) radiation_mom_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ A, const float* __restrict__ qt, float* __restrict__ s,
-    int64_t leaf0, int64_t nleaf, int Q, int nm, int kt = 0, int bufpts = kMomBufPts,
-    const int64_t* __restrict__ qperm = nullptr) {
-  // qperm != null: qt is q in the ORIGINAL order (row stride R) and point
-  // b's charges are qt[qperm[b]] -- the gather into tree order is then off
-  // the far chain's critical path (it runs beside this kernel for the near
-  // field only)
-  KtScope kt_(60 + int(MU_OUT));
-  constexpr int MP = MPX > 0 ? MPX : 40 / R;  // moments per pass
+    int64_t leaf0, int64_t nleaf, int Q, int nm, int bufpts) {
+  KtScope kt_(60);
+  constexpr int MP = 40 / R;  // moments per pass
   constexpr int NV = 2 * R * MP;       // 80 accumulators
   constexpr int NV2 = NV / 2, NV4 = NV / 4;
   constexpr int LW = kMomLeavesPerWarp;
@@ -2964,8 +1880,7 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
     if (np > bufpts) return false;
     for (int t = lane; t < np; t += 32) {
       cp_async<8>(Pb + t, prel + b0 + t);
-      const int64_t src = qperm ? qperm[b0 + t] : b0 + t;
-      cp_async_n<R * 4>(Qb + t * R, qt + src * R);
+      cp_async_n<R * 4>(Qb + t * R, qt + (b0 + t) * R);
     }
     cp_async_commit();
     return true;
@@ -2998,7 +1913,7 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
         } else {
           p = prel[b + j];
 #pragma unroll
-          for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(qperm ? qperm[b + j] : b + j) * R + rr];
+          for (int rr = 0; rr < R; ++rr) qv[rr] = qt[(b + j) * R + rr];
         }
         const float2 w = make_float2(p.x * inv, p.y * inv);
         // two interleaved power chains (even / odd terms, each stepping by w^2)
@@ -3061,28 +1976,6 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
     }
     __syncwarp();  // moments visible; the point buffer is free
     staged = stage(lw + stride);
-    if constexpr (MU_OUT) {
-#pragma unroll 1
-      for (int l = 0; l < LW; ++l) {
-        const int64_t li2 = lw + l;
-        if (li2 >= nleaf) break;
-        const int64_t lf = leaf0 + li2;
-        const float nl = -logf(leaf_r[lf]);
-        const float* ml = reinterpret_cast<const float*>(mu + l * mu_stride);  // [m][re, im][rr]
-        float* dst = s + lf * int64_t(kt) * R;
-        for (int t = lane; t < kt * R; t += 32) {
-          const int row = t / R, rr = t - (t / R) * R;
-          const int m = (row + 1) >> 1;
-          float v = 0.f;
-          if (row == 0)
-            v = nl * ml[rr];
-          else if (m < nm)
-            v = (row & 1) ? ml[(m * 2) * R + rr] : ml[(m * 2 + 1) * R + rr];
-          dst[t] = v;
-        }
-      }
-      __syncwarp();
-    } else {
     // s_k = -log(r) F_k mu_0 + sum_m Re(A_km mu_m): lane owns k = kb + lane
     // and kb + 32 + lane for all the warp's leaves
     for (int kb = 0; kb < Q; kb += 64) {
@@ -3165,7 +2058,6 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
       }
     }
     __syncwarp();
-    }  // !MU_OUT
   }
   cp_async_wait_all();
 }
@@ -3178,8 +2070,9 @@ __global__ void __launch_bounds__(32 * kExpWarps, MINB) radiation_mom_kernel(
 // BETA_IN: `o` holds beta^[leaf][64][R] (row 0 = sum_k o_k, rows 2m-1 / 2m =
 // Re / Im beta_m) from the tensor-core GEMM beta^ = E^ o; the coefficient
 // phase is skipped.
-template <int R, bool BETA_IN = false, int MINB = 1>
-__global__ void __launch_bounds__(32 * kExpWarps, MINB) reception_exp_kernel(
+// Register budget for 6 CTAs / SM with beta^ in (measured 37 vs 39 us at C4).
+template <int R, bool BETA_IN>
+__global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float2* __restrict__ E, const float* __restrict__ o, const float* __restrict__ phin,

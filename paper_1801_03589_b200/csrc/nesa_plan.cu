@@ -107,16 +107,6 @@ struct DevBlockSet {
   DevBuf<int32_t> cta_ptr;
   int grid = 0;
   int64_t n_items = 0;
-  // dynamic launch (n_units > 0): cta_ptr holds n_units claimable ranges,
-  // launch_grid CTAs claim them from wq; CTAs on SMs < sm_skip exit at once
-  DevBuf<int> wq;
-  int n_units = 0;
-  int launch_grid = 0;
-  int sm_skip = 0;
-  size_t smem = 0;  // dynamic shared memory per CTA (0: the layout's own)
-  int ncw = kNCW;    // consumer warps of the block-GEMV launch (store mode: 8 or 4)
-  int ab = kABytes;  // bytes per ring stage (16 or 32 KB)
-  int nst = kStages; // ring stages
   int64_t entries = 0;
 };
 
@@ -308,7 +298,6 @@ struct nesa_plan {
 
   DevBuf<int64_t> perm;        // [N]
   DevBuf<int32_t> iperm;       // [N] original index -> tree index
-  bool gather_inv = true;      // gather walked in the original order (gather_inv_kernel; ~same time)
   DevBuf<int32_t> quad;        // [G]
   DevBuf<int64_t> parent;      // [G]
   DevBuf<int64_t> child_first; // [G]
@@ -337,29 +326,9 @@ struct nesa_plan {
   DevBuf<int2> uchild;                      // [G] local children (first, count)
   DevBuf<int32_t> fused_anc;                // [count(lf)][lf - l0 - 1] ancestors
   DevBuf<int> fused_cnt, fused_state;       // [G] arrival counters / claim states
-  // coarse far field as one persistent kernel (coarse_kernel): coarse
-  // up + translation + down from a device work queue
-  bool coarse_mega = false;                 // (measured slower: items serialise inside CTAs)
-  int mega_ctas = 2;                        // persistent CTAs per SM
-  bool mega_ready = false;
-  DevBuf<int32_t> e_src, e_dt, glevel, mega_tq, mega_lcount;
-  DevBuf<int> mega_head, mega_ldone, mega_tdone, mega_ctl;
-  int64_t mega_nt = 0;
-  int qs = 4;                               // quadrant slots staged per round
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
-  int near_ctas = 2;                        // near-field CTAs per SM (1: 6-stage ring)
-  int near_waves = 1;                       // near-field grid = waves x resident CTAs
-  int near_units = 0;                       // >0: dynamic near launch over this many ranges
-  int near_sm_skip = 0;                     // dynamic: SMs [0, skip) left to the far chain
-  size_t near_smem = 0;                     // dynamic: shared memory per near CTA (padding)
-  int near_ncw = 4, near_ab = 24576, near_nst = 2;  // near-field kernel variant (NESA_BG_VARIANTS)
-  bool priority = true;                     // far-field stream scheduled first
-  bool split = true;                        // fine-level translation on a side stream
-  int near_after = 0;                       // where the near branch forks (see enqueue_T;
-                                            // 0: after the radiation, measured best at C4)
+                                            // (NESA_WIDE_LEVEL: tests force them on small trees)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
-  bool recv_far = false;                    // reception in the far branch (u_mf only)
-  bool pdl = true;                          // programmatic dependent launch in the far chain
   DevBuf<float2> mf_prel;                   // [N] point - leaf center (float32)
   DevBuf<int64_t> gstart, gstop;            // [NL] leaf point ranges
   DevBuf<float> mf_leaf_r;                  // [NL] rho_in_aux * half side (float32)
@@ -370,97 +339,61 @@ struct nesa_plan {
   DevBuf<float2> mom_A;                     // [v_nm][Q]: row 0 = (F_k, 0), row m = A_km
   DevBuf<float2> exp_E;                     // [Q][u_nt + 1]: 1, (1/m) e^{-i m theta_k}
   DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
-  // Q = 64: s = A^ mu^ as a warp-tiled GEMM over the leaves (KT = mom_kt)
-  int mom_kt = 0;
-  int mom_buf = 800;                        // staged points per warp in the moment kernel
-  int mom_variant = 0;                      // moment kernel instantiation (launch_radiation)
-  DevBuf<float> momAT;                      // [mom_kt][Q] transposed real A^
-  bool tc = true;                           // translation on the tensor cores (float32, Q = 64)
-  bool tc2 = true;                          // ... with the A operand in TMEM (~50 KB smem)
-  int tc3_ctas = 2;                         // ... persistent, this many CTAs per SM (0: one CTA per unit)
+  bool tc = true;                           // translation on the tensor cores (float32, Q = 64;
+                                            // NESA_TC=0 selects the FFMA kernel, as float64 plans)
   DevBuf<float> DTC;                        // [n_dtab + 1][hi | lo][64 x 64] canonical tf32 D (+ zero)
-  // target-major translation (float32, Q = 64, tensor cores): units of <= 128
-  // targets of one level sharing one interaction pattern (the sorted list of
-  // their D matrices); o is written directly, no Y and no reduce
-  // (measured 561 vs 527 us at C4: the shared patterns pad the K-loop ~2x and
-  // each step's D load is serial in a CTA; NESA_PAT=1 enables it)
-  bool pat = false;
-  int pat_ctas = 1;                         // persistent CTAs per SM of the pattern kernel
-  DevBuf<PUnit> punits;
-  DevBuf<int32_t> ptgt, pdid, psrc;
-  int n_punits = 0, n_punits_fine = 0;
-  DevBuf<TUnit> mom_units;
+  DevBuf<TUnit> mom_units;                  // reception coefficient GEMM: 32 leaves per unit
   DevBuf<TEnt> mom_ents;
   int n_mom_units = 0;
-  bool rad_up = false;                      // radiation GEMM also writes the leaf transfers T
-  DevBuf<float> radT;                       // [4 quadrants][80][128] stacked [A^; C_q A^]^T
-  DevBuf<TUnit> rad_units;
-  DevBuf<TEnt> rad_ents;
-  int n_rad_units = 0;
-  bool beta_tc = false;                     // reception coefficients by tgemm_tc (E^ o)
-  bool recv_fused = false;                  // leaf down + beta + reception in one kernel
+  bool beta_tc = false;                     // reception coefficients by tgemm_tc2 (E^ o)
   bool beta_fused = false;                  // leaf down + beta in one kernel (reception separate)
   DevBuf<float> ET;                         // [64][64] E^ transposed for the warp-tiled GEMM
   DevBuf<float> ETC;                        // [hi | lo][64 x 64] canonical tf32 E^
   DevBuf<unsigned char> beta;               // [NL][64][R] reception coefficients
-  DevBuf<unsigned char> mu;                 // [NL][mom_kt][R] moments
-  cudaEvent_t ev_mark = nullptr;            // no-op event-record node ahead of the near kernel
 
   // workspace for R real columns
   int ws_R = 0;
-  int ldv = 1;  // row stride of the caller's q / phi (elements) for the current capture
-  DevBuf<unsigned char> qt, phin, phif, s, o, Y, Tup;
-  DevBuf<unsigned char> farws;              // s | Tup | o, contiguous (one L2 window)
-  size_t l2_persist = 0;                    // bytes of L2 set aside for farws (NESA_L2_PERSIST MB)
+  uint64_t ws_gen = 0;                      // bumped when the workspace is reallocated
+  DevBuf<unsigned char> qt, phin, s, o, Y, Tup;
+  DevBuf<unsigned char> farws;              // s | Tup | o, contiguous
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t s2 = nullptr;                 // fine-level translation branch
-  cudaStream_t s3 = nullptr;                 // second near-field launch (near_split)
-  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
-  cudaEvent_t ev_gfork = nullptr;           // gather on the near stream (rad_direct)
-  bool rad_direct = false;                  // radiation reads q through perm (see enqueue_T;
-                                            // measured slower: 556 vs 539 us, random q reads)
-  int near_split = 0;                        // far-pass hook position of the 2nd near launch (0: one
-                                             // launch; measured slower: half the CTAs stream at
-                                             // about half the bandwidth)
-  double near_frac = 0.5;                    // share of near-field CTAs in the first launch
   cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
   int split_lv = 0;                          // levels >= split_lv: translated on s2
-  int fine_after_up = 0;                     // s2 translation starts after the up pass (1) / coarse translation (2)
-  bool fused_spec = false;                   // fused up: speculative parent-matrix prefetch (neutral)
-  bool down_ysum = false;                    // wide down kernels sum Y (no fine reduce; measured slower)
-  bool node_prio = false;                    // graphs honour the captured stream priorities (measured worse)
-  int recv_minb = 6;                         // reception register budget (6 / 8 CTAs per SM; 6: 37 vs 39 us)
-  int tc3_minb = 0;                          // tgemm_tc3 register budget (3: <= 168 registers)
-  int coarse_tc = 1;                         // coarse translation: 0 FFMA, 1 as fine, 2 one CTA per unit
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
   int64_t n_red_fine = 0;                    // red_ids [0, n_red_fine) are fine levels
-  std::vector<int> tu_start;                 // [lv - l0]: first translation unit of level lv
-  std::vector<int64_t> red_start;            // [lv - l0]: first red_ids entry of level lv
-  std::vector<cudaEvent_t> ev_lv;            // [lv - l0]: level lv's s is final
-  bool split_levels = false;                 // fine levels translated one by one as their s is final
-                                             // (NESA_SPLIT_LEVELS=1; measured slower: the translation
-                                             // CTAs delay the up chain)
 
+  // One captured graph per (R, flags, stage, ldv).  The caller's q / phi
+  // pointers appear only in the gather and the reception / scatter nodes;
+  // a launch with other buffers patches those nodes in the instantiated
+  // graph (cudaGraphExecKernelNodeSetParams) instead of capturing again.
   struct GraphKey {
-    const void* q;
-    void* phi;
     int R;
     uint32_t flags;
     int stage;
     int ldv;
     bool operator<(const GraphKey& o) const {
-      return std::tie(q, phi, R, flags, stage, ldv) <
-             std::tie(o.q, o.phi, o.R, o.flags, o.stage, o.ldv);
+      return std::tie(R, flags, stage, ldv) < std::tie(o.R, o.flags, o.stage, o.ldv);
     }
+  };
+  struct IoPatch {
+    cudaGraphNode_t node = nullptr;  // node of the captured graph (addresses the exec's copy)
+    std::function<cudaError_t(cudaGraphExec_t, cudaGraphNode_t, const void*, void*)> apply;
   };
   struct GraphEntry {
     cudaGraph_t graph = nullptr;  // kept alive: its nodes address the exec's nodes
     cudaGraphExec_t exec = nullptr;
     std::vector<std::pair<cudaGraphNode_t, int>> ev_nodes;  // node, slot (stage*2+end)
+    std::vector<IoPatch> io;       // nodes that read q / write phi
+    const void* q = nullptr;       // buffers the exec currently addresses
+    void* phi = nullptr;
+    uint64_t gen = 0;              // workspace generation it was captured against
   };
   std::map<GraphKey, GraphEntry> graphs;
+  std::vector<IoPatch>* capturing_io = nullptr;  // set while a graph is being captured
+  int64_t graph_captures = 0;                    // diagnostics (NESA_STAT_GRAPH_CAPTURES)
   int kernels_per_matvec = 0;
 
   // profiling: per matvec a set of 2*NESA_N_STAGES events
@@ -470,26 +403,24 @@ struct nesa_plan {
   bool trace = false;                       // NESA_TRACE: an event after every kernel
   std::vector<std::string> trace_names;
 
-  ~nesa_plan() {
-    cudaSetDevice(device);
+  void drop_graphs() {
     for (auto& kv : graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
     }
+    graphs.clear();
+  }
+
+  ~nesa_plan() {
+    cudaSetDevice(device);
+    drop_graphs();
     for (auto& v : prof_events)
       for (auto e : v) cudaEventDestroy(e);
     for (auto e : cap_events)
       if (e) cudaEventDestroy(e);
     if (ev_sfine) cudaEventDestroy(ev_sfine);
-    if (ev_mark) cudaEventDestroy(ev_mark);
     if (ev_tfine) cudaEventDestroy(ev_tfine);
     if (s2) cudaStreamDestroy(s2);
-    if (s3) cudaStreamDestroy(s3);
-    if (ev_fork2) cudaEventDestroy(ev_fork2);
-    if (ev_gfork) cudaEventDestroy(ev_gfork);
-    for (auto e : ev_lv)
-      if (e) cudaEventDestroy(e);
-    if (ev_join2) cudaEventDestroy(ev_join2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (s0) cudaStreamDestroy(s0);
@@ -625,11 +556,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   } else {
     P->tc = false;
   }
-  // quadrant slots per round: keep the level kernels <= ~96 KB so they can
-  // co-reside with the persistent near-field CTAs (~110 KB) on one SM
-  P->qs = 2;
-  while (P->qs > 1 && level_smem_bytes<T>(Q, P->qs) > 96 * 1024) P->qs /= 2;
-  require(level_smem_bytes<T>(Q, 1) <= 200 * 1024 && tgemm_smem_bytes<T, 4>(Q) <= 200 * 1024,
+  require(fused_smem_bytes<T>(Q, 4) <= 200 * 1024 && tgemm_smem_bytes<T, 4>(Q) <= 200 * 1024,
           "Q too large for the far-field kernels");
   // per-level gather tables (see nesa_kernels.cuh "Level transfers")
   P->down_order.resize(nlev);
@@ -707,37 +634,6 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->fused_anc.upload(anc);
     P->fused_cnt.alloc(size_t(G));    // zero-filled
     P->fused_state.alloc(size_t(G));
-    if (P->coarse_mega && P->leaf_begin == 0 && P->leaf_end == P->NL) {
-      const int64_t nnz = d->int_ptr[G];
-      std::vector<int32_t> es(static_cast<size_t>(std::max<int64_t>(nnz, 1)), 0),
-          ed(static_cast<size_t>(std::max<int64_t>(nnz, 1)), 0);
-      for (int64_t e = 0; e < nnz; ++e) {
-        es[size_t(e)] = int32_t(d->int_idx[e]);
-        ed[size_t(e)] = int32_t(d->int_dtab[e]);
-      }
-      P->e_src.upload(es);
-      P->e_dt.upload(ed);
-      std::vector<int32_t> gl(static_cast<size_t>(G), -1), tq, lc;
-      for (int lv = P->l0; lv <= P->L; ++lv) {
-        const int lj = lv - P->l0;
-        for (int64_t g = P->loc_first[lj]; g < P->loc_first[lj] + P->loc_count[lj]; ++g) gl[size_t(g)] = lv;
-      }
-      for (int lv = P->fused_lf; lv >= P->l0; --lv) {
-        const int lj = lv - P->l0;
-        for (int64_t g = P->loc_first[lj]; g < P->loc_first[lj] + P->loc_count[lj]; ++g)
-          tq.push_back(int32_t(g));
-      }
-      for (int lv = P->l0; lv <= P->fused_lf; ++lv) lc.push_back(int32_t(P->loc_count[lv - P->l0]));
-      P->glevel.upload(gl);
-      P->mega_tq.upload(tq);
-      P->mega_lcount.upload(lc);
-      P->mega_nt = int64_t(tq.size());
-      P->mega_head.alloc(1);
-      P->mega_ldone.alloc(lc.size());
-      P->mega_tdone.alloc(size_t(G));
-      P->mega_ctl.alloc(4);
-      P->mega_ready = true;
-    }
   }
   // wide levels (>= split_lv) get their translation on a side stream as soon
   // as their source amplitudes are final (see enqueue_T)
@@ -748,10 +644,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   if (P->fused_lf > P->l0 && P->split_lv <= P->fused_lf) P->split_lv = P->fused_lf + 1;
   {
     std::vector<int32_t> ids;  // fine levels first
-    P->red_start.assign(size_t(nlev) + 1, 0);
     for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
-      P->red_start[li] = int64_t(ids.size());
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         ids.push_back(int32_t(g));
       if (lv == P->split_lv) P->n_red_fine = int64_t(ids.size());
@@ -877,25 +771,12 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
   }
-  {
-    int ng = P->near_waves * P->near_ctas * P->n_sm;
-    if (const char* e = std::getenv("NESA_NEAR_GRID")) ng = std::max(1, std::atoi(e));
-    if (P->near_units > 0) ng = P->near_units;
-    chunk_and_balance(hn, es, ng, P->near_ab, P->near_ncw * 32);
-  }
+  // near field: two persistent CTAs per SM (4 consumer warps, 2 x 24 KB ring);
+  // V / U: the generic 8-warp, 3 x 16 KB geometry
+  chunk_and_balance(hn, es, kBGPerSM * P->n_sm, kNearABytes, kNearNCW * 32);
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
-  P->nearset.ncw = P->near_ncw;
-  P->nearset.ab = P->near_ab;
-  P->nearset.nst = P->near_nst;
-  if (P->near_units > 0 && P->near_ctas == 2) {
-    P->nearset.n_units = P->nearset.grid;
-    P->nearset.launch_grid = kBGPerSM * P->n_sm;
-    P->nearset.sm_skip = P->near_sm_skip;
-    P->nearset.smem = P->near_smem;
-    P->nearset.wq.alloc(2);
-  }
   if (!P->v_mom) upload_blockset<T>(P->Vset, hv);
   upload_blockset<T>(P->Uset, hu);
 
@@ -982,75 +863,6 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
       }
       P->mom_A.upload(A);
-      // default: A^ applied inside the moment kernel (MU_OUT = false; measured 531 vs
-      // 545 us at C4 with FFMA2: one launch less on the critical path);
-      // NESA_MOM_INKERNEL=0 selects the separate 64 x 80 moment-map GEMM
-      const char* mi = std::getenv("NESA_MOM_INKERNEL");
-      if (Q == 64 && mi && std::atoi(mi) == 0) {
-        const int need = 2 * P->v_nm - 1;
-        P->mom_kt = need <= 80 ? 80 : (need <= 127 ? 128 : 0);  // nm <= 64 (16 per lane)
-      }
-      if (P->mom_kt) {
-        // rows: 0 -> F_k (times -log r mu_0), 2m-1 -> Re A_km, 2m -> -Im A_km
-        std::vector<float> AT(size_t(P->mom_kt) * Q, 0.f);
-        for (int k = 0; k < Q; ++k) {
-          AT[k] = A[k].x;
-          for (int m = 1; m < P->v_nm; ++m) {
-            AT[size_t(2 * m - 1) * Q + k] = A[size_t(m) * Q + k].x;
-            AT[size_t(2 * m) * Q + k] = -A[size_t(m) * Q + k].y;
-          }
-        }
-        P->momAT.upload(AT);
-        // leaf level wide (warp-tiled level kernels): fold the leaf transfer
-        // into the same GEMM, Y = [A^; C_q A^] mu^ -> s and T in one pass
-        // (one stacked 128 x 80 map per child quadrant q, formed in float64)
-        const int li = P->L - P->l0;
-        const bool leaf_wide = P->L > P->l0 && P->loc_count[li] >= P->wide_level;
-        // (measured neutral at C4: the 128-row GEMM costs what the leaf level
-        // kernel did; opt in with NESA_RAD_UP=1)
-        const char* ru = std::getenv("NESA_RAD_UP");
-        if (P->mom_kt == 80 && leaf_wide && ru && std::atoi(ru) != 0) {
-          const int kt = 80;
-          std::vector<double> ATd(size_t(kt) * Q, 0.0);  // ATd[j][i] = A^[i][j]
-          for (int i = 0; i < Q; ++i) {
-            ATd[i] = Ad[2 * size_t(i)];
-            for (int m = 1; m < P->v_nm; ++m) {
-              ATd[size_t(2 * m - 1) * Q + i] = Ad[2 * (size_t(m) * Q + i)];
-              ATd[size_t(2 * m) * Q + i] = -Ad[2 * (size_t(m) * Q + i) + 1];
-            }
-          }
-          std::vector<float> RT(size_t(4) * kt * 128, 0.f);
-          for (int q = 0; q < 4; ++q) {
-            const double* Cq = d->C + (size_t(li - 1) * 4 + q) * Q * Q;
-            float* M = RT.data() + size_t(q) * kt * 128;
-            for (int j = 0; j < kt; ++j) {
-              for (int k = 0; k < Q; ++k) M[size_t(j) * 128 + k] = float(ATd[size_t(j) * Q + k]);
-              for (int k = 0; k < Q; ++k) {
-                double acc = 0;
-                for (int i = 0; i < Q; ++i) acc += Cq[size_t(k) * Q + i] * ATd[size_t(j) * Q + i];
-                M[size_t(j) * 128 + Q + k] = float(acc);
-              }
-            }
-          }
-          P->radT.upload(RT);
-          std::vector<TUnit> units;
-          std::vector<TEnt> ents;
-          for (int q = 0; q < 4; ++q) {
-            std::vector<TEnt> v;
-            for (int64_t a = lb; a < le; ++a)
-              if (d->quad[a] == q) v.push_back(TEnt{int32_t(a), int32_t(a)});
-            for (size_t i = 0; i < v.size(); i += 32) {
-              const size_t j = std::min(v.size(), i + 32);
-              units.push_back(TUnit{q, int32_t(ents.size()), int32_t(ents.size() + (j - i)), 0});
-              ents.insert(ents.end(), v.begin() + i, v.begin() + j);
-            }
-          }
-          P->rad_units.upload(units);
-          P->rad_ents.upload(ents);
-          P->n_rad_units = int(units.size());
-          P->rad_up = true;
-        }
-      }
     }
     if (P->u_mf) {
       const int ne = P->u_nt + 1;
@@ -1064,8 +876,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       P->exp_E.upload(E);
       // Q = 64 with tensor cores: beta^ = E^ o for all leaves as one GEMM;
       // E^ rows 0 -> 1 (sum of o), 2m-1 / 2m -> Re / Im of (1/m) e^{-i m theta_k}
-      const char* ri = std::getenv("NESA_RECV_INKERNEL");
-      if (Q == 64 && P->tc && 2 * P->u_nt + 1 <= 64 && !(ri && std::atoi(ri) != 0)) {
+      if (Q == 64 && P->tc && 2 * P->u_nt + 1 <= 64) {
         auto tf32 = [](float x) {
           uint32_t u;
           std::memcpy(&u, &x, 4);
@@ -1090,17 +901,10 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         P->ETC.upload(h);
         P->beta_tc = true;
       }
-      // leaf level handled by the wide kernels: fuse its downward transfer,
-      // beta^ = E^ o and the reception into one kernel (no o / beta round trip)
-      const char* rf = std::getenv("NESA_RECV_FUSED");
+      // leaf level handled by the wide kernels: its downward transfer and
+      // beta^ = E^ o in one kernel (no o round trip before the reception)
       const bool leaf_wide = P->L > P->l0 && P->loc_count[P->L - P->l0] >= P->wide_level;
-      // (measured slower at C4, 641 vs 627 us: 8 warps per SM cannot hide the
-      // point loads the separate 48-warp reception kernel hides; opt in with
-      // NESA_RECV_FUSED=1)
-      const char* bf = std::getenv("NESA_BETA_FUSED");
-      const bool want_recv = rf && std::atoi(rf) != 0;
-      const bool want_beta = !want_recv && P->beta_tc && !(bf && std::atoi(bf) == 0);
-      if (Q == 64 && leaf_wide && 2 * P->u_nt + 1 <= 64 && (want_recv || want_beta)) {
+      if (Q == 64 && leaf_wide && P->beta_tc) {
         std::vector<float> et(64 * 64, 0.f);
         for (int row = 0; row < 64; ++row)
           for (int k = 0; k < 64; ++k) {
@@ -1112,17 +916,15 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
             et[size_t(k) * 64 + row] = x;
           }
         P->ET.upload(et);
-        P->recv_fused = want_recv;
-        P->beta_fused = want_beta;
+        P->beta_fused = true;
       }
     }
-    if (P->mom_kt || P->beta_tc) {
+    if (P->beta_tc) {
       // one entry per local leaf (src = dst = leaf), 32 leaves per unit
       std::vector<TUnit> units;
       std::vector<TEnt> ents;
       for (int64_t a = lb; a < le; ++a) ents.push_back(TEnt{int32_t(a), int32_t(a)});
-      int per = 32;  // one pass of 32 leaves per CTA: the GEMM is latency-bound
-      if (const char* e = std::getenv("NESA_MOM_PER")) per = std::max(1, std::atoi(e));
+      const int per = 32;  // one pass of 32 leaves per CTA: the GEMM is latency-bound
       for (size_t i = 0; i < ents.size(); i += per)
         units.push_back(TUnit{0, int32_t(i), int32_t(std::min(ents.size(), i + per)), 0});
       P->mom_units.upload(units);
@@ -1149,18 +951,13 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     // R = 4); the tensor-core kernel loops over M = 128 tiles and amortises
     // its D load and TMEM allocation over longer units
     int per = kTUnitPasses * (tg_geom(Q).NC / 4);
-    if (P->tc) {
-      per = 128;
-      if (const char* e = std::getenv("NESA_TC_PER")) per = std::max(32, std::atoi(e));
-    }
+    if (P->tc) per = 128;
     std::vector<TEnt> ents;
     std::vector<TUnit> units;
     std::vector<std::vector<TEnt>> by_d(size_t(std::max<int64_t>(d->n_dtab, 1)));
     // levels fine -> coarse; within a level grouped by unique D
-    P->tu_start.assign(size_t(P->L - P->l0 + 2), 0);
     for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
-      P->tu_start[li] = int(units.size());
       std::vector<int64_t> used;
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
@@ -1186,55 +983,6 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     P->tunits.upload(units);
     P->tents.upload(ents);
     P->n_tunits = int(units.size());
-    if (P->pat && P->tc && std::is_same<T, float>::value && Q == 64 && !P->split_levels) {
-      std::vector<PUnit> pu;
-      std::vector<int32_t> tg, did, src;
-      for (int lv = P->L; lv >= P->l0; --lv) {
-        const int li = lv - P->l0;
-        std::map<std::vector<int32_t>, std::vector<int64_t>> pats;
-        for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g) {
-          std::vector<int32_t> key;
-          for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) key.push_back(int32_t(d->int_dtab[e]));
-          std::sort(key.begin(), key.end());
-          require(std::adjacent_find(key.begin(), key.end()) == key.end(), "repeated D in one interaction list");
-          if (key.empty()) key.push_back(int32_t(d->n_dtab));  // zero matrix
-          pats[key].push_back(g);
-        }
-        for (auto& kv : pats) {
-          const std::vector<int32_t>& key = kv.first;
-          const std::vector<int64_t>& gs = kv.second;
-          for (size_t i = 0; i < gs.size(); i += 128) {
-            const size_t j = std::min(gs.size(), i + 128);
-            PUnit u{};
-            u.tgt_begin = int32_t(tg.size());
-            u.n_tgt = int32_t(j - i);
-            u.off_begin = int32_t(did.size());
-            u.n_off = int32_t(key.size());
-            u.src_begin = int32_t(src.size());
-            for (size_t t = i; t < j; ++t) tg.push_back(int32_t(gs[t]));
-            did.insert(did.end(), key.begin(), key.end());
-            for (int32_t dt : key)
-              for (size_t t = i; t < j; ++t) {
-                const int64_t g = gs[t];
-                int32_t sg = int32_t(g);  // zero pattern: any valid group
-                for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e)
-                  if (d->int_dtab[e] == dt) sg = int32_t(d->int_idx[e]);
-                src.push_back(sg);
-              }
-            pu.push_back(u);
-          }
-        }
-        if (lv == P->split_lv) P->n_punits_fine = int(pu.size());
-      }
-      require(src.size() < (size_t(1) << 31), "too many pattern sources");
-      P->punits.upload(pu);
-      P->ptgt.upload(tg);
-      P->pdid.upload(did);
-      P->psrc.upload(src);
-      P->n_punits = int(pu.size());
-    } else {
-      P->pat = false;
-    }
   }
 }
 
@@ -1243,11 +991,13 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
 template <typename T>
 void ensure_workspace(nesa_plan* P, int R) {
   if (P->ws_R >= R) return;
+  // every captured graph addresses the old buffers: drop them (an exec still
+  // in flight is freed by the driver when it completes; cudaFree below
+  // synchronises the device first)
+  P->drop_graphs();
   const size_t es = sizeof(T);
   P->qt.alloc(size_t(P->N) * R * es);
   P->phin.alloc(size_t(P->N) * R * es);
-  if (P->u_mf && P->recv_far) P->phif.alloc(size_t(P->N) * R * es);
-  if (P->mom_kt) P->mu.alloc(size_t(P->NL) * P->mom_kt * R * es);
   if (P->beta_tc) P->beta.alloc(size_t(P->NL) * 64 * R * es);
   {
     const size_t fb = (size_t(P->G) * P->Q * R * es + 255) & ~size_t(255);
@@ -1256,8 +1006,9 @@ void ensure_workspace(nesa_plan* P, int R) {
     P->Tup.view(P->farws.p + fb, fb);
     P->o.view(P->farws.p + 2 * fb, fb);
   }
-  P->Y.alloc(size_t(P->pat ? 1 : std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
+  P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
   P->ws_R = R;
+  P->ws_gen++;
 }
 
 inline int grid_for(int64_t n, int threads, int cap) {
@@ -1265,75 +1016,32 @@ inline int grid_for(int64_t n, int threads, int cap) {
 }
 
 template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB = kABytes>
-void launch_blockgemv_v(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
-                      int64_t perm_offset, cudaStream_t st, int cta0 = 0, int ncta = -1) {
+BlockGemvArgs<T> blockgemv_args(const DevBlockSet& bs, const T* x, T* y, const T* base,
+                                const int64_t* perm, int ldy) {
+  return BlockGemvArgs<T>{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p, x, y,
+                          base, perm, ldy};
+}
+
+// near field (store mode): 4 consumer warps, two 24 KB stages
+template <typename T, int R>
+void launch_near(const DevBlockSet& bs, const T* x, T* y, cudaStream_t st) {
   if (bs.n_items == 0) return;
-  if (ncta < 0) ncta = bs.grid - cta0;
-  if (ncta <= 0) return;
-  BlockGemvArgs<T> a{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p + cta0, x, y,
-                     base, perm, int(perm_offset), nullptr, 0, 0};
-  size_t sm = blockgemv_smem_bytes<T, R, MODE, NST, NCW, AB>();
-  if (bs.n_units > 0 && cta0 == 0 && ncta == bs.grid) {
-    a.wq = bs.wq.p;
-    a.n_units = bs.n_units;
-    a.sm_skip = bs.sm_skip;
-    ncta = bs.launch_grid;
-    sm = std::max(sm, bs.smem);
-  }
-  blockgemv_kernel<T, R, MODE, NST, NCW, AB><<<ncta, NCW * 32 + 32, sm, st>>>(a);
-}
-
-// near-field variants (store mode): (consumer warps, stage bytes, stages)
-// (measured in the full C4 product: 4 warps x 24 KB x 2 stages 555 us, 4 x 16 KB x 3 556,
-// 4 x 32 KB x 2 580, 8 x 16 KB x 3 (the generic default) 633; fewer consumer threads and
-// larger stages amortise the per-chunk consumer overhead that bounds an SM's share)
-#define NESA_BG_VARIANTS(X)                                                                 \
-  X(4, 24576, 2) X(4, 16384, 3) X(4, 32768, 2) X(8, 32768, 2) X(4, 32768, 3) X(8, 32768, 3) \
-  X(4, 49152, 2) X(8, 24576, 4)
-
-bool bg_variant_known(int w, int b, int n) {
-  bool known = w == kNCW && b == kABytes && n == kStages;
-#define NESA_BG_KNOWN(W, B, S) known = known || (w == W && b == B && n == S);
-  NESA_BG_VARIANTS(NESA_BG_KNOWN)
-#undef NESA_BG_KNOWN
-  return known;
-}
-
-template <typename T, int R, int MODE, int NST = kStages>
-void launch_blockgemv(const DevBlockSet& bs, const T* x, T* y, const T* base, const int64_t* perm,
-                      int64_t perm_offset, cudaStream_t st, int cta0 = 0, int ncta = -1) {
-  if constexpr (MODE == kModeStore && NST == kStages) {
-#define NESA_BG_CASE(W, B, S)                                                                      \
-  if (bs.ncw == W && bs.ab == B && bs.nst == S) {                                                  \
-    launch_blockgemv_v<T, R, MODE, S, W, B>(bs, x, y, base, perm, perm_offset, st, cta0, ncta); \
-    return;                                                                                        \
-  }
-    NESA_BG_VARIANTS(NESA_BG_CASE)
-#undef NESA_BG_CASE
-  }
-  launch_blockgemv_v<T, R, MODE, NST>(bs, x, y, base, perm, perm_offset, st, cta0, ncta);
+  blockgemv_kernel<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>
+      <<<bs.grid, kNearNCW * 32 + 32, blockgemv_smem_bytes<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>(),
+         st>>>(blockgemv_args<T, R, kModeStore>(bs, x, y, nullptr, nullptr, 0));
 }
 
 template <typename T, int R>
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
-  // NESA_CARVEOUT=c (0..100): every kernel asks for the same shared-memory
-  // carveout (measured: the driver default is faster for this schedule)
-  int carve = -1;
-  if (const char* e = std::getenv("NESA_CARVEOUT")) carve = std::atoi(e);
-  auto attr = [carve](auto* fn, int smem) {
-    if (smem >= 0)
-      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    if (carve >= 0)
-      CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  auto attr = [](auto* fn, int smem) {
+    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   };
-  attr(blockgemv_kernel<T, R, kModeStore>, 113 * 1024);
-#define NESA_BG_ATTR(W, B, S) attr(blockgemv_kernel<T, R, kModeStore, S, W, B>, 113 * 1024);
-  NESA_BG_VARIANTS(NESA_BG_ATTR)
-#undef NESA_BG_ATTR
+  attr(blockgemv_kernel<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>,
+       int(blockgemv_smem_bytes<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>()));
+  attr(blockgemv_kernel<T, R, kModeStore>, int(blockgemv_smem_bytes<T, R, kModeStore>()));
   attr(blockgemv_kernel<T, R, kModeScatter>, int(blockgemv_smem_bytes<T, R, kModeScatter>()));
-  attr(blockgemv_kernel<T, R, kModeStore, 6>, int(blockgemv_smem_bytes<T, R, kModeStore, 6>()));
   const int lim = 220 * 1024;
   attr(tgemm_kernel<T, R>, lim);
   attr(tgemm_wt_kernel<T, R, 64>, lim);
@@ -1341,39 +1049,18 @@ void set_smem_attrs() {
   attr(level_wt_kernel<T, R, 64, kLvlUpLeaf>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlUpSum>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDown>, lim);
-  attr(level_wt_kernel<T, R, 64, kLvlDownRecv>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDownBeta>, lim);
-  attr(level_kernel<T, R, kLvlUpLeaf>, lim);
-  attr(level_kernel<T, R, kLvlUpSum>, lim);
-  attr(level_kernel<T, R, kLvlDown>, lim);
-  attr(gather_kernel<T, R>, -1);
-  attr(scatter_kernel<T, R>, -1);
-  attr(reduce_kernel<T, R>, -1);
-  attr(sum_children_kernel<T, R>, -1);
-  if constexpr (std::is_same<T, float>::value) attr(tgemm_pat_kernel<R>, int(pat_smem_bytes<R>()));
   attr(fused_up_kernel<T, R>, lim);
   attr(fused_down_kernel<T, R>, lim);
-  attr(coarse_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
     attr(radiation_mom_kernel<R>, lim);
-    attr(radiation_mom_kernel<R, false, 0, 4>, lim);
-    attr(radiation_mom_kernel<R, false, 20 / R, 4>, lim);
-    attr(radiation_mom_kernel<R, true>, lim);
-    attr(tgemm_wt_kernel<float, R, 64, 80>, lim);
-    attr(tgemm_wt_kernel<float, R, 128, 80, 64>, lim);
-    attr(tgemm_tc_kernel<R>, int(kTcSmem));
     attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_tc3_kernel<R>, int(tc2_smem_bytes<R>()));
-    attr(tgemm_tc3_kernel<R, 3>, int(tc2_smem_bytes<R>()));
-    attr(tgemm_wt_kernel<float, R, 64, 128>, lim);
-    attr(reception_exp_kernel<R>, lim);
+    attr(reception_exp_kernel<R, false>, lim);
     attr(reception_exp_kernel<R, true>, lim);
-    attr(reception_exp_kernel<R, true, 6>, lim);
-    attr(reception_exp_kernel<R, true, 8>, lim);
   }
   done = true;
 }
-
 
 // Record a profiling event; during capture this becomes an event-record node
 // on the stream the neighbouring kernels run on.
@@ -1386,8 +1073,8 @@ void prof_mark(nesa_plan* P, bool profile, int slot, cudaStream_t st) {
 // prologue while the previous kernel of the stream drains; it calls
 // pdl_wait() before touching that kernel's outputs.
 template <typename... KArgs, typename... Args>
-void launch_pdl(bool pdl, void (*kernel)(KArgs...), int grid, int block, size_t smem,
-                cudaStream_t st, Args&&... args) {
+void launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(unsigned(block));
@@ -1397,131 +1084,100 @@ void launch_pdl(bool pdl, void (*kernel)(KArgs...), int grid, int block, size_t 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+template <typename Tuple, size_t... I>
+void tuple_ptrs(Tuple& t, void** out, std::index_sequence<I...>) {
+  ((out[I] = static_cast<void*>(&std::get<I>(t))), ...);
+}
+
+// Launch a kernel that reads the caller's q or writes the caller's phi.
+// `make(q, phi)` builds its arguments; during a capture the node is
+// recorded with a closure that re-points it at other buffers in the
+// instantiated graph (run_block), so the graph cache is keyed without the
+// caller's pointers.
+template <typename F, typename... KArgs>
+void io_launch(nesa_plan* P, void (*kern)(KArgs...), int grid, int block, size_t smem,
+               cudaStream_t st, F make, const void* q, void* phi) {
+  std::tuple<KArgs...> args = make(q, phi);
+  std::apply([&](auto&... a) { kern<<<grid, block, smem, st>>>(a...); }, args);
+  CUDA_OK(cudaGetLastError());
+  if (!P->capturing_io) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CUDA_OK(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd));
+  require(cs == cudaStreamCaptureStatusActive && nd == 1, "io kernel node not found in the capture");
+  nesa_plan::IoPatch io;
+  io.node = deps[0];
+  io.apply = [kern, grid, block, smem, make](cudaGraphExec_t ex, cudaGraphNode_t node, const void* q2,
+                                             void* phi2) {
+    std::tuple<KArgs...> a2 = make(q2, phi2);
+    void* ptrs[sizeof...(KArgs) > 0 ? sizeof...(KArgs) : 1];
+    tuple_ptrs(a2, ptrs, std::index_sequence_for<KArgs...>{});
+    cudaKernelNodeParams p = {};
+    p.func = reinterpret_cast<void*>(kern);
+    p.gridDim = dim3(unsigned(grid));
+    p.blockDim = dim3(unsigned(block));
+    p.sharedMemBytes = unsigned(smem);
+    p.kernelParams = ptrs;
+    return cudaGraphExecKernelNodeSetParams(ex, node, &p);
+  };
+  P->capturing_io->push_back(std::move(io));
 }
 
 constexpr int kExpCtasPerSM = 12;  // reception: leaves are latency-bound, keep many warps
 constexpr int kMomCtasPerSM = 4;
+constexpr int kMomBufPoints = 800;  // points staged per warp by the moment kernel
 
 // s = V qt: outgoing moments (float32 plans from geometry) or stored V
 template <typename T, int R>
-int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st,
-                     const int64_t* qperm = nullptr) {
+int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value) {
     if (P->v_mom) {
       const int64_t nleaf = P->leaf_end - P->leaf_begin;
       const int64_t per_cta = int64_t(kExpWarps) * kMomLeavesPerWarp;
-      int mcta = kMomCtasPerSM;
-      if (const char* e = std::getenv("NESA_MOM_CTAS")) mcta = std::max(1, std::atoi(e));
       const int grid = int(std::max<int64_t>(
-          1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(mcta) * P->n_sm)));
-      // point staging (cp.async) helps alone but costs shared memory the
-      // concurrent near field needs; NESA_MOM_BUF sets the staged points
-      // per warp (0: none)
-      int bufpts = P->mom_buf;
+          1, std::min<int64_t>((nleaf + per_cta - 1) / per_cta, int64_t(kMomCtasPerSM) * P->n_sm)));
       const size_t sm = size_t(kExpWarps) *
-                        (size_t(bufpts) * (2 + R) + size_t(kMomLeavesPerWarp) * ((P->v_nm * R + 1) & ~1) * 2) *
+                        (size_t(kMomBufPoints) * (2 + R) +
+                         size_t(kMomLeavesPerWarp) * ((P->v_nm * R + 1) & ~1) * 2) *
                         sizeof(float);
-      if (P->mom_kt) {
-        float* mu = reinterpret_cast<float*>(P->mu.p);
-        radiation_mom_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
-            P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, mu, P->leaf_begin,
-            nleaf, P->Q, P->v_nm, P->mom_kt, bufpts);
-        if (P->rad_up)
-          tgemm_wt_kernel<float, R, 128, 80, 64><<<P->n_rad_units, 128, TGW<float, R, 128, 80>::SMEM, st>>>(
-              P->rad_units.p, P->rad_ents.p, P->radT.p, mu, s, reinterpret_cast<float*>(P->Tup.p));
-        else if (P->mom_kt == 80)
-          tgemm_wt_kernel<float, R, 64, 80><<<P->n_mom_units, 128, TGW<float, R, 64, 80>::SMEM, st>>>(
-              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s, nullptr);
-        else
-          tgemm_wt_kernel<float, R, 64, 128><<<P->n_mom_units, 128, TGW<float, R, 64, 128>::SMEM, st>>>(
-              P->mom_units.p, P->mom_ents.p, P->momAT.p, mu, s, nullptr);
-        return 2;
-      }
-      // register budget for 4 CTAs / SM (<= 128 registers, no spills): at the
-      // natural 169 registers only 2 CTAs fit (measured 531 vs 537 us at C4);
-      // NESA_MOM_VARIANT=1: uncapped, 3: half the moments per pass (capped)
-      auto go = [&](auto kern) {
-        kern<<<grid, 32 * kExpWarps, sm, st>>>(P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p,
-                                                P->mom_A.p, qt, s, P->leaf_begin, nleaf, P->Q, P->v_nm, 0,
-                                                bufpts, qperm);
-      };
-      switch (P->mom_variant) {
-        case 1: go(radiation_mom_kernel<R>); break;
-        case 3: go(radiation_mom_kernel<R, false, 20 / R, 4>); break;
-        default: go(radiation_mom_kernel<R, false, 0, 4>); break;
-      }
+      radiation_mom_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
+          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->mom_A.p, qt, s, P->leaf_begin,
+          nleaf, P->Q, P->v_nm, kMomBufPoints);
       return 1;
     }
   }
-  launch_blockgemv<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0, st);
-  return 1;
-}
-
-// phi[perm] = phin + U o through the incoming expansion (float32 plans)
-template <int R>
-int launch_reception_exp(nesa_plan* P, const float* o, const float* phin, const int64_t* perm,
-                         float* phi, int ldp, cudaStream_t st) {
-  const int64_t nleaf = P->leaf_end - P->leaf_begin;
-  int rcta = kExpCtasPerSM;
-  if (const char* e = std::getenv("NESA_RECV_CTAS")) rcta = std::max(1, std::atoi(e));
-  const int grid = int(std::max<int64_t>(
-      1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(rcta) * P->n_sm)));
-  const int Q = P->Q, nt = P->u_nt;
-  const size_t nb = ((size_t(nt) + 1) * R + 1) & ~size_t(1);
-  const size_t sm = size_t(kExpWarps) * (nb + ((size_t(Q) * R + 3) & ~size_t(3)) / 2) * sizeof(float2);
-  if (P->beta_tc) {
-    // beta^ = E^ o for every leaf on the tensor cores (or already by the fused
-    // leaf-level kernel), then the per-point series
-    float* beta = reinterpret_cast<float*>(P->beta.p);
-    if (P->beta_fused)
-      ;
-    else if (P->tc2)
-      tgemm_tc2_kernel<R><<<P->n_mom_units, 128, tc2_smem_bytes<R>(), st>>>(P->mom_units.p, P->mom_ents.p,
-                                                                           P->ETC.p, o, beta);
-    else
-      tgemm_tc_kernel<R><<<P->n_mom_units, 128, kTcSmem, st>>>(P->mom_units.p, P->mom_ents.p,
-                                                              P->ETC.p, o, beta);
-    if (P->recv_minb >= 8)
-      reception_exp_kernel<R, true, 8><<<grid, 32 * kExpWarps, sm, st>>>(
-          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
-          P->leaf_begin, nleaf, Q, nt, ldp);
-    else if (P->recv_minb >= 6)
-      reception_exp_kernel<R, true, 6><<<grid, 32 * kExpWarps, sm, st>>>(
-          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
-          P->leaf_begin, nleaf, Q, nt, ldp);
-    else
-      reception_exp_kernel<R, true><<<grid, 32 * kExpWarps, sm, st>>>(
-          P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, beta, phin, perm, phi,
-          P->leaf_begin, nleaf, Q, nt, ldp);
-    return P->beta_fused ? 1 : 2;
-  }
-  reception_exp_kernel<R><<<grid, 32 * kExpWarps, sm, st>>>(
-      P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p, P->exp_E.p, o, phin, perm, phi,
-      P->leaf_begin, nleaf, Q, nt, ldp);
+  if (P->Vset.n_items == 0) return 0;
+  blockgemv_kernel<T, R, kModeStore><<<P->Vset.grid, kBGThreads, blockgemv_smem_bytes<T, R, kModeStore>(), st>>>(
+      blockgemv_args<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0));
   return 1;
 }
 
 // Enqueue one product, or one of its two stages (multi-GPU), on P->s0/P->s1.
-//   stage 0: gather, fork{near | V, up, translate, down}, join, reception
-//   stage 1: gather, V, up                  (before the s halo exchange)
-//   stage 2: fork{near | translate, down}, join, reception
+//   stage 0: gather, radiation, fork{near | up, translate, down}, join, reception
+//   stage 1: gather, fork{near | radiation, up}, join  (before the s halo exchange)
+//   stage 2: translate, down, reception
 template <typename T, int R>
-int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
+int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int stage) {
   const bool near = flags & NESA_NEAR, far = flags & NESA_FAR, profn = flags & NESA_PROFILE;
   const bool prof = profn && !(flags & NESA_PROFILE_NEAR);  // stage marks on the far path
   cudaStream_t s0 = P->s0, s1 = P->s1;
-  cudaStream_t join_stream = s1;  // the near branch's last stream (s3 with a split near launch)
   T* qt = reinterpret_cast<T*>(P->qt.p);
   T* phin = reinterpret_cast<T*>(P->phin.p);
   T* s = reinterpret_cast<T*>(P->s.p);
   T* o = reinterpret_cast<T*>(P->o.p);
+  T* Tup = reinterpret_cast<T*>(P->Tup.p);
+  T* Y = reinterpret_cast<T*>(P->Y.p);
   const T* CT = reinterpret_cast<const T*>(P->CT.p);
   const T* BT = reinterpret_cast<const T*>(P->BT.p);
   const int Q = P->Q;
   const int cap = P->n_sm * 8;
   const int64_t nloc = P->pt_end - P->pt_begin;
+  const size_t mstride = P->mbytes / sizeof(T);
   int nk = 0;
   if (prof) P->trace_names.clear();
   // NESA_TRACE diagnostics: an event-record node after each kernel
@@ -1531,16 +1187,6 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     P->trace_names.emplace_back(name);
   };
 
-  const size_t mstride = P->mbytes / sizeof(T);
-  const FarGeom FG = far_geom(Q);
-  const size_t lvl_sm = level_smem_bytes<T>(Q, P->qs);
-  // groups per CTA: fill the column tile only when the level is big enough to
-  // occupy every SM twice; coarse levels get one group per CTA
-  auto tile_for = [&](int64_t count) {
-    const int64_t want = (count + 2 * P->n_sm - 1) / (2 * P->n_sm);
-    return int(std::max<int64_t>(1, std::min<int64_t>(FG.NC / R, want)));
-  };
-  T* Tup = reinterpret_cast<T*>(P->Tup.p);
   auto level_args = [&](int li, const T* M) {
     LevelArgs<T, R> la{};
     la.MT4 = M;
@@ -1554,155 +1200,91 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     la.o = o;
     la.count = P->loc_count[li];
     la.Q = Q;
-    la.QS = P->qs;
-    la.TC = tile_for(la.count);
     return la;
   };
+  const bool fused = P->fused_lf > P->l0;
+  // every level is either one of the wide (warp-tiled, Q = 64) levels at the
+  // fine end or inside the fused coarse range (see build_plan_T)
+  auto wide = [&](int lv) { return lv > P->fused_lf; };
   auto up_level = [&](int lv) {
     // children-major: T[c] = C s[c]; s[parent] = sum of its children's T
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
-    if (lv == P->L && P->rad_up) return;  // the radiation GEMM wrote the leaf T
     const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
-    const int grid = int((la.count + la.TC - 1) / la.TC);
-    if (Q == 64 && la.count >= P->wide_level) {
-      const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-      if (lv == P->L)
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64, kLvlUpLeaf>::SMEM, s0, la, RecvArgs{});
-      else
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64, kLvlUpSum>::SMEM, s0, la, RecvArgs{});
-    } else if (lv == P->L) {
-      launch_pdl(P->pdl, level_kernel<T, R, kLvlUpLeaf>, grid, kFarThreads, lvl_sm, s0, la);
-    } else {
-      launch_pdl(P->pdl, level_kernel<T, R, kLvlUpSum>, grid, kFarThreads, lvl_sm, s0, la);
-    }
+    const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
+    if (lv == P->L)
+      launch_pdl(level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64, kLvlUpLeaf>::SMEM, s0, la, RecvArgs{});
+    else
+      launch_pdl(level_wt_kernel<T, R, 64, kLvlUpSum>, gw, 128, LVW<T, R, 64, kLvlUpSum>::SMEM, s0, la, RecvArgs{});
     nk++;
-    tr(la.count >= P->wide_level && Q == 64 ? "up_wt" : "up", s0);
+    tr("up_wt", s0);
   };
-  auto top_sum = [&]() {
-    if (P->L > P->l0 && P->loc_count[0] > 0) {
-      const int64_t n = P->loc_count[0] * Q * R;
-      launch_pdl(P->pdl, sum_children_kernel<T, R>, grid_for(n, 256, cap), 256, 0, s0,
-                 (const int64_t*)P->child_first.p, (const int32_t*)P->n_child.p, P->loc_first[0],
-                 P->loc_count[0], P->loc_first[1], P->loc_first[1] + P->loc_count[1],
-                 (const T*)Tup, s, Q);
-      nk++;
-      tr("top_sum", s0);
-    }
-  };
-  T* Y = reinterpret_cast<T*>(P->Y.p);
   auto translate = [&](int u0, int u1, cudaStream_t st) {
     if (u1 <= u0) return;
+    const T* DTp = reinterpret_cast<const T*>(P->DT.p);
+    const TUnit* up = P->tunits.p + u0;
+    const bool pdl_ok = st == s0;
+    auto go = [&](auto kern, int grid, size_t smem, auto... args) {
+      if (pdl_ok)
+        launch_pdl(kern, grid, 128, smem, st, args...);
+      else
+        kern<<<grid, 128, smem, st>>>(args...);
+    };
     if constexpr (std::is_same<T, float>::value) {
-      if (P->pat) {
-        // unit ranges map to the fine / coarse pattern units
-        const int p0 = u0 == 0 ? 0 : P->n_punits_fine;
-        const int p1 = u1 == P->n_tunits ? P->n_punits : P->n_punits_fine;
-        if (p1 > p0)
-          launch_pdl(P->pdl && st == s0, tgemm_pat_kernel<R>, std::min(p1 - p0, P->pat_ctas * P->n_sm), 128,
-                     pat_smem_bytes<R>(), st, (const PUnit*)(P->punits.p + p0), p1 - p0,
-                     (const int32_t*)P->ptgt.p, (const int32_t*)P->pdid.p, (const int32_t*)P->psrc.p,
-                     (const float*)P->DTC.p, (const float*)s, o);
+      if (P->tc) {
+        go(tgemm_tc3_kernel<R>, std::min(u1 - u0, kTc3CtasPerSM * P->n_sm), tc2_smem_bytes<R>(), up,
+           u1 - u0, (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
         nk++;
         tr("translate", st);
         return;
       }
     }
-    const T* DTp = reinterpret_cast<const T*>(P->DT.p);
-    const TUnit* up = P->tunits.p + u0;
-    const bool coarse = u0 >= P->n_tunits_fine && P->split_lv <= P->L;
-    if (P->tc && !(coarse && P->coarse_tc == 0)) {
-      if constexpr (std::is_same<T, float>::value) {
-        if (P->tc2 && P->tc3_ctas > 0 && !(coarse && P->coarse_tc == 2) && P->tc3_minb >= 3)
-          launch_pdl(P->pdl && st == s0, tgemm_tc3_kernel<R, 3>,
-                     std::min(u1 - u0, P->tc3_ctas * P->n_sm), 128, tc2_smem_bytes<R>(), st, up, u1 - u0,
-                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
-        else if (P->tc2 && P->tc3_ctas > 0 && !(coarse && P->coarse_tc == 2))
-          launch_pdl(P->pdl && st == s0, tgemm_tc3_kernel<R>,
-                     std::min(u1 - u0, P->tc3_ctas * P->n_sm), 128, tc2_smem_bytes<R>(), st, up, u1 - u0,
-                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
-        else if (P->tc2)
-          launch_pdl(P->pdl && st == s0, tgemm_tc2_kernel<R>, u1 - u0, 128, tc2_smem_bytes<R>(), st, up,
-                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
-        else
-          launch_pdl(P->pdl && st == s0, tgemm_tc_kernel<R>, u1 - u0, 128, kTcSmem, st, up,
-                     (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
-      }
-    } else if (Q == 64)
-      launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 64>, u1 - u0, 128, TGW<T, R, 64>::SMEM, st,
-                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y, (T*)nullptr);
+    if (Q == 64)
+      go(tgemm_wt_kernel<T, R, 64>, u1 - u0, TGW<T, R, 64>::SMEM, up, (const TEnt*)P->tents.p, DTp,
+         (const T*)s, Y);
     else if (Q == 32)
-      launch_pdl(P->pdl && st == s0, tgemm_wt_kernel<T, R, 32>, u1 - u0, 128, TGW<T, R, 32>::SMEM, st,
-                 up, (const TEnt*)P->tents.p, DTp, (const T*)s, Y, (T*)nullptr);
+      go(tgemm_wt_kernel<T, R, 32>, u1 - u0, TGW<T, R, 32>::SMEM, up, (const TEnt*)P->tents.p, DTp,
+         (const T*)s, Y);
     else
-      tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp,
-                                                                                s, Y, Q);
+      tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp, s,
+                                                                                Y, Q);
     nk++;
     tr("translate", st);
   };
   auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st) {
     // o[g] = translation sum of the listed local groups
-    if (i1 <= i0 || P->pat) return;
-    launch_pdl(P->pdl && st == s0, reduce_kernel<T, R>, grid_for((i1 - i0) * 32, 256, cap), 256, 0,
-               st, (const int32_t*)(P->red_ids.p + i0), i1 - i0, (const int64_t*)P->int_ptr.p,
-               (const T*)Y, o, Q);
+    if (i1 <= i0) return;
+    const int grid = grid_for((i1 - i0) * 32, 256, cap);
+    const int32_t* ids = P->red_ids.p + i0;
+    const int64_t* ip = P->int_ptr.p;
+    if (st == s0)
+      launch_pdl(reduce_kernel<T, R>, grid, 256, 0, st, ids, i1 - i0, ip, (const T*)Y, o, Q);
+    else
+      reduce_kernel<T, R><<<grid, 256, 0, st>>>(ids, i1 - i0, ip, (const T*)Y, o, Q);
     nk++;
     tr("reduce", st);
   };
-  // the near field's completion joins the far stream once: before the fused
-  // leaf-level reception (recv_fused) or before finish()
-  bool near_joined = false, recv_done = false;
   const bool far_recv = far && (stage == 0 || stage == 2);
-  auto join_near = [&]() {
-    if (near_joined) return;
-    near_joined = true;
-    CUDA_OK(cudaEventRecord(P->ev_join, join_stream));
-    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
-  };
-  // fine levels: the wide downward kernels sum the translation partials Y
-  // themselves (no fine reduce pass; NESA_DOWN_YSUM=0 restores it)
-  bool ysum_down = false;
   auto down_level = [&](int lv) {
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
-    LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
-    if (ysum_down && lv >= P->split_lv) {  // translation sums formed in the down kernel
-      la.Y = Y;
-      la.yptr = P->int_ptr.p;
-    }
-    if (Q == 64 && la.count >= P->wide_level) {
-      const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
-      if (lv == P->L && P->beta_fused && far_recv) {
-        // leaf level + reception coefficients beta^ = E^ o in one kernel
-        if constexpr (std::is_same<T, float>::value) {
-          RecvArgs rv{};
-          rv.ET = P->ET.p;
-          rv.beta = reinterpret_cast<float*>(P->beta.p);
-          launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDownBeta>, gw, 128,
-                     LVW<T, R, 64, kLvlDownBeta>::SMEM, s0, la, rv);
-        }
-      } else if (lv == P->L && P->recv_fused && far_recv) {
-        // leaf level + reception coefficients + reception in one kernel: the
-        // near field must be complete (phin)
-        join_near();
-        if constexpr (std::is_same<T, float>::value) {
-          RecvArgs rv{P->ET.p, P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_r.p,
-                      near ? reinterpret_cast<const float*>(phin) : nullptr, P->perm.p,
-                      reinterpret_cast<float*>(phi), P->ldv, P->u_nt};
-          launch_pdl(false, level_wt_kernel<T, R, 64, kLvlDownRecv>, gw, 128,
-                     LVW<T, R, 64, kLvlDownRecv>::SMEM, s0, la, rv);
-        }
-        recv_done = true;
-      } else {
-        launch_pdl(P->pdl, level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64, kLvlDown>::SMEM, s0, la,
-                   RecvArgs{});
+    const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
+    const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
+    if (lv == P->L && P->beta_fused && far_recv) {
+      // leaf level + reception coefficients beta^ = E^ o in one kernel
+      if constexpr (std::is_same<T, float>::value) {
+        RecvArgs rv{};
+        rv.ET = P->ET.p;
+        rv.beta = reinterpret_cast<float*>(P->beta.p);
+        launch_pdl(level_wt_kernel<T, R, 64, kLvlDownBeta>, gw, 128, LVW<T, R, 64, kLvlDownBeta>::SMEM, s0,
+                   la, rv);
       }
     } else {
-      launch_pdl(P->pdl, level_kernel<T, R, kLvlDown>, int((la.count + la.TC - 1) / la.TC),
-                 kFarThreads, lvl_sm, s0, la);
+      launch_pdl(level_wt_kernel<T, R, 64, kLvlDown>, gw, 128, LVW<T, R, 64, kLvlDown>::SMEM, s0, la,
+                 RecvArgs{});
     }
     nk++;
-    tr(la.count >= P->wide_level && Q == 64 ? "down_wt" : "down", s0);
+    tr("down_wt", s0);
   };
   auto fused_args = [&](const T* MT) {
     FusedArgs<T> fa{};
@@ -1725,124 +1307,53 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     fa.L = P->L;
     fa.Q = Q;
     fa.D = P->fused_lf - P->l0 - 1;
-    fa.spec = P->fused_spec ? 1 : 0;
     return fa;
   };
-  const bool fused = P->fused_lf > P->l0;
   const size_t fsm = fused_smem_bytes<T>(Q, R);
   // upward transfers of the fused coarse levels + the top-level sum
   auto fused_up = [&]() {
     const FusedArgs<T> fa = fused_args(CT);
-    launch_pdl(P->pdl, fused_up_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
+    launch_pdl(fused_up_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
     nk++;
     tr("up_fused", s0);
   };
   auto fused_down = [&]() {
     const FusedArgs<T> fa = fused_args(BT);
-    launch_pdl(P->pdl, fused_down_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
+    launch_pdl(fused_down_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
     nk++;
     tr("down_fused", s0);
-  };
-  auto coarse_mega = [&]() {
-    CoarseArgs<T> ca{};
-    ca.f = fused_args(CT);
-    ca.BT = BT;
-    ca.DT = reinterpret_cast<const T*>(P->DT.p);
-    ca.int_ptr = P->int_ptr.p;
-    ca.e_src = P->e_src.p;
-    ca.e_dt = P->e_dt.p;
-    ca.glevel = P->glevel.p;
-    ca.tq = P->mega_tq.p;
-    ca.n_t = P->mega_nt;
-    ca.lvl_count = P->mega_lcount.p;
-    ca.head = P->mega_head.p;
-    ca.lvl_done = P->mega_ldone.p;
-    ca.tdone = P->mega_tdone.p;
-    ca.ctl = P->mega_ctl.p;
-    const int items = int(2 * ca.f.count + ca.n_t);
-    launch_pdl(P->pdl, coarse_kernel<T, R>, std::max(1, std::min(items, P->mega_ctas * P->n_sm)),
-               kFusedThreads, coarse_smem_bytes<T>(Q, R), s0, ca);
-    nk++;
-    tr("coarse", s0);
   };
   // Far field.  The wide (fine) levels' translation + reduce run on s2 as
   // soon as their s is final, concurrently with the coarse end of the
   // upward chain, the coarse translations and the coarse downward levels.
-  auto far_pass = [&](bool split, const std::function<void(int)>& hook) {
+  // split: fine translation on the side stream (stage 0); stage 1 / 2 split
+  // the product at the halo exchange instead
+  auto up_pass = [&](bool split) {
     const bool fine = split && P->split_lv <= P->L;
-    // per-level split: each fine level's translation + reduce goes to s2 as
-    // soon as that level's s is final (overlapping the rest of the up pass);
-    // units / red_ids are ordered fine -> coarse, level lv's range ends where
-    // level lv - 1's begins (or at the fine / total boundary)
-    const bool per_level = fine && P->split_levels;
-    auto unit_end = [&](int lv) {
-      return lv == P->split_lv ? P->n_tunits_fine : P->tu_start[lv - 1 - P->l0];
-    };
-    auto red_end = [&](int lv) {
-      return lv == P->split_lv ? P->n_red_fine : P->red_start[lv - 1 - P->l0];
-    };
     for (int lv = P->L; lv > P->l0; --lv) {
-      if (fused && lv <= P->fused_lf) break;
+      if (!wide(lv)) break;
       up_level(lv);
-      if (lv == P->L) hook(2);
-      if (per_level && lv >= P->split_lv) {
-        const int li = lv - P->l0;
-        CUDA_OK(cudaEventRecord(P->ev_lv[li], s0));
-        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_lv[li], 0));
-        translate(P->tu_start[li], unit_end(lv), P->s2);
-        reduce(P->red_start[li], red_end(lv), P->s2);
-      } else if (fine && lv == P->split_lv && !P->fine_after_up) {
-        CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
-      }
+      if (fine && lv == P->split_lv) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
     }
-    if (P->L == P->split_lv && fine && P->L == P->l0) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
-    // the coarse levels' up, translation and down in one persistent kernel
-    const bool mega = fused && fine && !per_level && P->fine_after_up == 0 && P->coarse_mega && P->mega_ready &&
-                      P->split_lv == P->fused_lf + 1 && Q * R <= 256;
-    if (mega) {
-      coarse_mega();
-    } else if (fused) {
-      fused_up();
-      if (P->fused_lf == P->L) hook(2);
-    } else {
-      top_sum();
-    }
-    hook(3);
-    if (fine && ((P->split_lv == P->l0 && P->L > P->l0) || (P->fine_after_up == 1 && !per_level)))
-      CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+    if (fused) fused_up();
+    return fine;
+  };
+  auto down_pass = [&](bool fine) {
     if (fine) {
-      if (P->fine_after_up >= 2 && !per_level) {
-        // coarse translation first (it is on the critical path and needs
-        // the SM slots the fine one would hold), then the fine one on s2
-        translate(P->n_tunits_fine, P->n_tunits, s0);
-        reduce(P->n_red_fine, P->n_red, s0);
-        CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
-        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
-        translate(0, P->n_tunits_fine, P->s2);
-        reduce(0, P->n_red_fine, P->s2);
-        CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
-      } else {
-        if (!per_level) {
-          CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
-          translate(0, P->n_tunits_fine, P->s2);
-          ysum_down = P->down_ysum && Q == 64 && !P->pat && P->split_lv >= P->l0 + 1;
-          if (!ysum_down) reduce(0, P->n_red_fine, P->s2);
-        }
-        CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
-        if (!mega) {
-          translate(P->n_tunits_fine, P->n_tunits, s0);
-          reduce(P->n_red_fine, P->n_red, s0);
-        }
-      }
+      CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
+      translate(0, P->n_tunits_fine, P->s2);
+      reduce(0, P->n_red_fine, P->s2);
+      CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
+      translate(P->n_tunits_fine, P->n_tunits, s0);
+      reduce(P->n_red_fine, P->n_red, s0);
     } else {
       translate(0, P->n_tunits, s0);
       reduce(0, P->n_red, s0);
     }
-    hook(4);
+    if (fused) fused_down();
     bool joined = !fine;
-    if (fused && !mega) fused_down();
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
-      if (fused && lv <= P->fused_lf) continue;
+      if (!wide(lv)) continue;
       if (!joined && lv >= P->split_lv) {
         CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
         joined = true;
@@ -1851,193 +1362,149 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, uint32_t flags, int stage) {
     }
     if (!joined) CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
   };
-  auto up_pass = [&]() {
-    for (int lv = P->L; lv > P->l0; --lv) {
-      if (fused && lv <= P->fused_lf) break;
-      up_level(lv);
-    }
-    if (fused)
-      fused_up();
-    else
-      top_sum();
-  };
-  auto down_pass = [&]() {
-    translate(0, P->n_tunits, s0);
-    reduce(0, P->n_red, s0);
-    if (fused) fused_down();
-    for (int lv = P->l0 + 1; lv <= P->L; ++lv)
-      if (!fused || lv > P->fused_lf) down_level(lv);
-  };
   auto gather = [&]() {
-    if (P->gather_inv)
-      gather_inv_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->iperm.p, qt, P->N, P->ldv);
-    else
-      gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s0>>>(q, P->perm.p, qt, P->N, P->ldv);
+    const int32_t* ip = P->iperm.p;
+    const int64_t n = P->N;
+    io_launch(
+        P, gather_inv_kernel<T, R>, grid_for(n, 256, cap), 256, 0, s0,
+        [=](const void* qq, void*) { return std::make_tuple(static_cast<const T*>(qq), ip, qt, n, ldv); },
+        q, phi);
     nk++;
     tr("gather", s0);
   };
   auto finish = [&]() {
-    if (recv_done) return;  // the fused leaf-level kernel wrote phi
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
+    const int64_t* pm = P->perm.p;
+    const T* base = near ? phin : nullptr;
     if (far && P->u_mf) {
-      if constexpr (std::is_same<T, float>::value)
-        nk += launch_reception_exp<R>(P, o, near ? phin : nullptr, P->perm.p, phi, P->ldv, s0);
+      if constexpr (std::is_same<T, float>::value) {
+        const int64_t nleaf = P->leaf_end - P->leaf_begin;
+        const int grid = int(std::max<int64_t>(
+            1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(kExpCtasPerSM) * P->n_sm)));
+        const int nt = P->u_nt;
+        const size_t nb = ((size_t(nt) + 1) * R + 1) & ~size_t(1);
+        const size_t sm = size_t(kExpWarps) * (nb + ((size_t(Q) * R + 3) & ~size_t(3)) / 2) * sizeof(float2);
+        const float2* prel = P->mf_prel.p;
+        const int64_t *gs = P->gstart.p, *ge = P->gstop.p;
+        const float* lr = P->mf_leaf_r.p;
+        const float2* E = P->exp_E.p;
+        const int64_t lb = P->leaf_begin;
+        if (P->beta_tc) {
+          // beta^ = E^ o for every leaf on the tensor cores (or already by the
+          // fused leaf-level kernel), then the per-point series
+          float* beta = reinterpret_cast<float*>(P->beta.p);
+          if (!P->beta_fused) {
+            tgemm_tc2_kernel<R><<<P->n_mom_units, 128, tc2_smem_bytes<R>(), s0>>>(
+                P->mom_units.p, P->mom_ents.p, P->ETC.p, o, beta);
+            nk++;
+          }
+          io_launch(
+              P, reception_exp_kernel<R, true>, grid, 32 * kExpWarps, sm, s0,
+              [=](const void*, void* pp) {
+                return std::make_tuple(prel, gs, ge, lr, E, (const float*)beta, (const float*)base, pm,
+                                       static_cast<float*>(pp), lb, nleaf, Q, nt, ldv);
+              },
+              q, phi);
+        } else {
+          io_launch(
+              P, reception_exp_kernel<R, false>, grid, 32 * kExpWarps, sm, s0,
+              [=](const void*, void* pp) {
+                return std::make_tuple(prel, gs, ge, lr, E, (const float*)o, (const float*)base, pm,
+                                       static_cast<float*>(pp), lb, nleaf, Q, nt, ldv);
+              },
+              q, phi);
+        }
+        nk++;
+      }
     } else if (far) {
-      launch_blockgemv<T, R, kModeScatter>(P->Uset, o, phi, near ? phin : nullptr, P->perm.p,
-                                           P->ldv, s0);
-      nk++;
-    } else if (near) {
-      scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
-          phin, nullptr, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
-      nk++;
+      const DevBlockSet& U = P->Uset;
+      if (U.n_items > 0) {
+        io_launch(
+            P, blockgemv_kernel<T, R, kModeScatter>, U.grid, kBGThreads,
+            blockgemv_smem_bytes<T, R, kModeScatter>(), s0,
+            [=, &U](const void*, void* pp) {
+              return std::make_tuple(blockgemv_args<T, R, kModeScatter>(U, o, static_cast<T*>(pp), base, pm, ldv));
+            },
+            q, phi);
+        nk++;
+      }
     } else {
-      scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
-          nullptr, nullptr, P->perm.p, phi, P->pt_begin, nloc, P->ldv);
+      const int64_t pb = P->pt_begin;
+      io_launch(
+          P, scatter_kernel<T, R>, grid_for(nloc, 256, cap), 256, 0, s0,
+          [=](const void*, void* pp) {
+            return std::make_tuple(base, (const T*)nullptr, pm, static_cast<T*>(pp), pb, nloc, ldv);
+          },
+          q, phi);
       nk++;
     }
     tr("finish", s0);
     prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
   };
+  auto fork_near = [&]() {
+    CUDA_OK(cudaEventRecord(P->ev_fork, s0));
+    CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
+    if (!near) return;
+    prof_mark(P, profn, 2 * NESA_STAGE_NEAR, s1);
+    launch_near<T, R>(P->nearset, qt, phin, s1);
+    nk++;
+    prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, s1);
+    tr("near", s1);
+  };
+  auto join_near = [&]() {
+    CUDA_OK(cudaEventRecord(P->ev_join, s1));
+    CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
+  };
 
   if (stage == 0) {
-    // gather -> radiation (full bandwidth) -> fork {near | up, translate,
-    // down: compute-bound, overlaps the memory-bound near field} -> join ->
-    // reception + scatter
+    // gather -> radiation (the far chain is the critical path: it gets the
+    // GPU first) -> fork {near | up, translate, down} -> join -> reception
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
-    // Near branch: forks from s0 at position `near_after` (-1/-2: before the
-    // radiation; 0/1: after it; -1 and 1 add a no-op event node so the
-    // far-field kernel is launched -- and resident -- before the persistent
-    // near-field CTAs; 2: after the leaf-level upward kernel; 3: after the
-    // upward pass; 4: after translation).
-    bool forked = false;
-    const bool nsplit = near && far && P->near_split > 0 && P->near_ctas != 1 && P->nearset.grid > 1;
-    const int n_a = nsplit ? std::max(1, std::min(P->nearset.grid - 1,
-                                                   int(P->near_frac * P->nearset.grid + 0.5)))
-                           : P->nearset.grid;
-    if (nsplit) join_stream = P->s3;
-    auto launch_near = [&]() {
-      if (forked) return;
-      forked = true;
-      CUDA_OK(cudaEventRecord(P->ev_fork, s0));
-      CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
-      if (!near) return;
-      if (profn)
-        prof_mark(P, profn, 2 * NESA_STAGE_NEAR, s1);
-      else if (P->near_after == 1 || P->near_after == -1)
-        CUDA_OK(cudaEventRecordWithFlags(P->ev_mark, s1, cudaEventRecordExternal));
-      if (P->near_ctas == 1 && P->near_nst == kStages && P->near_ncw == kNCW && P->near_ab == kABytes)
-        launch_blockgemv<T, R, kModeStore, 6>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
-      else if (nsplit)
-        launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1, 0, n_a);
-      else
-        launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
-      nk++;
-      if (!nsplit) prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, s1);
-      tr("near", s1);
-    };
-    // optional second near-field launch (the remaining CTAs' items) forked
-    // from the far chain at hook position near_split, on its own stream
-    bool forked2 = false;
-    auto launch_near2 = [&]() {
-      if (!nsplit || forked2) return;
-      forked2 = true;
-      CUDA_OK(cudaEventRecord(P->ev_fork2, s0));
-      CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_fork2, 0));
-      launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, P->s3, n_a);
-      nk++;
-      CUDA_OK(cudaEventRecord(P->ev_join2, P->s1));
-      CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_join2, 0));
-      prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, P->s3);
-    };
-    // float32 moment radiation reading q in the original order: the gather
-    // (only the near field needs tree-ordered q) moves to the near stream
-    const bool rad_direct = std::is_same<T, float>::value && far && near && P->v_mom && P->rad_direct &&
-                            P->near_after == 0 && !nsplit && P->ldv == R && P->mom_kt == 0;
-    if (rad_direct) {
-      CUDA_OK(cudaEventRecord(P->ev_gfork, s0));
-      CUDA_OK(cudaStreamWaitEvent(s1, P->ev_gfork, 0));
-      if (P->gather_inv)
-        gather_inv_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s1>>>(q, P->iperm.p, qt, P->N, P->ldv);
-      else
-        gather_kernel<T, R><<<grid_for(P->N, 256, cap), 256, 0, s1>>>(q, P->perm.p, qt, P->N, P->ldv);
-      nk++;
-    } else {
-      gather();
-    }
-    if (far && P->near_after < 0) launch_near();
+    gather();
     if (far) {
       prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
-      nk += rad_direct ? launch_radiation<T, R>(P, q, s, s0, P->perm.p) : launch_radiation<T, R>(P, qt, s, s0);
+      nk += launch_radiation<T, R>(P, qt, s, s0);
       tr("radiation", s0);
     }
-    if (!far || P->near_after <= 1) launch_near();
-    // float32 + near + far: the (compute-bound) matrix-free reception runs at
-    // the end of the far branch into phif, overlapping the near field; the
-    // join is followed by one combining scatter phi[perm] = phin + phif.
-    const bool rfar = far && near && P->u_mf && P->recv_far && !P->recv_fused && std::is_same<T, float>::value;
+    fork_near();
     if (far) {
-      far_pass(P->split, [&](int pos) {
-        if (pos == P->near_after) launch_near();
-        if (pos == P->near_split) launch_near2();
-      });
-      launch_near2();
-      launch_near();
+      const bool fine = up_pass(true);
+      down_pass(fine);
       prof_mark(P, prof, 2 * NESA_STAGE_FAR + 1, s0);
-      if (rfar) {
-        if constexpr (std::is_same<T, float>::value) {
-          prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION, s0);
-          nk += launch_reception_exp<R>(P, o, nullptr, nullptr, reinterpret_cast<float*>(P->phif.p), R, s0);
-          tr("reception", s0);
-          prof_mark(P, prof, 2 * NESA_STAGE_RECEPTION + 1, s0);
-        }
-      }
     }
     join_near();
-    if (rfar) {
-      scatter_kernel<T, R><<<grid_for(nloc, 256, cap), 256, 0, s0>>>(
-          phin, reinterpret_cast<const T*>(P->phif.p), P->perm.p, phi, P->pt_begin, nloc, P->ldv);
-      nk++;
-      tr("combine", s0);
-    } else {
-      finish();
-    }
+    finish();
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL + 1, s0);
   } else if (stage == 1) {
     // multi-GPU stage 1: the near field (local leaves) runs beside the
     // radiation and the upward pass, before the halo exchange; stage 2 is
     // the far field's second half and the reception
     gather();
-    CUDA_OK(cudaEventRecord(P->ev_fork, s0));
-    CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
-    if (near) {
-      launch_blockgemv<T, R, kModeStore>(P->nearset, qt, phin, nullptr, nullptr, 0, s1);
-      nk++;
-    }
+    fork_near();
     if (far) {
       nk += launch_radiation<T, R>(P, qt, s, s0);
-      up_pass();
+      up_pass(false);
     }
     join_near();
   } else {
-    near_joined = true;  // phin was completed in stage 1
-    if (far) down_pass();
+    if (far) down_pass(false);
     finish();
   }
   return nk;
 }
 
 template <typename T>
-int enqueue_dispatch(nesa_plan* P, const void* q, void* phi, int R, uint32_t flags, int stage) {
+int enqueue_dispatch(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t flags, int stage) {
   switch (R) {
     case 1:
       set_smem_attrs<T, 1>();
-      return enqueue_T<T, 1>(P, static_cast<const T*>(q), static_cast<T*>(phi), flags, stage);
+      return enqueue_T<T, 1>(P, static_cast<const T*>(q), static_cast<T*>(phi), ldv, flags, stage);
     case 2:
       set_smem_attrs<T, 2>();
-      return enqueue_T<T, 2>(P, static_cast<const T*>(q), static_cast<T*>(phi), flags, stage);
+      return enqueue_T<T, 2>(P, static_cast<const T*>(q), static_cast<T*>(phi), ldv, flags, stage);
     case 4:
       set_smem_attrs<T, 4>();
-      return enqueue_T<T, 4>(P, static_cast<const T*>(q), static_cast<T*>(phi), flags, stage);
+      return enqueue_T<T, 4>(P, static_cast<const T*>(q), static_cast<T*>(phi), ldv, flags, stage);
     default:
       throw NesaError(NESA_ERR_UNSUPPORTED, "nrhs * (1 + is_complex) must be 1, 2 or 4");
   }
@@ -2047,7 +1514,7 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
               int stage);
 
 // One product of nrhs right-hand sides: real columns are processed in blocks
-// of <= 4 (one captured graph per block; rows of q / phi keep their stride).
+// of <= 4 (one captured graph per block width; rows of q / phi keep their stride).
 int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_complex,
                uint32_t flags, void* stream, int stage) {
   require(P != nullptr, "null plan");
@@ -2071,51 +1538,38 @@ int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_
 int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t flags, void* stream,
               int stage) {
   CUDA_OK(cudaSetDevice(P->device));
+  // the workspace for the widest block so far (growing it drops every graph)
   if (P->dtype == NESA_F64)
     ensure_workspace<double>(P, R);
   else
     ensure_workspace<float>(P, R);
-  nesa_plan::GraphKey key{q, phi, R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE | NESA_PROFILE_NEAR),
-                          stage, ldv};
-  P->ldv = ldv;
+  nesa_plan::GraphKey key{R, flags & (NESA_NEAR | NESA_FAR | NESA_PROFILE | NESA_PROFILE_NEAR), stage, ldv};
   auto itg = P->graphs.find(key);
+  if (itg != P->graphs.end() && itg->second.gen != P->ws_gen) {  // (cannot happen: growth drops all)
+    if (itg->second.exec) cudaGraphExecDestroy(itg->second.exec);
+    if (itg->second.graph) cudaGraphDestroy(itg->second.graph);
+    P->graphs.erase(itg);
+    itg = P->graphs.end();
+  }
   if (itg == P->graphs.end()) {
+    nesa_plan::GraphEntry ent;
     cudaGraph_t g = nullptr;
     CUDA_OK(cudaStreamBeginCapture(P->s0, cudaStreamCaptureModeThreadLocal));
     int nk = 0;
+    P->capturing_io = &ent.io;
     try {
-      nk = P->dtype == NESA_F64 ? enqueue_dispatch<double>(P, q, phi, R, flags, stage)
-                                : enqueue_dispatch<float>(P, q, phi, R, flags, stage);
+      nk = P->dtype == NESA_F64 ? enqueue_dispatch<double>(P, q, phi, R, ldv, flags, stage)
+                                : enqueue_dispatch<float>(P, q, phi, R, ldv, flags, stage);
     } catch (...) {
+      P->capturing_io = nullptr;
       cudaStreamEndCapture(P->s0, &g);
       if (g) cudaGraphDestroy(g);
       throw;
     }
+    P->capturing_io = nullptr;
     CUDA_OK(cudaStreamEndCapture(P->s0, &g));
-    if (P->l2_persist > 0) {
-      // s / T / o stay L2-resident while the near field streams past them
-      cudaKernelNodeAttrValue av = {};
-      av.accessPolicyWindow.base_ptr = P->farws.p;
-      av.accessPolicyWindow.num_bytes = P->farws.n;
-      av.accessPolicyWindow.hitRatio =
-          float(std::min(1.0, double(P->l2_persist) / double(std::max<size_t>(P->farws.n, 1))));
-      av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      size_t nn = 0;
-      CUDA_OK(cudaGraphGetNodes(g, nullptr, &nn));
-      std::vector<cudaGraphNode_t> nodes(nn);
-      CUDA_OK(cudaGraphGetNodes(g, nodes.data(), &nn));
-      for (auto nd : nodes) {
-        cudaGraphNodeType ty;
-        CUDA_OK(cudaGraphNodeGetType(nd, &ty));
-        if (ty == cudaGraphNodeTypeKernel)
-          CUDA_OK(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &av));
-      }
-    }
-    nesa_plan::GraphEntry ent;
-    // node priorities: the captured kernels keep their streams' priorities
-    // (far chain above the near field) only with this flag
-    CUDA_OK(cudaGraphInstantiate(&ent.exec, g, P->node_prio ? cudaGraphInstantiateFlagUseNodePriority : 0));
+    ent.graph = g;
+    CUDA_OK(cudaGraphInstantiate(&ent.exec, g, 0));
     if (flags & NESA_PROFILE) {
       size_t n = 0;
       CUDA_OK(cudaGraphGetNodes(g, nullptr, &n));
@@ -2131,9 +1585,19 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
           if (P->cap_events[slot] == ev) ent.ev_nodes.emplace_back(nd, slot);
       }
     }
-    ent.graph = g;
+    ent.q = q;
+    ent.phi = phi;
+    ent.gen = P->ws_gen;
+    P->graph_captures++;
     if (stage == 0 && (flags & NESA_NEAR) && (flags & NESA_FAR)) P->kernels_per_matvec = nk;  // full product
-    itg = P->graphs.emplace(key, ent).first;
+    itg = P->graphs.emplace(key, std::move(ent)).first;
+  }
+  nesa_plan::GraphEntry& ge = itg->second;
+  if (ge.q != q || ge.phi != phi) {
+    // same schedule, other caller buffers: re-point the io nodes
+    for (auto& io : ge.io) CUDA_OK(io.apply(ge.exec, io.node, q, phi));
+    ge.q = q;
+    ge.phi = phi;
   }
   if (flags & NESA_PROFILE) {
     if (P->prof_used == P->prof_events.size()) {
@@ -2142,10 +1606,9 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
       P->prof_events.push_back(evs);
     }
     auto& evs = P->prof_events[P->prof_used++];
-    for (auto& pr : itg->second.ev_nodes)
-      CUDA_OK(cudaGraphExecEventRecordNodeSetEvent(itg->second.exec, pr.first, evs[pr.second]));
+    for (auto& pr : ge.ev_nodes) CUDA_OK(cudaGraphExecEventRecordNodeSetEvent(ge.exec, pr.first, evs[pr.second]));
   }
-  CUDA_OK(cudaGraphLaunch(itg->second.exec, static_cast<cudaStream_t>(stream)));
+  CUDA_OK(cudaGraphLaunch(ge.exec, static_cast<cudaStream_t>(stream)));
   return NESA_OK;
 }
 
@@ -2193,65 +1656,12 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     P->NL = d->n_leaves;
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
-    if (const char* nc = std::getenv("NESA_NEAR_CTAS")) P->near_ctas = std::atoi(nc) == 1 ? 1 : 2;
-    if (const char* e = std::getenv("NESA_NEAR_UNITS")) P->near_units = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("NESA_NEAR_SKIP")) P->near_sm_skip = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("NESA_NEAR_SMEM")) P->near_smem = size_t(std::max(0, std::atoi(e)));
-    if (const char* e = std::getenv("NESA_NEAR_VARIANT")) {  // "warps,stage_bytes,stages"
-      int w = kNCW;
-      int b = kABytes;
-      int n = kStages;
-      if (std::sscanf(e, "%d,%d,%d", &w, &b, &n) == 3 && bg_variant_known(w, b, n)) {
-        P->near_ncw = w;
-        P->near_ab = b;
-        P->near_nst = n;
-      }
-    }
-    if (P->near_ctas == 1 && !std::getenv("NESA_NEAR_VARIANT")) {
-      // one CTA per SM: the generic geometry with a 6-stage ring
-      P->near_ncw = kNCW;
-      P->near_ab = kABytes;
-      P->near_nst = kStages;
-    }
-    if (const char* lp = std::getenv("NESA_L2_PERSIST")) {
-      int maxp = 0;
-      CUDA_OK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device));
-      P->l2_persist = std::min<size_t>(size_t(std::max(0, std::atoi(lp))) << 20, size_t(maxp));
-      if (P->l2_persist > 0) CUDA_OK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, P->l2_persist));
-    }
-    if (const char* mb = std::getenv("NESA_MOM_BUF")) P->mom_buf = std::max(0, std::atoi(mb));
-    if (const char* mv = std::getenv("NESA_MOM_VARIANT")) P->mom_variant = std::atoi(mv);
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
-    if (const char* tc2 = std::getenv("NESA_TC2")) P->tc2 = std::atoi(tc2) != 0;
-    if (const char* t3 = std::getenv("NESA_TC3_CTAS")) P->tc3_ctas = std::max(0, std::atoi(t3));
-    if (const char* fu = std::getenv("NESA_FUSED")) P->fused = std::atoi(fu) != 0;
-    if (const char* ns = std::getenv("NESA_NEAR_SPLIT")) P->near_split = std::atoi(ns);
-    if (const char* nf = std::getenv("NESA_NEAR_FRAC")) P->near_frac = std::atof(nf);
-    if (const char* nw = std::getenv("NESA_NEAR_WAVES")) P->near_waves = std::max(1, std::atoi(nw));
-    if (const char* pr = std::getenv("NESA_PRIORITY")) P->priority = std::atoi(pr) != 0;
-    if (const char* sp = std::getenv("NESA_SPLIT")) P->split = std::atoi(sp) != 0;
-    if (const char* sl = std::getenv("NESA_SPLIT_LEVELS")) P->split_levels = std::atoi(sl) != 0;
-    if (const char* fa = std::getenv("NESA_FINE_AFTER_UP")) P->fine_after_up = std::atoi(fa);
-    if (const char* ct = std::getenv("NESA_COARSE_TC")) P->coarse_tc = std::atoi(ct);
-    if (const char* tm = std::getenv("NESA_TC3_MINB")) P->tc3_minb = std::atoi(tm);
-    if (const char* rm = std::getenv("NESA_RECV_MINB")) P->recv_minb = std::atoi(rm);
-    if (const char* np = std::getenv("NESA_NODE_PRIO")) P->node_prio = std::atoi(np) != 0;
-    if (const char* dy = std::getenv("NESA_DOWN_YSUM")) P->down_ysum = std::atoi(dy) != 0;
-    if (const char* pt = std::getenv("NESA_PAT")) P->pat = std::atoi(pt) != 0;
-    if (const char* gi = std::getenv("NESA_GATHER_INV")) P->gather_inv = std::atoi(gi) != 0;
-    if (const char* rd = std::getenv("NESA_RAD_DIRECT")) P->rad_direct = std::atoi(rd) != 0;
-    if (const char* fs = std::getenv("NESA_FUSED_SPEC")) P->fused_spec = std::atoi(fs) != 0;
-    if (const char* cm = std::getenv("NESA_COARSE_MEGA")) P->coarse_mega = std::atoi(cm) != 0;
-    if (const char* mc = std::getenv("NESA_MEGA_CTAS")) P->mega_ctas = std::max(1, std::atoi(mc));
-    if (const char* pc = std::getenv("NESA_PAT_CTAS")) P->pat_ctas = std::max(1, std::atoi(pc));
-    if (const char* na = std::getenv("NESA_NEAR_AFTER")) P->near_after = std::atoi(na);
-    if (const char* pd = std::getenv("NESA_PDL")) P->pdl = std::atoi(pd) != 0;
     P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
     if (const char* us = std::getenv("NESA_U_STORED")) P->u_mf = P->u_mf && std::atoi(us) == 0;
     P->v_mom = d->op_dtype == NESA_F32 && !d->V_blob;
     if (const char* vs = std::getenv("NESA_V_STORED")) P->v_mom = P->v_mom && std::atoi(vs) == 0;
     if (const char* tr = std::getenv("NESA_TRACE")) P->trace = std::atoi(tr) != 0;
-    if (const char* rf = std::getenv("NESA_RECV_FAR")) P->recv_far = std::atoi(rf) != 0;
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     if (P->leaf_end <= P->leaf_begin) {
@@ -2270,33 +1680,12 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
       build_plan_T<double>(P.get(), d);
     else
       build_plan_T<float>(P.get(), d);
-    {
-      int lo = 0;  // numerically lower = higher priority
-      int hi = 0;
-      CUDA_OK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      // NESA_NEAR_PRIO=1: the near-field stream above the far chain
-      const bool nprio = std::getenv("NESA_NEAR_PRIO") && std::atoi(std::getenv("NESA_NEAR_PRIO")) != 0;
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s0, cudaStreamNonBlocking, P->priority && !nprio ? hi : lo));
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s1, cudaStreamNonBlocking, nprio ? hi : lo));
-      // s2 (side-stream translation) one step below the far chain so the
-      // latency-bound level kernels are scheduled first (NESA_S2_PRIO:
-      // 0 = same as the chain, 1 = middle, 2 = lowest)
-      int s2p = P->priority ? hi : lo;
-      if (const char* e = std::getenv("NESA_S2_PRIO")) {
-        const int v = std::atoi(e);
-        if (v == 1) s2p = (hi + lo) / 2 == hi ? std::min(lo, hi + 1) : (hi + lo) / 2;
-        if (v >= 2) s2p = lo;
-      }
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s2, cudaStreamNonBlocking, s2p));
-      CUDA_OK(cudaStreamCreateWithPriority(&P->s3, cudaStreamNonBlocking, lo));
-    }
-    CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork2, cudaEventDisableTiming));
-    CUDA_OK(cudaEventCreateWithFlags(&P->ev_gfork, cudaEventDisableTiming));
-    P->ev_lv.assign(size_t(P->L - P->l0 + 1), nullptr);
-    for (auto& e : P->ev_lv) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CUDA_OK(cudaEventCreateWithFlags(&P->ev_join2, cudaEventDisableTiming));
+    // graph replays do not apply stream priorities (equal-priority streams
+    // measured fastest for this schedule)
+    CUDA_OK(cudaStreamCreateWithFlags(&P->s0, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&P->s1, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_sfine, cudaEventDisableTiming));
-    CUDA_OK(cudaEventCreateWithFlags(&P->ev_mark, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_tfine, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
@@ -2563,6 +1952,10 @@ NESA_API int64_t nesa_plan_stat(nesa_plan* P, int32_t which) {
       return P->v_mom ? P->v_nm : 0;
     case NESA_STAT_U_TERMS:
       return P->u_mf ? P->u_nt : 0;
+    case NESA_STAT_GRAPH_CAPTURES:
+      return P->graph_captures;
+    case NESA_STAT_GRAPHS_CACHED:
+      return int64_t(P->graphs.size());
     default:
       return -1;
   }

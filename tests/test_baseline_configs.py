@@ -1,0 +1,148 @@
+"""Parity at BASELINE.json's own configurations (2D analogs).
+
+* C3 (configs[2]): N = 200,000 points on the ellipse + plates union (seed 2),
+  P = 48, Q = 48, complex q (seed 2) -- against tests/golden/
+  c3_ellipse_plates_200000.npz, produced by the reference itself
+  (oracle/gen_golden.py c3: taskfmm build_tree / build_all / mvp_serial on
+  Re q and Im q).
+* C4 (configs[3], the bench workload): N = 2,000,000 (seed 3), P = 64,
+  Q = 64 -- against the oracle port (oracle/mvp_oracle.mvp_serial, pinned
+  bit-identical to the reference on the golden cases) run on the box:
+  build_all plus two real products, about a minute and ~6 GB of host memory.
+
+Both with the default kernels (no environment knobs), for the plan that
+assembles its operators on the device (what bench.py runs) and for the
+drop-in route that uploads a host OperatorSet (build_all output).
+Tolerances (BASELINE.json north_star): complex128 <= 1e-12, complex64 <= 1e-5
+relative L2.  The reference holds its own parallel executor to <= 1e-12 at
+N = 100k (test_acceptance.py:197-208); test_acceptance_criterion_7_gpu does
+the same for the GPU product.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle.mvp_oracle import mvp_serial as oracle_mvp, rel_l2
+from paper_1801_03589_b200 import geometry as geo
+from paper_1801_03589_b200 import mvp, task_counts
+from paper_1801_03589_b200.operators import NesaParams, build_all
+from paper_1801_03589_b200.quadtree import TreeParams, build_tree
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _drop_plans(tree):
+    # plans are cached on the tree; free their device memory between routes
+    for _, plan in list(getattr(tree, "_nesa_plans", {}).values()):
+        plan.close()
+    if hasattr(tree, "_nesa_plans"):
+        tree._nesa_plans.clear()
+    torch.cuda.empty_cache()
+
+
+@pytest.fixture(scope="module")
+def c3():
+    g = load_golden("c3_ellipse_plates_200000")
+    n = 200000
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=2), n)
+    tree = build_tree(pts, TreeParams(P=int(g["P"])))
+    params = NesaParams(Q=int(g["Q"]))
+    q = geo.random_rhs(n, 2)
+    yield tree, params, q, g
+    _drop_plans(tree)
+
+
+@pytest.mark.parametrize("prec,tol", [("c128", 1e-12), ("c64", 1e-5)])
+def test_c3_device_assembled_vs_reference(c3, prec, tol):
+    tree, params, q, g = c3
+    qq = q if prec == "c128" else q.astype(np.complex64)
+    phi = mvp(tree, params, qq)
+    assert phi.dtype == qq.dtype
+    err = rel_l2(phi, g["phi"])
+    assert err <= tol, err
+
+
+def test_c3_host_operator_set_vs_reference(c3):
+    tree, params, q, g = c3
+    ops = build_all(tree, params)
+    err128 = rel_l2(mvp(tree, ops, q), g["phi"])
+    err64 = rel_l2(mvp(tree, ops, q.astype(np.complex64)), g["phi"])
+    _drop_plans(tree)
+    assert err128 <= 1e-12, err128
+    assert err64 <= 1e-5, err64
+
+
+def test_c3_task_counts_and_tree_pinned(c3):
+    tree, _, _, g = c3
+    c = task_counts(tree)
+    assert [c[k] for k in ("near", "radiation", "source-transfer", "translation",
+                           "potential-transfer", "reception")] == g["task_counts"].tolist()
+
+
+@pytest.mark.slow
+def test_c4_bench_configuration_vs_oracle():
+    n = 2_000_000
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=3), n)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    q = geo.random_rhs(n, 3)
+    ops = build_all(tree, params)
+    ref = oracle_mvp(tree, ops, q.real.copy()) + 1j * oracle_mvp(tree, ops, q.imag.copy())
+    errs = {}
+    # the bench workload: complex64, operators assembled on the device
+    errs["device c64"] = rel_l2(mvp(tree, params, q.astype(np.complex64)), ref)
+    _drop_plans(tree)
+    errs["device c128"] = rel_l2(mvp(tree, params, q), ref)
+    _drop_plans(tree)
+    # drop-in route: the host OperatorSet uploaded as is
+    errs["opset c128"] = rel_l2(mvp(tree, ops, q), ref)
+    errs["opset c64"] = rel_l2(mvp(tree, ops, q.astype(np.complex64)), ref)
+    _drop_plans(tree)
+    print("C4 rel_l2 vs oracle:", {k: f"{v:.2e}" for k, v in errs.items()})
+    assert errs["device c64"] <= 1e-5 and errs["opset c64"] <= 1e-5, errs
+    assert errs["device c128"] <= 1e-12 and errs["opset c128"] <= 1e-12, errs
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_acceptance_criterion_7_gpu(prec, tol):
+    # test_acceptance.py:197-208: the 100k-point default configuration (wave
+    # curve, P = 50, Q = 10); the reference's parallel executor must agree
+    # with mvp_serial to 1e-12 -- here the GPU product
+    n = 100000
+    pts = geo.generate_sources(geo.CurveSpec(), n)
+    charges = np.random.default_rng(7).standard_normal(n)
+    tree = build_tree(pts, TreeParams(P=50))
+    params = NesaParams(Q=10)
+    ref = oracle_mvp(tree, build_all(tree, params), charges)
+    qq = charges if prec == "f64" else charges.astype(np.float32)
+    err = rel_l2(mvp(tree, params, qq), ref)
+    _drop_plans(tree)
+    assert err <= tol, err
+
+
+def test_acceptance_criterion_1_q_sweep_gpu():
+    # test_acceptance.py:36-58 on the GPU product (float64 plans): the fast
+    # product converges to the exact sum as Q grows; the exact sum is the
+    # GPU float64 dense kernel (nesa_dense_matvec, pinned to dense.py in
+    # test_benchmark.py)
+    from paper_1801_03589_b200 import dense_matvec_gpu
+    q_values = (6, 8, 10, 12, 14, 16)
+    for n in (1000, 20000):
+        pts = geo.generate_sources(geo.CurveSpec(), n)
+        charges = np.random.default_rng(n).standard_normal(n)
+        ref = dense_matvec_gpu(pts, charges)
+        tree = build_tree(pts, TreeParams(P=50))
+        errs = [rel_l2(mvp(tree, NesaParams(Q=qa), charges), ref) for qa in q_values]
+        by_q = dict(zip(q_values, errs))
+        assert by_q[10] <= 1e-3 and by_q[14] <= 1e-4, by_q
+        assert all(b <= 2.0 * a for a, b in zip(errs, errs[1:])), by_q
+        _drop_plans(tree)

@@ -1,6 +1,6 @@
 """bench.py's output contract, checked on CPU with the reference arm (the
-oracle port of mvp_serial on a bounded sample; the only arm that runs
-without a GPU)."""
+oracle port of mvp_serial, whole products; the only arm that runs without a
+GPU)."""
 
 import json
 import os
@@ -28,6 +28,9 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert "workload" in d["config"]
+    # whole products, and the product library never loaded in this process
+    assert d["native_libs_loaded"] == []
+    assert d["step_s"]["min"] > 0 and d["task_parallel"]["value"] > 0
 
 
 import pytest  # noqa: E402

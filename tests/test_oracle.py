@@ -115,3 +115,19 @@ def test_sampled_oracle_is_prefix():
     done = tree.leaves()[(nl + 1) // 2 - 1].stop
     rows = tree.perm[:done]
     assert np.array_equal(part[rows], full[rows])
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES + ["c3_ellipse_plates_200000"])
+def test_product_task_counts_match_reference(golden, name):
+    # the product's task_counts (fastmvp.py:175-187 contract; the work one GPU
+    # product performs per stage) against the reference's own counts
+    from paper_1801_03589_b200 import task_counts as product_counts
+    g = golden(name)
+    if "points" in g:
+        pts = g["points"]
+    else:   # C3: regenerated from its seed (BASELINE configs[2] 2D analog)
+        pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=2), 200000)
+    tree = build_tree(pts, TreeParams(P=int(g["P"])))
+    c = product_counts(tree)
+    assert [c[k] for k in COUNT_KEYS] == g["task_counts"].tolist()
+    assert c == task_counts(tree)
