@@ -1525,6 +1525,318 @@ constexpr size_t tc2_smem_bytes() {
 
 
 // ----------------------------------------------------------------------------
+// Level transfers on the tensor cores (float32 plans, Q = 64): the same
+// M = 128 row tiles as the translation (row m = component m % R of group
+// m / R, A in TMEM split hi / lo, tf32x3), with the tile's quadrant matrix
+// C_{lv,q} / B_{lv,q} as the B operand.  Tiles are quadrant-pure (the host
+// cuts each level's quadrant-sorted order at quadrant changes), so a tile
+// needs one matrix and one 3 x 8 MMA group:
+//   kLvlUpLeaf    T[g] = C s[g]                       (leaf level)
+//   kLvlUpSum     s[g] = sum of its children's T; T[g] = C s[g]
+//   kLvlDown      o[c] = o[c] + B o[parent c]         (o[c] = its translation sum)
+//   kLvlDownBeta  the leaf level's o, then beta^ = E^ o (a second MMA with
+//                 the same A slots; the leaf o itself is never stored)
+// One MMA per tile instead of the warp-tiled FFMA loop: the level kernels
+// were latency-bound (0.1-0.3 issued warps per scheduler, ~2300 dependent
+// instructions per warp) and competed with the near field for FP32 issue.
+// ----------------------------------------------------------------------------
+struct LevelTcArgs {
+  const float* MTC;       // this level's canonical tf32 tables: [4 quadrants][hi | lo][4096]
+  const float* ETC;       // kLvlDownBeta: E^ hi | lo
+  const int4* tiles;      // (first index into order, groups, quadrant, -)
+  const int32_t* order;   // level ids sorted by quadrant
+  const int32_t* opar;    // down: parent of order[i]
+  const int2* ochild;     // up-sum: (first child id, count) of order[i]
+  const float* Tin;       // up-sum: finer level's transfers
+  float* s;               // up: amplitudes (leaf level: read; else written)
+  float* Tout;            // up: transfers out
+  float* o;               // down: translation sums in, o out
+  float* beta;            // kLvlDownBeta: [NL][64][R] reception coefficients
+};
+
+template <int R>
+constexpr size_t level_tc_smem_bytes(int mode) {
+  constexpr int HALF = 64 / R, OS = 64 * R + 4;
+  return size_t(mode == kLvlDownBeta ? 4 : 2) * kTcBBytes + size_t((HALF * OS + 3) & ~3) * 4 + 64 + 4 * 128 +
+         256;
+}
+
+// the 64 values of tile row (group vector src, component rr) as 16 float4,
+// in the per-R arrangement tc_put_row expects (R = 1, 2: the rr-th contiguous
+// 1/R of the vector; R = 4: component rr strided)
+template <int R>
+__device__ __forceinline__ void tc_load_row(const float* src, int rr, float4 (&c)[16]) {
+  if constexpr (R == 1 || R == 2) {
+    const float4* src4 = reinterpret_cast<const float4*>(src) + rr * 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = src4[i];
+  } else {
+    const float* p = src + rr;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      c[i] = make_float4(p[(4 * i) * R], p[(4 * i + 1) * R], p[(4 * i + 2) * R], p[(4 * i + 3) * R]);
+  }
+}
+template <int R>
+__device__ __forceinline__ void tc_store_row(float* dst, int rr, const float4 (&c)[16]) {
+  if constexpr (R == 1 || R == 2) {
+    float4* d4 = reinterpret_cast<float4*>(dst) + rr * 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d4[i] = c[i];
+  } else {
+    float* p = dst + rr;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      p[(4 * i) * R] = c[i].x;
+      p[(4 * i + 1) * R] = c[i].y;
+      p[(4 * i + 2) * R] = c[i].z;
+      p[(4 * i + 3) * R] = c[i].w;
+    }
+  }
+}
+
+// split v = hi + lo (tf32) and store columns 4kb.. of this thread's TMEM lane
+__device__ __forceinline__ void tc_put4(uint32_t t_hi, uint32_t t_lo, int kb, float4 v) {
+  float4 h, l;
+  h.x = tf32_rna(v.x);
+  h.y = tf32_rna(v.y);
+  h.z = tf32_rna(v.z);
+  h.w = tf32_rna(v.w);
+  l.x = tf32_rna(v.x - h.x);
+  l.y = tf32_rna(v.y - h.y);
+  l.z = tf32_rna(v.z - h.z);
+  l.w = tf32_rna(v.w - h.w);
+  tmem_st4(t_hi + 4 * kb, h);
+  tmem_st4(t_lo + 4 * kb, l);
+}
+
+// A row (k = 0..63 of this thread's component) from tc_load_row's arrangement
+// into TMEM (warp-collective: every lane of the warp must call it)
+template <int R>
+__device__ __forceinline__ void tc_put_row(uint32_t t_hi, uint32_t t_lo, int rr, const float4 (&c)[16]) {
+  if constexpr (R == 1 || R == 4) {
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) tc_put4(t_hi, t_lo, kb, c[kb]);
+  } else {
+    // chunk i holds (k, 0), (k, 1), (k+1, 0), (k+1, 1) for k = 2i + 32 rr:
+    // swap the partner's component with the partner lane
+    float mine[32], other[32];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      mine[2 * i] = rr ? c[i].y : c[i].x;
+      mine[2 * i + 1] = rr ? c[i].w : c[i].z;
+      other[2 * i] = rr ? c[i].x : c[i].y;
+      other[2 * i + 1] = rr ? c[i].z : c[i].w;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) other[i] = __shfl_xor_sync(0xffffffffu, other[i], 1);
+#pragma unroll
+    for (int kb = 0; kb < 8; ++kb) {
+      const float4 x = make_float4(mine[4 * kb], mine[4 * kb + 1], mine[4 * kb + 2], mine[4 * kb + 3]);
+      const float4 y = make_float4(other[4 * kb], other[4 * kb + 1], other[4 * kb + 2], other[4 * kb + 3]);
+      tc_put4(t_hi, t_lo, kb, rr ? y : x);       // k in [0, 32)
+      tc_put4(t_hi, t_lo, 8 + kb, rr ? x : y);   // k in [32, 64)
+    }
+  }
+}
+
+// D[acc] = A B^T (tf32x3) with B = the canonical hi | lo pair at bsm; one thread
+__device__ __forceinline__ void tc_mma3(uint32_t tmem, const float* bsm, uint64_t* done) {
+  const uint32_t bh = smem_u32(bsm), bl = smem_u32(bsm + 4096);
+#pragma unroll
+  for (int cc = 0; cc < 3; ++cc) {
+    const uint32_t a0 = tmem + (cc == 2 ? 128u : 64u), b0 = cc == 1 ? bl : bh;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+      umma_tf32_ts(tmem, a0 + ks * 8, umma_desc_kmajor(b0 + ks * 2 * kTcLBO), (cc | ks) != 0);
+  }
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(done))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+      "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+      "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]),
+        "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]),
+        "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]),
+        "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),
+        "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
+  KtScope kt_(80 + MODE);
+  constexpr int QR = 64 * R, EPT = 128 / R, HALF = EPT / 2, OS = QR + 4, NV = QR / 4;
+  constexpr bool kDown = MODE == kLvlDown || MODE == kLvlDownBeta;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Bm = reinterpret_cast<float*>(smem);                          // hi | lo (32 KB)
+  float* Em = Bm + 8192;                                                // kLvlDownBeta: E^ hi | lo
+  float* stage = Bm + (MODE == kLvlDownBeta ? 16384 : 8192);            // HALF x OS
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + ((HALF * OS + 3) & ~3));  // [0] B, [1] MMA, [2] E
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  int32_t* gid = reinterpret_cast<int32_t*>(tslot + 4);                 // [EPT] group of each tile entry
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int4 tl = a.tiles[blockIdx.x];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+    // constant data ahead of the dependency wait (overlaps the predecessor)
+    mbar_arrive_expect_tx(&bar[0], 2 * kTcBBytes);
+    bulk_g2s(Bm, a.MTC + size_t(tl.z) * 8192, 2 * kTcBBytes, &bar[0]);
+    if constexpr (MODE == kLvlDownBeta) {
+      mbar_arrive_expect_tx(&bar[2], 2 * kTcBBytes);
+      bulk_g2s(Em, a.ETC, 2 * kTcBBytes, &bar[2]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const uint32_t t_acc = tmem + lane_base, t_hi = tmem + lane_base + 64, t_lo = tmem + lane_base + 128;
+  pdl_trigger();
+  pdl_wait();  // amplitudes come from the previous kernel in the chain
+  const int n = tl.y;
+  const int e = tid / R, rr = tid - (tid / R) * R;
+  const bool live = e < n;
+  const int64_t g = live ? int64_t(a.order[tl.x + e]) : 0;
+  if (rr == 0 && live) gid[e] = int32_t(g);
+  float4 c[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (live) {
+    if constexpr (MODE == kLvlUpLeaf) {
+      tc_load_row<R>(a.s + g * QR, rr, c);
+    } else if constexpr (MODE == kLvlUpSum) {
+      // s[g] = ordered sum of its children's T (fastmvp.py:160-162 child order)
+      const int2 kr = a.ochild[tl.x + e];
+      for (int k = 0; k < kr.y; ++k) {
+        float4 t[16];
+        tc_load_row<R>(a.Tin + (int64_t(kr.x) + k) * QR, rr, t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          c[i].x += t[i].x;
+          c[i].y += t[i].y;
+          c[i].z += t[i].z;
+          c[i].w += t[i].w;
+        }
+      }
+      tc_store_row<R>(a.s + g * QR, rr, c);
+    } else {
+      tc_load_row<R>(a.o + int64_t(a.opar[tl.x + e]) * QR, rr, c);
+    }
+  }
+  tc_put_row<R>(t_hi, t_lo, rr, c);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    mbar_wait(&bar[0], 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tc_mma3(tmem, Bm, &bar[1]);
+  }
+  mbar_wait(&bar[1], 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint32_t r[64];
+  tmem_ld64(t_acc, r);
+  float* out = kDown ? a.o : a.Tout;
+  // rows -> smem half a tile at a time -> coalesced 16-byte rows of the
+  // groups' vectors (down: + the translation sums already in o)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e0 = h * HALF;
+    const bool mine = e >= e0 && e < e0 + HALF;
+    if (mine && live)
+#pragma unroll
+      for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
+    __syncthreads();
+    const int nh = max(0, min(HALF, n - e0));
+    for (int i = tid; i < nh * NV; i += 128) {
+      const int ee = i / NV, v = i - (i / NV) * NV;
+      float4* sp = reinterpret_cast<float4*>(stage + ee * OS + 4 * v);
+      float* dst = out + int64_t(gid[e0 + ee]) * QR + 4 * v;
+      float4 val = *sp;
+      if constexpr (kDown) {
+        const float4 t = __ldcg(reinterpret_cast<const float4*>(dst));
+        val.x += t.x;
+        val.y += t.y;
+        val.z += t.z;
+        val.w += t.w;
+      }
+      if constexpr (MODE == kLvlDownBeta) {
+        *sp = val;  // the leaf o stays on chip: it only feeds beta^
+      } else {
+        *reinterpret_cast<float4*>(dst) = val;
+      }
+    }
+    if constexpr (MODE == kLvlDownBeta) {
+      __syncthreads();
+      if (mine && live)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) r[k] = __float_as_uint(stage[(e - e0) * OS + k * R + rr]);
+    }
+    __syncthreads();
+  }
+  if constexpr (MODE == kLvlDownBeta) {
+    // beta^ = E^ o: the leaf o rows back into the A slots, second MMA
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) {
+      const float4 v = live ? make_float4(__uint_as_float(r[4 * kb]), __uint_as_float(r[4 * kb + 1]),
+                                          __uint_as_float(r[4 * kb + 2]), __uint_as_float(r[4 * kb + 3]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      tc_put4(t_hi, t_lo, kb, v);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&bar[2], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      tc_mma3(tmem, Em, &bar[1]);
+    }
+    mbar_wait(&bar[1], 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tmem_ld64(t_acc, r);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e0 = h * HALF;
+      if (e >= e0 && e < e0 + HALF && live)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
+      __syncthreads();
+      const int nh = max(0, min(HALF, n - e0));
+      for (int i = tid; i < nh * NV; i += 128) {
+        const int ee = i / NV, v = i - (i / NV) * NV;
+        *reinterpret_cast<float4*>(a.beta + int64_t(gid[e0 + ee]) * QR + 4 * v) =
+            *reinterpret_cast<const float4*>(stage + ee * OS + 4 * v);
+      }
+      __syncthreads();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// ----------------------------------------------------------------------------
 // Warp-tiled level transfer for Q in {32, 64} on the large levels (same
 // roles as level_kernel).  The tile's groups (sorted by quadrant, so one or
 // two quadrant matrices) are staged group-major by bulk copy (UpLeaf, Down)

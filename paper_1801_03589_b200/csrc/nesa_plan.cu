@@ -319,6 +319,10 @@ struct nesa_plan {
   std::vector<DevBuf<int32_t>> down_order;  // per level (index lv-l0): children by quadrant
   std::vector<DevBuf<int32_t>> down_par;    // parents of down_order
   std::vector<DevBuf<int2>> down_child;     // local child range of down_order entries
+  // tensor-core level transfers (float32, Q = 64; level_tc_kernel)
+  bool level_tc = false;
+  DevBuf<float> CTC, BTC;                   // [(L-l0) * 4][hi | lo][4096] canonical tf32 C / B
+  std::vector<DevBuf<int4>> lvl_tiles;      // [(lv - l0) * 3 + r]: quadrant-pure tiles, R = 1 << r
   // fused coarse levels l0+1 .. fused_lf (one kernel per pass; see
   // nesa_kernels.cuh "Fused coarse levels"); fused_lf == l0: off
   bool fused = true;
@@ -430,6 +434,33 @@ struct nesa_plan {
 
 namespace {
 
+// round to tf32 (nearest, ties away: cvt.rna.tf32.f32 on the device)
+float tf32_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & ~0x1FFFu;
+  float y;
+  std::memcpy(&y, &u, 4);
+  return y;
+}
+
+// n_mats row-major 64 x 64 float64 matrices (y = M x) -> the canonical no-swizzle
+// K-major tf32 layout of a tcgen05 B operand, hi then lo per matrix (see
+// tgemm_tc2_kernel), plus `extra` zero matrices
+std::vector<float> canon_tf32(const double* M, int64_t n_mats, int64_t extra = 0) {
+  std::vector<float> h(size_t(n_mats + extra) * 8192, 0.f);
+  for (int64_t t = 0; t < n_mats; ++t)
+    for (int nn = 0; nn < 64; ++nn)
+      for (int k = 0; k < 64; ++k) {
+        const float x = float(M[(t * 64 + nn) * 64 + k]);
+        const float hi = tf32_host(x), lo = tf32_host(x - hi);
+        const size_t off = size_t(nn / 8) * 512 + size_t(k / 4) * 32 + size_t(nn % 8) * 4 + (k % 4);
+        h[size_t(t) * 8192 + off] = hi;
+        h[size_t(t) * 8192 + 4096 + off] = lo;
+      }
+  return h;
+}
+
 // Q x Q float64 row-major matrices -> padded transposed device layout
 // MT[j * Qp + k] = M[k][j], matrix stride mat_bytes(Q) (see nesa_kernels.cuh).
 template <typename T>
@@ -532,27 +563,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   // tensor-core translation (float32, Q = 64): D split into tf32 hi / lo in
   // the canonical K-major core-matrix layout (see tgemm_tc_kernel)
   if (std::is_same<T, float>::value && Q == 64 && P->tc && d->n_dtab > 0) {
-    // + one zero matrix at index n_dtab (the pattern of targets without
-    // interaction entries, so their translation sum is written as 0)
-    std::vector<float> h(size_t(d->n_dtab + 1) * 8192, 0.f);
-    auto tf32 = [](float x) {
-      uint32_t u;
-      std::memcpy(&u, &x, 4);
-      u = (u + 0x1000u) & ~0x1FFFu;  // round to nearest (ties away), 10-bit mantissa
-      float y;
-      std::memcpy(&y, &u, 4);
-      return y;
-    };
-    for (int64_t t = 0; t < d->n_dtab; ++t)
-      for (int nn = 0; nn < 64; ++nn)
-        for (int k = 0; k < 64; ++k) {
-          const float x = float(d->D[(t * 64 + nn) * 64 + k]);
-          const float hi = tf32(x), lo = tf32(x - hi);
-          const size_t off = size_t(nn / 8) * 512 + size_t(k / 4) * 32 + size_t(nn % 8) * 4 + (k % 4);
-          h[size_t(t) * 8192 + off] = hi;
-          h[size_t(t) * 8192 + 4096 + off] = lo;
-        }
-    P->DTC.upload(h);
+    // + one zero matrix at index n_dtab
+    P->DTC.upload(canon_tf32(d->D, d->n_dtab, 1));
   } else {
     P->tc = false;
   }
@@ -560,6 +572,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           "Q too large for the far-field kernels");
   // per-level gather tables (see nesa_kernels.cuh "Level transfers")
   P->down_order.resize(nlev);
+  P->lvl_tiles.resize(size_t(nlev) * 3);
   P->down_par.resize(nlev);
   P->down_child.resize(nlev);
   for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
@@ -575,6 +588,19 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     std::stable_sort(ord.begin(), ord.end(),
                      [&](int32_t x, int32_t y) { return d->quad[x] < d->quad[y]; });
     for (int64_t i = 0; i < cn; ++i) par[i] = int32_t(d->parent[ord[i]]);
+    // quadrant-pure tiles of <= 128 / R groups (level_tc_kernel)
+    for (int r = 0; r < 3; ++r) {
+      const int ept = 128 >> r;
+      std::vector<int4> tl;
+      for (int64_t i = 0; i < cn;) {
+        const int qd = d->quad[ord[i]];
+        int64_t j = i;
+        while (j < cn && j - i < ept && d->quad[ord[j]] == qd) ++j;
+        tl.push_back(int4{int(i), int(j - i), qd, 0});
+        i = j;
+      }
+      P->lvl_tiles[size_t(li) * 3 + r].upload(tl);
+    }
     P->down_order[li].upload(ord);
     P->down_par[li].upload(par);
     // children of each ordered group, clipped to the local range of level lv+1
@@ -607,6 +633,11 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       if (wide || P->loc_count[lv - P->l0] == 0) break;
       P->fused_lf = lv;
     }
+  }
+  P->level_tc = std::is_same<T, float>::value && Q == 64 && P->tc && nlt > 0 && P->fused_lf < P->L;
+  if (P->level_tc) {
+    P->CTC.upload(canon_tf32(d->C, nlt * 4));
+    P->BTC.upload(canon_tf32(d->B, nlt * 4));
   }
   if (P->fused_lf > P->l0) {
     std::vector<int2> uc(static_cast<size_t>(G), int2{0, 0});
@@ -877,15 +908,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       // Q = 64 with tensor cores: beta^ = E^ o for all leaves as one GEMM;
       // E^ rows 0 -> 1 (sum of o), 2m-1 / 2m -> Re / Im of (1/m) e^{-i m theta_k}
       if (Q == 64 && P->tc && 2 * P->u_nt + 1 <= 64) {
-        auto tf32 = [](float x) {
-          uint32_t u;
-          std::memcpy(&u, &x, 4);
-          u = (u + 0x1000u) & ~0x1FFFu;
-          float y;
-          std::memcpy(&y, &u, 4);
-          return y;
-        };
-        std::vector<float> h(8192, 0.f);
+        std::vector<double> Em(64 * 64, 0.0);  // E^[row][k]
         for (int row = 0; row < 64; ++row)
           for (int k = 0; k < 64; ++k) {
             float x = 0.f;
@@ -893,12 +916,9 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
               x = 1.f;
             else if (row <= 2 * P->u_nt)
               x = (row & 1) ? E[size_t(k) * ne + (row + 1) / 2].x : E[size_t(k) * ne + row / 2].y;
-            const float hi = tf32(x), lo = tf32(x - hi);
-            const size_t off = size_t(row / 8) * 512 + size_t(k / 4) * 32 + size_t(row % 8) * 4 + (k % 4);
-            h[off] = hi;
-            h[4096 + off] = lo;
+            Em[size_t(row) * 64 + k] = x;
           }
-        P->ETC.upload(h);
+        P->ETC.upload(canon_tf32(Em.data(), 1));
         P->beta_tc = true;
       }
       // leaf level handled by the wide kernels: its downward transfer and
@@ -1056,6 +1076,10 @@ void set_smem_attrs() {
     attr(radiation_mom_kernel<R>, lim);
     attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_tc3_kernel<R>, int(tc2_smem_bytes<R>()));
+    attr(level_tc_kernel<R, kLvlUpLeaf>, int(level_tc_smem_bytes<R>(kLvlUpLeaf)));
+    attr(level_tc_kernel<R, kLvlUpSum>, int(level_tc_smem_bytes<R>(kLvlUpSum)));
+    attr(level_tc_kernel<R, kLvlDown>, int(level_tc_smem_bytes<R>(kLvlDown)));
+    attr(level_tc_kernel<R, kLvlDownBeta>, int(level_tc_smem_bytes<R>(kLvlDownBeta)));
     attr(reception_exp_kernel<R, false>, lim);
     attr(reception_exp_kernel<R, true>, lim);
   }
@@ -1206,10 +1230,54 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
   // every level is either one of the wide (warp-tiled, Q = 64) levels at the
   // fine end or inside the fused coarse range (see build_plan_T)
   auto wide = [&](int lv) { return lv > P->fused_lf; };
+  constexpr int RI = R == 1 ? 0 : (R == 2 ? 1 : 2);
+  // float32 Q = 64: the level GEMMs on the tensor cores (level_tc_kernel)
+  auto level_tc = [&](int lv, int mode) -> bool {
+    if constexpr (std::is_same<T, float>::value) {
+      if (!P->level_tc) return false;
+      const int ci = lv - P->l0;
+      const DevBuf<int4>& tiles = P->lvl_tiles[size_t(ci) * 3 + RI];
+      LevelTcArgs ta{};
+      const bool down = mode == kLvlDown || mode == kLvlDownBeta;
+      ta.MTC = (down ? P->BTC.p : P->CTC.p) + size_t(ci - 1) * 4 * 8192;
+      ta.ETC = P->ETC.p;
+      ta.tiles = tiles.p;
+      ta.order = P->down_order[ci].p;
+      ta.opar = P->down_par[ci].p;
+      ta.ochild = P->down_child[ci].p;
+      ta.Tin = Tup;
+      ta.s = s;
+      ta.Tout = Tup;
+      ta.o = o;
+      ta.beta = reinterpret_cast<float*>(P->beta.p);
+      const int grid = int(tiles.n);
+      switch (mode) {
+        case kLvlUpLeaf:
+          launch_pdl(level_tc_kernel<R, kLvlUpLeaf>, grid, 128, level_tc_smem_bytes<R>(kLvlUpLeaf), s0, ta);
+          break;
+        case kLvlUpSum:
+          launch_pdl(level_tc_kernel<R, kLvlUpSum>, grid, 128, level_tc_smem_bytes<R>(kLvlUpSum), s0, ta);
+          break;
+        case kLvlDown:
+          launch_pdl(level_tc_kernel<R, kLvlDown>, grid, 128, level_tc_smem_bytes<R>(kLvlDown), s0, ta);
+          break;
+        default:
+          launch_pdl(level_tc_kernel<R, kLvlDownBeta>, grid, 128, level_tc_smem_bytes<R>(kLvlDownBeta), s0,
+                     ta);
+      }
+      return true;
+    }
+    return false;
+  };
   auto up_level = [&](int lv) {
     // children-major: T[c] = C s[c]; s[parent] = sum of its children's T
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
+    if (level_tc(lv, lv == P->L ? kLvlUpLeaf : kLvlUpSum)) {
+      nk++;
+      tr("up_tc", s0);
+      return;
+    }
     const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
     const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
     if (lv == P->L)
@@ -1268,6 +1336,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
   auto down_level = [&](int lv) {
     const int ci = lv - P->l0;
     if (P->loc_count[ci] == 0) return;
+    if (level_tc(lv, lv == P->L && P->beta_fused && far_recv ? kLvlDownBeta : kLvlDown)) {
+      nk++;
+      tr("down_tc", s0);
+      return;
+    }
     const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
     const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
     if (lv == P->L && P->beta_fused && far_recv) {
