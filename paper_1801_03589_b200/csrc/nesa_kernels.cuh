@@ -43,15 +43,19 @@ __device__ __forceinline__ float2 cmulf(float2 a, float2 b) {
 
 struct KtScope {
   unsigned long long t0;
+  unsigned long long* buf;  // the log, read once per CTA (thread 0)
   int tag;
-  __device__ __forceinline__ explicit KtScope(int t) : t0(0), tag(t) {
-    if (threadIdx.x == 0 && g_kt_buf) t0 = kt_now();
+  __device__ __forceinline__ explicit KtScope(int t) : t0(0), buf(nullptr), tag(t) {
+    if (threadIdx.x == 0) {  // the load is consumed only at the end: no stall here
+      buf = g_kt_buf;
+      t0 = kt_now();
+    }
   }
   __device__ __forceinline__ ~KtScope() {
-    if (threadIdx.x == 0 && g_kt_buf) {
+    if (threadIdx.x == 0 && buf) {
       const unsigned int i = atomicAdd(g_kt_cnt, 1u);
       if (i < g_kt_cap) {
-        unsigned long long* r = g_kt_buf + 4ull * i;
+        unsigned long long* r = buf + 4ull * i;
         r[0] = (unsigned long long)tag;
         r[1] = gridDim.x;
         r[2] = t0;
@@ -394,16 +398,48 @@ template <typename T, int R>
 __global__ void gather_inv_kernel(const T* __restrict__ q, const int32_t* __restrict__ iperm,
                                   T* __restrict__ qt, int64_t n, int ldq) {
   KtScope kt_(3);
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n;
-       j += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = iperm[j];
-    if constexpr (R == 2 && sizeof(T) == 4) {
-      const float2 v = ldq == 2 ? *reinterpret_cast<const float2*>(q + j * 2)
-                                : make_float2(q[j * ldq], q[j * ldq + 1]);
-      *reinterpret_cast<float2*>(qt + i * 2) = v;
+  // four consecutive points per thread, every load of the group issued before
+  // the first store (one memory round trip per group instead of per point)
+  constexpr int U = 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x * U;
+  for (int64_t j0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) * U; j0 < n; j0 += stride) {
+    int32_t ii[U];
+    T v[U][R];
+    if (j0 + U <= n && (j0 & 3) == 0) {
+      const int4 t = *reinterpret_cast<const int4*>(iperm + j0);
+      ii[0] = t.x;
+      ii[1] = t.y;
+      ii[2] = t.z;
+      ii[3] = t.w;
     } else {
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) qt[i * R + rr] = q[j * ldq + rr];
+      for (int u = 0; u < U; ++u) ii[u] = j0 + u < n ? iperm[j0 + u] : -1;
+    }
+    if constexpr (R == 2 && sizeof(T) == 4) {
+      if (ldq == 2 && j0 + U <= n && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+        const float4 a = *reinterpret_cast<const float4*>(q + j0 * 2);
+        const float4 b = *reinterpret_cast<const float4*>(q + j0 * 2 + 4);
+        v[0][0] = a.x; v[0][1] = a.y; v[1][0] = a.z; v[1][1] = a.w;
+        v[2][0] = b.x; v[2][1] = b.y; v[3][0] = b.z; v[3][1] = b.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) v[u][rr] = j0 + u < n ? q[(j0 + u) * ldq + rr] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j0 + u < n) *reinterpret_cast<float2*>(qt + int64_t(ii[u]) * 2) = make_float2(v[u][0], v[u][1]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) v[u][rr] = j0 + u < n ? q[(j0 + u) * ldq + rr] : T(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j0 + u < n)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) qt[int64_t(ii[u]) * R + rr] = v[u][rr];
     }
   }
 }
@@ -1680,6 +1716,7 @@ __global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
   KtScope kt_(80 + MODE);
   constexpr int QR = 64 * R, EPT = 128 / R, HALF = EPT / 2, OS = QR + 4, NV = QR / 4;
   constexpr bool kDown = MODE == kLvlDown || MODE == kLvlDownBeta;
+  static_assert(HALF * NV == 1024, "epilogue: 8 float4 per thread and half");
   extern __shared__ __align__(128) unsigned char smem[];
   float* Bm = reinterpret_cast<float*>(smem);                          // hi | lo (32 KB)
   float* Em = Bm + 8192;                                                // kLvlDownBeta: E^ hi | lo
@@ -1712,13 +1749,21 @@ __global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
   const uint32_t tmem = *tslot;
   const uint32_t lane_base = uint32_t(warp * 32) << 16;
   const uint32_t t_acc = tmem + lane_base, t_hi = tmem + lane_base + 64, t_lo = tmem + lane_base + 128;
-  pdl_trigger();
-  pdl_wait();  // amplitudes come from the previous kernel in the chain
+  // plan constants (tile rows, children, parents) before the dependency
+  // wait: they overlap the predecessor instead of adding a round trip
   const int n = tl.y;
   const int e = tid / R, rr = tid - (tid / R) * R;
   const bool live = e < n;
   const int64_t g = live ? int64_t(a.order[tl.x + e]) : 0;
+  int2 kr = make_int2(0, 0);
+  int64_t par = 0;
+  if (live) {
+    if constexpr (MODE == kLvlUpSum) kr = a.ochild[tl.x + e];
+    if constexpr (kDown) par = a.opar[tl.x + e];
+  }
   if (rr == 0 && live) gid[e] = int32_t(g);
+  pdl_trigger();
+  pdl_wait();  // amplitudes come from the previous kernel in the chain
   float4 c[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) c[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1726,22 +1771,30 @@ __global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
     if constexpr (MODE == kLvlUpLeaf) {
       tc_load_row<R>(a.s + g * QR, rr, c);
     } else if constexpr (MODE == kLvlUpSum) {
-      // s[g] = ordered sum of its children's T (fastmvp.py:160-162 child order)
-      const int2 kr = a.ochild[tl.x + e];
-      for (int k = 0; k < kr.y; ++k) {
-        float4 t[16];
-        tc_load_row<R>(a.Tin + (int64_t(kr.x) + k) * QR, rr, t);
+      // s[g] = ordered sum of its children's T (fastmvp.py:160-162 child
+      // order), two children's loads in flight at a time
+      for (int k = 0; k < kr.y; k += 2) {
+        float4 t0[16], t1[16];
+        tc_load_row<R>(a.Tin + (int64_t(kr.x) + k) * QR, rr, t0);
+        const bool two = k + 1 < kr.y;
+        if (two) tc_load_row<R>(a.Tin + (int64_t(kr.x) + k + 1) * QR, rr, t1);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          c[i].x += t[i].x;
-          c[i].y += t[i].y;
-          c[i].z += t[i].z;
-          c[i].w += t[i].w;
+          c[i].x += t0[i].x;
+          c[i].y += t0[i].y;
+          c[i].z += t0[i].z;
+          c[i].w += t0[i].w;
+          if (two) {
+            c[i].x += t1[i].x;
+            c[i].y += t1[i].y;
+            c[i].z += t1[i].z;
+            c[i].w += t1[i].w;
+          }
         }
       }
       tc_store_row<R>(a.s + g * QR, rr, c);
     } else {
-      tc_load_row<R>(a.o + int64_t(a.opar[tl.x + e]) * QR, rr, c);
+      tc_load_row<R>(a.o + par * QR, rr, c);
     }
   }
   tc_put_row<R>(t_hi, t_lo, rr, c);
@@ -1752,6 +1805,21 @@ __global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
     mbar_wait(&bar[0], 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     tc_mma3(tmem, Bm, &bar[1]);
+  }
+  // down: this thread's share of the translation sums (o[c] before the
+  // transfer), loaded while the tensor core runs: <= 8 float4 per half
+  float4 oc[2][8];
+  if constexpr (kDown) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int nh = max(0, min(HALF, n - h * HALF));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = tid + 128 * j, ee = i / NV, v = i - (i / NV) * NV;
+        oc[h][j] = ee < nh ? __ldcg(reinterpret_cast<const float4*>(a.o + int64_t(gid[h * HALF + ee]) * QR) + v)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
   }
   mbar_wait(&bar[1], 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1769,13 +1837,16 @@ __global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
       for (int k = 0; k < 64; ++k) stage[(e - e0) * OS + k * R + rr] = __uint_as_float(r[k]);
     __syncthreads();
     const int nh = max(0, min(HALF, n - e0));
-    for (int i = tid; i < nh * NV; i += 128) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = tid + 128 * j;
+      if (i >= nh * NV) break;
       const int ee = i / NV, v = i - (i / NV) * NV;
       float4* sp = reinterpret_cast<float4*>(stage + ee * OS + 4 * v);
       float* dst = out + int64_t(gid[e0 + ee]) * QR + 4 * v;
       float4 val = *sp;
       if constexpr (kDown) {
-        const float4 t = __ldcg(reinterpret_cast<const float4*>(dst));
+        const float4 t = oc[h][j];
         val.x += t.x;
         val.y += t.y;
         val.z += t.z;
@@ -2374,6 +2445,284 @@ __global__ void __launch_bounds__(32 * kExpWarps, 4) radiation_mom_kernel(
   cp_async_wait_all();
 }
 
+// ----------------------------------------------------------------------------
+// Radiation on FP32 pipes + tensor cores (float32 plans from geometry, Q = 64,
+// R <= 2, nm <= 38).  The moments mu_m = sum_j w_j^m q_j (m < nm) of a leaf
+// come from 8 lanes: lanes 0-3 take the even moments, lanes 4-7 the odd ones
+// (chains start at 1 / w and step by w^2, two interleaved chains stepping by
+// w^4 for ILP), each lane every 4th point of the leaf, then a fixed
+// transpose reduction over the 4 lanes of a half (deterministic).  The moment map s = A^ mu^ (operators.py:107-112
+// through the circle expansion, see the section comment above) runs on the
+// tensor cores: rows = (leaf, column) of a 32-leaf tile, K = 80 real moment
+// rows (row 0 = -log(r) mu_0, rows 2m-1 / 2m = Re / Im mu_m), N = 64 outputs,
+// tf32x3 with A^ pre-split on the host.  Persistent CTAs of 8 warps (4 leaves
+// per warp); warps 0-3 own the 128 TMEM lanes and do the tensor-core part
+// while warps 4-7 already form the next tile's moments.
+// ----------------------------------------------------------------------------
+constexpr int kRadTcWarps = 8;
+constexpr int kRadTcLeaves = kRadTcWarps * 4;  // leaves per tile
+constexpr int kRadTcK = 80;                    // moment rows (K) of the map
+constexpr int kRadTcMH = 19;                   // moments per lane half (nm <= 38: C4 uses 38)
+constexpr uint32_t kRadTcSBO = kRadTcK * 8 * 4;  // bytes between 8-row groups of A^
+constexpr int kRadTcKP = kRadTcK + 4;          // mu^ row stride in smem (conflict-free 16-byte reads)
+
+__device__ __forceinline__ uint64_t umma_desc_kmajor_sbo(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((kTcLBO >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  return d;
+}
+
+template <int R>
+constexpr size_t radiation_tc_smem_bytes() {
+  // A^ hi | lo, mu^ tile, output stage, barriers / TMEM slot
+  return size_t(2) * 64 * kRadTcK * 4 + size_t(kRadTcLeaves) * kRadTcKP * R * 4 +
+         size_t(kRadTcLeaves) * (64 * R + 4) * 4 + 128 + 8 * kRadTcLeaves;
+}
+
+template <int R>
+__global__ void __launch_bounds__(32 * kRadTcWarps, 2) radiation_tc_kernel(
+    const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
+    const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
+    const float* __restrict__ ATC, const float* __restrict__ qt, float* __restrict__ s,
+    const int32_t* __restrict__ leaf_order, int64_t nleaf, int nm) {
+  static_assert(R == 1 || R == 2, "radiation_tc_kernel: R <= 2");
+  KtScope kt_(62);
+  constexpr int QR = 64 * R, OS = QR + 4;
+  constexpr int NV = 2 * R * kRadTcMH;  // accumulators per lane
+  constexpr int NV2 = NV / 2, NV4 = NV / 4;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* Ah = reinterpret_cast<float*>(smem);                 // A^ hi (canonical, 64 x 80)
+  float* smu = Ah + 2 * 64 * kRadTcK;                         // [leaf][R][KP] (mu^ rows)
+  float* stage = smu + kRadTcLeaves * kRadTcKP * R;           // [leaf][OS]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage + kRadTcLeaves * OS);  // [0] A^, [1] MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  int32_t* tleaf2 = reinterpret_cast<int32_t*>(tslot + 2);   // [2][kRadTcLeaves] leaf of each tile row
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&bar[0], 2 * 64 * kRadTcK * 4);
+    bulk_g2s(Ah, ATC, 2 * 64 * kRadTcK * 4, &bar[0]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const int g8 = lane & 7, half = g8 >> 2, g = g8 & 3;
+  const int cnt = half ? nm >> 1 : (nm + 1) >> 1;  // odd / even moments below nm
+  const int64_t ntiles = (nleaf + kRadTcLeaves - 1) / kRadTcLeaves;
+  uint32_t mma_phase = 0;
+  bool first = true;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    // double-buffered: warps 4-7 fill the next tile's entries while warps
+    // 0-3 still store this one's rows
+    int32_t* tleaf = tleaf2 + (it & 1) * kRadTcLeaves;
+    // tiles hold leaves of similar size (leaf_order: descending point
+    // count), so a tile is not held up by one large leaf
+    const int le = warp * 4 + (lane >> 3);  // leaf of the tile
+    const int64_t li = tile * kRadTcLeaves + le;
+    const bool live = li < nleaf;
+    const int64_t leaf = live ? int64_t(leaf_order[li]) : int64_t(leaf_order[0]);
+    if ((lane & 7) == 0) tleaf[le] = int32_t(leaf);
+    const int64_t b = leaf_start[leaf];
+    const int n = live ? int(leaf_stop[leaf] - b) : 0;
+    const float rc = leaf_r[leaf];
+    const float inv = 1.f / rc;
+    // ---- moments of this lane's half over every 4th point (each point's
+    // data loaded two steps ahead)
+    float v[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) v[t] = 0.f;
+    float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+    float q0[R], q1[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) q0[rr] = q1[rr] = 0.f;
+    auto fetch = [&](int j, float2& pp, float (&qq)[R]) {
+      if (j < n) {
+        pp = prel[b + j];
+        if constexpr (R == 2) {
+          const float2 t = *reinterpret_cast<const float2*>(qt + (b + j) * 2);
+          qq[0] = t.x;
+          qq[1] = t.y;
+        } else {
+          qq[0] = qt[b + j];
+        }
+      }
+    };
+    auto point = [&](const float2 p, const float (&qv)[R]) {
+        const float2 w = make_float2(p.x * inv, p.y * inv);
+        const float2 w2 = cmulf(w, w);
+        const float2 w4 = cmulf(w2, w2);
+        const float2 W1 = w4, W2 = make_float2(-w4.y, w4.x);
+        float2 zc[2];
+        zc[0] = half ? w : make_float2(1.f, 0.f);   // moment 2 mm + half
+        zc[1] = cmulf(zc[0], w2);
+#pragma unroll
+        for (int mm = 0; mm < kRadTcMH; ++mm) {
+          const float2 z = zc[mm & 1];
+          // v layout [moment][re, im][rhs column] (column pairs share an FFMA2)
+          if constexpr (R == 2) {
+            ffma2(v[(mm * 2) * R], v[(mm * 2) * R + 1], z.x, qv[0], qv[1]);
+            ffma2(v[(mm * 2 + 1) * R], v[(mm * 2 + 1) * R + 1], z.y, qv[0], qv[1]);
+          } else {
+            v[mm * 2] = fmaf(z.x, qv[0], v[mm * 2]);
+            v[mm * 2 + 1] = fmaf(z.y, qv[0], v[mm * 2 + 1]);
+          }
+          zc[mm & 1] = cmul_pk(z, W1, W2);
+        }
+    };
+    fetch(g, p0, q0);
+    fetch(g + 4, p1, q1);
+    for (int j = g; j < n; j += 8) {
+      {
+        const float2 p = p0;
+        float qv[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) qv[rr] = q0[rr];
+        fetch(j + 8, p0, q0);
+        point(p, qv);
+      }
+      if (j + 4 < n) {
+        const float2 p = p1;
+        float qv[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) qv[rr] = q1[rr];
+        fetch(j + 12, p1, q1);
+        point(p, qv);
+      }
+    }
+    // ---- transpose reduction over the 4 lanes of the half: lane g keeps
+    // values [vb, vb + NV4)
+    {
+      const bool up = g & 2;
+#pragma unroll
+      for (int t = 0; t < NV2; ++t) {
+        const float send = up ? v[t] : v[t + NV2];
+        const float keep = up ? v[t + NV2] : v[t];
+        v[t] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+    }
+    {
+      const bool up = g & 1;
+#pragma unroll
+      for (int t = 0; t < NV4; ++t) {
+        const float send = up ? v[t] : v[t + NV4];
+        const float keep = up ? v[t + NV4] : v[t];
+        v[t] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      }
+    }
+    __syncthreads();  // the previous tile's mu^ has been moved into TMEM
+    {
+      // value index x = (mm * 2 + c) * R + rr -> mu^ row of moment m = 2 mm + half
+      const int vb = ((g & 2) ? NV2 : 0) + ((g & 1) ? NV4 : 0);
+      float* mrow = smu + le * R * kRadTcKP;  // column rr's rows at rr * KP
+      const float nl = -logf(rc);
+#pragma unroll
+      for (int t = 0; t < NV4; ++t) {
+        const int x = vb + t;
+        const int mm = x / (2 * R), c = (x / R) & 1, rr = x % R;
+        const int m = 2 * mm + half;
+        if (mm >= cnt) continue;
+        if (m == 0) {
+          if (c == 0) mrow[rr * kRadTcKP] = nl * v[t];  // row 0: -log(r) mu_0 (mu_0 is real)
+        } else {
+          mrow[rr * kRadTcKP + 2 * m - 1 + c] = v[t];
+        }
+      }
+      // zero rows past 2 nm - 1 (written once per tile by the second half's lane 0)
+      if (half && g == 0)
+        for (int row = 2 * nm - 1; row < kRadTcK; ++row)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr) mrow[rr * kRadTcKP + row] = 0.f;
+    }
+    __syncthreads();  // mu^ tile complete
+    {
+      // ---- rows -> TMEM: thread row m = tid % 128 (leaf m / R, column m % R;
+      // warp w reaches TMEM lanes 32 (w % 4) ..): warps 0-3 store the tf32 hi
+      // part, warps 4-7 the lo part; rows past the 32 leaves are zero
+      const int m = tid & 127;
+      const int e = m / R, rr = m - (m / R) * R;
+      const bool row_live = e < kRadTcLeaves && tile * kRadTcLeaves + e < nleaf;
+      const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+      const uint32_t t_dst = tmem + lane_base + 64 + (warp >= 4 ? kRadTcK : 0);
+      const float* mr = smu + ((e < kRadTcLeaves ? e : 0) * R + rr) * kRadTcKP;
+#pragma unroll 4
+      for (int kb = 0; kb < kRadTcK / 4; ++kb) {
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row_live) x = *reinterpret_cast<const float4*>(mr + 4 * kb);
+        float4 h;
+        h.x = tf32_rna(x.x);
+        h.y = tf32_rna(x.y);
+        h.z = tf32_rna(x.z);
+        h.w = tf32_rna(x.w);
+        if (warp >= 4) {
+          h.x = tf32_rna(x.x - h.x);
+          h.y = tf32_rna(x.y - h.y);
+          h.z = tf32_rna(x.z - h.z);
+          h.w = tf32_rna(x.w - h.w);
+        }
+        tmem_st4(t_dst + 4 * kb, h);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
+    __syncthreads();  // TMEM rows written; smu free for the next tile
+    if (warp < 4) {
+      if (tid == 0) {
+        if (first) mbar_wait(&bar[0], 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bh = smem_u32(Ah), bl = smem_u32(Ah + 64 * kRadTcK);
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const uint32_t a0 = tmem + (cc == 2 ? 64u + kRadTcK : 64u), b0 = cc == 1 ? bl : bh;
+#pragma unroll
+          for (int ks = 0; ks < kRadTcK / 8; ++ks)
+            umma_tf32_ts(tmem, a0 + ks * 8, umma_desc_kmajor_sbo(b0 + ks * 2 * kTcLBO, kRadTcSBO),
+                         (cc | ks) != 0);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar[1]))
+                     : "memory");
+      }
+      first = false;
+      mbar_wait(&bar[1], mma_phase);
+      mma_phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t r[64];
+      tmem_ld64(tmem + (uint32_t(warp * 32) << 16), r);
+      const int e = tid / R, rr = tid - (tid / R) * R;
+      if (e < kRadTcLeaves)
+#pragma unroll
+        for (int k = 0; k < 64; ++k) stage[e * OS + k * R + rr] = __uint_as_float(r[k]);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      named_bar_sync(2, 128);
+      const int64_t l0t = tile * kRadTcLeaves;
+      const int nt = int(nleaf - l0t < kRadTcLeaves ? nleaf - l0t : int64_t(kRadTcLeaves));
+      constexpr int NVQ = QR / 4;
+      for (int i = tid; i < nt * NVQ; i += 128) {
+        const int ee = i / NVQ, vq = i - (i / NVQ) * NVQ;
+        *reinterpret_cast<float4*>(s + int64_t(tleaf[ee]) * QR + 4 * vq) =
+            *reinterpret_cast<const float4*>(stage + ee * OS + 4 * vq);
+      }
+      named_bar_sync(2, 128);  // stage reusable
+    } else {
+      first = false;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
 // Reception through the incoming expansion.  One warp per leaf, one lane per
 // point; the point data and the leaf's amplitudes are loaded before the
 // coefficient phase so their latency overlaps it.  E [Q][nt + 1] float2
@@ -2399,18 +2748,38 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
   float* os = reinterpret_cast<float*>(beta + nb);
   const int ne = nt + 1;
   constexpr int kSlots = 4;
-  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf;
-       li += int64_t(gridDim.x) * kExpWarps) {
+  const int nq = BETA_IN ? 64 * R : Q * R;
+  constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
+  const int64_t stride = int64_t(gridDim.x) * kExpWarps;
+  // the next leaf's extent, radius and amplitudes (or coefficients) are
+  // loaded one leaf ahead, so a leaf starts with one memory round trip (its
+  // points) instead of a chain of dependent loads
+  int64_t nx_b = 0;
+  int nx_n = 0;
+  float nx_r = 1.f;
+  float nx_ov[NOV];
+  auto meta = [&](int64_t l) {
+    if (l < nleaf) {
+      const int64_t lf = leaf0 + l;
+      const int64_t b0 = leaf_start[lf], b1 = leaf_stop[lf];
+      nx_r = leaf_r[lf];
+#pragma unroll
+      for (int t = 0; t < NOV; ++t) nx_ov[t] = lane + 32 * t < nq ? o[lf * nq + lane + 32 * t] : 0.f;
+      nx_b = b0;
+      nx_n = int(b1 - b0);
+    }
+  };
+  meta(int64_t(blockIdx.x) * kExpWarps + warp);
+  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf; li += stride) {
     const int64_t leaf = leaf0 + li;
-    const int64_t b = leaf_start[leaf];
-    const int n = int(leaf_stop[leaf] - b);
-    const float r = leaf_r[leaf];
-    // prefetch: amplitudes (or coefficients) and the first kSlots * 32 points
-    const int nq = BETA_IN ? 64 * R : Q * R;
-    constexpr int NOV = BETA_IN ? 2 * R : 4;  // prefetched words per lane
+    const int64_t b = nx_b;
+    const int n = nx_n;
+    const float r = nx_r;
     float ov[NOV];
 #pragma unroll
-    for (int t = 0; t < NOV; ++t) ov[t] = lane + 32 * t < nq ? o[leaf * nq + lane + 32 * t] : 0.f;
+    for (int t = 0; t < NOV; ++t) ov[t] = nx_ov[t];
+    meta(li + stride);
+    // the first kSlots * 32 points
     float2 pp[kSlots];
     int64_t dd[kSlots];
     float bb[kSlots][R];
@@ -2474,51 +2843,67 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
       __syncwarp();
     }
     const float inv = 1.f / r;
-    auto eval = [&](float2 p, int64_t dst, const float* base) {
-      const float2 w = make_float2(p.x * inv, p.y * inv);
-      const float2 W1 = w, W2 = make_float2(-w.y, w.x);
-      float2 z = w;
-      const float* bf = reinterpret_cast<const float*>(beta);
-      float acc[R];
+    const float* bf = reinterpret_cast<const float*>(beta);
+    auto coef = [&](int m, float (&br)[R], float (&nbi)[R]) {  // re and -im of beta_m per column
+      if constexpr (R == 2) {
+        const float4 t = *reinterpret_cast<const float4*>(bf + m * 4);
+        br[0] = t.x; br[1] = t.y; nbi[0] = t.z; nbi[1] = t.w;
+      } else {
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] = bf[rr];
-#pragma unroll 4
+        for (int rr = 0; rr < R; ++rr) {
+          br[rr] = bf[m * 2 * R + rr];
+          nbi[rr] = bf[m * 2 * R + R + rr];
+        }
+      }
+    };
+    // acc += Re(beta_m z) = re z.x - im z.y (the -im term first)
+    auto term = [&](float (&acc)[R], float2 z, const float (&br)[R], const float (&nbi)[R]) {
+      if constexpr (R % 2 == 0) {
+#pragma unroll
+        for (int rr = 0; rr < R; rr += 2) {
+          ffma2(acc[rr], acc[rr + 1], z.y, nbi[rr], nbi[rr + 1]);
+          ffma2(acc[rr], acc[rr + 1], z.x, br[rr], br[rr + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(br[rr], z.x, fmaf(nbi[rr], z.y, acc[rr]));
+      }
+    };
+    // two points per pass: their power and sum chains interleave (the series
+    // is a dependent chain per point); per-point arithmetic as one point alone
+    auto eval2 = [&](float2 pa, int64_t da, const float* ba, float2 pb, int64_t db, const float* bb2,
+                     bool two) {
+      const float2 wa = make_float2(pa.x * inv, pa.y * inv), wb = make_float2(pb.x * inv, pb.y * inv);
+      const float2 Wa2 = make_float2(-wa.y, wa.x), Wb2 = make_float2(-wb.y, wb.x);
+      float2 za = wa, zb = wb;
+      float acca[R], accb[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acca[rr] = accb[rr] = bf[rr];
+#pragma unroll 2
       for (int m = 1; m <= nt; ++m) {
-        float br[R], nbi[R];  // re and -im of beta_m per column
-        if constexpr (R == 2) {
-          const float4 t = *reinterpret_cast<const float4*>(bf + m * 4);
-          br[0] = t.x; br[1] = t.y; nbi[0] = t.z; nbi[1] = t.w;
-        } else {
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) {
-            br[rr] = bf[m * 2 * R + rr];
-            nbi[rr] = bf[m * 2 * R + R + rr];
-          }
-        }
-        // acc += Re(beta_m z) = re z.x - im z.y (the -im term first, as before)
-        if constexpr (R % 2 == 0) {
-#pragma unroll
-          for (int rr = 0; rr < R; rr += 2) {
-            ffma2(acc[rr], acc[rr + 1], z.y, nbi[rr], nbi[rr + 1]);
-            ffma2(acc[rr], acc[rr + 1], z.x, br[rr], br[rr + 1]);
-          }
-        } else {
-#pragma unroll
-          for (int rr = 0; rr < R; ++rr) acc[rr] = fmaf(br[rr], z.x, fmaf(nbi[rr], z.y, acc[rr]));
-        }
-        z = cmul_pk(z, W1, W2);
+        float br[R], nbi[R];
+        coef(m, br, nbi);
+        term(acca, za, br, nbi);
+        term(accb, zb, br, nbi);
+        za = cmul_pk(za, wa, Wa2);
+        zb = cmul_pk(zb, wb, Wb2);
       }
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) phi[dst * ldp + rr] = base[rr] + acc[rr];
+      for (int rr = 0; rr < R; ++rr) phi[da * ldp + rr] = ba[rr] + acca[rr];
+      if (two)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) phi[db * ldp + rr] = bb2[rr] + accb[rr];
     };
 #pragma unroll
-    for (int i = 0; i < kSlots; ++i)
-      if (lane + 32 * i < n) eval(pp[i], dd[i], bb[i]);
+    for (int i = 0; i < kSlots; i += 2)
+      if (lane + 32 * i < n)
+        eval2(pp[i], dd[i], bb[i], pp[i + 1], dd[i + 1], bb[i + 1], lane + 32 * (i + 1) < n);
     for (int j = lane + 32 * kSlots; j < n; j += 32) {
       float base[R];
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) base[rr] = phin ? phin[(b + j) * R + rr] : 0.f;
-      eval(prel[b + j], perm ? perm[b + j] : b + j, base);
+      const float2 p = prel[b + j];
+      eval2(p, perm ? perm[b + j] : b + j, base, p, 0, base, false);
     }
     __syncwarp();
   }

@@ -341,6 +341,9 @@ struct nesa_plan {
   int v_nm = 0;                             // moments m = 0 .. v_nm - 1
   int u_nt = 0;                             // reception terms m = 1 .. u_nt
   DevBuf<float2> mom_A;                     // [v_nm][Q]: row 0 = (F_k, 0), row m = A_km
+  bool rad_tc = false;                      // moment map on the tensor cores (radiation_tc_kernel)
+  DevBuf<float> ATC;                        // [hi | lo][64 x 80] canonical tf32 A^ (K = 80)
+  DevBuf<int32_t> rad_order;                // local leaves by descending point count
   DevBuf<float2> exp_E;                     // [Q][u_nt + 1]: 1, (1/m) e^{-i m theta_k}
   DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64;
@@ -894,6 +897,32 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
       }
       P->mom_A.upload(A);
+      // Q = 64: s = A^ mu^ on the tensor cores (K = 2 nm - 1 <= 80 real rows:
+      // 0 -> F_k, 2m-1 -> Re A_km, 2m -> -Im A_km)
+      if (Q == 64 && P->tc && P->v_nm <= 2 * kRadTcMH) {
+        std::vector<float> h(size_t(2) * 64 * kRadTcK, 0.f);
+        for (int k = 0; k < 64; ++k)
+          for (int j = 0; j < kRadTcK; ++j) {
+            float x = 0.f;
+            const int m = (j + 1) / 2;
+            if (j == 0)
+              x = A[k].x;
+            else if (m < P->v_nm)
+              x = (j & 1) ? A[size_t(m) * Q + k].x : -A[size_t(m) * Q + k].y;
+            const float hi = tf32_host(x), lo = tf32_host(x - hi);
+            const size_t off = size_t(k / 8) * (kRadTcK * 8) + size_t(j / 4) * 32 + size_t(k % 8) * 4 + (j % 4);
+            h[off] = hi;
+            h[size_t(64) * kRadTcK + off] = lo;
+          }
+        P->ATC.upload(h);
+        std::vector<int32_t> ord;
+        for (int64_t a = lb; a < le; ++a) ord.push_back(int32_t(a));
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+          return d->group_stop[x] - d->group_start[x] > d->group_stop[y] - d->group_start[y];
+        });
+        P->rad_order.upload(ord);
+        P->rad_tc = true;
+      }
     }
     if (P->u_mf) {
       const int ne = P->u_nt + 1;
@@ -1074,6 +1103,7 @@ void set_smem_attrs() {
   attr(fused_down_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
     attr(radiation_mom_kernel<R>, lim);
+    if constexpr (R <= 2) attr(radiation_tc_kernel<R>, int(radiation_tc_smem_bytes<R>()));
     attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_tc3_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(level_tc_kernel<R, kLvlUpLeaf>, int(level_tc_smem_bytes<R>(kLvlUpLeaf)));
@@ -1152,7 +1182,7 @@ void io_launch(nesa_plan* P, void (*kern)(KArgs...), int grid, int block, size_t
   P->capturing_io->push_back(std::move(io));
 }
 
-constexpr int kExpCtasPerSM = 12;  // reception: leaves are latency-bound, keep many warps
+constexpr int kExpCtasPerSM = 6;   // reception: one wave of resident CTAs (register budget: 6 per SM)
 constexpr int kMomCtasPerSM = 4;
 constexpr int kMomBufPoints = 800;  // points staged per warp by the moment kernel
 
@@ -1160,6 +1190,17 @@ constexpr int kMomBufPoints = 800;  // points staged per warp by the moment kern
 template <typename T, int R>
 int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value) {
+    if (P->v_mom && P->rad_tc && R <= 2) {
+      if constexpr (R <= 2) {
+        const int64_t nleaf = P->leaf_end - P->leaf_begin;
+        const int64_t ntiles = (nleaf + kRadTcLeaves - 1) / kRadTcLeaves;
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * P->n_sm)));
+        radiation_tc_kernel<R><<<grid, 32 * kRadTcWarps, radiation_tc_smem_bytes<R>(), st>>>(
+            P->mf_prel.p, P->gstart.p, P->gstop.p, P->mf_leaf_rc.p, P->ATC.p, qt, s, P->rad_order.p, nleaf,
+            P->v_nm);
+        return 1;
+      }
+    }
     if (P->v_mom) {
       const int64_t nleaf = P->leaf_end - P->leaf_begin;
       const int64_t per_cta = int64_t(kExpWarps) * kMomLeavesPerWarp;
@@ -1439,7 +1480,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     const int32_t* ip = P->iperm.p;
     const int64_t n = P->N;
     io_launch(
-        P, gather_inv_kernel<T, R>, grid_for(n, 256, cap), 256, 0, s0,
+        P, gather_inv_kernel<T, R>, grid_for((n + 3) / 4, 256, cap), 256, 0, s0,
         [=](const void* qq, void*) { return std::make_tuple(static_cast<const T*>(qq), ip, qt, n, ldv); },
         q, phi);
     nk++;

@@ -15,12 +15,12 @@ import sys
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, HERE)
 
-TAGS = {1: "gather", 2: "scatter", 3: "gather (original order)", 35: "coarse far (up + translation + down)", 10: "blockgemv(store: near)", 11: "blockgemv(scatter: U)",
-        20: "level_kernel up-leaf", 21: "level_kernel up-sum", 22: "level_kernel down",
-        30: "fused_up", 31: "fused_down", 32: "sum_children", 33: "reduce", 40: "tgemm",
-        41: "tgemm_wt (FFMA)", 42: "tgemm_tc (tcgen05)", 43: "tgemm_tc2 (tcgen05, A in TMEM)", 44: "tgemm_tc3 (persistent)", 45: "tgemm_pat (target-major, tcgen05)", 50: "level_wt up-leaf",
-        51: "level_wt up-sum", 52: "level_wt down", 53: "level_wt down + reception (leaf)", 54: "level_wt down + beta (leaf)", 60: "radiation moments (in-kernel A)",
-        61: "radiation moments", 70: "reception (in-kernel beta)", 71: "reception series"}
+TAGS = {2: "scatter", 3: "gather (original order)", 10: "blockgemv(store: near)", 11: "blockgemv(scatter: U)",
+        30: "fused_up", 31: "fused_down", 33: "reduce", 40: "tgemm",
+        41: "tgemm_wt (FFMA)", 43: "tgemm_tc2 (tcgen05, A in TMEM)", 44: "tgemm_tc3 (persistent)", 50: "level_wt up-leaf",
+        51: "level_wt up-sum", 52: "level_wt down", 54: "level_wt down + beta (leaf)", 60: "radiation moments (in-kernel A)",
+        70: "reception series", 71: "reception series (beta in)", 80: "level_tc up-leaf", 81: "level_tc up-sum",
+        82: "level_tc down", 84: "level_tc down + beta (leaf)"}
 
 
 def main():
