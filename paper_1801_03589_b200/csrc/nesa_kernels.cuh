@@ -575,12 +575,16 @@ struct LevelArgs {
 //                     by one CTA, in child order -> deterministic).  At level
 //                     l0 only s is formed (the old top-level sum).  No CTA
 //                     ever waits, so residency does not matter.
-//  fused_down_kernel  one CTA per level-lf group walks its ancestor chain top
-//                     down.  Each ancestor is CLAIMED by one CTA (CAS 0 -> 1),
-//                     which computes o[a] += B_{lv, quad a} o[parent a] and
-//                     publishes it (state 2); other CTAs needing it wait.  A
-//                     claimer only ever reads finished parents, so every wait
-//                     ends (no deadlock even if CTAs are not co-resident).
+//  fused_down_kernel  one CTA per level-lf group g.  Every coarse group is
+//                     OWNED by the CTA of its first level-lf descendant (a
+//                     host table), which computes o[a] += B_{lv, quad a}
+//                     o[parent a] and publishes it (state 2).  A CTA waits
+//                     once (for the parent of its top owned group), then runs
+//                     its chain down to g.  CTAs take their group in start
+//                     order (an atomic ticket, as decoupled look-back scans
+//                     do), and an owner always precedes the groups below it,
+//                     so a waited-for CTA has started: no deadlock without
+//                     co-residency.
 //
 // The up kernel also resets the down-claim state of every group it passes
 // and the last arriver resets the parent's counter, so no memset is needed
@@ -594,8 +598,10 @@ struct FusedArgs {
   const int64_t* parent;  // [G]
   const int2* uchild;     // [G] local children (first id, count)
   const int32_t* anc;     // down: [count][D] ancestors of the level-lf groups (level lf-1 first)
+  const int32_t* own;     // down: [count] ancestors each level-lf group's CTA owns (computes)
   int* cnt;               // up: arrivals per group
-  int* state;             // down: 0 free, 1 claimed, 2 done
+  int* state;             // down: 0 pending, 2 done (reset by the up kernel)
+  int* ticket;            // down: [2] start-order counter, finished CTAs
   T* Tup;
   T* s;
   T* o;
@@ -607,6 +613,13 @@ __device__ __forceinline__ int ld_acquire_s32(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// acquire-release fence at GPU scope: publishes the CTA's prior writes
+// (ordered before by bar.sync) / makes other CTAs' published writes visible;
+// lighter than the sequentially consistent __threadfence()
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_release_s32(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 constexpr int kFusedThreads = 128;
@@ -642,7 +655,18 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
   pdl_wait();
   uint32_t phase = 0;
   while (true) {
-    if (tid == 0) a.state[g] = 0;
+    // plan constants of this step (parent, its child count and quadrant)
+    // loaded before they are needed
+    int64_t p_next = -1;
+    int p_nch = 0, p_quad = 0;
+    if (tid == 0) {
+      a.state[g] = 0;
+      if (lv > a.l0) {
+        p_next = a.parent[g];
+        p_nch = a.uchild[p_next].y;
+        p_quad = a.quad[p_next];
+      }
+    }
     const int2 uc = a.uchild[g];
     for (int w = tid; w < QR; w += kFusedThreads) {
       T v;
@@ -668,14 +692,17 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
     }
     __syncthreads();  // T[g] written, M and X consumed
     if (tid == 0) {
-      const int64_t p = a.parent[g];
-      __threadfence();
+      const int64_t p = p_next;
+      fence_acq_rel_gpu();  // release T[g] (and s[g]) to the parent's CTA
       const int old = atomicAdd(a.cnt + p, 1);
-      const bool last = old == a.uchild[p].y - 1;
+      const bool last = old == p_nch - 1;
       if (last) {
-        a.cnt[p] = 0;
-        __threadfence();
-        if (lv - 1 > a.l0) load_mat(lv - 1, p);
+        fence_acq_rel_gpu();  // acquire the siblings' T
+        a.cnt[p] = 0;         // (visible to the next launch at the kernel boundary)
+        if (lv - 1 > a.l0) {
+          mbar_arrive_expect_tx(bar, uint32_t(mb));
+          bulk_g2s(M, a.MT + (size_t(lv - 1 - a.l0 - 1) * 4 + p_quad) * a.mstride, uint32_t(mb), bar);
+        }
       }
       *nxt = last ? p : -1;
     }
@@ -696,38 +723,45 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   T* M = reinterpret_cast<T*>(smem);
   T* X = reinterpret_cast<T*>(smem + mb);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + ((size_t(QR) * sizeof(T) + 15) & ~size_t(15)));
-  int* flag = reinterpret_cast<int*>(bar + 1);
-  const int64_t g = a.first + blockIdx.x;
+  int* ticket = reinterpret_cast<int*>(bar + 1);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
+    *ticket = atomicAdd(a.ticket, 1);  // start-order index
   }
   __syncthreads();
+  const int vid = *ticket;
+  const int64_t g = a.first + vid;
   pdl_trigger();
   pdl_wait();  // o holds the translation sums
   uint32_t phase = 0;
-  for (int i = a.D - 1; i >= -1; --i) {
-    const int64_t x = i >= 0 ? int64_t(a.anc[blockIdx.x * int64_t(a.D) + i]) : g;
+  // This CTA owns the ancestors whose first level-lf descendant is g (its
+  // chain up to own[cta] levels; every coarse group has exactly one owner).
+  // It waits once -- for the parent of its top owned group, published by
+  // that group's owner -- then computes its chain top down without further
+  // waits, publishing each owned group for the CTAs below.
+  const int own = a.own[vid];
+  const int32_t* anc = a.anc + vid * int64_t(a.D);
+  for (int i = own - 1; i >= -1; --i) {
+    const int64_t x = i >= 0 ? int64_t(anc[i]) : g;
     const int lvx = a.lf - 1 - i;
-    if (i >= 0) {
-      __syncthreads();  // everyone has read the previous flag
-      if (tid == 0) {
-        int st = atomicCAS(a.state + x, 0, 1);
-        if (st == 1) {
-          while (ld_acquire_s32(a.state + x) != 2) __nanosleep(128);
-          st = 2;
-        }
-        *flag = st;
-      }
-      __syncthreads();
-      if (*flag != 0) continue;  // finished by another CTA
-    }
-    // o[x] += B_{lvx, quad x} o[parent x]
+    const int64_t px = a.parent[x];
     if (tid == 0) {
       mbar_arrive_expect_tx(bar, uint32_t(mb));
       bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * 4 + a.quad[x]) * a.mstride, uint32_t(mb), bar);
     }
-    const int64_t px = a.parent[x];
+    if (i == own - 1 && lvx - 1 > a.l0) {
+      // the parent of the top owned group belongs to another CTA
+      if (tid == 0) {
+        unsigned ns = 64;
+        while (ld_acquire_s32(a.state + px) != 2) {
+          __nanosleep(ns);
+          if (ns < 512) ns *= 2;
+        }
+      }
+      __syncthreads();
+    }
+    // o[x] += B_{lvx, quad x} o[parent x]
     for (int w = tid; w < QR; w += kFusedThreads) X[w] = __ldcg(a.o + px * QR + w);
     __syncthreads();
     mbar_wait(bar, phase);
@@ -741,9 +775,14 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
     }
     __syncthreads();  // o[x] written, M and X consumed
     if (i >= 0 && tid == 0) {
-      __threadfence();
-      atomicExch(a.state + x, 2);
+      fence_acq_rel_gpu();
+      st_release_s32(a.state + x, 2);
     }
+  }
+  // the last CTA to finish resets the ticket counter for the next launch
+  if (tid == 0 && atomicAdd(a.ticket + 1, 1) == int(gridDim.x) - 1) {
+    a.ticket[0] = 0;
+    a.ticket[1] = 0;
   }
 }
 

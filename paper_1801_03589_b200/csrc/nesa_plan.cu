@@ -329,7 +329,9 @@ struct nesa_plan {
   int fused_lf = 0;
   DevBuf<int2> uchild;                      // [G] local children (first, count)
   DevBuf<int32_t> fused_anc;                // [count(lf)][lf - l0 - 1] ancestors
-  DevBuf<int> fused_cnt, fused_state;       // [G] arrival counters / claim states
+  DevBuf<int> fused_cnt, fused_state;       // [G] arrival counters / done flags
+  DevBuf<int32_t> fused_own;                // [count(lf)] ancestors owned by each level-lf group's CTA
+  DevBuf<int> fused_ticket;                 // [2] fused_down start-order counter
   int64_t wide_level = 2048;                // warp-tiled level kernels from this size
                                             // (NESA_WIDE_LEVEL: tests force them on small trees)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
@@ -666,6 +668,20 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       }
     }
     P->fused_anc.upload(anc);
+    // ownership: a coarse group is computed by its first level-lf
+    // descendant's CTA, i.e. g owns its ancestors while it is a first child
+    std::vector<int32_t> own(static_cast<size_t>(std::max<int64_t>(1, P->loc_count[li])), 0);
+    for (int64_t i = 0; i < P->loc_count[li]; ++i) {
+      int64_t x = P->loc_first[li] + i;
+      int k = 0;
+      while (k < D && uc[size_t(d->parent[x])].x == x) {
+        x = d->parent[x];
+        ++k;
+      }
+      own[size_t(i)] = k;
+    }
+    P->fused_own.upload(own);
+    P->fused_ticket.alloc(2);
     P->fused_cnt.alloc(size_t(G));    // zero-filled
     P->fused_state.alloc(size_t(G));
   }
@@ -1410,6 +1426,8 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     fa.anc = P->fused_anc.p;
     fa.cnt = P->fused_cnt.p;
     fa.state = P->fused_state.p;
+    fa.own = P->fused_own.p;
+    fa.ticket = P->fused_ticket.p;
     fa.Tup = Tup;
     fa.s = s;
     fa.o = o;
