@@ -363,12 +363,14 @@ def run_ours(args):
 
     def step(profile=False):
         if engine is not None:
-            engine.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream)
+            # one graph per rank: the halo exchange (NCCL all_gather) is inside
+            engine.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream,
+                              profile="near" if profile else False)
         else:
             plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, stream=stream.cuda_stream,
                             profile="near" if profile else False)
 
-    prof = engine is None
+    prof = True
     for _ in range(max(args.warmup, 3)):
         step(prof)
     # grow the profiling event pool to K before timing, soak clocks ~1 s
@@ -429,21 +431,30 @@ def run_ours(args):
                     "alg_bytes_per_launch": near_bytes, "avg_launch_ms": near_ms,
                     "peak_source": peak_src,
                     "note": "near kernel inside the full product, concurrent with the radiation "
-                            "and far-field chain (they share HBM and SMs)"}
+                            "and far-field chain (they share HBM and SMs)"
+                            + (f"; rank {rank} of {world}, its own leaves" if world > 1 else "")}
+        if world > 1:
+            # per-rank figures (each rank streams its own leaves' operator)
+            t = torch.tensor([ach, near_ms], device=dev, dtype=torch.float64)
+            allr = [torch.zeros_like(t) for _ in range(world)]
+            torch.distributed.all_gather(allr, t)
+            roofline["per_rank"] = [{"rank": i, "achieved": float(x[0]), "frac": float(x[0]) / peak,
+                                     "avg_launch_ms": float(x[1])} for i, x in enumerate(allr)]
         # the same kernel with nothing concurrent (near-only product), for context
-        for _ in range(5):
+        for _ in range(5 if world == 1 else 0):
             plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, far=False,
                             stream=stream.cuda_stream, profile="near")
-        plan.profile_reset()
-        for _ in range(50):
-            plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, far=False,
-                            stream=stream.cuda_stream, profile="near")
-        torch.cuda.synchronize()
-        iso = float(np.mean(plan.profile_read("near")))
-        roofline["isolated"] = {"achieved": near_bytes / (iso * 1e-3) / 1e9,
-                                "frac": near_bytes / (iso * 1e-3) / 1e9 / peak,
-                                "avg_launch_ms": iso,
-                                "note": "near-only product, nothing concurrent"}
+        if world == 1:
+            plan.profile_reset()
+            for _ in range(50):
+                plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 1, True, far=False,
+                                stream=stream.cuda_stream, profile="near")
+            torch.cuda.synchronize()
+            iso = float(np.mean(plan.profile_read("near")))
+            roofline["isolated"] = {"achieved": near_bytes / (iso * 1e-3) / 1e9,
+                                    "frac": near_bytes / (iso * 1e-3) / 1e9 / peak,
+                                    "avg_launch_ms": iso,
+                                    "note": "near-only product, nothing concurrent"}
     matvec_bw = alg["total"] / (ms_step * 1e-3) / 1e9
 
     # the reference's own precision: a complex128 product (float64 plan,
@@ -529,8 +540,9 @@ def run_ours(args):
         e2e = {"value": 1e3 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(qh.numel() * 8) * world,
                "d2h_bytes_per_step": int(ph.numel() * 8) * world, "ms_per_step": e_ms,
                "api": "paper_1801_03589_b200.dist.DistNesa.matvec_ptr per rank: H2D of q from pinned "
-                      "memory, product (stage 1, NCCL all_gather of partial source amplitudes, "
-                      "stage 2), D2H of the rank's phi; max over ranks"}
+                      "memory, product (one graph: near field || radiation + upward pass, NCCL "
+                      "all_gather of partial source amplitudes, translation + downward pass, "
+                      "reception), D2H of the rank's phi; max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

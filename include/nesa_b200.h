@@ -153,6 +153,38 @@ int nesa_matvec_stage(nesa_plan* plan, int32_t stage, const void* q_dev,
                       uint32_t flags, void* stream);
 void* nesa_plan_s_dev(nesa_plan* plan, int32_t nrhs_real);
 
+/*
+ * Multi-GPU plan (the reference has no distributed layer,
+ * SPEC.md:9): `desc` describes this rank's sub-plan (leaf_begin / leaf_end
+ * set), `nccl_comm` is the caller's ncclComm_t (not owned) and `xd` the halo
+ * exchange tables (paper_1801_03589_b200.dist.build_exchange).  nesa_matvec
+ * on such a plan is the whole distributed product as ONE graph launch:
+ * gather, near field (local leaves, concurrent), radiation and upward pass,
+ * pack -> ncclAllGather -> combine of the partial source amplitudes,
+ * translation and downward pass, reception of the rank's points (its rows of
+ * phi; the other rows are left untouched).  NCCL is loaded at run time
+ * (libnccl.so.2).
+ */
+typedef struct nesa_exchange_desc {
+  int64_t n_export;             /* groups whose partial s this rank sends       */
+  const int64_t* export_ids;    /* [n_export]                                   */
+  int64_t max_export;           /* send rows per rank (>= every rank's n_export) */
+  int64_t n_import;             /* groups whose s this rank completes           */
+  const int64_t* import_ids;    /* [n_import]                                   */
+  int32_t max_contrib;          /* contributors per imported group             */
+  const int64_t* contrib;       /* [n_import][max_contrib]: row < nranks*max_export
+                                   = gathered row, else own s row (row - that); -1 none */
+} nesa_exchange_desc;
+
+int nesa_plan_create_dist(const nesa_plan_desc* desc, int device, void* nccl_comm, int32_t rank,
+                          int32_t nranks, const nesa_exchange_desc* xd, nesa_plan** out);
+/* NCCL bootstrap helpers: a 128-byte ncclUniqueId (rank 0; share it with the
+ * other ranks out of band) and a communicator per rank (ncclCommInitRank). */
+int nesa_nccl_unique_id(void* out, int32_t bytes);
+int nesa_nccl_comm_init(const void* unique_id, int32_t nranks, int32_t rank, int32_t device,
+                        void** comm_out);
+int nesa_nccl_comm_destroy(void* comm);
+
 /* Columns [col0, col0 + ncols_real) of an (N, ld_real) row-major real block
  * (a complex right-hand side is 2 adjacent real columns) -- the same product
  * as nesa_matvec on that column range, in blocks of <= 4 columns.  Lets a

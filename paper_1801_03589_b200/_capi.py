@@ -36,7 +36,8 @@ EXPORTED_SYMBOLS = (
     "nesa_profile_reset", "nesa_profile_read", "nesa_trace_read", "nesa_trace_name",
     "nesa_ktrace_enable", "nesa_ktrace_read", "nesa_dense_matvec", "nesa_matvec_cols",
     "nesa_tree_build", "nesa_tree_error", "nesa_tree_size", "nesa_tree_copy", "nesa_tree_free",
-    "nesa_exchange_pack", "nesa_exchange_combine",
+    "nesa_exchange_pack", "nesa_exchange_combine", "nesa_plan_create_dist", "nesa_nccl_unique_id",
+    "nesa_nccl_comm_init", "nesa_nccl_comm_destroy",
 )
 
 _p = ctypes.c_void_p
@@ -64,6 +65,16 @@ class NesaPlanDesc(ctypes.Structure):
         ("leaf_r_inaux", _f64p), ("out_fit_leaf", _f64p),
         ("check_cos", _f64p), ("check_sin", _f64p), ("aux_cos", _f64p), ("aux_sin", _f64p),
         ("leaf_begin", ctypes.c_int64), ("leaf_end", ctypes.c_int64),
+    ]
+
+
+class NesaExchangeDesc(ctypes.Structure):
+    """Mirror of ``struct nesa_exchange_desc``."""
+
+    _fields_ = [
+        ("n_export", ctypes.c_int64), ("export_ids", _i64p), ("max_export", ctypes.c_int64),
+        ("n_import", ctypes.c_int64), ("import_ids", _i64p), ("max_contrib", ctypes.c_int32),
+        ("contrib", _i64p),
     ]
 
 
@@ -133,6 +144,17 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_exchange_combine.argtypes = [_p, _p, _p, _p, ctypes.c_int64, ctypes.c_int32,
                                           ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _p]
     lib.nesa_exchange_combine.restype = ctypes.c_int
+    lib.nesa_plan_create_dist.argtypes = [ctypes.POINTER(NesaPlanDesc), ctypes.c_int, _p, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.POINTER(NesaExchangeDesc),
+                                          ctypes.POINTER(_p)]
+    lib.nesa_plan_create_dist.restype = ctypes.c_int
+    lib.nesa_nccl_unique_id.argtypes = [_p, ctypes.c_int32]
+    lib.nesa_nccl_unique_id.restype = ctypes.c_int
+    lib.nesa_nccl_comm_init.argtypes = [_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.POINTER(_p)]
+    lib.nesa_nccl_comm_init.restype = ctypes.c_int
+    lib.nesa_nccl_comm_destroy.argtypes = [_p]
+    lib.nesa_nccl_comm_destroy.restype = ctypes.c_int
     if lib.nesa_abi_version() != NESA_ABI_VERSION:
         raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
     _lib = lib

@@ -2948,4 +2948,39 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
   }
 }
 
+// ----------------------------------------------------------------------------
+// Multi-GPU halo exchange (paper_1801_03589_b200/dist.py):
+// pack this rank's partial source amplitudes that other ranks need into the
+// all_gather send buffer, and complete the needed groups' amplitudes as the
+// rank-ordered sum of their contributors' partials (contrib rows < n_recv
+// index the gathered buffer, rows >= n_recv this rank's own s[row - n_recv]).
+// ----------------------------------------------------------------------------
+template <typename T>
+__global__ void xpack_kernel(const T* __restrict__ s, const int64_t* __restrict__ ids, int64_t n_ids,
+                             int64_t rows, int qr, T* __restrict__ send) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < rows * qr;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = t / qr, w = t - r * qr;
+    send[t] = r < n_ids ? s[ids[r] * qr + w] : T(0);
+  }
+}
+
+template <typename T>
+__global__ void xcombine_kernel(T* s, const T* __restrict__ recv, const int64_t* __restrict__ imp,
+                                const int64_t* __restrict__ contrib, int64_t n_imp, int max_c,
+                                int64_t n_recv, int qr) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_imp * qr;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / qr, w = t - i * qr;
+    T acc = T(0);
+    for (int k = 0; k < max_c; ++k) {  // fixed rank order: deterministic
+      const int64_t c = contrib[i * max_c + k];
+      if (c < 0) continue;
+      acc += c < n_recv ? recv[c * qr + w] : s[(c - n_recv) * qr + w];
+    }
+    s[imp[i] * qr + w] = acc;  // the only local row read is imp[i]'s own
+  }
+}
+
+
 }  // namespace nesa

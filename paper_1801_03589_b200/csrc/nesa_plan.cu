@@ -9,6 +9,8 @@
 // levels} -> reception), and the near-field branch runs concurrently with the
 // far-field chain (the paper's near/far task mixing).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -51,6 +53,45 @@ struct NesaError : std::runtime_error {
 void require(bool ok, const std::string& msg) {
   if (!ok) throw NesaError(NESA_ERR_INVALID, msg);
 }
+
+// NCCL, resolved at run time (dlopen "libnccl.so.2": the copy the process
+// already has -- e.g. torch's -- or the system one), so the library has no
+// link-time dependency and single-GPU use never touches it.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.h) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw NesaError(NESA_ERR_UNSUPPORTED, std::string("libnccl.so.2 not found: ") + dlerror());
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) throw NesaError(NESA_ERR_UNSUPPORTED, std::string("NCCL symbol missing: ") + name);
+      return f;
+    };
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(sym("ncclAllGather"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(sym("ncclGetErrorString"));
+    api.h = h;
+  }
+  return api;
+}
+
+#define NCCL_OK(expr)                                                                           \
+  do {                                                                                          \
+    ncclResult_t _r = (expr);                                                                   \
+    if (_r != ncclSuccess)                                                                      \
+      throw NesaError(NESA_ERR_CUDA, std::string(#expr) + ": " + nccl().errorString(_r));       \
+  } while (0)
 
 template <typename T>
 struct DevBuf {
@@ -359,6 +400,16 @@ struct nesa_plan {
   DevBuf<float> ET;                         // [64][64] E^ transposed for the warp-tiled GEMM
   DevBuf<float> ETC;                        // [hi | lo][64 x 64] canonical tf32 E^
   DevBuf<unsigned char> beta;               // [NL][64][R] reception coefficients
+
+  // multi-GPU plan (nesa_plan_create_dist): the halo exchange of partial
+  // source amplitudes inside the product graph (pack -> ncclAllGather ->
+  // combine), so a distributed product is one graph launch per rank
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t x_n_export = 0, x_max_export = 1, x_n_import = 0;
+  int x_max_contrib = 1;
+  DevBuf<int64_t> x_export, x_import, x_contrib;
+  DevBuf<unsigned char> x_send, x_recv;      // [max_export][Q R] / [nranks * max_export][Q R]
 
   // workspace for R real columns
   int ws_R = 0;
@@ -1072,6 +1123,11 @@ void ensure_workspace(nesa_plan* P, int R) {
     P->o.view(P->farws.p + 2 * fb, fb);
   }
   P->Y.alloc(size_t(std::max<int64_t>(P->nnz, 1)) * P->Q * R * es);
+  if (P->comm) {
+    const size_t row = size_t(P->Q) * R * es;
+    P->x_send.alloc(size_t(P->x_max_export) * row);
+    P->x_recv.alloc(size_t(P->nranks) * P->x_max_export * row);
+  }
   P->ws_R = R;
   P->ws_gen++;
 }
@@ -1588,7 +1644,42 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     CUDA_OK(cudaStreamWaitEvent(s0, P->ev_join, 0));
   };
 
-  if (stage == 0) {
+  // halo exchange of a distributed plan (nesa_plan_create_dist): pack the
+  // partials other ranks need, all_gather them over NCCL (captured into
+  // this graph), complete the needed groups' s in rank order
+  auto exchange = [&]() {
+    const int qr = Q * R;
+    T* send = reinterpret_cast<T*>(P->x_send.p);
+    T* recv = reinterpret_cast<T*>(P->x_recv.p);
+    const int64_t rows = P->x_max_export;
+    xpack_kernel<T><<<grid_for(rows * qr, 256, 4096), 256, 0, s0>>>(s, P->x_export.p, P->x_n_export, rows, qr,
+                                                                      send);
+    NCCL_OK(nccl().allGather(send, recv, size_t(rows) * qr, sizeof(T) == 8 ? ncclFloat64 : ncclFloat32,
+                             P->comm, s0));
+    if (P->x_n_import > 0)
+      xcombine_kernel<T><<<grid_for(P->x_n_import * qr, 256, 4096), 256, 0, s0>>>(
+          s, recv, P->x_import.p, P->x_contrib.p, P->x_n_import, P->x_max_contrib, P->nranks * rows, qr);
+    nk += 2;
+    tr("exchange", s0);
+  };
+
+  if (stage == 0 && P->comm) {
+    // distributed product, one graph per rank: gather -> fork {near (local
+    // leaves) | radiation, upward pass -> halo exchange -> translation,
+    // downward pass} -> join -> reception of the local points
+    prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
+    gather();
+    fork_near();
+    if (far) {
+      nk += launch_radiation<T, R>(P, qt, s, s0);
+      up_pass(false);
+      exchange();
+      down_pass(false);
+    }
+    join_near();
+    finish();
+    prof_mark(P, prof, 2 * NESA_STAGE_TOTAL + 1, s0);
+  } else if (stage == 0) {
     // gather -> radiation (the far chain is the critical path: it gets the
     // GPU first) -> fork {near | up, translate, down} -> join -> reception
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
@@ -1759,10 +1850,65 @@ int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t f
     return NESA_ERR_INVALID;                          \
   }
 
+nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int rank, int nranks,
+                            const nesa_exchange_desc* xd);
+
 NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** out) {
   NESA_GUARD({
-    require(d != nullptr && out != nullptr, "null argument");
+    require(out != nullptr, "null argument");
     *out = nullptr;
+    *out = plan_create_impl(d, device, nullptr, 0, 1, nullptr);
+    return NESA_OK;
+  })
+}
+
+NESA_API int nesa_plan_create_dist(const nesa_plan_desc* d, int device, void* nccl_comm, int32_t rank,
+                                   int32_t nranks, const nesa_exchange_desc* xd, nesa_plan** out) {
+  NESA_GUARD({
+    require(out != nullptr && nccl_comm != nullptr && xd != nullptr, "null argument");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    *out = nullptr;
+    *out = plan_create_impl(d, device, nccl_comm, rank, nranks, xd);
+    return NESA_OK;
+  })
+}
+
+NESA_API int nesa_nccl_unique_id(void* out, int32_t bytes) {
+  NESA_GUARD({
+    require(out != nullptr && bytes >= int32_t(sizeof(ncclUniqueId)), "need a 128-byte buffer");
+    ncclUniqueId id;
+    NCCL_OK(nccl().getUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+    return NESA_OK;
+  })
+}
+
+NESA_API int nesa_nccl_comm_init(const void* unique_id, int32_t nranks, int32_t rank, int32_t device,
+                                 void** comm_out) {
+  NESA_GUARD({
+    require(unique_id != nullptr && comm_out != nullptr, "null argument");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / nranks");
+    CUDA_OK(cudaSetDevice(device));
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t c = nullptr;
+    NCCL_OK(nccl().commInitRank(&c, nranks, id, rank));
+    *comm_out = c;
+    return NESA_OK;
+  })
+}
+
+NESA_API int nesa_nccl_comm_destroy(void* comm) {
+  NESA_GUARD({
+    if (comm) NCCL_OK(nccl().commDestroy(static_cast<ncclComm_t>(comm)));
+    return NESA_OK;
+  })
+}
+
+nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int rank, int nranks,
+                            const nesa_exchange_desc* xd) {
+  {
+    require(d != nullptr, "null argument");
     require(d->abi_version == NESA_ABI_VERSION, "ABI version mismatch");
     require(d->op_dtype == NESA_F64 || d->op_dtype == NESA_F32, "op_dtype must be F64 or F32");
     require(d->Q >= 3 && d->Q <= 256, "Q must be in [3, 256]");
@@ -1822,9 +1968,31 @@ NESA_API int nesa_plan_create(const nesa_plan_desc* d, int device, nesa_plan** o
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
     for (auto& e : P->cap_events) CUDA_OK(cudaEventCreate(&e));
-    *out = P.release();
-    return NESA_OK;
-  })
+    if (comm) {
+      // the plan uses (does not own) the caller's communicator
+      P->comm = static_cast<ncclComm_t>(comm);
+      P->rank = rank;
+      P->nranks = nranks;
+      require(xd->n_export >= 0 && xd->max_export >= std::max<int64_t>(1, xd->n_export) &&
+                  xd->n_import >= 0 && xd->max_contrib >= 1,
+              "bad exchange descriptor");
+      P->x_n_export = xd->n_export;
+      P->x_max_export = xd->max_export;
+      P->x_n_import = xd->n_import;
+      P->x_max_contrib = xd->max_contrib;
+      const int64_t n_recv = int64_t(nranks) * xd->max_export;
+      std::vector<int64_t> ex(xd->export_ids, xd->export_ids + xd->n_export);
+      std::vector<int64_t> im(xd->import_ids, xd->import_ids + xd->n_import);
+      std::vector<int64_t> ct(xd->contrib, xd->contrib + xd->n_import * xd->max_contrib);
+      for (auto v : ex) require(v >= 0 && v < P->G, "export id out of range");
+      for (auto v : im) require(v >= 0 && v < P->G, "import id out of range");
+      for (auto v : ct) require(v >= -1 && v < n_recv + P->G, "contribution row out of range");
+      P->x_export.upload(ex);
+      P->x_import.upload(im);
+      P->x_contrib.upload(ct);
+    }
+    return P.release();
+  }
 }
 
 NESA_API int nesa_matvec(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t nrhs,
@@ -1974,41 +2142,9 @@ NESA_API int nesa_dense_matvec(const double* points_dev, const double* q_dev, do
 }
 
 // ---------------------------------------------------------------------------
-// Multi-GPU halo exchange (paper_1801_03589_b200/dist.py):
-// pack this rank's partial source amplitudes that other ranks need into the
-// all_gather send buffer, and complete the needed groups' amplitudes as the
-// rank-ordered sum of their contributors' partials (contrib rows < n_recv
-// index the gathered buffer, rows >= n_recv this rank's own s[row - n_recv]).
-// One kernel each instead of a dozen torch ops per product.
+// Multi-GPU halo exchange as separate calls (the CPU-side dist layer's path)
 // ---------------------------------------------------------------------------
 namespace {
-template <typename T>
-__global__ void xpack_kernel(const T* __restrict__ s, const int64_t* __restrict__ ids, int64_t n_ids,
-                             int64_t rows, int qr, T* __restrict__ send) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < rows * qr;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = t / qr, w = t - r * qr;
-    send[t] = r < n_ids ? s[ids[r] * qr + w] : T(0);
-  }
-}
-
-template <typename T>
-__global__ void xcombine_kernel(T* s, const T* __restrict__ recv, const int64_t* __restrict__ imp,
-                                const int64_t* __restrict__ contrib, int64_t n_imp, int max_c,
-                                int64_t n_recv, int qr) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < n_imp * qr;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = t / qr, w = t - i * qr;
-    T acc = T(0);
-    for (int k = 0; k < max_c; ++k) {  // fixed rank order: deterministic
-      const int64_t c = contrib[i * max_c + k];
-      if (c < 0) continue;
-      acc += c < n_recv ? recv[c * qr + w] : s[(c - n_recv) * qr + w];
-    }
-    s[imp[i] * qr + w] = acc;  // the only local row read is imp[i]'s own
-  }
-}
-
 int xpack_run(const void* s, const int64_t* ids, int64_t n_ids, int64_t rows, int32_t qr, int32_t f64,
               void* send, void* stream) {
   require(s && send && (ids || n_ids == 0) && rows >= n_ids && qr > 0, "bad exchange pack arguments");

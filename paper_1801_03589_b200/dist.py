@@ -20,9 +20,15 @@ every group covers a contiguous leaf range, so:
 Points are owned by exactly one rank, so phi is partitioned; ``gather=True``
 sums the per-rank outputs (each point written once) into the full vector.
 
-The exchange is plain torch (index_select / all_gather_into_tensor / index
-adds) on whatever device the buffers live on, so the same code runs over
-NCCL on GPUs and over gloo in the CPU tests (tests/test_dist_gloo.py).
+On GPUs the exchange runs inside the product graph: ``DistNesa`` builds a
+distributed plan (C ABI ``nesa_plan_create_dist``) on an NCCL communicator of
+its own (``NcclComm``, bootstrapped over the existing torch.distributed
+group), and one ``nesa_matvec`` per rank captures pack -> ncclAllGather ->
+combine between the upward pass and the translation, with the near field
+running concurrently.  The same exchange tables drive a torch-op version
+(index_select / all_gather_into_tensor / index adds; ``native=False``) that
+runs over gloo in the CPU tests (tests/test_dist_gloo.py) and serves as the
+reference for the CUDA pack / combine kernels.
 """
 
 from __future__ import annotations
@@ -204,10 +210,47 @@ def exchange_tensors(xp: ExchangePlan, device):
             torch.as_tensor(xp.contrib, dtype=torch.long, device=device))
 
 
-class DistNesa:
-    """One rank of a multi-GPU product (torch.distributed already initialised)."""
+class NcclComm:
+    """An NCCL communicator of the product library (nesa_nccl_comm_init),
+    bootstrapped over an initialised torch.distributed group: rank 0 draws
+    the unique id, the group broadcasts it."""
 
-    def __init__(self, tree: Tree, ops, dtype: str = "f32", device: int = 0, group=None):
+    def __init__(self, device: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+        from . import _capi
+        self.lib = _capi.load()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = bytearray(128)
+        if rank == 0:
+            buf = (ctypes.c_char * 128)()
+            _capi.check(self.lib.nesa_nccl_unique_id(buf, 128))
+            uid = bytearray(buf.raw)
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        raw = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        _capi.check(self.lib.nesa_nccl_comm_init(raw, world, rank, device, ctypes.byref(h)))
+        self.handle = h.value
+        self.rank, self.world = rank, world
+
+    def close(self) -> None:
+        if self.handle:
+            self.lib.nesa_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+class DistNesa:
+    """One rank of a multi-GPU product (torch.distributed already initialised).
+
+    ``native`` (default on CUDA): the distributed plan with the exchange in
+    its graph -- one ``nesa_matvec`` launch per product and rank.  Otherwise
+    the stage-1 / Python exchange / stage-2 sequence (the CPU-testable path).
+    """
+
+    def __init__(self, tree: Tree, ops, dtype: str = "f32", device: int = 0, group=None,
+                 native: bool = True):
         import torch.distributed as dist
         from .plan import NesaPlan
         self.tree = tree
@@ -218,15 +261,30 @@ class DistNesa:
         self.Q = params.Q
         self.ranges = partition_leaves(tree, self.world, self.Q)
         self.leaf_range = self.ranges[self.rank]
-        self.plan = NesaPlan(tree, ops, dtype=dtype, device=device, leaf_range=self.leaf_range)
         self.xp = build_exchange(tree, self.ranges, self.rank)
+        self.comm = NcclComm(device, group) if native else None
+        self.plan = NesaPlan(tree, ops, dtype=dtype, device=device, leaf_range=self.leaf_range,
+                             comm=self.comm.handle if native else None, rank=self.rank,
+                             nranks=self.world, exchange=self.xp if native else None)
+        self.native = native
         self._tensors = None
         self.device = device
 
+    def close(self) -> None:
+        self.plan.close()
+        if self.comm is not None:
+            self.comm.close()
+
     def matvec_ptr(self, q_ptr: int, phi_ptr: int, nrhs: int, is_complex: bool,
-                   near: bool = True, far: bool = True, stream: int = 0) -> None:
+                   near: bool = True, far: bool = True, stream: int = 0, profile=False) -> None:
         import torch
         R = nrhs * (2 if is_complex else 1)
+        if self.native:
+            # one graph: gather, near || radiation + upward pass, exchange over
+            # NCCL, translation + downward pass, reception (this rank's points)
+            self.plan.matvec_ptr(q_ptr, phi_ptr, nrhs, is_complex, near=near, far=far, stream=stream,
+                                 profile=profile)
+            return
         self.plan.matvec_ptr(q_ptr, phi_ptr, nrhs, is_complex, near=near, far=far,
                              stream=stream, stage=1)
         if far:

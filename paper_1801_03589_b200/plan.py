@@ -127,7 +127,8 @@ class NesaPlan:
     """
 
     def __init__(self, tree: Tree, ops, dtype: str = "f64", device: int = 0,
-                 leaf_range: tuple[int, int] | None = None, v_on_host: bool | None = None):
+                 leaf_range: tuple[int, int] | None = None, v_on_host: bool | None = None,
+                 comm=None, rank: int = 0, nranks: int = 1, exchange=None):
         self.lib = _capi.load()
         if dtype not in _DTYPES:
             raise ValueError(f"unknown dtype {dtype!r}")
@@ -211,7 +212,23 @@ class NesaPlan:
             d.leaf_begin, d.leaf_end = int(leaf_range[0]), int(leaf_range[1])
         self.leaf_range = leaf_range
         h = ctypes.c_void_p()
-        _capi.check(self.lib.nesa_plan_create(ctypes.byref(d), self.device, ctypes.byref(h)))
+        if comm is None:
+            _capi.check(self.lib.nesa_plan_create(ctypes.byref(d), self.device, ctypes.byref(h)))
+        else:
+            # distributed plan: the halo exchange (pack -> ncclAllGather ->
+            # combine) is captured into the product graph (nesa_plan_create_dist)
+            xp = exchange
+            x = _capi.NesaExchangeDesc()
+            x.n_export = int(xp.export_ids.size)
+            x.export_ids = _ptr(arr("xe", xp.export_ids, np.int64), i64)
+            x.max_export = int(xp.max_export)
+            x.n_import = int(xp.import_ids.size)
+            x.import_ids = _ptr(arr("xi", xp.import_ids, np.int64), i64)
+            x.max_contrib = int(xp.contrib.shape[1]) if xp.contrib.ndim == 2 else 1
+            x.contrib = _ptr(arr("xc", xp.contrib.reshape(-1), np.int64), i64)
+            _capi.check(self.lib.nesa_plan_create_dist(ctypes.byref(d), self.device, ctypes.c_void_p(comm),
+                                                       int(rank), int(nranks), ctypes.byref(x),
+                                                       ctypes.byref(h)))
         self._h = h
         self.n_dtab = int(D.shape[0])
 

@@ -551,3 +551,34 @@ def test_mixed_widths_on_one_plan(dtype, tol):
         assert rel_l2(phi.cpu().numpy(), ref) <= tol
         del qd, phi
     plan.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_distributed_plan_one_rank_matches_plan(dtype):
+    # the in-graph exchange path (nesa_plan_create_dist: pack -> ncclAllGather
+    # -> combine captured into the product graph) on a one-rank NCCL
+    # communicator: bitwise the single-plan product (multi-rank correctness
+    # of the exchange tables is covered by the gloo tests)
+    import torch.distributed as dist
+    from paper_1801_03589_b200.dist import DistNesa
+    if not dist.is_initialized():
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=3), 40000)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    eng = DistNesa(tree, params, dtype=dtype, device=0)
+    plan = NesaPlan(tree, params, dtype=dtype)
+    cdt = np.complex64 if dtype == "f32" else np.complex128
+    q = torch.from_numpy(geo.random_rhs(40000, 3).astype(cdt)).cuda()
+    a, b = torch.zeros_like(q), torch.zeros_like(q)
+    st = torch.cuda.current_stream().cuda_stream
+    eng.matvec_ptr(q.data_ptr(), a.data_ptr(), 1, True, stream=st)
+    plan.matvec_ptr(q.data_ptr(), b.data_ptr(), 1, True, stream=st)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    eng.close()
+    plan.close()
