@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define NESA_ABI_VERSION 1
+#define NESA_ABI_VERSION 2
 
 typedef enum {
   NESA_OK = 0,
@@ -127,7 +127,13 @@ typedef struct nesa_plan_desc {
    * source amplitudes of remote interaction partners arrive through the
    * halo exchange between nesa_matvec_stage 1 and 2. */
   int64_t leaf_begin, leaf_end;
+
+  uint32_t options;             /* NESA_PLAN_* bits                                 */
 } nesa_plan_desc;
+
+/* nesa_plan_desc.options */
+#define NESA_PLAN_FAR_ONLY 1u   /* no near operator: far-field products only (extra
+                                   plans that share the columns of a many-RHS product) */
 
 int nesa_plan_create(const nesa_plan_desc* desc, int device, nesa_plan** out);
 
@@ -193,6 +199,17 @@ int nesa_nccl_comm_destroy(void* comm);
 int nesa_matvec_cols(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t ld_real,
                      int32_t col0, int32_t ncols_real, uint32_t flags, void* stream);
 
+/* phi[:, col0 : col0 + ncols_real] += near field of q for real columns of
+ * (N, ld_real) row-major blocks in original order: float32 plans with tensor
+ * cores, 128 columns per tcgen05 GEMM pass with the operator streamed once
+ * (C5: many right-hand sides).  nesa_matvec / nesa_matvec_cols with more
+ * than 4 real columns on such a plan run the far field in blocks and this
+ * for the near field; callers splitting the far field over several plans
+ * (nesa_matvec_cols with NESA_FAR only) add the near field with this call.
+ * The first call packs the operator into the tensor-core layout. */
+int nesa_matvec_near_wide(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t ld_real,
+                          int32_t col0, int32_t ncols_real, void* stream);
+
 int nesa_plan_destroy(nesa_plan* plan);
 
 const char* nesa_last_error(void);
@@ -211,6 +228,7 @@ int nesa_abi_version(void);
 #define NESA_STAT_U_TERMS 9          /* incoming expansion terms (0: stored U)    */
 #define NESA_STAT_GRAPH_CAPTURES 10  /* stream captures so far (one per schedule)  */
 #define NESA_STAT_GRAPHS_CACHED 11   /* instantiated graphs held by the plan       */
+#define NESA_STAT_NEAR_WIDE 12       /* 1: nesa_matvec_near_wide available          */
 int64_t nesa_plan_stat(nesa_plan* plan, int32_t which);
 
 /* Profiling: with NESA_PROFILE in flags each nesa_matvec records CUDA

@@ -12,7 +12,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NESA_LIB") or os.path.join(_HERE, "libnesa_b200.so")  # NESA_LIB: A/B builds
 
-NESA_ABI_VERSION = 1
+NESA_ABI_VERSION = 2
+NESA_PLAN_FAR_ONLY = 1
 NESA_OK = 0
 NESA_ERR_INVALID = 1
 NESA_ERR_CUDA = 2
@@ -27,7 +28,7 @@ NESA_PROFILE_NEAR = 32
 
 STAT = {"near_entries": 0, "v_entries": 1, "u_entries": 2, "d_refs": 3, "n_dtab": 4,
         "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7, "v_moments": 8,
-        "u_terms": 9, "graph_captures": 10, "graphs_cached": 11}
+        "u_terms": 9, "graph_captures": 10, "graphs_cached": 11, "near_wide": 12}
 STAGE = {"total": 0, "near": 1, "far": 2, "reception": 3}
 
 EXPORTED_SYMBOLS = (
@@ -37,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "nesa_ktrace_enable", "nesa_ktrace_read", "nesa_dense_matvec", "nesa_matvec_cols",
     "nesa_tree_build", "nesa_tree_error", "nesa_tree_size", "nesa_tree_copy", "nesa_tree_free",
     "nesa_exchange_pack", "nesa_exchange_combine", "nesa_plan_create_dist", "nesa_nccl_unique_id",
-    "nesa_nccl_comm_init", "nesa_nccl_comm_destroy",
+    "nesa_nccl_comm_init", "nesa_nccl_comm_destroy", "nesa_matvec_near_wide",
 )
 
 _p = ctypes.c_void_p
@@ -65,6 +66,7 @@ class NesaPlanDesc(ctypes.Structure):
         ("leaf_r_inaux", _f64p), ("out_fit_leaf", _f64p),
         ("check_cos", _f64p), ("check_sin", _f64p), ("aux_cos", _f64p), ("aux_sin", _f64p),
         ("leaf_begin", ctypes.c_int64), ("leaf_end", ctypes.c_int64),
+        ("options", ctypes.c_uint32),
     ]
 
 
@@ -155,6 +157,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_nccl_comm_init.restype = ctypes.c_int
     lib.nesa_nccl_comm_destroy.argtypes = [_p]
     lib.nesa_nccl_comm_destroy.restype = ctypes.c_int
+    lib.nesa_matvec_near_wide.argtypes = [_p, _p, _p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _p]
+    lib.nesa_matvec_near_wide.restype = ctypes.c_int
     if lib.nesa_abi_version() != NESA_ABI_VERSION:
         raise RuntimeError("libnesa_b200.so ABI version mismatch; rebuild")
     _lib = lib

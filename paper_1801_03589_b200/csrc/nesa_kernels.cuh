@@ -2949,6 +2949,221 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
 }
 
 // ----------------------------------------------------------------------------
+// Near field for many right-hand sides on the tensor cores (float32 plans;
+// C5: 64 plane waves = 128 real columns).  phi[perm p] += sum_j K_pj q_j for
+// up to 128 real columns at once.  An item = <= 256 target rows of a leaf
+// (padded to N = 16 k) against the leaf's near slab (W source points).  The
+// MMA computes D (128 x N) = X^T (128 x W) K^T (W x N): M = the right-hand-side
+// columns, so one tile covers 128 columns and the operator is streamed ONCE
+// for all of them (the 4-column blocks streamed it 32 times).  K arrives by
+// bulk copy in chunks of 32 source points, tf32 hi | lo pre-split in the
+// canonical K-major layout (N rows x 32 k); X^T rows (thread r = column r)
+// are read straight from the caller's q in ORIGINAL order (the permutation is
+// folded into the item's source table: coalesced 512-byte rows), split and
+// stored to TMEM; the chunk pipeline keeps the next chunk's X in registers
+// and its K in flight while the tensor core works.  The epilogue adds the
+// 128 x N tile into phi (each target row a coalesced 512-byte row).
+// ----------------------------------------------------------------------------
+struct NearTcItem {
+  int64_t b_off;      // float offset of the item's canonical blob (kchunks x [hi | lo] x npad x 32)
+  int64_t a_off;      // column-major near blob offset of the block item (packing input)
+  int32_t m, npad;    // target rows, rows padded to a multiple of 16 (<= 256)
+  int32_t w, kchunks; // slab width (source points), 32-point chunks
+  int32_t y_row0;     // first target row (tree order)
+  int32_t src_off;    // first entry of the item's source table (original indices)
+  int32_t ld, r0;     // packing: leading dimension and first row within the block item
+};
+constexpr int kNearTcK = 32;
+constexpr int kNearTcMaxN = 256;
+constexpr uint32_t kNearTcSBO = kNearTcK * 8 * 4;  // bytes between 8-row groups of a chunk
+
+// column-major near blob -> per-item canonical tf32 hi | lo chunks
+__global__ void near_tc_pack_kernel(const NearTcItem* __restrict__ items, const float* __restrict__ blob,
+                                    float* __restrict__ out) {
+  const NearTcItem it = items[blockIdx.x];
+  const int64_t per_chunk = int64_t(it.npad) * kNearTcK;
+  for (int64_t e = threadIdx.x; e < int64_t(it.kchunks) * per_chunk; e += blockDim.x) {
+    const int c = int(e / per_chunk);
+    const int rem = int(e - int64_t(c) * per_chunk);
+    const int n = rem / kNearTcK, kk = rem - (rem / kNearTcK) * kNearTcK;
+    const int k = c * kNearTcK + kk;
+    const float x = (n < it.m && k < it.w) ? blob[it.a_off + int64_t(k) * it.ld + it.r0 + n] : 0.f;
+    const float hi = tf32_rna(x), lo = tf32_rna(x - hi);
+    const int64_t base = it.b_off + int64_t(c) * 2 * per_chunk;
+    const int off = (n >> 3) * (kNearTcK * 8) + (kk >> 2) * 32 + (n & 7) * 4 + (kk & 3);
+    out[base + off] = hi;
+    out[base + per_chunk + off] = lo;
+  }
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void umma_tf32_ts_n(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(accumulate), "r"(idesc), "r"(0u));
+}
+
+constexpr size_t near_tc_smem_bytes() {
+  return size_t(2) * 2 * kNearTcMaxN * kNearTcK * 4 + 64;
+}
+
+__global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __restrict__ items, int n_items,
+                                                         const int32_t* __restrict__ src,
+                                                         const float* __restrict__ blob,
+                                                         const float* __restrict__ q, int ldq, int c0,
+                                                         int ncols, const int64_t* __restrict__ perm,
+                                                         float* __restrict__ phi) {
+  KtScope kt_(90);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* Bs = reinterpret_cast<float*>(smem);  // 2 buffers x [hi | lo] x npad x 32
+  constexpr int kBufFloats = 2 * kNearTcMaxN * kNearTcK;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + size_t(2) * kBufFloats * 4);  // [0,1] B, [2,3] MMA
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  const bool col_live = tid < ncols;
+  const float* qc = q + c0 + tid;
+  // per-slot state as bits (slot s = bit s): barrier phases, MMA outstanding
+  uint32_t bphase = 0u, mphase = 0u, pending = 0u;
+  auto wait_mma = [&](int slot) {
+    if (pending & (1u << slot)) {
+      mbar_wait(&bar[2 + slot], (mphase >> slot) & 1u);
+      mphase ^= 1u << slot;
+      pending &= ~(1u << slot);
+    }
+  };
+  auto issue_b = [&](const NearTcItem& it, int c, int slot) {
+    const uint32_t bytes = uint32_t(it.npad) * kNearTcK * 4 * 2;
+    mbar_arrive_expect_tx(&bar[slot], bytes);
+    bulk_g2s(Bs + slot * kBufFloats, blob + it.b_off + int64_t(c) * 2 * it.npad * kNearTcK, bytes, &bar[slot]);
+  };
+  // X^T values of chunk c of item it for this thread's column: 32 source rows
+  auto load_x = [&](const NearTcItem& it, int c, float (&x)[kNearTcK]) {
+#pragma unroll
+    for (int kk = 0; kk < kNearTcK; ++kk) {
+      const int k = c * kNearTcK + kk;
+      x[kk] = (col_live && k < it.w) ? __ldg(qc + int64_t(src[it.src_off + k]) * ldq) : 0.f;
+    }
+  };
+  int gc = 0;  // chunks issued by this CTA (slot = gc & 1)
+  int item = blockIdx.x;
+  NearTcItem it{};
+  float xn[kNearTcK];
+  if (item < n_items) {
+    it = items[item];
+    if (tid == 0) issue_b(it, 0, 0);
+    load_x(it, 0, xn);
+  }
+  while (item < n_items) {
+    const int next_item = item + int(gridDim.x);
+    NearTcItem nx{};
+    if (next_item < n_items) nx = items[next_item];
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t(it.npad) >> 3) << 17) |
+                           ((128u >> 4) << 24);
+    for (int c = 0; c < it.kchunks; ++c, ++gc) {
+      const int slot = gc & 1;
+      float x[kNearTcK];
+#pragma unroll
+      for (int kk = 0; kk < kNearTcK; ++kk) x[kk] = xn[kk];
+      // the next chunk (this item's or the next item's first) in flight
+      const bool last = c + 1 == it.kchunks;
+      if (!last)
+        load_x(it, c + 1, xn);
+      else if (next_item < n_items)
+        load_x(nx, 0, xn);
+      wait_mma(slot);  // chunk gc - 2 released this A slot
+      const uint32_t t_hi = tmem + lane_base + 256 + 64 * slot, t_lo = t_hi + 32;
+#pragma unroll
+      for (int kb = 0; kb < kNearTcK / 4; ++kb)
+        tc_put4(t_hi, t_lo, kb, make_float4(x[4 * kb], x[4 * kb + 1], x[4 * kb + 2], x[4 * kb + 3]));
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        mbar_wait(&bar[slot], (bphase >> slot) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bh = smem_u32(Bs + slot * kBufFloats);
+        const uint32_t bl = bh + uint32_t(it.npad) * kNearTcK * 4;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const uint32_t a0 = tmem + 256 + 64 * slot + (cc == 2 ? 32u : 0u), b0 = cc == 1 ? bl : bh;
+#pragma unroll
+          for (int ks = 0; ks < kNearTcK / 8; ++ks)
+            umma_tf32_ts_n(tmem, a0 + ks * 8, umma_desc_kmajor_sbo(b0 + ks * 2 * kTcLBO, kNearTcSBO), idesc,
+                           (c | cc | ks) != 0);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&bar[2 + slot]))
+                     : "memory");
+      }
+      bphase ^= 1u << slot;
+      pending |= 1u << slot;
+      // the next chunk's K into the other buffer once its previous MMA is done
+      if (!last || next_item < n_items) {
+        const int ns = (gc + 1) & 1;
+        wait_mma(ns);
+        if (tid == 0) issue_b(last ? nx : it, last ? 0 : c + 1, ns);
+      }
+    }
+    // ---- epilogue: the item's 128 x npad tile into phi (rows = targets)
+    wait_mma((gc - 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int n0 = 0; n0 < it.m; n0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_base + uint32_t(n0), r);
+      const int nn = it.m - n0 < 32 ? it.m - n0 : 32;
+      int64_t dst[32];
+      float cur[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) dst[j] = j < nn ? perm[it.y_row0 + n0 + j] : 0;
+      if (col_live) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) cur[j] = j < nn ? phi[dst[j] * ldq + c0 + tid] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nn) phi[dst[j] * ldq + c0 + tid] = cur[j] + __uint_as_float(r[j]);
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // accumulator read before the next item overwrites it
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    item = next_item;
+    it = nx;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ----------------------------------------------------------------------------
 // Multi-GPU halo exchange (paper_1801_03589_b200/dist.py):
 // pack this rank's partial source amplitudes that other ranks need into the
 // all_gather send buffer, and complete the needed groups' amplitudes as the

@@ -331,6 +331,7 @@ struct nesa_plan {
   int Q = 0, n_check = 0, l0 = 0, L = 0;
   int64_t N = 0, NL = 0, G = 0;
   int64_t leaf_begin = 0, leaf_end = 0;  // local target leaves
+  bool far_only = false;                 // NESA_PLAN_FAR_ONLY: no near operator at all
   int64_t pt_begin = 0, pt_end = 0;      // local tree-order point range
   int n_sm = 148;
 
@@ -347,6 +348,15 @@ struct nesa_plan {
   int64_t n_dtab = 0, d_refs = 0;
 
   DevBlockSet nearset, Vset, Uset;
+  // many right-hand sides (float32 with tensor cores): the near field as one
+  // tcgen05 GEMM over up to 128 columns (near_tc_kernel); its canonical tf32
+  // blob is packed from the near blob on first use
+  bool near_tc = false;                     // float32 and NESA_TC != 0 (any Q)
+  DevBuf<NearTcItem> ntc_items;
+  DevBuf<int32_t> ntc_src;                  // slab columns -> original point index
+  DevBuf<float> ntc_blob;
+  int64_t ntc_floats = 0;
+  int ntc_n = 0;
 
   // translation: entries grouped by unique D (see tgemm_kernel)
   DevBuf<TUnit> tunits;
@@ -607,6 +617,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
   }
 
+  // the many-RHS near field on the tensor cores works for any Q
+  P->near_tc = std::is_same<T, float>::value && P->tc;
   // ---- tables
   const int64_t nlt = P->L - P->l0;
   P->mbytes = mat_bytes(Q, sizeof(T));
@@ -804,7 +816,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         W += d->group_stop[b] - d->group_start[b];
       }
       require(W < (int64_t(1) << 31), "near slab too wide");
-      if (a >= lb && a < le) {
+      if (a >= lb && a < le && !P->far_only) {
         // near item(s): panels of <= kMaxRows rows
         const int32_t seg_begin = int32_t(hn.segs.size());
         int32_t col = 0;
@@ -833,6 +845,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           hn.blob_elems += int64_t(ld) * W;
           hn.entries += int64_t(m) * W;
         }
+      }
+      if (a >= lb && a < le) {
         // V: Q x na, x = qt rows of the leaf, y = s rows of leaf a
         {
           const int32_t sb = int32_t(hv.segs.size());
@@ -878,6 +892,41 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
+  if (P->near_tc && !hn.items.empty()) {
+    // tensor-core items: <= 256 target rows each, the slab's source points
+    // as original indices (the caller's q is read without a gather)
+    std::vector<NearTcItem> ti;
+    std::vector<int32_t> src;
+    int64_t off = 0;
+    for (const BlockItem& bi : hn.items) {
+      const int32_t src_off = int32_t(src.size());
+      require(int64_t(src.size()) + bi.n < (int64_t(1) << 31), "near source table too large");
+      for (int sg = bi.seg_begin; sg < bi.seg_begin + bi.seg_count; ++sg) {
+        const BlockSeg S = hn.segs[size_t(sg)];
+        const int c1 = sg + 1 < bi.seg_begin + bi.seg_count ? hn.segs[size_t(sg) + 1].col0 : bi.n;
+        for (int c = S.col0; c < c1; ++c) src.push_back(int32_t(d->perm[S.x_row0 + (c - S.col0)]));
+      }
+      for (int r0 = 0; r0 < bi.m; r0 += kNearTcMaxN) {
+        NearTcItem t{};
+        t.b_off = off;
+        t.a_off = bi.a_off;
+        t.m = std::min(kNearTcMaxN, bi.m - r0);
+        t.npad = (t.m + 15) / 16 * 16;
+        t.w = bi.n;
+        t.kchunks = (bi.n + kNearTcK - 1) / kNearTcK;
+        t.y_row0 = bi.y_row0 + r0;
+        t.src_off = src_off;
+        t.ld = bi.ld;
+        t.r0 = r0;
+        off += int64_t(t.kchunks) * 2 * t.npad * kNearTcK;
+        ti.push_back(t);
+      }
+    }
+    P->ntc_items.upload(ti);
+    P->ntc_src.upload(src);
+    P->ntc_floats = off;
+    P->ntc_n = int(ti.size());
+  }
   if (!P->v_mom) upload_blockset<T>(P->Vset, hv);
   upload_blockset<T>(P->Uset, hu);
 
@@ -1736,6 +1785,33 @@ int enqueue_dispatch(nesa_plan* P, const void* q, void* phi, int R, int ldv, uin
 int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t flags, void* stream,
               int stage);
 
+bool near_wide_ok(const nesa_plan* P) { return P->dtype == NESA_F32 && P->near_tc && P->ntc_n > 0; }
+
+// phi[:, col0 : col0 + ncols] += near(q) for real columns of (N, ld) blocks in
+// original order, 128 columns per tensor-core pass (stream-ordered)
+void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int ncols, cudaStream_t st) {
+  require(near_wide_ok(P), "the wide near field needs a float32 plan with tensor cores");
+  require(ld >= 1 && col0 >= 0 && ncols >= 1 && col0 + ncols <= ld, "bad column range");
+  CUDA_OK(cudaSetDevice(P->device));
+  if (!P->ntc_blob.p) {
+    P->ntc_blob.alloc(size_t(std::max<int64_t>(P->ntc_floats, 1)));
+    near_tc_pack_kernel<<<P->ntc_n, 256>>>(P->ntc_items.p, reinterpret_cast<const float*>(P->nearset.blob.p),
+                                           P->ntc_blob.p);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaFuncSetAttribute(near_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(near_tc_smem_bytes())));
+  }
+  const int grid = std::min(P->ntc_n, P->n_sm);
+  for (int c = col0; c < col0 + ncols; c += 128) {
+    const int nc = std::min(128, col0 + ncols - c);
+    near_tc_kernel<<<grid, 128, near_tc_smem_bytes(), st>>>(
+        P->ntc_items.p, P->ntc_n, P->ntc_src.p, P->ntc_blob.p, static_cast<const float*>(q), ld, c, nc,
+        P->perm.p, static_cast<float*>(phi));
+    CUDA_OK(cudaGetLastError());
+  }
+}
+
 // One product of nrhs right-hand sides: real columns are processed in blocks
 // of <= 4 (one captured graph per block width; rows of q / phi keep their stride).
 int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_complex,
@@ -1749,18 +1825,24 @@ int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_
   require(stage == 0, "the staged (multi-GPU) product takes at most 4 real columns");
   require(!(flags & NESA_PROFILE), "profiling takes at most 4 real columns");
   const size_t es = P->esz;
+  // float32 with tensor cores: the far field in blocks of <= 4 columns, then
+  // the near field ONCE for all columns (tcgen05 GEMM, operator read once)
+  const bool wide = (flags & NESA_NEAR) && near_wide_ok(P) && P->comm == nullptr;
+  const uint32_t bflags = wide ? (flags & ~NESA_NEAR) : flags;
   for (int c0 = 0; c0 < Rt;) {
     const int Rb = Rt - c0 >= 4 ? 4 : (Rt - c0 >= 2 ? 2 : 1);
     run_block(P, static_cast<const char*>(q) + c0 * es, static_cast<char*>(phi) + c0 * es, Rb, Rt,
-              flags, stream, stage);
+              bflags, stream, stage);
     c0 += Rb;
   }
+  if (wide) run_near_wide(P, q, phi, Rt, 0, Rt, static_cast<cudaStream_t>(stream));
   return NESA_OK;
 }
 
 int run_block(nesa_plan* P, const void* q, void* phi, int R, int ldv, uint32_t flags, void* stream,
               int stage) {
   CUDA_OK(cudaSetDevice(P->device));
+  require(!(P->far_only && (flags & NESA_NEAR)), "this plan was created without the near field (NESA_PLAN_FAR_ONLY)");
   // the workspace for the widest block so far (growing it drops every graph)
   if (P->dtype == NESA_F64)
     ensure_workspace<double>(P, R);
@@ -1942,6 +2024,7 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     if (const char* tr = std::getenv("NESA_TRACE")) P->trace = std::atoi(tr) != 0;
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
+    P->far_only = (d->options & NESA_PLAN_FAR_ONLY) != 0;
     if (P->leaf_end <= P->leaf_begin) {
       P->leaf_begin = 0;
       P->leaf_end = P->NL;
@@ -2015,6 +2098,15 @@ int run_cols(nesa_plan* P, const void* q, void* phi, int32_t ld, int32_t col0, i
     c0 += Rb;
   }
   return NESA_OK;
+}
+
+NESA_API int nesa_matvec_near_wide(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t ld_real,
+                                   int32_t col0, int32_t ncols_real, void* stream) {
+  NESA_GUARD({
+    require(plan != nullptr && q_dev != nullptr && phi_dev != nullptr, "null argument");
+    run_near_wide(plan, q_dev, phi_dev, ld_real, col0, ncols_real, static_cast<cudaStream_t>(stream));
+    return NESA_OK;
+  })
 }
 
 NESA_API int nesa_matvec_cols(nesa_plan* plan, const void* q_dev, void* phi_dev, int32_t ld_real,
@@ -2224,6 +2316,8 @@ NESA_API int64_t nesa_plan_stat(nesa_plan* P, int32_t which) {
       return P->graph_captures;
     case NESA_STAT_GRAPHS_CACHED:
       return int64_t(P->graphs.size());
+    case NESA_STAT_NEAR_WIDE:
+      return near_wide_ok(P) ? 1 : 0;
     default:
       return -1;
   }

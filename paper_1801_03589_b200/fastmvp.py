@@ -92,18 +92,23 @@ class RhsLanes:
     """Many right-hand sides spread over ``lanes`` plans of the same problem
     (each with its own workspace and CUDA graphs) on ``lanes`` streams.
 
-    One plan runs a multi-column product as blocks of <= 4 real columns one
-    after another; every block walks the latency-bound far-field chain again.
-    Blocks of different lanes run concurrently, so their far chains overlap
-    each other and the near-field streams (C5's 64 plane waves).  The column
-    ranges are multiples of 4, so the block decomposition -- and every result
-    bit -- is that of the single-plan product.
+    The far field runs in blocks of <= 4 real columns, and every block walks
+    the latency-bound far-field chain again; blocks of different lanes run
+    concurrently, so their chains overlap.  On float32 plans with tensor
+    cores the near field is ONE tcgen05 GEMM over all columns
+    (nesa_matvec_near_wide, operator streamed once) after the lanes join, and
+    the extra lanes are far-only plans (no near operator uploaded).  Otherwise
+    each block also carries its near field.  The column ranges are multiples
+    of 4, so the block decomposition -- and every result bit -- is that of
+    the single-plan product.
     """
 
     def __init__(self, plan: NesaPlan, lanes: int):
         import torch
+        self.wide = plan.stat("near_wide") == 1
         self.plans = [plan] + [NesaPlan(plan.tree, plan.ops_in, dtype=plan.dtype,
-                                        device=plan.device) for _ in range(lanes - 1)]
+                                        device=plan.device, far_only=self.wide)
+                               for _ in range(lanes - 1)]
         self.streams = [torch.cuda.Stream(plan.device) for _ in range(lanes)]
         self.events = [torch.cuda.Event() for _ in range(lanes)]
 
@@ -115,6 +120,7 @@ class RhsLanes:
         lanes = min(len(self.plans), blocks)
         per = -(-blocks // lanes) * 4
         caller = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        wide_near = near and self.wide
         fork = torch.cuda.Event()
         fork.record(caller)
         used = []
@@ -125,12 +131,14 @@ class RhsLanes:
                 break
             s = self.streams[k]
             s.wait_event(fork)
-            self.plans[k].matvec_cols_ptr(q_ptr, phi_ptr, rt, c0, n, near=near, far=far,
-                                          stream=s.cuda_stream)
+            self.plans[k].matvec_cols_ptr(q_ptr, phi_ptr, rt, c0, n, near=near and not wide_near,
+                                          far=far, stream=s.cuda_stream)
             self.events[k].record(s)
             used.append(k)
         for k in used:
             caller.wait_event(self.events[k])
+        if wide_near:
+            self.plans[0].near_wide_ptr(q_ptr, phi_ptr, rt, 0, rt, stream=caller.cuda_stream)
 
 
 def get_lanes(tree, ops, dtype: str = "f64", device: int = 0, lanes: int | None = None) -> RhsLanes:

@@ -128,7 +128,7 @@ class NesaPlan:
 
     def __init__(self, tree: Tree, ops, dtype: str = "f64", device: int = 0,
                  leaf_range: tuple[int, int] | None = None, v_on_host: bool | None = None,
-                 comm=None, rank: int = 0, nranks: int = 1, exchange=None):
+                 comm=None, rank: int = 0, nranks: int = 1, exchange=None, far_only: bool = False):
         self.lib = _capi.load()
         if dtype not in _DTYPES:
             raise ValueError(f"unknown dtype {dtype!r}")
@@ -210,6 +210,9 @@ class NesaPlan:
             assert tables.leaf_h.shape[0] == nl
         if leaf_range is not None:
             d.leaf_begin, d.leaf_end = int(leaf_range[0]), int(leaf_range[1])
+        # far_only: no near operator (extra plans of a many-RHS product)
+        d.options = _capi.NESA_PLAN_FAR_ONLY if far_only else 0
+        self.far_only = far_only
         self.leaf_range = leaf_range
         h = ctypes.c_void_p()
         if comm is None:
@@ -287,6 +290,14 @@ class NesaPlan:
         _capi.check(self.lib.nesa_matvec_cols(self.handle, ctypes.c_void_p(q_ptr),
                                               ctypes.c_void_p(phi_ptr), ld_real, col0, ncols, flags,
                                               ctypes.c_void_p(stream)))
+
+    def near_wide_ptr(self, q_ptr: int, phi_ptr: int, ld_real: int, col0: int, ncols: int,
+                      stream: int = 0) -> None:
+        """phi[:, col0:col0+ncols] += near field of q (float32 + tensor cores,
+        128 real columns per tcgen05 pass; operator streamed once)."""
+        _capi.check(self.lib.nesa_matvec_near_wide(self.handle, ctypes.c_void_p(q_ptr),
+                                                   ctypes.c_void_p(phi_ptr), ld_real, col0, ncols,
+                                                   ctypes.c_void_p(stream)))
 
     def s_dev_ptr(self, nrhs_real: int) -> int:
         p = self.lib.nesa_plan_s_dev(self.handle, nrhs_real)

@@ -36,9 +36,11 @@ def test_descriptor_layout_matches_header():
 #include <stddef.h>
 #include "nesa_b200.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu\n", sizeof(nesa_plan_desc), offsetof(nesa_plan_desc, perm),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(nesa_plan_desc), offsetof(nesa_plan_desc, perm),
          offsetof(nesa_plan_desc, near_blob), offsetof(nesa_plan_desc, aux_sin),
-         offsetof(nesa_plan_desc, leaf_end));
+         offsetof(nesa_plan_desc, leaf_end), offsetof(nesa_plan_desc, options),
+         sizeof(nesa_exchange_desc), offsetof(nesa_exchange_desc, max_contrib),
+         offsetof(nesa_exchange_desc, contrib));
   return 0;
 }
 '''
@@ -52,8 +54,10 @@ int main(void) {
             pytest.skip("no C compiler")
         out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout.split()
     D = _capi.NesaPlanDesc
+    X = _capi.NesaExchangeDesc
     assert [int(x) for x in out] == [ctypes.sizeof(D), D.perm.offset, D.near_blob.offset,
-                                     D.aux_sin.offset, D.leaf_end.offset]
+                                     D.aux_sin.offset, D.leaf_end.offset, D.options.offset,
+                                     ctypes.sizeof(X), X.max_contrib.offset, X.contrib.offset]
 
 
 def test_create_rejects_bad_descriptor_without_gpu():

@@ -582,3 +582,47 @@ def test_distributed_plan_one_rank_matches_plan(dtype):
     assert torch.equal(a, b)
     eng.close()
     plan.close()
+
+
+@pytest.mark.parametrize("Q,P", [(48, 64), (64, 64), (24, 32)])
+def test_c5_plane_waves_near_on_tensor_cores(Q, P):
+    # C5 (BASELINE configs[4]) at a reduced size: 64 plane waves = 128 real
+    # columns.  float32 plans run the near field as ONE tcgen05 GEMM over all
+    # columns (nesa_matvec_near_wide) and the far field in 4-column blocks;
+    # every column against the oracle, and the lanes path (extra far-only
+    # plans) bitwise equal to the one-plan product
+    from paper_1801_03589_b200.fastmvp import RhsLanes
+    n = 20000
+    spec = geo.CurveSpec(kind="ellipse-plates", seed=4)
+    pts = geo.generate_sources(spec, n)
+    tree = build_tree(pts, TreeParams(P=P))
+    params = NesaParams(Q=Q)
+    k = geo.wavenumber(spec, n)
+    Qm = geo.plane_wave_rhs(pts, k, n_waves=64)
+    plan = NesaPlan(tree, params, dtype="f32")
+    assert plan.stat("near_wide") == 1
+    qd = torch.from_numpy(Qm.astype(np.complex64)).cuda()
+    a, b = torch.empty_like(qd), torch.empty_like(qd)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.matvec_ptr(qd.data_ptr(), a.data_ptr(), 64, True, stream=st)
+    lanes = RhsLanes(plan, 4)
+    assert all(p.far_only for p in lanes.plans[1:])
+    lanes.matvec_ptr(qd.data_ptr(), b.data_ptr(), 64, True, stream=st)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    ops = build_all(tree, params)
+    cols = [0, 17, 63]
+    ref = oracle_mvp(tree, ops, Qm[:, cols])
+    got = a.cpu().numpy()[:, cols]
+    for j in range(len(cols)):
+        assert rel_l2(got[:, j], ref[:, j]) <= 1e-5
+    # the near field alone (wide GEMM) against the oracle's near part
+    c = torch.zeros_like(qd)
+    plan.near_wide_ptr(qd.data_ptr(), c.data_ptr(), 128, 0, 128, stream=st)
+    torch.cuda.synchronize()
+    refn = oracle_mvp(tree, ops, Qm[:, cols], far=False)
+    for j, col in enumerate(cols):
+        assert rel_l2(c.cpu().numpy()[:, col], refn[:, j]) <= 1e-5
+    for p in lanes.plans[1:]:
+        p.close()
+    plan.close()

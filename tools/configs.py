@@ -95,7 +95,8 @@ def c5(a):
             rec = {"config": "C5", "N": n, "P": P, "Q": Q, "rhs": 64, "levels": tree.L - tree.l0 + 1,
                    "plan": "f32"}
             lanes = RhsLanes(plan, 4)
-            for tag, eng in (("one_plan", plan), ("lanes4", lanes)):
+            lanes8 = RhsLanes(plan, 8)
+            for tag, eng in (("one_plan", plan), ("lanes4", lanes), ("lanes8", lanes8)):
                 for _ in range(3):
                     eng.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -108,8 +109,20 @@ def c5(a):
                 ms = e0.elapsed_time(e1) / reps
                 rec[f"ms_per_64rhs_product_{tag}"] = round(ms, 3)
                 rec[f"rhs_products_per_s_{tag}"] = round(64e3 / ms, 1)
+            # the near field alone: one tcgen05 GEMM pass over the 128 real columns
+            if plan.stat("near_wide"):
+                for _ in range(3):
+                    plan.near_wide_ptr(qd.data_ptr(), phi.data_ptr(), 128, 0, 128, stream=st.cuda_stream)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(20):
+                    plan.near_wide_ptr(qd.data_ptr(), phi.data_ptr(), 128, 0, 128, stream=st.cuda_stream)
+                e1.record(st)
+                e1.synchronize()
+                rec["near_wide_ms"] = round(e0.elapsed_time(e1) / 20, 4)
+                rec["near_entries"] = plan.stat("near_entries")
             print(json.dumps(rec), flush=True)
-            for p_ in lanes.plans[1:]:
+            for p_ in lanes.plans[1:] + lanes8.plans[1:]:
                 p_.close()
             plan.close()
 
