@@ -213,6 +213,19 @@ int nesa_matvec_near_wide(nesa_plan* plan, const void* q_dev, void* phi_dev, int
 int nesa_plan_destroy(nesa_plan* plan);
 
 const char* nesa_last_error(void);
+
+/* One Arnoldi step of the GMRES solver around the product (SURVEY.md §8f row
+ * 2; the reference has no solver): orthogonalise w against the basis
+ * V[0..kk) (V[j] = basis + j * stride elements; complex vectors of n
+ * elements, float32 or float64) by classical Gram-Schmidt applied twice in
+ * three passes over the basis, write v_out = w'' / |w''| and the Hessenberg
+ * column hcol[0..kk] (float64 (re, im) pairs: h1 + h2, then |w''|).  work:
+ * nesa_gs_work_bytes() bytes of device memory.  Stream-ordered, no host
+ * synchronisation, bitwise reproducible; 1 <= kk <= 128. */
+int64_t nesa_gs_work_bytes(void);
+int nesa_gs_step(const void* basis, int64_t stride, int32_t kk, void* w, void* v_out, int64_t n,
+                 int32_t is_f64, void* work, void* hcol, void* stream);
+const char* nesa_gs_last_error(void);
 int nesa_abi_version(void);
 
 /* Plan statistics: see NESA_STAT_* */

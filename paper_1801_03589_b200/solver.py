@@ -12,10 +12,13 @@ side: the columns run independent Arnoldi processes in lockstep, so each
 iteration is ONE multi-column product (the plan streams the near-field
 operator once for up to 4 real columns, see nesa_plan.cu run_matvec).
 
-Orthogonalisation is classical Gram-Schmidt applied twice (CGS2: two
-batched projections against the basis per iteration).  Only the small
-Hessenberg / Givens bookkeeping (restart x restart per column) lives on the
-host.  ``shift`` turns the first-kind log-kernel system
+Orthogonalisation is classical Gram-Schmidt applied twice (CGS2).  For one
+complex column it is the library's fused step (``nesa_gs_step``: three
+passes over the basis, the Hessenberg column written on the device, no
+host round trip); the host applies the Givens rotations of iteration k while
+the GPU already runs iteration k+1 (the convergence test lags one iteration,
+the extra product is discarded).  Several columns run in lockstep with
+batched torch projections.  ``shift`` turns the first-kind log-kernel system
 into a second-kind one when wanted (the first-kind system is ill conditioned
 and converges slowly, as for any first-kind integral equation).
 """
@@ -52,8 +55,67 @@ def _givens(a: complex, b: complex):
     return c, s
 
 
+def _arnoldi_fused(A, V, H, cs, sn, g, k_max, bnorm, done, tol, history, iters, maxiter, w_buf,
+                   gs_work, lib, stream, is_f64):
+    """One restart cycle for one complex column: products and CGS2 steps on
+    the device (nesa_gs_step), Givens rotations on the host one iteration
+    behind.  Returns the number of basis columns to use."""
+    import torch
+    from . import _capi
+    n = V.shape[1]
+    stride = V[1].data_ptr() - V[0].data_ptr()
+    stride //= V.element_size() // 2           # in real elements
+    hdev = torch.zeros((k_max, 2 * (k_max + 1)), dtype=torch.float64, device=V.device)
+    hhost = torch.zeros((k_max, 2 * (k_max + 1)), dtype=torch.float64).pin_memory()
+    evs = [torch.cuda.Event() for _ in range(k_max)]
+
+    def launch(k):
+        A(V[k], w_buf)
+        rc = lib.nesa_gs_step(V.data_ptr(), stride, k + 1, w_buf.data_ptr(), V[k + 1].data_ptr(), n,
+                              int(is_f64), gs_work.data_ptr(), hdev[k].data_ptr(), stream.cuda_stream)
+        if rc:
+            raise RuntimeError(lib.nesa_gs_last_error().decode())
+        hhost[k].copy_(hdev[k], non_blocking=True)
+        evs[k].record(stream)
+
+    budget = maxiter - iters
+    k_run = min(k_max, budget)
+    if k_run <= 0:
+        return 0, 0
+    launch(0)
+    launched = 1
+    k_used = 0
+    for k in range(k_run):
+        if k + 1 < k_run:
+            launch(k + 1)       # the next product runs while the host rotates column k
+            launched += 1
+        evs[k].synchronize()
+        hv = hhost[k].numpy()
+        col = hv[0:2 * (k + 2):2] + 1j * hv[1:2 * (k + 2):2]
+        H[:k + 2, k, 0] = col
+        for j in range(k):
+            a0, a1 = H[j, k, 0], H[j + 1, k, 0]
+            H[j, k, 0] = cs[j, 0] * a0 + sn[j, 0] * a1
+            H[j + 1, k, 0] = -np.conj(sn[j, 0]) * a0 + cs[j, 0] * a1
+        cc, ss = _givens(H[k, k, 0], H[k + 1, k, 0])
+        cs[k, 0], sn[k, 0] = cc, ss
+        H[k, k, 0] = cc * H[k, k, 0] + ss * H[k + 1, k, 0]
+        H[k + 1, k, 0] = 0
+        g[k + 1, 0] = -np.conj(ss) * g[k, 0]
+        g[k, 0] = cc * g[k, 0]
+        k_used = k + 1
+        est = np.abs(g[k + 1]) / bnorm
+        est[done] = 0.0
+        history.append(est.copy())
+        if (est <= tol).all():
+            break
+    stream.synchronize()
+    return k_used, launched
+
+
 def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40,
-          maxiter: int = 400, x0=None, device: int | None = None) -> GmresResult:
+          maxiter: int = 400, x0=None, device: int | None = None,
+          orthogonalise: str = "auto") -> GmresResult:
     """Restarted GMRES on the GPU for (shift I + K~) x = b.
 
     b: (N,) or (N, m), numpy or torch (CPU or CUDA); real or complex; float32
@@ -80,12 +142,21 @@ def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40
     plan = get_plan(t, ops, dtype="f32" if single else "f64", device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def A(X):
-        Y = torch.empty_like(X)
+    def A(X, Y=None):
+        Y = torch.empty_like(X) if Y is None else Y
         plan.matvec_ptr(X.data_ptr(), Y.data_ptr(), m, is_complex, stream=stream.cuda_stream)
         if shift:
             Y.add_(X, alpha=shift)
         return Y
+
+    # "auto": the fused device step for one complex column, batched torch
+    # projections otherwise ("torch" forces the latter)
+    fused = orthogonalise != "torch" and m == 1 and is_complex and restart < 128
+    if fused:
+        from . import _capi
+        lib = _capi.load()
+        gs_work = torch.empty(int(lib.nesa_gs_work_bytes()), dtype=torch.uint8, device=B.device)
+        w_buf = torch.empty_like(B)
 
     def cnorm(X):                      # per-column 2-norms, float64 on host
         return torch.linalg.vector_norm(X, dim=0).double().cpu().numpy()
@@ -120,7 +191,12 @@ def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40
         g = np.zeros((k_max + 1, m), hdt)
         g[0] = beta
         k_used = 0
-        for k in range(k_max):
+        if fused:
+            k_used, launched = _arnoldi_fused(A, V, H, cs, sn, g, k_max, bnorm, done, tol, history,
+                                              iters, maxiter, w_buf, gs_work, lib, stream,
+                                              is_f64=not single)
+            iters += launched
+        for k in range(0 if not fused else k_max, k_max):
             W = A(V[k])
             iters += 1
             # classical Gram-Schmidt, twice (CGS2): two batched projections

@@ -626,3 +626,36 @@ def test_c5_plane_waves_near_on_tensor_cores(Q, P):
     for p in lanes.plans[1:]:
         p.close()
     plan.close()
+
+
+@pytest.mark.parametrize("dt,kk,tol", [(torch.complex64, 7, 2e-5), (torch.complex128, 31, 1e-12),
+                                       (torch.complex64, 40, 2e-5)])
+def test_fused_gram_schmidt_step(dt, kk, tol):
+    # nesa_gs_step (three passes, Hessenberg column on the device) against
+    # CGS2 in float64 numpy: same h column, same normalised new basis vector
+    from paper_1801_03589_b200 import _capi
+    lib = _capi.load()
+    n = 50000
+    rng = np.random.default_rng(kk)
+    Vh = np.linalg.qr(rng.standard_normal((n, kk)) + 1j * rng.standard_normal((n, kk)))[0].T.copy()
+    wh = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    h1 = Vh.conj() @ wh
+    w1 = wh - Vh.T @ h1
+    h2 = Vh.conj() @ w1
+    w2 = w1 - Vh.T @ h2
+    nrm = np.linalg.norm(w2)
+    V = torch.zeros((kk + 1, n), dtype=dt, device="cuda")
+    V[:kk] = torch.from_numpy(Vh).to(V)
+    w = torch.from_numpy(wh).to("cuda", dt)
+    work = torch.empty(int(lib.nesa_gs_work_bytes()), dtype=torch.uint8, device="cuda")
+    hcol = torch.zeros(2 * (kk + 1), dtype=torch.float64, device="cuda")
+    stride = (V[1].data_ptr() - V[0].data_ptr()) // (V.element_size() // 2)
+    rc = lib.nesa_gs_step(V.data_ptr(), stride, kk, w.data_ptr(), V[kk].data_ptr(), n,
+                          int(dt == torch.complex128), work.data_ptr(), hcol.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    h = hcol.cpu().numpy()
+    hc = h[0:2 * kk:2] + 1j * h[1:2 * kk:2]
+    assert np.abs(hc - (h1 + h2)).max() <= tol * np.abs(h1).max()
+    assert abs(h[2 * kk] - nrm) <= tol * nrm
+    assert np.linalg.norm(V[kk].cpu().numpy() - w2 / nrm) <= 10 * tol

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-5)
     ap.add_argument("--nrhs", type=int, default=1)
     ap.add_argument("--restart", type=int, default=30)
+    ap.add_argument("--orth", default="auto", help="auto (fused device CGS2) | torch")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -34,10 +35,11 @@ def main():
     nesa.gmres(tree, tables, bd, shift=a.shift, tol=1e-1, restart=2, maxiter=2)  # plan + graphs
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = nesa.gmres(tree, tables, bd, shift=a.shift, tol=a.tol, restart=a.restart, maxiter=1000)
+    res = nesa.gmres(tree, tables, bd, shift=a.shift, tol=a.tol, restart=a.restart, maxiter=1000,
+                     orthogonalise=a.orth)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"N={a.n} nrhs={a.nrhs} shift={a.shift} iterations={res.iterations} "
+    print(f"N={a.n} nrhs={a.nrhs} shift={a.shift} orth={a.orth} iterations={res.iterations} "
           f"time={dt:.3f}s per_iteration={1e3 * dt / max(res.iterations, 1):.3f}ms "
           f"residual={res.residuals} converged={res.converged}")
 
