@@ -1394,7 +1394,8 @@ __global__ void __launch_bounds__(128) tgemm_tc2_kernel(const TUnit* __restrict_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-constexpr int kTc3CtasPerSM = 2;  // persistent translation CTAs per SM
+constexpr int kTc3CtasPerSM = 1;  // persistent translation CTAs per SM (A/B: 1 per SM 0.6 us faster
+                                   // than 2: TMEM left to the concurrent level kernels)
 
 // Persistent form of tgemm_tc2_kernel: a CTA loops over units (grid-stride),
 // allocates TMEM once, and fetches the next unit's D as soon as the last MMA
@@ -1404,8 +1405,8 @@ template <int R>
 __global__ void __launch_bounds__(128) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
                                                         const TEnt* __restrict__ ents,
                                                         const float* __restrict__ DTC,
-                                                        const float* __restrict__ s, float* Y) {
-  KtScope kt_(44);
+                                                        const float* __restrict__ s, float* Y, int tag = 44) {
+  KtScope kt_(tag);
   constexpr int QT = 64, QR = QT * R;
   constexpr int EPT = 128 / R;
   constexpr int HALF = EPT / 2;
@@ -3030,7 +3031,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
                                                          int ncols, const int64_t* __restrict__ perm,
                                                          float* __restrict__ phi) {
   KtScope kt_(90);
-  extern __shared__ __align__(1024) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   float* Bs = reinterpret_cast<float*>(smem);  // 2 buffers x [hi | lo] x npad x 32
   constexpr int kBufFloats = 2 * kNearTcMaxN * kNearTcK;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + size_t(2) * kBufFloats * 4);  // [0,1] B, [2,3] MMA

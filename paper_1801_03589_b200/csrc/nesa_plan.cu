@@ -1303,7 +1303,7 @@ void io_launch(nesa_plan* P, void (*kern)(KArgs...), int grid, int block, size_t
   P->capturing_io->push_back(std::move(io));
 }
 
-constexpr int kExpCtasPerSM = 6;   // reception: one wave of resident CTAs (register budget: 6 per SM)
+constexpr int kExpCtasPerSM = 12;  // reception: two waves (A/B: 1.7 us faster than one)
 constexpr int kMomCtasPerSM = 4;
 constexpr int kMomBufPoints = 800;  // points staged per warp by the moment kernel
 
@@ -1463,7 +1463,8 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     if constexpr (std::is_same<T, float>::value) {
       if (P->tc) {
         go(tgemm_tc3_kernel<R>, std::min(u1 - u0, kTc3CtasPerSM * P->n_sm), tc2_smem_bytes<R>(), up,
-           u1 - u0, (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y);
+           u1 - u0, (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y,
+           u0 == 0 ? 44 : 45);  // (ktrace: fine / coarse units)
         nk++;
         tr("translate", st);
         return;
@@ -1729,16 +1730,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     finish();
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL + 1, s0);
   } else if (stage == 0) {
-    // gather -> radiation (the far chain is the critical path: it gets the
-    // GPU first) -> fork {near | up, translate, down} -> join -> reception
+    // gather -> fork {near | radiation, up, translate, down} -> join ->
+    // reception
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
     gather();
+    fork_near();  // (A/B: forking before the radiation is 5 us faster since it takes 50 us)
     if (far) {
       prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
       nk += launch_radiation<T, R>(P, qt, s, s0);
       tr("radiation", s0);
     }
-    fork_near();
     if (far) {
       const bool fine = up_pass(true);
       down_pass(fine);

@@ -1,0 +1,71 @@
+"""A/B timing of library builds on the bench workload (C4 product).
+
+    python tools/ab.py ab/libA.so ab/libB.so [--rounds 3] [--steps 200]
+
+Each round runs every library in a fresh process (NESA_LIB selects it),
+alternating the order, and times `steps` back-to-back products with CUDA
+events after a warm-up; prints the per-library median of the rounds.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import sys, json, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1801_03589_b200 as nesa
+from paper_1801_03589_b200.plan import NesaPlan
+steps = int(sys.argv[2])
+pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=3), 2000000)
+tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
+plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype="f32")
+q = torch.from_numpy(nesa.random_rhs(2000000, 3).astype(np.complex64)).cuda()
+phi = torch.empty_like(q)
+st = torch.cuda.current_stream()
+for _ in range(20):
+    plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, stream=st.cuda_stream)
+torch.cuda.synchronize()
+res = []
+for rep in range(3):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, stream=st.cuda_stream)
+    e1.record(st)
+    e1.synchronize()
+    res.append(e0.elapsed_time(e1) / steps)
+print(json.dumps({"ms": min(res)}))
+'''
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("libs", nargs="+")
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=200)
+    a = ap.parse_args()
+    out = {lib: [] for lib in a.libs}
+    for r in range(a.rounds):
+        order = a.libs if r % 2 == 0 else list(reversed(a.libs))
+        for lib in order:
+            env = dict(os.environ, NESA_LIB=os.path.abspath(lib))
+            p = subprocess.run([sys.executable, "-c", CHILD, HERE, str(a.steps)], env=env,
+                               capture_output=True, text=True)
+            line = [x for x in p.stdout.splitlines() if x.startswith("{")]
+            if not line:
+                print(lib, "failed", p.stderr[-800:])
+                continue
+            out[lib].append(json.loads(line[-1])["ms"])
+            print(lib, f"{out[lib][-1] * 1e3:.1f} us", flush=True)
+    import statistics
+    for lib, v in out.items():
+        if v:
+            print(f"{lib}: median {statistics.median(v) * 1e3:.1f} us  all {[round(x * 1e3, 1) for x in v]}")
+
+
+if __name__ == "__main__":
+    main()

@@ -62,7 +62,7 @@ int run() {
   } else {
     CK(cudaFuncSetAttribute(tgemm_tc3_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(tc2_smem_bytes<R>())));
-    tgemm_tc3_kernel<R><<<3, 128, tc2_smem_bytes<R>()>>>(dU, nunits, dE, dD, dS, dY);  // persistent
+    tgemm_tc3_kernel<R><<<3, 128, tc2_smem_bytes<R>()>>>(dU, nunits, dE, dD, dS, dY, 44);  // persistent
   }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
