@@ -146,3 +146,33 @@ def test_acceptance_criterion_1_q_sweep_gpu():
         assert by_q[10] <= 1e-3 and by_q[14] <= 1e-4, by_q
         assert all(b <= 2.0 * a for a, b in zip(errs, errs[1:])), by_q
         _drop_plans(tree)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,P,Q,seed", [(2_000_000, 64, 64, 3), (200_000, 48, 48, 2)])
+def test_inter_cta_protocols_stress(n, P, Q, seed):
+    # The fused up / down kernels synchronise CTAs through last-arriver
+    # counters, owner chains with start-order tickets and release / acquire
+    # flags, reset by the kernels themselves for the next launch.
+    # compute-sanitizer is closed on this GPU pool (profiles/r2_sanitizer.txt),
+    # so the protocols are checked by replaying the product graph many times
+    # back to back (every replay reuses the counters the previous one reset)
+    # and requiring every result to be bitwise the first one, which matched
+    # the oracle in the parity tests above.
+    from paper_1801_03589_b200.plan import NesaPlan
+    from paper_1801_03589_b200.operators import build_tables
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=seed), n)
+    tree = build_tree(pts, TreeParams(P=P))
+    plan = NesaPlan(tree, build_tables(tree, NesaParams(Q=Q)), dtype="f32")
+    q = torch.from_numpy(geo.random_rhs(n, seed).astype(np.complex64)).cuda()
+    first = torch.empty_like(q)
+    plan.matvec_ptr(q.data_ptr(), first.data_ptr(), 1, True)
+    outs = [torch.empty_like(q) for _ in range(4)]
+    mismatches = 0
+    for rep in range(100):
+        for o in outs:
+            plan.matvec_ptr(q.data_ptr(), o.data_ptr(), 1, True)
+        torch.cuda.synchronize()
+        mismatches += sum(int(not torch.equal(o, first)) for o in outs)
+    plan.close()
+    assert mismatches == 0, f"{mismatches} of 400 replays differ from the first product"
