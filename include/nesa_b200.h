@@ -86,7 +86,7 @@ typedef struct nesa_plan_desc {
   const int64_t* group_start;   /* [G] point range in tree order           */
   const int64_t* group_stop;    /* [G]                                     */
   const int64_t* parent;        /* [G] parent id, -1 at level l0           */
-  const int32_t* quad;          /* [G] 2*(ix&1)+(iy&1)                     */
+  const int32_t* quad;          /* [G] 2*(ix&1)+(iy&1); octant with NESA_PLAN_OCTREE */
   const int64_t* level_first;   /* [L-l0+1] first id of level l0+i         */
   const int64_t* level_count;   /* [L-l0+1]                                */
   const int64_t* nbr_ptr;       /* [n_leaves+1] Group.neighbors CSR        */
@@ -96,7 +96,8 @@ typedef struct nesa_plan_desc {
   const int64_t* int_dtab;      /* [nnz] index of the entry's D matrix     */
 
   /* shared operator tables, float64 row-major (y = M x) */
-  const double* C;              /* [(L-l0) * 4 * Q * Q] child level l -> row l-l0-1 */
+  const double* C;              /* [(L-l0) * 4 * Q * Q] child level l -> row l-l0-1
+                                   (8 matrices per level with NESA_PLAN_OCTREE)    */
   const double* B;              /* same layout                                      */
   const double* D;              /* [n_dtab * Q * Q]                                 */
   int64_t n_dtab;
@@ -134,6 +135,14 @@ typedef struct nesa_plan_desc {
 /* nesa_plan_desc.options */
 #define NESA_PLAN_FAR_ONLY 1u   /* no near operator: far-field products only (extra
                                    plans that share the columns of a many-RHS product) */
+#define NESA_PLAN_OCTREE 2u     /* Track B: an octree (quad[] holds the child octant
+                                   4(ix&1) + 2(iy&1) + (iz&1), C / B tables have 8 matrices
+                                   per level), operators from the host (near / V / U blobs
+                                   required).  Complex operators are passed in their real
+                                   embedding: every complex entry a+ib becomes the 2x2 block
+                                   [[a, -b], [b, a]], so N, Q and the group point ranges are
+                                   doubled and a complex vector is a real one of 2N entries
+                                   (paper_1801_03589_b200.plan3). */
 
 int nesa_plan_create(const nesa_plan_desc* desc, int device, nesa_plan** out);
 

@@ -593,8 +593,8 @@ struct LevelArgs {
 template <typename T>
 struct FusedArgs {
   const T* MT;            // C (up) / B (down) tables, padded + transposed
-  size_t mstride;         // elements per matrix; level ci = lv - l0 >= 1: ((ci-1)*4 + quad)
-  const int32_t* quad;    // [G]
+  size_t mstride;         // elements per matrix; level ci = lv - l0 >= 1: ((ci-1)*nkind + quad)
+  const int32_t* quad;    // [G] child kind: quadrant (quadtree) or octant (octree)
   const int64_t* parent;  // [G]
   const int2* uchild;     // [G] local children (first id, count)
   const int32_t* anc;     // down: [count][D] ancestors of the level-lf groups (level lf-1 first)
@@ -607,6 +607,7 @@ struct FusedArgs {
   T* o;
   int64_t first, count;   // level-lf groups (local)
   int lf, l0, L, Q, D;
+  int nkind;              // child kinds per level: 4 (quadtree) or 8 (octree)
 };
 
 __device__ __forceinline__ int ld_acquire_s32(const int* p) {
@@ -643,7 +644,7 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
   int lv = a.lf;
   auto load_mat = [&](int lvx, int64_t gx) {
     mbar_arrive_expect_tx(bar, uint32_t(mb));
-    bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * 4 + a.quad[gx]) * a.mstride, uint32_t(mb), bar);
+    bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * a.nkind + a.quad[gx]) * a.mstride, uint32_t(mb), bar);
   };
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
         a.cnt[p] = 0;         // (visible to the next launch at the kernel boundary)
         if (lv - 1 > a.l0) {
           mbar_arrive_expect_tx(bar, uint32_t(mb));
-          bulk_g2s(M, a.MT + (size_t(lv - 1 - a.l0 - 1) * 4 + p_quad) * a.mstride, uint32_t(mb), bar);
+          bulk_g2s(M, a.MT + (size_t(lv - 1 - a.l0 - 1) * a.nkind + p_quad) * a.mstride, uint32_t(mb), bar);
         }
       }
       *nxt = last ? p : -1;
@@ -748,7 +749,7 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
     const int64_t px = a.parent[x];
     if (tid == 0) {
       mbar_arrive_expect_tx(bar, uint32_t(mb));
-      bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * 4 + a.quad[x]) * a.mstride, uint32_t(mb), bar);
+      bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * a.nkind + a.quad[x]) * a.mstride, uint32_t(mb), bar);
     }
     if (i == own - 1 && lvx - 1 > a.l0) {
       // the parent of the top owned group belongs to another CTA

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <utility>
 #include <map>
 #include <string>
@@ -332,6 +333,7 @@ struct nesa_plan {
   int64_t N = 0, NL = 0, G = 0;
   int64_t leaf_begin = 0, leaf_end = 0;  // local target leaves
   bool far_only = false;                 // NESA_PLAN_FAR_ONLY: no near operator at all
+  int nkind = 4;                         // child kinds per level (NESA_PLAN_OCTREE: 8)
   int64_t pt_begin = 0, pt_end = 0;      // local tree-order point range
   int n_sm = 148;
 
@@ -623,8 +625,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   const int64_t nlt = P->L - P->l0;
   P->mbytes = mat_bytes(Q, sizeof(T));
   if (nlt > 0) {
-    upload_table_T<T>(P->CT, d->C, nlt * 4, Q);
-    upload_table_T<T>(P->BT, d->B, nlt * 4, Q);
+    upload_table_T<T>(P->CT, d->C, nlt * P->nkind, Q);
+    upload_table_T<T>(P->BT, d->B, nlt * P->nkind, Q);
   }
   P->n_dtab = d->n_dtab;
   upload_table_T<T>(P->DT, d->D, d->n_dtab, Q);
@@ -686,7 +688,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         cnt[i]++;
       }
       for (int64_t i = 0; i < cn; ++i) {
-        require(cnt[i] <= 4, "more than four children");
+        require(cnt[i] <= P->nkind, "more children than child kinds");
         och[i] = int2{int(std::max<int64_t>(first[i], 0)), int(cnt[i])};
       }
     }
@@ -1527,6 +1529,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     fa.MT = MT;
     fa.mstride = mstride;
     fa.quad = P->quad.p;
+    fa.nkind = P->nkind;
     fa.parent = P->parent.p;
     fa.uchild = P->uchild.p;
     fa.anc = P->fused_anc.p;
@@ -2026,6 +2029,19 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
     P->far_only = (d->options & NESA_PLAN_FAR_ONLY) != 0;
+    if (d->options & NESA_PLAN_OCTREE) {
+      // Track B: octree (8 child kinds), operators from the host.  The
+      // quadtree-specialised kernels (tensor-core levels / translation,
+      // warp-tiled wide levels, circle expansions) do not apply: every level
+      // runs in the fused kernels, translation in the generic GEMM.
+      P->nkind = 8;
+      P->tc = false;
+      P->wide_level = std::numeric_limits<int64_t>::max();
+      require(d->V_blob && d->U_blob && (d->near_blob || P->far_only),
+              "octree plans take their near / V / U blocks from the host");
+    }
+    for (int64_t g = 0; g < d->n_groups; ++g)
+      require(d->quad[g] >= 0 && d->quad[g] < P->nkind, "child kind out of range");
     if (P->leaf_end <= P->leaf_begin) {
       P->leaf_begin = 0;
       P->leaf_end = P->NL;

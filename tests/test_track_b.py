@@ -1,0 +1,248 @@
+"""Track B: 3D octree, Helmholtz kernel, complex operators.
+
+The reference is 2D / log-kernel only, so this track's parity is pinned
+against restatements: the vectorised octree against oracle/octree_ref.py
+(the reference's quadtree.py:123-245 loop for loop in 3D, bit-exact), the
+GPU product against the dtype-generic serial oracle (fastmvp.py:142-172) on
+the same complex operators (c128 <= 1e-12, c64 <= 1e-5), and the operators
+against the O(N^2) Helmholtz sum at low frequency (convergence in Q).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle.mvp_oracle import mvp_serial as oracle_mvp, rel_l2
+from oracle.octree_ref import build_octree_ref
+from paper_1801_03589_b200 import helmholtz as hz
+from paper_1801_03589_b200.octree import build_octree, morton3
+from paper_1801_03589_b200.plan3 import embed
+from paper_1801_03589_b200.quadtree import TreeParams
+
+
+def _cloud(n, seed, stretch=1.0):
+    v = np.random.default_rng(seed).standard_normal((n, 3))
+    v /= np.linalg.norm(v, axis=1)[:, None]
+    v[:, 0] *= stretch
+    return v
+
+
+@pytest.mark.parametrize("n,P,seed,stretch", [(2000, 32, 0, 1.0), (5000, 16, 1, 1.0),
+                                              (3000, 8, 2, 5.0), (64, 1, 3, 1.0)])
+def test_octree_bit_exact_vs_loop_restatement(n, P, seed, stretch):
+    pts = _cloud(n, seed, stretch)
+    t = build_octree(pts, TreeParams(P=P))
+    l0, L, perm, groups, lids = build_octree_ref(pts, P)
+    a = t.arrays
+    assert (t.l0, t.L) == (l0, L)
+    assert np.array_equal(t.perm, perm)
+    assert a.n_groups == len(groups)
+    for g in groups:
+        assert (g.ix, g.iy, g.iz) == tuple(a.ijk[g.id].tolist())
+        assert (g.start, g.stop) == (a.start[g.id], a.stop[g.id])
+        assert (-1 if g.parent is None else g.parent) == a.parent[g.id]
+        assert g.interaction == a.int_idx[a.int_ptr[g.id]:a.int_ptr[g.id + 1]].tolist()
+        if g.level == L:
+            assert g.neighbors == a.nbr_idx[a.nbr_ptr[g.id]:a.nbr_ptr[g.id + 1]].tolist()
+        kids = list(range(a.child_first[g.id], a.child_first[g.id] + a.n_children[g.id]))
+        assert g.children == (kids if a.n_children[g.id] else [])
+
+
+def test_octree_errors_and_morton():
+    assert morton3(np.array([1]), np.array([0]), np.array([0]))[0] == 1
+    assert morton3(np.array([0]), np.array([1]), np.array([0]))[0] == 2
+    assert morton3(np.array([0]), np.array([0]), np.array([1]))[0] == 4
+    assert morton3(np.array([3]), np.array([3]), np.array([3]))[0] == 63
+    with pytest.raises(ValueError):
+        build_octree(np.zeros((10, 3)), TreeParams(P=2))           # coincident
+    with pytest.raises(ValueError):
+        build_octree(np.random.rand(10, 2), TreeParams(P=2))       # not 3D
+    with pytest.raises(ValueError):
+        build_octree(np.random.rand(3, 3), TreeParams(P=1))        # too few points
+
+
+def test_params_validation():
+    hz.HelmholtzParams(Q=24, k=3.0)
+    with pytest.raises(ValueError):
+        hz.HelmholtzParams(Q=2)
+    with pytest.raises(ValueError):
+        hz.HelmholtzParams(rho_out_aux=1.6)                         # inside the box corner
+    with pytest.raises(ValueError):
+        hz.HelmholtzParams(rho_out_check=2.5)                       # breaks 4h separation
+    with pytest.raises(ValueError):
+        hz.HelmholtzParams(k=-1.0)
+
+
+def test_geometry_generators():
+    s = hz.generate_surface("sphere", 1000, 0)
+    assert np.allclose(np.linalg.norm(s, axis=1), 1.0)
+    e = hz.generate_surface("ellipsoid-plates", 20000, 2)
+    assert np.array_equal(e, hz.generate_surface("ellipsoid-plates", 20000, 2))
+    on_plate = np.isclose(np.abs(e[:, 2]), hz.PLATE_Z)
+    frac = on_plate.mean()
+    want = 2 * 4.0 / hz.surface_area("ellipsoid-plates")
+    assert abs(frac - want) < 0.01
+    ell = e[~on_plate]
+    r = (ell[:, 0] / 5.0) ** 2 + (ell[:, 1] / 0.5) ** 2 + (ell[:, 2] / 0.5) ** 2
+    assert np.allclose(r, 1.0)
+    # area-uniform: the share of ellipsoid points with |x| < 2.5 matches the
+    # surface-of-revolution integral dA = 2 pi y sqrt(1 + y'^2) dx
+    x = np.linspace(-5.0, 5.0, 400001)[1:-1]
+    y = 0.5 * np.sqrt(1.0 - (x / 5.0) ** 2)
+    dy = -0.5 * (x / 25.0) / np.sqrt(1.0 - (x / 5.0) ** 2)
+    dA = 2 * math.pi * y * np.sqrt(1.0 + dy * dy)
+    want_mid = dA[np.abs(x) < 2.5].sum() / dA.sum()
+    assert abs((np.abs(ell[:, 0]) < 2.5).mean() - want_mid) < 0.01
+    k = hz.wavenumber3("sphere", 2000)
+    assert abs(2 * math.pi / k - 10 * math.sqrt(4 * math.pi / 2000)) < 1e-12
+
+
+def test_embedding():
+    rng = np.random.default_rng(0)
+    M = rng.standard_normal((5, 7)) + 1j * rng.standard_normal((5, 7))
+    x = rng.standard_normal(7) + 1j * rng.standard_normal(7)
+    y = embed(M) @ x.view(np.float64)
+    assert np.allclose(y.view(np.complex128), M @ x, rtol=0, atol=1e-13)
+
+
+def test_operators_shared_and_translation_invariant():
+    pts = hz.generate_surface("sphere", 3000, 5)
+    tree = build_octree(pts, TreeParams(P=8))
+    p = hz.HelmholtzParams(Q=16, k=2.0)
+    ops = hz.build_all3(tree, p)
+    a = tree.arrays
+    assert tree.L > tree.l0
+    # C / B shared per (level, octant), D per (level, offset)
+    seen = {}
+    for g, C in ops.C.items():
+        key = (int(a.level[g]), int(a.octant()[g]))
+        assert seen.setdefault(key, C) is C
+    dseen = {}
+    for (g, b), D in ops.D.items():
+        key = (int(a.level[g]),) + tuple((a.ijk[b] - a.ijk[g]).tolist())
+        assert dseen.setdefault(key, D) is D
+    # near blocks: the transposed partner is shared and G is symmetric
+    for (g, b), K in list(ops.near.items())[:50]:
+        assert np.array_equal(ops.near[(b, g)], K.T)
+    # operator counts match the lists (task_counts, fastmvp.py:175-187)
+    assert len(ops.near) == int(a.nbr_ptr[-1])
+    assert len(ops.D) == int(a.int_ptr[-1])
+
+
+def test_oracle_converges_to_dense_at_low_frequency():
+    pts = hz.generate_surface("sphere", 2500, 1)
+    tree = build_octree(pts, TreeParams(P=8))
+    rng = np.random.default_rng(1)
+    q = rng.standard_normal(2500) + 1j * rng.standard_normal(2500)
+    k = 1.5
+    ref = hz.dense_helmholtz(pts, q, k)
+    errs = [rel_l2(oracle_mvp(tree, hz.build_all3(tree, hz.HelmholtzParams(Q=Qa, k=k)), q), ref)
+            for Qa in (16, 32, 64)]
+    assert errs[2] < errs[1] < errs[0], errs
+    assert errs[2] < 2e-3, errs
+
+
+def test_oracle_near_only_is_exact():
+    pts = hz.generate_surface("sphere", 1500, 2)
+    tree = build_octree(pts, TreeParams(P=16))
+    p = hz.HelmholtzParams(Q=12, k=4.0)
+    ops = hz.build_all3(tree, p)
+    q = np.random.default_rng(2).standard_normal(1500) + 0j
+    near = oracle_mvp(tree, ops, q, far=False)
+    # dense near-field restriction
+    a = tree.arrays
+    ref = np.zeros(1500, np.complex128)
+    inv = tree.inverse_perm()
+    qt = q[tree.perm]
+    for g in range(a.level_count[tree.L]):
+        s0, s1 = a.start[g], a.stop[g]
+        for b in a.nbr_idx[a.nbr_ptr[g]:a.nbr_ptr[g + 1]]:
+            ref[s0:s1] += hz.near_block3(tree, g, int(b), p.k) @ qt[a.start[b]:a.stop[b]]
+    assert rel_l2(near, ref[inv]) < 1e-14
+
+
+# ---------------------------------------------------------------------------
+# GPU: the product through the C ABI against the oracle
+# ---------------------------------------------------------------------------
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+TRACK_B = {
+    # BASELINE configs[0..2] in 3D: (surface, N, seed, leaf P, Q)
+    "C1": ("sphere", 2000, 0, 32, 24),
+    "C2": ("sphere", 20000, 1, 32, 32),
+    "C3": ("ellipsoid-plates", 200000, 2, 48, 48),
+}
+
+
+def _case(name):
+    kind, n, seed, P, Q = TRACK_B[name]
+    return hz.track_b_problem(kind, n, seed, P, Q)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_track_b_gpu_vs_oracle(name):
+    _gpu()
+    from paper_1801_03589_b200.plan3 import HelmholtzPlan
+    pts, tree, params, q = _case(name)
+    tables = hz.build_tables3(tree, params)
+    ops = hz.build_all3(tree, params, tables)
+    ref = oracle_mvp(tree, ops, q)
+    ref_near = oracle_mvp(tree, ops, q, far=False)
+    for src in (tables, ops):
+        p128 = HelmholtzPlan(tree, src, "c128")
+        assert rel_l2(p128.matvec(q), ref) <= 1e-12
+        assert rel_l2(p128.matvec(q, far=False), ref_near) <= 1e-13
+        p128.close()
+        p64 = HelmholtzPlan(tree, src, "c64")
+        out = p64.matvec(q.astype(np.complex64))
+        assert out.dtype == np.complex64
+        assert rel_l2(out, ref) <= 1e-5
+        p64.close()
+
+
+@pytest.mark.gpu
+def test_track_b_gpu_multi_rhs_and_linearity():
+    torch = _gpu()
+    from paper_1801_03589_b200.plan3 import HelmholtzPlan
+    pts, tree, params, q = _case("C1")
+    ops = hz.build_all3(tree, params)
+    rng = np.random.default_rng(9)
+    Qm = rng.standard_normal((2000, 3)) + 1j * rng.standard_normal((2000, 3))
+    plan = HelmholtzPlan(tree, ops, "c128")
+    out = plan.matvec(Qm)
+    for j in range(3):
+        assert rel_l2(out[:, j], oracle_mvp(tree, ops, Qm[:, j])) <= 1e-12
+    # device tensors in, device tensors out; linear; bitwise rerun
+    qd = torch.from_numpy(q).cuda()
+    a = plan.matvec(qd)
+    b = plan.matvec(2.0 * qd)
+    assert torch.equal(plan.matvec(qd), a)
+    assert torch.allclose(b, 2.0 * a, rtol=1e-13, atol=0)
+    with pytest.raises(ValueError):
+        plan.matvec(q[:-1])
+    plan.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_track_b_c3_gpu_vs_oracle():
+    _gpu()
+    from paper_1801_03589_b200.plan3 import HelmholtzPlan
+    pts, tree, params, q = _case("C3")
+    tables = hz.build_tables3(tree, params)
+    ops = hz.build_all3(tree, params, tables)
+    ref = oracle_mvp(tree, ops, q)
+    del ops
+    for dt, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        plan = HelmholtzPlan(tree, tables, dt)
+        qq = q if dt == "c128" else q.astype(np.complex64)
+        err = rel_l2(plan.matvec(qq), ref)
+        plan.close()
+        assert err <= tol, (dt, err)
