@@ -143,6 +143,12 @@ typedef struct nesa_plan_desc {
                                    [[a, -b], [b, a]], so N, Q and the group point ranges are
                                    doubled and a complex vector is a real one of 2N entries
                                    (paper_1801_03589_b200.plan3). */
+#define NESA_PLAN_COMPLEX_NEAR 4u /* with NESA_PLAN_OCTREE: near_blob holds each leaf's complex
+                                   slab row-split (2 n_a x W_a real, column-major: row 2r = Re,
+                                   row 2r+1 = Im of complex row r; W_a complex columns), read
+                                   once per product with complex vectors -- 8 bytes per complex
+                                   float32 entry instead of the embedding's 16.  Products run
+                                   one complex right-hand side per pass. */
 
 int nesa_plan_create(const nesa_plan_desc* desc, int device, nesa_plan** out);
 

@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("NESA_LIB") or os.path.join(_HERE, "libnesa_b200.so") 
 NESA_ABI_VERSION = 2
 NESA_PLAN_FAR_ONLY = 1
 NESA_PLAN_OCTREE = 2
+NESA_PLAN_COMPLEX_NEAR = 4
 NESA_OK = 0
 NESA_ERR_INVALID = 1
 NESA_ERR_CUDA = 2

@@ -140,7 +140,10 @@ constexpr int kNearNCW = 4;
 constexpr int kNearABytes = 24 * 1024;
 constexpr int kNearStages = 2;
 
-enum { kModeStore = 0, kModeScatter = 1 };
+// kModeStoreCplx: store mode for a complex operator held row-split (rows
+// 2r / 2r+1 = Re / Im of operator row r, R = 2: one complex column), the
+// epilogue combines each row pair into y_r = (Re K) x + i (Im K) x
+enum { kModeStore = 0, kModeScatter = 1, kModeStoreCplx = 2 };
 
 template <typename T>
 struct BlockGemvArgs {
@@ -359,7 +362,25 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
             for (int rr = 0; rr < R; ++rr) sRed[(cl * ld + 4 * rq + q) * R + rr] = acc[q][rr];
         }
         named_bar_sync(1, kNCT);
-        for (int row = tid; row < m; row += kNCT) {
+        if constexpr (MODE == kModeStoreCplx) {
+          // rows 2cr, 2cr+1 of the item hold (Re K_cr) x and (Im K_cr) x,
+          // each a complex value: y_cr = first + i * second
+          static_assert(R == 2, "complex near: one complex column");
+          for (int cr = tid; cr < (m >> 1); cr += kNCT) {
+            T u0 = sRed[(2 * cr) * 2], u1 = sRed[(2 * cr) * 2 + 1];
+            T w0 = sRed[(2 * cr + 1) * 2], w1 = sRed[(2 * cr + 1) * 2 + 1];
+            for (int l = 1; l < CL; ++l) {
+              u0 += sRed[(l * ld + 2 * cr) * 2];
+              u1 += sRed[(l * ld + 2 * cr) * 2 + 1];
+              w0 += sRed[(l * ld + 2 * cr + 1) * 2];
+              w1 += sRed[(l * ld + 2 * cr + 1) * 2 + 1];
+            }
+            const int64_t o = (int64_t(h.y_row0) + cr) * 2;
+            a.y[o] = u0 - w1;
+            a.y[o + 1] = u1 + w0;
+          }
+        }
+        for (int row = tid; MODE != kModeStoreCplx && row < m; row += kNCT) {
           T v[R];
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) v[rr] = sRed[row * R + rr];
@@ -367,7 +388,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) v[rr] += sRed[(l * ld + row) * R + rr];
           }
-          if constexpr (MODE == kModeStore) {
+          if constexpr (MODE == kModeStore || MODE == kModeStoreCplx) {
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) a.y[int64_t(h.y_row0 + row) * R + rr] = v[rr];
           } else {

@@ -333,6 +333,7 @@ struct nesa_plan {
   int64_t N = 0, NL = 0, G = 0;
   int64_t leaf_begin = 0, leaf_end = 0;  // local target leaves
   bool far_only = false;                 // NESA_PLAN_FAR_ONLY: no near operator at all
+  bool cnear = false;                    // NESA_PLAN_COMPLEX_NEAR: row-split complex near blob
   int nkind = 4;                         // child kinds per level (NESA_PLAN_OCTREE: 8)
   int64_t pt_begin = 0, pt_end = 0;      // local tree-order point range
   int n_sm = 148;
@@ -619,8 +620,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     }
   }
 
-  // the many-RHS near field on the tensor cores works for any Q
-  P->near_tc = std::is_same<T, float>::value && P->tc;
+  // the many-RHS near field on the tensor cores works for any Q (real operators)
+  P->near_tc = std::is_same<T, float>::value && P->tc && !P->cnear;
   // ---- tables
   const int64_t nlt = P->L - P->l0;
   P->mbytes = mat_bytes(Q, sizeof(T));
@@ -811,11 +812,14 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     for (int64_t a = 0; a < NL; ++a) {
       const int64_t na = d->group_stop[a] - d->group_start[a];
       require(na >= 1, "empty leaf");
+      // complex near (NESA_PLAN_COMPLEX_NEAR): slab columns and x rows
+      // count complex points (half the embedded ones); rows stay re / im
+      const int64_t cdiv = P->cnear ? 2 : 1;
       int64_t W = 0;
       for (int64_t e = d->nbr_ptr[a]; e < d->nbr_ptr[a + 1]; ++e) {
         const int64_t b = d->nbr_idx[e];
         require(b >= 0 && b < NL, "neighbor id out of range");
-        W += d->group_stop[b] - d->group_start[b];
+        W += (d->group_stop[b] - d->group_start[b]) / cdiv;
       }
       require(W < (int64_t(1) << 31), "near slab too wide");
       if (a >= lb && a < le && !P->far_only) {
@@ -824,7 +828,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         int32_t col = 0;
         for (int64_t e = d->nbr_ptr[a]; e < d->nbr_ptr[a + 1]; ++e) {
           const int64_t b = d->nbr_idx[e];
-          const int64_t bs = d->group_start[b], bn = d->group_stop[b] - bs;
+          const int64_t bs = d->group_start[b] / cdiv, bn = (d->group_stop[b] - d->group_start[b]) / cdiv;
           if (int32_t(hn.segs.size()) > seg_begin) {
             BlockSeg& last = hn.segs.back();
             if (int64_t(last.x_row0) + (col - last.col0) == bs) {
@@ -840,7 +844,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           const int32_t m = int32_t(std::min<int64_t>(kMaxRows, na - r0));
           const int32_t ld = (m + 3) / 4 * 4;
           hn.items.push_back(BlockItem{hn.blob_elems, m, int32_t(W), ld,
-                                       int32_t(d->group_start[a] + r0), seg_begin, seg_count, 0, 0});
+                                       int32_t((d->group_start[a] + r0) / cdiv), seg_begin, seg_count, 0, 0});
           near_src_off.push_back(near_off);
           near_src_rows.push_back(int32_t(na));
           near_row0.push_back(int32_t(r0));
@@ -1203,6 +1207,17 @@ void launch_near(const DevBlockSet& bs, const T* x, T* y, cudaStream_t st) {
          st>>>(blockgemv_args<T, R, kModeStore>(bs, x, y, nullptr, nullptr, 0));
 }
 
+// complex near field (NESA_PLAN_COMPLEX_NEAR): the same engine on the
+// row-split complex blob, x / y read as complex (R = 2) values
+template <typename T>
+void launch_near_cplx(const DevBlockSet& bs, const T* x, T* y, cudaStream_t st) {
+  if (bs.n_items == 0) return;
+  blockgemv_kernel<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>
+      <<<bs.grid, kNearNCW * 32 + 32,
+         blockgemv_smem_bytes<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>(), st>>>(
+          blockgemv_args<T, 2, kModeStoreCplx>(bs, x, y, nullptr, nullptr, 0));
+}
+
 template <typename T, int R>
 void set_smem_attrs() {
   static bool done = false;
@@ -1213,6 +1228,9 @@ void set_smem_attrs() {
   attr(blockgemv_kernel<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>,
        int(blockgemv_smem_bytes<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>()));
   attr(blockgemv_kernel<T, R, kModeStore>, int(blockgemv_smem_bytes<T, R, kModeStore>()));
+  if constexpr (R == 1)
+    attr(blockgemv_kernel<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>,
+         int(blockgemv_smem_bytes<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>()));
   attr(blockgemv_kernel<T, R, kModeScatter>, int(blockgemv_smem_bytes<T, R, kModeScatter>()));
   const int lim = 220 * 1024;
   attr(tgemm_kernel<T, R>, lim);
@@ -1687,7 +1705,12 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     CUDA_OK(cudaStreamWaitEvent(s1, P->ev_fork, 0));
     if (!near) return;
     prof_mark(P, profn, 2 * NESA_STAGE_NEAR, s1);
-    launch_near<T, R>(P->nearset, qt, phin, s1);
+    if (P->cnear) {
+      // complex operator row-split: one complex column (R = 1 embedded)
+      if constexpr (R == 1) launch_near_cplx<T>(P->nearset, qt, phin, s1);
+    } else {
+      launch_near<T, R>(P->nearset, qt, phin, s1);
+    }
     nk++;
     prof_mark(P, profn, 2 * NESA_STAGE_NEAR + 1, s1);
     tr("near", s1);
@@ -1825,6 +1848,14 @@ int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_
   require(q != nullptr && phi != nullptr, "null vector");
   require(stage == 0 || !(flags & NESA_PROFILE), "profiling needs a full product");
   const int Rt = nrhs * (is_complex ? 2 : 1);
+  if (P->cnear) {
+    // complex near field: one (embedded) column per block
+    require(!is_complex, "an embedded complex plan takes real (embedded) vectors");
+    for (int c = 0; c < Rt; ++c)
+      run_block(P, static_cast<const char*>(q) + c * P->esz, static_cast<char*>(phi) + c * P->esz, 1, Rt,
+                flags, stream, stage);
+    return NESA_OK;
+  }
   if (Rt == 1 || Rt == 2 || Rt == 4) return run_block(P, q, phi, Rt, Rt, flags, stream, stage);
   require(stage == 0, "the staged (multi-GPU) product takes at most 4 real columns");
   require(!(flags & NESA_PROFILE), "profiling takes at most 4 real columns");
@@ -2039,6 +2070,13 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
       P->wide_level = std::numeric_limits<int64_t>::max();
       require(d->V_blob && d->U_blob && (d->near_blob || P->far_only),
               "octree plans take their near / V / U blocks from the host");
+    }
+    P->cnear = (d->options & NESA_PLAN_COMPLEX_NEAR) != 0;
+    if (P->cnear) {
+      require(d->near_blob && !P->far_only, "NESA_PLAN_COMPLEX_NEAR needs a near blob");
+      for (int64_t g = 0; g < d->n_leaves; ++g)
+        require(d->group_start[g] % 2 == 0 && d->group_stop[g] % 2 == 0,
+                "NESA_PLAN_COMPLEX_NEAR needs embedded (even) point ranges");
     }
     for (int64_t g = 0; g < d->n_groups; ++g)
       require(d->quad[g] >= 0 && d->quad[g] < P->nkind, "child kind out of range");

@@ -6,10 +6,14 @@ real embedding: every entry a + ib becomes the 2 x 2 block [[a, -b], [b, a]]
 acting on the (re, im) pair of one complex unknown.  Laid out that way a
 complex vector of N entries is, byte for byte, a real vector of 2N entries,
 so the plan sees a "tree" whose point ranges, Q and N are doubled and runs
-the product with one real column -- the near field, the radiation /
-reception blocks and the C / D / B transfers all do complex arithmetic
-(4 real multiply-adds per complex one, exactly the complex flop count) with
-no new kernel.  NESA_PLAN_OCTREE tells the plan that the tree has 8 child
+the product with one real column -- the radiation / reception blocks and
+the C / D / B transfers all do complex arithmetic (4 real multiply-adds per
+complex one, exactly the complex flop count) with no new kernel.  The near
+field, which streams the dominant operator bytes, does not pay the
+embedding's 2x storage: its blob is row-split (rows Re / Im of each complex
+row, NESA_PLAN_COMPLEX_NEAR) and the near kernel's complex-store epilogue
+(kModeStoreCplx) combines each row pair, so it reads 8 bytes per complex
+float32 entry.  NESA_PLAN_OCTREE tells the plan that the tree has 8 child
 kinds (octants) per level and that its operators come from the host.
 
 Reference anchor: the product is fastmvp.py:142-172 on the operators of
@@ -38,6 +42,15 @@ def embed(M: np.ndarray) -> np.ndarray:
     R[..., 0::2, 1::2] = -M.imag
     R[..., 1::2, 0::2] = M.imag
     R[..., 1::2, 1::2] = M.real
+    return R
+
+
+def row_split(M: np.ndarray) -> np.ndarray:
+    """Complex (m, n) -> real (2m, n): row 2r = Re M[r], row 2r+1 = Im M[r]."""
+    M = np.asarray(M)
+    R = np.empty((2 * M.shape[0], M.shape[1]), np.float64)
+    R[0::2] = M.real
+    R[1::2] = M.imag
     return R
 
 
@@ -75,7 +88,8 @@ class HelmholtzPlan(NesaPlan):
     dtype: "c128" (float64 engine) or "c64" (float32 engine).
     """
 
-    def __init__(self, tree: Octree, ops, dtype: str = "c128", device: int = 0):
+    def __init__(self, tree: Octree, ops, dtype: str = "c128", device: int = 0,
+                 complex_near: bool = True):
         self.lib = _capi.load()
         dt = {"c128": "f64", "complex128": "f64", "f64": "f64",
               "c64": "f32", "complex64": "f32", "f32": "f32"}.get(dtype)
@@ -108,7 +122,7 @@ class HelmholtzPlan(NesaPlan):
         for g in range(nl):
             nb = a.nbr_idx[a.nbr_ptr[g]:a.nbr_ptr[g + 1]].tolist()
             slab = np.hstack([near_of(g, b) for b in nb])
-            near.append(embed(slab).ravel(order="F"))
+            near.append((row_split(slab) if complex_near else embed(slab)).ravel(order="F"))
             Vb.append(embed(V[g]).ravel(order="F"))
             Ub.append(embed(U[g]).ravel(order="F"))
         keep = {}
@@ -147,7 +161,8 @@ class HelmholtzPlan(NesaPlan):
         d.near_blob = _ptr(arr("near", np.concatenate(near), np.float64), f64)
         d.V_blob = _ptr(arr("V", np.concatenate(Vb), np.float64), f64)
         d.U_blob = _ptr(arr("U", np.concatenate(Ub), np.float64), f64)
-        d.options = _capi.NESA_PLAN_OCTREE
+        d.options = _capi.NESA_PLAN_OCTREE | (_capi.NESA_PLAN_COMPLEX_NEAR if complex_near else 0)
+        self.complex_near = complex_near
         h = ctypes.c_void_p()
         _capi.check(self.lib.nesa_plan_create(ctypes.byref(d), self.device, ctypes.byref(h)))
         self._h = h

@@ -187,7 +187,8 @@ def _case(name):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["C1", "C2"])
-def test_track_b_gpu_vs_oracle(name):
+@pytest.mark.parametrize("complex_near", [True, False])
+def test_track_b_gpu_vs_oracle(name, complex_near):
     _gpu()
     from paper_1801_03589_b200.plan3 import HelmholtzPlan
     pts, tree, params, q = _case(name)
@@ -196,11 +197,11 @@ def test_track_b_gpu_vs_oracle(name):
     ref = oracle_mvp(tree, ops, q)
     ref_near = oracle_mvp(tree, ops, q, far=False)
     for src in (tables, ops):
-        p128 = HelmholtzPlan(tree, src, "c128")
+        p128 = HelmholtzPlan(tree, src, "c128", complex_near=complex_near)
         assert rel_l2(p128.matvec(q), ref) <= 1e-12
         assert rel_l2(p128.matvec(q, far=False), ref_near) <= 1e-13
         p128.close()
-        p64 = HelmholtzPlan(tree, src, "c64")
+        p64 = HelmholtzPlan(tree, src, "c64", complex_near=complex_near)
         out = p64.matvec(q.astype(np.complex64))
         assert out.dtype == np.complex64
         assert rel_l2(out, ref) <= 1e-5

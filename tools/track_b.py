@@ -43,9 +43,9 @@ def main():
         if not a.no_oracle:
             ref = mvp_serial(tree, hz.build_all3(tree, params, tables), q)
         dense = hz.dense_helmholtz(pts, q, params.k) if n <= a.dense_max else None
-        for dt in ("c64", "c128"):
+        for dt, cn in (("c64", True), ("c128", True), ("c64", False)):
             t1 = time.perf_counter()
-            plan = HelmholtzPlan(tree, tables, dt)
+            plan = HelmholtzPlan(tree, tables, dt, complex_near=cn)
             t_plan = time.perf_counter() - t1
             cq = np.complex64 if dt == "c64" else np.complex128
             qd = torch.from_numpy(q.astype(cq)).cuda()
@@ -66,8 +66,10 @@ def main():
             phi = out.cpu().numpy()
             rec = {"config": name, "surface": kind, "N": n, "P": P, "Q": Q, "k": round(params.k, 4),
                    "levels": tree.L - tree.l0 + 1, "leaves": tree.n_leaves, "dtype": dt,
+                   "near": "complex row-split" if cn else "real 2x2 embedding",
                    "us_per_product": round(us, 1), "products_per_s": round(1e6 / us, 1),
-                   "near_entries_complex": plan.stat("near_entries") // 4,
+                   "near_entries_complex": plan.stat("near_entries") // (2 if cn else 4),
+                   "near_bytes": plan.stat("near_entries") * (4 if dt == "c64" else 8),
                    "kernels": plan.stat("kernels_per_matvec"),
                    "rel_l2_vs_oracle": None if ref is None else float(f"{rel_l2(phi, ref):.3e}"),
                    "rel_l2_vs_dense": None if dense is None else float(f"{rel_l2(phi, dense):.3e}"),
