@@ -149,6 +149,11 @@ typedef struct nesa_plan_desc {
                                    once per product with complex vectors -- 8 bytes per complex
                                    float32 entry instead of the embedding's 16.  Products run
                                    one complex right-hand side per pass. */
+#define NESA_PLAN_STORED_VU 8u   /* store the per-leaf V and U blocks (assembled on the device) even
+                                   for float32 plans from geometry: products of more than 4 real
+                                   columns then run the far field as batched GEMMs over 128-column
+                                   passes (C5: many right-hand sides), float32 adds the near field
+                                   as one tensor-core GEMM per pass (nesa_matvec_near_wide) */
 
 int nesa_plan_create(const nesa_plan_desc* desc, int device, nesa_plan** out);
 
@@ -257,6 +262,7 @@ int nesa_abi_version(void);
 #define NESA_STAT_GRAPH_CAPTURES 10  /* stream captures so far (one per schedule)  */
 #define NESA_STAT_GRAPHS_CACHED 11   /* instantiated graphs held by the plan       */
 #define NESA_STAT_NEAR_WIDE 12       /* 1: nesa_matvec_near_wide available          */
+#define NESA_STAT_FAR_WIDE 13        /* 1: many-column products run the far field as GEMMs */
 int64_t nesa_plan_stat(nesa_plan* plan, int32_t which);
 
 /* Profiling: with NESA_PROFILE in flags each nesa_matvec records CUDA

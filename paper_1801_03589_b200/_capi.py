@@ -16,6 +16,7 @@ NESA_ABI_VERSION = 2
 NESA_PLAN_FAR_ONLY = 1
 NESA_PLAN_OCTREE = 2
 NESA_PLAN_COMPLEX_NEAR = 4
+NESA_PLAN_STORED_VU = 8
 NESA_OK = 0
 NESA_ERR_INVALID = 1
 NESA_ERR_CUDA = 2
@@ -30,7 +31,8 @@ NESA_PROFILE_NEAR = 32
 
 STAT = {"near_entries": 0, "v_entries": 1, "u_entries": 2, "d_refs": 3, "n_dtab": 4,
         "device_bytes": 5, "near_ctas": 6, "kernels_per_matvec": 7, "v_moments": 8,
-        "u_terms": 9, "graph_captures": 10, "graphs_cached": 11, "near_wide": 12}
+        "u_terms": 9, "graph_captures": 10, "graphs_cached": 11, "near_wide": 12,
+        "far_wide": 13}
 STAGE = {"total": 0, "near": 1, "far": 2, "reception": 3}
 
 EXPORTED_SYMBOLS = (

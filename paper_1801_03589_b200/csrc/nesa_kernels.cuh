@@ -3187,6 +3187,193 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
 }
 
 // ----------------------------------------------------------------------------
+// Many right-hand sides (C5): the far field as batched GEMMs over up to 128
+// columns.  With one or two columns every far-field step is a latency-bound
+// GEMV; with 128 it is a dense GEMM per group (M = Q or leaf rows, N = 128,
+// K = Q or leaf points), so the whole chain -- radiation V q, the upward
+// C s, translation D s plus downward B o, reception U o -- runs through ONE
+// register-tiled kernel fed by host-built work lists:
+//
+//   item  = one output tile (<= 64 rows x 128 columns: a group's s or o, or
+//           a leaf panel of phi), written by exactly one CTA;
+//   terms = the (matrix, input rows) products summed into it, in the
+//           reference's order (children in id order; interaction entries in
+//           list order, then B o_parent -- fastmvp.py:160-169).
+//
+// Matrices are column-major with a leading dimension (the plan's transposed
+// C / B / D tables, the stored V / U blobs), inputs are rows of kWCols
+// values (tree-order charges, s, o).  Each CTA stages K chunks of A and X in
+// shared memory (double-buffered through registers) and every thread owns a
+// 4 x 8 tile (FFMA2 on column pairs for float32).  One launch per stage and
+// level, every launch independent of the column count up to 128.
+// ----------------------------------------------------------------------------
+constexpr int kWCols = 128;
+constexpr int kWRows = 64;
+constexpr int kWThreads = 256;
+
+struct WTerm {
+  int64_t a_off;  // A(0, 0) of the tile: element offset in matrix base `abase`
+  int64_t x_row;  // first input row (K rows of kWCols values)
+  int32_t lda;    // column stride of A (multiple of 4)
+  int32_t k;      // inner dimension
+  int32_t abase;  // 0 C table, 1 B table, 2 D table, 3 V blob, 4 U blob
+  int32_t xsel;   // 0 charges (tree order), 1 s, 2 o
+};
+struct WItem {
+  int64_t y_row;  // first output row (workspace row, or tree row when scattering)
+  int32_t m;      // rows of the tile (<= kWRows)
+  int32_t t0, t1; // terms
+  int32_t pad;
+};
+static_assert(sizeof(WTerm) == 32 && sizeof(WItem) == 24, "work-list records");
+
+template <typename T>
+struct WArgs {
+  const WItem* items;
+  const WTerm* terms;
+  const T* abase[5];
+  const T* xs[3];
+  T* y;                 // store: workspace rows of kWCols; scatter: phi rows of ldy
+  const int64_t* perm;  // scatter: tree row -> original row
+  int64_t ldy;
+  int col0, ncols;      // scatter: the caller's columns [col0, col0 + ncols)
+};
+
+template <typename T>
+struct WTile {
+  static constexpr int KC = sizeof(T) == 4 ? 16 : 8;      // K chunk
+  static constexpr int AV = KC * kWRows / kWThreads;      // A values per thread per chunk
+  static constexpr int XV = KC * kWCols / kWThreads;      // X values per thread per chunk
+};
+
+template <typename T, bool SCATTER>
+__global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant__ WArgs<T> a) {
+  using W = WTile<T>;
+  constexpr int KC = W::KC, AV = W::AV, XV = W::XV;
+  __shared__ __align__(16) T As[2][KC][kWRows];
+  __shared__ __align__(16) T Xs[2][KC][kWCols];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const WItem it = a.items[blockIdx.x];
+  // loader mapping: A  k = tid / (64 / AV), rows (tid % (64 / AV)) * AV ...
+  //                 X  k = tid / (128 / XV), columns (tid % (128 / XV)) * XV ...
+  const int a_k = tid / (kWRows / AV), a_r = (tid % (kWRows / AV)) * AV;
+  const int x_k = tid / (kWCols / XV), x_c = (tid % (kWCols / XV)) * XV;
+  T ra[AV], rx[XV];
+  int t = it.t0, k0 = 0;
+  auto load = [&](int tt, int kk0) {
+    const WTerm w = a.terms[tt];
+    const int k = kk0 + a_k;
+    const T* A = a.abase[w.abase] + w.a_off + int64_t(k) * w.lda + a_r;
+#pragma unroll
+    for (int v = 0; v < AV; ++v) ra[v] = (k < w.k && a_r + v < it.m) ? A[v] : T(0);
+    const int kx = kk0 + x_k;
+    if (kx < w.k) {
+      const T* X = a.xs[w.xsel] + (w.x_row + kx) * kWCols + x_c;
+#pragma unroll
+      for (int v = 0; v < XV; v += 16 / int(sizeof(T))) {
+        if constexpr (sizeof(T) == 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(X + v));
+          rx[v] = f.x; rx[v + 1] = f.y; rx[v + 2] = f.z; rx[v + 3] = f.w;
+        } else {
+          const double2 f = __ldg(reinterpret_cast<const double2*>(X + v));
+          rx[v] = f.x; rx[v + 1] = f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < XV; ++v) rx[v] = T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int v = 0; v < AV; ++v) As[buf][a_k][a_r + v] = ra[v];
+#pragma unroll
+    for (int v = 0; v < XV; ++v) Xs[buf][x_k][x_c + v] = rx[v];
+  };
+  T acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = T(0);
+  int buf = 0;
+  bool have = t < it.t1;
+  if (have) load(t, 0);
+  while (have) {
+    store(buf);
+    __syncthreads();
+    // next chunk (the same term's next K chunk, or the next term)
+    const int kt = a.terms[t].k;
+    k0 += KC;
+    if (k0 >= kt) {
+      k0 = 0;
+      ++t;
+    }
+    have = t < it.t1;
+    if (have) load(t, k0);
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      T av[4], x0[4], x1[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[buf][kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        x0[j] = Xs[buf][kk][tx * 4 + j];
+        x1[j] = Xs[buf][kk][64 + tx * 4 + j];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if constexpr (sizeof(T) == 4) {
+          ffma2(acc[i][0], acc[i][1], av[i], x0[0], x0[1]);
+          ffma2(acc[i][2], acc[i][3], av[i], x0[2], x0[3]);
+          ffma2(acc[i][4], acc[i][5], av[i], x1[0], x1[1]);
+          ffma2(acc[i][6], acc[i][7], av[i], x1[2], x1[3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[i][j] = fma(av[i], x0[j], acc[i][j]);
+            acc[i][4 + j] = fma(av[i], x1[j], acc[i][4 + j]);
+          }
+        }
+      }
+    }
+    buf ^= 1;
+  }
+  // epilogue: this CTA is the tile's only writer
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty * 4 + i;
+    if (r >= it.m) continue;
+    if constexpr (!SCATTER) {
+      T* y = a.y + (it.y_row + r) * kWCols;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        y[tx * 4 + j] = acc[i][j];
+        y[64 + tx * 4 + j] = acc[i][4 + j];
+      }
+    } else {
+      T* y = a.y + a.perm[it.y_row + r] * a.ldy + a.col0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (tx * 4 + j < a.ncols) y[tx * 4 + j] = acc[i][j];
+        if (64 + tx * 4 + j < a.ncols) y[64 + tx * 4 + j] = acc[i][4 + j];
+      }
+    }
+  }
+}
+
+// qt[t][c] = q[perm[t]][col0 + c] for c < ncols, 0 beyond (rows of kWCols)
+template <typename T>
+__global__ void wgather_kernel(const T* __restrict__ q, int64_t ldq, int col0, int ncols,
+                               const int64_t* __restrict__ perm, int64_t n, T* __restrict__ qt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * kWCols;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i / kWCols;
+    const int c = int(i - t * kWCols);
+    qt[i] = c < ncols ? q[perm[t] * ldq + col0 + c] : T(0);
+  }
+}
+
+// ----------------------------------------------------------------------------
 // Multi-GPU halo exchange (paper_1801_03589_b200/dist.py):
 // pack this rank's partial source amplitudes that other ranks need into the
 // all_gather send buffer, and complete the needed groups' amplitudes as the

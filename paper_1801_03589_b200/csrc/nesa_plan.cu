@@ -401,6 +401,17 @@ struct nesa_plan {
   DevBuf<float> ATC;                        // [hi | lo][64 x 80] canonical tf32 A^ (K = 80)
   DevBuf<int32_t> rad_order;                // local leaves by descending point count
   DevBuf<float2> exp_E;                     // [Q][u_nt + 1]: 1, (1/m) e^{-i m theta_k}
+  // many right-hand sides: the far field as batched GEMMs over up to 128
+  // columns (wgemm_kernel; plans with stored V and U)
+  struct WStage {
+    int64_t begin, end;  // item range
+    int ysel;            // 0 s, 1 o, 2 phi (scatter)
+  };
+  bool wide_far = false;
+  DevBuf<WItem> w_items;
+  DevBuf<WTerm> w_terms;
+  std::vector<WStage> w_stages;
+  DevBuf<unsigned char> w_qt, w_s, w_o;  // N x 128, G x Q x 128 (allocated on first use)
   DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64;
                                             // NESA_TC=0 selects the FFMA kernel, as float64 plans)
@@ -935,6 +946,82 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
   if (!P->v_mom) upload_blockset<T>(P->Vset, hv);
   upload_blockset<T>(P->Uset, hu);
+  // ---- many right-hand sides: work lists of the wide far field
+  if (!P->v_mom && !P->u_mf && !P->cnear && lb == 0 && le == NL) {
+    const int Qp = (Q + 3) / 4 * 4;
+    const int64_t ms = int64_t(mat_bytes(Q, sizeof(T)) / sizeof(T));
+    std::vector<WItem> wi;
+    std::vector<WTerm> wt;
+    // one item per <= kWRows output rows; add(r0) appends the tile's terms
+    auto tiles = [&](int64_t y_row, int m_total, const std::function<void(int)>& add) {
+      for (int r0 = 0; r0 < m_total; r0 += kWRows) {
+        WItem I{};
+        I.y_row = y_row + r0;
+        I.m = std::min(kWRows, m_total - r0);
+        I.t0 = int32_t(wt.size());
+        add(r0);
+        I.t1 = int32_t(wt.size());
+        wi.push_back(I);
+      }
+    };
+    auto stage = [&](int64_t b, int ysel) { P->w_stages.push_back({b, int64_t(wi.size()), ysel}); };
+    std::vector<int64_t> cfirst(size_t(G), -1);
+    std::vector<int32_t> ccount(size_t(G), 0);
+    for (int64_t g = 0; g < G; ++g) {
+      const int64_t p = d->parent[g];
+      if (p < 0) continue;
+      if (cfirst[size_t(p)] < 0) cfirst[size_t(p)] = g;
+      ccount[size_t(p)]++;
+    }
+    // radiation: s_leaf = V_leaf q_leaf (fastmvp.py:158-159)
+    int64_t b = int64_t(wi.size());
+    for (const BlockItem& v : hv.items)
+      tiles(v.y_row0, Q, [&](int r0) {
+        wt.push_back(WTerm{v.a_off + r0, int64_t(v.x0), v.ld, v.n, 3, 0});
+      });
+    stage(b, 0);
+    // source transfer, levels L-1 .. l0: s_p = sum_children C_{quad c} s_c (160-162)
+    for (int lv = P->L - 1; lv >= P->l0; --lv) {
+      b = int64_t(wi.size());
+      const int64_t f = P->lvl_first[lv - P->l0], n = P->lvl_count[lv - P->l0];
+      for (int64_t p = f; p < f + n; ++p)
+        tiles(p * Q, Q, [&](int r0) {
+          for (int k = 0; k < ccount[size_t(p)]; ++k) {
+            const int64_t c = cfirst[size_t(p)] + k;
+            wt.push_back(WTerm{(int64_t(lv - P->l0) * P->nkind + d->quad[c]) * ms + r0, c * Q, Qp, Q, 0, 1});
+          }
+        });
+      stage(b, 0);
+    }
+    // translation + potential transfer, levels l0 .. L:
+    // o_g = sum_e D_e s_src(e) (163-166) + B_{quad g} o_parent (167-169)
+    for (int lv = P->l0; lv <= P->L; ++lv) {
+      b = int64_t(wi.size());
+      const int64_t f = P->lvl_first[lv - P->l0], n = P->lvl_count[lv - P->l0];
+      for (int64_t g = f; g < f + n; ++g)
+        tiles(g * Q, Q, [&](int r0) {
+          for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e)
+            wt.push_back(WTerm{d->int_dtab[e] * ms + r0, d->int_idx[e] * Q, Qp, Q, 2, 1});
+          if (lv > P->l0)
+            wt.push_back(WTerm{(int64_t(lv - P->l0 - 1) * P->nkind + d->quad[g]) * ms + r0,
+                               d->parent[g] * Q, Qp, Q, 1, 2});
+        });
+      stage(b, 1);
+    }
+    // reception: phi[perm] = U_leaf o_leaf (170-172), panels of the stored U
+    b = int64_t(wi.size());
+    for (size_t i = 0; i < hu.items.size(); ++i) {
+      const BlockItem& u = hu.items[i];
+      tiles(u.y_row0, u.m, [&](int r0) {
+        wt.push_back(WTerm{u.a_off + r0, u_leaf[i] * Q, u.ld, Q, 4, 2});
+      });
+    }
+    stage(b, 2);
+    require(wt.size() < (size_t(1) << 31), "wide work list too large");
+    P->w_items.upload(wi);
+    P->w_terms.upload(wt);
+    P->wide_far = true;
+  }
 
   // ---- fill the blobs: from host operators or assembled on the device
   DevBuf<double> pts;
@@ -1839,6 +1926,52 @@ void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int
   }
 }
 
+// Far field of real columns [col0, col0 + ncols) (ncols <= kWCols) of
+// (N, ld) row-major blocks in original order as batched GEMMs (wgemm_kernel):
+// phi[:, cols] = far field (stored, not accumulated).  Stream-ordered.
+template <typename T>
+void run_far_wide_T(nesa_plan* P, const void* q, void* phi, int ld, int col0, int ncols, cudaStream_t st) {
+  const size_t es = sizeof(T);
+  if (!P->w_qt.p) {
+    P->w_qt.alloc(size_t(P->N) * kWCols * es);
+    P->w_s.alloc(size_t(P->G) * P->Q * kWCols * es);
+    P->w_o.alloc(size_t(P->G) * P->Q * kWCols * es);
+  }
+  T* qt = reinterpret_cast<T*>(P->w_qt.p);
+  T* s = reinterpret_cast<T*>(P->w_s.p);
+  T* o = reinterpret_cast<T*>(P->w_o.p);
+  wgather_kernel<T><<<grid_for(P->N * kWCols, 256, 8 * P->n_sm), 256, 0, st>>>(
+      static_cast<const T*>(q), ld, col0, ncols, P->perm.p, P->N, qt);
+  CUDA_OK(cudaGetLastError());
+  WArgs<T> a{};
+  a.terms = P->w_terms.p;
+  a.abase[0] = reinterpret_cast<const T*>(P->CT.p);
+  a.abase[1] = reinterpret_cast<const T*>(P->BT.p);
+  a.abase[2] = reinterpret_cast<const T*>(P->DT.p);
+  a.abase[3] = reinterpret_cast<const T*>(P->Vset.blob.p);
+  a.abase[4] = reinterpret_cast<const T*>(P->Uset.blob.p);
+  a.xs[0] = qt;
+  a.xs[1] = s;
+  a.xs[2] = o;
+  a.perm = P->perm.p;
+  a.ldy = ld;
+  a.col0 = col0;
+  a.ncols = ncols;
+  for (const auto& S : P->w_stages) {
+    if (S.end <= S.begin) continue;
+    a.items = P->w_items.p + S.begin;
+    const unsigned grid = unsigned(S.end - S.begin);
+    if (S.ysel == 2) {
+      a.y = static_cast<T*>(phi);
+      wgemm_kernel<T, true><<<grid, kWThreads, 0, st>>>(a);
+    } else {
+      a.y = S.ysel == 0 ? s : o;
+      wgemm_kernel<T, false><<<grid, kWThreads, 0, st>>>(a);
+    }
+    CUDA_OK(cudaGetLastError());
+  }
+}
+
 // One product of nrhs right-hand sides: real columns are processed in blocks
 // of <= 4 (one captured graph per block width; rows of q / phi keep their stride).
 int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_complex,
@@ -1860,6 +1993,21 @@ int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_
   require(stage == 0, "the staged (multi-GPU) product takes at most 4 real columns");
   require(!(flags & NESA_PROFILE), "profiling takes at most 4 real columns");
   const size_t es = P->esz;
+  if ((flags & NESA_FAR) && P->wide_far && P->comm == nullptr && (!(flags & NESA_NEAR) || near_wide_ok(P))) {
+    // many right-hand sides: the far field as batched GEMMs over 128-column
+    // passes (writes phi), then the near field's tensor-core GEMM adds to it
+    CUDA_OK(cudaSetDevice(P->device));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int c0 = 0; c0 < Rt; c0 += kWCols) {
+      const int nc = std::min(kWCols, Rt - c0);
+      if (P->dtype == NESA_F64)
+        run_far_wide_T<double>(P, q, phi, Rt, c0, nc, st);
+      else
+        run_far_wide_T<float>(P, q, phi, Rt, c0, nc, st);
+      if (flags & NESA_NEAR) run_near_wide(P, q, phi, Rt, c0, nc, st);
+    }
+    return NESA_OK;
+  }
   // float32 with tensor cores: the far field in blocks of <= 4 columns, then
   // the near field ONCE for all columns (tcgen05 GEMM, operator read once)
   const bool wide = (flags & NESA_NEAR) && near_wide_ok(P) && P->comm == nullptr;
@@ -2056,6 +2204,12 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     if (const char* us = std::getenv("NESA_U_STORED")) P->u_mf = P->u_mf && std::atoi(us) == 0;
     P->v_mom = d->op_dtype == NESA_F32 && !d->V_blob;
     if (const char* vs = std::getenv("NESA_V_STORED")) P->v_mom = P->v_mom && std::atoi(vs) == 0;
+    if (d->options & NESA_PLAN_STORED_VU) {
+      // many right-hand sides: stored V / U blocks (assembled on the device),
+      // the far field then runs as batched GEMMs over all columns
+      P->v_mom = false;
+      P->u_mf = false;
+    }
     if (const char* tr = std::getenv("NESA_TRACE")) P->trace = std::atoi(tr) != 0;
     P->leaf_begin = d->leaf_begin;
     P->leaf_end = d->leaf_end;
@@ -2373,6 +2527,8 @@ NESA_API int64_t nesa_plan_stat(nesa_plan* P, int32_t which) {
       return int64_t(P->graphs.size());
     case NESA_STAT_NEAR_WIDE:
       return near_wide_ok(P) ? 1 : 0;
+    case NESA_STAT_FAR_WIDE:
+      return P->wide_far ? 1 : 0;
     default:
       return -1;
   }

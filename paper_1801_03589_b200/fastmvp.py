@@ -69,21 +69,27 @@ def as_tree(tree) -> Tree:
     return out
 
 
-def get_plan(tree, ops, dtype: str = "f64", device: int = 0) -> NesaPlan:
-    """Cached plan for (tree, ops, dtype, device); built on first use."""
+def get_plan(tree, ops, dtype: str = "f64", device: int = 0, wide: bool = False) -> NesaPlan:
+    """Cached plan for (tree, ops, dtype, device); built on first use.
+
+    ``wide``: the plan for products of more than 4 real columns -- stored
+    V / U blocks, so the far field runs as batched GEMMs over 128-column
+    passes (for a host OperatorSet that is the ordinary plan)."""
     t = as_tree(tree)
     cache = getattr(t, "_nesa_plans", None)
     if cache is None:
         cache = {}
         t._nesa_plans = cache
-    key = (id(ops), dtype, device)
+    if wide and isinstance(ops, OperatorSet):
+        wide = False
+    key = (id(ops), dtype, device, wide)
     ent = cache.get(key)
     if ent is None or ent[0] is not ops:
         if not isinstance(ops, (OperatorSet, OperatorTables, NesaParams)):
             ops_in = _adopt_opset(ops)
         else:
             ops_in = ops
-        ent = (ops, NesaPlan(t, ops_in, dtype=dtype, device=device))
+        ent = (ops, NesaPlan(t, ops_in, dtype=dtype, device=device, stored_vu=wide))
         cache[key] = ent
     return ent[1]
 
@@ -209,7 +215,15 @@ def mvp(tree, ops, q, runtime=None, vec=None, near: bool = True, far: bool = Tru
         else:
             qd = torch.from_numpy(np.ascontiguousarray(q)).to(f"cuda:{dev}", dtype=tdt)
         phi = torch.empty_like(qd)
-        if nrhs * (2 if is_complex else 1) > 4:   # several blocks: spread over lanes
+        wide = nrhs * (2 if is_complex else 1) > 4
+        if wide and far:
+            # many right-hand sides: the far field as batched GEMMs over all
+            # columns, the near field as one tensor-core GEMM (float32)
+            wplan = get_plan(t, ops, dtype=dtype, device=dev, wide=True)
+        if wide and far and wplan.stat("far_wide") == 1 and (not near or dtype == "f32"):
+            wplan.matvec_ptr(qd.data_ptr(), phi.data_ptr(), nrhs, is_complex, near=near, far=far,
+                             stream=stream.cuda_stream)
+        elif wide:   # several blocks of <= 4 columns, spread over lanes
             get_lanes(t, ops, dtype=dtype, device=dev).matvec_ptr(
                 qd.data_ptr(), phi.data_ptr(), nrhs, is_complex, near=near, far=far,
                 stream=stream.cuda_stream)

@@ -117,6 +117,10 @@ class NesaPlan:
     dtype : "f64" (float64 / complex128 vectors) or "f32" (float32 / complex64).
     device : CUDA device ordinal.
     leaf_range : (begin, end) leaf ids of this rank's targets (multi-GPU).
+    stored_vu : keep stored V / U blocks even for a float32 plan from
+        geometry; products of more than 4 real columns then run the far
+        field as batched GEMMs over 128-column passes (many right-hand
+        sides, C5).
     v_on_host : assemble the radiation blocks V = fit @ K(check, pts) on the
         host, per leaf, exactly as operators.py:107-112 does (default for
         float64 plans).  V goes through the ill-conditioned pinv fit, which
@@ -128,7 +132,8 @@ class NesaPlan:
 
     def __init__(self, tree: Tree, ops, dtype: str = "f64", device: int = 0,
                  leaf_range: tuple[int, int] | None = None, v_on_host: bool | None = None,
-                 comm=None, rank: int = 0, nranks: int = 1, exchange=None, far_only: bool = False):
+                 comm=None, rank: int = 0, nranks: int = 1, exchange=None, far_only: bool = False,
+                 stored_vu: bool = False):
         self.lib = _capi.load()
         if dtype not in _DTYPES:
             raise ValueError(f"unknown dtype {dtype!r}")
@@ -211,8 +216,10 @@ class NesaPlan:
         if leaf_range is not None:
             d.leaf_begin, d.leaf_end = int(leaf_range[0]), int(leaf_range[1])
         # far_only: no near operator (extra plans of a many-RHS product)
-        d.options = _capi.NESA_PLAN_FAR_ONLY if far_only else 0
+        d.options = (_capi.NESA_PLAN_FAR_ONLY if far_only else 0) | \
+            (_capi.NESA_PLAN_STORED_VU if stored_vu else 0)
         self.far_only = far_only
+        self.stored_vu = stored_vu
         self.leaf_range = leaf_range
         h = ctypes.c_void_p()
         if comm is None:

@@ -659,3 +659,28 @@ def test_fused_gram_schmidt_step(dt, kk, tol):
     assert np.abs(hc - (h1 + h2)).max() <= tol * np.abs(h1).max()
     assert abs(h[2 * kk] - nrm) <= tol * nrm
     assert np.linalg.norm(V[kk].cpu().numpy() - w2 / nrm) <= 10 * tol
+
+
+@pytest.mark.parametrize("dtype,tol,nw,Q,P", [("f32", 1e-5, 70, 24, 32), ("f32", 1e-5, 64, 96, 64),
+                                              ("f64", 1e-12, 9, 48, 32)])
+def test_many_rhs_far_field_as_gemms(dtype, tol, nw, Q, P):
+    # C5: more than 4 real columns on a plan with stored V / U run the far
+    # field as batched GEMMs over 128-column passes (wgemm_kernel) -- here 140
+    # real columns (two passes), Q = 96 (two row tiles per group) and the
+    # float64 engine (far field only: its near field has no tensor-core path)
+    from paper_1801_03589_b200.fastmvp import get_plan
+    n = 12000
+    spec = geo.CurveSpec(kind="ellipse-plates", seed=4)
+    pts = geo.generate_sources(spec, n)
+    tree = build_tree(pts, TreeParams(P=P))
+    params = NesaParams(Q=Q)
+    Qm = geo.plane_wave_rhs(pts, geo.wavenumber(spec, n), n_waves=nw)
+    ops = build_all(tree, params)
+    cols = [0, nw // 2, nw - 1]
+    qq = Qm if dtype == "f64" else Qm.astype(np.complex64)
+    near = dtype == "f32"
+    phi = mvp(tree, params, qq, near=near)
+    assert get_plan(tree, params, dtype=dtype, wide=True).stat("far_wide") == 1
+    ref = oracle_mvp(tree, ops, Qm[:, cols], near=near)
+    for j, c in enumerate(cols):
+        assert rel_l2(phi[:, c], ref[:, j]) <= tol, (c, rel_l2(phi[:, c], ref[:, j]))

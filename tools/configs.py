@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--only", default="")
     ap.add_argument("--c5", action="store_true")
+    ap.add_argument("--gemm-only", action="store_true", help="C5: time only the GEMM far-field path")
     a = ap.parse_args()
     if a.c5:
         return c5(a)
@@ -96,7 +97,13 @@ def c5(a):
                    "plan": "f32"}
             lanes = RhsLanes(plan, 4)
             lanes8 = RhsLanes(plan, 8)
-            for tag, eng in (("one_plan", plan), ("lanes4", lanes), ("lanes8", lanes8)):
+            # stored V / U: the far field as batched GEMMs over the 128 columns
+            gplan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=Q)), dtype="f32",
+                             stored_vu=True)
+            assert gplan.stat("far_wide") == 1
+            engines = [("gemm", gplan)] + ([] if a.gemm_only else
+                                            [("one_plan", plan), ("lanes4", lanes), ("lanes8", lanes8)])
+            for tag, eng in engines:
                 for _ in range(3):
                     eng.matvec_ptr(qd.data_ptr(), phi.data_ptr(), 64, True, stream=st.cuda_stream)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -125,6 +132,7 @@ def c5(a):
             for p_ in lanes.plans[1:] + lanes8.plans[1:]:
                 p_.close()
             plan.close()
+            gplan.close()
 
 
 if __name__ == "__main__":
