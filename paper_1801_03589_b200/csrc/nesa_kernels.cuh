@@ -3051,7 +3051,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
                                                          const float* __restrict__ blob,
                                                          const float* __restrict__ q, int ldq, int c0,
                                                          int ncols, const int64_t* __restrict__ perm,
-                                                         float* __restrict__ phi) {
+                                                         float* __restrict__ phi, int accumulate) {
   KtScope kt_(90);
   extern __shared__ __align__(128) unsigned char smem[];
   float* Bs = reinterpret_cast<float*>(smem);  // 2 buffers x [hi | lo] x npad x 32
@@ -3169,7 +3169,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
       for (int j = 0; j < 32; ++j) dst[j] = j < nn ? perm[it.y_row0 + n0 + j] : 0;
       if (col_live) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) cur[j] = j < nn ? phi[dst[j] * ldq + c0 + tid] : 0.f;
+        for (int j = 0; j < 32; ++j) cur[j] = (accumulate && j < nn) ? phi[dst[j] * ldq + c0 + tid] : 0.f;
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (j < nn) phi[dst[j] * ldq + c0 + tid] = cur[j] + __uint_as_float(r[j]);
@@ -3232,34 +3232,59 @@ struct WArgs {
   const WItem* items;
   const WTerm* terms;
   const T* abase[5];
-  const T* xs[3];
+  const T* xs[3];       // xsel 1 s, 2 o (rows of kWCols); xsel 0 reads the caller's q
   T* y;                 // store: workspace rows of kWCols; scatter: phi rows of ldy
-  const int64_t* perm;  // scatter: tree row -> original row
+  const int64_t* perm;  // tree row -> original row (charges in, phi out)
+  const T* q;           // xsel 0: the caller's charges, (N, ldy) in original order
   int64_t ldy;
-  int col0, ncols;      // scatter: the caller's columns [col0, col0 + ncols)
+  int col0, ncols;      // the caller's columns [col0, col0 + ncols)
+  int vec4;             // ldy and col0 multiples of 16 bytes: vector loads of q rows
 };
+enum { kWStore = 0, kWScatter = 1, kWScatterAdd = 2 };
 
-template <typename T>
+// Tile geometry: NC output columns per CTA (blockIdx.y picks the column
+// block), KG groups of 256 / KG threads that split an item's terms between
+// them (term-strided; each group has its own barrier and double buffer) and
+// add their partial tiles in a fixed order at the end.  Wide levels use
+// <128, 1>; the coarse levels -- few groups, many terms each -- <32, 4>,
+// which gives 16x the CTAs and a quarter of the serial chunk chain.
+template <typename T, int NC, int KG>
 struct WTile {
-  static constexpr int KC = sizeof(T) == 4 ? 16 : 8;      // K chunk
-  static constexpr int AV = KC * kWRows / kWThreads;      // A values per thread per chunk
-  static constexpr int XV = KC * kWCols / kWThreads;      // X values per thread per chunk
+  static constexpr int KC = sizeof(T) == 4 ? 16 : 8;  // K chunk
+  static constexpr int GT = kWThreads / KG;           // threads per group
+  static constexpr int CG = NC / 8;                   // column groups (8 columns per thread)
+  static constexpr int AV = KC * kWRows / GT;         // A values per thread per chunk
+  static constexpr int XV = KC * NC / GT;             // X values per thread per chunk
+  static constexpr int kBuf = 2 * KC * (kWRows + NC); // one group's double buffer (elements)
+  static constexpr size_t kSmem =
+      sizeof(T) * (size_t(KG) * kBuf > (KG > 1 ? size_t(KG) * kWRows * NC : 0)
+                       ? size_t(KG) * kBuf
+                       : size_t(KG) * kWRows * NC);
+  static_assert(GT == 16 * CG, "4 x 8 thread tiles cover 64 rows x NC columns");
+  static_assert(AV >= 1 && XV >= 4 && XV % 4 == 0, "loader geometry");
 };
 
-template <typename T, bool SCATTER>
+template <typename T, int MODE, int NC, int KG>
 __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant__ WArgs<T> a) {
-  using W = WTile<T>;
-  constexpr int KC = W::KC, AV = W::AV, XV = W::XV;
-  __shared__ __align__(16) T As[2][KC][kWRows];
-  __shared__ __align__(16) T Xs[2][KC][kWCols];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  using W = WTile<T, NC, KG>;
+  constexpr int KC = W::KC, AV = W::AV, XV = W::XV, GT = W::GT, CG = W::CG;
+  extern __shared__ __align__(16) unsigned char wsm[];
+  const int tid = threadIdx.x, grp = tid / GT, lt = tid % GT;
+  const int tx = lt % CG, ty = lt / CG;
+  T* const gbuf = reinterpret_cast<T*>(wsm) + size_t(grp) * W::kBuf;
+  auto As = [&](int buf, int k) { return gbuf + (buf * KC + k) * kWRows; };
+  auto Xs = [&](int buf, int k) { return gbuf + 2 * KC * kWRows + (buf * KC + k) * NC; };
+  auto gsync = [&]() {
+    if constexpr (KG == 1)
+      __syncthreads();
+    else
+      named_bar_sync(1 + grp, GT);
+  };
   const WItem it = a.items[blockIdx.x];
-  // loader mapping: A  k = tid / (64 / AV), rows (tid % (64 / AV)) * AV ...
-  //                 X  k = tid / (128 / XV), columns (tid % (128 / XV)) * XV ...
-  const int a_k = tid / (kWRows / AV), a_r = (tid % (kWRows / AV)) * AV;
-  const int x_k = tid / (kWCols / XV), x_c = (tid % (kWCols / XV)) * XV;
+  const int cb = blockIdx.y * NC;  // first column of this CTA
+  const int a_k = lt / (kWRows / AV), a_r = (lt % (kWRows / AV)) * AV;
+  const int x_k = lt / (NC / XV), x_c = (lt % (NC / XV)) * XV;
   T ra[AV], rx[XV];
-  int t = it.t0, k0 = 0;
   auto load = [&](int tt, int kk0) {
     const WTerm w = a.terms[tt];
     const int k = kk0 + a_k;
@@ -3267,8 +3292,27 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
 #pragma unroll
     for (int v = 0; v < AV; ++v) ra[v] = (k < w.k && a_r + v < it.m) ? A[v] : T(0);
     const int kx = kk0 + x_k;
-    if (kx < w.k) {
-      const T* X = a.xs[w.xsel] + (w.x_row + kx) * kWCols + x_c;
+    const int col = cb + x_c;  // column within the pass
+    if (kx < w.k && w.xsel == 0) {
+      // charges straight from the caller's q through perm (no gather pass)
+      const T* X = a.q + a.perm[w.x_row + kx] * a.ldy + a.col0 + col;
+      if (a.vec4 && col + XV <= a.ncols) {
+#pragma unroll
+        for (int v = 0; v < XV; v += 16 / int(sizeof(T))) {
+          if constexpr (sizeof(T) == 4) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(X + v));
+            rx[v] = f.x; rx[v + 1] = f.y; rx[v + 2] = f.z; rx[v + 3] = f.w;
+          } else {
+            const double2 f = __ldg(reinterpret_cast<const double2*>(X + v));
+            rx[v] = f.x; rx[v + 1] = f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < XV; ++v) rx[v] = col + v < a.ncols ? __ldg(X + v) : T(0);
+      }
+    } else if (kx < w.k) {
+      const T* X = a.xs[w.xsel] + (w.x_row + kx) * kWCols + col;
 #pragma unroll
       for (int v = 0; v < XV; v += 16 / int(sizeof(T))) {
         if constexpr (sizeof(T) == 4) {
@@ -3286,39 +3330,41 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int v = 0; v < AV; ++v) As[buf][a_k][a_r + v] = ra[v];
+    for (int v = 0; v < AV; ++v) As(buf, a_k)[a_r + v] = ra[v];
 #pragma unroll
-    for (int v = 0; v < XV; ++v) Xs[buf][x_k][x_c + v] = rx[v];
+    for (int v = 0; v < XV; ++v) Xs(buf, x_k)[x_c + v] = rx[v];
   };
   T acc[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = T(0);
-  int buf = 0;
+  // this group's terms: t0 + grp, t0 + grp + KG, ...
+  int t = it.t0 + grp, k0 = 0, buf = 0;
   bool have = t < it.t1;
   if (have) load(t, 0);
   while (have) {
     store(buf);
-    __syncthreads();
-    // next chunk (the same term's next K chunk, or the next term)
+    gsync();
     const int kt = a.terms[t].k;
     k0 += KC;
     if (k0 >= kt) {
       k0 = 0;
-      ++t;
+      t += KG;
     }
     have = t < it.t1;
     if (have) load(t, k0);
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
+      const T* Ap = As(buf, kk) + ty * 4;
+      const T* Xp = Xs(buf, kk) + tx * 4;
       T av[4], x0[4], x1[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[buf][kk][ty * 4 + i];
+      for (int i = 0; i < 4; ++i) av[i] = Ap[i];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        x0[j] = Xs[buf][kk][tx * 4 + j];
-        x1[j] = Xs[buf][kk][64 + tx * 4 + j];
+        x0[j] = Xp[j];
+        x1[j] = Xp[NC / 2 + j];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -3337,39 +3383,70 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
       }
     }
     buf ^= 1;
+    // the other buffer is rewritten only after every thread of the group
+    // passed this iteration's barrier (two-deep ring, one barrier per chunk)
   }
-  // epilogue: this CTA is the tile's only writer
+  // columns of this thread: cb + tx*4 + j and cb + NC/2 + tx*4 + j
+  if constexpr (KG > 1) {
+    // add the groups' partial tiles in group order (deterministic)
+    __syncthreads();
+    T* red = reinterpret_cast<T*>(wsm);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        red[(size_t(grp) * kWRows + ty * 4 + i) * NC + tx * 4 + j] = acc[i][j];
+        red[(size_t(grp) * kWRows + ty * 4 + i) * NC + NC / 2 + tx * 4 + j] = acc[i][4 + j];
+      }
+    __syncthreads();
+    for (int e = tid; e < kWRows * NC; e += kWThreads) {
+      const int r = e / NC, c = e - (e / NC) * NC;
+      if (r >= it.m) continue;
+      T v = red[e];
+#pragma unroll
+      for (int g = 1; g < KG; ++g) v += red[size_t(g) * kWRows * NC + e];
+      if constexpr (MODE == kWStore) {
+        a.y[(it.y_row + r) * kWCols + cb + c] = v;
+      } else {
+        if (cb + c < a.ncols) {
+          T* y = a.y + a.perm[it.y_row + r] * a.ldy + a.col0 + cb + c;
+          *y = (MODE == kWScatterAdd ? *y : T(0)) + v;
+        }
+      }
+    }
+  } else {
+  // epilogue: this CTA is the tile's only writer; 16-byte stores
+  // (4 consecutive columns per thread and half)
+  auto put4 = [&](T* y, const T* v, int ncol_left) {
+    if constexpr (sizeof(T) == 4) {
+      if (ncol_left >= 4 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+        float4 o = make_float4(v[0], v[1], v[2], v[3]);
+        if (MODE == kWScatterAdd) {
+          const float4 c = *reinterpret_cast<const float4*>(y);
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+        }
+        *reinterpret_cast<float4*>(y) = o;
+        return;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < ncol_left) y[j] = (MODE == kWScatterAdd ? y[j] : T(0)) + v[j];
+  };
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = ty * 4 + i;
     if (r >= it.m) continue;
-    if constexpr (!SCATTER) {
-      T* y = a.y + (it.y_row + r) * kWCols;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        y[tx * 4 + j] = acc[i][j];
-        y[64 + tx * 4 + j] = acc[i][4 + j];
-      }
+    if constexpr (MODE == kWStore) {
+      T* y = a.y + (it.y_row + r) * kWCols + cb;
+      put4(y + tx * 4, &acc[i][0], 4);
+      put4(y + NC / 2 + tx * 4, &acc[i][4], 4);
     } else {
-      T* y = a.y + a.perm[it.y_row + r] * a.ldy + a.col0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (tx * 4 + j < a.ncols) y[tx * 4 + j] = acc[i][j];
-        if (64 + tx * 4 + j < a.ncols) y[64 + tx * 4 + j] = acc[i][4 + j];
-      }
+      T* y = a.y + a.perm[it.y_row + r] * a.ldy + a.col0 + cb;
+      put4(y + tx * 4, &acc[i][0], a.ncols - (cb + tx * 4));
+      put4(y + NC / 2 + tx * 4, &acc[i][4], a.ncols - (cb + NC / 2 + tx * 4));
     }
   }
-}
-
-// qt[t][c] = q[perm[t]][col0 + c] for c < ncols, 0 beyond (rows of kWCols)
-template <typename T>
-__global__ void wgather_kernel(const T* __restrict__ q, int64_t ldq, int col0, int ncols,
-                               const int64_t* __restrict__ perm, int64_t n, T* __restrict__ qt) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n * kWCols;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = i / kWCols;
-    const int c = int(i - t * kWCols);
-    qt[i] = c < ncols ? q[perm[t] * ldq + col0 + c] : T(0);
   }
 }
 

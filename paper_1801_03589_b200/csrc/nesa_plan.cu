@@ -411,7 +411,8 @@ struct nesa_plan {
   DevBuf<WItem> w_items;
   DevBuf<WTerm> w_terms;
   std::vector<WStage> w_stages;
-  DevBuf<unsigned char> w_qt, w_s, w_o;  // N x 128, G x Q x 128 (allocated on first use)
+  DevBuf<unsigned char> w_s, w_o;  // G x Q x 128 (allocated on first use)
+  cudaEvent_t w_ev_fork = nullptr, w_ev_near = nullptr;
   DevBuf<float> mf_leaf_rc;                 // [NL] rho_out_check * half side (float32)
   bool tc = true;                           // translation on the tensor cores (float32, Q = 64;
                                             // NESA_TC=0 selects the FFMA kernel, as float64 plans)
@@ -503,6 +504,8 @@ struct nesa_plan {
     for (auto e : cap_events)
       if (e) cudaEventDestroy(e);
     if (ev_sfine) cudaEventDestroy(ev_sfine);
+    if (w_ev_fork) cudaEventDestroy(w_ev_fork);
+    if (w_ev_near) cudaEventDestroy(w_ev_near);
     if (ev_tfine) cudaEventDestroy(ev_tfine);
     if (s2) cudaStreamDestroy(s2);
     if (ev_fork) cudaEventDestroy(ev_fork);
@@ -1903,7 +1906,8 @@ bool near_wide_ok(const nesa_plan* P) { return P->dtype == NESA_F32 && P->near_t
 
 // phi[:, col0 : col0 + ncols] += near(q) for real columns of (N, ld) blocks in
 // original order, 128 columns per tensor-core pass (stream-ordered)
-void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int ncols, cudaStream_t st) {
+void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int ncols, cudaStream_t st,
+                   bool accumulate = true) {
   require(near_wide_ok(P), "the wide near field needs a float32 plan with tensor cores");
   require(ld >= 1 && col0 >= 0 && ncols >= 1 && col0 + ncols <= ld, "bad column range");
   CUDA_OK(cudaSetDevice(P->device));
@@ -1921,7 +1925,7 @@ void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int
     const int nc = std::min(128, col0 + ncols - c);
     near_tc_kernel<<<grid, 128, near_tc_smem_bytes(), st>>>(
         P->ntc_items.p, P->ntc_n, P->ntc_src.p, P->ntc_blob.p, static_cast<const float*>(q), ld, c, nc,
-        P->perm.p, static_cast<float*>(phi));
+        P->perm.p, static_cast<float*>(phi), accumulate ? 1 : 0);
     CUDA_OK(cudaGetLastError());
   }
 }
@@ -1929,20 +1933,36 @@ void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int
 // Far field of real columns [col0, col0 + ncols) (ncols <= kWCols) of
 // (N, ld) row-major blocks in original order as batched GEMMs (wgemm_kernel):
 // phi[:, cols] = far field (stored, not accumulated).  Stream-ordered.
+template <typename T, int NC, int KG>
+void launch_wgemm(const WArgs<T>& a, int mode, int64_t n, cudaStream_t st) {
+  using W = WTile<T, NC, KG>;
+  static bool attr = false;
+  if (!attr) {
+    for (auto* f : {wgemm_kernel<T, kWStore, NC, KG>, wgemm_kernel<T, kWScatter, NC, KG>,
+                    wgemm_kernel<T, kWScatterAdd, NC, KG>})
+      CUDA_OK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(W::kSmem)));
+    attr = true;
+  }
+  const dim3 grid(unsigned(n), kWCols / NC);
+  if (mode == kWStore)
+    wgemm_kernel<T, kWStore, NC, KG><<<grid, kWThreads, W::kSmem, st>>>(a);
+  else if (mode == kWScatter)
+    wgemm_kernel<T, kWScatter, NC, KG><<<grid, kWThreads, W::kSmem, st>>>(a);
+  else
+    wgemm_kernel<T, kWScatterAdd, NC, KG><<<grid, kWThreads, W::kSmem, st>>>(a);
+  CUDA_OK(cudaGetLastError());
+}
+
 template <typename T>
-void run_far_wide_T(nesa_plan* P, const void* q, void* phi, int ld, int col0, int ncols, cudaStream_t st) {
+void run_far_wide_T(nesa_plan* P, const void* q, void* phi, int ld, int col0, int ncols, cudaStream_t st,
+                    bool reception, bool rec_add) {
   const size_t es = sizeof(T);
-  if (!P->w_qt.p) {
-    P->w_qt.alloc(size_t(P->N) * kWCols * es);
+  if (!P->w_s.p) {
     P->w_s.alloc(size_t(P->G) * P->Q * kWCols * es);
     P->w_o.alloc(size_t(P->G) * P->Q * kWCols * es);
   }
-  T* qt = reinterpret_cast<T*>(P->w_qt.p);
   T* s = reinterpret_cast<T*>(P->w_s.p);
   T* o = reinterpret_cast<T*>(P->w_o.p);
-  wgather_kernel<T><<<grid_for(P->N * kWCols, 256, 8 * P->n_sm), 256, 0, st>>>(
-      static_cast<const T*>(q), ld, col0, ncols, P->perm.p, P->N, qt);
-  CUDA_OK(cudaGetLastError());
   WArgs<T> a{};
   a.terms = P->w_terms.p;
   a.abase[0] = reinterpret_cast<const T*>(P->CT.p);
@@ -1950,25 +1970,28 @@ void run_far_wide_T(nesa_plan* P, const void* q, void* phi, int ld, int col0, in
   a.abase[2] = reinterpret_cast<const T*>(P->DT.p);
   a.abase[3] = reinterpret_cast<const T*>(P->Vset.blob.p);
   a.abase[4] = reinterpret_cast<const T*>(P->Uset.blob.p);
-  a.xs[0] = qt;
+  a.xs[0] = nullptr;
   a.xs[1] = s;
   a.xs[2] = o;
   a.perm = P->perm.p;
+  a.q = static_cast<const T*>(q);
   a.ldy = ld;
   a.col0 = col0;
   a.ncols = ncols;
+  a.vec4 = (size_t(ld) * es) % 16 == 0 && (size_t(col0) * es) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(q) % 16 == 0;
   for (const auto& S : P->w_stages) {
-    if (S.end <= S.begin) continue;
+    if (S.end <= S.begin || (S.ysel == 2) != reception) continue;
     a.items = P->w_items.p + S.begin;
-    const unsigned grid = unsigned(S.end - S.begin);
-    if (S.ysel == 2) {
-      a.y = static_cast<T*>(phi);
-      wgemm_kernel<T, true><<<grid, kWThreads, 0, st>>>(a);
-    } else {
-      a.y = S.ysel == 0 ? s : o;
-      wgemm_kernel<T, false><<<grid, kWThreads, 0, st>>>(a);
-    }
-    CUDA_OK(cudaGetLastError());
+    a.y = S.ysel == 0 ? s : (S.ysel == 1 ? o : static_cast<T*>(phi));
+    const int mode = S.ysel < 2 ? kWStore : (rec_add ? kWScatterAdd : kWScatter);
+    const int64_t n = S.end - S.begin;
+    // coarse levels (few items, many terms): 32-column blocks, terms split
+    // over 4 thread groups; wide levels: one CTA per 64 x 128 tile
+    if (n < 2 * P->n_sm)
+      launch_wgemm<T, 32, 4>(a, mode, n, st);
+    else
+      launch_wgemm<T, 128, 1>(a, mode, n, st);
   }
 }
 
@@ -1994,17 +2017,32 @@ int run_matvec(nesa_plan* P, const void* q, void* phi, int32_t nrhs, int32_t is_
   require(!(flags & NESA_PROFILE), "profiling takes at most 4 real columns");
   const size_t es = P->esz;
   if ((flags & NESA_FAR) && P->wide_far && P->comm == nullptr && (!(flags & NESA_NEAR) || near_wide_ok(P))) {
-    // many right-hand sides: the far field as batched GEMMs over 128-column
-    // passes (writes phi), then the near field's tensor-core GEMM adds to it
+    // many right-hand sides: the near field's tensor-core GEMM (storing phi)
+    // on a side stream, concurrently with the far field as batched GEMMs
+    // over 128-column passes up to o; the reception then adds U o to phi
     CUDA_OK(cudaSetDevice(P->device));
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool near = (flags & NESA_NEAR) != 0;
+    if (!P->w_ev_fork) {
+      CUDA_OK(cudaEventCreateWithFlags(&P->w_ev_fork, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&P->w_ev_near, cudaEventDisableTiming));
+    }
+    if (near) {
+      CUDA_OK(cudaEventRecord(P->w_ev_fork, st));
+      CUDA_OK(cudaStreamWaitEvent(P->s1, P->w_ev_fork, 0));
+      for (int c0 = 0; c0 < Rt; c0 += kWCols)
+        run_near_wide(P, q, phi, Rt, c0, std::min(kWCols, Rt - c0), P->s1, /*accumulate=*/false);
+      CUDA_OK(cudaEventRecord(P->w_ev_near, P->s1));
+    }
     for (int c0 = 0; c0 < Rt; c0 += kWCols) {
       const int nc = std::min(kWCols, Rt - c0);
-      if (P->dtype == NESA_F64)
-        run_far_wide_T<double>(P, q, phi, Rt, c0, nc, st);
-      else
-        run_far_wide_T<float>(P, q, phi, Rt, c0, nc, st);
-      if (flags & NESA_NEAR) run_near_wide(P, q, phi, Rt, c0, nc, st);
+      for (int part = 0; part < 2; ++part) {
+        if (part == 1 && c0 == 0 && near) CUDA_OK(cudaStreamWaitEvent(st, P->w_ev_near, 0));
+        if (P->dtype == NESA_F64)
+          run_far_wide_T<double>(P, q, phi, Rt, c0, nc, st, part == 1, near);
+        else
+          run_far_wide_T<float>(P, q, phi, Rt, c0, nc, st, part == 1, near);
+      }
     }
     return NESA_OK;
   }
