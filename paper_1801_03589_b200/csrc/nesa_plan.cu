@@ -445,9 +445,13 @@ struct nesa_plan {
   cudaStream_t s0 = nullptr, s1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t s2 = nullptr;                 // fine-level translation branch
-  cudaEvent_t ev_sfine = nullptr, ev_tfine = nullptr;
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
+  // per level (index lv - l0): translation units and translation-sum groups,
+  // so each fine level is translated as soon as its own s is final
+  std::vector<int> tunit_lv_begin, tunit_lv_end;
+  std::vector<int64_t> red_lv_begin, red_lv_end;
+  std::vector<cudaEvent_t> ev_s_lv, ev_t_lv;
   int64_t n_red_fine = 0;                    // red_ids [0, n_red_fine) are fine levels
 
   // One captured graph per (R, flags, stage, ldv).  The caller's q / phi
@@ -503,10 +507,10 @@ struct nesa_plan {
       for (auto e : v) cudaEventDestroy(e);
     for (auto e : cap_events)
       if (e) cudaEventDestroy(e);
-    if (ev_sfine) cudaEventDestroy(ev_sfine);
     if (w_ev_fork) cudaEventDestroy(w_ev_fork);
+    for (auto e : ev_s_lv) cudaEventDestroy(e);
+    for (auto e : ev_t_lv) cudaEventDestroy(e);
     if (w_ev_near) cudaEventDestroy(w_ev_near);
-    if (ev_tfine) cudaEventDestroy(ev_tfine);
     if (s2) cudaStreamDestroy(s2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -774,10 +778,14 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   if (P->fused_lf > P->l0 && P->split_lv <= P->fused_lf) P->split_lv = P->fused_lf + 1;
   {
     std::vector<int32_t> ids;  // fine levels first
+    P->red_lv_begin.assign(size_t(nlev), 0);
+    P->red_lv_end.assign(size_t(nlev), 0);
     for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
+      P->red_lv_begin[size_t(li)] = int64_t(ids.size());
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         ids.push_back(int32_t(g));
+      P->red_lv_end[size_t(li)] = int64_t(ids.size());
       if (lv == P->split_lv) P->n_red_fine = int64_t(ids.size());
     }
     P->n_red = int64_t(ids.size());
@@ -1217,8 +1225,11 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     std::vector<TUnit> units;
     std::vector<std::vector<TEnt>> by_d(size_t(std::max<int64_t>(d->n_dtab, 1)));
     // levels fine -> coarse; within a level grouped by unique D
+    P->tunit_lv_begin.assign(size_t(P->L - P->l0 + 1), 0);
+    P->tunit_lv_end.assign(size_t(P->L - P->l0 + 1), 0);
     for (int lv = P->L; lv >= P->l0; --lv) {
       const int li = lv - P->l0;
+      P->tunit_lv_begin[size_t(li)] = int(units.size());
       std::vector<int64_t> used;
       for (int64_t g = P->loc_first[li]; g < P->loc_first[li] + P->loc_count[li]; ++g)
         for (int64_t e = d->int_ptr[g]; e < d->int_ptr[g + 1]; ++e) {
@@ -1240,6 +1251,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         v.clear();
       }
       if (lv == P->split_lv) P->n_tunits_fine = int(units.size());
+      P->tunit_lv_end[size_t(li)] = int(units.size());
     }
     P->tunits.upload(units);
     P->tents.upload(ents);
@@ -1574,7 +1586,7 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
       if (P->tc) {
         go(tgemm_tc3_kernel<R>, std::min(u1 - u0, kTc3CtasPerSM * P->n_sm), tc2_smem_bytes<R>(), up,
            u1 - u0, (const TEnt*)P->tents.p, (const float*)P->DTC.p, (const float*)s, Y,
-           u0 == 0 ? 44 : 45);  // (ktrace: fine / coarse units)
+           u0 < P->n_tunits_fine ? 44 : 45);  // (ktrace: fine / coarse units)
         nk++;
         tr("translate", st);
         return;
@@ -1677,22 +1689,30 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
   // upward chain, the coarse translations and the coarse downward levels.
   // split: fine translation on the side stream (stage 0); stage 1 / 2 split
   // the product at the halo exchange instead
+  // fine levels: level lv's s is final after the radiation (lv = L) or
+  // after up_level(lv); its translation + translation sums go to s2 right
+  // then, one level at a time, and down_level(lv) waits for its own level
   auto up_pass = [&](bool split) {
     const bool fine = split && P->split_lv <= P->L;
     for (int lv = P->L; lv > P->l0; --lv) {
       if (!wide(lv)) break;
+      if (fine && lv == P->L) CUDA_OK(cudaEventRecord(P->ev_s_lv[size_t(lv - P->l0)], s0));
       up_level(lv);
-      if (fine && lv == P->split_lv) CUDA_OK(cudaEventRecord(P->ev_sfine, s0));
+      if (fine && lv < P->L && lv >= P->split_lv)
+        CUDA_OK(cudaEventRecord(P->ev_s_lv[size_t(lv - P->l0)], s0));
     }
     if (fused) fused_up();
     return fine;
   };
   auto down_pass = [&](bool fine) {
     if (fine) {
-      CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_sfine, 0));
-      translate(0, P->n_tunits_fine, P->s2);
-      reduce(0, P->n_red_fine, P->s2);
-      CUDA_OK(cudaEventRecord(P->ev_tfine, P->s2));
+      for (int lv = P->L; lv >= P->split_lv; --lv) {
+        const size_t li = size_t(lv - P->l0);
+        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[li], 0));
+        translate(P->tunit_lv_begin[li], P->tunit_lv_end[li], P->s2);
+        reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s2);
+        CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s2));
+      }
       translate(P->n_tunits_fine, P->n_tunits, s0);
       reduce(P->n_red_fine, P->n_red, s0);
     } else {
@@ -1700,16 +1720,16 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
       reduce(0, P->n_red, s0);
     }
     if (fused) fused_down();
-    bool joined = !fine;
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
       if (!wide(lv)) continue;
-      if (!joined && lv >= P->split_lv) {
-        CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
-        joined = true;
-      }
+      if (fine && lv >= P->split_lv) CUDA_OK(cudaStreamWaitEvent(s0, P->ev_t_lv[size_t(lv - P->l0)], 0));
       down_level(lv);
     }
-    if (!joined) CUDA_OK(cudaStreamWaitEvent(s0, P->ev_tfine, 0));
+    // s2's work joins s0 (every fine level's event, also when a level had
+    // no down kernel)
+    if (fine)
+      for (int lv = P->split_lv; lv <= P->L; ++lv)
+        CUDA_OK(cudaStreamWaitEvent(s0, P->ev_t_lv[size_t(lv - P->l0)], 0));
   };
   auto gather = [&]() {
     const int32_t* ip = P->iperm.p;
@@ -2293,8 +2313,13 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     CUDA_OK(cudaStreamCreateWithFlags(&P->s0, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&P->s1, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking));
-    CUDA_OK(cudaEventCreateWithFlags(&P->ev_sfine, cudaEventDisableTiming));
-    CUDA_OK(cudaEventCreateWithFlags(&P->ev_tfine, cudaEventDisableTiming));
+    for (int i = 0; i < P->L - P->l0 + 1; ++i) {
+      cudaEvent_t a = nullptr, b = nullptr;
+      CUDA_OK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      P->ev_s_lv.push_back(a);
+      P->ev_t_lv.push_back(b);
+    }
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
     for (auto& e : P->cap_events) CUDA_OK(cudaEventCreate(&e));
