@@ -240,11 +240,16 @@ const char* nesa_last_error(void);
  * elements, float32 or float64) by classical Gram-Schmidt applied twice in
  * three passes over the basis, write v_out = w'' / |w''| and the Hessenberg
  * column hcol[0..kk] (float64 (re, im) pairs: h1 + h2, then |w''|).  work:
- * nesa_gs_work_bytes() bytes of device memory.  Stream-ordered, no host
- * synchronisation, bitwise reproducible; 1 <= kk <= 128. */
+ * nesa_gs_work_bytes() bytes of device memory, zero-filled once before the
+ * first step (it holds self-resetting arrival counters).  Stream-ordered, no
+ * host synchronisation, bitwise reproducible; 1 <= kk <= 128.
+ * nesa_gs_step_shifted first adds shift * V[kk-1] to w (the (shift I + K~)
+ * operator of the solver, fused into the first pass). */
 int64_t nesa_gs_work_bytes(void);
 int nesa_gs_step(const void* basis, int64_t stride, int32_t kk, void* w, void* v_out, int64_t n,
                  int32_t is_f64, void* work, void* hcol, void* stream);
+int nesa_gs_step_shifted(const void* basis, int64_t stride, int32_t kk, void* w, void* v_out, int64_t n,
+                         int32_t is_f64, double shift, void* work, void* hcol, void* stream);
 const char* nesa_gs_last_error(void);
 int nesa_abi_version(void);
 

@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = (
     "nesa_tree_build", "nesa_tree_error", "nesa_tree_size", "nesa_tree_copy", "nesa_tree_free",
     "nesa_exchange_pack", "nesa_exchange_combine", "nesa_plan_create_dist", "nesa_nccl_unique_id",
     "nesa_nccl_comm_init", "nesa_nccl_comm_destroy", "nesa_matvec_near_wide",
-    "nesa_gs_work_bytes", "nesa_gs_step", "nesa_gs_last_error",
+    "nesa_gs_work_bytes", "nesa_gs_step", "nesa_gs_step_shifted", "nesa_gs_last_error",
 )
 
 _p = ctypes.c_void_p
@@ -169,6 +169,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nesa_gs_step.argtypes = [_p, ctypes.c_int64, ctypes.c_int32, _p, _p, ctypes.c_int64,
                                  ctypes.c_int32, _p, _p, _p]
     lib.nesa_gs_step.restype = ctypes.c_int
+    lib.nesa_gs_step_shifted.argtypes = [_p, ctypes.c_int64, ctypes.c_int32, _p, _p, ctypes.c_int64,
+                                         ctypes.c_int32, ctypes.c_double, _p, _p, _p]
+    lib.nesa_gs_step_shifted.restype = ctypes.c_int
     lib.nesa_gs_last_error.argtypes = []
     lib.nesa_gs_last_error.restype = ctypes.c_char_p
     if lib.nesa_abi_version() != NESA_ABI_VERSION:

@@ -56,7 +56,7 @@ def _givens(a: complex, b: complex):
 
 
 def _arnoldi_fused(A, V, H, cs, sn, g, k_max, bnorm, done, tol, history, iters, maxiter, w_buf,
-                   gs_work, lib, stream, is_f64):
+                   gs_work, lib, stream, is_f64, shift=0.0):
     """One restart cycle for one complex column: products and CGS2 steps on
     the device (nesa_gs_step), Givens rotations on the host one iteration
     behind.  Returns the number of basis columns to use."""
@@ -70,9 +70,10 @@ def _arnoldi_fused(A, V, H, cs, sn, g, k_max, bnorm, done, tol, history, iters, 
     evs = [torch.cuda.Event() for _ in range(k_max)]
 
     def launch(k):
-        A(V[k], w_buf)
-        rc = lib.nesa_gs_step(V.data_ptr(), stride, k + 1, w_buf.data_ptr(), V[k + 1].data_ptr(), n,
-                              int(is_f64), gs_work.data_ptr(), hdev[k].data_ptr(), stream.cuda_stream)
+        A(V[k], w_buf, with_shift=False)  # the shift is added inside the first GS pass
+        rc = lib.nesa_gs_step_shifted(V.data_ptr(), stride, k + 1, w_buf.data_ptr(), V[k + 1].data_ptr(),
+                                      n, int(is_f64), float(shift), gs_work.data_ptr(), hdev[k].data_ptr(),
+                                      stream.cuda_stream)
         if rc:
             raise RuntimeError(lib.nesa_gs_last_error().decode())
         hhost[k].copy_(hdev[k], non_blocking=True)
@@ -142,10 +143,10 @@ def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40
     plan = get_plan(t, ops, dtype="f32" if single else "f64", device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def A(X, Y=None):
+    def A(X, Y=None, with_shift=True):
         Y = torch.empty_like(X) if Y is None else Y
         plan.matvec_ptr(X.data_ptr(), Y.data_ptr(), m, is_complex, stream=stream.cuda_stream)
-        if shift:
+        if shift and with_shift:
             Y.add_(X, alpha=shift)
         return Y
 
@@ -155,7 +156,7 @@ def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40
     if fused:
         from . import _capi
         lib = _capi.load()
-        gs_work = torch.empty(int(lib.nesa_gs_work_bytes()), dtype=torch.uint8, device=B.device)
+        gs_work = torch.zeros(int(lib.nesa_gs_work_bytes()), dtype=torch.uint8, device=B.device)
         w_buf = torch.empty_like(B)
 
     def cnorm(X):                      # per-column 2-norms, float64 on host
@@ -194,7 +195,7 @@ def gmres(tree, ops, b, shift: float = 0.0, tol: float = 1e-6, restart: int = 40
         if fused:
             k_used, launched = _arnoldi_fused(A, V, H, cs, sn, g, k_max, bnorm, done, tol, history,
                                               iters, maxiter, w_buf, gs_work, lib, stream,
-                                              is_f64=not single)
+                                              is_f64=not single, shift=shift)
             iters += launched
         for k in range(0 if not fused else k_max, k_max):
             W = A(V[k])

@@ -647,7 +647,7 @@ def test_fused_gram_schmidt_step(dt, kk, tol):
     V = torch.zeros((kk + 1, n), dtype=dt, device="cuda")
     V[:kk] = torch.from_numpy(Vh).to(V)
     w = torch.from_numpy(wh).to("cuda", dt)
-    work = torch.empty(int(lib.nesa_gs_work_bytes()), dtype=torch.uint8, device="cuda")
+    work = torch.zeros(int(lib.nesa_gs_work_bytes()), dtype=torch.uint8, device="cuda")
     hcol = torch.zeros(2 * (kk + 1), dtype=torch.float64, device="cuda")
     stride = (V[1].data_ptr() - V[0].data_ptr()) // (V.element_size() // 2)
     rc = lib.nesa_gs_step(V.data_ptr(), stride, kk, w.data_ptr(), V[kk].data_ptr(), n,
