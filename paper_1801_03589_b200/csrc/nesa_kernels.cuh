@@ -2974,7 +2974,7 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
 // ----------------------------------------------------------------------------
 // Near field for many right-hand sides on the tensor cores (float32 plans;
 // C5: 64 plane waves = 128 real columns).  phi[perm p] += sum_j K_pj q_j for
-// up to 128 real columns at once.  An item = <= 256 target rows of a leaf
+// up to 128 real columns at once.  An item = <= 128 target rows of a leaf
 // (padded to N = 16 k) against the leaf's near slab (W source points).  The
 // MMA computes D (128 x N) = X^T (128 x W) K^T (W x N): M = the right-hand-side
 // columns, so one tile covers 128 columns and the operator is streamed ONCE
@@ -2997,7 +2997,7 @@ struct NearTcItem {
   int32_t ld, r0;     // packing: leading dimension and first row within the block item
 };
 constexpr int kNearTcK = 32;
-constexpr int kNearTcMaxN = 256;
+constexpr int kNearTcMaxN = 128;  // target rows per item: 256 TMEM columns, two CTAs per SM
 constexpr uint32_t kNearTcSBO = kNearTcK * 8 * 4;  // bytes between 8-row groups of a chunk
 
 // column-major near blob -> per-item canonical tf32 hi | lo chunks
@@ -3046,7 +3046,7 @@ constexpr size_t near_tc_smem_bytes() {
   return size_t(2) * 2 * kNearTcMaxN * kNearTcK * 4 + 64;
 }
 
-__global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __restrict__ items, int n_items,
+__global__ void __launch_bounds__(128, 2) near_tc_kernel(const NearTcItem* __restrict__ items, int n_items,
                                                          const int32_t* __restrict__ src,
                                                          const float* __restrict__ blob,
                                                          const float* __restrict__ q, int ldq, int c0,
@@ -3060,7 +3060,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
   const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -3123,7 +3123,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
       else if (next_item < n_items)
         load_x(nx, 0, xn);
       wait_mma(slot);  // chunk gc - 2 released this A slot
-      const uint32_t t_hi = tmem + lane_base + 256 + 64 * slot, t_lo = t_hi + 32;
+      const uint32_t t_hi = tmem + lane_base + kNearTcMaxN + 64 * slot, t_lo = t_hi + 32;
 #pragma unroll
       for (int kb = 0; kb < kNearTcK / 4; ++kb)
         tc_put4(t_hi, t_lo, kb, make_float4(x[4 * kb], x[4 * kb + 1], x[4 * kb + 2], x[4 * kb + 3]));
@@ -3137,7 +3137,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
         const uint32_t bl = bh + uint32_t(it.npad) * kNearTcK * 4;
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
-          const uint32_t a0 = tmem + 256 + 64 * slot + (cc == 2 ? 32u : 0u), b0 = cc == 1 ? bl : bh;
+          const uint32_t a0 = tmem + kNearTcMaxN + 64 * slot + (cc == 2 ? 32u : 0u), b0 = cc == 1 ? bl : bh;
 #pragma unroll
           for (int ks = 0; ks < kNearTcK / 8; ++ks)
             umma_tf32_ts_n(tmem, a0 + ks * 8, umma_desc_kmajor_sbo(b0 + ks * 2 * kTcLBO, kNearTcSBO), idesc,
@@ -3183,7 +3183,7 @@ __global__ void __launch_bounds__(128, 1) near_tc_kernel(const NearTcItem* __res
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
 // ----------------------------------------------------------------------------

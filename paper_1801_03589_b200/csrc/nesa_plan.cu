@@ -921,7 +921,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
   if (P->near_tc && !hn.items.empty()) {
-    // tensor-core items: <= 256 target rows each, the slab's source points
+    // tensor-core items: <= 128 target rows each, the slab's source points
     // as original indices (the caller's q is read without a gather)
     std::vector<NearTcItem> ti;
     std::vector<int32_t> src;
@@ -1940,7 +1940,7 @@ void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int
     CUDA_OK(cudaFuncSetAttribute(near_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(near_tc_smem_bytes())));
   }
-  const int grid = std::min(P->ntc_n, P->n_sm);
+  const int grid = std::min(P->ntc_n, 2 * P->n_sm);
   for (int c = col0; c < col0 + ncols; c += 128) {
     const int nc = std::min(128, col0 + ncols - c);
     near_tc_kernel<<<grid, 128, near_tc_smem_bytes(), st>>>(
