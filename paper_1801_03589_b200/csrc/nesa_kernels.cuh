@@ -3248,11 +3248,12 @@ enum { kWStore = 0, kWScatter = 1, kWScatterAdd = 2 };
 // add their partial tiles in a fixed order at the end.  Wide levels use
 // <128, 1>; the coarse levels -- few groups, many terms each -- <32, 4>,
 // which gives 16x the CTAs and a quarter of the serial chunk chain.
-template <typename T, int NC, int KG>
+template <typename T, int NC, int KG, int TR>
 struct WTile {
   static constexpr int KC = sizeof(T) == 4 ? 16 : 8;  // K chunk
-  static constexpr int GT = kWThreads / KG;           // threads per group
   static constexpr int CG = NC / 8;                   // column groups (8 columns per thread)
+  static constexpr int GT = (kWRows / TR) * CG;       // threads per group (TR rows x 8 columns each)
+  static constexpr int kThreads = GT * KG;
   static constexpr int AV = KC * kWRows / GT;         // A values per thread per chunk
   static constexpr int XV = KC * NC / GT;             // X values per thread per chunk
   static constexpr int kBuf = 2 * KC * (kWRows + NC); // one group's double buffer (elements)
@@ -3260,13 +3261,13 @@ struct WTile {
       sizeof(T) * (size_t(KG) * kBuf > (KG > 1 ? size_t(KG) * kWRows * NC : 0)
                        ? size_t(KG) * kBuf
                        : size_t(KG) * kWRows * NC);
-  static_assert(GT == 16 * CG, "4 x 8 thread tiles cover 64 rows x NC columns");
+  static_assert(kThreads <= 256 && kWRows % TR == 0, "TR x 8 thread tiles cover 64 rows x NC columns");
   static_assert(AV >= 1 && XV >= 4 && XV % 4 == 0, "loader geometry");
 };
 
-template <typename T, int MODE, int NC, int KG>
-__global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant__ WArgs<T> a) {
-  using W = WTile<T, NC, KG>;
+template <typename T, int MODE, int NC, int KG, int TR>
+__global__ void __launch_bounds__(WTile<T, NC, KG, TR>::kThreads) wgemm_kernel(const __grid_constant__ WArgs<T> a) {
+  using W = WTile<T, NC, KG, TR>;
   constexpr int KC = W::KC, AV = W::AV, XV = W::XV, GT = W::GT, CG = W::CG;
   extern __shared__ __align__(16) unsigned char wsm[];
   const int tid = threadIdx.x, grp = tid / GT, lt = tid % GT;
@@ -3334,9 +3335,9 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
 #pragma unroll
     for (int v = 0; v < XV; ++v) Xs(buf, x_k)[x_c + v] = rx[v];
   };
-  T acc[4][8];
+  T acc[TR][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TR; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = T(0);
   // this group's terms: t0 + grp, t0 + grp + KG, ...
@@ -3356,18 +3357,18 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
     if (have) load(t, k0);
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
-      const T* Ap = As(buf, kk) + ty * 4;
+      const T* Ap = As(buf, kk) + ty * TR;
       const T* Xp = Xs(buf, kk) + tx * 4;
-      T av[4], x0[4], x1[4];
+      T av[TR], x0[4], x1[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = Ap[i];
+      for (int i = 0; i < TR; ++i) av[i] = Ap[i];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         x0[j] = Xp[j];
         x1[j] = Xp[NC / 2 + j];
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < TR; ++i) {
         if constexpr (sizeof(T) == 4) {
           ffma2(acc[i][0], acc[i][1], av[i], x0[0], x0[1]);
           ffma2(acc[i][2], acc[i][3], av[i], x0[2], x0[3]);
@@ -3392,14 +3393,14 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
     __syncthreads();
     T* red = reinterpret_cast<T*>(wsm);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TR; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        red[(size_t(grp) * kWRows + ty * 4 + i) * NC + tx * 4 + j] = acc[i][j];
-        red[(size_t(grp) * kWRows + ty * 4 + i) * NC + NC / 2 + tx * 4 + j] = acc[i][4 + j];
+        red[(size_t(grp) * kWRows + ty * TR + i) * NC + tx * 4 + j] = acc[i][j];
+        red[(size_t(grp) * kWRows + ty * TR + i) * NC + NC / 2 + tx * 4 + j] = acc[i][4 + j];
       }
     __syncthreads();
-    for (int e = tid; e < kWRows * NC; e += kWThreads) {
+    for (int e = tid; e < kWRows * NC; e += W::kThreads) {
       const int r = e / NC, c = e - (e / NC) * NC;
       if (r >= it.m) continue;
       T v = red[e];
@@ -3434,8 +3435,8 @@ __global__ void __launch_bounds__(kWThreads) wgemm_kernel(const __grid_constant_
       if (j < ncol_left) y[j] = (MODE == kWScatterAdd ? y[j] : T(0)) + v[j];
   };
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = ty * 4 + i;
+  for (int i = 0; i < TR; ++i) {
+    const int r = ty * TR + i;
     if (r >= it.m) continue;
     if constexpr (MODE == kWStore) {
       T* y = a.y + (it.y_row + r) * kWCols + cb;

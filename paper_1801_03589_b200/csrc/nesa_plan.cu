@@ -1953,23 +1953,23 @@ void run_near_wide(nesa_plan* P, const void* q, void* phi, int ld, int col0, int
 // Far field of real columns [col0, col0 + ncols) (ncols <= kWCols) of
 // (N, ld) row-major blocks in original order as batched GEMMs (wgemm_kernel):
 // phi[:, cols] = far field (stored, not accumulated).  Stream-ordered.
-template <typename T, int NC, int KG>
+template <typename T, int NC, int KG, int TR>
 void launch_wgemm(const WArgs<T>& a, int mode, int64_t n, cudaStream_t st) {
-  using W = WTile<T, NC, KG>;
+  using W = WTile<T, NC, KG, TR>;
   static bool attr = false;
   if (!attr) {
-    for (auto* f : {wgemm_kernel<T, kWStore, NC, KG>, wgemm_kernel<T, kWScatter, NC, KG>,
-                    wgemm_kernel<T, kWScatterAdd, NC, KG>})
+    for (auto* f : {wgemm_kernel<T, kWStore, NC, KG, TR>, wgemm_kernel<T, kWScatter, NC, KG, TR>,
+                    wgemm_kernel<T, kWScatterAdd, NC, KG, TR>})
       CUDA_OK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(W::kSmem)));
     attr = true;
   }
   const dim3 grid(unsigned(n), kWCols / NC);
   if (mode == kWStore)
-    wgemm_kernel<T, kWStore, NC, KG><<<grid, kWThreads, W::kSmem, st>>>(a);
+    wgemm_kernel<T, kWStore, NC, KG, TR><<<grid, W::kThreads, W::kSmem, st>>>(a);
   else if (mode == kWScatter)
-    wgemm_kernel<T, kWScatter, NC, KG><<<grid, kWThreads, W::kSmem, st>>>(a);
+    wgemm_kernel<T, kWScatter, NC, KG, TR><<<grid, W::kThreads, W::kSmem, st>>>(a);
   else
-    wgemm_kernel<T, kWScatterAdd, NC, KG><<<grid, kWThreads, W::kSmem, st>>>(a);
+    wgemm_kernel<T, kWScatterAdd, NC, KG, TR><<<grid, W::kThreads, W::kSmem, st>>>(a);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -2009,9 +2009,9 @@ void run_far_wide_T(nesa_plan* P, const void* q, void* phi, int ld, int col0, in
     // coarse levels (few items, many terms): 32-column blocks, terms split
     // over 4 thread groups; wide levels: one CTA per 64 x 128 tile
     if (n < 2 * P->n_sm)
-      launch_wgemm<T, 32, 4>(a, mode, n, st);
+      launch_wgemm<T, 32, 4, 4>(a, mode, n, st);
     else
-      launch_wgemm<T, 128, 1>(a, mode, n, st);
+      launch_wgemm<T, 128, 1, 8>(a, mode, n, st);
   }
 }
 
