@@ -66,6 +66,8 @@ def parse_args(argv=None):
                     help="reference arm: skip the task-parallel form's timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c128", action="store_true", help="skip the complex128 product timing")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the C5 (64 right-hand sides) and Track B (3D Helmholtz) timings")
     ap.add_argument("--pipe-slots", type=int, default=1,
                     help="compute slots of the pipelined e2e API (independent plans)")
     return ap.parse_args(argv)
@@ -331,6 +333,87 @@ def time_c128(args, tree, tables, q, dev, stream):
     return out
 
 
+def _time_events(fn, steps, stream):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def time_c5(args, dev, stream):
+    """BASELINE configs[4] (2D analog): 200k points (ellipse + plates, seed 4),
+    64 plane-wave right-hand sides = 128 real columns, leaf P = 64, Q = 48,
+    complex64: one product of all 64 columns (near field as one tensor-core
+    GEMM, far field as batched GEMMs over the 128 columns)."""
+    import torch
+    import paper_1801_03589_b200 as nesa
+    from paper_1801_03589_b200.plan import NesaPlan
+    n, P, Qa = 200_000, 64, 48
+    spec = nesa.CurveSpec(kind="ellipse-plates", seed=4)
+    pts = nesa.generate_sources(spec, n)
+    Qm = nesa.plane_wave_rhs(pts, nesa.wavenumber(spec, n), 64).astype(np.complex64)
+    tree = nesa.build_tree(pts, nesa.TreeParams(P=P))
+    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=Qa)), dtype="f32",
+                    device=dev.index, stored_vu=True)
+    qd = torch.from_numpy(np.ascontiguousarray(Qm)).to(dev)
+    phid = torch.empty_like(qd)
+
+    def step():
+        plan.matvec_ptr(qd.data_ptr(), phid.data_ptr(), 64, True, stream=stream.cuda_stream)
+
+    for _ in range(3):
+        step()
+    ms = _time_events(step, 20, stream)
+    out = {"workload": f"C5 2D analog: N={n:,}, seed 4, leaf P={P}, Q={Qa}, 64 plane waves "
+                       "(complex64, 128 real columns)",
+           "ms_per_64rhs_product": ms, "rhs_per_s": 64e3 / ms, "products_64rhs_per_s": 1e3 / ms,
+           "far_field_gemms": plan.stat("far_wide") == 1, "near_tensor_core_gemm": plan.stat("near_wide") == 1}
+    plan.close()
+    del qd, phid
+    torch.cuda.empty_cache()
+    return out
+
+
+def time_track_b(args, dev, stream):
+    """Track B: BASELINE configs[2] literally -- 200k points on the 3D
+    ellipsoid (5, 0.5, 0.5) + two 4 x 1 plates (seed 2), octree leaf P = 48,
+    Q = 48, Helmholtz kernel at 10 points per wavelength, complex operators,
+    complex64 vectors (float32 engine)."""
+    import torch
+    from paper_1801_03589_b200 import helmholtz as hz
+    from paper_1801_03589_b200.plan3 import HelmholtzPlan
+    t0 = time.perf_counter()
+    pts, tree, params, q = hz.track_b_problem("ellipsoid-plates", 200_000, 2, 48, 48)
+    plan = HelmholtzPlan(tree, hz.build_tables3(tree, params), "c64", device=dev.index)
+    build_s = time.perf_counter() - t0
+    qd = torch.from_numpy(q.astype(np.complex64)).to(dev)
+    xr = torch.view_as_real(qd.reshape(-1, 1)).permute(0, 2, 1).contiguous()
+    yr = torch.empty_like(xr)
+
+    def step():
+        plan.matvec_ptr(xr.data_ptr(), yr.data_ptr(), 1, False, stream=stream.cuda_stream)
+
+    for _ in range(3):
+        step()
+    ms = _time_events(step, 50, stream)
+    near_bytes = plan.stat("near_entries") * 4
+    out = {"workload": f"Track B C3: N=200,000 3D ellipsoid+plates, seed 2, octree leaf P=48, Q=48, "
+                       f"Helmholtz k={params.k:.2f}, complex64",
+           "us_per_product": ms * 1e3, "products_per_s": 1e3 / ms,
+           "near_bytes": near_bytes, "near_bytes_per_s_over_product": near_bytes / (ms * 1e-3),
+           "levels": tree.L - tree.l0 + 1, "host_build_s": build_s}
+    plan.close()
+    del qd, xr, yr
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # (our arm)
 # ---------------------------------------------------------------------------
@@ -544,6 +627,11 @@ def run_ours(args):
                       "all_gather of partial source amplitudes, translation + downward pass, "
                       "reception), D2H of the rank's phi; max over ranks"}
 
+    c5 = track_b = None
+    if world == 1 and not args.no_extras:
+        c5 = time_c5(args, dev, stream)
+        track_b = time_track_b(args, dev, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_cpu_baseline(tree, args.n)
@@ -556,6 +644,7 @@ def run_ours(args):
             "dtype": "c64", "data": "synthetic (seeded ellipse+plates geometry, N(0,1) rhs)",
             "config": workload_config(args.n, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "c128": c128,
+            "c5": c5, "track_b": track_b,
             "gpu_launches": plan.stat("kernels_per_matvec") * args.steps,
             "clocks": clocks,
             "matvec_alg_bytes": alg["total"], "matvec_achieved_gbs": matvec_bw,

@@ -55,3 +55,6 @@ def test_bench_json_line_on_gpu():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 200000 * 8 and e["d2h_bytes_per_step"] == 200000 * 8
     assert d["gpu_launches"] == d["steps"] * d["gpu_launches"] // d["steps"] > 0
     assert d["clocks"]["sm_mhz"] > 0 and d["cpu_baseline"]["value"] > 0
+    # the extra configurations: C5 (64 right-hand sides) and Track B (3D Helmholtz)
+    assert d["c5"]["far_field_gemms"] and d["c5"]["ms_per_64rhs_product"] > 0
+    assert d["track_b"]["us_per_product"] > 0
