@@ -1,6 +1,7 @@
 """A/B timing of library builds on the bench workload (C4 product).
 
     python tools/ab.py ab/libA.so ab/libB.so [--rounds 3] [--steps 200]
+    python tools/ab.py lib.so lib.so:NESA_U_TERMS=22     (a spec may add environment settings)
 
 Each round runs every library in a fresh process (NESA_LIB selects it),
 alternating the order, and times `steps` back-to-back products with CUDA
@@ -52,7 +53,11 @@ def main():
     for r in range(a.rounds):
         order = a.libs if r % 2 == 0 else list(reversed(a.libs))
         for lib in order:
-            env = dict(os.environ, NESA_LIB=os.path.abspath(lib))
+            path, _, extra = lib.partition(":")
+            env = dict(os.environ, NESA_LIB=os.path.abspath(path))
+            for kv in filter(None, extra.split(",")):
+                k, _, v = kv.partition("=")
+                env[k] = v
             p = subprocess.run([sys.executable, "-c", CHILD, HERE, str(a.steps)], env=env,
                                capture_output=True, text=True)
             line = [x for x in p.stdout.splitlines() if x.startswith("{")]
