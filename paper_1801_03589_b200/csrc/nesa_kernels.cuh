@@ -3355,8 +3355,11 @@ __global__ void __launch_bounds__(WTile<T, NC, KG, TR>::kThreads) wgemm_kernel(c
     }
     have = t < it.t1;
     if (have) load(t, k0);
+    // row groups entirely past the tile's rows (Q = 48 in a 64-row tile,
+    // the short last panel of a leaf) skip the math -- whole warps for 8-row
+    // thread tiles
 #pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
+    for (int kk = 0; kk < KC && ty * TR < it.m; ++kk) {
       const T* Ap = As(buf, kk) + ty * TR;
       const T* Xp = Xs(buf, kk) + tx * 4;
       T av[TR], x0[4], x1[4];
