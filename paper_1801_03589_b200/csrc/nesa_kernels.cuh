@@ -3262,7 +3262,8 @@ struct WTile {
                        ? size_t(KG) * kBuf
                        : size_t(KG) * kWRows * NC);
   static_assert(kThreads <= 256 && kWRows % TR == 0, "TR x 8 thread tiles cover 64 rows x NC columns");
-  static_assert(AV >= 1 && XV >= 4 && XV % 4 == 0, "loader geometry");
+  static_assert(AV % (16 / sizeof(T)) == 0 && XV >= 4 && XV % 4 == 0 && TR % (16 / sizeof(T)) == 0,
+                "loader geometry (16-byte vectors)");
 };
 
 template <typename T, int MODE, int NC, int KG, int TR>
@@ -3329,11 +3330,28 @@ __global__ void __launch_bounds__(WTile<T, NC, KG, TR>::kThreads) wgemm_kernel(c
       for (int v = 0; v < XV; ++v) rx[v] = T(0);
     }
   };
+  // 16-byte shared accesses throughout (every offset is a multiple of 16 bytes)
+  using V4 = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  constexpr int VW = 16 / int(sizeof(T));  // elements per 16-byte vector
+  auto st16 = [&](T* p, const T* v) {
+    if constexpr (sizeof(T) == 4)
+      *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    else
+      *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  };
+  auto ld16 = [&](const T* p, T* v) {
+    const V4 x = *reinterpret_cast<const V4*>(p);
+    if constexpr (sizeof(T) == 4) {
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+      v[0] = x.x; v[1] = x.y;
+    }
+  };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int v = 0; v < AV; ++v) As(buf, a_k)[a_r + v] = ra[v];
+    for (int v = 0; v < AV; v += VW) st16(As(buf, a_k) + a_r + v, ra + v);
 #pragma unroll
-    for (int v = 0; v < XV; ++v) Xs(buf, x_k)[x_c + v] = rx[v];
+    for (int v = 0; v < XV; v += VW) st16(Xs(buf, x_k) + x_c + v, rx + v);
   };
   T acc[TR][8];
 #pragma unroll
@@ -3364,11 +3382,11 @@ __global__ void __launch_bounds__(WTile<T, NC, KG, TR>::kThreads) wgemm_kernel(c
       const T* Xp = Xs(buf, kk) + tx * 4;
       T av[TR], x0[4], x1[4];
 #pragma unroll
-      for (int i = 0; i < TR; ++i) av[i] = Ap[i];
+      for (int i = 0; i < TR; i += VW) ld16(Ap + i, av + i);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        x0[j] = Xp[j];
-        x1[j] = Xp[NC / 2 + j];
+      for (int j = 0; j < 4; j += VW) {
+        ld16(Xp + j, x0 + j);
+        ld16(Xp + NC / 2 + j, x1 + j);
       }
 #pragma unroll
       for (int i = 0; i < TR; ++i) {
