@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define NESA_ABI_VERSION 2
+#define NESA_ABI_VERSION 3
 
 typedef enum {
   NESA_OK = 0,
@@ -130,6 +130,13 @@ typedef struct nesa_plan_desc {
   int64_t leaf_begin, leaf_end;
 
   uint32_t options;             /* NESA_PLAN_* bits                                 */
+
+  /* NESA_PLAN_HELMHOLTZ_NEAR (Track B): the near blocks are assembled on the
+   * device from the tree-order 3D points (one per complex unknown) and the
+   * wavenumber, G = exp(-j k r) / (4 pi r), zero on the diagonal
+   * (paper_1801_03589_b200.helmholtz.helmholtz_matrix). */
+  const double* points3;        /* [N/2 * 3] with the real embedding's doubled N    */
+  double wavenumber;
 } nesa_plan_desc;
 
 /* nesa_plan_desc.options */
@@ -154,6 +161,9 @@ typedef struct nesa_plan_desc {
                                    columns then run the far field as batched GEMMs over 128-column
                                    passes (C5: many right-hand sides), float32 adds the near field
                                    as one tensor-core GEMM per pass (nesa_matvec_near_wide) */
+#define NESA_PLAN_HELMHOLTZ_NEAR 16u /* with NESA_PLAN_OCTREE | NESA_PLAN_COMPLEX_NEAR: near_blob may be
+                                   NULL; the row-split complex near blocks are evaluated on the
+                                   device from points3 / wavenumber (float64, stored in op_dtype) */
 
 int nesa_plan_create(const nesa_plan_desc* desc, int device, nesa_plan** out);
 

@@ -12,11 +12,12 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("NESA_LIB") or os.path.join(_HERE, "libnesa_b200.so")  # NESA_LIB: A/B builds
 
-NESA_ABI_VERSION = 2
+NESA_ABI_VERSION = 3
 NESA_PLAN_FAR_ONLY = 1
 NESA_PLAN_OCTREE = 2
 NESA_PLAN_COMPLEX_NEAR = 4
 NESA_PLAN_STORED_VU = 8
+NESA_PLAN_HELMHOLTZ_NEAR = 16
 NESA_OK = 0
 NESA_ERR_INVALID = 1
 NESA_ERR_CUDA = 2
@@ -72,6 +73,7 @@ class NesaPlanDesc(ctypes.Structure):
         ("check_cos", _f64p), ("check_sin", _f64p), ("aux_cos", _f64p), ("aux_sin", _f64p),
         ("leaf_begin", ctypes.c_int64), ("leaf_end", ctypes.c_int64),
         ("options", ctypes.c_uint32),
+        ("points3", _f64p), ("wavenumber", ctypes.c_double),
     ]
 
 

@@ -264,6 +264,41 @@ __global__ void assemble_near_kernel(const BlockItem* items, const BlockSeg* seg
   }
 }
 
+// Track B near blocks, row-split complex (NESA_PLAN_HELMHOLTZ_NEAR): item
+// rows 2r / 2r+1 = Re / Im of G(x_i, x_j) = exp(-j k r) / (4 pi r) for the
+// complex target row r (point i = y_row0 + r) and source column c (point j
+// from the item's segments); zero for i == j (helmholtz.helmholtz_matrix).
+template <typename T>
+__global__ void assemble_near_helm_kernel(const BlockItem* items, const BlockSeg* segs,
+                                          const double* pts3, double k, T* blob) {
+  const BlockItem it = items[blockIdx.x];
+  const int mc = it.m / 2;  // complex rows
+  const double inv4pi = 1.0 / (4.0 * 3.14159265358979323846);
+  for (int sg = it.seg_begin; sg < it.seg_begin + it.seg_count; ++sg) {
+    const BlockSeg S = segs[sg];
+    const int scol1 = (sg + 1 < it.seg_begin + it.seg_count) ? segs[sg + 1].col0 : it.n;
+    const int64_t cnt = int64_t(scol1 - S.col0) * mc;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int c = S.col0 + int(e / mc), r = int(e % mc);
+      const int64_t i = it.y_row0 + r, j = S.x_row0 + (c - S.col0);
+      double re = 0.0, im = 0.0;
+      if (i != j) {
+        const double dx = __dsub_rn(pts3[3 * i], pts3[3 * j]);
+        const double dy = __dsub_rn(pts3[3 * i + 1], pts3[3 * j + 1]);
+        const double dz = __dsub_rn(pts3[3 * i + 2], pts3[3 * j + 2]);
+        const double d = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        double sn, cs;
+        sincos(k * d, &sn, &cs);
+        const double a = inv4pi / d;
+        re = cs * a;
+        im = -sn * a;
+      }
+      blob[it.a_off + int64_t(c) * it.ld + 2 * r] = T(re);
+      blob[it.a_off + int64_t(c) * it.ld + 2 * r + 1] = T(im);
+    }
+  }
+}
+
 // V_b = fit @ K(out_check_b, pts_b): item m = Q rows, n = n_b columns.
 template <typename T>
 __global__ void assemble_V_kernel(const BlockItem* items, const int64_t* item_leaf,
@@ -1036,7 +1071,8 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
 
   // ---- fill the blobs: from host operators or assembled on the device
   DevBuf<double> pts;
-  const bool need_geom = !d->near_blob || !d->V_blob || !d->U_blob;
+  const bool helm_near = !d->near_blob && (d->options & NESA_PLAN_HELMHOLTZ_NEAR);
+  const bool need_geom = (!d->near_blob && !helm_near) || !d->V_blob || !d->U_blob;
   if (need_geom) {
     require(d->points_tree && d->leaf_center && d->leaf_r_check && d->leaf_r_inaux &&
                 d->out_fit_leaf && d->check_cos && d->check_sin && d->aux_cos && d->aux_sin,
@@ -1048,6 +1084,15 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   T* ublob = reinterpret_cast<T*>(P->Uset.blob.p);
   if (d->near_blob) {
     upload_host_blob<T>(P->nearset, hn, d->near_blob, near_src_off, near_src_rows, near_row0);
+  } else if (helm_near) {
+    if (!hn.items.empty()) {
+      DevBuf<double> p3;
+      p3.upload(std::vector<double>(d->points3, d->points3 + 3 * (P->N / 2)));
+      assemble_near_helm_kernel<T><<<int(hn.items.size()), 256>>>(P->nearset.items.p, P->nearset.segs.p, p3.p,
+                                                                  d->wavenumber, nblob);
+      CUDA_OK(cudaGetLastError());
+      CUDA_OK(cudaDeviceSynchronize());
+    }
   } else if (!hn.items.empty()) {
     assemble_near_kernel<T><<<int(hn.items.size()), 256>>>(P->nearset.items.p, P->nearset.segs.p,
                                                             pts.p, nblob);
@@ -2280,12 +2325,15 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
       P->nkind = 8;
       P->tc = false;
       P->wide_level = std::numeric_limits<int64_t>::max();
-      require(d->V_blob && d->U_blob && (d->near_blob || P->far_only),
-              "octree plans take their near / V / U blocks from the host");
+      require(d->V_blob && d->U_blob &&
+                  (d->near_blob || P->far_only ||
+                   ((d->options & NESA_PLAN_HELMHOLTZ_NEAR) && (d->options & NESA_PLAN_COMPLEX_NEAR) && d->points3)),
+              "octree plans take their near (or NESA_PLAN_HELMHOLTZ_NEAR points) / V / U blocks from the host");
     }
     P->cnear = (d->options & NESA_PLAN_COMPLEX_NEAR) != 0;
     if (P->cnear) {
-      require(d->near_blob && !P->far_only, "NESA_PLAN_COMPLEX_NEAR needs a near blob");
+      require((d->near_blob || ((d->options & NESA_PLAN_HELMHOLTZ_NEAR) && d->points3)) && !P->far_only,
+              "NESA_PLAN_COMPLEX_NEAR needs a near blob or NESA_PLAN_HELMHOLTZ_NEAR points");
       for (int64_t g = 0; g < d->n_leaves; ++g)
         require(d->group_start[g] % 2 == 0 && d->group_stop[g] % 2 == 0,
                 "NESA_PLAN_COMPLEX_NEAR needs embedded (even) point ranges");

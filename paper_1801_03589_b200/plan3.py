@@ -84,7 +84,10 @@ class HelmholtzPlan(NesaPlan):
     """Device plan of one (octree, Helmholtz operators, precision) triple.
 
     ops: HelmholtzParams (tables built here), HelmholtzTables, or a
-    HelmholtzOperatorSet (build_all3 dicts, uploaded as they are).
+    HelmholtzOperatorSet (build_all3 dicts, uploaded as they are).  From
+    params / tables the near blocks are evaluated on the device
+    (NESA_PLAN_HELMHOLTZ_NEAR); V / U (through the pinv fits) come from the
+    host.
     dtype: "c128" (float64 engine) or "c64" (float32 engine).
     """
 
@@ -115,14 +118,17 @@ class HelmholtzPlan(NesaPlan):
             params = t.params
             C, B, D, dindex, octant = t.C, t.B, t.D, t.d_index, t.octant
             V, U = t.V, t.U
-            near_of = lambda g, b: near_block3(tree, g, b, params.k)  # noqa: E731
+            near_of = None   # assembled on the device (NESA_PLAN_HELMHOLTZ_NEAR)
         self.params: HelmholtzParams = params
         Q = params.Q
+        if near_of is None and not complex_near:
+            near_of = lambda g, b: near_block3(tree, g, b, params.k)  # noqa: E731
         near, Vb, Ub = [], [], []
         for g in range(nl):
-            nb = a.nbr_idx[a.nbr_ptr[g]:a.nbr_ptr[g + 1]].tolist()
-            slab = np.hstack([near_of(g, b) for b in nb])
-            near.append((row_split(slab) if complex_near else embed(slab)).ravel(order="F"))
+            if near_of is not None:
+                nb = a.nbr_idx[a.nbr_ptr[g]:a.nbr_ptr[g + 1]].tolist()
+                slab = np.hstack([near_of(g, b) for b in nb])
+                near.append((row_split(slab) if complex_near else embed(slab)).ravel(order="F"))
             Vb.append(embed(V[g]).ravel(order="F"))
             Ub.append(embed(U[g]).ravel(order="F"))
         keep = {}
@@ -158,10 +164,16 @@ class HelmholtzPlan(NesaPlan):
         d.B = _ptr(arr("B", embed(B.reshape(-1, Q, Q)) if B.size else np.zeros(1), np.float64), f64)
         d.D = _ptr(arr("D", embed(D) if D.size else np.zeros(1), np.float64), f64)
         d.n_dtab = D.shape[0]
-        d.near_blob = _ptr(arr("near", np.concatenate(near), np.float64), f64)
+        if near:
+            d.near_blob = _ptr(arr("near", np.concatenate(near), np.float64), f64)
+        else:
+            # near blocks evaluated on the device from the 3D points
+            d.points3 = _ptr(arr("pts3", tree.points, np.float64), f64)
+            d.wavenumber = float(params.k)
         d.V_blob = _ptr(arr("V", np.concatenate(Vb), np.float64), f64)
         d.U_blob = _ptr(arr("U", np.concatenate(Ub), np.float64), f64)
-        d.options = _capi.NESA_PLAN_OCTREE | (_capi.NESA_PLAN_COMPLEX_NEAR if complex_near else 0)
+        d.options = _capi.NESA_PLAN_OCTREE | (_capi.NESA_PLAN_COMPLEX_NEAR if complex_near else 0) | \
+            (0 if near else _capi.NESA_PLAN_HELMHOLTZ_NEAR)
         self.complex_near = complex_near
         h = ctypes.c_void_p()
         _capi.check(self.lib.nesa_plan_create(ctypes.byref(d), self.device, ctypes.byref(h)))
