@@ -1383,6 +1383,7 @@ void set_smem_attrs() {
   attr(tgemm_kernel<T, R>, lim);
   attr(tgemm_wt_kernel<T, R, 64>, lim);
   attr(tgemm_wt_kernel<T, R, 32>, lim);
+  if constexpr (TGW<T, R, 128>::SMEM <= 220 * 1024) attr(tgemm_wt_kernel<T, R, 128>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlUpLeaf>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlUpSum>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDown>, lim);
@@ -1642,6 +1643,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
          (const T*)s, Y);
     else if (Q == 32)
       go(tgemm_wt_kernel<T, R, 32>, u1 - u0, TGW<T, R, 32>::SMEM, up, (const TEnt*)P->tents.p, DTp,
+         (const T*)s, Y);
+    else if (Q == 128 && TGW<T, R, 128>::SMEM <= 220 * 1024)
+      // (Track B's complex Q = 64 in the real embedding, or a real Q = 128)
+      go(tgemm_wt_kernel<T, R, 128>, u1 - u0, TGW<T, R, 128>::SMEM, up, (const TEnt*)P->tents.p, DTp,
          (const T*)s, Y);
     else
       tgemm_kernel<T, R><<<u1 - u0, kTGThreads, tgemm_smem_bytes<T, R>(Q), st>>>(up, P->tents.p, DTp, s,

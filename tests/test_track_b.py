@@ -247,3 +247,20 @@ def test_track_b_c3_gpu_vs_oracle():
         err = rel_l2(plan.matvec(qq), ref)
         plan.close()
         assert err <= tol, (dt, err)
+
+
+@pytest.mark.gpu
+def test_track_b_gpu_q64_embedded_128():
+    # Q = 64 complex = 128 in the real embedding: the warp-tiled translation
+    # kernel at Q = 128 (the literal C4's operator size) against the oracle
+    _gpu()
+    from paper_1801_03589_b200.plan3 import HelmholtzPlan
+    pts, tree, params, q = hz.track_b_problem("sphere", 20000, 1, 32, 64)
+    tables = hz.build_tables3(tree, params)
+    ref = oracle_mvp(tree, hz.build_all3(tree, params, tables), q)
+    for dt, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        plan = HelmholtzPlan(tree, tables, dt)
+        qq = q if dt == "c128" else q.astype(np.complex64)
+        err = rel_l2(plan.matvec(qq), ref)
+        plan.close()
+        assert err <= tol, (dt, err)
