@@ -1920,12 +1920,18 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     // reception
     prof_mark(P, prof, 2 * NESA_STAGE_TOTAL, s0);
     gather();
-    fork_near();  // (A/B: forking before the radiation is 5 us faster since it takes 50 us)
+    // the radiation from outgoing moments is compute-bound: fork the near
+    // field first (A/B: 5 us faster); stored V blocks stream from HBM like
+    // the near operator, so they go first and the near field streams
+    // beside the latency-bound chain that follows
+    const bool v_first = far && !P->v_mom;
+    if (!v_first) fork_near();
     if (far) {
       prof_mark(P, prof, 2 * NESA_STAGE_FAR, s0);
       nk += launch_radiation<T, R>(P, qt, s, s0);
       tr("radiation", s0);
     }
+    if (v_first) fork_near();
     if (far) {
       const bool fine = up_pass(true);
       down_pass(fine);

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--chrome", default="")
     ap.add_argument("--near", type=int, default=1)
     ap.add_argument("--far", type=int, default=1)
+    ap.add_argument("--dtype", default="f32", help="f32 (complex64) or f64 (complex128)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -37,8 +38,9 @@ def main():
     from paper_1801_03589_b200.plan import NesaPlan
     pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=3), a.n)
     tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
-    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype="f32")
-    q = torch.from_numpy(nesa.random_rhs(a.n, 3).astype(np.complex64)).cuda()
+    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype=a.dtype)
+    cdt = np.complex64 if a.dtype == "f32" else np.complex128
+    q = torch.from_numpy(nesa.random_rhs(a.n, 3).astype(cdt)).cuda()
     phi = torch.empty_like(q)
     st = torch.cuda.current_stream()
     lib = plan.lib
