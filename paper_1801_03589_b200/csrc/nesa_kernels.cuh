@@ -2971,6 +2971,77 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
   }
 }
 
+// float64 plans: the same incoming expansion in float64 (the reference's
+// precision).  Per leaf one warp forms beta_m = sum_k (1/m) e^{-i m theta_k}
+// o_k (beta_0 = -log(r) sum_k o_k) in shared memory, then every lane
+// evaluates phi_j = phi_near_j + Re sum_m beta_m w_j^m for its points; the
+// plan sets the number of terms for a float64 truncation (<= 1e-15 relative
+// at the largest |w|).  Replaces streaming the stored float64 U (1 GB at C4)
+// by ~8 FP64 FMAs per point, term and column.
+template <int R>
+__global__ void __launch_bounds__(32 * kExpWarps) reception_exp64_kernel(
+    const double2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
+    const int64_t* __restrict__ leaf_stop, const double* __restrict__ leaf_r,
+    const double2* __restrict__ E, const double* __restrict__ o, const double* __restrict__ phin,
+    const int64_t* __restrict__ perm, double* __restrict__ phi, int64_t leaf0, int64_t nleaf, int Q, int nt,
+    int ldp) {
+  KtScope kt_(72);
+  extern __shared__ double2 smd[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = nt + 1;
+  double2* beta = smd + size_t(warp) * (size_t(ne) * R + (size_t(Q) * R + 1) / 2);  // [m][rr] (re, -im)
+  double* os = reinterpret_cast<double*>(beta + size_t(ne) * R);
+  const int64_t stride = int64_t(gridDim.x) * kExpWarps;
+  for (int64_t li = int64_t(blockIdx.x) * kExpWarps + warp; li < nleaf; li += stride) {
+    const int64_t leaf = leaf0 + li;
+    const int64_t b = leaf_start[leaf];
+    const int n = int(leaf_stop[leaf] - b);
+    const double r = leaf_r[leaf];
+    for (int t = lane; t < Q * R; t += 32) os[t] = o[leaf * int64_t(Q) * R + t];
+    __syncwarp();
+    const double nlr = -log(r);
+    for (int m = lane; m < ne; m += 32) {
+      double ar[R], ai[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) ar[rr] = ai[rr] = 0.0;
+      for (int k = 0; k < Q; ++k) {
+        const double2 e = __ldg(E + k * ne + m);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const double ok = os[k * R + rr];
+          ar[rr] = fma(e.x, ok, ar[rr]);
+          ai[rr] = fma(e.y, ok, ai[rr]);
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        beta[m * R + rr] = m ? make_double2(ar[rr], -ai[rr]) : make_double2(nlr * ar[rr], 0.0);
+    }
+    __syncwarp();
+    const double inv = 1.0 / r;
+    for (int j = lane; j < n; j += 32) {
+      const double2 p = prel[b + j];
+      const double2 w = make_double2(p.x * inv, p.y * inv);
+      double2 z = w;
+      double acc[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = beta[rr].x;
+      for (int m = 1; m <= nt; ++m) {
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          const double2 bm = beta[m * R + rr];  // (re, -im): Re(beta z) = re z.x - im z.y
+          acc[rr] = fma(bm.x, z.x, fma(bm.y, z.y, acc[rr]));
+        }
+        z = make_double2(z.x * w.x - z.y * w.y, z.x * w.y + z.y * w.x);
+      }
+      const int64_t dst = perm ? perm[b + j] : b + j;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) phi[dst * ldp + rr] = (phin ? phin[(b + j) * R + rr] : 0.0) + acc[rr];
+    }
+    __syncwarp();
+  }
+}
+
 // ----------------------------------------------------------------------------
 // Near field for many right-hand sides on the tensor cores (float32 plans;
 // C5: 64 plane waves = 128 real columns).  phi[perm p] += sum_j K_pj q_j for

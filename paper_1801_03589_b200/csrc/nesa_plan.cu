@@ -436,6 +436,8 @@ struct nesa_plan {
   DevBuf<float> ATC;                        // [hi | lo][64 x 80] canonical tf32 A^ (K = 80)
   DevBuf<int32_t> rad_order;                // local leaves by descending point count
   DevBuf<float2> exp_E;                     // [Q][u_nt + 1]: 1, (1/m) e^{-i m theta_k}
+  DevBuf<double2> mf_prel64, exp_E64;       // float64 plans: the same inputs in float64
+  DevBuf<double> mf_leaf_r64;
   // many right-hand sides: the far field as batched GEMMs over up to 128
   // columns (wgemm_kernel; plans with stored V and U)
   struct WStage {
@@ -833,7 +835,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
                       d->out_fit_leaf && d->check_cos && d->check_sin && d->aux_cos && d->aux_sin;
     const bool f32 = std::is_same<T, float>::value;
     P->v_mom = P->v_mom && f32 && !d->V_blob && geom;
-    P->u_mf = P->u_mf && f32 && !d->U_blob && geom;
+    P->u_mf = P->u_mf && !d->U_blob && geom;
     if (P->v_mom || P->u_mf) {
       double rv = 0, ru = 0;
       for (int64_t a = lb; a < le; ++a) {
@@ -853,7 +855,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       if (rv >= 0.9) P->v_mom = false;  // stored V for (non-quadtree) geometry this far out
       if (ru >= 0.9) P->u_mf = false;
       P->v_nm = terms(rv, 1e-9) + 1;     // V: the fit amplifies truncation; keep a margin
-      P->u_nt = terms(ru, 1e-8);
+      P->u_nt = terms(ru, f32 ? 1e-8 : 1e-15);  // float64: truncation below its rounding
       if (const char* e = std::getenv("NESA_V_MOMENTS")) P->v_nm = std::max(2, std::atoi(e));
       if (const char* e = std::getenv("NESA_U_TERMS")) P->u_nt = std::max(1, std::atoi(e));
     }
@@ -1133,6 +1135,18 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       }
     }
     P->mf_prel.upload(prel);
+    if (!std::is_same<T, float>::value && P->u_mf) {
+      std::vector<double2> p64(static_cast<size_t>(P->N));
+      std::vector<double> r64(static_cast<size_t>(NL));
+      for (int64_t a = 0; a < NL; ++a) {
+        const double cx = d->leaf_center[2 * a], cy = d->leaf_center[2 * a + 1];
+        r64[a] = d->leaf_r_inaux[a];
+        for (int64_t i = d->group_start[a]; i < d->group_stop[a]; ++i)
+          p64[i] = double2{d->points_tree[2 * i] - cx, d->points_tree[2 * i + 1] - cy};
+      }
+      P->mf_prel64.upload(p64);
+      P->mf_leaf_r64.upload(r64);
+    }
     P->gstart.upload(std::vector<int64_t>(d->group_start, d->group_start + NL));
     P->gstop.upload(std::vector<int64_t>(d->group_stop, d->group_stop + NL));
     P->mf_leaf_r.upload(lr);
@@ -1199,6 +1213,16 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
           E[size_t(k) * ne + m] = float2{float(std::cos(m * th) / m), float(-std::sin(m * th) / m)};
       }
       P->exp_E.upload(E);
+      if (!std::is_same<T, float>::value) {
+        std::vector<double2> E64(size_t(Q) * ne);
+        for (int k = 0; k < Q; ++k) {
+          const double th = std::atan2(d->aux_sin[k], d->aux_cos[k]);
+          E64[size_t(k) * ne] = double2{1.0, 0.0};
+          for (int m = 1; m <= P->u_nt; ++m)
+            E64[size_t(k) * ne + m] = double2{std::cos(m * th) / m, -std::sin(m * th) / m};
+        }
+        P->exp_E64.upload(E64);
+      }
       // Q = 64 with tensor cores: beta^ = E^ o for all leaves as one GEMM;
       // E^ rows 0 -> 1 (sum of o), 2m-1 / 2m -> Re / Im of (1/m) e^{-i m theta_k}
       if (Q == 64 && P->tc && 2 * P->u_nt + 1 <= 64) {
@@ -1834,6 +1858,26 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
               q, phi);
         }
         nk++;
+      } else {
+        // float64: the expansion in float64 (reception_exp64_kernel)
+        const int64_t nleaf = P->leaf_end - P->leaf_begin;
+        const int grid = int(std::max<int64_t>(
+            1, std::min<int64_t>((nleaf + kExpWarps - 1) / kExpWarps, int64_t(kExpCtasPerSM) * P->n_sm)));
+        const int nt = P->u_nt;
+        const size_t sm = size_t(kExpWarps) * (size_t(nt + 1) * R + (size_t(Q) * R + 1) / 2) * sizeof(double2);
+        const double2* prel = P->mf_prel64.p;
+        const int64_t *gs = P->gstart.p, *ge = P->gstop.p;
+        const double* lr = P->mf_leaf_r64.p;
+        const double2* E = P->exp_E64.p;
+        const int64_t lb = P->leaf_begin;
+        io_launch(
+            P, reception_exp64_kernel<R>, grid, 32 * kExpWarps, sm, s0,
+            [=](const void*, void* pp) {
+              return std::make_tuple(prel, gs, ge, lr, E, (const double*)o, (const double*)base, pm,
+                                     static_cast<double*>(pp), lb, nleaf, Q, nt, ldv);
+            },
+            q, phi);
+        nk++;
       }
     } else if (far) {
       const DevBlockSet& U = P->Uset;
@@ -2314,7 +2358,7 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     P->G = d->n_groups;
     if (const char* wl = std::getenv("NESA_WIDE_LEVEL")) P->wide_level = std::atoll(wl);
     if (const char* tc = std::getenv("NESA_TC")) P->tc = std::atoi(tc) != 0;
-    P->u_mf = d->op_dtype == NESA_F32 && !d->U_blob;
+    P->u_mf = !d->U_blob;
     if (const char* us = std::getenv("NESA_U_STORED")) P->u_mf = P->u_mf && std::atoi(us) == 0;
     P->v_mom = d->op_dtype == NESA_F32 && !d->V_blob;
     if (const char* vs = std::getenv("NESA_V_STORED")) P->v_mom = P->v_mom && std::atoi(vs) == 0;

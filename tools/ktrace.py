@@ -19,7 +19,7 @@ TAGS = {2: "scatter", 3: "gather (original order)", 10: "blockgemv(store: near)"
         30: "fused_up", 31: "fused_down", 33: "reduce", 40: "tgemm",
         41: "tgemm_wt (FFMA)", 43: "tgemm_tc2 (tcgen05, A in TMEM)", 44: "tgemm_tc3 (fine units)", 45: "tgemm_tc3 (coarse units)", 50: "level_wt up-leaf",
         51: "level_wt up-sum", 52: "level_wt down", 54: "level_wt down + beta (leaf)", 60: "radiation moments (in-kernel A)", 62: "radiation (tcgen05 moment map)",
-        70: "reception series", 71: "reception series (beta in)", 80: "level_tc up-leaf", 81: "level_tc up-sum",
+        70: "reception series", 71: "reception series (beta in)", 72: "reception series (float64)", 80: "level_tc up-leaf", 81: "level_tc up-sum",
         82: "level_tc down", 84: "level_tc down + beta (leaf)"}
 
 
