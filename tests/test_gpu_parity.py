@@ -165,10 +165,12 @@ def test_plan_stats(golden):
     assert 8 <= plan.stat("v_moments") <= 96 and 4 <= plan.stat("u_terms") <= 96
     assert plan.stat("d_refs") == int(a.int_ptr[-1])
     plan.close()
+    # float64 plans: stored V (the pinv fit on the host), reception through
+    # the incoming expansion in float64 (more terms than float32)
     plan = NesaPlan(tree, params, dtype="f64")
     assert plan.stat("v_entries") == tree.n_points * params.Q
-    assert plan.stat("u_entries") == tree.n_points * params.Q
-    assert plan.stat("v_moments") == 0 and plan.stat("u_terms") == 0
+    assert plan.stat("u_entries") == 0 and plan.stat("v_moments") == 0
+    assert plan.stat("u_terms") > 4 and plan.stat("u_terms") <= 96
     plan.close()
 
 
