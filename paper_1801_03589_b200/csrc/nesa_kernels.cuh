@@ -2055,6 +2055,13 @@ __global__ void __launch_bounds__(128) level_wt_kernel(const LevelArgs<T, R> a, 
             if (k < kr[b].y)
 #pragma unroll
               for (int i = 0; i < 4; ++i) v[i] += t[b][k][i];
+          // octree parents: children 5..8, in order after the preloaded four
+          for (int k = 4; k < kr[b].y; ++k) {
+            T u[4];
+            ld4(a.Tin + (int64_t(kr[b].x) + k) * W::QR + w, u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] += u[i];
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             a.s[cid[b] * W::QR + w + i] = v[i];

@@ -755,8 +755,13 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   P->fused_lf = P->l0;
   if (P->fused) {
     for (int lv = P->l0 + 1; lv <= P->L; ++lv) {
-      const bool wide = Q == 64 && P->loc_count[lv - P->l0] >= P->wide_level;
-      if (wide || P->loc_count[lv - P->l0] == 0) break;
+      // warp-tiled level kernels: Q = 64, and Q = 128 when their shared
+      // memory fits (float32: Track B's embedded complex Q = 64)
+      const bool wide_q = Q == 64 || (Q == 128 && LVW<T, 4, 128, kLvlDown>::SMEM <= 220 * 1024);
+      const bool wide = wide_q && P->loc_count[lv - P->l0] >= P->wide_level;
+      // level l0 + 1 always stays fused: the fused up kernel also forms the
+      // top level's sums (no per-level kernel does)
+      if ((wide && lv > P->l0 + 1) || P->loc_count[lv - P->l0] == 0) break;
       P->fused_lf = lv;
     }
   }
@@ -1412,11 +1417,16 @@ void set_smem_attrs() {
   attr(level_wt_kernel<T, R, 64, kLvlUpSum>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDown>, lim);
   attr(level_wt_kernel<T, R, 64, kLvlDownBeta>, lim);
+  if constexpr (LVW<T, R, 128, kLvlDown>::SMEM <= 220 * 1024) {
+    attr(level_wt_kernel<T, R, 128, kLvlUpLeaf>, lim);
+    attr(level_wt_kernel<T, R, 128, kLvlUpSum>, lim);
+    attr(level_wt_kernel<T, R, 128, kLvlDown>, lim);
+  }
   attr(fused_up_kernel<T, R>, lim);
   attr(fused_down_kernel<T, R>, lim);
   if constexpr (std::is_same<T, float>::value) {
     attr(radiation_mom_kernel<R>, lim);
-    if constexpr (R <= 2) attr(radiation_tc_kernel<R>, int(radiation_tc_smem_bytes<R>()));
+    if constexpr (R == 2) attr(radiation_tc_kernel<R>, int(radiation_tc_smem_bytes<R>()));
     attr(tgemm_tc2_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(tgemm_tc3_kernel<R>, int(tc2_smem_bytes<R>()));
     attr(level_tc_kernel<R, kLvlUpLeaf>, int(level_tc_smem_bytes<R>(kLvlUpLeaf)));
@@ -1503,8 +1513,10 @@ constexpr int kMomBufPoints = 800;  // points staged per warp by the moment kern
 template <typename T, int R>
 int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value) {
-    if (P->v_mom && P->rad_tc && R <= 2) {
-      if constexpr (R <= 2) {
+    // the tensor-core moment map pairs the two real columns of one complex
+    // right-hand side; one or four real columns take the FFMA2 moment kernel
+    if (P->v_mom && P->rad_tc && R == 2) {
+      if constexpr (R == 2) {
         const int64_t nleaf = P->leaf_end - P->leaf_begin;
         const int64_t ntiles = (nleaf + kRadTcLeaves - 1) / kRadTcLeaves;
         const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ntiles, 2 * P->n_sm)));
@@ -1632,7 +1644,22 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
       tr("up_tc", s0);
       return;
     }
-    const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * 4 * mstride);
+    const LevelArgs<T, R> la = level_args(ci, CT + size_t(ci - 1) * P->nkind * mstride);
+    if (Q == 128) {
+      // (Track B's complex Q = 64 in the real embedding)
+      if constexpr (LVW<T, R, 128, kLvlDown>::SMEM <= 220 * 1024) {
+        const int gw = int((la.count + TGW<T, R, 128>::PER - 1) / TGW<T, R, 128>::PER);
+        if (lv == P->L)
+          launch_pdl(level_wt_kernel<T, R, 128, kLvlUpLeaf>, gw, 128, LVW<T, R, 128, kLvlUpLeaf>::SMEM, s0, la,
+                     RecvArgs{});
+        else
+          launch_pdl(level_wt_kernel<T, R, 128, kLvlUpSum>, gw, 128, LVW<T, R, 128, kLvlUpSum>::SMEM, s0, la,
+                     RecvArgs{});
+      }
+      nk++;
+      tr("up_wt", s0);
+      return;
+    }
     const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
     if (lv == P->L)
       launch_pdl(level_wt_kernel<T, R, 64, kLvlUpLeaf>, gw, 128, LVW<T, R, 64, kLvlUpLeaf>::SMEM, s0, la, RecvArgs{});
@@ -1700,7 +1727,17 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
       tr("down_tc", s0);
       return;
     }
-    const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * 4 * mstride);
+    const LevelArgs<T, R> la = level_args(ci, BT + size_t(ci - 1) * P->nkind * mstride);
+    if (Q == 128) {
+      if constexpr (LVW<T, R, 128, kLvlDown>::SMEM <= 220 * 1024) {
+        const int gw = int((la.count + TGW<T, R, 128>::PER - 1) / TGW<T, R, 128>::PER);
+        launch_pdl(level_wt_kernel<T, R, 128, kLvlDown>, gw, 128, LVW<T, R, 128, kLvlDown>::SMEM, s0, la,
+                   RecvArgs{});
+      }
+      nk++;
+      tr("down_wt", s0);
+      return;
+    }
     const int gw = int((la.count + TGW<T, R, 64>::PER - 1) / TGW<T, R, 64>::PER);
     if (lv == P->L && P->beta_fused && far_recv) {
       // leaf level + reception coefficients beta^ = E^ o in one kernel
@@ -2374,12 +2411,12 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     P->far_only = (d->options & NESA_PLAN_FAR_ONLY) != 0;
     if (d->options & NESA_PLAN_OCTREE) {
       // Track B: octree (8 child kinds), operators from the host.  The
-      // quadtree-specialised kernels (tensor-core levels / translation,
-      // warp-tiled wide levels, circle expansions) do not apply: every level
-      // runs in the fused kernels, translation in the generic GEMM.
+      // quadtree-specialised tensor-core kernels (levels, translation) and
+      // the circle expansions do not apply; wide levels use the warp-tiled
+      // FFMA kernels (per child kind, 8 matrices per level), the coarse
+      // levels the fused kernels.
       P->nkind = 8;
       P->tc = false;
-      P->wide_level = std::numeric_limits<int64_t>::max();
       require(d->V_blob && d->U_blob &&
                   (d->near_blob || P->far_only ||
                    ((d->options & NESA_PLAN_HELMHOLTZ_NEAR) && (d->options & NESA_PLAN_COMPLEX_NEAR) && d->points3)),

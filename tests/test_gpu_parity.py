@@ -686,3 +686,40 @@ def test_many_rhs_far_field_as_gemms(dtype, tol, nw, Q, P):
     ref = oracle_mvp(tree, ops, Qm[:, cols], near=near)
     for j, c in enumerate(cols):
         assert rel_l2(phi[:, c], ref[:, j]) <= tol, (c, rel_l2(phi[:, c], ref[:, j]))
+
+
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-12), ("f32", 1e-5)])
+def test_q128_warp_tiled_levels_and_translation(monkeypatch, dtype, tol):
+    # Q = 128: the warp-tiled level kernels (forced onto every level with
+    # >= 64 groups) and translation at their largest operator size
+    monkeypatch.setenv("NESA_WIDE_LEVEL", "64")
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=5), 12000)
+    tree = build_tree(pts, TreeParams(P=32))
+    params = NesaParams(Q=128)
+    q = geo.random_rhs(12000, 5)
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    qq = q if dtype == "f64" else q.astype(np.complex64)
+    plan = NesaPlan(tree, params, dtype=dtype)
+    qd = torch.from_numpy(qq).cuda()
+    ph = torch.empty_like(qd)
+    plan.matvec_ptr(qd.data_ptr(), ph.data_ptr(), 1, True)
+    err = rel_l2(ph.cpu().numpy(), ref)
+    plan.close()
+    assert err <= tol, err
+
+
+@pytest.mark.parametrize("n", [60000, 200000])
+def test_real_charges_float32_q64(n):
+    # the reference's own input: real charges (fastmvp.py:145-146), on the
+    # float32 Q = 64 bench-geometry plan (moment radiation, tensor-core
+    # levels / translation, expansion reception) -- one real column
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=3), n)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    q = geo.random_rhs(n, 3, complex_=False)
+    ops = build_all(tree, params)
+    for near, far in ((True, True), (False, True)):
+        ref = oracle_mvp(tree, ops, q, near=near, far=far)
+        phi = mvp(tree, params, q.astype(np.float32), near=near, far=far)
+        assert phi.dtype == np.float32
+        assert rel_l2(phi, ref) <= 1e-5, (near, far, rel_l2(phi, ref))

@@ -250,10 +250,14 @@ def test_track_b_c3_gpu_vs_oracle():
 
 
 @pytest.mark.gpu
-def test_track_b_gpu_q64_embedded_128():
+@pytest.mark.parametrize("wide_level", [None, "64"])
+def test_track_b_gpu_q64_embedded_128(monkeypatch, wide_level):
     # Q = 64 complex = 128 in the real embedding: the warp-tiled translation
-    # kernel at Q = 128 (the literal C4's operator size) against the oracle
+    # and (forced onto every level with >= 64 groups) level kernels at Q = 128,
+    # 8 child kinds -- the literal C4's operator size -- against the oracle
     _gpu()
+    if wide_level:
+        monkeypatch.setenv("NESA_WIDE_LEVEL", wide_level)
     from paper_1801_03589_b200.plan3 import HelmholtzPlan
     pts, tree, params, q = hz.track_b_problem("sphere", 20000, 1, 32, 64)
     tables = hz.build_tables3(tree, params)
