@@ -723,3 +723,24 @@ def test_real_charges_float32_q64(n):
         phi = mvp(tree, params, q.astype(np.float32), near=near, far=far)
         assert phi.dtype == np.float32
         assert rel_l2(phi, ref) <= 1e-5, (near, far, rel_l2(phi, ref))
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("f64", 1e-12)])
+@pytest.mark.parametrize("cplx,nrhs", [(False, 1), (False, 2), (False, 3), (False, 4), (True, 1),
+                                       (True, 2)])
+def test_column_count_matrix_q64(dtype, tol, cplx, nrhs):
+    # every vector width the engine specialises (R = 1, 2, 4 real columns per
+    # block; complex = column pairs) on the Q = 64 bench geometry, whose float32
+    # plan runs the tensor-core and expansion kernels
+    n = 30000
+    pts = geo.generate_sources(geo.CurveSpec(kind="ellipse-plates", seed=6), n)
+    tree = build_tree(pts, TreeParams(P=64))
+    params = NesaParams(Q=64)
+    rng = np.random.default_rng(6)
+    q = rng.standard_normal((n, nrhs)) + (1j * rng.standard_normal((n, nrhs)) if cplx else 0.0)
+    if nrhs == 1:
+        q = q[:, 0]
+    ref = oracle_mvp(tree, build_all(tree, params), q)
+    if dtype == "f32":
+        q = q.astype(np.complex64 if cplx else np.float32)
+    assert rel_l2(mvp(tree, params, q), ref) <= tol
