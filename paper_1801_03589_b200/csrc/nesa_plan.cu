@@ -919,18 +919,22 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       if (a >= lb && a < le) {
         // V: Q x na, x = qt rows of the leaf, y = s rows of leaf a
         {
+          // (complex operators, NESA_PLAN_COMPLEX_NEAR: V row-split like the
+          // near blocks -- columns and x rows in complex points, output rows
+          // combined pairwise into complex s rows)
           const int32_t sb = int32_t(hv.segs.size());
-          hv.segs.push_back(BlockSeg{int32_t(d->group_start[a]), 0});
+          hv.segs.push_back(BlockSeg{int32_t(d->group_start[a] / cdiv), 0});
           const int32_t ld = (Q + 3) / 4 * 4;
-          BlockItem it{hv.blob_elems, Q, int32_t(na), ld, int32_t(a * Q), sb, 1,
-                       int32_t(d->group_start[a]), 0};
+          const int64_t vn = na / cdiv;
+          BlockItem it{hv.blob_elems, Q, int32_t(vn), ld, int32_t(a * Q / cdiv), sb, 1,
+                       int32_t(d->group_start[a] / cdiv), 0};
           hv.items.push_back(it);
           v_src_off.push_back(v_off);
           v_src_rows.push_back(Q);
           v_row0.push_back(0);
           v_leaf.push_back(a);
-          hv.blob_elems += int64_t(ld) * na;
-          hv.entries += int64_t(Q) * na;
+          hv.blob_elems += int64_t(ld) * vn;
+          hv.entries += int64_t(Q) * vn;
         }
         // U: na x Q, x = o rows of leaf a, y = phi rows (stored mode only)
         if (!P->u_mf) {
@@ -951,7 +955,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
       }
       near_off += na * W;
-      v_off += int64_t(Q) * na;
+      v_off += int64_t(Q) * na / cdiv;
       u_off += na * Q;
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
@@ -1404,9 +1408,11 @@ void set_smem_attrs() {
   attr(blockgemv_kernel<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>,
        int(blockgemv_smem_bytes<T, R, kModeStore, kNearStages, kNearNCW, kNearABytes>()));
   attr(blockgemv_kernel<T, R, kModeStore>, int(blockgemv_smem_bytes<T, R, kModeStore>()));
-  if constexpr (R == 1)
+  if constexpr (R == 1) {
     attr(blockgemv_kernel<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>,
          int(blockgemv_smem_bytes<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>()));
+    attr(blockgemv_kernel<T, 2, kModeStoreCplx>, int(blockgemv_smem_bytes<T, 2, kModeStoreCplx>()));
+  }
   attr(blockgemv_kernel<T, R, kModeScatter>, int(blockgemv_smem_bytes<T, R, kModeScatter>()));
   const int lim = 220 * 1024;
   attr(tgemm_kernel<T, R>, lim);
@@ -1542,6 +1548,14 @@ int launch_radiation(nesa_plan* P, const T* qt, T* s, cudaStream_t st) {
     }
   }
   if (P->Vset.n_items == 0) return 0;
+  if (P->cnear) {
+    // complex V row-split (Track B): one complex column
+    if constexpr (R == 1)
+      blockgemv_kernel<T, 2, kModeStoreCplx><<<P->Vset.grid, kBGThreads, blockgemv_smem_bytes<T, 2, kModeStoreCplx>(),
+                                               st>>>(blockgemv_args<T, 2, kModeStoreCplx>(P->Vset, qt, s, nullptr,
+                                                                                          nullptr, 0));
+    return 1;
+  }
   blockgemv_kernel<T, R, kModeStore><<<P->Vset.grid, kBGThreads, blockgemv_smem_bytes<T, R, kModeStore>(), st>>>(
       blockgemv_args<T, R, kModeStore>(P->Vset, qt, s, nullptr, nullptr, 0));
   return 1;

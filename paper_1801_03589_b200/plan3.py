@@ -129,7 +129,7 @@ class HelmholtzPlan(NesaPlan):
                 nb = a.nbr_idx[a.nbr_ptr[g]:a.nbr_ptr[g + 1]].tolist()
                 slab = np.hstack([near_of(g, b) for b in nb])
                 near.append((row_split(slab) if complex_near else embed(slab)).ravel(order="F"))
-            Vb.append(embed(V[g]).ravel(order="F"))
+            Vb.append((row_split(V[g]) if complex_near else embed(V[g])).ravel(order="F"))
             Ub.append(embed(U[g]).ravel(order="F"))
         keep = {}
 
