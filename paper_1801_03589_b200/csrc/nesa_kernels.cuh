@@ -143,7 +143,11 @@ constexpr int kNearStages = 2;
 // kModeStoreCplx: store mode for a complex operator held row-split (rows
 // 2r / 2r+1 = Re / Im of operator row r, R = 2: one complex column), the
 // epilogue combines each row pair into y_r = (Re K) x + i (Im K) x
-enum { kModeStore = 0, kModeScatter = 1, kModeStoreCplx = 2 };
+// kModeScatterCplx: the scatter mode for a row-split complex operator (the
+// reception U of Track B): row pairs combine into one complex value, written
+// to the original-order position of its real part (perm of the embedded
+// vector) and the next element, plus the base (near-field) value.
+enum { kModeStore = 0, kModeScatter = 1, kModeStoreCplx = 2, kModeScatterCplx = 3 };
 
 template <typename T>
 struct BlockGemvArgs {
@@ -170,8 +174,9 @@ struct BGLayout {
   static constexpr int kMaxC = AB / 64;  // columns per chunk
   static constexpr size_t kA = AB;
   static constexpr size_t kX = size_t(kMaxC) * R * sizeof(T);
-  static constexpr size_t kFinPerm = MODE == kModeScatter ? size_t(kMaxRows) * 8 : 0;
-  static constexpr size_t kFinBase = MODE == kModeScatter ? size_t(kMaxRows) * R * sizeof(T) : 0;
+  static constexpr bool kScat = MODE == kModeScatter || MODE == kModeScatterCplx;
+  static constexpr size_t kFinPerm = kScat ? size_t(kMaxRows) * 8 : 0;
+  static constexpr size_t kFinBase = kScat ? size_t(kMaxRows) * R * sizeof(T) : 0;
   static constexpr size_t kStage =
       ((kA + kX + sizeof(StageHdr) + kFinPerm + kFinBase) + 127) & ~size_t(127);
   // the end-of-item column-lane reduction reuses the finished chunk's A
@@ -303,6 +308,17 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
             if (a.base) cp_async_n<R * sizeof(T)>(sb + r * R, a.base + int64_t(y_row0 + r) * R);
           }
         }
+      } else if constexpr (MODE == kModeScatterCplx) {
+        // complex rows: y_row0 and the rows below count complex points; perm
+        // and base are those of the embedded (real, one column) vector
+        if (flags & 2) {
+          int64_t* sp = reinterpret_cast<int64_t*>(stg + Lay::offPerm);
+          T* sb = reinterpret_cast<T*>(stg + Lay::offBase);
+          for (int r = lane; r < (m >> 1); r += 32) {
+            cp_async<8>(sp + r, a.perm + 2 * int64_t(y_row0 + r));
+            if (a.base) cp_async_n<2 * sizeof(T)>(sb + 2 * r, a.base + 2 * int64_t(y_row0 + r));
+          }
+        }
       }
       cp_async_mbar_arrive_noinc(&full[st]);
     }
@@ -362,7 +378,7 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
             for (int rr = 0; rr < R; ++rr) sRed[(cl * ld + 4 * rq + q) * R + rr] = acc[q][rr];
         }
         named_bar_sync(1, kNCT);
-        if constexpr (MODE == kModeStoreCplx) {
+        if constexpr (MODE == kModeStoreCplx || MODE == kModeScatterCplx) {
           // rows 2cr, 2cr+1 of the item hold (Re K_cr) x and (Im K_cr) x,
           // each a complex value: y_cr = first + i * second
           static_assert(R == 2, "complex near: one complex column");
@@ -375,12 +391,20 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
               w0 += sRed[(l * ld + 2 * cr + 1) * 2];
               w1 += sRed[(l * ld + 2 * cr + 1) * 2 + 1];
             }
-            const int64_t o = (int64_t(h.y_row0) + cr) * 2;
-            a.y[o] = u0 - w1;
-            a.y[o + 1] = u1 + w0;
+            if constexpr (MODE == kModeStoreCplx) {
+              const int64_t o = (int64_t(h.y_row0) + cr) * 2;
+              a.y[o] = u0 - w1;
+              a.y[o + 1] = u1 + w0;
+            } else {
+              const int64_t* sperm = reinterpret_cast<const int64_t*>(stg + Lay::offPerm);
+              const T* sbase = reinterpret_cast<const T*>(stg + Lay::offBase);
+              const int64_t dst = sperm[cr];
+              a.y[dst * a.ldy] = (a.base ? sbase[2 * cr] : T(0)) + (u0 - w1);
+              a.y[(dst + 1) * a.ldy] = (a.base ? sbase[2 * cr + 1] : T(0)) + (u1 + w0);
+            }
           }
         }
-        for (int row = tid; MODE != kModeStoreCplx && row < m; row += kNCT) {
+        for (int row = tid; MODE != kModeStoreCplx && MODE != kModeScatterCplx && row < m; row += kNCT) {
           T v[R];
 #pragma unroll
           for (int rr = 0; rr < R; ++rr) v[rr] = sRed[row * R + rr];

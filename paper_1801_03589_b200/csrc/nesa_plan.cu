@@ -938,25 +938,28 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
         }
         // U: na x Q, x = o rows of leaf a, y = phi rows (stored mode only)
         if (!P->u_mf) {
+          // (complex operators: U row-split, columns / x rows / output rows
+          // in complex units, kModeScatterCplx)
           const int32_t sb = int32_t(hu.segs.size());
-          hu.segs.push_back(BlockSeg{int32_t(a * Q), 0});
+          const int32_t uq = int32_t(Q / cdiv);
+          hu.segs.push_back(BlockSeg{int32_t(a * uq), 0});
           for (int64_t r0 = 0; r0 < na; r0 += kMaxRows) {
             const int32_t m = int32_t(std::min<int64_t>(kMaxRows, na - r0));
             const int32_t ld = (m + 3) / 4 * 4;
-            hu.items.push_back(BlockItem{hu.blob_elems, m, Q, ld,
-                                         int32_t(d->group_start[a] + r0), sb, 1, 0, 0});
+            hu.items.push_back(BlockItem{hu.blob_elems, m, uq, ld,
+                                         int32_t((d->group_start[a] + r0) / cdiv), sb, 1, 0, 0});
             u_src_off.push_back(u_off);
             u_src_rows.push_back(int32_t(na));
             u_row0.push_back(int32_t(r0));
             u_leaf.push_back(a);
-            hu.blob_elems += int64_t(ld) * Q;
-            hu.entries += int64_t(m) * Q;
+            hu.blob_elems += int64_t(ld) * uq;
+            hu.entries += int64_t(m) * uq;
           }
         }
       }
       near_off += na * W;
       v_off += int64_t(Q) * na / cdiv;
-      u_off += na * Q;
+      u_off += na * Q / cdiv;
     }
     require(int64_t(NL) * Q < (int64_t(1) << 31), "too many groups for int32 rows");
   }
@@ -1412,6 +1415,7 @@ void set_smem_attrs() {
     attr(blockgemv_kernel<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>,
          int(blockgemv_smem_bytes<T, 2, kModeStoreCplx, kNearStages, kNearNCW, kNearABytes>()));
     attr(blockgemv_kernel<T, 2, kModeStoreCplx>, int(blockgemv_smem_bytes<T, 2, kModeStoreCplx>()));
+    attr(blockgemv_kernel<T, 2, kModeScatterCplx>, int(blockgemv_smem_bytes<T, 2, kModeScatterCplx>()));
   }
   attr(blockgemv_kernel<T, R, kModeScatter>, int(blockgemv_smem_bytes<T, R, kModeScatter>()));
   const int lim = 220 * 1024;
@@ -1929,6 +1933,22 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
             },
             q, phi);
         nk++;
+      }
+    } else if (far && P->cnear) {
+      // complex U row-split (Track B): one complex column
+      const DevBlockSet& U = P->Uset;
+      if constexpr (R == 1) {
+        if (U.n_items > 0) {
+          io_launch(
+              P, blockgemv_kernel<T, 2, kModeScatterCplx>, U.grid, kBGThreads,
+              blockgemv_smem_bytes<T, 2, kModeScatterCplx>(), s0,
+              [=, &U](const void*, void* pp) {
+                return std::make_tuple(
+                    blockgemv_args<T, 2, kModeScatterCplx>(U, o, static_cast<T*>(pp), base, pm, ldv));
+              },
+              q, phi);
+          nk++;
+        }
       }
     } else if (far) {
       const DevBlockSet& U = P->Uset;

@@ -13,7 +13,8 @@ field, which streams the dominant operator bytes, does not pay the
 embedding's 2x storage: its blob is row-split (rows Re / Im of each complex
 row, NESA_PLAN_COMPLEX_NEAR) and the near kernel's complex-store epilogue
 (kModeStoreCplx) combines each row pair, so it reads 8 bytes per complex
-float32 entry.  NESA_PLAN_OCTREE tells the plan that the tree has 8 child
+float32 entry; the radiation V and reception U blocks are row-split the same
+way (kModeScatterCplx scatters the reception's complex rows).  NESA_PLAN_OCTREE tells the plan that the tree has 8 child
 kinds (octants) per level and that its operators come from the host.
 
 Reference anchor: the product is fastmvp.py:142-172 on the operators of
@@ -130,7 +131,7 @@ class HelmholtzPlan(NesaPlan):
                 slab = np.hstack([near_of(g, b) for b in nb])
                 near.append((row_split(slab) if complex_near else embed(slab)).ravel(order="F"))
             Vb.append((row_split(V[g]) if complex_near else embed(V[g])).ravel(order="F"))
-            Ub.append(embed(U[g]).ravel(order="F"))
+            Ub.append((row_split(U[g]) if complex_near else embed(U[g])).ravel(order="F"))
         keep = {}
 
         def arr(name, x, dtype_):
