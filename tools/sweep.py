@@ -1,7 +1,7 @@
 """Time the bench product under several NESA_* environment settings in one
 process (the tree and tables are built once; each setting gets its own plan).
 
-    python tools/sweep.py "" "NESA_NEAR_UNITS=1184" "NESA_NEAR_UNITS=1184;NESA_NEAR_SKIP=32" ...
+    python tools/sweep.py "" "NESA_WIDE_LEVEL=1024" "NESA_U_TERMS=22;NESA_V_MOMENTS=32" ...
 
 Per setting: median / min us per product over --reps blocks of --k graph
 launches (CUDA events on the launch stream), and whether phi is bitwise equal
