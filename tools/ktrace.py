@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--near", type=int, default=1)
     ap.add_argument("--far", type=int, default=1)
     ap.add_argument("--dtype", default="f32", help="f32 (complex64) or f64 (complex128)")
+    ap.add_argument("--world", type=int, default=1, help="trace rank --rank's sub-plan of this partition")
+    ap.add_argument("--rank", type=int, default=0)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -38,7 +40,11 @@ def main():
     from paper_1801_03589_b200.plan import NesaPlan
     pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=3), a.n)
     tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
-    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype=a.dtype)
+    lr = None
+    if a.world > 1:
+        from paper_1801_03589_b200.dist import partition_leaves
+        lr = partition_leaves(tree, a.world, 64)[a.rank]
+    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype=a.dtype, leaf_range=lr)
     cdt = np.complex64 if a.dtype == "f32" else np.complex128
     q = torch.from_numpy(nesa.random_rhs(a.n, 3).astype(cdt)).cuda()
     phi = torch.empty_like(q)
