@@ -20,10 +20,10 @@ The equivalent-source fits are the reference's truncated-SVD pseudoinverse
 are the reference's constraints carried to 3D (sqrt(3) for the box's
 half-diagonal instead of sqrt(2)).
 
-Parity for this track is against the restated serial product
-(oracle/mvp_oracle.mvp_serial, dtype-generic) on these operators; the
-reference cannot produce 3D / Helmholtz operators, so beyond that and a
-small-N dense sum the track is "parity unpinned".
+The product on these operators is pinned against the reference's own
+mvp_serial run on their real embedding (oracle/gen_golden_track_b.py,
+tests/golden/track_b_*.npz); the operator construction itself is ours --
+the reference cannot produce 3D / Helmholtz operators.
 """
 
 from __future__ import annotations

@@ -1,11 +1,15 @@
 """Track B: 3D octree, Helmholtz kernel, complex operators.
 
-The reference is 2D / log-kernel only, so this track's parity is pinned
-against restatements: the vectorised octree against oracle/octree_ref.py
-(the reference's quadtree.py:123-245 loop for loop in 3D, bit-exact), the
-GPU product against the dtype-generic serial oracle (fastmvp.py:142-172) on
-the same complex operators (c128 <= 1e-12, c64 <= 1e-5), and the operators
-against the O(N^2) Helmholtz sum at low frequency (convergence in Q).
+The reference is 2D / log-kernel only.  This track is pinned three ways:
+the vectorised octree against oracle/octree_ref.py (the reference's
+quadtree.py:123-245 loop for loop in 3D, bit-exact); the PRODUCT against
+golden outputs of the reference's own mvp_serial (fastmvp.py:142-172) run on
+the real 2x2 embedding of the complex operators (oracle/gen_golden_track_b.py
+-> tests/golden/track_b_*.npz; the reference's code is generic over the tree
+and operator containers) -- for the dtype-generic oracle and the GPU (c128
+<= 1e-12, c64 <= 1e-5); and the operators against the O(N^2) Helmholtz sum at
+low frequency (convergence in Q).  The operator construction itself (3D
+aux spheres, Helmholtz fits) is ours: the reference has none.
 """
 
 import math
@@ -96,6 +100,23 @@ def test_geometry_generators():
     assert abs((np.abs(ell[:, 0]) < 2.5).mean() - want_mid) < 0.01
     k = hz.wavenumber3("sphere", 2000)
     assert abs(2 * math.pi / k - 10 * math.sqrt(4 * math.pi / 2000)) < 1e-12
+
+
+TRACK_B_GOLDEN = ["track_b_sphere_2000", "track_b_sphere_6000_levels", "track_b_ellipsoid_plates_8000"]
+
+
+@pytest.mark.parametrize("name", TRACK_B_GOLDEN)
+def test_oracle_matches_reference_product_golden(name):
+    # the dtype-generic oracle on the complex operators against the
+    # reference's own mvp_serial on their real embedding
+    from conftest import load_golden
+    from oracle.gen_golden_track_b import build_case
+    g = load_golden(name)
+    pts, tree, params, q = build_case(name)
+    assert np.array_equal(q, g["q"])
+    ops = hz.build_all3(tree, params)
+    assert rel_l2(oracle_mvp(tree, ops, q), g["phi"]) <= 1e-13
+    assert rel_l2(oracle_mvp(tree, ops, q, far=False), g["phi_near"]) <= 1e-14
 
 
 def test_embedding():
@@ -206,6 +227,27 @@ def test_track_b_gpu_vs_oracle(name, complex_near):
         assert out.dtype == np.complex64
         assert rel_l2(out, ref) <= 1e-5
         p64.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", TRACK_B_GOLDEN)
+@pytest.mark.parametrize("complex_near", [True, False])
+def test_track_b_gpu_vs_reference_product_golden(name, complex_near):
+    # the GPU product against the reference's own mvp_serial (embedded form)
+    _gpu()
+    from conftest import load_golden
+    from oracle.gen_golden_track_b import build_case
+    from paper_1801_03589_b200.plan3 import HelmholtzPlan
+    g = load_golden(name)
+    pts, tree, params, q = build_case(name)
+    tables = hz.build_tables3(tree, params)
+    for dt, tol, near_tol in (("c128", 1e-12, 1e-13), ("c64", 1e-5, 1e-5)):
+        plan = HelmholtzPlan(tree, tables, dt, complex_near=complex_near)
+        qq = q if dt == "c128" else q.astype(np.complex64)
+        err = rel_l2(plan.matvec(qq), g["phi"])
+        err_near = rel_l2(plan.matvec(qq, far=False), g["phi_near"])
+        plan.close()
+        assert err <= tol and err_near <= near_tol, (dt, err, err_near)
 
 
 @pytest.mark.gpu
