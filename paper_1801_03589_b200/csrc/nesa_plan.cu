@@ -1835,12 +1835,22 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
   };
   auto down_pass = [&](bool fine) {
     if (fine) {
-      for (int lv = P->L; lv >= P->split_lv; --lv) {
-        const size_t li = size_t(lv - P->l0);
+      // the leaf level alone (its s is final first: right after the
+      // radiation), the other wide levels together once the coarsest of
+      // them is final (fewer, fuller launches)
+      {
+        const size_t li = size_t(P->L - P->l0);
         CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[li], 0));
         translate(P->tunit_lv_begin[li], P->tunit_lv_end[li], P->s2);
         reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s2);
         CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s2));
+      }
+      if (P->split_lv < P->L) {
+        const size_t hi = size_t(P->L - 1 - P->l0), lo = size_t(P->split_lv - P->l0);
+        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[lo], 0));
+        translate(P->tunit_lv_begin[hi], P->tunit_lv_end[lo], P->s2);
+        reduce(P->red_lv_begin[hi], P->red_lv_end[lo], P->s2);
+        for (size_t li = lo; li <= hi; ++li) CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s2));
       }
       translate(P->n_tunits_fine, P->n_tunits, s0);
       reduce(P->n_red_fine, P->n_red, s0);
