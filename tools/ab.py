@@ -2,6 +2,7 @@
 
     python tools/ab.py ab/libA.so ab/libB.so [--rounds 3] [--steps 200]
     python tools/ab.py lib.so lib.so:NESA_U_TERMS=22     (a spec may add environment settings)
+    python tools/ab.py lib.so lib.so:AB_PROFILE=1        (with the near-field event nodes bench.py times)
 
 Each round runs every library in a fresh process (NESA_LIB selects it),
 alternating the order, and times `steps` back-to-back products with CUDA
@@ -16,8 +17,9 @@ import sys
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 CHILD = r'''
-import sys, json, numpy as np, torch
+import os, sys, json, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
+prof = "near" if os.environ.get("AB_PROFILE") else False
 import paper_1801_03589_b200 as nesa
 from paper_1801_03589_b200.plan import NesaPlan
 steps = int(sys.argv[2])
@@ -26,16 +28,21 @@ tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
 plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype="f32")
 q = torch.from_numpy(nesa.random_rhs(2000000, 3).astype(np.complex64)).cuda()
 phi = torch.empty_like(q)
+bufs = [(q, phi)]
+if os.environ.get("AB_ALT"):  # two buffer pairs, alternating (the io nodes re-pointed every launch)
+    bufs.append((q.clone(), torch.empty_like(q)))
 st = torch.cuda.current_stream()
-for _ in range(20):
-    plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, stream=st.cuda_stream)
+for i in range(20):
+    qq, pp = bufs[i % len(bufs)]
+    plan.matvec_ptr(qq.data_ptr(), pp.data_ptr(), 1, True, stream=st.cuda_stream, profile=prof)
 torch.cuda.synchronize()
 res = []
 for rep in range(3):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for _ in range(steps):
-        plan.matvec_ptr(q.data_ptr(), phi.data_ptr(), 1, True, stream=st.cuda_stream)
+    for i in range(steps):
+        qq, pp = bufs[i % len(bufs)]
+        plan.matvec_ptr(qq.data_ptr(), pp.data_ptr(), 1, True, stream=st.cuda_stream, profile=prof)
     e1.record(st)
     e1.synchronize()
     res.append(e0.elapsed_time(e1) / steps)
