@@ -644,6 +644,8 @@ struct FusedArgs {
   const int2* uchild;     // [G] local children (first id, count)
   const int32_t* anc;     // down: [count][D] ancestors of the level-lf groups (level lf-1 first)
   const int32_t* own;     // down: [count] ancestors each level-lf group's CTA owns (computes)
+  const int4* chain_up;   // up: [count][D + 2] (group, first child, children, quad) from level lf to l0
+  const int4* chain_down; // down: [count][D + 1] (x, parent x, quad x, own) top owned group first
   int* cnt;               // up: arrivals per group
   int* state;             // down: 0 pending, 2 done (reset by the up kernel)
   int* ticket;            // down: [2] start-order counter, finished CTAs
@@ -669,10 +671,11 @@ __device__ __forceinline__ void st_release_s32(int* p, int v) {
 }
 
 constexpr int kFusedThreads = 128;
+constexpr int kFusedMaxChain = 32;  // levels a fused chain can span (l0 .. lf)
 
 template <typename T>
 __host__ __device__ inline size_t fused_smem_bytes(int Q, int R) {
-  return mat_bytes(Q, sizeof(T)) + ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 64;
+  return mat_bytes(Q, sizeof(T)) + 2 * ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 64;
 }
 
 template <typename T, int R>
@@ -687,33 +690,36 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
   int64_t* nxt = reinterpret_cast<int64_t*>(bar + 1);
   int64_t g = a.first + blockIdx.x;
   int lv = a.lf;
-  auto load_mat = [&](int lvx, int64_t gx) {
-    mbar_arrive_expect_tx(bar, uint32_t(mb));
-    bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * a.nkind + a.quad[gx]) * a.mstride, uint32_t(mb), bar);
-  };
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    if (lv > a.l0) load_mat(lv, g);   // constant data: before the dependency wait
+  // plan constants of the CTA's whole ancestor chain (group, children,
+  // quadrant per step): one packed 16-byte record per step, fetched in one
+  // round trip ahead of the dependency wait, so the climb pays no index
+  // round trips between its levels
+  __shared__ int32_t ch_x[kFusedMaxChain];
+  __shared__ int2 ch_uc[kFusedMaxChain];
+  __shared__ int32_t ch_quad[kFusedMaxChain];
+  const int nstep = a.lf - a.l0 + 1;  // groups on the chain, level lf down to l0 (= D + 2)
+  if (tid < nstep) {
+    const int4 c = a.chain_up[int64_t(blockIdx.x) * nstep + tid];
+    ch_x[tid] = c.x;
+    ch_uc[tid] = make_int2(c.y, c.z);
+    ch_quad[tid] = c.w;
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      if (lv > a.l0) {  // constant data: before the dependency wait
+        mbar_arrive_expect_tx(bar, uint32_t(mb));
+        bulk_g2s(M, a.MT + (size_t(lv - a.l0 - 1) * a.nkind + c.w) * a.mstride, uint32_t(mb), bar);
+      }
+    }
   }
   __syncthreads();
   pdl_trigger();
   pdl_wait();
   uint32_t phase = 0;
+  int step = 0;
   while (true) {
-    // plan constants of this step (parent, its child count and quadrant)
-    // loaded before they are needed
-    int64_t p_next = -1;
-    int p_nch = 0, p_quad = 0;
-    if (tid == 0) {
-      a.state[g] = 0;
-      if (lv > a.l0) {
-        p_next = a.parent[g];
-        p_nch = a.uchild[p_next].y;
-        p_quad = a.quad[p_next];
-      }
-    }
-    const int2 uc = a.uchild[g];
+    if (tid == 0) a.state[g] = 0;
+    const int2 uc = ch_uc[step];
     for (int w = tid; w < QR; w += kFusedThreads) {
       T v;
       if (lv == a.L) {
@@ -738,7 +744,8 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
     }
     __syncthreads();  // T[g] written, M and X consumed
     if (tid == 0) {
-      const int64_t p = p_next;
+      const int64_t p = ch_x[step + 1];
+      const int p_nch = ch_uc[step + 1].y, p_quad = ch_quad[step + 1];
       fence_acq_rel_gpu();  // release T[g] (and s[g]) to the parent's CTA
       const int old = atomicAdd(a.cnt + p, 1);
       const bool last = old == p_nch - 1;
@@ -757,6 +764,7 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
     if (p < 0) break;
     g = p;
     --lv;
+    ++step;
   }
 }
 
@@ -766,10 +774,14 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   extern __shared__ __align__(128) unsigned char smem[];
   const int Q = a.Q, Qp = (Q + 3) / 4 * 4, QR = Q * R, tid = threadIdx.x;
   const size_t mb = mat_bytes(Q, sizeof(T));
+  const size_t vb = (size_t(QR) * sizeof(T) + 15) & ~size_t(15);
   T* M = reinterpret_cast<T*>(smem);
-  T* X = reinterpret_cast<T*>(smem + mb);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + ((size_t(QR) * sizeof(T) + 15) & ~size_t(15)));
+  T* X = reinterpret_cast<T*>(smem + mb);        // o[parent]
+  T* Xo = reinterpret_cast<T*>(smem + mb + vb);  // o[x], the next step's parent vector
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + 2 * vb);
   int* ticket = reinterpret_cast<int*>(bar + 1);
+  __shared__ int32_t ch_x[kFusedMaxChain], ch_px[kFusedMaxChain], ch_quad[kFusedMaxChain];
+  __shared__ int s_own;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -777,53 +789,74 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   }
   __syncthreads();
   const int vid = *ticket;
-  const int64_t g = a.first + vid;
+  // This CTA owns the ancestors whose first level-lf descendant is g = first
+  // + vid (its chain up to own[cta] levels; every coarse group has exactly
+  // one owner).  It waits once -- for the parent of its top owned group,
+  // published by that group's owner -- then computes its chain top down
+  // without further waits, publishing each owned group for the CTAs below.
+  // Step st handles x = anc[own - 1 - st] (st = own: g itself).  The chain's
+  // plan constants (one packed record per step, one round trip) and the first
+  // matrix are fetched ahead of the dependency wait; from the second step on
+  // the parent's vector is the previous step's result (kept in shared
+  // memory), so a step costs one matrix copy, overlapped with the release of
+  // the previous group.
+  if (tid <= a.D) {
+    const int4 c = a.chain_down[vid * int64_t(a.D + 1) + tid];  // (entries past own are zero-filled)
+    ch_x[tid] = c.x;
+    ch_px[tid] = c.y;
+    ch_quad[tid] = c.z;
+    if (tid == 0) s_own = c.w;
+  }
+  __syncthreads();
+  const int own = s_own;
+  auto load_mat = [&](int st) {
+    const int lvx = a.lf - own + st;  // level of step st's group
+    mbar_arrive_expect_tx(bar, uint32_t(mb));
+    bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * a.nkind + ch_quad[st]) * a.mstride, uint32_t(mb), bar);
+  };
+  if (tid == 0) load_mat(0);  // constant data: before the dependency wait
   pdl_trigger();
   pdl_wait();  // o holds the translation sums
   uint32_t phase = 0;
-  // This CTA owns the ancestors whose first level-lf descendant is g (its
-  // chain up to own[cta] levels; every coarse group has exactly one owner).
-  // It waits once -- for the parent of its top owned group, published by
-  // that group's owner -- then computes its chain top down without further
-  // waits, publishing each owned group for the CTAs below.
-  const int own = a.own[vid];
-  const int32_t* anc = a.anc + vid * int64_t(a.D);
-  for (int i = own - 1; i >= -1; --i) {
-    const int64_t x = i >= 0 ? int64_t(anc[i]) : g;
-    const int lvx = a.lf - 1 - i;
-    const int64_t px = a.parent[x];
-    if (tid == 0) {
-      mbar_arrive_expect_tx(bar, uint32_t(mb));
-      bulk_g2s(M, a.MT + (size_t(lvx - a.l0 - 1) * a.nkind + a.quad[x]) * a.mstride, uint32_t(mb), bar);
-    }
-    if (i == own - 1 && lvx - 1 > a.l0) {
-      // the parent of the top owned group belongs to another CTA
-      if (tid == 0) {
-        unsigned ns = 64;
-        while (ld_acquire_s32(a.state + px) != 2) {
-          __nanosleep(ns);
-          if (ns < 512) ns *= 2;
+  for (int st = 0; st <= own; ++st) {
+    const int64_t x = ch_x[st], px = ch_px[st];
+    if (st == 0) {
+      if (a.lf - own - 1 > a.l0) {
+        // the parent of the top owned group belongs to another CTA
+        if (tid == 0) {
+          unsigned ns = 64;
+          while (ld_acquire_s32(a.state + px) != 2) {
+            __nanosleep(ns);
+            if (ns < 512) ns *= 2;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
+      for (int w = tid; w < QR; w += kFusedThreads) X[w] = __ldcg(a.o + px * QR + w);
     }
-    // o[x] += B_{lvx, quad x} o[parent x]
-    for (int w = tid; w < QR; w += kFusedThreads) X[w] = __ldcg(a.o + px * QR + w);
     __syncthreads();
     mbar_wait(bar, phase);
     phase ^= 1u;
+    // o[x] += B_{lvx, quad x} o[parent x]
     for (int w = tid; w < QR; w += kFusedThreads) {
       const int k = w / R, rr = w - (w / R) * R;
       T acc = T(0);
 #pragma unroll 8
       for (int j = 0; j < Q; ++j) acc = fma(M[j * Qp + k], X[j * R + rr], acc);
-      a.o[x * QR + w] = __ldcg(a.o + x * QR + w) + acc;
+      // (x's own translation sum: an independent load, overlapped with the FMAs)
+      const T val = __ldcg(a.o + x * QR + w) + acc;
+      a.o[x * QR + w] = val;
+      Xo[w] = val;
     }
     __syncthreads();  // o[x] written, M and X consumed
-    if (i >= 0 && tid == 0) {
+    if (tid == 0 && st < own) {
+      load_mat(st + 1);  // overlaps the release below
       fence_acq_rel_gpu();
       st_release_s32(a.state + x, 2);
     }
+    T* t = X;  // the next step's parent vector is this step's result
+    X = Xo;
+    Xo = t;
   }
   // the last CTA to finish resets the ticket counter for the next launch
   if (tid == 0 && atomicAdd(a.ticket + 1, 1) == int(gridDim.x) - 1) {
@@ -1447,8 +1480,17 @@ constexpr int kTc3CtasPerSM = 1;  // persistent translation CTAs per SM (A/B: 1 
 // allocates TMEM once, and fetches the next unit's D as soon as the last MMA
 // of the current one has consumed the D buffer, so the D copy, the next
 // sources and the epilogue overlap instead of paying one CTA start per unit.
+// Register budget of the tensor-core far-field kernels (128 threads, one warp
+// per SM sub-partition).  A sub-partition's 16384 registers hold up to 3 of the
+// near field's 10 warps (2 CTAs x 5 warps x 64 registers x 32 = 6144), which
+// leaves 10240 for one translation warp AND one level-kernel warp: 160 + 160
+// registers per thread.  At the natural 240 + 168 the upward level kernels
+// could not become resident beside the persistent translation and waited
+// ~40 us for its CTAs to exit (ktrace, profiles/r2_ktrace_sched.txt).  Only
+// the complex64 bench path (R = 2) is capped; R = 1 / 4 would spill.
+constexpr int kTcFarMaxReg = 160;
 template <int R>
-__global__ void __launch_bounds__(128) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
+__global__ void __maxnreg__(R == 2 ? kTcFarMaxReg : 255) tgemm_tc3_kernel(const TUnit* __restrict__ units, int n_units,
                                                         const TEnt* __restrict__ ents,
                                                         const float* __restrict__ DTC,
                                                         const float* __restrict__ s, float* Y, int tag = 44) {
@@ -1798,7 +1840,7 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(128) level_tc_kernel(const LevelTcArgs a) {
+__global__ void __maxnreg__(R == 2 ? kTcFarMaxReg : 255) level_tc_kernel(const LevelTcArgs a) {
   KtScope kt_(80 + MODE);
   constexpr int QR = 64 * R, EPT = 128 / R, HALF = EPT / 2, OS = QR + 4, NV = QR / 4;
   constexpr bool kDown = MODE == kLvlDown || MODE == kLvlDownBeta;

@@ -419,9 +419,10 @@ struct nesa_plan {
   DevBuf<int2> uchild;                      // [G] local children (first, count)
   DevBuf<int32_t> fused_anc;                // [count(lf)][lf - l0 - 1] ancestors
   DevBuf<int> fused_cnt, fused_state;       // [G] arrival counters / done flags
+  DevBuf<int4> fused_chain_up, fused_chain_down;  // packed per-CTA chain records (see build)
   DevBuf<int32_t> fused_own;                // [count(lf)] ancestors owned by each level-lf group's CTA
   DevBuf<int> fused_ticket;                 // [2] fused_down start-order counter
-  int64_t wide_level = 2048;                // warp-tiled level kernels from this size
+  int64_t wide_level = 1024;                // per-level (warp-tiled / tensor-core) kernels from this size
                                             // (NESA_WIDE_LEVEL: tests force them on small trees)
   bool u_mf = false;                        // matrix-free reception (float32 plans)
   DevBuf<float2> mf_prel;                   // [N] point - leaf center (float32)
@@ -480,8 +481,8 @@ struct nesa_plan {
   DevBuf<unsigned char> farws;              // s | Tup | o, contiguous
 
   cudaStream_t s0 = nullptr, s1 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaStream_t s2 = nullptr;                 // fine-level translation branch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_tx = nullptr;
+  cudaStream_t s2 = nullptr, s3 = nullptr;   // fine-level translation branch, leaf-level translation sums
   int split_lv = 0;                          // levels >= split_lv: translated on s2
   int n_tunits_fine = 0;                     // units [0, n_tunits_fine) are fine levels
   // per level (index lv - l0): translation units and translation-sum groups,
@@ -549,7 +550,9 @@ struct nesa_plan {
     for (auto e : ev_t_lv) cudaEventDestroy(e);
     if (w_ev_near) cudaEventDestroy(w_ev_near);
     if (s2) cudaStreamDestroy(s2);
+    if (s3) cudaStreamDestroy(s3);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_tx) cudaEventDestroy(ev_tx);
     if (ev_join) cudaEventDestroy(ev_join);
     if (s0) cudaStreamDestroy(s0);
     if (s1) cudaStreamDestroy(s1);
@@ -807,6 +810,32 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
       own[size_t(i)] = k;
     }
     P->fused_own.upload(own);
+    // packed chain records, one 16-byte load per step (the kernels fetch a
+    // CTA's whole chain in one round trip instead of walking anc -> parent /
+    // quad / uchild):
+    //   up   [i][k], k = 0 .. D+1: (group at level lf-k, first child, children, quad)
+    //   down [i][st], st = 0 .. own: (x = anc[own-1-st] or g, parent x, quad x, own)
+    {
+      require(D + 2 <= kFusedMaxChain, "fused chain longer than kFusedMaxChain levels");
+      const int64_t cnt = P->loc_count[li];
+      std::vector<int4> cup(static_cast<size_t>(std::max<int64_t>(1, cnt * (D + 2))), int4{0, 0, 0, 0});
+      std::vector<int4> cdn(static_cast<size_t>(std::max<int64_t>(1, cnt * (D + 1))), int4{0, 0, 0, 0});
+      for (int64_t i = 0; i < cnt; ++i) {
+        int64_t x = P->loc_first[li] + i;
+        for (int k = 0; k <= D + 1; ++k) {
+          cup[size_t(i * (D + 2) + k)] = int4{int(x), uc[size_t(x)].x, uc[size_t(x)].y, d->quad[x]};
+          if (k <= D) x = d->parent[x];
+        }
+        const int ow = own[size_t(i)];
+        for (int st = 0; st <= ow; ++st) {
+          const int a = ow - 1 - st;
+          const int64_t y = a >= 0 ? int64_t(anc[size_t(i * D + a)]) : P->loc_first[li] + i;
+          cdn[size_t(i * (D + 1) + st)] = int4{int(y), int(d->parent[y]), d->quad[y], ow};
+        }
+      }
+      P->fused_chain_up.upload(cup);
+      P->fused_chain_down.upload(cdn);
+    }
     P->fused_ticket.alloc(2);
     P->fused_cnt.alloc(size_t(G));    // zero-filled
     P->fused_state.alloc(size_t(G));
@@ -1686,11 +1715,11 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     nk++;
     tr("up_wt", s0);
   };
-  auto translate = [&](int u0, int u1, cudaStream_t st) {
+  auto translate = [&](int u0, int u1, cudaStream_t st, bool pdl = true) {
     if (u1 <= u0) return;
     const T* DTp = reinterpret_cast<const T*>(P->DT.p);
     const TUnit* up = P->tunits.p + u0;
-    const bool pdl_ok = st == s0;
+    const bool pdl_ok = pdl && st == s0;
     auto go = [&](auto kern, int grid, size_t smem, auto... args) {
       if (pdl_ok)
         launch_pdl(kern, grid, 128, smem, st, args...);
@@ -1785,6 +1814,8 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     fa.cnt = P->fused_cnt.p;
     fa.state = P->fused_state.p;
     fa.own = P->fused_own.p;
+    fa.chain_up = P->fused_chain_up.p;
+    fa.chain_down = P->fused_chain_down.p;
     fa.ticket = P->fused_ticket.p;
     fa.Tup = Tup;
     fa.s = s;
@@ -1835,24 +1866,38 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
   };
   auto down_pass = [&](bool fine) {
     if (fine) {
-      // the leaf level alone (its s is final first: right after the
-      // radiation), the other wide levels together once the coarsest of
-      // them is final (fewer, fuller launches)
+      // Side stream s2: the leaf level's translation (its s is final right
+      // after the radiation), then the other wide levels' in one launch once
+      // the coarsest of them is final -- back to back, so the second
+      // persistent launch takes the SM slots the first one's CTAs leave
+      // (beside the near field's two CTAs an SM holds ONE more 50 KB
+      // tensor-core CTA plus a level kernel or three fused-chain CTAs; two
+      // resident translations starve the upward chain).  The leaf level's
+      // translation sums run on a third stream beside the second
+      // translation; the other levels' sums follow it.  The coarse
+      // translation on s0 gets no early programmatic start: its persistent
+      // CTAs would hold their slots idle until the fused upward chain ends.
+      // (ktrace before / after: profiles/r2_ktrace_sched.txt)
       {
         const size_t li = size_t(P->L - P->l0);
+        const size_t lo = size_t(P->split_lv - P->l0);
         CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[li], 0));
         translate(P->tunit_lv_begin[li], P->tunit_lv_end[li], P->s2);
-        reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s2);
-        CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s2));
+        if (P->split_lv < P->L) {
+          CUDA_OK(cudaEventRecord(P->ev_tx, P->s2));
+          CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_tx, 0));
+          reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s3);
+          CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s3));
+          CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[lo], 0));
+          translate(P->tunit_lv_begin[li - 1], P->tunit_lv_end[lo], P->s2);
+          reduce(P->red_lv_begin[li - 1], P->red_lv_end[lo], P->s2);
+          for (size_t l = lo; l < li; ++l) CUDA_OK(cudaEventRecord(P->ev_t_lv[l], P->s2));
+        } else {
+          reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s2);
+          CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s2));
+        }
       }
-      if (P->split_lv < P->L) {
-        const size_t hi = size_t(P->L - 1 - P->l0), lo = size_t(P->split_lv - P->l0);
-        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[lo], 0));
-        translate(P->tunit_lv_begin[hi], P->tunit_lv_end[lo], P->s2);
-        reduce(P->red_lv_begin[hi], P->red_lv_end[lo], P->s2);
-        for (size_t li = lo; li <= hi; ++li) CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s2));
-      }
-      translate(P->n_tunits_fine, P->n_tunits, s0);
+      translate(P->n_tunits_fine, P->n_tunits, s0, false);
       reduce(P->n_red_fine, P->n_red, s0);
     } else {
       translate(0, P->n_tunits, s0);
@@ -2497,6 +2542,7 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
     CUDA_OK(cudaStreamCreateWithFlags(&P->s0, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&P->s1, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&P->s2, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&P->s3, cudaStreamNonBlocking));
     for (int i = 0; i < P->L - P->l0 + 1; ++i) {
       cudaEvent_t a = nullptr, b = nullptr;
       CUDA_OK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -2505,6 +2551,7 @@ nesa_plan* plan_create_impl(const nesa_plan_desc* d, int device, void* comm, int
       P->ev_t_lv.push_back(b);
     }
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&P->ev_tx, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
     for (auto& e : P->cap_events) CUDA_OK(cudaEventCreate(&e));
     if (comm) {

@@ -3,6 +3,7 @@
     python tools/ab.py ab/libA.so ab/libB.so [--rounds 3] [--steps 200]
     python tools/ab.py lib.so lib.so:NESA_U_TERMS=22     (a spec may add environment settings)
     python tools/ab.py lib.so lib.so:AB_PROFILE=1        (with the near-field event nodes bench.py times)
+    python tools/ab.py a.so:AB_CFG=200000/48/48/2,AB_DTYPE=f64 b.so:AB_CFG=200000/48/48/2,AB_DTYPE=f64   (C3, float64 plan)
 
 Each round runs every library in a fresh process (NESA_LIB selects it),
 alternating the order, and times `steps` back-to-back products with CUDA
@@ -23,10 +24,13 @@ prof = "near" if os.environ.get("AB_PROFILE") else False
 import paper_1801_03589_b200 as nesa
 from paper_1801_03589_b200.plan import NesaPlan
 steps = int(sys.argv[2])
-pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=3), 2000000)
-tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
-plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype="f32")
-q = torch.from_numpy(nesa.random_rhs(2000000, 3).astype(np.complex64)).cuda()
+# AB_CFG=N,P,Q,seed (default the C4 bench workload), AB_DTYPE=f32|f64
+N, PP, QQ, SEED = (int(x) for x in os.environ.get("AB_CFG", "2000000/64/64/3").split("/"))
+dt = os.environ.get("AB_DTYPE", "f32")
+pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=SEED), N)
+tree = nesa.build_tree(pts, nesa.TreeParams(P=PP))
+plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=QQ)), dtype=dt)
+q = torch.from_numpy(nesa.random_rhs(N, SEED).astype(np.complex64 if dt == "f32" else np.complex128)).cuda()
 phi = torch.empty_like(q)
 bufs = [(q, phi)]
 if os.environ.get("AB_ALT"):  # two buffer pairs, alternating (the io nodes re-pointed every launch)

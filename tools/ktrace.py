@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--dtype", default="f32", help="f32 (complex64) or f64 (complex128)")
     ap.add_argument("--world", type=int, default=1, help="trace rank --rank's sub-plan of this partition")
     ap.add_argument("--rank", type=int, default=0)
+    ap.add_argument("--split", action="store_true",
+                    help="separate repeated launches of one (kernel, grid): CTA records in start order, grid at a time")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -65,8 +67,22 @@ def main():
         rec = np.frombuffer(buf, dtype=np.uint64, count=4 * n).reshape(n, 4).astype(np.int64)
         t0 = rec[:, 2].min()
         launches = {}
-        for tag, grid, s, e in rec:
-            k = (int(tag), int(grid))
+        if a.split:
+            # launch index of each record: rank of its start among the records of its (tag, grid), // grid
+            order = np.lexsort((rec[:, 2], rec[:, 1], rec[:, 0]))
+            rec = rec[order]
+            sub = np.zeros(len(rec), dtype=np.int64)
+            i = 0
+            while i < len(rec):
+                j = i
+                while j < len(rec) and rec[j, 0] == rec[i, 0] and rec[j, 1] == rec[i, 1]:
+                    j += 1
+                sub[i:j] = np.arange(j - i) // max(1, int(rec[i, 1]))
+                i = j
+        else:
+            sub = np.zeros(len(rec), dtype=np.int64)
+        for (tag, grid, s, e), sb in zip(rec, sub):
+            k = (int(tag), int(grid), int(sb))
             lo, hi, c = launches.get(k, (1 << 62, 0, 0))
             launches[k] = (min(lo, s - t0), max(hi, e - t0), c + 1)
         runs.append(launches)
