@@ -671,11 +671,17 @@ __device__ __forceinline__ void st_release_s32(int* p, int v) {
 }
 
 constexpr int kFusedThreads = 128;
-constexpr int kFusedMaxChain = 32;  // levels a fused chain can span (l0 .. lf)
 
 template <typename T>
-__host__ __device__ inline size_t fused_smem_bytes(int Q, int R) {
-  return mat_bytes(Q, sizeof(T)) + 2 * ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 64;
+// dynamic shared memory of the fused kernels: matrix, nvec vectors (up: 1,
+// down: 2), 16 bytes of mbarrier + ticket / next, the chain constants
+// (nchain = lf - l0 + 1 steps: group, quad; up also the children).  Kept
+// tight: the float64 Q = 48 downward kernel fits 11 CTAs per SM only up to
+// 20096 bytes per CTA (10 CTAs cost a third wave at C3: 56 -> 68 us).
+__host__ __device__ inline size_t fused_smem_bytes(int Q, int R, int nvec, int nchain) {
+  const size_t chain = size_t(nchain) * (nvec == 1 ? 13 : 5);
+  return mat_bytes(Q, sizeof(T)) + nvec * ((size_t(Q) * R * sizeof(T) + 15) & ~size_t(15)) + 16 +
+         ((chain + 15) & ~size_t(15));
 }
 
 template <typename T, int R>
@@ -694,15 +700,15 @@ __global__ void __launch_bounds__(kFusedThreads) fused_up_kernel(const FusedArgs
   // quadrant per step): one packed 16-byte record per step, fetched in one
   // round trip ahead of the dependency wait, so the climb pays no index
   // round trips between its levels
-  __shared__ int32_t ch_x[kFusedMaxChain];
-  __shared__ int2 ch_uc[kFusedMaxChain];
-  __shared__ int32_t ch_quad[kFusedMaxChain];
   const int nstep = a.lf - a.l0 + 1;  // groups on the chain, level lf down to l0 (= D + 2)
+  int2* ch_uc = reinterpret_cast<int2*>(nxt + 1);
+  int32_t* ch_x = reinterpret_cast<int32_t*>(ch_uc + nstep);
+  uint8_t* ch_quad = reinterpret_cast<uint8_t*>(ch_x + nstep);
   if (tid < nstep) {
     const int4 c = a.chain_up[int64_t(blockIdx.x) * nstep + tid];
     ch_x[tid] = c.x;
     ch_uc[tid] = make_int2(c.y, c.z);
-    ch_quad[tid] = c.w;
+    ch_quad[tid] = uint8_t(c.w);
     if (tid == 0) {
       mbar_init(bar, 1);
       fence_mbar_init();
@@ -780,8 +786,9 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   T* Xo = reinterpret_cast<T*>(smem + mb + vb);  // o[x], the next step's parent vector
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + mb + 2 * vb);
   int* ticket = reinterpret_cast<int*>(bar + 1);
-  __shared__ int32_t ch_x[kFusedMaxChain], ch_px[kFusedMaxChain], ch_quad[kFusedMaxChain];
-  __shared__ int s_own;
+  int* s_own = ticket + 1;               // owned steps
+  int32_t* ch_x = s_own + 1;             // [D + 2]: x per step, then the parent of the top owned group
+  uint8_t* ch_quad = reinterpret_cast<uint8_t*>(ch_x + a.D + 2);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -803,12 +810,14 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   if (tid <= a.D) {
     const int4 c = a.chain_down[vid * int64_t(a.D + 1) + tid];  // (entries past own are zero-filled)
     ch_x[tid] = c.x;
-    ch_px[tid] = c.y;
-    ch_quad[tid] = c.z;
-    if (tid == 0) s_own = c.w;
+    ch_quad[tid] = uint8_t(c.z);
+    if (tid == 0) {
+      *s_own = c.w;
+      ch_x[a.D + 1] = c.y;
+    }
   }
   __syncthreads();
-  const int own = s_own;
+  const int own = *s_own;
   auto load_mat = [&](int st) {
     const int lvx = a.lf - own + st;  // level of step st's group
     mbar_arrive_expect_tx(bar, uint32_t(mb));
@@ -819,8 +828,9 @@ __global__ void __launch_bounds__(kFusedThreads) fused_down_kernel(const FusedAr
   pdl_wait();  // o holds the translation sums
   uint32_t phase = 0;
   for (int st = 0; st <= own; ++st) {
-    const int64_t x = ch_x[st], px = ch_px[st];
+    const int64_t x = ch_x[st];
     if (st == 0) {
+      const int64_t px = ch_x[a.D + 1];
       if (a.lf - own - 1 > a.l0) {
         // the parent of the top owned group belongs to another CTA
         if (tid == 0) {

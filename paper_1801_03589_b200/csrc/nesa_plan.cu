@@ -697,7 +697,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   } else {
     P->tc = false;
   }
-  require(fused_smem_bytes<T>(Q, 4) <= 200 * 1024 && tgemm_smem_bytes<T, 4>(Q) <= 200 * 1024,
+  require(fused_smem_bytes<T>(Q, 4, 2, 64) <= 200 * 1024 && tgemm_smem_bytes<T, 4>(Q) <= 200 * 1024,
           "Q too large for the far-field kernels");
   // per-level gather tables (see nesa_kernels.cuh "Level transfers")
   P->down_order.resize(nlev);
@@ -816,7 +816,6 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
     //   up   [i][k], k = 0 .. D+1: (group at level lf-k, first child, children, quad)
     //   down [i][st], st = 0 .. own: (x = anc[own-1-st] or g, parent x, quad x, own)
     {
-      require(D + 2 <= kFusedMaxChain, "fused chain longer than kFusedMaxChain levels");
       const int64_t cnt = P->loc_count[li];
       std::vector<int4> cup(static_cast<size_t>(std::max<int64_t>(1, cnt * (D + 2))), int4{0, 0, 0, 0});
       std::vector<int4> cdn(static_cast<size_t>(std::max<int64_t>(1, cnt * (D + 1))), int4{0, 0, 0, 0});
@@ -1830,11 +1829,12 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     fa.D = P->fused_lf - P->l0 - 1;
     return fa;
   };
-  const size_t fsm = fused_smem_bytes<T>(Q, R);
+  const int nchain = P->fused_lf - P->l0 + 1;
+  const size_t fsm_up = fused_smem_bytes<T>(Q, R, 1, nchain), fsm = fused_smem_bytes<T>(Q, R, 2, nchain);
   // upward transfers of the fused coarse levels + the top-level sum
   auto fused_up = [&]() {
     const FusedArgs<T> fa = fused_args(CT);
-    launch_pdl(fused_up_kernel<T, R>, int(fa.count), kFusedThreads, fsm, s0, fa);
+    launch_pdl(fused_up_kernel<T, R>, int(fa.count), kFusedThreads, fsm_up, s0, fa);
     nk++;
     tr("up_fused", s0);
   };

@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--dtype", default="f32", help="f32 (complex64) or f64 (complex128)")
     ap.add_argument("--world", type=int, default=1, help="trace rank --rank's sub-plan of this partition")
     ap.add_argument("--rank", type=int, default=0)
+    ap.add_argument("--P", type=int, default=64)
+    ap.add_argument("--Q", type=int, default=64)
+    ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--split", action="store_true",
                     help="separate repeated launches of one (kernel, grid): CTA records in start order, grid at a time")
     a = ap.parse_args()
@@ -40,15 +43,15 @@ def main():
     import torch
     import paper_1801_03589_b200 as nesa
     from paper_1801_03589_b200.plan import NesaPlan
-    pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=3), a.n)
-    tree = nesa.build_tree(pts, nesa.TreeParams(P=64))
+    pts = nesa.generate_sources(nesa.CurveSpec(kind="ellipse-plates", seed=a.seed), a.n)
+    tree = nesa.build_tree(pts, nesa.TreeParams(P=a.P))
     lr = None
     if a.world > 1:
         from paper_1801_03589_b200.dist import partition_leaves
-        lr = partition_leaves(tree, a.world, 64)[a.rank]
-    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=64)), dtype=a.dtype, leaf_range=lr)
+        lr = partition_leaves(tree, a.world, a.Q)[a.rank]
+    plan = NesaPlan(tree, nesa.build_tables(tree, nesa.NesaParams(Q=a.Q)), dtype=a.dtype, leaf_range=lr)
     cdt = np.complex64 if a.dtype == "f32" else np.complex128
-    q = torch.from_numpy(nesa.random_rhs(a.n, 3).astype(cdt)).cuda()
+    q = torch.from_numpy(nesa.random_rhs(a.n, a.seed).astype(cdt)).cuda()
     phi = torch.empty_like(q)
     st = torch.cuda.current_stream()
     lib = plan.lib
