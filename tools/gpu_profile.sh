@@ -7,7 +7,7 @@ set -u
 O=gpurun_out/prof
 mkdir -p $O
 T="timeout 900"
-$T python tools/ktrace.py --reps 7 > $O/ktrace.txt 2>&1
+$T python tools/ktrace.py --reps 7 --split > $O/ktrace.txt 2>&1
 $T python tools/configs.py --reps 200 > $O/configs.txt 2>&1
 $T python tools/configs.py --c5 > $O/configs_c5.txt 2>&1
 $T python tools/solve_c4.py > $O/solve_c4.txt 2>&1
@@ -18,6 +18,6 @@ $T ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv \
 $T ncu --set full --clock-control none --import-source on -k regex:blockgemv -c 1 \
   -o $O/near python tools/prof_matvec.py --k 2 > $O/ncu_near.log 2>&1
 $T ncu --set full --clock-control none --import-source on \
-  -k regex:'level_tc|tgemm_tc3|fused_up|fused_down|radiation|reception|reduce|gather' -s 17 -c 17 \
+  -k regex:'level_tc|tgemm_tc3|fused_up|fused_down|radiation|reception|reduce|gather' -s 21 -c 21 \
   -o $O/far python tools/prof_matvec.py --k 2 > $O/ncu_far.log 2>&1
 echo done
