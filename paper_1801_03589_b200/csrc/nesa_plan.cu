@@ -1881,7 +1881,13 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
       {
         const size_t li = size_t(P->L - P->l0);
         const size_t lo = size_t(P->split_lv - P->l0);
-        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[li], 0));
+        // FFMA translation (float64 / no tensor cores): its CTAs fill the
+        // shared memory the upward level kernels need (ktrace at C4 float64:
+        // the upward chain stalled 190 us behind the leaf translation), so
+        // there the side stream waits for the wide levels' upward pass
+        // (C4 complex128 1340 -> 1316 us)
+        const bool tc_tr = std::is_same<T, float>::value && P->tc;
+        CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[tc_tr ? li : lo], 0));
         translate(P->tunit_lv_begin[li], P->tunit_lv_end[li], P->s2);
         if (P->split_lv < P->L) {
           CUDA_OK(cudaEventRecord(P->ev_tx, P->s2));
