@@ -2627,8 +2627,12 @@ constexpr size_t radiation_tc_smem_bytes() {
          size_t(kRadTcLeaves) * (64 * R + 4) * 4 + 128 + 8 * kRadTcLeaves;
 }
 
+// Registers: beside the near field's two CTAs only ONE radiation CTA fits an
+// SM (8 warps: 2 per sub-partition, 2 x 160 x 32 + the near field's 6144 =
+// 16384), so the former 128-register squeeze for two CTAs per SM bought
+// nothing inside the product (A/B 475.3 -> 470.4 us at the natural 148-160).
 template <int R>
-__global__ void __launch_bounds__(32 * kRadTcWarps, 2) radiation_tc_kernel(
+__global__ void __maxnreg__(kTcFarMaxReg) radiation_tc_kernel(
     const float2* __restrict__ prel, const int64_t* __restrict__ leaf_start,
     const int64_t* __restrict__ leaf_stop, const float* __restrict__ leaf_r,
     const float* __restrict__ ATC, const float* __restrict__ qt, float* __restrict__ s,
@@ -2725,25 +2729,54 @@ __global__ void __launch_bounds__(32 * kRadTcWarps, 2) radiation_tc_kernel(
           zc[mm & 1] = cmul_pk(z, W1, W2);
         }
     };
+    // two points at a time: four independent power chains per lane (with one
+    // CTA per SM beside the near field, two chains left the FP32 pipes idle)
+    auto point2 = [&](const float2 pa, const float (&qa)[R], const float2 pb, const float (&qb)[R]) {
+      const float2 wa = make_float2(pa.x * inv, pa.y * inv), wb = make_float2(pb.x * inv, pb.y * inv);
+      const float2 wa2 = cmulf(wa, wa), wb2 = cmulf(wb, wb);
+      const float2 wa4 = cmulf(wa2, wa2), wb4 = cmulf(wb2, wb2);
+      const float2 A1 = wa4, A2 = make_float2(-wa4.y, wa4.x);
+      const float2 B1 = wb4, B2 = make_float2(-wb4.y, wb4.x);
+      float2 za[2], zb[2];
+      za[0] = half ? wa : make_float2(1.f, 0.f);
+      zb[0] = half ? wb : make_float2(1.f, 0.f);
+      za[1] = cmulf(za[0], wa2);
+      zb[1] = cmulf(zb[0], wb2);
+#pragma unroll
+      for (int mm = 0; mm < kRadTcMH; ++mm) {
+        const float2 ya = za[mm & 1], yb = zb[mm & 1];
+        if constexpr (R == 2) {
+          ffma2(v[(mm * 2) * R], v[(mm * 2) * R + 1], ya.x, qa[0], qa[1]);
+          ffma2(v[(mm * 2 + 1) * R], v[(mm * 2 + 1) * R + 1], ya.y, qa[0], qa[1]);
+          ffma2(v[(mm * 2) * R], v[(mm * 2) * R + 1], yb.x, qb[0], qb[1]);
+          ffma2(v[(mm * 2 + 1) * R], v[(mm * 2 + 1) * R + 1], yb.y, qb[0], qb[1]);
+        } else {
+          v[mm * 2] = fmaf(ya.x, qa[0], v[mm * 2]);
+          v[mm * 2 + 1] = fmaf(ya.y, qa[0], v[mm * 2 + 1]);
+          v[mm * 2] = fmaf(yb.x, qb[0], v[mm * 2]);
+          v[mm * 2 + 1] = fmaf(yb.y, qb[0], v[mm * 2 + 1]);
+        }
+        za[mm & 1] = cmul_pk(ya, A1, A2);
+        zb[mm & 1] = cmul_pk(yb, B1, B2);
+      }
+    };
     fetch(g, p0, q0);
     fetch(g + 4, p1, q1);
     for (int j = g; j < n; j += 8) {
-      {
-        const float2 p = p0;
-        float qv[R];
+      const float2 pa = p0, pb = p1;
+      float qa[R], qb[R];
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) qv[rr] = q0[rr];
-        fetch(j + 8, p0, q0);
-        point(p, qv);
+      for (int rr = 0; rr < R; ++rr) {
+        qa[rr] = q0[rr];
+        qb[rr] = q1[rr];
       }
-      if (j + 4 < n) {
-        const float2 p = p1;
-        float qv[R];
-#pragma unroll
-        for (int rr = 0; rr < R; ++rr) qv[rr] = q1[rr];
-        fetch(j + 12, p1, q1);
-        point(p, qv);
-      }
+      const bool two = j + 4 < n;
+      fetch(j + 8, p0, q0);
+      fetch(j + 12, p1, q1);
+      if (two)
+        point2(pa, qa, pb, qb);
+      else
+        point(pa, qa);
     }
     // ---- transpose reduction over the 4 lanes of the half: lane g keeps
     // values [vb, vb + NV4)
