@@ -883,7 +883,6 @@ __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
                               const int64_t* __restrict__ int_ptr, const T* __restrict__ Y, T* o,
                               int Q) {
   KtScope kt_(33);
-  pdl_trigger();
   pdl_wait();
   const int QR = Q * R;
   const int lane = threadIdx.x & 31;
@@ -927,6 +926,9 @@ __global__ void reduce_kernel(const int32_t* __restrict__ ids, int64_t n_ids,
       }
     }
   }
+  // (dependents start their prologue once this CTA's sums are done: the fused
+  // downward kernel's 770 CTAs otherwise sit resident through the whole pass)
+  pdl_trigger();
 }
 
 // ----------------------------------------------------------------------------
@@ -1900,7 +1902,6 @@ __global__ void __maxnreg__(R == 2 ? kTcFarMaxReg : 255) level_tc_kernel(const L
     if constexpr (kDown) par = a.opar[tl.x + e];
   }
   if (rr == 0 && live) gid[e] = int32_t(g);
-  pdl_trigger();
   pdl_wait();  // amplitudes come from the previous kernel in the chain
   float4 c[16];
 #pragma unroll
@@ -1961,6 +1962,11 @@ __global__ void __maxnreg__(R == 2 ? kTcFarMaxReg : 255) level_tc_kernel(const L
   }
   mbar_wait(&bar[1], 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // the dependent kernel may start its prologue now, one epilogue ahead of
+  // its inputs: triggered at the top of the kernel, the next kernel's CTAs
+  // (770 fused-chain CTAs after the last upward level) sat resident for the
+  // whole level and kept the side stream's translation out (ktrace: 31 us)
+  pdl_trigger();
   uint32_t r[64];
   tmem_ld64(t_acc, r);
   float* out = kDown ? a.o : a.Tout;

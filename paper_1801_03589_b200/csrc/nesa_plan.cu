@@ -1751,10 +1751,10 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     nk++;
     tr("translate", st);
   };
-  auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st) {
+  auto reduce = [&](int64_t i0, int64_t i1, cudaStream_t st, int per_sm = 8) {
     // o[g] = translation sum of the listed local groups
     if (i1 <= i0) return;
-    const int grid = grid_for((i1 - i0) * 32, 256, cap);
+    const int grid = grid_for((i1 - i0) * 32, 256, P->n_sm * per_sm);
     const int32_t* ids = P->red_ids.p + i0;
     const int64_t* ip = P->int_ptr.p;
     if (st == s0)
@@ -1892,7 +1892,14 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
         if (P->split_lv < P->L) {
           CUDA_OK(cudaEventRecord(P->ev_tx, P->s2));
           CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_tx, 0));
-          reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s3);
+          // (and not before the wide levels' upward pass is done: started
+          // earlier, its 256-thread CTAs filled the register file and the
+          // fused upward chain's CTAs waited ~10 us to become resident)
+          CUDA_OK(cudaStreamWaitEvent(P->s3, P->ev_s_lv[lo], 0));
+          // (half the usual grid: at 8 CTAs per SM this pass filled every
+          // thread slot and kept the fused upward chain's CTAs out for 12 us;
+          // its result is not needed before the leaf level's downward kernel)
+          reduce(P->red_lv_begin[li], P->red_lv_end[li], P->s3, 4);
           CUDA_OK(cudaEventRecord(P->ev_t_lv[li], P->s3));
           CUDA_OK(cudaStreamWaitEvent(P->s2, P->ev_s_lv[lo], 0));
           translate(P->tunit_lv_begin[li - 1], P->tunit_lv_end[lo], P->s2);
