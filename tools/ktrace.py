@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--P", type=int, default=64)
     ap.add_argument("--Q", type=int, default=64)
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--ends", type=int, default=0, help="print the distribution of CTA end times of this kernel tag")
     ap.add_argument("--split", action="store_true",
                     help="separate repeated launches of one (kernel, grid): CTA records in start order, grid at a time")
     a = ap.parse_args()
@@ -69,6 +70,11 @@ def main():
         n = lib.nesa_ktrace_read(plan.handle, buf, cap)
         rec = np.frombuffer(buf, dtype=np.uint64, count=4 * n).reshape(n, 4).astype(np.int64)
         t0 = rec[:, 2].min()
+        if a.ends:
+            e = np.sort(rec[rec[:, 0] == a.ends, 3] - t0) / 1e3
+            if len(e):
+                print(f"tag {a.ends}: CTA end times (us) min {e[0]:.1f} p10 {e[len(e)//10]:.1f} "
+                      f"p50 {e[len(e)//2]:.1f} p90 {e[len(e)*9//10]:.1f} max {e[-1]:.1f} (n={len(e)})")
         launches = {}
         if a.split:
             # launch index of each record: rank of its start among the records of its (tag, grid), // grid
