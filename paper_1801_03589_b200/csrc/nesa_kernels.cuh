@@ -159,9 +159,6 @@ struct BlockGemvArgs {
   const T* base;                 // scatter: added per tree row (may be null)
   const int64_t* perm;           // scatter: tree row -> original row
   int ldy;                       // scatter: row stride of y (elements)
-  const int32_t* pool_ptr;       // [n_pool + 1] first chunk of each shared-tail item (n_pool = 0: none)
-  int n_pool;
-  int* pool_ctl;                 // [2] next pool item, finished CTAs (reset by the last CTA)
 };
 
 struct StageHdr {
@@ -257,41 +254,14 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
     // ------------------------------ producer ------------------------------
     const int32_t* recw = reinterpret_cast<const int32_t*>(a.recs);
     const uint64_t pol = l2_evict_first_policy();
-    // chunk stream: the CTA's own range [c0, c1), then items of the shared
-    // tail taken one at a time from pool_ctl[0]; the range after the current
-    // one is known one range ahead so its first record is prefetched like
-    // any other
-    int i0 = c0, i1 = c1;
-    int n0 = 0, n1 = 0;  // next range (empty: none)
-    auto take = [&]() {  // next pool item -> [n0, n1)
-      n0 = n1 = 0;
-      if (a.n_pool > 0) {
-        int u = 0;
-        if (lane == 0) u = atomicAdd(a.pool_ctl, 1);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u < a.n_pool) {
-          n0 = __ldg(a.pool_ptr + u);
-          n1 = __ldg(a.pool_ptr + u + 1);
-        }
-      }
-    };
-    take();
-    if (i0 >= i1) {
-      i0 = n0;
-      i1 = n1;
-      take();
-    }
+    int i0 = c0;
+    const int i1 = c1;
     int k = 0;
     int32_t w_next = i0 < i1 ? __ldg(recw + int64_t(i0) * 32 + lane) : 0;
     while (i0 < i1) {
       const int i = i0++;
       const int32_t w = w_next;
-      if (i + 1 < i1) {
-        w_next = __ldg(recw + int64_t(i + 1) * 32 + lane);
-      } else if (n0 < n1) {
-        w_next = __ldg(recw + int64_t(n0) * 32 + lane);
-      }
-      const bool range_done = i0 >= i1 && n0 < n1;
+      if (i + 1 < i1) w_next = __ldg(recw + int64_t(i + 1) * 32 + lane);
       const int st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
       ++k;
@@ -351,30 +321,6 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
         }
       }
       cp_async_mbar_arrive_noinc(&full[st]);
-      if (range_done) {
-        // continue with the next range and look one further ahead (the
-        // counter's round trip is paid with this range's last chunk in flight)
-        i0 = n0;
-        i1 = n1;
-        take();
-      }
-    }
-    // end of stream: a stage that carries only the stop flag
-    {
-      const int st = k % kStages;
-      const uint32_t round = uint32_t(k / kStages);
-      unsigned char* stg = smem + size_t(st) * Lay::kStage;
-      mbar_wait(&empty[st], (round & 1u) ^ 1u);
-      if (lane == 0) {
-        reinterpret_cast<StageHdr*>(stg + Lay::offHdr)->flags = 4;
-        mbar_arrive_expect_tx(&full[st], 0);
-      }
-      cp_async_mbar_arrive_noinc(&full[st]);
-    }
-    // the last CTA to run out of work resets the pool for the next launch
-    if (a.n_pool > 0 && lane == 0 && atomicAdd(a.pool_ctl + 1, 1) == int(gridDim.x) - 1) {
-      a.pool_ctl[0] = 0;
-      a.pool_ctl[1] = 0;
     }
   } else {
     // ------------------------------ consumers -----------------------------
@@ -387,13 +333,12 @@ __global__ void __launch_bounds__(NCW * 32 + 32, NST * AB <= 3 * 16384 ? 2 : 1)
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int rr = 0; rr < R; ++rr) acc[i][rr] = T(0);
-    for (int k = 0;; ++k) {
+    for (int k = 0; k < c1 - c0; ++k) {
       const int st = k % kStages;
       const uint32_t round = uint32_t(k / kStages);
       const unsigned char* stg = smem + size_t(st) * Lay::kStage;
       mbar_wait(&full[st], round & 1u);
       const StageHdr h = *reinterpret_cast<const StageHdr*>(stg + Lay::offHdr);
-      if (h.flags & 4) break;  // end of the producer's stream
       const int m = h.m, nc = h.ncols, ld = h.ld, CL = h.CL;
       const int RQ = ld >> 2;
       const int cl = RQ == 1 ? tid : int(__umulhi(uint32_t(tid), h.magic));

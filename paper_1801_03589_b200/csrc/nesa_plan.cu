@@ -31,9 +31,6 @@
 
 #include "../../include/nesa_b200.h"
 #include "nesa_kernels.cuh"
-// share of the near field's bytes left to the dynamic tail (chunk_and_balance;
-// A/B at C4: 0 / 0.04 / 0.10 / 0.20 / 0.40 -> 472.1 / 467.6 / 465.9 / 464.8 / 465.9 us)
-constexpr double kNearPoolFrac = 0.20;
 
 using namespace nesa;
 
@@ -140,7 +137,6 @@ struct HostBlockSet {
   std::vector<BlockSeg> segs;
   std::vector<ChunkRec> recs;
   std::vector<int32_t> cta_ptr;
-  std::vector<int32_t> pool_ptr;  // shared tail: first chunk of each pool item (+ end), empty = none
   int64_t blob_elems = 0;
   int64_t entries = 0;
 };
@@ -151,9 +147,6 @@ struct DevBlockSet {
   DevBuf<BlockSeg> segs;
   DevBuf<ChunkRec> recs;
   DevBuf<int32_t> cta_ptr;
-  DevBuf<int32_t> pool_ptr;    // shared tail of whole items, taken by an atomic counter
-  DevBuf<int32_t> pool_ctl;    // [2] next pool item, finished CTAs (self-resetting)
-  int n_pool = 0;
   int grid = 0;
   int64_t n_items = 0;
   int64_t entries = 0;
@@ -162,13 +155,8 @@ struct DevBlockSet {
 // Split items into bulk-copy chunks and give each CTA a contiguous,
 // byte-balanced range of whole items (a target row is never split across
 // CTAs, so it has exactly one writer).
-// pool_frac > 0: the last items holding that fraction of the bytes are not
-// assigned; every CTA takes them one item at a time from an atomic counter
-// once its own range is done, so CTAs slowed by co-resident kernels hand the
-// tail to the others (in the C4 product the statically balanced CTAs ended
-// between 368 and 415 us).
 void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid, int ab = kABytes,
-                       int nct = kNCT, double pool_frac = 0.0) {
+                       int nct = kNCT) {
   hs.recs.clear();
   std::vector<int64_t> item_first_chunk(hs.items.size() + 1);
   std::vector<double> item_bytes(hs.items.size());
@@ -213,27 +201,16 @@ void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid, int ab
     item_bytes[i] = double(it.ld) * it.n * elem_bytes + 256.0;  // + per-item overhead
   }
   item_first_chunk[hs.items.size()] = int64_t(hs.recs.size());
-  double total_all = 0;
-  for (double b : item_bytes) total_all += b;
-  // static part: items [0, n_static)
-  size_t n_static = hs.items.size();
-  hs.pool_ptr.clear();
-  if (pool_frac > 0.0 && hs.items.size() >= size_t(16) * size_t(max_grid)) {
-    double tail = 0;
-    while (n_static > 0 && tail + item_bytes[n_static - 1] <= pool_frac * total_all) tail += item_bytes[--n_static];
-    for (size_t i = n_static; i <= hs.items.size(); ++i) hs.pool_ptr.push_back(int32_t(item_first_chunk[i]));
-    if (hs.pool_ptr.size() < 2) hs.pool_ptr.clear();
-  }
-  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_grid, int64_t(n_static))));
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(max_grid, int64_t(hs.items.size()))));
   double total = 0;
-  for (size_t i = 0; i < n_static; ++i) total += item_bytes[i];
+  for (double b : item_bytes) total += b;
   hs.cta_ptr.assign(grid + 1, 0);
   size_t it = 0;
   double acc = 0;
   for (int c = 0; c < grid; ++c) {
     hs.cta_ptr[c] = int32_t(item_first_chunk[it]);
     const double target = total * double(c + 1) / grid;
-    while (it < n_static && c < grid - 1) {
+    while (it < hs.items.size() && c < grid - 1) {
       const double nb = acc + item_bytes[it];
       // stop before an item that overshoots the target by more than it undershoots
       if (nb > target && (nb - target) > (target - acc) && int64_t(hs.cta_ptr[c]) != item_first_chunk[it])
@@ -243,7 +220,7 @@ void chunk_and_balance(HostBlockSet& hs, size_t elem_bytes, int max_grid, int ab
       if (acc >= target) break;
     }
   }
-  hs.cta_ptr[grid] = int32_t(item_first_chunk[n_static]);
+  hs.cta_ptr[grid] = int32_t(hs.recs.size());
 }
 
 template <typename T>
@@ -253,9 +230,6 @@ void upload_blockset(DevBlockSet& d, const HostBlockSet& h) {
   d.segs.upload(h.segs);
   d.recs.upload(h.recs);
   d.cta_ptr.upload(h.cta_ptr);
-  d.n_pool = h.pool_ptr.empty() ? 0 : int(h.pool_ptr.size()) - 1;
-  if (d.n_pool > 0) d.pool_ptr.upload(h.pool_ptr);
-  d.pool_ctl.alloc(2);  // zero-filled
   d.grid = int(h.cta_ptr.size()) - 1;
   d.n_items = int64_t(h.items.size());
   d.entries = h.entries;
@@ -1019,7 +993,7 @@ void build_plan_T(nesa_plan* P, const nesa_plan_desc* d) {
   }
   // near field: two persistent CTAs per SM (4 consumer warps, 2 x 24 KB ring);
   // V / U: the generic 8-warp, 3 x 16 KB geometry
-  chunk_and_balance(hn, es, kBGPerSM * P->n_sm, kNearABytes, kNearNCW * 32, kNearPoolFrac);
+  chunk_and_balance(hn, es, kBGPerSM * P->n_sm, kNearABytes, kNearNCW * 32);
   chunk_and_balance(hv, es, kBGPerSM * P->n_sm);
   chunk_and_balance(hu, es, kBGPerSM * P->n_sm);
   upload_blockset<T>(P->nearset, hn);
@@ -1432,7 +1406,7 @@ template <typename T, int R, int MODE, int NST = kStages, int NCW = kNCW, int AB
 BlockGemvArgs<T> blockgemv_args(const DevBlockSet& bs, const T* x, T* y, const T* base,
                                 const int64_t* perm, int ldy) {
   return BlockGemvArgs<T>{reinterpret_cast<const T*>(bs.blob.p), bs.recs.p, bs.cta_ptr.p, x, y,
-                          base, perm, ldy, bs.pool_ptr.p, bs.n_pool, bs.pool_ctl.p};
+                          base, perm, ldy};
 }
 
 // near field (store mode): 4 consumer warps, two 24 KB stages
