@@ -3078,10 +3078,33 @@ __global__ void __launch_bounds__(32 * kExpWarps, BETA_IN ? 6 : 1) reception_exp
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) phi[db * ldp + rr] = bb2[rr] + accb[rr];
     };
+    // one point per lane: the last pass of a leaf whose remainder fits 32
+    // lanes (3 of 4 leaves at C4: 65-96 points) costs half the two-point pass
+    auto eval1 = [&](float2 pa, int64_t da, const float* ba) {
+      const float2 wa = make_float2(pa.x * inv, pa.y * inv);
+      const float2 Wa2 = make_float2(-wa.y, wa.x);
+      float2 za = wa;
+      float acca[R];
 #pragma unroll
-    for (int i = 0; i < kSlots; i += 2)
-      if (lane + 32 * i < n)
+      for (int rr = 0; rr < R; ++rr) acca[rr] = bf[rr];
+#pragma unroll 2
+      for (int m = 1; m <= nt; ++m) {
+        float br[R], nbi[R];
+        coef(m, br, nbi);
+        term(acca, za, br, nbi);
+        za = cmul_pk(za, wa, Wa2);
+      }
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) phi[da * ldp + rr] = ba[rr] + acca[rr];
+    };
+#pragma unroll
+    for (int i = 0; i < kSlots; i += 2) {
+      if (32 * (i + 1) >= n) {  // (warp-uniform) no lane has a second point in this pass
+        if (lane + 32 * i < n) eval1(pp[i], dd[i], bb[i]);
+      } else if (lane + 32 * i < n) {
         eval2(pp[i], dd[i], bb[i], pp[i + 1], dd[i + 1], bb[i + 1], lane + 32 * (i + 1) < n);
+      }
+    }
     for (int j = lane + 32 * kSlots; j < n; j += 32) {
       float base[R];
 #pragma unroll
