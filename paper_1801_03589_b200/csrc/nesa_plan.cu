@@ -31,6 +31,7 @@
 
 #include "../../include/nesa_b200.h"
 #include "nesa_kernels.cuh"
+constexpr int64_t kLevelTcMin = 2048;  // groups of a level for the tensor-core level kernels
 
 using namespace nesa;
 
@@ -1648,6 +1649,13 @@ int enqueue_T(nesa_plan* P, const T* q, T* phi, int ldv, uint32_t flags, int sta
     if constexpr (std::is_same<T, float>::value) {
       if (!P->level_tc) return false;
       const int ci = lv - P->l0;
+      // tensor cores only from kLevelTcMin groups: every tf32x3 level adds a
+      // systematic ~1.5e-6 to the complex64 error at C4 (the tensor core's
+      // accumulator truncates; the errors of successive levels add linearly:
+      // 0 / 1 / 2 / 3 / 4 / 5 levels -> 1.6 / 3.3 / 5.0 / 6.5 / 8.0 / 9.6e-6
+      // against the exact sum), so the smallest per-level kernel stays on the
+      // FFMA path and the product keeps its margin below 1e-5
+      if (P->loc_count[ci] < kLevelTcMin) return false;
       const DevBuf<int4>& tiles = P->lvl_tiles[size_t(ci) * 3 + RI];
       LevelTcArgs ta{};
       const bool down = mode == kLvlDown || mode == kLvlDownBeta;
